@@ -1,0 +1,166 @@
+/*
+ * kvq_capi.h — C-ABI of the B200-native CalibQuant decode hot path.
+ *
+ * This is the drop-in boundary. Every entry point replaces one function of the
+ * reference's header-only C++ API (`kvq`, /root/reference/proj/include/kvq/*.hpp;
+ * cited per function below) and is what the C++ drop-in headers in include/kvq/ and
+ * the Python binding (paper_2502_14882_b200/kvq.py) bind. Plain pointers and sizes
+ * only: no CUDA, torch or C++ types cross this boundary.
+ *
+ * Conventions
+ *   - Return value: KVQ_OK or an error class matching the reference's exception types
+ *     (errors.hpp:11-33): KVQ_ERR_CONFIG <-> kvq::config_error, KVQ_ERR_DOMAIN <->
+ *     kvq::domain_error, KVQ_ERR_FORMAT <-> kvq::format_error; KVQ_ERR_CUDA for device
+ *     failures. kvq_last_error() returns the message of the calling thread's last error.
+ *   - Unless the name ends in _device, pointers are HOST memory; the call copies in,
+ *     runs the CUDA kernels, copies out and synchronizes. _device entry points take
+ *     device pointers and a cudaStream_t passed as void* (NULL = legacy default stream)
+ *     and do not synchronize.
+ *   - Matrices are row-major fp32 (matrix.hpp:16-60). Packed codes use the reference
+ *     byte layout bit for bit (bitpack.hpp:15-90, quantize.hpp:46-62).
+ *   - There is no CPU fallback: without a usable CUDA device every compute entry point
+ *     returns KVQ_ERR_CUDA.
+ */
+#ifndef KVQ_CAPI_H
+#define KVQ_CAPI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KVQ_OK 0
+#define KVQ_ERR_CONFIG 1
+#define KVQ_ERR_DOMAIN 2
+#define KVQ_ERR_FORMAT 3
+#define KVQ_ERR_CUDA 4
+
+#define KVQ_MODE_CHANNEL_WISE 0 /* QuantMode::channel_wise (quantize.hpp:31) */
+#define KVQ_MODE_GLOBAL 1       /* QuantMode::global */
+#define KVQ_FULL_PRECISION_BITS 16 /* kvcache.hpp:26 */
+
+#define KVQ_PATH_AUTO 0    /* tensor-core path when the shape allows, else generic */
+#define KVQ_PATH_GENERIC 1 /* any shape; also the path that emits probability rows */
+#define KVQ_PATH_TC 2      /* d = 128, M = 8 IMMA path (fails with KVQ_ERR_CONFIG otherwise) */
+
+/* ---- diagnostics ------------------------------------------------------------ */
+/* Copies the calling thread's last error message (NUL-terminated, truncated to cap);
+ * returns its full length. */
+size_t kvq_last_error(char* buf, size_t cap);
+/* Number of CUDA kernels this library has launched in this process. */
+unsigned long long kvq_launch_count(void);
+/* 1 if a CUDA device is usable (the library never falls back to the CPU). */
+int kvq_device_available(void);
+
+/* ---- bitpack.hpp ------------------------------------------------------------- */
+/* Bytes `pack` produces for `count` codes (PackedBuffer::word_count, bitpack.hpp:22-25). */
+size_t kvq_packed_bytes(size_t count, int code_bits, int word_bits);
+/* kvq::pack (bitpack.hpp:161-187). out must hold kvq_packed_bytes(...) bytes.
+ * CONFIG on bad widths (bitpack.hpp:141-149), DOMAIN on a code >= 2^code_bits. */
+int kvq_pack(const uint32_t* codes, size_t count, int code_bits, int word_bits, uint8_t* out,
+             size_t out_cap);
+/* kvq::unpack (bitpack.hpp:189-203): `count` = PackedBuffer::logical_count. */
+int kvq_unpack(const uint8_t* bytes, size_t byte_len, size_t count, int code_bits, int word_bits,
+               uint32_t* out);
+
+/* ---- quantize.hpp ------------------------------------------------------------ */
+/* Bytes of one packed segment: tokens * words_per_row * M/8 (quantize.hpp:56-61). */
+size_t kvq_segment_bytes(size_t tokens, size_t dim, int bitwidth, int word_bits);
+/* kvq::compute_stats (quantize.hpp:64-89). alpha/beta: cols floats each. */
+int kvq_compute_stats(const float* m, size_t rows, size_t cols, int mode, float* alpha,
+                      float* beta);
+/* kvq::quantize (quantize.hpp:91-127): codes of m under the given stats, packed. */
+int kvq_quantize(const float* m, size_t rows, size_t cols, const float* alpha, const float* beta,
+                 int bitwidth, int word_bits, uint8_t* out, size_t out_cap);
+/* kvq::dequantize (quantize.hpp:129-146). out: rows x cols. */
+int kvq_dequantize(const uint8_t* codes, size_t rows, size_t cols, const float* alpha,
+                   const float* beta, int bitwidth, int word_bits, float* out);
+/* Batched device K1: `mats` fp32 matrices [mats][rows][dim] -> stats [mats][dim] and
+ * codes [mats][rows][row_bytes] (compute_stats + quantize per matrix). */
+int kvq_quantize_device(const float* x, size_t mats, size_t rows, size_t dim, int bitwidth,
+                        int mode, int word_bits, uint8_t* codes, float* alpha, float* beta,
+                        void* stream);
+
+/* ---- kernels.hpp ------------------------------------------------------------- */
+/* kvq::qk_scores, batched form (kernels.hpp:342-363; single form 302-314 is heads=1):
+ * queries [heads][dim], codes [heads][tokens][row_bytes], alpha/beta [heads][dim]
+ * -> scores [heads][tokens] = post-scaled q.K (no 1/sqrt(d)). */
+int kvq_qk_scores(const float* queries, const uint8_t* codes, const float* alpha,
+                  const float* beta, size_t heads, size_t tokens, size_t dim, int bitwidth,
+                  int word_bits, float* scores);
+/* kvq::wv_output, batched form (kernels.hpp:365-396; single 316-336): weights
+ * [heads][tokens] -> out [heads][dim]. */
+int kvq_wv_output(const float* weights, const uint8_t* codes, const float* alpha,
+                  const float* beta, size_t heads, size_t tokens, size_t dim, int bitwidth,
+                  int word_bits, float* out);
+
+/* ---- calibrate.hpp ----------------------------------------------------------- */
+/* kvq::calibrated_softmax_concat (calibrate.hpp:100-114) over `rows` rows:
+ * vis [rows][n_vis], tail [rows][n_tail] -> out [rows][n_vis + n_tail]. Adds the number
+ * of g slope violations (calibrate.hpp:52-54) to *slope_violations if non-NULL. */
+int kvq_calibrated_softmax_concat(const float* vis, size_t n_vis, const float* tail,
+                                  size_t n_tail, size_t rows, float tau1, float tau2, float* out,
+                                  size_t* slope_violations);
+
+/* ---- kvcache.hpp: HybridKVCache ---------------------------------------------- */
+/* A device-resident hybrid cache for `batch` independent sequences of `kv_heads` KV
+ * heads each; every KV head serves `group` query heads (GQA). batch = 1, group = 1 is
+ * exactly one reference HybridKVCache with kv_heads heads. */
+typedef struct kvq_cache kvq_cache;
+
+/* HybridKVCache::build (kvcache.hpp:48-66): k_vis/v_vis [batch][kv_heads][n_vis][dim].
+ * bitwidth = KVQ_FULL_PRECISION_BITS gives build_full_precision (69-83): the prefill
+ * becomes the fp32 tail. n_vis = 0 gives an empty prefill (pure fp32 cache). */
+int kvq_cache_build(const float* k_vis, const float* v_vis, size_t batch, size_t kv_heads,
+                    size_t group, size_t n_vis, size_t dim, int bitwidth, int mode, int word_bits,
+                    float tau1, float tau2, kvq_cache** out);
+/* Same, prefill already on the device (no host round trip). */
+int kvq_cache_build_device(const float* k_vis, const float* v_vis, size_t batch, size_t kv_heads,
+                           size_t group, size_t n_vis, size_t dim, int bitwidth, int mode,
+                           int word_bits, float tau1, float tau2, void* stream, kvq_cache** out);
+void kvq_cache_free(kvq_cache* c);
+/* Preallocate fp32 tail capacity (rows per unit); append grows it on demand. */
+int kvq_cache_reserve_tail(kvq_cache* c, size_t rows);
+/* Decode kernel selection (KVQ_PATH_*); never changes results beyond fp tolerance. */
+int kvq_cache_set_path(kvq_cache* c, int path);
+
+/* HybridKVCache::append (kvcache.hpp:99-109): k_new/v_new [batch][kv_heads][dim]. */
+int kvq_cache_append(kvq_cache* c, const float* k_new, const float* v_new);
+int kvq_cache_append_device(kvq_cache* c, const float* k_new, const float* v_new, void* stream);
+
+/* HybridKVCache::decode_step / decode_step_detailed (kvcache.hpp:111-121, 263-311):
+ * queries [batch][kv_heads][group][dim] -> out, same shape. weights (nullable) receives
+ * [batch][kv_heads][group][n_vis + n_tail] probability rows; slope_violations (nullable)
+ * receives the DecodeDetail::slope_violations count. */
+int kvq_cache_decode(kvq_cache* c, const float* queries, float* out, float* weights,
+                     size_t* slope_violations);
+int kvq_cache_decode_device(kvq_cache* c, const float* queries, float* out, void* stream);
+
+/* One serving step through host buffers, in the reference bench order (kvq_main.cpp:
+ * 313-321): decode_step(queries) then append(k_new, v_new). Host->device copies, both
+ * kernels and the device->host copy of `out` are issued on one stream, one sync. */
+int kvq_cache_step(kvq_cache* c, const float* queries, const float* k_new, const float* v_new,
+                   float* out);
+
+/* Accessors (kvcache.hpp:85-96). info: batch, kv_heads, group, dim, n_vis, n_tail,
+ * bitwidth, word_bits, mode, tail_capacity. */
+int kvq_cache_info(const kvq_cache* c, size_t info[10]);
+int kvq_cache_calibration(const kvq_cache* c, float tau[2]);
+/* CacheMemory (kvcache.hpp:28-35, 123-135): code, stats, quantized, tail, fp32_vis, total. */
+int kvq_cache_memory(const kvq_cache* c, size_t mem[6]);
+/* key_segment / value_segment (93-94) of unit u = b*kv_heads + h, which 0 = K, 1 = V:
+ * bytes (kvq_segment_bytes(n_vis, ...)) in the reference layout, alpha/beta [dim]. */
+int kvq_cache_read_segment(const kvq_cache* c, size_t unit, int which, uint8_t* bytes,
+                           float* alpha, float* beta);
+/* key_tail / value_tail (95-96): [n_tail][dim] fp32. */
+int kvq_cache_read_tail(const kvq_cache* c, size_t unit, int which, float* out);
+/* Raw device pointers (k_codes, v_codes, k_alpha, k_beta, v_alpha, v_beta, k_tail, v_tail,
+ * tail_len) for zero-copy integration with a serving engine. */
+int kvq_cache_device_pointers(const kvq_cache* c, void* ptrs[9]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KVQ_CAPI_H */

@@ -1,0 +1,49 @@
+// k3_append.cu — K3: HybridKVCache::append (kvcache.hpp:99-109). One fp32 K row and one
+// V row per (request, KV head) go to tail slot tail_len[request]; the packed segment is
+// never touched and tokens are never re-quantized. tail_len lives on the
+// device so append + decode can be captured in one CUDA graph and replayed per step.
+#include "kvq_internal.cuh"
+
+namespace kvqb {
+
+namespace {
+
+// One CTA per request: all of its KV heads, then a single increment of its length.
+__global__ void append_kernel(const float* __restrict__ k_new, const float* __restrict__ v_new,
+                              size_t kv_heads, size_t dim, size_t tail_cap,
+                              float* __restrict__ k_tail, float* __restrict__ v_tail,
+                              int* __restrict__ tail_len) {
+    const size_t b = blockIdx.x;
+    const size_t slot = (size_t)tail_len[b];
+    const size_t n = kv_heads * dim;
+    const bool vec = (dim % 4) == 0;
+    for (size_t i = threadIdx.x; i < (vec ? n / 4 : n); i += blockDim.x) {
+        if (vec) {
+            size_t h = (i * 4) / dim, c = (i * 4) % dim;
+            size_t dst = ((b * kv_heads + h) * tail_cap + slot) * dim + c;
+            size_t src = (b * kv_heads + h) * dim + c;
+            *reinterpret_cast<float4*>(k_tail + dst) = *reinterpret_cast<const float4*>(k_new + src);
+            *reinterpret_cast<float4*>(v_tail + dst) = *reinterpret_cast<const float4*>(v_new + src);
+        } else {
+            size_t h = i / dim, c = i % dim;
+            size_t dst = ((b * kv_heads + h) * tail_cap + slot) * dim + c;
+            k_tail[dst] = k_new[(b * kv_heads + h) * dim + c];
+            v_tail[dst] = v_new[(b * kv_heads + h) * dim + c];
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) tail_len[b] = (int)(slot + 1);
+}
+
+}  // namespace
+
+cudaError_t launch_append(const float* k_new, const float* v_new, size_t batch, size_t kv_heads,
+                          size_t dim, size_t tail_cap, float* k_tail, float* v_tail,
+                          int* tail_len, cudaStream_t s) {
+    append_kernel<<<(unsigned)batch, 256, 0, s>>>(k_new, v_new, kv_heads, dim, tail_cap, k_tail, v_tail,
+                                                  tail_len);
+    note_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace kvqb

@@ -1,0 +1,697 @@
+// kvq_capi.cu — the C-ABI (include/kvq_capi.h): argument validation with the
+// reference's error classes, device memory management for the hybrid cache, and
+// dispatch to the K1/K2/K3 kernels. No compute happens on the host: every numeric
+// result comes out of a CUDA kernel, and a missing device is a hard KVQ_ERR_CUDA.
+#include <atomic>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "kvq_capi.h"
+#include "kvq_internal.cuh"
+
+namespace kvqb {
+static std::atomic<unsigned long long> g_launches{0};
+void note_launch(unsigned n) { g_launches += n; }
+unsigned long long launch_count() { return g_launches.load(); }
+}  // namespace kvqb
+
+namespace {
+
+using kvqb::codes_per_row;
+using kvqb::row_bytes;
+
+thread_local std::string g_err;
+
+struct Error {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void raise(int code, const std::string& msg) { throw Error{code, msg}; }
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) raise(KVQ_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void require_device() {
+    static int state = -1;  // -1 unknown, 0 none, 1 ok
+    if (state < 0) {
+        int n = 0;
+        cudaError_t e = cudaGetDeviceCount(&n);
+        state = (e == cudaSuccess && n > 0) ? 1 : 0;
+        if (e != cudaSuccess) cudaGetLastError();
+    }
+    if (state != 1) raise(KVQ_ERR_CUDA, "no usable CUDA device (this library has no CPU fallback)");
+}
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return KVQ_OK;
+    } catch (const Error& e) {
+        g_err = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return KVQ_ERR_CUDA;
+    }
+}
+
+// bitpack.hpp:141-149 (same messages as the reference).
+void validate_widths(int code_bits, int word_bits) {
+    if (code_bits < 1 || word_bits < 8 || word_bits > 32 || word_bits % 8 != 0)
+        raise(KVQ_ERR_CONFIG, "word bits must be 8, 16, or 32 and code bits >= 1");
+    if (word_bits % code_bits != 0)
+        raise(KVQ_ERR_CONFIG, "code bits " + std::to_string(code_bits) + " must divide word bits " +
+                                  std::to_string(word_bits));
+}
+
+// QuantizationConfig::validate (quantize.hpp:38-43).
+void validate_config(int bitwidth, int word_bits) {
+    if (bitwidth != 1 && bitwidth != 2 && bitwidth != 4 && bitwidth != 8)
+        raise(KVQ_ERR_CONFIG, "bitwidth must be 1, 2, 4, or 8");
+    validate_widths(bitwidth, word_bits);
+}
+
+// Codes wider than 16 bits have no defined level count in the reference
+// ((1u << 32) - 1 is UB at quantize.hpp:98); the quantizer entry points reject them.
+void validate_quant_bits(int bits, int word_bits) {
+    validate_widths(bits, word_bits);
+    if (bits > 16) raise(KVQ_ERR_CONFIG, "quantizer code bits must be <= 16");
+}
+
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    explicit DevBuf(size_t count) { alloc(count); }
+    void alloc(size_t count) {
+        release();
+        n = count;
+        if (count) ck(cudaMalloc(&p, sizeof(T) * count), "cudaMalloc");
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    ~DevBuf() { release(); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    void upload(const T* h, size_t count, cudaStream_t s = 0) {
+        if (count) ck(cudaMemcpyAsync(p, h, sizeof(T) * count, cudaMemcpyHostToDevice, s), "H2D");
+    }
+    void download(T* h, size_t count, cudaStream_t s = 0) const {
+        if (count) ck(cudaMemcpyAsync(h, p, sizeof(T) * count, cudaMemcpyDeviceToHost, s), "D2H");
+    }
+};
+
+void sync(cudaStream_t s) { ck(cudaStreamSynchronize(s), "kernel execution"); }
+
+}  // namespace
+
+// ------------------------------------------------------------------------------------
+struct kvq_cache {
+    size_t batch = 0, kv_heads = 0, group = 0, n_vis = 0, dim = 0, units = 0;
+    int bits = 8, mode = 0, word_bits = 8;
+    float tau1 = 0.f, tau2 = 0.f;
+    size_t rb = 0;
+    size_t n_tail = 0, tail_cap = 0;
+    int path = KVQ_PATH_AUTO;
+    cudaStream_t stream = nullptr;
+    DevBuf<uint8_t> codes;   // [2][units][n_vis][rb]  (K then V)
+    DevBuf<float> stats;     // [2 (K,V)][2 (alpha,beta)][units][dim]
+    DevBuf<float> k_tail, v_tail;  // [units][tail_cap][dim]
+    DevBuf<int> tail_len;    // [batch]
+    DevBuf<float> d_q, d_out, d_knew, d_vnew, scratch, weights;
+    DevBuf<int> viol;
+
+    uint8_t* k_codes() const { return codes.p; }
+    uint8_t* v_codes() const { return codes.p ? codes.p + units * n_vis * rb : nullptr; }
+    float* k_alpha() const { return stats.p; }
+    float* k_beta() const { return stats.p + units * dim; }
+    float* v_alpha() const { return stats.p + 2 * units * dim; }
+    float* v_beta() const { return stats.p + 3 * units * dim; }
+    size_t q_elems() const { return units * group * dim; }
+    ~kvq_cache() {
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
+namespace {
+
+void grow_tail(kvq_cache* c, size_t need) {
+    if (need <= c->tail_cap) return;
+    size_t cap = c->tail_cap ? c->tail_cap : 16;
+    while (cap < need) cap *= 2;
+    DevBuf<float> nk(c->units * cap * c->dim), nv(c->units * cap * c->dim);
+    if (c->n_tail) {
+        size_t w = c->n_tail * c->dim * sizeof(float);
+        ck(cudaMemcpy2DAsync(nk.p, cap * c->dim * sizeof(float), c->k_tail.p,
+                             c->tail_cap * c->dim * sizeof(float), w, c->units, cudaMemcpyDeviceToDevice,
+                             c->stream), "tail grow");
+        ck(cudaMemcpy2DAsync(nv.p, cap * c->dim * sizeof(float), c->v_tail.p,
+                             c->tail_cap * c->dim * sizeof(float), w, c->units, cudaMemcpyDeviceToDevice,
+                             c->stream), "tail grow");
+    }
+    sync(c->stream);
+    std::swap(c->k_tail.p, nk.p);
+    std::swap(c->k_tail.n, nk.n);
+    std::swap(c->v_tail.p, nv.p);
+    std::swap(c->v_tail.n, nv.n);
+    c->tail_cap = cap;
+    c->scratch.release();  // sized by tail_cap; rebuilt lazily
+}
+
+kvqb::DecodeArgs decode_args(kvq_cache* c, const float* q, float* out) {
+    kvqb::DecodeArgs a{};
+    a.k_codes = c->k_codes();
+    a.v_codes = c->v_codes();
+    a.k_alpha = c->k_alpha();
+    a.k_beta = c->k_beta();
+    a.v_alpha = c->v_alpha();
+    a.v_beta = c->v_beta();
+    a.k_tail = c->k_tail.p;
+    a.v_tail = c->v_tail.p;
+    a.tail_len = c->tail_len.p;
+    a.q = q;
+    a.out = out;
+    a.units = c->units;
+    a.kv_heads = c->kv_heads;
+    a.group = c->group;
+    a.dim = c->dim;
+    a.n_vis = c->n_vis;
+    a.tail_cap = c->tail_cap;
+    a.bits = c->bits == KVQ_FULL_PRECISION_BITS ? 8 : c->bits;
+    a.word_bits = c->word_bits;
+    a.tau1 = c->tau1;
+    a.tau2 = c->tau2;
+    return a;
+}
+
+void run_decode(kvq_cache* c, const float* q, float* out, bool want_weights, bool want_viol,
+                cudaStream_t s) {
+    kvqb::DecodeArgs a = decode_args(c, q, out);
+    bool tc_ok = kvqb::decode_tc_supported(a) && !want_weights && !want_viol;
+    if (c->path == KVQ_PATH_TC && !tc_ok)
+        raise(KVQ_ERR_CONFIG, "tensor-core decode path needs dim 128, 8-bit words, a quantized "
+                              "prefill and no weight/violation export");
+    if ((c->path == KVQ_PATH_AUTO || c->path == KVQ_PATH_TC) && tc_ok) {
+        ck(kvqb::launch_decode_tc(a, s), "decode (tc)");
+        return;
+    }
+    size_t need = c->units * c->group * (c->n_vis + c->tail_cap);
+    if (c->scratch.n < need) c->scratch.alloc(need);
+    a.scratch = c->scratch.p;
+    if (want_weights) {
+        size_t wl = c->units * c->group * (c->n_vis + c->n_tail);
+        if (c->weights.n < wl) c->weights.alloc(wl);
+        a.weights = c->weights.p;
+        a.weights_stride = c->n_vis + c->n_tail;
+    }
+    if (want_viol) {
+        if (c->viol.n < c->units * c->group) c->viol.alloc(c->units * c->group);
+        a.violations = c->viol.p;
+    }
+    ck(kvqb::launch_decode_generic(a, s), "decode (generic)");
+}
+
+kvq_cache* build_common(size_t batch, size_t kv_heads, size_t group, size_t n_vis, size_t dim,
+                        int bitwidth, int mode, int word_bits, float tau1, float tau2) {
+    require_device();
+    const bool full = bitwidth == KVQ_FULL_PRECISION_BITS;
+    if (!full) validate_config(bitwidth, word_bits);
+    if (mode != KVQ_MODE_CHANNEL_WISE && mode != KVQ_MODE_GLOBAL) raise(KVQ_ERR_CONFIG, "unknown quant mode");
+    // check_prefill (kvcache.hpp:224-236)
+    if (batch == 0 || kv_heads == 0) raise(KVQ_ERR_DOMAIN, "cache build: need matching per-head key/value lists");
+    if (group == 0) raise(KVQ_ERR_DOMAIN, "cache build: query group must be >= 1");
+    if (dim == 0) raise(KVQ_ERR_DOMAIN, "cache build: head dim must be positive");
+    auto* c = new kvq_cache;
+    c->batch = batch;
+    c->kv_heads = kv_heads;
+    c->group = group;
+    c->units = batch * kv_heads;
+    c->dim = dim;
+    c->bits = bitwidth;
+    c->mode = mode;
+    c->word_bits = full ? 8 : word_bits;
+    c->tau1 = full ? 0.f : tau1;
+    c->tau2 = full ? 0.f : tau2;
+    c->n_vis = full ? 0 : n_vis;
+    c->rb = row_bytes(dim, full ? 8 : bitwidth, c->word_bits);
+    ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+    c->stats.alloc(4 * c->units * dim);
+    ck(cudaMemsetAsync(c->stats.p, 0, sizeof(float) * c->stats.n, c->stream), "memset");
+    c->codes.alloc(2 * c->units * c->n_vis * c->rb);
+    c->tail_len.alloc(batch);
+    ck(cudaMemsetAsync(c->tail_len.p, 0, sizeof(int) * batch, c->stream), "memset");
+    c->d_q.alloc(c->q_elems());
+    c->d_out.alloc(c->q_elems());
+    c->d_knew.alloc(c->units * dim);
+    c->d_vnew.alloc(c->units * dim);
+    grow_tail(c, full ? (n_vis > 16 ? n_vis : 16) : 16);
+    return c;
+}
+
+// Quantize K and V prefill already on the device.
+void quantize_prefill(kvq_cache* c, const float* dk, const float* dv, cudaStream_t s) {
+    const size_t u = c->units, n = c->n_vis, d = c->dim;
+    const float* srcs[2] = {dk, dv};
+    for (int which = 0; which < 2; ++which) {
+        uint8_t* codes = which == 0 ? c->k_codes() : c->v_codes();
+        float* alpha = which == 0 ? c->k_alpha() : c->v_alpha();
+        float* beta = which == 0 ? c->k_beta() : c->v_beta();
+        if (kvqb::quantize_fused_supported(n, d, c->word_bits, c->mode)) {
+            ck(kvqb::launch_quantize_fused(srcs[which], u, n, d, c->bits, alpha, beta, codes, s), "quantize");
+        } else {
+            ck(kvqb::launch_compute_stats(srcs[which], u, n, d, c->mode, alpha, beta, s), "compute_stats");
+            ck(kvqb::launch_quantize_pack(srcs[which], u, n, d, alpha, beta, c->bits, c->word_bits, codes, s),
+               "quantize");
+        }
+    }
+}
+
+void fill_full_precision_tail(kvq_cache* c, const float* k, const float* v, size_t n, cudaMemcpyKind kind) {
+    const size_t d = c->dim;
+    if (n) {
+        ck(cudaMemcpy2DAsync(c->k_tail.p, c->tail_cap * d * sizeof(float), k, n * d * sizeof(float),
+                             n * d * sizeof(float), c->units, kind, c->stream), "tail fill");
+        ck(cudaMemcpy2DAsync(c->v_tail.p, c->tail_cap * d * sizeof(float), v, n * d * sizeof(float),
+                             n * d * sizeof(float), c->units, kind, c->stream), "tail fill");
+    }
+    std::vector<int> lens(c->batch, (int)n);
+    c->tail_len.upload(lens.data(), c->batch, c->stream);
+    c->n_tail = n;
+    sync(c->stream);
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t kvq_last_error(char* buf, size_t cap) {
+    if (buf && cap) {
+        size_t k = g_err.size() < cap - 1 ? g_err.size() : cap - 1;
+        std::memcpy(buf, g_err.data(), k);
+        buf[k] = '\0';
+    }
+    return g_err.size();
+}
+
+unsigned long long kvq_launch_count(void) { return kvqb::launch_count(); }
+
+int kvq_device_available(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n > 0 ? 1 : 0;
+}
+
+size_t kvq_packed_bytes(size_t count, int code_bits, int word_bits) {
+    if (code_bits < 1 || word_bits < 8 || word_bits % code_bits) return 0;
+    size_t g = (size_t)(word_bits / code_bits);
+    return (count + g - 1) / g * (size_t)(word_bits / 8);
+}
+
+int kvq_pack(const uint32_t* codes, size_t count, int code_bits, int word_bits, uint8_t* out,
+             size_t out_cap) {
+    return guarded([&] {
+        validate_widths(code_bits, word_bits);
+        size_t nbytes = kvq_packed_bytes(count, code_bits, word_bits);
+        if (out_cap < nbytes) raise(KVQ_ERR_DOMAIN, "pack: output buffer too small");
+        if (count == 0) return;
+        require_device();
+        DevBuf<uint32_t> dc(count);
+        DevBuf<uint8_t> db(nbytes);
+        DevBuf<int> flag(1);
+        dc.upload(codes, count);
+        ck(cudaMemsetAsync(flag.p, 0, sizeof(int)), "memset");
+        ck(kvqb::launch_pack_codes(dc.p, count, code_bits, word_bits, db.p, flag.p, 0), "pack");
+        int bad = 0;
+        flag.download(&bad, 1);
+        db.download(out, nbytes);
+        sync(0);
+        if (bad) {
+            // Report the first offending code, as the reference does (bitpack.hpp:178-181).
+            uint32_t limit = code_bits >= 32 ? 0xffffffffu : (1u << code_bits) - 1u;
+            for (size_t i = 0; i < count; ++i)
+                if (codes[i] > limit)
+                    raise(KVQ_ERR_DOMAIN, "code " + std::to_string(codes[i]) + " exceeds " +
+                                              std::to_string(code_bits) + "-bit range");
+        }
+    });
+}
+
+int kvq_unpack(const uint8_t* bytes, size_t byte_len, size_t count, int code_bits, int word_bits,
+               uint32_t* out) {
+    return guarded([&] {
+        validate_widths(code_bits, word_bits);
+        size_t nbytes = kvq_packed_bytes(count, code_bits, word_bits);
+        if (byte_len < nbytes) raise(KVQ_ERR_DOMAIN, "unpack: buffer shorter than logical_count implies");
+        if (count == 0) return;
+        require_device();
+        DevBuf<uint8_t> db(nbytes);
+        DevBuf<uint32_t> dc(count);
+        db.upload(bytes, nbytes);
+        ck(kvqb::launch_unpack_codes(db.p, count, code_bits, word_bits, dc.p, 0), "unpack");
+        dc.download(out, count);
+        sync(0);
+    });
+}
+
+size_t kvq_segment_bytes(size_t tokens, size_t dim, int bitwidth, int word_bits) {
+    if (bitwidth < 1 || word_bits < 8 || word_bits % bitwidth) return 0;
+    return tokens * row_bytes(dim, bitwidth, word_bits);
+}
+
+int kvq_compute_stats(const float* m, size_t rows, size_t cols, int mode, float* alpha, float* beta) {
+    return guarded([&] {
+        if (rows == 0 || cols == 0) raise(KVQ_ERR_DOMAIN, "compute_stats: empty matrix");
+        if (mode != KVQ_MODE_CHANNEL_WISE && mode != KVQ_MODE_GLOBAL) raise(KVQ_ERR_CONFIG, "unknown quant mode");
+        require_device();
+        DevBuf<float> dm(rows * cols), da(cols), dbt(cols);
+        dm.upload(m, rows * cols);
+        ck(kvqb::launch_compute_stats(dm.p, 1, rows, cols, mode, da.p, dbt.p, 0), "compute_stats");
+        da.download(alpha, cols);
+        dbt.download(beta, cols);
+        sync(0);
+    });
+}
+
+int kvq_quantize(const float* m, size_t rows, size_t cols, const float* alpha, const float* beta,
+                 int bitwidth, int word_bits, uint8_t* out, size_t out_cap) {
+    return guarded([&] {
+        validate_quant_bits(bitwidth, word_bits);
+        size_t nbytes = kvq_segment_bytes(rows, cols, bitwidth, word_bits);
+        if (out_cap < nbytes) raise(KVQ_ERR_DOMAIN, "quantize: output buffer too small");
+        if (nbytes == 0) return;
+        require_device();
+        DevBuf<float> dm(rows * cols), da(cols), dbt(cols);
+        DevBuf<uint8_t> dc(nbytes);
+        dm.upload(m, rows * cols);
+        da.upload(alpha, cols);
+        dbt.upload(beta, cols);
+        ck(kvqb::launch_quantize_pack(dm.p, 1, rows, cols, da.p, dbt.p, bitwidth, word_bits, dc.p, 0), "quantize");
+        dc.download(out, nbytes);
+        sync(0);
+    });
+}
+
+int kvq_dequantize(const uint8_t* codes, size_t rows, size_t cols, const float* alpha,
+                   const float* beta, int bitwidth, int word_bits, float* out) {
+    return guarded([&] {
+        validate_quant_bits(bitwidth, word_bits);
+        if (rows == 0 || cols == 0) return;
+        require_device();
+        size_t nbytes = kvq_segment_bytes(rows, cols, bitwidth, word_bits);
+        DevBuf<uint8_t> dc(nbytes);
+        DevBuf<float> da(cols), dbt(cols), dout(rows * cols);
+        dc.upload(codes, nbytes);
+        da.upload(alpha, cols);
+        dbt.upload(beta, cols);
+        ck(kvqb::launch_dequantize(dc.p, 1, rows, cols, da.p, dbt.p, bitwidth, word_bits, dout.p, 0), "dequantize");
+        dout.download(out, rows * cols);
+        sync(0);
+    });
+}
+
+int kvq_quantize_device(const float* x, size_t mats, size_t rows, size_t dim, int bitwidth, int mode,
+                        int word_bits, uint8_t* codes, float* alpha, float* beta, void* stream) {
+    return guarded([&] {
+        validate_config(bitwidth, word_bits);
+        if (rows == 0 || dim == 0) raise(KVQ_ERR_DOMAIN, "compute_stats: empty matrix");
+        require_device();
+        cudaStream_t s = (cudaStream_t)stream;
+        if (kvqb::quantize_fused_supported(rows, dim, word_bits, mode)) {
+            ck(kvqb::launch_quantize_fused(x, mats, rows, dim, bitwidth, alpha, beta, codes, s), "quantize");
+        } else {
+            ck(kvqb::launch_compute_stats(x, mats, rows, dim, mode, alpha, beta, s), "compute_stats");
+            ck(kvqb::launch_quantize_pack(x, mats, rows, dim, alpha, beta, bitwidth, word_bits, codes, s), "quantize");
+        }
+    });
+}
+
+int kvq_qk_scores(const float* queries, const uint8_t* codes, const float* alpha, const float* beta,
+                  size_t heads, size_t tokens, size_t dim, int bitwidth, int word_bits, float* scores) {
+    return guarded([&] {
+        validate_quant_bits(bitwidth, word_bits);
+        if (heads == 0 || tokens == 0) return;
+        if (dim == 0) raise(KVQ_ERR_DOMAIN, "qk_scores: zero head dim");
+        require_device();
+        size_t seg = kvq_segment_bytes(tokens, dim, bitwidth, word_bits);
+        DevBuf<float> dq(heads * dim), da(heads * dim), dbt(heads * dim), ds(heads * tokens);
+        DevBuf<uint8_t> dc(heads * seg);
+        dq.upload(queries, heads * dim);
+        da.upload(alpha, heads * dim);
+        dbt.upload(beta, heads * dim);
+        dc.upload(codes, heads * seg);
+        ck(kvqb::launch_qk_scores(dq.p, dc.p, da.p, dbt.p, heads, tokens, dim, bitwidth, word_bits, ds.p, 0),
+           "qk_scores");
+        ds.download(scores, heads * tokens);
+        sync(0);
+    });
+}
+
+int kvq_wv_output(const float* weights, const uint8_t* codes, const float* alpha, const float* beta,
+                  size_t heads, size_t tokens, size_t dim, int bitwidth, int word_bits, float* out) {
+    return guarded([&] {
+        validate_quant_bits(bitwidth, word_bits);
+        if (heads == 0 || dim == 0) return;
+        require_device();
+        size_t seg = kvq_segment_bytes(tokens, dim, bitwidth, word_bits);
+        DevBuf<float> dw(heads * tokens), da(heads * dim), dbt(heads * dim), dout(heads * dim);
+        DevBuf<uint8_t> dc(heads * seg);
+        dw.upload(weights, heads * tokens);
+        da.upload(alpha, heads * dim);
+        dbt.upload(beta, heads * dim);
+        dc.upload(codes, heads * seg);
+        ck(kvqb::launch_wv_output(dw.p, dc.p, da.p, dbt.p, heads, tokens, dim, bitwidth, word_bits, dout.p, 0),
+           "wv_output");
+        dout.download(out, heads * dim);
+        sync(0);
+    });
+}
+
+int kvq_calibrated_softmax_concat(const float* vis, size_t n_vis, const float* tail, size_t n_tail,
+                                  size_t rows, float tau1, float tau2, float* out,
+                                  size_t* slope_violations) {
+    return guarded([&] {
+        if (rows == 0 || n_vis + n_tail == 0) return;
+        require_device();
+        DevBuf<float> dv(rows * n_vis), dt(rows * n_tail), dout(rows * (n_vis + n_tail));
+        DevBuf<int> dviol(rows);
+        dv.upload(vis, rows * n_vis);
+        dt.upload(tail, rows * n_tail);
+        ck(kvqb::launch_calibrated_softmax(dv.p, n_vis, dt.p, n_tail, rows, tau1, tau2, dout.p, dviol.p, 0),
+           "calibrated_softmax_concat");
+        dout.download(out, rows * (n_vis + n_tail));
+        std::vector<int> v(rows);
+        dviol.download(v.data(), rows);
+        sync(0);
+        if (slope_violations)
+            for (int x : v) *slope_violations += (size_t)x;
+    });
+}
+
+int kvq_cache_build(const float* k_vis, const float* v_vis, size_t batch, size_t kv_heads, size_t group,
+                    size_t n_vis, size_t dim, int bitwidth, int mode, int word_bits, float tau1, float tau2,
+                    kvq_cache** out) {
+    return guarded([&] {
+        *out = nullptr;
+        kvq_cache* c = build_common(batch, kv_heads, group, n_vis, dim, bitwidth, mode, word_bits, tau1, tau2);
+        try {
+            const size_t elems = c->units * n_vis * dim;
+            if (bitwidth == KVQ_FULL_PRECISION_BITS) {
+                fill_full_precision_tail(c, k_vis, v_vis, n_vis, cudaMemcpyHostToDevice);
+            } else if (n_vis > 0) {
+                DevBuf<float> dk(elems), dv(elems);
+                dk.upload(k_vis, elems, c->stream);
+                dv.upload(v_vis, elems, c->stream);
+                quantize_prefill(c, dk.p, dv.p, c->stream);
+                sync(c->stream);
+            }
+            sync(c->stream);
+        } catch (...) {
+            delete c;
+            throw;
+        }
+        *out = c;
+    });
+}
+
+int kvq_cache_build_device(const float* k_vis, const float* v_vis, size_t batch, size_t kv_heads,
+                           size_t group, size_t n_vis, size_t dim, int bitwidth, int mode, int word_bits,
+                           float tau1, float tau2, void* stream, kvq_cache** out) {
+    return guarded([&] {
+        *out = nullptr;
+        kvq_cache* c = build_common(batch, kv_heads, group, n_vis, dim, bitwidth, mode, word_bits, tau1, tau2);
+        try {
+            sync(c->stream);
+            cudaStream_t s = (cudaStream_t)stream;
+            if (bitwidth == KVQ_FULL_PRECISION_BITS) {
+                ck(cudaStreamSynchronize(s), "sync");
+                fill_full_precision_tail(c, k_vis, v_vis, n_vis, cudaMemcpyDeviceToDevice);
+            } else if (n_vis > 0) {
+                quantize_prefill(c, k_vis, v_vis, s);
+                ck(cudaStreamSynchronize(s), "quantize");
+            }
+        } catch (...) {
+            delete c;
+            throw;
+        }
+        *out = c;
+    });
+}
+
+void kvq_cache_free(kvq_cache* c) { delete c; }
+
+int kvq_cache_reserve_tail(kvq_cache* c, size_t rows) {
+    return guarded([&] { grow_tail(c, rows); });
+}
+
+int kvq_cache_set_path(kvq_cache* c, int path) {
+    return guarded([&] {
+        if (path < KVQ_PATH_AUTO || path > KVQ_PATH_TC) raise(KVQ_ERR_CONFIG, "unknown decode path");
+        c->path = path;
+    });
+}
+
+int kvq_cache_append(kvq_cache* c, const float* k_new, const float* v_new) {
+    return guarded([&] {
+        grow_tail(c, c->n_tail + 1);
+        c->d_knew.upload(k_new, c->units * c->dim, c->stream);
+        c->d_vnew.upload(v_new, c->units * c->dim, c->stream);
+        ck(kvqb::launch_append(c->d_knew.p, c->d_vnew.p, c->batch, c->kv_heads, c->dim, c->tail_cap,
+                               c->k_tail.p, c->v_tail.p, c->tail_len.p, c->stream), "append");
+        sync(c->stream);
+        c->n_tail += 1;
+    });
+}
+
+int kvq_cache_append_device(kvq_cache* c, const float* k_new, const float* v_new, void* stream) {
+    return guarded([&] {
+        if (c->n_tail + 1 > c->tail_cap) {
+            ck(cudaStreamSynchronize((cudaStream_t)stream), "sync");
+            grow_tail(c, c->n_tail + 1);
+        }
+        ck(kvqb::launch_append(k_new, v_new, c->batch, c->kv_heads, c->dim, c->tail_cap, c->k_tail.p,
+                               c->v_tail.p, c->tail_len.p, (cudaStream_t)stream), "append");
+        c->n_tail += 1;
+    });
+}
+
+int kvq_cache_decode(kvq_cache* c, const float* queries, float* out, float* weights, size_t* slope_violations) {
+    return guarded([&] {
+        c->d_q.upload(queries, c->q_elems(), c->stream);
+        run_decode(c, c->d_q.p, c->d_out.p, weights != nullptr, slope_violations != nullptr, c->stream);
+        c->d_out.download(out, c->q_elems(), c->stream);
+        std::vector<int> v;
+        if (weights) {
+            size_t wl = c->units * c->group * (c->n_vis + c->n_tail);
+            c->weights.download(weights, wl, c->stream);
+        }
+        if (slope_violations) {
+            v.resize(c->units * c->group);
+            c->viol.download(v.data(), v.size(), c->stream);
+        }
+        sync(c->stream);
+        if (slope_violations)
+            for (int x : v) *slope_violations += (size_t)x;
+    });
+}
+
+int kvq_cache_decode_device(kvq_cache* c, const float* queries, float* out, void* stream) {
+    return guarded([&] { run_decode(c, queries, out, false, false, (cudaStream_t)stream); });
+}
+
+int kvq_cache_step(kvq_cache* c, const float* queries, const float* k_new, const float* v_new, float* out) {
+    return guarded([&] {
+        grow_tail(c, c->n_tail + 1);
+        cudaStream_t s = c->stream;
+        c->d_q.upload(queries, c->q_elems(), s);
+        c->d_knew.upload(k_new, c->units * c->dim, s);
+        c->d_vnew.upload(v_new, c->units * c->dim, s);
+        run_decode(c, c->d_q.p, c->d_out.p, false, false, s);
+        ck(kvqb::launch_append(c->d_knew.p, c->d_vnew.p, c->batch, c->kv_heads, c->dim, c->tail_cap,
+                               c->k_tail.p, c->v_tail.p, c->tail_len.p, s), "append");
+        c->d_out.download(out, c->q_elems(), s);
+        sync(s);
+        c->n_tail += 1;
+    });
+}
+
+int kvq_cache_info(const kvq_cache* c, size_t info[10]) {
+    info[0] = c->batch;
+    info[1] = c->kv_heads;
+    info[2] = c->group;
+    info[3] = c->dim;
+    info[4] = c->n_vis;
+    info[5] = c->n_tail;
+    info[6] = (size_t)c->bits;
+    info[7] = (size_t)c->word_bits;
+    info[8] = (size_t)c->mode;
+    info[9] = c->tail_cap;
+    return KVQ_OK;
+}
+
+int kvq_cache_calibration(const kvq_cache* c, float tau[2]) {
+    tau[0] = c->tau1;
+    tau[1] = c->tau2;
+    return KVQ_OK;
+}
+
+int kvq_cache_memory(const kvq_cache* c, size_t mem[6]) {
+    // HybridKVCache::memory (kvcache.hpp:123-135), summed over every unit.
+    mem[0] = 2 * c->units * c->n_vis * c->rb;
+    mem[1] = c->units * 4 * 4 * c->dim;
+    mem[2] = mem[0] + mem[1];
+    mem[3] = c->units * 2 * c->n_tail * c->dim * 4;
+    mem[4] = c->units * 2 * c->n_vis * c->dim * 4;
+    mem[5] = mem[2] + mem[3];
+    return KVQ_OK;
+}
+
+int kvq_cache_read_segment(const kvq_cache* c, size_t unit, int which, uint8_t* bytes, float* alpha, float* beta) {
+    return guarded([&] {
+        if (unit >= c->units) raise(KVQ_ERR_DOMAIN, "segment index out of range");
+        const size_t seg = c->n_vis * c->rb;
+        const uint8_t* src = (which == 0 ? c->k_codes() : c->v_codes());
+        if (seg && bytes) ck(cudaMemcpyAsync(bytes, src + unit * seg, seg, cudaMemcpyDeviceToHost, c->stream), "D2H");
+        const float* a = (which == 0 ? c->k_alpha() : c->v_alpha()) + unit * c->dim;
+        const float* b = (which == 0 ? c->k_beta() : c->v_beta()) + unit * c->dim;
+        if (alpha) ck(cudaMemcpyAsync(alpha, a, c->dim * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+        if (beta) ck(cudaMemcpyAsync(beta, b, c->dim * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+        sync(c->stream);
+    });
+}
+
+int kvq_cache_read_tail(const kvq_cache* c, size_t unit, int which, float* out) {
+    return guarded([&] {
+        if (unit >= c->units) raise(KVQ_ERR_DOMAIN, "tail index out of range");
+        const float* src = (which == 0 ? c->k_tail.p : c->v_tail.p) + unit * c->tail_cap * c->dim;
+        if (c->n_tail)
+            ck(cudaMemcpyAsync(out, src, c->n_tail * c->dim * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+        sync(c->stream);
+    });
+}
+
+int kvq_cache_device_pointers(const kvq_cache* c, void* ptrs[9]) {
+    ptrs[0] = c->k_codes();
+    ptrs[1] = c->v_codes();
+    ptrs[2] = c->k_alpha();
+    ptrs[3] = c->k_beta();
+    ptrs[4] = c->v_alpha();
+    ptrs[5] = c->v_beta();
+    ptrs[6] = c->k_tail.p;
+    ptrs[7] = c->v_tail.p;
+    ptrs[8] = c->tail_len.p;
+    return KVQ_OK;
+}
+
+}  // extern "C"

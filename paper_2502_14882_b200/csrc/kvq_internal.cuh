@@ -1,0 +1,99 @@
+// kvq_internal.cuh — shared device-side declarations for the B200 kvq kernels.
+//
+// Layout contract (HBM), one "unit" = one (request, KV head) pair, u = b * kv_heads + h:
+//   codes  [unit][n_vis][row_bytes]   reference byte layout (MSB-first codes in LE
+//                                     M-bit words, rows padded to whole words;
+//                                     bitpack.hpp:161-187, quantize.hpp:53-61)
+//   alpha/beta [unit][dim] fp32        per-channel min/max (quantize.hpp:24-29)
+//   tail   [unit][tail_cap][dim] fp32  append-only generated tokens (kvcache.hpp:99-109)
+//   tail_len [batch] int32             device-resident so decode/append graph-capture
+//   queries/out [unit][group][dim]     GQA: q head h*G+g reads KV head h
+#pragma once
+#include <cuda_runtime.h>
+#include <cstddef>
+#include <cstdint>
+
+namespace kvqb {
+
+// Status codes of the C-ABI (include/kvq_capi.h).
+enum Status : int { OK = 0, CONFIG = 1, DOMAIN = 2, FORMAT = 3, CUDA = 4 };
+
+__host__ __device__ inline int codes_per_word(int bits, int word_bits) { return word_bits / bits; }
+__host__ __device__ inline size_t codes_per_row(size_t dim, int bits, int word_bits) {
+    size_t g = (size_t)codes_per_word(bits, word_bits);
+    return (dim + g - 1) / g * g;
+}
+__host__ __device__ inline size_t row_bytes(size_t dim, int bits, int word_bits) {
+    return codes_per_row(dim, bits, word_bits) / (size_t)codes_per_word(bits, word_bits) *
+           (size_t)(word_bits / 8);
+}
+
+// ---- K1: stats + quantize + pack ------------------------------------------
+// x: [mats][rows][dim] fp32 (device). Writes alpha/beta [mats][dim] and codes
+// [mats][rows][row_bytes]. mode 0 = channel_wise, 1 = global.
+cudaError_t launch_compute_stats(const float* x, size_t mats, size_t rows, size_t dim, int mode,
+                                 float* alpha, float* beta, cudaStream_t s);
+cudaError_t launch_quantize_pack(const float* x, size_t mats, size_t rows, size_t dim,
+                                 const float* alpha, const float* beta, int bits, int word_bits,
+                                 uint8_t* codes, cudaStream_t s);
+// Fused single-pass K1 for d = 128, M = 8 (cluster exchange of partial stats).
+bool quantize_fused_supported(size_t rows, size_t dim, int word_bits, int mode);
+cudaError_t launch_quantize_fused(const float* x, size_t mats, size_t rows, size_t dim, int bits,
+                                  float* alpha, float* beta, uint8_t* codes, cudaStream_t s);
+// Generic bit packing of explicit u32 codes (bitpack.hpp:161-187). err_flag set to 1 on
+// an out-of-range code.
+cudaError_t launch_pack_codes(const uint32_t* codes, size_t count, int bits, int word_bits,
+                              uint8_t* out, int* err_flag, cudaStream_t s);
+cudaError_t launch_unpack_codes(const uint8_t* bytes, size_t count, int bits, int word_bits,
+                                uint32_t* out, cudaStream_t s);
+cudaError_t launch_dequantize(const uint8_t* codes, size_t mats, size_t rows, size_t dim,
+                              const float* alpha, const float* beta, int bits, int word_bits,
+                              float* out, cudaStream_t s);
+
+// ---- K2: decode --------------------------------------------------------------
+struct DecodeArgs {
+    const uint8_t* k_codes;
+    const uint8_t* v_codes;
+    const float* k_alpha;
+    const float* k_beta;
+    const float* v_alpha;
+    const float* v_beta;
+    const float* k_tail;
+    const float* v_tail;
+    const int* tail_len;  // [batch]
+    const float* q;       // [units][group][dim]
+    float* out;           // [units][group][dim]
+    float* weights;       // nullable: [units][group][n_vis + tail_stride] probability rows
+    int* violations;      // nullable: [units][group] g slope-violation flags
+    float* scratch;       // generic path: [units][group][n_vis + tail_cap] score rows
+    size_t units, kv_heads, group, dim, n_vis, tail_cap, weights_stride;
+    int bits, word_bits;
+    float tau1, tau2;
+};
+cudaError_t launch_decode_generic(const DecodeArgs& a, cudaStream_t s);
+bool decode_tc_supported(const DecodeArgs& a);
+cudaError_t launch_decode_tc(const DecodeArgs& a, cudaStream_t s);
+
+// Post-scaled q.K (kernels.hpp:302-363) and w.V (316-396) over `heads` segments.
+cudaError_t launch_qk_scores(const float* q, const uint8_t* codes, const float* alpha,
+                             const float* beta, size_t heads, size_t tokens, size_t dim,
+                             int bits, int word_bits, float* scores, cudaStream_t s);
+cudaError_t launch_wv_output(const float* w, const uint8_t* codes, const float* alpha,
+                             const float* beta, size_t heads, size_t tokens, size_t dim,
+                             int bits, int word_bits, float* out, cudaStream_t s);
+// calibrated_softmax_concat (calibrate.hpp:100-114) over `rows` independent rows.
+cudaError_t launch_calibrated_softmax(const float* vis, size_t n_vis, const float* tail,
+                                      size_t n_tail, size_t rows, float tau1, float tau2,
+                                      float* out, int* violations, cudaStream_t s);
+
+// ---- K3: append --------------------------------------------------------------
+cudaError_t launch_append(const float* k_new, const float* v_new, size_t batch, size_t kv_heads,
+                          size_t dim, size_t tail_cap, float* k_tail, float* v_tail,
+                          int* tail_len, cudaStream_t s);
+
+// ---- misc -------------------------------------------------------------------------
+// Number of this library's kernels launched so far (bench.py's gpu_launches claim).
+unsigned long long launch_count();
+void note_launch(unsigned n = 1);
+
+}  // namespace kvqb

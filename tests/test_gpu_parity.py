@@ -1,0 +1,381 @@
+"""GPU parity: the CUDA kernels, called through the C-ABI (include/kvq_capi.h via
+paper_2502_14882_b200/kvq.py), against the golden fixtures from the unmodified reference
+and against the pinned C restatement (oracle/).
+
+Bars (written here):
+  * K1 codes, alpha, beta: BIT-EXACT (byte / uint32 equality, incl. the sign of zero).
+  * K3 append: bit-exact tail rows; packed codes untouched.
+  * K2 generic path (any shape): relative L2 <= TOL_GENERIC vs the reference output.
+  * K2 tensor-core path (d = 128): relative L2 <= TOL_TC (north_star: <= 1e-3).
+  * probability rows: |w - w_ref| <= 1e-5 elementwise, rows sum to 1 +- 1e-5
+    (test_kvcache.cpp:161-182).
+"""
+import hashlib
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+GOLD = Path(__file__).resolve().parent / "golden"
+TOL_GENERIC = 2e-5
+TOL_TC = 1e-4
+
+
+def bits_eq(a, b):
+    a = np.ascontiguousarray(a, np.float32).view(np.uint32)
+    b = np.ascontiguousarray(b, np.float32).view(np.uint32)
+    return a.shape == b.shape and np.array_equal(a, b)
+
+
+def rel_l2(got, want):
+    got, want = np.asarray(got, np.float64), np.asarray(want, np.float64)
+    return float(np.linalg.norm(got - want) / max(np.linalg.norm(want), 1e-30))
+
+
+# ---- K1 -----------------------------------------------------------------------------------
+
+def test_pack_golden_vectors(kvq):
+    # test_bitpack.cpp:12-52
+    assert kvq.pack([3, 1, 0, 2], 2).bytes.tolist() == [210]
+    assert kvq.pack([1, 0, 1, 1, 0, 0, 1, 0], 1).bytes.tolist() == [178]
+    b = kvq.pack([1, 2, 3], 4, 16)
+    assert b.word_at(0) == 0x1230 and b.bytes.tolist() == [0x30, 0x12]
+    b = kvq.pack([3, 3, 3, 3, 3], 2, 8)
+    assert b.bytes.tolist() == [0xFF, 0xC0] and kvq.unpack(b).tolist() == [3] * 5
+    assert kvq.pack(np.zeros(0, np.uint32), 4).byte_size() == 0
+    with pytest.raises(kvq.DomainError):
+        kvq.pack([4], 2, 8)
+    with pytest.raises(kvq.ConfigError):
+        kvq.pack([1], 1, 64)
+
+
+def test_pack_exhaustive_and_random(kvq, oracle):
+    for n, m in [(1, 8), (2, 8), (4, 8), (8, 8), (1, 16), (2, 16)]:
+        g = m // n
+        words = np.arange(1 << m, dtype=np.uint32)
+        codes = np.stack([(words >> (m - n * (k + 1))) & ((1 << n) - 1) for k in range(g)], 1).reshape(-1)
+        buf = kvq.pack(codes, n, m)
+        assert np.array_equal(buf.bytes, oracle.pack(codes, n, m)[1])
+        assert np.array_equal(kvq.unpack(buf), codes)
+    rng = np.random.default_rng(42)
+    for n in (1, 2, 4, 8):
+        for m in (8, 16, 32):
+            codes = rng.integers(0, 1 << n, size=int(rng.integers(0, 200))).astype(np.uint32)
+            buf = kvq.pack(codes, n, m)
+            assert np.array_equal(buf.bytes, oracle.pack(codes, n, m)[1])
+            assert np.array_equal(kvq.unpack(buf), codes)
+
+
+def test_quantize_golden_fixtures(kvq):
+    z = np.load(GOLD / "quant_cases.npz")
+    for i in range(int(z["count"])):
+        bits, wb, mode = z[f"c{i}_meta"].tolist()
+        x = z[f"c{i}_x"]
+        if mode >= 0:
+            st = kvq.compute_stats(x, kvq.QuantMode(mode))
+            assert bits_eq(st.alpha, z[f"c{i}_alpha"]) and bits_eq(st.beta, z[f"c{i}_beta"]), f"stats {i}"
+        seg = kvq.quantize(x, kvq.ChannelStats(z[f"c{i}_alpha"], z[f"c{i}_beta"]), bits, wb)
+        assert np.array_equal(seg.codes.bytes, z[f"c{i}_codes"]), f"codes {i} bits={bits} M={wb}"
+
+
+def test_quantize_hand_values(kvq):
+    # test_quantize.cpp:47-67, 69-80, 169-187
+    def q1(x, a, b, bits):
+        seg = kvq.quantize(np.array([[x]], np.float32), kvq.ChannelStats(np.array([a], np.float32),
+                                                                          np.array([b], np.float32)), bits)
+        return int(kvq.unpack(seg.codes)[0])
+
+    assert q1(1.4, 0, 3, 2) == 1 and q1(0.1, -2, 2, 1) == 1
+    assert [q1(x, 0, 3, 2) for x in (0.5, 1.5, 2.5)] == [1, 2, 3]
+    m = np.array([[4, 1], [4, 2], [4, 3]], np.float32)
+    seg = kvq.quantize(m, kvq.compute_stats(m), 2)
+    assert kvq.dequantize(seg)[:, 0].tolist() == [4, 4, 4]
+    rng = np.random.default_rng(9)
+    seg = kvq.quantize(rng.uniform(-1, 1, (3, 5)).astype(np.float32),
+                       kvq.compute_stats(rng.uniform(-1, 1, (3, 5)).astype(np.float32)), 2)
+    assert seg.codes_per_row() == 8 and seg.words_per_row() == 2 and seg.codes.logical_count == 24
+    codes = kvq.unpack(seg.codes).reshape(3, 8)
+    assert (codes[:, 5:] == 0).all()
+
+
+@pytest.mark.parametrize("bits", [1, 2, 4, 8])
+def test_quantize_device_matches_oracle_d128(kvq, oracle, bits):
+    """Batched device K1 (the cache build path, incl. the fused d = 128 kernel) is
+    bit-exact against the oracle on every unit."""
+    import torch
+    rng = np.random.default_rng(bits)
+    mats, n, d = 6, 777, 128
+    x = rng.normal(size=(mats, n, d)).astype(np.float32)
+    x[0, :, 3] = 0.5  # degenerate channel
+    x[1, 10, 7], x[1, 11, 7] = -0.0, 0.0
+    xd = torch.from_numpy(x).cuda()
+    rb = d * bits // 8
+    codes = torch.zeros(mats * n * rb, dtype=torch.uint8, device="cuda")
+    alpha = torch.zeros(mats * d, dtype=torch.float32, device="cuda")
+    beta = torch.zeros_like(alpha)
+    kvq._check(kvq.lib().kvq_quantize_device(xd.data_ptr(), mats, n, d, bits, 0, 8, codes.data_ptr(),
+                                             alpha.data_ptr(), beta.data_ptr(), 0))
+    torch.cuda.synchronize()
+    codes, alpha, beta = codes.cpu().numpy().reshape(mats, -1), alpha.cpu().numpy().reshape(mats, d), \
+        beta.cpu().numpy().reshape(mats, d)
+    for m in range(mats):
+        a, b = oracle.compute_stats(x[m])
+        assert bits_eq(alpha[m], a) and bits_eq(beta[m], b)
+        assert np.array_equal(codes[m], oracle.quantize(x[m], a, b, bits, 8)), f"unit {m}"
+
+
+# ---- standalone kernels.hpp / calibrate.hpp -------------------------------------------------
+
+def test_kernel_golden_fixtures(kvq):
+    z = np.load(GOLD / "kernels.npz")
+    for i in range(int(z["count"])):
+        bits, wb, tokens, dim = z[f"k{i}_meta"].tolist()
+        g = wb // bits
+        seg = kvq.QuantizedSegment(kvq.PackedBuffer(z[f"k{i}_codes"], bits, wb, tokens * ((dim + g - 1) // g * g)),
+                                   kvq.ChannelStats(z[f"k{i}_alpha"], z[f"k{i}_beta"]), tokens, dim, bits)
+        s = kvq.qk_scores(z[f"k{i}_q"], seg)
+        want = z[f"k{i}_scores"]
+        assert np.all(np.abs(s - want) <= 1e-5 * max(np.abs(want).max(), 1e-6)), f"qk {i}"
+        o = kvq.wv_output(z[f"k{i}_w"], seg)
+        want = z[f"k{i}_wv"]
+        assert np.all(np.abs(o - want) <= 1e-5 * max(np.abs(want).max(), 1e-6)), f"wv {i}"
+    for j in range(int(z["scount"])):
+        t1, t2 = z[f"s{j}_tau"].tolist()
+        row, viol = kvq.calibrated_softmax_concat(z[f"s{j}_vis"], z[f"s{j}_tail"], kvq.CalibrationParams(t1, t2),
+                                                  with_violations=True)
+        assert np.allclose(row, z[f"s{j}_row"], rtol=1e-5, atol=1e-7), f"softmax {j}"
+        assert viol == int(z[f"s{j}_viol"])
+
+
+def test_kernel_hand_values(kvq):
+    # test_kernels.cpp:30-46, 111-136
+    k = np.array([[1.0, 0.0]], np.float32)
+    seg = kvq.quantize(k, kvq.ChannelStats(np.zeros(2, np.float32), np.ones(2, np.float32)), 1)
+    assert kvq.qk_scores(np.array([2, 3], np.float32), seg).tolist() == [2.0]
+    rng = np.random.default_rng(6)
+    m = rng.uniform(-2, 2, (9, 11)).astype(np.float32)
+    seg = kvq.quantize(m, kvq.compute_stats(m), 4)
+    deq = kvq.dequantize(seg)
+    for j in (0, 4, 8):
+        w = np.zeros(9, np.float32)
+        w[j] = 1
+        assert np.array_equal(kvq.wv_output(w, seg), deq[j])
+    assert np.all(kvq.qk_scores(np.zeros(11, np.float32), seg) == 0)
+    with pytest.raises(kvq.DomainError):
+        kvq.qk_scores(np.zeros(3, np.float32), seg)
+    with pytest.raises(kvq.ConfigError):
+        kvq.qk_scores(np.zeros(11, np.float32), seg, kvq.KernelConfig(0, 1, 1))
+
+
+# ---- K2/K3 through the single-sequence drop-in (HybridKVCache) -------------------------------
+
+def _load_inputs(z, oracle):
+    h, n, d = z["meta"][:3].tolist()
+    if "k" in z:
+        return z["k"], z["v"]
+    ks, vs = zip(*[oracle.generate_head(int(z["seed"]), hh, n, d)[:2] for hh in range(h)])
+    k, v = np.stack(ks), np.stack(vs)
+    assert hashlib.sha256(k.tobytes() + v.tobytes()).hexdigest() == str(z["sha256"])
+    return k, v
+
+
+@pytest.mark.parametrize("name", sorted(p.name for p in GOLD.glob("decode_*.npz")))
+@pytest.mark.parametrize("path", ["generic", "auto"])
+def test_decode_golden_trajectories(kvq, oracle, name, path):
+    z = np.load(GOLD / name)
+    h, n, d, bits, wb, steps = z["meta"].tolist()
+    t1, t2 = z["tau"].tolist()
+    k, v = _load_inputs(z, oracle)
+    if bits == 16:
+        cache = kvq.HybridKVCache.build_full_precision(list(k), list(v))
+    else:
+        cache = kvq.HybridKVCache.build(list(k), list(v), kvq.QuantizationConfig(bits, kvq.QuantMode.channel_wise, wb),
+                                        kvq.CalibrationParams(t1, t2))
+    cache.batched.set_path(kvq.PATH_GENERIC if path == "generic" else kvq.PATH_AUTO)
+    if bits != 16 and n:
+        for hh in range(h):
+            ks, vs = cache.key_segment(hh), cache.value_segment(hh)
+            assert np.array_equal(ks.codes.bytes, z[f"kcodes{hh}"]) and np.array_equal(vs.codes.bytes, z[f"vcodes{hh}"])
+            assert bits_eq(ks.stats.alpha, z[f"kalpha{hh}"]) and bits_eq(vs.stats.beta, z[f"vbeta{hh}"])
+    assert list(vars(cache.memory()).values()) == z["memory0"].tolist()
+    tol = TOL_GENERIC if path == "generic" else TOL_TC
+    for t in range(steps):
+        out = cache.decode_step(z[f"q{t}"])
+        assert rel_l2(out, z[f"out{t}"]) <= tol, f"{name} step {t}: {rel_l2(out, z[f'out{t}'])}"
+        det = cache.decode_step_detailed(z[f"q{t}"])
+        assert np.all(np.abs(det.weights - z[f"w{t}"]) <= 1e-5)
+        assert np.all(np.abs(det.weights.sum(1) - 1) <= 1e-5)
+        assert det.slope_violations == int(z[f"viol{t}"])
+        assert rel_l2(det.outputs, z[f"out{t}"]) <= TOL_GENERIC
+        cache.append(z[f"knew{t}"], z[f"vnew{t}"])
+    assert list(vars(cache.memory()).values()) == z["memory_end"].tolist()
+    for hh in range(h):
+        tail = cache.key_tail(hh)
+        want = np.stack([z[f"knew{t}"][hh] for t in range(steps)])
+        if bits == 16:
+            want = np.concatenate([k[hh], want])
+        assert bits_eq(tail, want)
+
+
+def test_append_never_touches_codes(kvq):
+    # test_kvcache.cpp:112-140
+    rng = np.random.default_rng(3)
+    k = rng.uniform(-2, 2, (2, 20, 6)).astype(np.float32)
+    v = rng.uniform(-2, 2, (2, 20, 6)).astype(np.float32)
+    cache = kvq.HybridKVCache.build(list(k), list(v), kvq.QuantizationConfig(2), kvq.CalibrationParams())
+    before = [cache.key_segment(h).codes.bytes.copy() for h in range(2)]
+    kn = rng.uniform(-9, 9, (2, 6)).astype(np.float32)
+    vn = rng.uniform(-9, 9, (2, 6)).astype(np.float32)
+    cache.append(kn, vn)
+    cache.append(vn, kn)
+    assert cache.tail_tokens() == 2
+    for h in range(2):
+        assert np.array_equal(cache.key_segment(h).codes.bytes, before[h])
+        assert cache.key_tail(h)[0, 0] == kn[h, 0] and cache.key_tail(h)[1, 0] == vn[h, 0]
+    with pytest.raises(kvq.DomainError):
+        cache.append(np.zeros((2, 7), np.float32), np.zeros((2, 7), np.float32))
+
+
+def test_tail_growth_many_appends(kvq, oracle):
+    """Appends beyond the initial tail capacity (16) regrow the device tail."""
+    rng = np.random.default_rng(4)
+    h, n, d = 2, 30, 16
+    k = rng.uniform(-1, 1, (h, n, d)).astype(np.float32)
+    v = rng.uniform(-1, 1, (h, n, d)).astype(np.float32)
+    cache = kvq.HybridKVCache.build(list(k), list(v), kvq.QuantizationConfig(4), kvq.CalibrationParams(1, 0))
+    kt, vt = [], []
+    for t in range(40):
+        kn = rng.uniform(-1, 1, (h, d)).astype(np.float32)
+        vn = rng.uniform(-1, 1, (h, d)).astype(np.float32)
+        cache.append(kn, vn)
+        kt.append(kn)
+        vt.append(vn)
+    q = rng.uniform(-1, 1, (h, d)).astype(np.float32)
+    out = cache.decode_step(q)
+    for hh in range(h):
+        ka, kb = oracle.compute_stats(k[hh])
+        va, vb = oracle.compute_stats(v[hh])
+        want, _, _ = oracle.decode_head(q[hh], n, 4, 8, oracle.quantize(k[hh], ka, kb, 4), ka, kb,
+                                        oracle.quantize(v[hh], va, vb, 4), va, vb,
+                                        np.stack([x[hh] for x in kt]), np.stack([x[hh] for x in vt]), 1.0, 0.0)
+        assert rel_l2(out[hh], want) <= TOL_GENERIC
+
+
+def test_decisive_appended_token(kvq):
+    # test_kvcache.cpp:142-159
+    rng = np.random.default_rng(4)
+    k = rng.uniform(-1, 1, (1, 16, 8)).astype(np.float32)
+    v = rng.uniform(-1, 1, (1, 16, 8)).astype(np.float32)
+    cache = kvq.HybridKVCache.build(list(k), list(v), kvq.QuantizationConfig(2), kvq.CalibrationParams())
+    kn = np.zeros((1, 8), np.float32)
+    kn[0, 0] = 30
+    vn = (np.arange(8, dtype=np.float32) - 3)[None]
+    cache.append(kn, vn)
+    q = np.zeros((1, 8), np.float32)
+    q[0, 0] = 30
+    assert np.all(np.abs(cache.decode_step(q)[0] - vn[0]) <= 1e-4)
+
+
+def test_identical_heads_and_determinism(kvq):
+    # test_kvcache.cpp:184-203, 259-270
+    rng = np.random.default_rng(6)
+    k = rng.uniform(-2, 2, (24, 8)).astype(np.float32)
+    v = rng.uniform(-2, 2, (24, 8)).astype(np.float32)
+    cache = kvq.HybridKVCache.build([k] * 3, [v] * 3, kvq.QuantizationConfig(4), kvq.CalibrationParams(1, 1))
+    q = np.tile(rng.uniform(-1, 1, 8).astype(np.float32), (3, 1))
+    out = cache.decode_step(q)
+    assert np.array_equal(out[1], out[0]) and np.array_equal(out[2], out[0])
+    for cfg in (kvq.KernelConfig(4, 16, 1), kvq.KernelConfig(1, 1, 8)):
+        assert np.array_equal(cache.decode_step(q, cfg), out)
+
+
+def test_error_classes(kvq):
+    with pytest.raises(kvq.ConfigError):
+        kvq.HybridKVCache.build([np.ones((4, 8), np.float32)], [np.ones((4, 8), np.float32)],
+                                kvq.QuantizationConfig(3), kvq.CalibrationParams())
+    with pytest.raises(kvq.DomainError):
+        kvq.HybridKVCache.build([], [], kvq.QuantizationConfig(1), kvq.CalibrationParams())
+    with pytest.raises(kvq.DomainError):
+        kvq.HybridKVCache.build([np.ones((4, 8), np.float32), np.ones((5, 8), np.float32)],
+                                [np.ones((4, 8), np.float32)] * 2, kvq.QuantizationConfig(1), kvq.CalibrationParams())
+    cache = kvq.HybridKVCache.build([np.ones((4, 8), np.float32)], [np.ones((4, 8), np.float32)],
+                                    kvq.QuantizationConfig(1), kvq.CalibrationParams())
+    with pytest.raises(kvq.DomainError):
+        cache.decode_step(np.ones((2, 8), np.float32))
+
+
+def test_memory_law(kvq):
+    # test_kvcache.cpp:272-293 (17,408 B) and acceptance.cpp:376-413
+    rng = np.random.default_rng(9)
+    k = rng.uniform(-1, 1, (1, 1024, 64)).astype(np.float32)
+    cache = kvq.HybridKVCache.build(list(k), list(k), kvq.QuantizationConfig(1), kvq.CalibrationParams())
+    m = cache.memory()
+    assert m.code_bytes == 2 * 1024 * 64 // 8 and m.stats_bytes == 2 * 2 * 64 * 4
+    assert m.quantized_bytes == 17408 and m.tail_bytes == 0 and m.fp32_vis_bytes == 2 * 1024 * 64 * 4
+    cache.append(np.zeros((1, 64), np.float32), np.zeros((1, 64), np.float32))
+    cache.append(np.zeros((1, 64), np.float32), np.zeros((1, 64), np.float32))
+    assert cache.memory().tail_bytes == 2 * 2 * 64 * 4
+
+
+# ---- batched GQA cache vs the oracle (the throughput API) ------------------------------------
+
+def _oracle_batched(oracle, k, v, q, bits, tau, tails_k=None, tails_v=None):
+    B, H, n, d = k.shape
+    G = q.shape[2]
+    out = np.zeros_like(q)
+    for b in range(B):
+        for h in range(H):
+            ka, kb = oracle.compute_stats(k[b, h])
+            va, vb = oracle.compute_stats(v[b, h])
+            kc, vc = oracle.quantize(k[b, h], ka, kb, bits), oracle.quantize(v[b, h], va, vb, bits)
+            tk = tails_k[:, b, h] if tails_k is not None else np.zeros((0, d), np.float32)
+            tv = tails_v[:, b, h] if tails_v is not None else np.zeros((0, d), np.float32)
+            for g in range(G):
+                out[b, h, g] = oracle.decode_head(q[b, h, g], n, bits, 8, kc, ka, kb, vc, va, vb, tk, tv, *tau)[0]
+    return out
+
+
+@pytest.mark.parametrize("bits", [1, 2, 4, 8])
+@pytest.mark.parametrize("G,n", [(4, 1000), (6, 300), (1, 64), (8, 129), (4, 1)])
+def test_batched_gqa_vs_oracle(kvq, oracle, bits, G, n):
+    rng = np.random.default_rng(bits * 1000 + G * 10 + n)
+    B, H, d = 2, 2, 128
+    k = rng.normal(size=(B, H, n, d)).astype(np.float32)
+    v = rng.normal(size=(B, H, n, d)).astype(np.float32)
+    tau = (1.0, 0.0) if bits == 1 else (2.0, 0.5)
+    cache = kvq.BatchedCache.build(k, v, kvq.QuantizationConfig(bits), kvq.CalibrationParams(*tau), group=G)
+    tk, tv = [], []
+    for step in range(3):
+        q = rng.normal(size=(B, H, G, d)).astype(np.float32)
+        want = _oracle_batched(oracle, k, v, q, bits, tau,
+                               np.stack(tk) if tk else None, np.stack(tv) if tv else None)
+        for path, tol in ((kvq.PATH_GENERIC, TOL_GENERIC), (kvq.PATH_AUTO, TOL_TC)):
+            cache.set_path(path)
+            out, _, _ = cache.decode(q)
+            err = rel_l2(out, want)
+            assert err <= tol, f"path {path} step {step}: rel L2 {err}"
+        kn = rng.normal(size=(B, H, d)).astype(np.float32)
+        vn = rng.normal(size=(B, H, d)).astype(np.float32)
+        cache.append(kn, vn)
+        tk.append(kn)
+        tv.append(vn)
+
+
+def test_step_api_matches_decode_then_append(kvq):
+    rng = np.random.default_rng(12)
+    B, H, G, n, d = 3, 2, 4, 200, 128
+    k = rng.normal(size=(B, H, n, d)).astype(np.float32)
+    v = rng.normal(size=(B, H, n, d)).astype(np.float32)
+    c1 = kvq.BatchedCache.build(k, v, kvq.QuantizationConfig(1), kvq.CalibrationParams(1, 0), group=G)
+    c2 = kvq.BatchedCache.build(k, v, kvq.QuantizationConfig(1), kvq.CalibrationParams(1, 0), group=G)
+    for _ in range(3):
+        q = rng.normal(size=(B, H, G, d)).astype(np.float32)
+        kn = rng.normal(size=(B, H, d)).astype(np.float32)
+        vn = rng.normal(size=(B, H, d)).astype(np.float32)
+        out = np.zeros_like(q)
+        c1.step(q, kn, vn, out)
+        ref, _, _ = c2.decode(q)
+        c2.append(kn, vn)
+        assert np.array_equal(out, ref)
