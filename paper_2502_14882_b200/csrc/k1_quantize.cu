@@ -85,10 +85,15 @@ stats_kernel(const float* __restrict__ x, size_t rows, size_t dim, float* __rest
     s_any[part][threadIdx.x] = any;
     __syncthreads();
     if (part != 0 || c >= dim) return;
-    // Parts hold consecutive row ranges: fold them left to right.
+    // Parts hold consecutive row ranges: fold the non-empty ones left to right.
+    bool have = any;
     for (int p = 1; p < kStatParts; ++p) {
         if (!s_any[p][threadIdx.x]) continue;
         float plo = s_lo[p][threadIdx.x], phi = s_hi[p][threadIdx.x];
+        if (!have) {
+            lo = plo, hi = phi, lr = s_lr[p][threadIdx.x], hr = s_hr[p][threadIdx.x], have = true;
+            continue;
+        }
         if (plo < lo) { lo = plo; lr = s_lr[p][threadIdx.x]; }
         if (hi < phi) { hi = phi; hr = s_hr[p][threadIdx.x]; }
     }

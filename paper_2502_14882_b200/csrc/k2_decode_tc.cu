@@ -1,6 +1,748 @@
-// k2_decode_tc.cu — placeholder until the tensor-core path lands.
+// k2_decode_tc.cu — K2 throughput path: fused, calibrated, post-scaled quantized decode
+// attention on the sm_100a integer tensor cores (mma.sync m16n8k32 IMMA), d = 128,
+// reference M = 8 byte layout, b in {1,2,4,8}, G <= 8 query heads per KV head.
+//
+// Math (reference: kernels.hpp:14-26, 183-194, 277-283; calibrate.hpp:62-114;
+// kvcache.hpp:263-311), per (unit, query head h):
+//   score_j = (sum_c qs_c code_jc + q.alpha) / sqrt(d),  qs_c = q_c (beta_c-alpha_c)/L
+//   row     = [g(score_vis) | score_tail],  g affine from (gamma, delta) of the vis part
+//   out_c   = (s_c sum_j p_j code_jc + alpha_c sum_j p_j + sum_t p_t v_tc) / sum p
+//
+// Kernel 1 (prep, one CTA per unit): folds the K scale into the query: Q'_c =
+//   round(S_h qs_c / 2^sh_c) split into 4 balanced int8 digit planes; S_h bounds the
+//   int32 score so IMMA accumulation is exact. Emits the A-fragments of the q.K MMA.
+// Kernel 2 (decode, cluster of S CTAs per unit, each a contiguous token chunk):
+//   producer warp : cp.async.bulk (TMA) ring of 8-16 KB stages, K chunk then V chunk
+//   phase A       : IMMA  [16 head-planes x 32 ch] x [32 ch x 8 tokens]; B operand is
+//                   the raw code bytes: one LOP3 extracts 4 codes (x 2^sh) per register
+//   cluster #1    : DSMEM exchange of per-CTA (min, max, tail max) -> gamma, delta, m
+//   phase B       : p = exp(g(s) - m) as u16 (two u8 planes) -> IMMA [16 ch x 32 tok]
+//                   x [32 tok x 8 head-planes]; V codes byte-transposed with PRMT
+//   cluster #2/#3 : DSMEM reduction of partial numerators/denominators -> out
+// Packed K/V are never dequantized; the only fp32 math per token is the softmax.
+#include <cooperative_groups.h>
+
 #include "kvq_internal.cuh"
+
+namespace cg = cooperative_groups;
+
 namespace kvqb {
-bool decode_tc_supported(const DecodeArgs&) { return false; }
-cudaError_t launch_decode_tc(const DecodeArgs&, cudaStream_t) { return cudaErrorNotSupported; }
+
+namespace {
+
+constexpr int kDim = 128;
+constexpr int kConsumerWarps = 4;
+constexpr int kThreads = (kConsumerWarps + 1) * 32;
+constexpr int kStages = 4;
+constexpr int kTailMax = 64;   // fp32 tail tokens per CTA
+constexpr int kMaxT = 2048;    // visual tokens per CTA
+constexpr int kMaxCluster = 16;
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: float -> int rounding trick
+constexpr uint32_t kMagicBits = 0x4B400000u;
+
+template <int BITS>
+struct Geo {
+    static constexpr int kRowBytes = 16 * BITS;
+    static constexpr int kStageTokens = BITS <= 2 ? 512 / BITS : 128;
+    static constexpr int kStageBytes = kStageTokens * kRowBytes;
+    static constexpr int kCpb = 8 / BITS;  // codes per byte
+    static constexpr uint32_t kMask = 0x01010101u * ((1u << BITS) - 1u);
+};
+
+struct TcParams {
+    DecodeArgs a;
+    const uint32_t* frag;  // [units][NT][4 kb][4 reg][32 lanes] A fragments (q planes)
+    const float2* qconst;  // [units][G] (isd / S_h, qdota_h * isd)
+    int S, T;              // cluster size, visual tokens per CTA (multiple of 32)
+};
+
+// ---- PTX helpers ---------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void cluster_arrive() {
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;"); }
+__device__ __forceinline__ void consumers_sync() {
+    asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
+}
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+    uint32_t r;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+    return r;
+}
+__device__ __forceinline__ float ex2(float x) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+// D += A(16x32, s8) * B(32x8, u8)
+__device__ __forceinline__ void imma_s8u8(int (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm("mma.sync.aligned.m16n8k32.row.col.s32.s8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+        : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+// D += A(16x32, u8) * B(32x8, u8)
+__device__ __forceinline__ void imma_u8u8(int (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                          uint32_t b0, uint32_t b1) {
+    asm("mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+        : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// K side: channel held by byte j of B-register rho of lane-group t (a row's words
+// t*BITS .. t*BITS+BITS-1; register rho = u*cpb + s extracts code slot s of word u).
+template <int BITS>
+__device__ __forceinline__ int k_channel(int t, int rho, int j, int& shift) {
+    constexpr int cpb = Geo<BITS>::kCpb;
+    const int u = rho / cpb, s = rho % cpb;
+    shift = s * BITS;
+    return (4 * (t * BITS + u) + j) * cpb + (cpb - 1 - s);
+}
+// V side: channel of A-register index iota (= q*cpb + s) of lane-group g.
+template <int BITS>
+__device__ __forceinline__ int v_channel(int g, int iota, int& shift) {
+    constexpr int cpb = Geo<BITS>::kCpb;
+    const int q = iota / cpb, s = iota % cpb;
+    shift = s * BITS;
+    return (2 * BITS * g + q) * cpb + (cpb - 1 - s);
+}
+
+// ---- prep: fold the K scales into the query -------------------------------------------
+template <int BITS>
+__global__ void __launch_bounds__(kDim) prep_kernel(DecodeArgs a, int NT, uint32_t* __restrict__ frag,
+                                                    float2* __restrict__ qconst) {
+    griddep_launch();  // the decode grid may start streaming codes right away
+    __shared__ float s_qs[8][kDim];
+    __shared__ float s_red[2][8][4];
+    __shared__ float s_scale[8];
+    const int unit = blockIdx.x, c = threadIdx.x, G = (int)a.group;
+    const int lane = c & 31, wid = c >> 5;
+    const float levels = (float)((1u << BITS) - 1u);
+    const float isd = __fdiv_rn(1.0f, sqrtf((float)kDim));
+    const float ka = a.k_alpha[unit * kDim + c];
+    const float range = __fsub_rn(a.k_beta[unit * kDim + c], ka);
+    const float step = range > 0.0f ? __fdiv_rn(range, levels) : 0.0f;
+    for (int h = 0; h < 8; ++h) {
+        float qs = 0.f, qa = 0.f;
+        if (h < G) {
+            const float q = a.q[(unit * G + h) * kDim + c];
+            qs = range > 0.0f ? __fmul_rn(q, step) : 0.0f;  // detail::scale_query
+            qa = __fmul_rn(q, ka);
+        }
+        s_qs[h][c] = qs;
+        float ab = fabsf(qs), sa = qa;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            ab += __shfl_xor_sync(0xffffffffu, ab, o);
+            sa += __shfl_xor_sync(0xffffffffu, sa, o);
+        }
+        if (lane == 0) {
+            s_red[0][h][wid] = ab;
+            s_red[1][h][wid] = sa;
+        }
+    }
+    __syncthreads();
+    if (c < 8) {
+        const int h = c;
+        float sum_abs = (s_red[0][h][0] + s_red[0][h][1]) + (s_red[0][h][2] + s_red[0][h][3]);
+        float qdota = (s_red[1][h][0] + s_red[1][h][1]) + (s_red[1][h][2] + s_red[1][h][3]);
+        // |score_int| <= (2^b - 1) * sum|Q_c| <= 2^30: exact int32 accumulation.
+        float S = sum_abs > 0.0f ? 1073741824.0f / (levels * sum_abs) : 0.0f;
+        s_scale[h] = S;
+        if (h < G) qconst[unit * G + h] = make_float2(S > 0.0f ? isd / S : 0.0f, qdota * isd);
+    }
+    __syncthreads();
+    // A fragments: entry (nt, kb, reg, lane) packs bytes j = 0..3 of row r, k = 4t+j(+16).
+    const int total = NT * 4 * 4 * 32;
+    for (int e = c; e < total; e += kDim) {
+        const int ln = e & 31, reg = (e >> 5) & 3, kb = (e >> 7) & 3, nt = e >> 9;
+        const int g = ln >> 2, t = ln & 3;
+        const int row = (reg & 1) ? g + 8 : g;
+        const int half = reg >> 1;
+        const int plane = ((row >> 2) & 1) + 2 * (row >> 3);
+        const int h = 4 * nt + (row & 3);
+        uint32_t word = 0;
+        if (h < G) {
+            for (int j = 0; j < 4; ++j) {
+                int sh;
+                const int ch = k_channel<BITS>(t, 2 * kb + half, j, sh);
+                const int Q = __float2int_rn(__fmul_rn(s_qs[h][ch], s_scale[h]) * __int_as_float((127 - sh) << 23));
+                // balanced base-256 digits: Q = d0 + 2^8 d1 + 2^16 d2 + 2^24 d3
+                int d0 = ((Q + 128) & 255) - 128;
+                int q1 = (Q - d0) >> 8;
+                int d1 = ((q1 + 128) & 255) - 128;
+                int q2 = (q1 - d1) >> 8;
+                int d2 = ((q2 + 128) & 255) - 128;
+                int d3 = (q2 - d2) >> 8;
+                const int d = plane == 0 ? d0 : plane == 1 ? d1 : plane == 2 ? d2 : d3;
+                word |= (uint32_t)(d & 255) << (8 * j);
+            }
+        }
+        frag[(size_t)unit * total + e] = word;
+    }
+}
+
+// ---- decode ------------------------------------------------------------------------------
+struct Partial {  // per-CTA softmax statistics, exchanged through DSMEM
+    float lo[8], hi[8], tmax[8];
+};
+
+template <int BITS, int NT>
+__global__ void __launch_bounds__(kThreads, 3) decode_tc_kernel(const TcParams p) {
+    using Gm = Geo<BITS>;
+    const DecodeArgs& a = p.a;
+    const int G = (int)a.group;
+    const int S = p.S, T = p.T, TS = T + 4;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int rank = (int)cluster.block_rank();
+    const int unit = blockIdx.x / S;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, t = lane & 3;
+
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint8_t* ring = smem;                                                  // kStages x stage bytes
+    float* scores = reinterpret_cast<float*>(ring + kStages * Gm::kStageBytes);  // [G][TS]
+    float* tail_s = scores + G * TS;                                       // [G][kTailMax]
+    float* q_s = tail_s + G * kTailMax;                                    // [G][128]
+    Partial* part = reinterpret_cast<Partial*>(q_s + G * kDim);
+    float* gpar = reinterpret_cast<float*>(part + 1);                      // [8][4]: A', B', tail B', -
+    float* pub = gpar + 32;                                                // [G][128] numerators
+    float* pub_den = pub + G * kDim;                                       // [8]
+    float* wpart = pub_den + 8;                                            // [4 warps][8][3]
+    uint64_t* full = reinterpret_cast<uint64_t*>(wpart + kConsumerWarps * 8 * 3 + 2);  // 8-byte aligned below
+    full = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(full) + 7) & ~uintptr_t(7));
+    uint64_t* empty = full + kStages;
+
+    // Work split: visual tokens [tok0, tok0 + nv), tail tokens [tt0, tt0 + ntl).
+    const int n = (int)a.n_vis;
+    const int tok0 = rank * T;
+    const int nv = max(0, min(T, n - tok0));
+    const int n_tail = a.tail_len[unit / a.kv_heads];
+    const int tail_per = (n_tail + S - 1) / S;
+    const int tt0 = rank * tail_per;
+    const int ntl = max(0, min(tail_per, n_tail - tt0));
+    const size_t rb = Gm::kRowBytes;
+    const uint8_t* kcodes = a.k_codes + ((size_t)unit * n + tok0) * rb;
+    const uint8_t* vcodes = a.v_codes + ((size_t)unit * n + tok0) * rb;
+    const int nstage = (nv + Gm::kStageTokens - 1) / Gm::kStageTokens;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kStages; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], kConsumerWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == kConsumerWarps) {
+        // ===== producer: K stages then V stages through the ring =====
+        auto issue = [&](int i) {
+            const int slot = i % kStages;
+            if (i >= kStages) mbar_wait(&empty[slot], ((i / kStages) - 1) & 1);
+            const int si = i < nstage ? i : i - nstage;
+            const uint8_t* src = (i < nstage ? kcodes : vcodes) + (size_t)si * Gm::kStageBytes;
+            const int ntok = min(Gm::kStageTokens, nv - si * Gm::kStageTokens);
+            const uint32_t bytes = (uint32_t)(ntok * Gm::kRowBytes);
+            mbar_expect_tx(&full[slot], bytes);
+            bulk_g2s(ring + slot * Gm::kStageBytes, src, bytes, &full[slot]);
+        };
+        // Everything that can be in flight before phase B frees ring slots.
+        const int pre = min(2 * nstage, nstage + kStages);
+        if (lane == 0)
+            for (int i = 0; i < pre; ++i) issue(i);
+        __syncwarp();
+        cluster_arrive();  // #1 (nothing to publish)
+        if (lane == 0)
+            for (int i = pre; i < 2 * nstage; ++i) issue(i);
+        __syncwarp();
+        cluster_wait();
+        cluster_arrive();  // #2
+        cluster_wait();
+        cluster_arrive();  // #3
+        cluster_wait();
+        return;
+    }
+
+    // ===== consumers =====
+    for (int i = threadIdx.x; i < G * kDim; i += kConsumerWarps * 32)
+        q_s[i] = a.q[(size_t)unit * G * kDim + i];
+    griddep_wait();  // prep results visible
+    uint32_t afrag[NT][4][4];
+    const uint32_t* fr = p.frag + (size_t)unit * NT * 512;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int kb = 0; kb < 4; ++kb)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) afrag[nt][kb][r] = fr[((nt * 4 + kb) * 4 + r) * 32 + lane];
+    // Phase-A epilogue constants: this lane's head and plane weights.
+    const bool lowlane = g < 4;
+    const int wl = lowlane ? 1 : 256, wh = lowlane ? 65536 : (1 << 24);
+    float cA[NT], cB[NT];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+        const int h = 4 * nt + (g & 3);
+        float2 qc = h < G ? p.qconst[(size_t)unit * G + h] : make_float2(0.f, 0.f);
+        cA[nt] = qc.x;
+        cB[nt] = qc.y;
+    }
+    float lo[NT], hi[NT];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) lo[nt] = INFINITY, hi[nt] = -INFINITY;
+
+    // ---------------- phase A: scores of the visual chunk ----------------
+    for (int st = 0; st < nstage; ++st) {
+        const int slot = st % kStages;
+        mbar_wait(&full[slot], (st / kStages) & 1);
+        const uint8_t* buf = ring + slot * Gm::kStageBytes;
+        const int ns = min(Gm::kStageTokens, nv - st * Gm::kStageTokens);
+        const int ntiles = (ns + 7) >> 3;
+        for (int tile = warp; tile < ntiles; tile += kConsumerWarps) {
+            // B operand: this lane's BITS words of token row (tile*8 + g).
+            const uint8_t* rowp = buf + (tile * 8 + g) * Gm::kRowBytes + t * 4 * BITS;
+            uint32_t w[BITS];
+            if (BITS == 1) {
+                w[0] = *reinterpret_cast<const uint32_t*>(rowp);
+            } else if (BITS == 2) {
+                uint2 v = *reinterpret_cast<const uint2*>(rowp);
+                w[0] = v.x, w[1 % BITS] = v.y;
+            } else {
+#pragma unroll
+                for (int u = 0; u < BITS; u += 4) {
+                    uint4 v = *reinterpret_cast<const uint4*>(rowp + 4 * u);
+                    w[u] = v.x, w[(u + 1) % BITS] = v.y, w[(u + 2) % BITS] = v.z, w[(u + 3) % BITS] = v.w;
+                }
+            }
+            uint32_t breg[8];
+#pragma unroll
+            for (int rho = 0; rho < 8; ++rho)
+                breg[rho] = w[rho / Gm::kCpb] & (Gm::kMask << ((rho % Gm::kCpb) * BITS));
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+                int acc[4] = {0, 0, 0, 0};
+#pragma unroll
+                for (int kb = 0; kb < 4; ++kb) imma_s8u8(acc, afrag[nt][kb], breg[2 * kb], breg[2 * kb + 1]);
+                // rows g / g+8 hold digit planes (0,2) [g<4] or (1,3) [g>=4] of head g%4.
+                const int p0 = acc[0] * wl + acc[2] * wh;  // token 2t   (mod 2^32; exact total)
+                const int p1 = acc[1] * wl + acc[3] * wh;  // token 2t+1
+                const int send = lowlane ? p1 : p0;
+                const int recv = __shfl_xor_sync(0xffffffffu, send, 16);
+                const int total = (lowlane ? p0 : p1) + recv;
+                const int tok = st * Gm::kStageTokens + tile * 8 + 2 * t + (lowlane ? 0 : 1);
+                const int h = 4 * nt + (g & 3);
+                if (h < G && tok < nv) {
+                    const float s = __fmaf_rn((float)total, cA[nt], cB[nt]);
+                    scores[h * TS + tok] = s;
+                    lo[nt] = fminf(lo[nt], s);
+                    hi[nt] = fmaxf(hi[nt], s);
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+    }
+
+    // fp32 tail tokens of this CTA: warp per token, lanes split the 128 channels.
+    const float isd = __fdiv_rn(1.0f, sqrtf((float)kDim));
+    float tmax_l[8];
+#pragma unroll
+    for (int h = 0; h < 8; ++h) tmax_l[h] = -INFINITY;
+    for (int j = warp; j < ntl; j += kConsumerWarps) {
+        const float4 kv = *reinterpret_cast<const float4*>(
+            a.k_tail + ((size_t)unit * a.tail_cap + tt0 + j) * kDim + 4 * lane);
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+            if (h >= G) break;
+            const float* qh = q_s + h * kDim + 4 * lane;
+            float d = kv.x * qh[0] + kv.y * qh[1] + kv.z * qh[2] + kv.w * qh[3];
+#pragma unroll
+            for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+            d *= isd;
+            if (lane == 0) tail_s[h * kTailMax + j] = d;
+            tmax_l[h] = fmaxf(tmax_l[h], d);
+        }
+    }
+
+    // CTA partial (min, max) per head: lanes of one head differ in lane bits 0,1,4.
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+#pragma unroll
+        for (int o : {1, 2, 16}) {
+            lo[nt] = fminf(lo[nt], __shfl_xor_sync(0xffffffffu, lo[nt], o));
+            hi[nt] = fmaxf(hi[nt], __shfl_xor_sync(0xffffffffu, hi[nt], o));
+        }
+        if ((lane & 3) == 0 && lane < 16) {  // lane (g, 0), g < 4, holds head g of this tile
+            wpart[(warp * 8 + 4 * nt + (lane >> 2)) * 3 + 0] = lo[nt];
+            wpart[(warp * 8 + 4 * nt + (lane >> 2)) * 3 + 1] = hi[nt];
+        }
+    }
+    if (lane == 0)
+        for (int h = 0; h < 8; ++h) wpart[(warp * 8 + h) * 3 + 2] = tmax_l[h];
+    consumers_sync();
+    if (threadIdx.x < 8) {
+        const int h = threadIdx.x;
+        float l = INFINITY, u = -INFINITY, tm = -INFINITY;
+        if (h < 4 * NT)
+            for (int w2 = 0; w2 < kConsumerWarps; ++w2) {
+                l = fminf(l, wpart[(w2 * 8 + h) * 3 + 0]);
+                u = fmaxf(u, wpart[(w2 * 8 + h) * 3 + 1]);
+            }
+        for (int w2 = 0; w2 < kConsumerWarps; ++w2) tm = fmaxf(tm, wpart[(w2 * 8 + h) * 3 + 2]);
+        part->lo[h] = l;
+        part->hi[h] = u;
+        part->tmax[h] = tm;
+    }
+    cluster_arrive();  // #1: partials published
+    cluster_wait();
+
+    // Global softmax parameters per head (identical in every CTA of the cluster).
+    if (threadIdx.x < 8) {
+        const int h = threadIdx.x;
+        float gamma = INFINITY, delta = -INFINITY, tm = -INFINITY;
+        for (int r = 0; r < S; ++r) {
+            const Partial* pr = cluster.map_shared_rank(part, r);
+            gamma = fminf(gamma, pr->lo[h]);
+            delta = fmaxf(delta, pr->hi[h]);
+            tm = fmaxf(tm, pr->tmax[h]);
+        }
+        // g(x) = A x + B (calibrate.hpp:62-67); endpoints g(gamma) = gamma - tau1,
+        // g(delta) = delta - tau2; the calibrated row max is attained at an endpoint.
+        const float width = __fsub_rn(delta, gamma);
+        float A = 1.0f, B = -a.tau1, m = tm;
+        if (n > 0) {
+            if (width > 0.0f) {
+                const float r = __fdiv_rn(__fsub_rn(a.tau2, a.tau1), width);
+                A = 1.0f - r;
+                B = __fmaf_rn(r, gamma, -a.tau1);
+                m = fmaxf(m, fmaxf(__fsub_rn(gamma, a.tau1), __fsub_rn(delta, a.tau2)));
+            } else {
+                m = fmaxf(m, __fsub_rn(gamma, a.tau1));
+            }
+        }
+        gpar[h * 4 + 0] = A * kLog2e;
+        gpar[h * 4 + 1] = (B - m) * kLog2e;
+        gpar[h * 4 + 2] = -m * kLog2e;
+    }
+    consumers_sync();
+
+    // ---------------- phase B: p . V over the visual chunk ----------------
+    int vacc[NT][8][4];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) vacc[nt][mt][r] = 0;
+    uint32_t wsum[NT];
+    int wcount[NT];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) wsum[nt] = 0, wcount[nt] = 0;
+    float pa[NT], pb[NT];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+        const int h = 4 * nt + (g >> 1);
+        pa[nt] = gpar[h * 4 + 0];
+        pb[nt] = gpar[h * 4 + 1];
+    }
+    const int e = g & 1;
+    for (int st = 0; st < nstage; ++st) {
+        const int i = nstage + st;
+        const int slot = i % kStages;
+        mbar_wait(&full[slot], (i / kStages) & 1);
+        const uint8_t* buf = ring + slot * Gm::kStageBytes;
+        const int ns = min(Gm::kStageTokens, nv - st * Gm::kStageTokens);
+        const int nblk = (ns + 31) >> 5;
+        for (int blk = warp; blk < nblk; blk += kConsumerWarps) {
+            const int btok = st * Gm::kStageTokens + blk * 32;  // chunk-local first token
+            // B operand: u16 probabilities of head (g/2 + 4nt), as two u8 digit planes.
+            uint32_t bq[NT][2];
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+                const int h = 4 * nt + (g >> 1);
+                uint32_t pv[4];
+#pragma unroll
+                for (int ii = 0; ii < 4; ++ii) {
+                    const int tok = btok + 16 * e + t + 4 * ii;
+                    float pr = 0.0f;
+                    if (h < G && tok < nv) pr = ex2(__fmaf_rn(scores[h * TS + tok], pa[nt], pb[nt]));
+                    // round(p * 65535) in the low bits of the float (magic-number rounding)
+                    pv[ii] = __float_as_uint(__fmaf_rn(fminf(pr, 1.0f), 65535.0f, kMagic));
+                }
+                wsum[nt] += pv[0] + pv[1] + pv[2] + pv[3];
+                wcount[nt] += 4;
+                const uint32_t p01 = prmt(pv[0], pv[1], 0x5140), p23 = prmt(pv[2], pv[3], 0x5140);
+                const uint32_t lo8 = prmt(p01, p23, 0x5410), hi8 = prmt(p01, p23, 0x7632);
+                const uint32_t send = e ? hi8 : lo8;
+                const uint32_t recv = __shfl_xor_sync(0xffffffffu, send, 4);
+                bq[nt][0] = e ? recv : hi8;  // tokens t+4i       (plane: hi for even g)
+                bq[nt][1] = e ? lo8 : recv;  // tokens 16+t+4i
+            }
+            // A operand: V codes of this lane's 2*BITS bytes for 8 tokens, byte-transposed.
+            constexpr int NW = (2 * BITS + 3) / 4;  // 32-bit words per token slice
+            uint32_t X[2][2 * BITS];
+#pragma unroll
+            for (int grp = 0; grp < 2; ++grp) {
+                uint32_t raw[4][NW];
+#pragma unroll
+                for (int ii = 0; ii < 4; ++ii) {
+                    const uint8_t* rp = buf + (blk * 32 + 16 * grp + t + 4 * ii) * Gm::kRowBytes + 2 * BITS * g;
+                    if (BITS == 1) {
+                        raw[ii][0] = *reinterpret_cast<const uint16_t*>(rp);
+                    } else if (BITS == 2) {
+                        raw[ii][0] = *reinterpret_cast<const uint32_t*>(rp);
+                    } else if (BITS == 4) {
+                        uint2 v = *reinterpret_cast<const uint2*>(rp);
+                        raw[ii][0] = v.x, raw[ii][NW - 1] = v.y;
+                    } else {
+                        uint4 v = *reinterpret_cast<const uint4*>(rp);
+                        raw[ii][0] = v.x, raw[ii][1 % NW] = v.y, raw[ii][2 % NW] = v.z, raw[ii][3 % NW] = v.w;
+                    }
+                }
+#pragma unroll
+                for (int wi = 0; wi < NW; ++wi) {
+                    const uint32_t P0 = prmt(raw[0][wi], raw[1][wi], 0x5140);
+                    const uint32_t P2 = prmt(raw[2][wi], raw[3][wi], 0x5140);
+                    X[grp][(4 * wi + 0) % (2 * BITS)] = prmt(P0, P2, 0x5410);
+                    X[grp][(4 * wi + 1) % (2 * BITS)] = prmt(P0, P2, 0x7632);
+                    if (2 * BITS > 2) {
+                        const uint32_t P1 = prmt(raw[0][wi], raw[1][wi], 0x7362);
+                        const uint32_t P3 = prmt(raw[2][wi], raw[3][wi], 0x7362);
+                        X[grp][(4 * wi + 2) % (2 * BITS)] = prmt(P1, P3, 0x5410);
+                        X[grp][(4 * wi + 3) % (2 * BITS)] = prmt(P1, P3, 0x7632);
+                    }
+                }
+            }
+#pragma unroll
+            for (int mt = 0; mt < 8; ++mt) {
+                constexpr int cpb = Gm::kCpb;
+                const int i0 = mt, i1 = 8 + mt;
+                const uint32_t m0 = Gm::kMask << ((i0 % cpb) * BITS), m1 = Gm::kMask << ((i1 % cpb) * BITS);
+                const uint32_t a0 = X[0][i0 / cpb] & m0, a1 = X[0][i1 / cpb] & m1;
+                const uint32_t a2 = X[1][i0 / cpb] & m0, a3 = X[1][i1 / cpb] & m1;
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) imma_u8u8(vacc[nt][mt], a0, a1, a2, a3, bq[nt][0], bq[nt][1]);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+    }
+
+    // ---------------- CTA partial numerators / denominators ----------------
+    // Ring is free once every consumer warp is past its last stage: reuse it for the
+    // cross-warp reduction [warp][G][128] + [warp][8].
+    consumers_sync();
+    float* red = reinterpret_cast<float*>(ring);
+    float* redw = red + kConsumerWarps * G * kDim;
+    const float levels = (float)((1u << BITS) - 1u);
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+        const int h = 4 * nt + t;  // C columns 2t, 2t+1: head t's (hi, lo) digit planes
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt) {
+#pragma unroll
+            for (int rr = 0; rr < 2; ++rr) {
+                int sh;
+                const int ch = v_channel<BITS>(g, rr * 8 + mt, sh);
+                const uint32_t chi = (uint32_t)vacc[nt][mt][2 * rr] >> sh;
+                const uint32_t clo = (uint32_t)vacc[nt][mt][2 * rr + 1] >> sh;
+                if (h < G) red[(warp * G + h) * kDim + ch] = (float)chi * 256.0f + (float)clo;
+            }
+        }
+        // sum of u16 weights of head (g/2 + 4nt) over this warp's tokens
+        uint32_t ws = wsum[nt] - (uint32_t)wcount[nt] * kMagicBits;
+#pragma unroll
+        for (int o : {1, 2, 4}) ws += __shfl_xor_sync(0xffffffffu, ws, o);
+        if ((lane & 7) == 0 && 4 * nt + (g >> 1) < G) redw[warp * 8 + 4 * nt + (g >> 1)] = (float)ws;
+    }
+    consumers_sync();
+    // fp32 tail weights and values of this CTA (already on the 65535 scale).
+    for (int idx = threadIdx.x; idx < G * kDim; idx += kConsumerWarps * 32) {
+        const int h = idx / kDim, ch = idx % kDim;
+        float num = 0.f;
+        for (int w2 = 0; w2 < kConsumerWarps; ++w2) num += red[(w2 * G + h) * kDim + ch];
+        const float va = a.v_alpha[unit * kDim + ch];
+        const float vr = __fsub_rn(a.v_beta[unit * kDim + ch], va);
+        const float step = vr > 0.0f ? __fdiv_rn(vr, levels) : 0.0f;
+        float wv = 0.f;
+        for (int w2 = 0; w2 < kConsumerWarps; ++w2) wv += redw[w2 * 8 + h];
+        float tnum = 0.f;
+        for (int j = 0; j < ntl; ++j) {
+            const float pt = ex2(__fmaf_rn(tail_s[h * kTailMax + j], kLog2e, gpar[h * 4 + 2])) * 65535.0f;
+            tnum = __fmaf_rn(pt, a.v_tail[((size_t)unit * a.tail_cap + tt0 + j) * kDim + ch], tnum);
+        }
+        pub[h * kDim + ch] = __fmaf_rn(step, num, __fmaf_rn(va, wv, tnum));
+    }
+    if (threadIdx.x < 8) {
+        const int h = threadIdx.x;
+        float wv = 0.f, wt = 0.f;
+        if (h < G) {
+            for (int w2 = 0; w2 < kConsumerWarps; ++w2) wv += redw[w2 * 8 + h];
+            for (int j = 0; j < ntl; ++j)
+                wt += ex2(__fmaf_rn(tail_s[h * kTailMax + j], kLog2e, gpar[h * 4 + 2])) * 65535.0f;
+        }
+        pub_den[h] = wv + wt;
+    }
+    cluster_arrive();  // #2: partial numerators published
+    cluster_wait();
+    // Each CTA finalizes a slice of the G x 128 outputs (fixed-order sum over ranks).
+    const int per = (G * kDim + S - 1) / S;
+    for (int idx = rank * per + threadIdx.x; idx < min(G * kDim, (rank + 1) * per); idx += kConsumerWarps * 32) {
+        const int h = idx / kDim;
+        float num = 0.f, den = 0.f;
+        for (int r = 0; r < S; ++r) {
+            num += cluster.map_shared_rank(pub, r)[idx];
+            den += cluster.map_shared_rank(pub_den, r)[h];
+        }
+        a.out[((size_t)unit * G + h) * kDim + (idx % kDim)] = num / den;
+    }
+    cluster_arrive();  // #3: keep shared memory alive until every peer has read it
+    cluster_wait();
+}
+
+size_t tc_smem_bytes(int bits, int G, int T) {
+    const size_t stage = (size_t)(bits <= 2 ? 8192 : 128 * 16 * bits);
+    size_t ring = kStages * stage;
+    const size_t red = (size_t)kConsumerWarps * (G * kDim + 8) * 4;
+    if (ring < red) ring = red;
+    return ring + (size_t)G * (T + 4) * 4 + (size_t)G * kTailMax * 4 + (size_t)G * kDim * 4 + sizeof(Partial) +
+           32 * 4 + (size_t)G * kDim * 4 + 8 * 4 + kConsumerWarps * 8 * 3 * 4 + 16 + 2 * kStages * 8 + 16;
+}
+
+// Scratch for the prep kernel's outputs (grown on demand, per device).
+struct PrepScratch {
+    uint32_t* frag = nullptr;
+    float2* qconst = nullptr;
+    size_t units = 0, G = 0;
+};
+PrepScratch g_scratch[16];
+
+void plan(const DecodeArgs& a, int& S, int& T) {
+    const int n = (int)a.n_vis;
+    const int units = (int)a.units;
+    int s_min = (n + kMaxT - 1) / kMaxT;                 // smem cap on tokens per CTA
+    int s_pref = (n + 511) / 512;                        // ~512 tokens per CTA
+    const int want_ctas = 2 * 148;
+    if (units * s_pref < want_ctas) s_pref = (want_ctas + units - 1) / units;
+    S = std::max(1, std::min(kMaxCluster, std::max(s_min, s_pref)));
+    S = std::min(S, std::max(1, (n + 31) / 32));  // >= 32 tokens per CTA
+    T = ((n + S - 1) / S + 31) / 32 * 32;
+    S = (n + T - 1) / T;
+}
+
+template <int BITS, int NT>
+cudaError_t launch_bits(const DecodeArgs& a, cudaStream_t s, uint32_t* frag, float2* qconst) {
+    int S, T;
+    plan(a, S, T);
+    prep_kernel<BITS><<<(unsigned)a.units, kDim, 0, s>>>(a, NT, frag, qconst);
+    note_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    TcParams p{a, frag, qconst, S, T};
+    const size_t smem = tc_smem_bytes(BITS, (int)a.group, T);
+    auto kern = decode_tc_kernel<BITS, NT>;
+    static bool attr_done = false;  // per instantiation
+    if (!attr_done) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        if (e != cudaSuccess) return e;
+        attr_done = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(a.units * S));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attrs[2];
+    attrs[0].id = cudaLaunchAttributeClusterDimension;
+    attrs[0].val.clusterDim.x = (unsigned)S;
+    attrs[0].val.clusterDim.y = 1;
+    attrs[0].val.clusterDim.z = 1;
+    attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attrs[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attrs;
+    cfg.numAttrs = 2;
+    e = cudaLaunchKernelEx(&cfg, kern, p);
+    note_launch();
+    return e;
+}
+
+}  // namespace
+
+bool decode_tc_supported(const DecodeArgs& a) {
+    if (a.dim != (size_t)kDim || a.word_bits != 8 || a.n_vis == 0) return false;
+    if (a.bits != 1 && a.bits != 2 && a.bits != 4 && a.bits != 8) return false;
+    if (a.group < 1 || a.group > 8) return false;
+    if (a.units == 0) return false;
+    int S, T;
+    plan(a, S, T);
+    if (T > kMaxT) return false;
+    // fp32 tail split over the cluster: at most kTailMax rows per CTA.
+    if (a.tail_cap > (size_t)kTailMax * S) return false;
+    return tc_smem_bytes(a.bits, (int)a.group, T) <= 200 * 1024;
+}
+
+cudaError_t launch_decode_tc(const DecodeArgs& a, cudaStream_t s) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    PrepScratch& sc = g_scratch[dev & 15];
+    const int NT = a.group > 4 ? 2 : 1;
+    if (sc.units < a.units || sc.G < a.group) {
+        cudaFree(sc.frag);
+        cudaFree(sc.qconst);
+        sc.frag = nullptr;
+        sc.qconst = nullptr;
+        cudaError_t e = cudaMalloc(&sc.frag, a.units * 2 * 512 * sizeof(uint32_t));
+        if (e != cudaSuccess) return e;
+        e = cudaMalloc(&sc.qconst, a.units * 8 * sizeof(float2));
+        if (e != cudaSuccess) return e;
+        sc.units = a.units;
+        sc.G = 8;
+    }
+    switch (a.bits * 10 + NT) {
+        case 11: return launch_bits<1, 1>(a, s, sc.frag, sc.qconst);
+        case 12: return launch_bits<1, 2>(a, s, sc.frag, sc.qconst);
+        case 21: return launch_bits<2, 1>(a, s, sc.frag, sc.qconst);
+        case 22: return launch_bits<2, 2>(a, s, sc.frag, sc.qconst);
+        case 41: return launch_bits<4, 1>(a, s, sc.frag, sc.qconst);
+        case 42: return launch_bits<4, 2>(a, s, sc.frag, sc.qconst);
+        case 81: return launch_bits<8, 1>(a, s, sc.frag, sc.qconst);
+        case 82: return launch_bits<8, 2>(a, s, sc.frag, sc.qconst);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
 }  // namespace kvqb
