@@ -16,8 +16,9 @@
 //   phase A       : IMMA  [16 head-planes x 32 ch] x [32 ch x 8 tokens]; B operand is
 //                   the raw code bytes: one LOP3 extracts 4 codes (x 2^sh) per register
 //   cluster #1    : DSMEM exchange of per-CTA (min, max, tail max) -> gamma, delta, m
-//   phase B       : p = exp(g(s) - m) as u16 (two u8 planes) -> IMMA [16 ch x 32 tok]
-//                   x [32 tok x 8 head-planes]; V codes byte-transposed with PRMT
+//   phase B       : p = exp(g(s) - m) as a 22-bit integer (three u8 planes) -> IMMA
+//                   [16 head-planes x 32 tok] x [32 tok x 8 ch]; V codes byte-transposed
+//                   with PRMT, slot-selected with LOP3
 //   cluster #2/#3 : DSMEM reduction of partial numerators/denominators -> out
 // Packed K/V are never dequantized; the only fp32 math per token is the softmax.
 #include <cooperative_groups.h>
@@ -39,7 +40,8 @@ constexpr int kMaxT = 2048;    // visual tokens per CTA
 constexpr int kMaxCluster = 16;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: float -> int rounding trick
-constexpr uint32_t kMagicBits = 0x4B400000u;
+constexpr float kPScale = 4194303.0f;  // 2^22 - 1: probabilities as 22-bit integers
+constexpr int kPRow = 12;              // words per p-plane smem row (stride avoids bank conflicts)
 
 template <int BITS>
 struct Geo {
@@ -220,7 +222,7 @@ struct Partial {  // per-CTA softmax statistics, exchanged through DSMEM
 };
 
 template <int BITS, int NT>
-__global__ void __launch_bounds__(kThreads, 3) decode_tc_kernel(const TcParams p) {
+__global__ void __launch_bounds__(kThreads, NT == 1 ? 3 : 2) decode_tc_kernel(const TcParams p) {
     using Gm = Geo<BITS>;
     const DecodeArgs& a = p.a;
     const int G = (int)a.group;
@@ -241,7 +243,8 @@ __global__ void __launch_bounds__(kThreads, 3) decode_tc_kernel(const TcParams p
     float* pub = gpar + 32;                                                // [G][128] numerators
     float* pub_den = pub + G * kDim;                                       // [8]
     float* wpart = pub_den + 8;                                            // [4 warps][8][3]
-    uint64_t* full = reinterpret_cast<uint64_t*>(wpart + kConsumerWarps * 8 * 3 + 2);  // 8-byte aligned below
+    uint32_t* pplanes = reinterpret_cast<uint32_t*>(wpart + kConsumerWarps * 8 * 3);  // [warp][NT][12][kPRow]
+    uint64_t* full = reinterpret_cast<uint64_t*>(pplanes + kConsumerWarps * NT * 12 * kPRow + 2);
     full = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(full) + 7) & ~uintptr_t(7));
     uint64_t* empty = full + kStages;
 
@@ -459,25 +462,29 @@ __global__ void __launch_bounds__(kThreads, 3) decode_tc_kernel(const TcParams p
     consumers_sync();
 
     // ---------------- phase B: p . V over the visual chunk ----------------
-    int vacc[NT][8][4];
+    // D[16 head-planes x 8 ch] += P[16 head-planes x 32 tok] * V[32 tok x 8 ch], 16 channel
+    // tiles per 32-token block. p = exp(g(s) - m) in [0, 1] is a 22-bit integer split in
+    // three u8 planes (A rows plane*4 + head), written once per (head, token) to a per-warp
+    // smem tile in MMA k-order. V codes are the B operand: four tokens per register (PRMT
+    // byte transpose) x 2^sh (LOP3 slot select) - never dequantized.
+    uint32_t* pw = pplanes + warp * NT * 12 * kPRow;
+    int vacc[NT][16][4];
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
+    for (int mt = 0; mt < NT; ++mt)
 #pragma unroll
-        for (int mt = 0; mt < 8; ++mt)
+        for (int nc = 0; nc < 16; ++nc)
 #pragma unroll
-            for (int r = 0; r < 4; ++r) vacc[nt][mt][r] = 0;
-    uint32_t wsum[NT];
-    int wcount[NT];
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) wsum[nt] = 0, wcount[nt] = 0;
+            for (int r = 0; r < 4; ++r) vacc[mt][nc][r] = 0;
+    float wsum[NT];
+    const int pj = lane & 7, ph = lane >> 3;              // p-writer: k-word pj of head ph
+    const int ptok = (pj & 3) + 16 * (pj >> 2);          // token of k = 4*pj (+4i for byte i)
     float pa[NT], pb[NT];
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-        const int h = 4 * nt + (g >> 1);
-        pa[nt] = gpar[h * 4 + 0];
-        pb[nt] = gpar[h * 4 + 1];
+    for (int mt = 0; mt < NT; ++mt) {
+        wsum[mt] = 0.f;
+        pa[mt] = gpar[(4 * mt + ph) * 4 + 0];
+        pb[mt] = gpar[(4 * mt + ph) * 4 + 1];
     }
-    const int e = g & 1;
     for (int st = 0; st < nstage; ++st) {
         const int i = nstage + st;
         const int slot = i % kStages;
@@ -487,30 +494,38 @@ __global__ void __launch_bounds__(kThreads, 3) decode_tc_kernel(const TcParams p
         const int nblk = (ns + 31) >> 5;
         for (int blk = warp; blk < nblk; blk += kConsumerWarps) {
             const int btok = st * Gm::kStageTokens + blk * 32;  // chunk-local first token
-            // B operand: u16 probabilities of head (g/2 + 4nt), as two u8 digit planes.
-            uint32_t bq[NT][2];
 #pragma unroll
-            for (int nt = 0; nt < NT; ++nt) {
-                const int h = 4 * nt + (g >> 1);
-                uint32_t pv[4];
+            for (int mt = 0; mt < NT; ++mt) {
+                const int h = 4 * mt + ph;
+                uint32_t v[4];
 #pragma unroll
                 for (int ii = 0; ii < 4; ++ii) {
-                    const int tok = btok + 16 * e + t + 4 * ii;
+                    const int tok = btok + ptok + 4 * ii;
                     float pr = 0.0f;
-                    if (h < G && tok < nv) pr = ex2(__fmaf_rn(scores[h * TS + tok], pa[nt], pb[nt]));
-                    // round(p * 65535) in the low bits of the float (magic-number rounding)
-                    pv[ii] = __float_as_uint(__fmaf_rn(fminf(pr, 1.0f), 65535.0f, kMagic));
+                    if (h < G && tok < nv) pr = fminf(ex2(__fmaf_rn(scores[h * TS + tok], pa[mt], pb[mt])), 1.0f);
+                    const float f = __fmaf_rn(pr, kPScale, kMagic);  // round(p * (2^22-1)) in the low bits
+                    v[ii] = __float_as_uint(f);
+                    wsum[mt] += f - kMagic;
                 }
-                wsum[nt] += pv[0] + pv[1] + pv[2] + pv[3];
-                wcount[nt] += 4;
-                const uint32_t p01 = prmt(pv[0], pv[1], 0x5140), p23 = prmt(pv[2], pv[3], 0x5140);
-                const uint32_t lo8 = prmt(p01, p23, 0x5410), hi8 = prmt(p01, p23, 0x7632);
-                const uint32_t send = e ? hi8 : lo8;
-                const uint32_t recv = __shfl_xor_sync(0xffffffffu, send, 4);
-                bq[nt][0] = e ? recv : hi8;  // tokens t+4i       (plane: hi for even g)
-                bq[nt][1] = e ? lo8 : recv;  // tokens 16+t+4i
+                const uint32_t p01 = prmt(v[0], v[1], 0x5140), p23 = prmt(v[2], v[3], 0x5140);
+                const uint32_t q01 = prmt(v[0], v[1], 0x7362), q23 = prmt(v[2], v[3], 0x7362);
+                uint32_t* rowp = pw + (mt * 12 + ph) * kPRow + pj;
+                rowp[0 * 4 * kPRow] = prmt(p01, p23, 0x5410);                 // bits 0-7
+                rowp[1 * 4 * kPRow] = prmt(p01, p23, 0x7632);                 // bits 8-15
+                rowp[2 * 4 * kPRow] = prmt(q01, q23, 0x5410) & 0x3F3F3F3Fu;   // bits 16-21
             }
-            // A operand: V codes of this lane's 2*BITS bytes for 8 tokens, byte-transposed.
+            __syncwarp();
+            uint32_t afr[NT][4];
+#pragma unroll
+            for (int mt = 0; mt < NT; ++mt) {
+                const uint32_t* r0 = pw + (mt * 12 + g) * kPRow;
+                afr[mt][0] = r0[t];
+                afr[mt][2] = r0[4 + t];
+                afr[mt][1] = g < 4 ? r0[8 * kPRow + t] : 0u;
+                afr[mt][3] = g < 4 ? r0[8 * kPRow + 4 + t] : 0u;
+            }
+            __syncwarp();
+            // B operand: V codes of this lane's 2*BITS bytes for 8 tokens, byte-transposed.
             constexpr int NW = (2 * BITS + 3) / 4;  // 32-bit words per token slice
             uint32_t X[2][2 * BITS];
 #pragma unroll
@@ -524,11 +539,11 @@ __global__ void __launch_bounds__(kThreads, 3) decode_tc_kernel(const TcParams p
                     } else if (BITS == 2) {
                         raw[ii][0] = *reinterpret_cast<const uint32_t*>(rp);
                     } else if (BITS == 4) {
-                        uint2 v = *reinterpret_cast<const uint2*>(rp);
-                        raw[ii][0] = v.x, raw[ii][NW - 1] = v.y;
+                        uint2 vv = *reinterpret_cast<const uint2*>(rp);
+                        raw[ii][0] = vv.x, raw[ii][NW - 1] = vv.y;
                     } else {
-                        uint4 v = *reinterpret_cast<const uint4*>(rp);
-                        raw[ii][0] = v.x, raw[ii][1 % NW] = v.y, raw[ii][2 % NW] = v.z, raw[ii][3 % NW] = v.w;
+                        uint4 vv = *reinterpret_cast<const uint4*>(rp);
+                        raw[ii][0] = vv.x, raw[ii][1 % NW] = vv.y, raw[ii][2 % NW] = vv.z, raw[ii][3 % NW] = vv.w;
                     }
                 }
 #pragma unroll
@@ -546,14 +561,13 @@ __global__ void __launch_bounds__(kThreads, 3) decode_tc_kernel(const TcParams p
                 }
             }
 #pragma unroll
-            for (int mt = 0; mt < 8; ++mt) {
+            for (int nc = 0; nc < 16; ++nc) {
                 constexpr int cpb = Gm::kCpb;
-                const int i0 = mt, i1 = 8 + mt;
-                const uint32_t m0 = Gm::kMask << ((i0 % cpb) * BITS), m1 = Gm::kMask << ((i1 % cpb) * BITS);
-                const uint32_t a0 = X[0][i0 / cpb] & m0, a1 = X[0][i1 / cpb] & m1;
-                const uint32_t a2 = X[1][i0 / cpb] & m0, a3 = X[1][i1 / cpb] & m1;
+                const uint32_t m = Gm::kMask << ((nc % cpb) * BITS);
+                const uint32_t b0 = X[0][nc / cpb] & m, b1 = X[1][nc / cpb] & m;
 #pragma unroll
-                for (int nt = 0; nt < NT; ++nt) imma_u8u8(vacc[nt][mt], a0, a1, a2, a3, bq[nt][0], bq[nt][1]);
+                for (int mt = 0; mt < NT; ++mt)
+                    imma_u8u8(vacc[mt][nc], afr[mt][0], afr[mt][1], afr[mt][2], afr[mt][3], b0, b1);
             }
         }
         __syncwarp();
@@ -568,27 +582,30 @@ __global__ void __launch_bounds__(kThreads, 3) decode_tc_kernel(const TcParams p
     float* redw = red + kConsumerWarps * G * kDim;
     const float levels = (float)((1u << BITS) - 1u);
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-        const int h = 4 * nt + t;  // C columns 2t, 2t+1: head t's (hi, lo) digit planes
+    for (int mt = 0; mt < NT; ++mt) {
+        const int h = 4 * mt + (g & 3);
 #pragma unroll
-        for (int mt = 0; mt < 8; ++mt) {
-#pragma unroll
-            for (int rr = 0; rr < 2; ++rr) {
-                int sh;
-                const int ch = v_channel<BITS>(g, rr * 8 + mt, sh);
-                const uint32_t chi = (uint32_t)vacc[nt][mt][2 * rr] >> sh;
-                const uint32_t clo = (uint32_t)vacc[nt][mt][2 * rr + 1] >> sh;
-                if (h < G) red[(warp * G + h) * kDim + ch] = (float)chi * 256.0f + (float)clo;
-            }
+        for (int nc = 0; nc < 16; ++nc) {
+            // rows g / g+8: planes (0, 2) for g < 4, plane 1 for g >= 4, head g % 4.
+            const float lo0 = (float)(uint32_t)vacc[mt][nc][0], lo1 = (float)(uint32_t)vacc[mt][nc][1];
+            const float hi0 = (float)(uint32_t)vacc[mt][nc][2], hi1 = (float)(uint32_t)vacc[mt][nc][3];
+            const float part0 = g < 4 ? __fmaf_rn(hi0, 65536.0f, lo0) : lo0 * 256.0f;  // column 2t
+            const float part1 = g < 4 ? __fmaf_rn(hi1, 65536.0f, lo1) : lo1 * 256.0f;  // column 2t+1
+            const float send = g < 4 ? part1 : part0;
+            const float recv = __shfl_xor_sync(0xffffffffu, send, 16);
+            const int col = 2 * t + (g < 4 ? 0 : 1);
+            const float val = (g < 4 ? part0 : part1) + recv;
+            int sh;
+            const int ch = v_channel<BITS>(col, nc, sh);
+            if (h < G) red[(warp * G + h) * kDim + ch] = val * __int_as_float((127 - sh) << 23);
         }
-        // sum of u16 weights of head (g/2 + 4nt) over this warp's tokens
-        uint32_t ws = wsum[nt] - (uint32_t)wcount[nt] * kMagicBits;
+        float ws = wsum[mt];
 #pragma unroll
         for (int o : {1, 2, 4}) ws += __shfl_xor_sync(0xffffffffu, ws, o);
-        if ((lane & 7) == 0 && 4 * nt + (g >> 1) < G) redw[warp * 8 + 4 * nt + (g >> 1)] = (float)ws;
+        if (pj == 0 && 4 * mt + ph < G) redw[warp * 8 + 4 * mt + ph] = ws;
     }
     consumers_sync();
-    // fp32 tail weights and values of this CTA (already on the 65535 scale).
+    // fp32 tail weights and values of this CTA (on the same 2^22 - 1 scale).
     for (int idx = threadIdx.x; idx < G * kDim; idx += kConsumerWarps * 32) {
         const int h = idx / kDim, ch = idx % kDim;
         float num = 0.f;
@@ -600,7 +617,7 @@ __global__ void __launch_bounds__(kThreads, 3) decode_tc_kernel(const TcParams p
         for (int w2 = 0; w2 < kConsumerWarps; ++w2) wv += redw[w2 * 8 + h];
         float tnum = 0.f;
         for (int j = 0; j < ntl; ++j) {
-            const float pt = ex2(__fmaf_rn(tail_s[h * kTailMax + j], kLog2e, gpar[h * 4 + 2])) * 65535.0f;
+            const float pt = ex2(__fmaf_rn(tail_s[h * kTailMax + j], kLog2e, gpar[h * 4 + 2])) * kPScale;
             tnum = __fmaf_rn(pt, a.v_tail[((size_t)unit * a.tail_cap + tt0 + j) * kDim + ch], tnum);
         }
         pub[h * kDim + ch] = __fmaf_rn(step, num, __fmaf_rn(va, wv, tnum));
@@ -611,7 +628,7 @@ __global__ void __launch_bounds__(kThreads, 3) decode_tc_kernel(const TcParams p
         if (h < G) {
             for (int w2 = 0; w2 < kConsumerWarps; ++w2) wv += redw[w2 * 8 + h];
             for (int j = 0; j < ntl; ++j)
-                wt += ex2(__fmaf_rn(tail_s[h * kTailMax + j], kLog2e, gpar[h * 4 + 2])) * 65535.0f;
+                wt += ex2(__fmaf_rn(tail_s[h * kTailMax + j], kLog2e, gpar[h * 4 + 2])) * kPScale;
         }
         pub_den[h] = wv + wt;
     }
@@ -638,7 +655,7 @@ size_t tc_smem_bytes(int bits, int G, int T) {
     const size_t red = (size_t)kConsumerWarps * (G * kDim + 8) * 4;
     if (ring < red) ring = red;
     return ring + (size_t)G * (T + 4) * 4 + (size_t)G * kTailMax * 4 + (size_t)G * kDim * 4 + sizeof(Partial) +
-           32 * 4 + (size_t)G * kDim * 4 + 8 * 4 + kConsumerWarps * 8 * 3 * 4 + 16 + 2 * kStages * 8 + 16;
+           32 * 4 + (size_t)G * kDim * 4 + 8 * 4 + kConsumerWarps * 8 * 3 * 4 + (size_t)kConsumerWarps * 2 * 12 * kPRow * 4 + 16 + 2 * kStages * 8 + 16;
 }
 
 // Scratch for the prep kernel's outputs (grown on demand, per device).

@@ -206,7 +206,8 @@ def test_decode_golden_trajectories(kvq, oracle, name, path):
         assert rel_l2(out, z[f"out{t}"]) <= tol, f"{name} step {t}: {rel_l2(out, z[f'out{t}'])}"
         det = cache.decode_step_detailed(z[f"q{t}"])
         assert np.all(np.abs(det.weights - z[f"w{t}"]) <= 1e-5)
-        assert np.all(np.abs(det.weights.sum(1) - 1) <= 1e-5)
+        if det.weights.shape[1]:
+            assert np.all(np.abs(det.weights.sum(1) - 1) <= 1e-5)
         assert det.slope_violations == int(z[f"viol{t}"])
         assert rel_l2(det.outputs, z[f"out{t}"]) <= TOL_GENERIC
         cache.append(z[f"knew{t}"], z[f"vnew{t}"])
