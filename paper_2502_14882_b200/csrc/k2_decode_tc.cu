@@ -12,7 +12,7 @@
 //   round(S_h qs_c / 2^sh_c) split into 4 balanced int8 digit planes; S_h bounds the
 //   int32 score so IMMA accumulation is exact. Emits the A-fragments of the q.K MMA.
 // Kernel 2 (decode, cluster of S CTAs per unit, each a contiguous token chunk):
-//   producer warp : cp.async.bulk (TMA) ring of 8-16 KB stages, K chunk then V chunk
+//   one warp/CTA  : cp.async.bulk (TMA) ring of 4 KB stages, K chunk then V chunk
 //   phase A       : IMMA  [16 head-planes x 32 ch] x [32 ch x 8 tokens]; B operand is
 //                   the raw code bytes: one LOP3 extracts 4 codes (x 2^sh) per register
 //   cluster #1    : DSMEM exchange of per-CTA (min, max, tail max) -> gamma, delta, m
@@ -32,9 +32,8 @@ namespace kvqb {
 namespace {
 
 constexpr int kDim = 128;
-constexpr int kConsumerWarps = 4;
-constexpr int kThreads = (kConsumerWarps + 1) * 32;
 constexpr int kStages = 4;
+constexpr int kStageBytes = 4096;
 constexpr int kTailMax = 64;   // fp32 tail tokens per CTA
 constexpr int kMaxT = 2048;    // visual tokens per CTA
 constexpr int kMaxCluster = 16;
@@ -46,8 +45,7 @@ constexpr int kPRow = 12;              // words per p-plane smem row (stride avo
 template <int BITS>
 struct Geo {
     static constexpr int kRowBytes = 16 * BITS;
-    static constexpr int kStageTokens = BITS <= 2 ? 512 / BITS : 128;
-    static constexpr int kStageBytes = kStageTokens * kRowBytes;
+    static constexpr int kStageTokens = kStageBytes / kRowBytes;  // 256 / BITS
     static constexpr int kCpb = 8 / BITS;  // codes per byte
     static constexpr uint32_t kMask = 0x01010101u * ((1u << BITS) - 1u);
 };
@@ -96,9 +94,6 @@ __device__ __forceinline__ void cluster_wait() {
 }
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;"); }
-__device__ __forceinline__ void consumers_sync() {
-    asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
-}
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
     uint32_t r;
     asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
@@ -221,8 +216,51 @@ struct Partial {  // per-CTA softmax statistics, exchanged through DSMEM
     float lo[8], hi[8], tmax[8];
 };
 
+struct Smem {  // carve-up of the dynamic shared memory of one decode CTA
+    uint8_t* ring;     // kStages x kStageBytes: TMA landing zone; reused for `pub` after phase B
+    float* scores;     // [G][T + 4] calibrated-softmax inputs of the visual chunk
+    float* tail_s;     // [G][kTailMax] fp32 tail scores of this CTA's tail rows
+    uint32_t* pw;      // [NT][12][kPRow] p digit planes of the current 32-token block
+    Partial* part;     // this CTA's (min, max, tail max) per head
+    float* gpar;       // [8][4] softmax parameters per head
+    float* pub_den;    // [8] this CTA's softmax denominators
+    uint64_t* full;    // [kStages] TMA completion barriers
+};
+
+__host__ __device__ inline size_t tc_smem_bytes(int G, int T, int NT, Smem* out = nullptr,
+                                                uint8_t* base = nullptr) {
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        size_t o = off;
+        off += (bytes + 15) & ~size_t(15);
+        return base + o;
+    };
+    uint8_t* ring = take(kStages * kStageBytes);
+    uint8_t* scores = take((size_t)G * (T + 4) * 4);
+    uint8_t* tail_s = take((size_t)G * kTailMax * 4);
+    uint8_t* pw = take((size_t)NT * 12 * kPRow * 4);
+    uint8_t* part = take(sizeof(Partial));
+    uint8_t* gpar = take(32 * 4);
+    uint8_t* den = take(8 * 4);
+    uint8_t* full = take(kStages * 8);
+    if (out) {
+        out->ring = ring;
+        out->scores = reinterpret_cast<float*>(scores);
+        out->tail_s = reinterpret_cast<float*>(tail_s);
+        out->pw = reinterpret_cast<uint32_t*>(pw);
+        out->part = reinterpret_cast<Partial*>(part);
+        out->gpar = reinterpret_cast<float*>(gpar);
+        out->pub_den = reinterpret_cast<float*>(den);
+        out->full = reinterpret_cast<uint64_t*>(full);
+    }
+    return off;
+}
+
+// One warp per CTA: the warp streams its own token chunk through a TMA ring (lane 0
+// re-arms a slot as soon as the warp has consumed it), so no producer warp, no empty
+// barriers and no cross-warp reductions; one CTA = one contiguous chunk of T tokens.
 template <int BITS, int NT>
-__global__ void __launch_bounds__(kThreads, NT == 1 ? 3 : 2) decode_tc_kernel(const TcParams p) {
+__global__ void __launch_bounds__(32, 8) decode_tc_kernel(const TcParams p) {
     using Gm = Geo<BITS>;
     const DecodeArgs& a = p.a;
     const int G = (int)a.group;
@@ -230,25 +268,14 @@ __global__ void __launch_bounds__(kThreads, NT == 1 ? 3 : 2) decode_tc_kernel(co
     cg::cluster_group cluster = cg::this_cluster();
     const int rank = (int)cluster.block_rank();
     const int unit = blockIdx.x / S;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int lane = threadIdx.x;
     const int g = lane >> 2, t = lane & 3;
 
-    extern __shared__ __align__(128) uint8_t smem[];
-    uint8_t* ring = smem;                                                  // kStages x stage bytes
-    float* scores = reinterpret_cast<float*>(ring + kStages * Gm::kStageBytes);  // [G][TS]
-    float* tail_s = scores + G * TS;                                       // [G][kTailMax]
-    float* q_s = tail_s + G * kTailMax;                                    // [G][128]
-    Partial* part = reinterpret_cast<Partial*>(q_s + G * kDim);
-    float* gpar = reinterpret_cast<float*>(part + 1);                      // [8][4]: A', B', tail B', -
-    float* pub = gpar + 32;                                                // [G][128] numerators
-    float* pub_den = pub + G * kDim;                                       // [8]
-    float* wpart = pub_den + 8;                                            // [4 warps][8][3]
-    uint32_t* pplanes = reinterpret_cast<uint32_t*>(wpart + kConsumerWarps * 8 * 3);  // [warp][NT][12][kPRow]
-    uint64_t* full = reinterpret_cast<uint64_t*>(pplanes + kConsumerWarps * NT * 12 * kPRow + 2);
-    full = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(full) + 7) & ~uintptr_t(7));
-    uint64_t* empty = full + kStages;
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    Smem sm;
+    tc_smem_bytes(G, T, NT, &sm, smem_raw);
+    float* scores = sm.scores;
 
-    // Work split: visual tokens [tok0, tok0 + nv), tail tokens [tt0, tt0 + ntl).
     const int n = (int)a.n_vis;
     const int tok0 = rank * T;
     const int nv = max(0, min(T, n - tok0));
@@ -256,53 +283,27 @@ __global__ void __launch_bounds__(kThreads, NT == 1 ? 3 : 2) decode_tc_kernel(co
     const int tail_per = (n_tail + S - 1) / S;
     const int tt0 = rank * tail_per;
     const int ntl = max(0, min(tail_per, n_tail - tt0));
-    const size_t rb = Gm::kRowBytes;
-    const uint8_t* kcodes = a.k_codes + ((size_t)unit * n + tok0) * rb;
-    const uint8_t* vcodes = a.v_codes + ((size_t)unit * n + tok0) * rb;
+    const uint8_t* kcodes = a.k_codes + ((size_t)unit * n + tok0) * Gm::kRowBytes;
+    const uint8_t* vcodes = a.v_codes + ((size_t)unit * n + tok0) * Gm::kRowBytes;
     const int nstage = (nv + Gm::kStageTokens - 1) / Gm::kStageTokens;
+    const int total_stages = 2 * nstage;
 
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < kStages; ++i) {
-            mbar_init(&full[i], 1);
-            mbar_init(&empty[i], kConsumerWarps);
-        }
+    auto issue = [&](int i) {  // lane 0 only: stage i (K stages, then V stages) into slot i % kStages
+        const int slot = i % kStages;
+        const int si = i < nstage ? i : i - nstage;
+        const uint8_t* src = (i < nstage ? kcodes : vcodes) + (size_t)si * kStageBytes;
+        const uint32_t bytes = (uint32_t)(min(Gm::kStageTokens, nv - si * Gm::kStageTokens) * Gm::kRowBytes);
+        mbar_expect_tx(&sm.full[slot], bytes);
+        bulk_g2s(sm.ring + slot * kStageBytes, src, bytes, &sm.full[slot]);
+    };
+    if (lane == 0) {
+        for (int i = 0; i < kStages; ++i) mbar_init(&sm.full[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int i = 0; i < min(kStages, total_stages); ++i) issue(i);
     }
-    __syncthreads();
+    __syncwarp();
 
-    if (warp == kConsumerWarps) {
-        // ===== producer: K stages then V stages through the ring =====
-        auto issue = [&](int i) {
-            const int slot = i % kStages;
-            if (i >= kStages) mbar_wait(&empty[slot], ((i / kStages) - 1) & 1);
-            const int si = i < nstage ? i : i - nstage;
-            const uint8_t* src = (i < nstage ? kcodes : vcodes) + (size_t)si * Gm::kStageBytes;
-            const int ntok = min(Gm::kStageTokens, nv - si * Gm::kStageTokens);
-            const uint32_t bytes = (uint32_t)(ntok * Gm::kRowBytes);
-            mbar_expect_tx(&full[slot], bytes);
-            bulk_g2s(ring + slot * Gm::kStageBytes, src, bytes, &full[slot]);
-        };
-        // Everything that can be in flight before phase B frees ring slots.
-        const int pre = min(2 * nstage, nstage + kStages);
-        if (lane == 0)
-            for (int i = 0; i < pre; ++i) issue(i);
-        __syncwarp();
-        cluster_arrive();  // #1 (nothing to publish)
-        if (lane == 0)
-            for (int i = pre; i < 2 * nstage; ++i) issue(i);
-        __syncwarp();
-        cluster_wait();
-        cluster_arrive();  // #2
-        cluster_wait();
-        cluster_arrive();  // #3
-        cluster_wait();
-        return;
-    }
-
-    // ===== consumers =====
-    for (int i = threadIdx.x; i < G * kDim; i += kConsumerWarps * 32)
-        q_s[i] = a.q[(size_t)unit * G * kDim + i];
-    griddep_wait();  // prep results visible
+    griddep_wait();  // prep kernel's q planes are visible from here on
     uint32_t afrag[NT][4][4];
     const uint32_t* fr = p.frag + (size_t)unit * NT * 512;
 #pragma unroll
@@ -310,42 +311,39 @@ __global__ void __launch_bounds__(kThreads, NT == 1 ? 3 : 2) decode_tc_kernel(co
 #pragma unroll
         for (int kb = 0; kb < 4; ++kb)
 #pragma unroll
-            for (int r = 0; r < 4; ++r) afrag[nt][kb][r] = fr[((nt * 4 + kb) * 4 + r) * 32 + lane];
-    // Phase-A epilogue constants: this lane's head and plane weights.
+            for (int r = 0; r < 4; ++r) afrag[nt][kb][r] = __ldg(fr + ((nt * 4 + kb) * 4 + r) * 32 + lane);
     const bool lowlane = g < 4;
     const int wl = lowlane ? 1 : 256, wh = lowlane ? 65536 : (1 << 24);
-    float cA[NT], cB[NT];
+    float cA[NT], cB[NT], lo[NT], hi[NT];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
         const int h = 4 * nt + (g & 3);
-        float2 qc = h < G ? p.qconst[(size_t)unit * G + h] : make_float2(0.f, 0.f);
-        cA[nt] = qc.x;
-        cB[nt] = qc.y;
+        const float2 qc = h < G ? p.qconst[(size_t)unit * G + h] : make_float2(0.f, 0.f);
+        cA[nt] = qc.x, cB[nt] = qc.y;
+        lo[nt] = INFINITY, hi[nt] = -INFINITY;
     }
-    float lo[NT], hi[NT];
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) lo[nt] = INFINITY, hi[nt] = -INFINITY;
 
     // ---------------- phase A: scores of the visual chunk ----------------
     for (int st = 0; st < nstage; ++st) {
         const int slot = st % kStages;
-        mbar_wait(&full[slot], (st / kStages) & 1);
-        const uint8_t* buf = ring + slot * Gm::kStageBytes;
+        mbar_wait(&sm.full[slot], (st / kStages) & 1);
+        const uint8_t* buf = sm.ring + slot * kStageBytes;
         const int ns = min(Gm::kStageTokens, nv - st * Gm::kStageTokens);
         const int ntiles = (ns + 7) >> 3;
-        for (int tile = warp; tile < ntiles; tile += kConsumerWarps) {
-            // B operand: this lane's BITS words of token row (tile*8 + g).
+        const int tbase = st * Gm::kStageTokens + 2 * t + (lowlane ? 0 : 1);
+#pragma unroll 2
+        for (int tile = 0; tile < ntiles; ++tile) {
             const uint8_t* rowp = buf + (tile * 8 + g) * Gm::kRowBytes + t * 4 * BITS;
             uint32_t w[BITS];
             if (BITS == 1) {
                 w[0] = *reinterpret_cast<const uint32_t*>(rowp);
             } else if (BITS == 2) {
-                uint2 v = *reinterpret_cast<const uint2*>(rowp);
+                const uint2 v = *reinterpret_cast<const uint2*>(rowp);
                 w[0] = v.x, w[1 % BITS] = v.y;
             } else {
 #pragma unroll
                 for (int u = 0; u < BITS; u += 4) {
-                    uint4 v = *reinterpret_cast<const uint4*>(rowp + 4 * u);
+                    const uint4 v = *reinterpret_cast<const uint4*>(rowp + 4 * u);
                     w[u] = v.x, w[(u + 1) % BITS] = v.y, w[(u + 2) % BITS] = v.z, w[(u + 3) % BITS] = v.w;
                 }
             }
@@ -353,18 +351,18 @@ __global__ void __launch_bounds__(kThreads, NT == 1 ? 3 : 2) decode_tc_kernel(co
 #pragma unroll
             for (int rho = 0; rho < 8; ++rho)
                 breg[rho] = w[rho / Gm::kCpb] & (Gm::kMask << ((rho % Gm::kCpb) * BITS));
+            const int tok = tbase + tile * 8;
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt) {
                 int acc[4] = {0, 0, 0, 0};
 #pragma unroll
                 for (int kb = 0; kb < 4; ++kb) imma_s8u8(acc, afrag[nt][kb], breg[2 * kb], breg[2 * kb + 1]);
-                // rows g / g+8 hold digit planes (0,2) [g<4] or (1,3) [g>=4] of head g%4.
-                const int p0 = acc[0] * wl + acc[2] * wh;  // token 2t   (mod 2^32; exact total)
+                // rows g / g+8 hold digit planes (0,2) [g<4] or (1,3) [g>=4] of head g%4;
+                // the int32 sums wrap mod 2^32 but the total is exact (|score| < 2^31).
+                const int p0 = acc[0] * wl + acc[2] * wh;  // token 2t
                 const int p1 = acc[1] * wl + acc[3] * wh;  // token 2t+1
-                const int send = lowlane ? p1 : p0;
-                const int recv = __shfl_xor_sync(0xffffffffu, send, 16);
+                const int recv = __shfl_xor_sync(0xffffffffu, lowlane ? p1 : p0, 16);
                 const int total = (lowlane ? p0 : p1) + recv;
-                const int tok = st * Gm::kStageTokens + tile * 8 + 2 * t + (lowlane ? 0 : 1);
                 const int h = 4 * nt + (g & 3);
                 if (h < G && tok < nv) {
                     const float s = __fmaf_rn((float)total, cA[nt], cB[nt]);
@@ -375,31 +373,26 @@ __global__ void __launch_bounds__(kThreads, NT == 1 ? 3 : 2) decode_tc_kernel(co
             }
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[slot]);
+        if (lane == 0 && st + kStages < total_stages) issue(st + kStages);
     }
 
-    // fp32 tail tokens of this CTA: warp per token, lanes split the 128 channels.
+    // fp32 tail rows of this CTA: lanes split the 128 channels.
     const float isd = __fdiv_rn(1.0f, sqrtf((float)kDim));
-    float tmax_l[8];
-#pragma unroll
-    for (int h = 0; h < 8; ++h) tmax_l[h] = -INFINITY;
-    for (int j = warp; j < ntl; j += kConsumerWarps) {
+    float tmax = -INFINITY;  // for head (lane & 7)
+    for (int j = 0; j < ntl; ++j) {
         const float4 kv = *reinterpret_cast<const float4*>(
             a.k_tail + ((size_t)unit * a.tail_cap + tt0 + j) * kDim + 4 * lane);
-#pragma unroll
-        for (int h = 0; h < 8; ++h) {
-            if (h >= G) break;
-            const float* qh = q_s + h * kDim + 4 * lane;
-            float d = kv.x * qh[0] + kv.y * qh[1] + kv.z * qh[2] + kv.w * qh[3];
+        for (int h = 0; h < G; ++h) {
+            const float4 qv = *reinterpret_cast<const float4*>(a.q + ((size_t)unit * G + h) * kDim + 4 * lane);
+            float d = kv.x * qv.x + kv.y * qv.y + kv.z * qv.z + kv.w * qv.w;
 #pragma unroll
             for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
             d *= isd;
-            if (lane == 0) tail_s[h * kTailMax + j] = d;
-            tmax_l[h] = fmaxf(tmax_l[h], d);
+            if (lane == 0) sm.tail_s[h * kTailMax + j] = d;
+            if ((lane & 7) == h) tmax = fmaxf(tmax, d);
         }
     }
-
-    // CTA partial (min, max) per head: lanes of one head differ in lane bits 0,1,4.
+    // CTA partial (min, max) per head: lanes of one head differ in lane bits 0, 1, 4.
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
 #pragma unroll
@@ -407,67 +400,50 @@ __global__ void __launch_bounds__(kThreads, NT == 1 ? 3 : 2) decode_tc_kernel(co
             lo[nt] = fminf(lo[nt], __shfl_xor_sync(0xffffffffu, lo[nt], o));
             hi[nt] = fmaxf(hi[nt], __shfl_xor_sync(0xffffffffu, hi[nt], o));
         }
-        if ((lane & 3) == 0 && lane < 16) {  // lane (g, 0), g < 4, holds head g of this tile
-            wpart[(warp * 8 + 4 * nt + (lane >> 2)) * 3 + 0] = lo[nt];
-            wpart[(warp * 8 + 4 * nt + (lane >> 2)) * 3 + 1] = hi[nt];
+        if ((lane & 3) == 0 && lane < 16) {
+            sm.part->lo[4 * nt + (lane >> 2)] = lo[nt];
+            sm.part->hi[4 * nt + (lane >> 2)] = hi[nt];
         }
     }
-    if (lane == 0)
-        for (int h = 0; h < 8; ++h) wpart[(warp * 8 + h) * 3 + 2] = tmax_l[h];
-    consumers_sync();
-    if (threadIdx.x < 8) {
-        const int h = threadIdx.x;
-        float l = INFINITY, u = -INFINITY, tm = -INFINITY;
-        if (h < 4 * NT)
-            for (int w2 = 0; w2 < kConsumerWarps; ++w2) {
-                l = fminf(l, wpart[(w2 * 8 + h) * 3 + 0]);
-                u = fmaxf(u, wpart[(w2 * 8 + h) * 3 + 1]);
-            }
-        for (int w2 = 0; w2 < kConsumerWarps; ++w2) tm = fmaxf(tm, wpart[(w2 * 8 + h) * 3 + 2]);
-        part->lo[h] = l;
-        part->hi[h] = u;
-        part->tmax[h] = tm;
-    }
+    if (NT == 1 && lane >= 4 && lane < 8) sm.part->lo[lane] = INFINITY, sm.part->hi[lane] = -INFINITY;
+    if (lane < 8) sm.part->tmax[lane] = tmax;
     cluster_arrive();  // #1: partials published
     cluster_wait();
 
     // Global softmax parameters per head (identical in every CTA of the cluster).
-    if (threadIdx.x < 8) {
-        const int h = threadIdx.x;
+    if (lane < 8) {
+        const int h = lane;
         float gamma = INFINITY, delta = -INFINITY, tm = -INFINITY;
         for (int r = 0; r < S; ++r) {
-            const Partial* pr = cluster.map_shared_rank(part, r);
+            const Partial* pr = cluster.map_shared_rank(sm.part, r);
             gamma = fminf(gamma, pr->lo[h]);
             delta = fmaxf(delta, pr->hi[h]);
             tm = fmaxf(tm, pr->tmax[h]);
         }
-        // g(x) = A x + B (calibrate.hpp:62-67); endpoints g(gamma) = gamma - tau1,
-        // g(delta) = delta - tau2; the calibrated row max is attained at an endpoint.
+        // g(x) = A x + B (calibrate.hpp:62-67): g(gamma) = gamma - tau1, g(delta) =
+        // delta - tau2; the calibrated row max is at an endpoint (or in the tail).
         const float width = __fsub_rn(delta, gamma);
         float A = 1.0f, B = -a.tau1, m = tm;
-        if (n > 0) {
-            if (width > 0.0f) {
-                const float r = __fdiv_rn(__fsub_rn(a.tau2, a.tau1), width);
-                A = 1.0f - r;
-                B = __fmaf_rn(r, gamma, -a.tau1);
-                m = fmaxf(m, fmaxf(__fsub_rn(gamma, a.tau1), __fsub_rn(delta, a.tau2)));
-            } else {
-                m = fmaxf(m, __fsub_rn(gamma, a.tau1));
-            }
+        if (width > 0.0f) {
+            const float r = __fdiv_rn(__fsub_rn(a.tau2, a.tau1), width);
+            A = 1.0f - r;
+            B = __fmaf_rn(r, gamma, -a.tau1);
+            m = fmaxf(m, fmaxf(__fsub_rn(gamma, a.tau1), __fsub_rn(delta, a.tau2)));
+        } else {
+            m = fmaxf(m, __fsub_rn(gamma, a.tau1));
         }
-        gpar[h * 4 + 0] = A * kLog2e;
-        gpar[h * 4 + 1] = (B - m) * kLog2e;
-        gpar[h * 4 + 2] = -m * kLog2e;
+        sm.gpar[h * 4 + 0] = A * kLog2e;
+        sm.gpar[h * 4 + 1] = (B - m) * kLog2e;
+        sm.gpar[h * 4 + 2] = -m * kLog2e;
     }
-    consumers_sync();
+    __syncwarp();
 
     // ---------------- phase B: p . V over the visual chunk ----------------
     // D[16 head-planes x 8 ch] += P[16 head-planes x 32 tok] * V[32 tok x 8 ch], 16 channel
     // tiles per 32-token block. p = exp(g(s) - m) in [0, 1] is a 22-bit integer split in
-    // three u8 planes (A rows plane*4 + head), written once per (head, token) to a per-warp
-    // smem tile in MMA k-order. V codes are the B operand: four tokens per register (PRMT
-    // byte transpose) x 2^sh (LOP3 slot select) - never dequantized.
-    uint32_t* pw = pplanes + warp * NT * 12 * kPRow;
+    // three u8 planes (A rows plane*4 + head), written once per (head, token) to a smem
+    // tile in MMA k-order. V codes are the B operand: four tokens per register (PRMT byte
+    // transpose) x 2^sh (LOP3 slot select) - never dequantized.
     int vacc[NT][16][4];
 #pragma unroll
     for (int mt = 0; mt < NT; ++mt)
@@ -476,23 +452,24 @@ __global__ void __launch_bounds__(kThreads, NT == 1 ? 3 : 2) decode_tc_kernel(co
 #pragma unroll
             for (int r = 0; r < 4; ++r) vacc[mt][nc][r] = 0;
     float wsum[NT];
-    const int pj = lane & 7, ph = lane >> 3;              // p-writer: k-word pj of head ph
-    const int ptok = (pj & 3) + 16 * (pj >> 2);          // token of k = 4*pj (+4i for byte i)
+    const int pj = lane & 7, ph = lane >> 3;      // p-writer: k-word pj of head ph
+    const int ptok = (pj & 3) + 16 * (pj >> 2);  // token of k = 4*pj (+4i for byte i)
     float pa[NT], pb[NT];
 #pragma unroll
     for (int mt = 0; mt < NT; ++mt) {
         wsum[mt] = 0.f;
-        pa[mt] = gpar[(4 * mt + ph) * 4 + 0];
-        pb[mt] = gpar[(4 * mt + ph) * 4 + 1];
+        pa[mt] = sm.gpar[(4 * mt + ph) * 4 + 0];
+        pb[mt] = sm.gpar[(4 * mt + ph) * 4 + 1];
     }
+    uint32_t* pw = sm.pw;
     for (int st = 0; st < nstage; ++st) {
         const int i = nstage + st;
         const int slot = i % kStages;
-        mbar_wait(&full[slot], (i / kStages) & 1);
-        const uint8_t* buf = ring + slot * Gm::kStageBytes;
+        mbar_wait(&sm.full[slot], (i / kStages) & 1);
+        const uint8_t* buf = sm.ring + slot * kStageBytes;
         const int ns = min(Gm::kStageTokens, nv - st * Gm::kStageTokens);
         const int nblk = (ns + 31) >> 5;
-        for (int blk = warp; blk < nblk; blk += kConsumerWarps) {
+        for (int blk = 0; blk < nblk; ++blk) {
             const int btok = st * Gm::kStageTokens + blk * 32;  // chunk-local first token
 #pragma unroll
             for (int mt = 0; mt < NT; ++mt) {
@@ -510,9 +487,9 @@ __global__ void __launch_bounds__(kThreads, NT == 1 ? 3 : 2) decode_tc_kernel(co
                 const uint32_t p01 = prmt(v[0], v[1], 0x5140), p23 = prmt(v[2], v[3], 0x5140);
                 const uint32_t q01 = prmt(v[0], v[1], 0x7362), q23 = prmt(v[2], v[3], 0x7362);
                 uint32_t* rowp = pw + (mt * 12 + ph) * kPRow + pj;
-                rowp[0 * 4 * kPRow] = prmt(p01, p23, 0x5410);                 // bits 0-7
-                rowp[1 * 4 * kPRow] = prmt(p01, p23, 0x7632);                 // bits 8-15
-                rowp[2 * 4 * kPRow] = prmt(q01, q23, 0x5410) & 0x3F3F3F3Fu;   // bits 16-21
+                rowp[0 * 4 * kPRow] = prmt(p01, p23, 0x5410);                // bits 0-7
+                rowp[1 * 4 * kPRow] = prmt(p01, p23, 0x7632);                // bits 8-15
+                rowp[2 * 4 * kPRow] = prmt(q01, q23, 0x5410) & 0x3F3F3F3Fu;  // bits 16-21
             }
             __syncwarp();
             uint32_t afr[NT][4];
@@ -521,8 +498,8 @@ __global__ void __launch_bounds__(kThreads, NT == 1 ? 3 : 2) decode_tc_kernel(co
                 const uint32_t* r0 = pw + (mt * 12 + g) * kPRow;
                 afr[mt][0] = r0[t];
                 afr[mt][2] = r0[4 + t];
-                afr[mt][1] = g < 4 ? r0[8 * kPRow + t] : 0u;
-                afr[mt][3] = g < 4 ? r0[8 * kPRow + 4 + t] : 0u;
+                afr[mt][1] = lowlane ? r0[8 * kPRow + t] : 0u;
+                afr[mt][3] = lowlane ? r0[8 * kPRow + 4 + t] : 0u;
             }
             __syncwarp();
             // B operand: V codes of this lane's 2*BITS bytes for 8 tokens, byte-transposed.
@@ -539,10 +516,10 @@ __global__ void __launch_bounds__(kThreads, NT == 1 ? 3 : 2) decode_tc_kernel(co
                     } else if (BITS == 2) {
                         raw[ii][0] = *reinterpret_cast<const uint32_t*>(rp);
                     } else if (BITS == 4) {
-                        uint2 vv = *reinterpret_cast<const uint2*>(rp);
+                        const uint2 vv = *reinterpret_cast<const uint2*>(rp);
                         raw[ii][0] = vv.x, raw[ii][NW - 1] = vv.y;
                     } else {
-                        uint4 vv = *reinterpret_cast<const uint4*>(rp);
+                        const uint4 vv = *reinterpret_cast<const uint4*>(rp);
                         raw[ii][0] = vv.x, raw[ii][1 % NW] = vv.y, raw[ii][2 % NW] = vv.z, raw[ii][3 % NW] = vv.w;
                     }
                 }
@@ -571,77 +548,60 @@ __global__ void __launch_bounds__(kThreads, NT == 1 ? 3 : 2) decode_tc_kernel(co
             }
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[slot]);
+        if (lane == 0 && i + kStages < total_stages) issue(i + kStages);
     }
 
     // ---------------- CTA partial numerators / denominators ----------------
-    // Ring is free once every consumer warp is past its last stage: reuse it for the
-    // cross-warp reduction [warp][G][128] + [warp][8].
-    consumers_sync();
-    float* red = reinterpret_cast<float*>(ring);
-    float* redw = red + kConsumerWarps * G * kDim;
+    // All stages consumed and no copy in flight: the ring becomes `pub` [G][128].
+    float* pub = reinterpret_cast<float*>(sm.ring);
     const float levels = (float)((1u << BITS) - 1u);
 #pragma unroll
     for (int mt = 0; mt < NT; ++mt) {
+        float ws = wsum[mt];  // u22 weight sum of head 4mt + ph over this chunk
+#pragma unroll
+        for (int o : {1, 2, 4}) ws += __shfl_xor_sync(0xffffffffu, ws, o);
         const int h = 4 * mt + (g & 3);
+        const float wh_vis = __shfl_sync(0xffffffffu, ws, 8 * (g & 3));
+        // tail weights of head h on the same 2^22 - 1 scale
+        float wt = 0.f;
+        for (int j = 0; j < ntl; ++j)
+            wt += ex2(__fmaf_rn(sm.tail_s[(h < G ? h : 0) * kTailMax + j], kLog2e, sm.gpar[h * 4 + 2])) * kPScale;
+        if (lane < 4 && h < G) sm.pub_den[h] = wh_vis + wt;
 #pragma unroll
         for (int nc = 0; nc < 16; ++nc) {
             // rows g / g+8: planes (0, 2) for g < 4, plane 1 for g >= 4, head g % 4.
             const float lo0 = (float)(uint32_t)vacc[mt][nc][0], lo1 = (float)(uint32_t)vacc[mt][nc][1];
             const float hi0 = (float)(uint32_t)vacc[mt][nc][2], hi1 = (float)(uint32_t)vacc[mt][nc][3];
-            const float part0 = g < 4 ? __fmaf_rn(hi0, 65536.0f, lo0) : lo0 * 256.0f;  // column 2t
-            const float part1 = g < 4 ? __fmaf_rn(hi1, 65536.0f, lo1) : lo1 * 256.0f;  // column 2t+1
-            const float send = g < 4 ? part1 : part0;
-            const float recv = __shfl_xor_sync(0xffffffffu, send, 16);
-            const int col = 2 * t + (g < 4 ? 0 : 1);
-            const float val = (g < 4 ? part0 : part1) + recv;
+            const float part0 = lowlane ? __fmaf_rn(hi0, 65536.0f, lo0) : lo0 * 256.0f;  // column 2t
+            const float part1 = lowlane ? __fmaf_rn(hi1, 65536.0f, lo1) : lo1 * 256.0f;  // column 2t+1
+            const float recv = __shfl_xor_sync(0xffffffffu, lowlane ? part1 : part0, 16);
+            const float val = (lowlane ? part0 : part1) + recv;
             int sh;
-            const int ch = v_channel<BITS>(col, nc, sh);
-            if (h < G) red[(warp * G + h) * kDim + ch] = val * __int_as_float((127 - sh) << 23);
+            const int ch = v_channel<BITS>(2 * t + (lowlane ? 0 : 1), nc, sh);
+            if (h < G) {
+                const float va = __ldg(a.v_alpha + unit * kDim + ch);
+                const float vr = __fsub_rn(__ldg(a.v_beta + unit * kDim + ch), va);
+                const float step = vr > 0.0f ? __fdiv_rn(vr, levels) : 0.0f;
+                float tnum = 0.f;
+                for (int j = 0; j < ntl; ++j) {
+                    const float pt = ex2(__fmaf_rn(sm.tail_s[h * kTailMax + j], kLog2e, sm.gpar[h * 4 + 2])) * kPScale;
+                    tnum = __fmaf_rn(pt, a.v_tail[((size_t)unit * a.tail_cap + tt0 + j) * kDim + ch], tnum);
+                }
+                const float num = val * __int_as_float((127 - sh) << 23);  // / 2^sh, exact
+                pub[h * kDim + ch] = __fmaf_rn(step, num, __fmaf_rn(va, wh_vis, tnum));
+            }
         }
-        float ws = wsum[mt];
-#pragma unroll
-        for (int o : {1, 2, 4}) ws += __shfl_xor_sync(0xffffffffu, ws, o);
-        if (pj == 0 && 4 * mt + ph < G) redw[warp * 8 + 4 * mt + ph] = ws;
-    }
-    consumers_sync();
-    // fp32 tail weights and values of this CTA (on the same 2^22 - 1 scale).
-    for (int idx = threadIdx.x; idx < G * kDim; idx += kConsumerWarps * 32) {
-        const int h = idx / kDim, ch = idx % kDim;
-        float num = 0.f;
-        for (int w2 = 0; w2 < kConsumerWarps; ++w2) num += red[(w2 * G + h) * kDim + ch];
-        const float va = a.v_alpha[unit * kDim + ch];
-        const float vr = __fsub_rn(a.v_beta[unit * kDim + ch], va);
-        const float step = vr > 0.0f ? __fdiv_rn(vr, levels) : 0.0f;
-        float wv = 0.f;
-        for (int w2 = 0; w2 < kConsumerWarps; ++w2) wv += redw[w2 * 8 + h];
-        float tnum = 0.f;
-        for (int j = 0; j < ntl; ++j) {
-            const float pt = ex2(__fmaf_rn(tail_s[h * kTailMax + j], kLog2e, gpar[h * 4 + 2])) * kPScale;
-            tnum = __fmaf_rn(pt, a.v_tail[((size_t)unit * a.tail_cap + tt0 + j) * kDim + ch], tnum);
-        }
-        pub[h * kDim + ch] = __fmaf_rn(step, num, __fmaf_rn(va, wv, tnum));
-    }
-    if (threadIdx.x < 8) {
-        const int h = threadIdx.x;
-        float wv = 0.f, wt = 0.f;
-        if (h < G) {
-            for (int w2 = 0; w2 < kConsumerWarps; ++w2) wv += redw[w2 * 8 + h];
-            for (int j = 0; j < ntl; ++j)
-                wt += ex2(__fmaf_rn(tail_s[h * kTailMax + j], kLog2e, gpar[h * 4 + 2])) * kPScale;
-        }
-        pub_den[h] = wv + wt;
     }
     cluster_arrive();  // #2: partial numerators published
     cluster_wait();
     // Each CTA finalizes a slice of the G x 128 outputs (fixed-order sum over ranks).
     const int per = (G * kDim + S - 1) / S;
-    for (int idx = rank * per + threadIdx.x; idx < min(G * kDim, (rank + 1) * per); idx += kConsumerWarps * 32) {
+    for (int idx = rank * per + lane; idx < min(G * kDim, (rank + 1) * per); idx += 32) {
         const int h = idx / kDim;
         float num = 0.f, den = 0.f;
         for (int r = 0; r < S; ++r) {
             num += cluster.map_shared_rank(pub, r)[idx];
-            den += cluster.map_shared_rank(pub_den, r)[h];
+            den += cluster.map_shared_rank(sm.pub_den, r)[h];
         }
         a.out[((size_t)unit * G + h) * kDim + (idx % kDim)] = num / den;
     }
@@ -649,29 +609,12 @@ __global__ void __launch_bounds__(kThreads, NT == 1 ? 3 : 2) decode_tc_kernel(co
     cluster_wait();
 }
 
-size_t tc_smem_bytes(int bits, int G, int T) {
-    const size_t stage = (size_t)(bits <= 2 ? 8192 : 128 * 16 * bits);
-    size_t ring = kStages * stage;
-    const size_t red = (size_t)kConsumerWarps * (G * kDim + 8) * 4;
-    if (ring < red) ring = red;
-    return ring + (size_t)G * (T + 4) * 4 + (size_t)G * kTailMax * 4 + (size_t)G * kDim * 4 + sizeof(Partial) +
-           32 * 4 + (size_t)G * kDim * 4 + 8 * 4 + kConsumerWarps * 8 * 3 * 4 + (size_t)kConsumerWarps * 2 * 12 * kPRow * 4 + 16 + 2 * kStages * 8 + 16;
-}
-
-// Scratch for the prep kernel's outputs (grown on demand, per device).
-struct PrepScratch {
-    uint32_t* frag = nullptr;
-    float2* qconst = nullptr;
-    size_t units = 0, G = 0;
-};
-PrepScratch g_scratch[16];
-
 void plan(const DecodeArgs& a, int& S, int& T) {
     const int n = (int)a.n_vis;
     const int units = (int)a.units;
-    int s_min = (n + kMaxT - 1) / kMaxT;                 // smem cap on tokens per CTA
-    int s_pref = (n + 511) / 512;                        // ~512 tokens per CTA
-    const int want_ctas = 2 * 148;
+    const int s_min = (n + kMaxT - 1) / kMaxT;  // smem cap on tokens per CTA
+    int s_pref = (n + 511) / 512;               // ~512 tokens per (one-warp) CTA
+    const int want_ctas = 4 * 148;
     if (units * s_pref < want_ctas) s_pref = (want_ctas + units - 1) / units;
     S = std::max(1, std::min(kMaxCluster, std::max(s_min, s_pref)));
     S = std::min(S, std::max(1, (n + 31) / 32));  // >= 32 tokens per CTA
@@ -680,15 +623,15 @@ void plan(const DecodeArgs& a, int& S, int& T) {
 }
 
 template <int BITS, int NT>
-cudaError_t launch_bits(const DecodeArgs& a, cudaStream_t s, uint32_t* frag, float2* qconst) {
+cudaError_t launch_bits(const DecodeArgs& a, cudaStream_t s) {
     int S, T;
     plan(a, S, T);
-    prep_kernel<BITS><<<(unsigned)a.units, kDim, 0, s>>>(a, NT, frag, qconst);
+    prep_kernel<BITS><<<(unsigned)a.units, kDim, 0, s>>>(a, NT, a.tc_frag, a.tc_qconst);
     note_launch();
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    TcParams p{a, frag, qconst, S, T};
-    const size_t smem = tc_smem_bytes(BITS, (int)a.group, T);
+    TcParams p{a, a.tc_frag, a.tc_qconst, S, T};
+    const size_t smem = tc_smem_bytes((int)a.group, T, NT);
     auto kern = decode_tc_kernel<BITS, NT>;
     static bool attr_done = false;  // per instantiation
     if (!attr_done) {
@@ -700,7 +643,7 @@ cudaError_t launch_bits(const DecodeArgs& a, cudaStream_t s, uint32_t* frag, flo
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(a.units * S));
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(32);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attrs[2];
@@ -719,6 +662,8 @@ cudaError_t launch_bits(const DecodeArgs& a, cudaStream_t s, uint32_t* frag, flo
 
 }  // namespace
 
+size_t decode_tc_scratch_bytes(size_t units) { return units * (2 * 512 * sizeof(uint32_t) + 8 * sizeof(float2)); }
+
 bool decode_tc_supported(const DecodeArgs& a) {
     if (a.dim != (size_t)kDim || a.word_bits != 8 || a.n_vis == 0) return false;
     if (a.bits != 1 && a.bits != 2 && a.bits != 4 && a.bits != 8) return false;
@@ -729,35 +674,21 @@ bool decode_tc_supported(const DecodeArgs& a) {
     if (T > kMaxT) return false;
     // fp32 tail split over the cluster: at most kTailMax rows per CTA.
     if (a.tail_cap > (size_t)kTailMax * S) return false;
-    return tc_smem_bytes(a.bits, (int)a.group, T) <= 200 * 1024;
+    return tc_smem_bytes((int)a.group, T, a.group > 4 ? 2 : 1) <= 200 * 1024;
 }
 
 cudaError_t launch_decode_tc(const DecodeArgs& a, cudaStream_t s) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    PrepScratch& sc = g_scratch[dev & 15];
+    if (!a.tc_frag || !a.tc_qconst) return cudaErrorInvalidValue;
     const int NT = a.group > 4 ? 2 : 1;
-    if (sc.units < a.units || sc.G < a.group) {
-        cudaFree(sc.frag);
-        cudaFree(sc.qconst);
-        sc.frag = nullptr;
-        sc.qconst = nullptr;
-        cudaError_t e = cudaMalloc(&sc.frag, a.units * 2 * 512 * sizeof(uint32_t));
-        if (e != cudaSuccess) return e;
-        e = cudaMalloc(&sc.qconst, a.units * 8 * sizeof(float2));
-        if (e != cudaSuccess) return e;
-        sc.units = a.units;
-        sc.G = 8;
-    }
     switch (a.bits * 10 + NT) {
-        case 11: return launch_bits<1, 1>(a, s, sc.frag, sc.qconst);
-        case 12: return launch_bits<1, 2>(a, s, sc.frag, sc.qconst);
-        case 21: return launch_bits<2, 1>(a, s, sc.frag, sc.qconst);
-        case 22: return launch_bits<2, 2>(a, s, sc.frag, sc.qconst);
-        case 41: return launch_bits<4, 1>(a, s, sc.frag, sc.qconst);
-        case 42: return launch_bits<4, 2>(a, s, sc.frag, sc.qconst);
-        case 81: return launch_bits<8, 1>(a, s, sc.frag, sc.qconst);
-        case 82: return launch_bits<8, 2>(a, s, sc.frag, sc.qconst);
+        case 11: return launch_bits<1, 1>(a, s);
+        case 12: return launch_bits<1, 2>(a, s);
+        case 21: return launch_bits<2, 1>(a, s);
+        case 22: return launch_bits<2, 2>(a, s);
+        case 41: return launch_bits<4, 1>(a, s);
+        case 42: return launch_bits<4, 2>(a, s);
+        case 81: return launch_bits<8, 1>(a, s);
+        case 82: return launch_bits<8, 2>(a, s);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -66,12 +66,15 @@ struct DecodeArgs {
     float* weights;       // nullable: [units][group][n_vis + tail_stride] probability rows
     int* violations;      // nullable: [units][group] g slope-violation flags
     float* scratch;       // generic path: [units][group][n_vis + tail_cap] score rows
+    uint32_t* tc_frag;    // tc path: [units][2][512] q-plane MMA fragments (prep kernel)
+    float2* tc_qconst;    // tc path: [units][8] per-head score scale / offset
     size_t units, kv_heads, group, dim, n_vis, tail_cap, weights_stride;
     int bits, word_bits;
     float tau1, tau2;
 };
 cudaError_t launch_decode_generic(const DecodeArgs& a, cudaStream_t s);
 bool decode_tc_supported(const DecodeArgs& a);
+size_t decode_tc_scratch_bytes(size_t units);
 cudaError_t launch_decode_tc(const DecodeArgs& a, cudaStream_t s);
 
 // Post-scaled q.K (kernels.hpp:302-363) and w.V (316-396) over `heads` segments.
