@@ -32,7 +32,7 @@ namespace kvqb {
 namespace {
 
 constexpr int kDim = 128;
-constexpr int kStages = 4;
+constexpr int kStages = 2;
 constexpr int kStageBytes = 4096;
 constexpr int kTailMax = 64;   // fp32 tail tokens per CTA
 constexpr int kMaxT = 2048;    // visual tokens per CTA
@@ -214,6 +214,7 @@ __global__ void __launch_bounds__(kDim) prep_kernel(DecodeArgs a, int NT, uint32
 // ---- decode ------------------------------------------------------------------------------
 struct Partial {  // per-CTA softmax statistics, exchanged through DSMEM
     float lo[8], hi[8], tmax[8];
+    int has_tail;    // written after cluster barrier #1, read after #2
 };
 
 struct Smem {  // carve-up of the dynamic shared memory of one decode CTA
@@ -223,7 +224,7 @@ struct Smem {  // carve-up of the dynamic shared memory of one decode CTA
     uint32_t* pw;      // [NT][12][kPRow] p digit planes of the current 32-token block
     Partial* part;     // this CTA's (min, max, tail max) per head
     float* gpar;       // [8][4] softmax parameters per head
-    float* pub_den;    // [8] this CTA's softmax denominators
+    float* pub_den;    // [16] this CTA's visual / tail softmax denominators per head
     uint64_t* full;    // [kStages] TMA completion barriers
 };
 
@@ -235,13 +236,14 @@ __host__ __device__ inline size_t tc_smem_bytes(int G, int T, int NT, Smem* out 
         off += (bytes + 15) & ~size_t(15);
         return base + o;
     };
-    uint8_t* ring = take(kStages * kStageBytes);
+    const size_t pub_bytes = (size_t)NT * 16 * 32 * 16 + (size_t)G * kDim * 4;
+    uint8_t* ring = take(kStages * kStageBytes > pub_bytes ? kStages * kStageBytes : pub_bytes);
     uint8_t* scores = take((size_t)G * (T + 4) * 4);
     uint8_t* tail_s = take((size_t)G * kTailMax * 4);
     uint8_t* pw = take((size_t)NT * 12 * kPRow * 4);
     uint8_t* part = take(sizeof(Partial));
     uint8_t* gpar = take(32 * 4);
-    uint8_t* den = take(8 * 4);
+    uint8_t* den = take(16 * 4);
     uint8_t* full = take(kStages * 8);
     if (out) {
         out->ring = ring;
@@ -331,44 +333,53 @@ __global__ void __launch_bounds__(32, 8) decode_tc_kernel(const TcParams p) {
         const int ns = min(Gm::kStageTokens, nv - st * Gm::kStageTokens);
         const int ntiles = (ns + 7) >> 3;
         const int tbase = st * Gm::kStageTokens + 2 * t + (lowlane ? 0 : 1);
-#pragma unroll 2
-        for (int tile = 0; tile < ntiles; ++tile) {
-            const uint8_t* rowp = buf + (tile * 8 + g) * Gm::kRowBytes + t * 4 * BITS;
-            uint32_t w[BITS];
-            if (BITS == 1) {
-                w[0] = *reinterpret_cast<const uint32_t*>(rowp);
-            } else if (BITS == 2) {
-                const uint2 v = *reinterpret_cast<const uint2*>(rowp);
-                w[0] = v.x, w[1 % BITS] = v.y;
-            } else {
+        // Two tiles per iteration: two independent IMMA accumulator chains in flight.
+        for (int tile = 0; tile < ntiles; tile += 2) {
+            uint32_t breg[2][8];
 #pragma unroll
-                for (int u = 0; u < BITS; u += 4) {
-                    const uint4 v = *reinterpret_cast<const uint4*>(rowp + 4 * u);
-                    w[u] = v.x, w[(u + 1) % BITS] = v.y, w[(u + 2) % BITS] = v.z, w[(u + 3) % BITS] = v.w;
+            for (int u2 = 0; u2 < 2; ++u2) {
+                const uint8_t* rowp = buf + ((tile + u2) * 8 + g) * Gm::kRowBytes + t * 4 * BITS;
+                uint32_t w[BITS];
+                if (BITS == 1) {
+                    w[0] = *reinterpret_cast<const uint32_t*>(rowp);
+                } else if (BITS == 2) {
+                    const uint2 v = *reinterpret_cast<const uint2*>(rowp);
+                    w[0] = v.x, w[1 % BITS] = v.y;
+                } else {
+#pragma unroll
+                    for (int u = 0; u < BITS; u += 4) {
+                        const uint4 v = *reinterpret_cast<const uint4*>(rowp + 4 * u);
+                        w[u] = v.x, w[(u + 1) % BITS] = v.y, w[(u + 2) % BITS] = v.z, w[(u + 3) % BITS] = v.w;
+                    }
                 }
-            }
-            uint32_t breg[8];
 #pragma unroll
-            for (int rho = 0; rho < 8; ++rho)
-                breg[rho] = w[rho / Gm::kCpb] & (Gm::kMask << ((rho % Gm::kCpb) * BITS));
-            const int tok = tbase + tile * 8;
+                for (int rho = 0; rho < 8; ++rho)
+                    breg[u2][rho] = w[rho / Gm::kCpb] & (Gm::kMask << ((rho % Gm::kCpb) * BITS));
+            }
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt) {
-                int acc[4] = {0, 0, 0, 0};
+                int acc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
 #pragma unroll
-                for (int kb = 0; kb < 4; ++kb) imma_s8u8(acc, afrag[nt][kb], breg[2 * kb], breg[2 * kb + 1]);
-                // rows g / g+8 hold digit planes (0,2) [g<4] or (1,3) [g>=4] of head g%4;
-                // the int32 sums wrap mod 2^32 but the total is exact (|score| < 2^31).
-                const int p0 = acc[0] * wl + acc[2] * wh;  // token 2t
-                const int p1 = acc[1] * wl + acc[3] * wh;  // token 2t+1
-                const int recv = __shfl_xor_sync(0xffffffffu, lowlane ? p1 : p0, 16);
-                const int total = (lowlane ? p0 : p1) + recv;
+                for (int kb = 0; kb < 4; ++kb) {
+                    imma_s8u8(acc[0], afrag[nt][kb], breg[0][2 * kb], breg[0][2 * kb + 1]);
+                    imma_s8u8(acc[1], afrag[nt][kb], breg[1][2 * kb], breg[1][2 * kb + 1]);
+                }
                 const int h = 4 * nt + (g & 3);
-                if (h < G && tok < nv) {
-                    const float s = __fmaf_rn((float)total, cA[nt], cB[nt]);
-                    scores[h * TS + tok] = s;
-                    lo[nt] = fminf(lo[nt], s);
-                    hi[nt] = fmaxf(hi[nt], s);
+#pragma unroll
+                for (int u2 = 0; u2 < 2; ++u2) {
+                    // rows g / g+8 hold digit planes (0,2) [g<4] or (1,3) [g>=4] of head g%4;
+                    // the int32 sums wrap mod 2^32 but the total is exact (|score| < 2^31).
+                    const int p0 = acc[u2][0] * wl + acc[u2][2] * wh;  // token 2t
+                    const int p1 = acc[u2][1] * wl + acc[u2][3] * wh;  // token 2t+1
+                    const int recv = __shfl_xor_sync(0xffffffffu, lowlane ? p1 : p0, 16);
+                    const int total = (lowlane ? p0 : p1) + recv;
+                    const int tok = tbase + (tile + u2) * 8;
+                    if (h < G && tok < nv) {
+                        const float sc = __fmaf_rn((float)total, cA[nt], cB[nt]);
+                        scores[h * TS + tok] = sc;
+                        lo[nt] = fminf(lo[nt], sc);
+                        hi[nt] = fmaxf(hi[nt], sc);
+                    }
                 }
             }
         }
@@ -551,59 +562,84 @@ __global__ void __launch_bounds__(32, 8) decode_tc_kernel(const TcParams p) {
         if (lane == 0 && i + kStages < total_stages) issue(i + kStages);
     }
 
-    // ---------------- CTA partial numerators / denominators ----------------
-    // All stages consumed and no copy in flight: the ring becomes `pub` [G][128].
-    float* pub = reinterpret_cast<float*>(sm.ring);
-    const float levels = (float)((1u << BITS) - 1u);
+    // ---------------- CTA partials -> cluster reduction ----------------
+    // All stages consumed and no copy in flight: the ring becomes the publication area.
+    // Raw u32 digit-plane accumulators are published as is; plane combination, the 2^-sh
+    // slot scale, the V step / zero-point and the division happen once per output in the
+    // cluster reduction below.
+    uint4* pubv = reinterpret_cast<uint4*>(sm.ring);  // [NT][16 nc][32 lanes]
+#pragma unroll
+    for (int mt = 0; mt < NT; ++mt)
+#pragma unroll
+        for (int nc = 0; nc < 16; ++nc)
+            pubv[(mt * 16 + nc) * 32 + lane] =
+                make_uint4((uint32_t)vacc[mt][nc][0], (uint32_t)vacc[mt][nc][1], (uint32_t)vacc[mt][nc][2],
+                           (uint32_t)vacc[mt][nc][3]);
+    float* pubt = reinterpret_cast<float*>(pubv + NT * 16 * 32);  // [G][128] tail numerators (if ntl)
 #pragma unroll
     for (int mt = 0; mt < NT; ++mt) {
         float ws = wsum[mt];  // u22 weight sum of head 4mt + ph over this chunk
 #pragma unroll
         for (int o : {1, 2, 4}) ws += __shfl_xor_sync(0xffffffffu, ws, o);
-        const int h = 4 * mt + (g & 3);
-        const float wh_vis = __shfl_sync(0xffffffffu, ws, 8 * (g & 3));
-        // tail weights of head h on the same 2^22 - 1 scale
-        float wt = 0.f;
-        for (int j = 0; j < ntl; ++j)
-            wt += ex2(__fmaf_rn(sm.tail_s[(h < G ? h : 0) * kTailMax + j], kLog2e, sm.gpar[h * 4 + 2])) * kPScale;
-        if (lane < 4 && h < G) sm.pub_den[h] = wh_vis + wt;
-#pragma unroll
-        for (int nc = 0; nc < 16; ++nc) {
-            // rows g / g+8: planes (0, 2) for g < 4, plane 1 for g >= 4, head g % 4.
-            const float lo0 = (float)(uint32_t)vacc[mt][nc][0], lo1 = (float)(uint32_t)vacc[mt][nc][1];
-            const float hi0 = (float)(uint32_t)vacc[mt][nc][2], hi1 = (float)(uint32_t)vacc[mt][nc][3];
-            const float part0 = lowlane ? __fmaf_rn(hi0, 65536.0f, lo0) : lo0 * 256.0f;  // column 2t
-            const float part1 = lowlane ? __fmaf_rn(hi1, 65536.0f, lo1) : lo1 * 256.0f;  // column 2t+1
-            const float recv = __shfl_xor_sync(0xffffffffu, lowlane ? part1 : part0, 16);
-            const float val = (lowlane ? part0 : part1) + recv;
-            int sh;
-            const int ch = v_channel<BITS>(2 * t + (lowlane ? 0 : 1), nc, sh);
-            if (h < G) {
-                const float va = __ldg(a.v_alpha + unit * kDim + ch);
-                const float vr = __fsub_rn(__ldg(a.v_beta + unit * kDim + ch), va);
-                const float step = vr > 0.0f ? __fdiv_rn(vr, levels) : 0.0f;
-                float tnum = 0.f;
-                for (int j = 0; j < ntl; ++j) {
-                    const float pt = ex2(__fmaf_rn(sm.tail_s[h * kTailMax + j], kLog2e, sm.gpar[h * 4 + 2])) * kPScale;
-                    tnum = __fmaf_rn(pt, a.v_tail[((size_t)unit * a.tail_cap + tt0 + j) * kDim + ch], tnum);
-                }
-                const float num = val * __int_as_float((127 - sh) << 23);  // / 2^sh, exact
-                pub[h * kDim + ch] = __fmaf_rn(step, num, __fmaf_rn(va, wh_vis, tnum));
+        if (pj == 0 && 4 * mt + ph < G) sm.pub_den[4 * mt + ph] = ws;
+    }
+    if (ntl > 0) {
+        // fp32 tail rows of this CTA, on the same 2^22 - 1 weight scale.
+        for (int h = 0; h < G; ++h) {
+            float wt = 0.f;
+            float4 tn = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int j = 0; j < ntl; ++j) {
+                const float pt = ex2(__fmaf_rn(sm.tail_s[h * kTailMax + j], kLog2e, sm.gpar[h * 4 + 2])) * kPScale;
+                const float4 vv = *reinterpret_cast<const float4*>(
+                    a.v_tail + ((size_t)unit * a.tail_cap + tt0 + j) * kDim + 4 * lane);
+                tn.x = __fmaf_rn(pt, vv.x, tn.x);
+                tn.y = __fmaf_rn(pt, vv.y, tn.y);
+                tn.z = __fmaf_rn(pt, vv.z, tn.z);
+                tn.w = __fmaf_rn(pt, vv.w, tn.w);
+                wt += pt;
             }
+            reinterpret_cast<float4*>(pubt + h * kDim)[lane] = tn;
+            if (lane == 0) sm.pub_den[8 + h] = wt;
         }
     }
-    cluster_arrive();  // #2: partial numerators published
+    if (lane == 0) sm.part->has_tail = ntl > 0;  // tail flag for the reducers
+    cluster_arrive();  // #2: partials published
     cluster_wait();
-    // Each CTA finalizes a slice of the G x 128 outputs (fixed-order sum over ranks).
+    // Each CTA finalizes a slice of the G x 128 outputs: exact u32 plane sums over the
+    // cluster, then out = (s_c V_c / 2^sh + alpha_c W_vis + T_c) / (W_vis + W_tail).
+    constexpr float kInvLevels = 1.0f / (float)((1u << BITS) - 1u);
     const int per = (G * kDim + S - 1) / S;
     for (int idx = rank * per + lane; idx < min(G * kDim, (rank + 1) * per); idx += 32) {
-        const int h = idx / kDim;
-        float num = 0.f, den = 0.f;
+        const int h = idx / kDim, ch = idx % kDim;
+        // locate (plane rows, column) of (h, ch) in the MMA accumulator layout
+        constexpr int cpb = Gm::kCpb;
+        const int byte = ch / cpb, s = cpb - 1 - ch % cpb;
+        const int gcol = byte / (2 * BITS), q = byte % (2 * BITS);
+        const int nc = q * cpb + s, sh = s * BITS;
+        const int mt = h >> 2, hl = h & 3;
+        const int lane0 = 4 * hl + (gcol >> 1);        // rows hl (plane 0) / hl+8 (plane 2)
+        const int lane1 = 4 * (hl + 4) + (gcol >> 1);  // row hl+4 (plane 1)
+        const int odd = gcol & 1;
+        uint32_t p0 = 0, p1 = 0, p2 = 0;
+        float wv = 0.f, wt = 0.f, tn = 0.f;
         for (int r = 0; r < S; ++r) {
-            num += cluster.map_shared_rank(pub, r)[idx];
-            den += cluster.map_shared_rank(sm.pub_den, r)[h];
+            const uint32_t* pv = reinterpret_cast<const uint32_t*>(cluster.map_shared_rank(pubv, r) + (mt * 16 + nc) * 32);
+            p0 += pv[lane0 * 4 + odd];
+            p2 += pv[lane0 * 4 + 2 + odd];
+            p1 += pv[lane1 * 4 + odd];
+            const float* pd = cluster.map_shared_rank(sm.pub_den, r);
+            wv += pd[h];
+            if (cluster.map_shared_rank(sm.part, r)->has_tail) {
+                wt += pd[8 + h];
+                tn += reinterpret_cast<const float*>(cluster.map_shared_rank(pubv, r) + NT * 16 * 32)[h * kDim + ch];
+            }
         }
-        a.out[((size_t)unit * G + h) * kDim + (idx % kDim)] = num / den;
+        const float V = __fmaf_rn((float)p2, 65536.0f, __fmaf_rn((float)p1, 256.0f, (float)p0)) *
+                        __int_as_float((127 - sh) << 23);
+        const float va = __ldg(a.v_alpha + unit * kDim + ch);
+        const float step = __fsub_rn(__ldg(a.v_beta + unit * kDim + ch), va) * kInvLevels;
+        a.out[((size_t)unit * G + h) * kDim + ch] =
+            __fmaf_rn(step > 0.0f ? step : 0.0f, V, __fmaf_rn(va, wv, tn)) / (wv + wt);
     }
     cluster_arrive();  // #3: keep shared memory alive until every peer has read it
     cluster_wait();
