@@ -212,23 +212,19 @@ __global__ void __launch_bounds__(kDim) prep_kernel(DecodeArgs a, int NT, uint32
 }
 
 // ---- decode ------------------------------------------------------------------------------
-struct Partial {  // per-CTA softmax statistics, exchanged through DSMEM
-    float lo[8], hi[8], tmax[8];
-    int has_tail;    // written after cluster barrier #1, read after #2
-};
-
 struct Smem {  // carve-up of the dynamic shared memory of one decode CTA
-    uint8_t* ring;     // kStages x kStageBytes: TMA landing zone; reused for `pub` after phase B
-    float* scores;     // [G][T + 4] calibrated-softmax inputs of the visual chunk
-    float* tail_s;     // [G][kTailMax] fp32 tail scores of this CTA's tail rows
-    uint32_t* pw;      // [NT][12][kPRow] p digit planes of the current 32-token block
-    Partial* part;     // this CTA's (min, max, tail max) per head
-    float* gpar;       // [8][4] softmax parameters per head
-    float* pub_den;    // [16] this CTA's visual / tail softmax denominators per head
-    uint64_t* full;    // [kStages] TMA completion barriers
+    uint8_t* ring;       // kStages x kStageBytes: TMA landing zone
+    float* scores;       // [G][T + 4] calibrated-softmax inputs of the visual chunk
+    float* tail_s;       // [G][kTailMax] fp32 tail scores (rank 0 only)
+    uint32_t* pw;        // [NT][12][kPRow] p digit planes of the current 32-token block
+    float* allpart;      // [S][24] (min[8], max[8], tail max[8]) pushed by every CTA
+    float* gpar;         // [8][4] softmax parameters per head
+    uint32_t* vsum;      // [3][G][128] rank 0: cluster-wide u32 digit-plane sums
+    unsigned long long* wsum;  // [8] rank 0: cluster-wide u22 weight sums per head
+    uint64_t* full;      // [kStages] TMA completion barriers
 };
 
-__host__ __device__ inline size_t tc_smem_bytes(int G, int T, int NT, Smem* out = nullptr,
+__host__ __device__ inline size_t tc_smem_bytes(int G, int T, int NT, int S, Smem* out = nullptr,
                                                 uint8_t* base = nullptr) {
     size_t off = 0;
     auto take = [&](size_t bytes) {
@@ -236,55 +232,70 @@ __host__ __device__ inline size_t tc_smem_bytes(int G, int T, int NT, Smem* out 
         off += (bytes + 15) & ~size_t(15);
         return base + o;
     };
-    const size_t pub_bytes = (size_t)NT * 16 * 32 * 16 + (size_t)G * kDim * 4;
-    uint8_t* ring = take(kStages * kStageBytes > pub_bytes ? kStages * kStageBytes : pub_bytes);
+    uint8_t* ring = take(kStages * kStageBytes);
     uint8_t* scores = take((size_t)G * (T + 4) * 4);
     uint8_t* tail_s = take((size_t)G * kTailMax * 4);
     uint8_t* pw = take((size_t)NT * 12 * kPRow * 4);
-    uint8_t* part = take(sizeof(Partial));
+    uint8_t* allpart = take((size_t)S * 24 * 4);
     uint8_t* gpar = take(32 * 4);
-    uint8_t* den = take(16 * 4);
+    uint8_t* vsum = take((size_t)3 * G * kDim * 4);
+    uint8_t* wsum = take(8 * 8);
     uint8_t* full = take(kStages * 8);
     if (out) {
         out->ring = ring;
         out->scores = reinterpret_cast<float*>(scores);
         out->tail_s = reinterpret_cast<float*>(tail_s);
         out->pw = reinterpret_cast<uint32_t*>(pw);
-        out->part = reinterpret_cast<Partial*>(part);
+        out->allpart = reinterpret_cast<float*>(allpart);
         out->gpar = reinterpret_cast<float*>(gpar);
-        out->pub_den = reinterpret_cast<float*>(den);
+        out->vsum = reinterpret_cast<uint32_t*>(vsum);
+        out->wsum = reinterpret_cast<unsigned long long*>(wsum);
         out->full = reinterpret_cast<uint64_t*>(full);
     }
     return off;
 }
 
-// One warp per CTA: the warp streams its own token chunk through a TMA ring (lane 0
-// re-arms a slot as soon as the warp has consumed it), so no producer warp, no empty
-// barriers and no cross-warp reductions; one CTA = one contiguous chunk of T tokens.
+__device__ __forceinline__ void st_cluster_f32(float* local_ptr, int rank, float v) {
+    uint32_t addr;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(addr) : "r"(smem_u32(local_ptr)), "r"(rank));
+    asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+__device__ __forceinline__ void red_cluster_u32(uint32_t* local_ptr, int rank, uint32_t v) {
+    uint32_t addr;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(addr) : "r"(smem_u32(local_ptr)), "r"(rank));
+    asm volatile("red.shared::cluster.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_cluster_u64(unsigned long long* local_ptr, int rank, unsigned long long v) {
+    uint32_t addr;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(addr) : "r"(smem_u32(local_ptr)), "r"(rank));
+    asm volatile("red.shared::cluster.add.u64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
+}
+
+// One warp per CTA, one contiguous chunk of T visual tokens per CTA, a cluster of S
+// CTAs per unit. The warp streams its chunk through a 2-slot TMA ring (lane 0 re-arms a
+// slot once the warp has consumed it). Cross-CTA traffic is push-only: softmax stats
+// are stored into every peer before barrier #1, integer accumulators are reduced into
+// rank 0 (red.shared::cluster) before barrier #2; no CTA ever waits on a remote load.
 template <int BITS, int NT>
 __global__ void __launch_bounds__(32, 8) decode_tc_kernel(const TcParams p) {
     using Gm = Geo<BITS>;
     const DecodeArgs& a = p.a;
     const int G = (int)a.group;
     const int S = p.S, T = p.T, TS = T + 4;
-    cg::cluster_group cluster = cg::this_cluster();
-    const int rank = (int)cluster.block_rank();
+    const int rank = (int)cg::this_cluster().block_rank();
     const int unit = blockIdx.x / S;
     const int lane = threadIdx.x;
     const int g = lane >> 2, t = lane & 3;
 
     extern __shared__ __align__(128) uint8_t smem_raw[];
     Smem sm;
-    tc_smem_bytes(G, T, NT, &sm, smem_raw);
+    tc_smem_bytes(G, T, NT, S, &sm, smem_raw);
     float* scores = sm.scores;
 
     const int n = (int)a.n_vis;
     const int tok0 = rank * T;
     const int nv = max(0, min(T, n - tok0));
-    const int n_tail = a.tail_len[unit / a.kv_heads];
-    const int tail_per = (n_tail + S - 1) / S;
-    const int tt0 = rank * tail_per;
-    const int ntl = max(0, min(tail_per, n_tail - tt0));
+    const int ntl = rank == 0 ? a.tail_len[unit / a.kv_heads] : 0;  // fp32 tail: rank 0
     const uint8_t* kcodes = a.k_codes + ((size_t)unit * n + tok0) * Gm::kRowBytes;
     const uint8_t* vcodes = a.v_codes + ((size_t)unit * n + tok0) * Gm::kRowBytes;
     const int nstage = (nv + Gm::kStageTokens - 1) / Gm::kStageTokens;
@@ -302,6 +313,13 @@ __global__ void __launch_bounds__(32, 8) decode_tc_kernel(const TcParams p) {
         for (int i = 0; i < kStages; ++i) mbar_init(&sm.full[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         for (int i = 0; i < min(kStages, total_stages); ++i) issue(i);
+    }
+    // #0: peers may push into this CTA's shared memory only once every CTA of the
+    // cluster is running; arrive now, wait just before the first push.
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+    if (rank == 0) {  // cluster-wide accumulators, zeroed before barrier #1 lets peers in
+        for (int i = lane; i < 3 * G * kDim; i += 32) sm.vsum[i] = 0u;
+        if (lane < 8) sm.wsum[lane] = 0ull;
     }
     __syncwarp();
 
@@ -387,12 +405,11 @@ __global__ void __launch_bounds__(32, 8) decode_tc_kernel(const TcParams p) {
         if (lane == 0 && st + kStages < total_stages) issue(st + kStages);
     }
 
-    // fp32 tail rows of this CTA: lanes split the 128 channels.
+    // fp32 tail rows (rank 0): lanes split the 128 channels.
     const float isd = __fdiv_rn(1.0f, sqrtf((float)kDim));
     float tmax = -INFINITY;  // for head (lane & 7)
     for (int j = 0; j < ntl; ++j) {
-        const float4 kv = *reinterpret_cast<const float4*>(
-            a.k_tail + ((size_t)unit * a.tail_cap + tt0 + j) * kDim + 4 * lane);
+        const float4 kv = *reinterpret_cast<const float4*>(a.k_tail + ((size_t)unit * a.tail_cap + j) * kDim + 4 * lane);
         for (int h = 0; h < G; ++h) {
             const float4 qv = *reinterpret_cast<const float4*>(a.q + ((size_t)unit * G + h) * kDim + 4 * lane);
             float d = kv.x * qv.x + kv.y * qv.y + kv.z * qv.z + kv.w * qv.w;
@@ -403,7 +420,8 @@ __global__ void __launch_bounds__(32, 8) decode_tc_kernel(const TcParams p) {
             if ((lane & 7) == h) tmax = fmaxf(tmax, d);
         }
     }
-    // CTA partial (min, max) per head: lanes of one head differ in lane bits 0, 1, 4.
+    // CTA partial (min, max, tail max) per head -> pushed into every peer.
+    float mine = -INFINITY;  // lane k < 24 owns value k of the partial record
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
 #pragma unroll
@@ -411,14 +429,19 @@ __global__ void __launch_bounds__(32, 8) decode_tc_kernel(const TcParams p) {
             lo[nt] = fminf(lo[nt], __shfl_xor_sync(0xffffffffu, lo[nt], o));
             hi[nt] = fmaxf(hi[nt], __shfl_xor_sync(0xffffffffu, hi[nt], o));
         }
-        if ((lane & 3) == 0 && lane < 16) {
-            sm.part->lo[4 * nt + (lane >> 2)] = lo[nt];
-            sm.part->hi[4 * nt + (lane >> 2)] = hi[nt];
-        }
+        // lane (g, 0), g < 4 holds head 4nt + g
+        const float l8 = __shfl_sync(0xffffffffu, lo[nt], 4 * (lane & 3));
+        const float h8 = __shfl_sync(0xffffffffu, hi[nt], 4 * ((lane - 8) & 3));
+        if (lane >> 2 == nt) mine = l8;                 // lanes 4nt .. 4nt+3: min of head lane&3 (+4nt)
+        if ((lane - 8) >> 2 == nt && lane >= 8 && lane < 16) mine = h8;
     }
-    if (NT == 1 && lane >= 4 && lane < 8) sm.part->lo[lane] = INFINITY, sm.part->hi[lane] = -INFINITY;
-    if (lane < 8) sm.part->tmax[lane] = tmax;
-    cluster_arrive();  // #1: partials published
+    if (lane >= 4 * NT && lane < 8) mine = INFINITY;   // min of absent heads
+    if (lane >= 8 + 4 * NT && lane < 16) mine = -INFINITY;
+    if (lane >= 16 && lane < 24) mine = __shfl_sync(0xffffffffu, tmax, lane - 16);
+    cluster_wait();  // #0
+    if (lane < 24)
+        for (int r = 0; r < S; ++r) st_cluster_f32(sm.allpart + rank * 24 + lane, r, mine);
+    cluster_arrive();  // #1: partials pushed everywhere, rank 0 accumulators zeroed
     cluster_wait();
 
     // Global softmax parameters per head (identical in every CTA of the cluster).
@@ -426,10 +449,9 @@ __global__ void __launch_bounds__(32, 8) decode_tc_kernel(const TcParams p) {
         const int h = lane;
         float gamma = INFINITY, delta = -INFINITY, tm = -INFINITY;
         for (int r = 0; r < S; ++r) {
-            const Partial* pr = cluster.map_shared_rank(sm.part, r);
-            gamma = fminf(gamma, pr->lo[h]);
-            delta = fmaxf(delta, pr->hi[h]);
-            tm = fmaxf(tm, pr->tmax[h]);
+            gamma = fminf(gamma, sm.allpart[r * 24 + h]);
+            delta = fmaxf(delta, sm.allpart[r * 24 + 8 + h]);
+            tm = fmaxf(tm, sm.allpart[r * 24 + 16 + h]);
         }
         // g(x) = A x + B (calibrate.hpp:62-67): g(gamma) = gamma - tau1, g(delta) =
         // delta - tau2; the calibrated row max is at an endpoint (or in the tail).
@@ -462,13 +484,13 @@ __global__ void __launch_bounds__(32, 8) decode_tc_kernel(const TcParams p) {
         for (int nc = 0; nc < 16; ++nc)
 #pragma unroll
             for (int r = 0; r < 4; ++r) vacc[mt][nc][r] = 0;
-    float wsum[NT];
+    uint32_t wacc[NT];
     const int pj = lane & 7, ph = lane >> 3;      // p-writer: k-word pj of head ph
     const int ptok = (pj & 3) + 16 * (pj >> 2);  // token of k = 4*pj (+4i for byte i)
     float pa[NT], pb[NT];
 #pragma unroll
     for (int mt = 0; mt < NT; ++mt) {
-        wsum[mt] = 0.f;
+        wacc[mt] = 0u;
         pa[mt] = sm.gpar[(4 * mt + ph) * 4 + 0];
         pb[mt] = sm.gpar[(4 * mt + ph) * 4 + 1];
     }
@@ -491,9 +513,8 @@ __global__ void __launch_bounds__(32, 8) decode_tc_kernel(const TcParams p) {
                     const int tok = btok + ptok + 4 * ii;
                     float pr = 0.0f;
                     if (h < G && tok < nv) pr = fminf(ex2(__fmaf_rn(scores[h * TS + tok], pa[mt], pb[mt])), 1.0f);
-                    const float f = __fmaf_rn(pr, kPScale, kMagic);  // round(p * (2^22-1)) in the low bits
-                    v[ii] = __float_as_uint(f);
-                    wsum[mt] += f - kMagic;
+                    v[ii] = __float_as_uint(__fmaf_rn(pr, kPScale, kMagic));  // round(p (2^22-1)) in low bits
+                    wacc[mt] += v[ii] & 0x3FFFFFu;
                 }
                 const uint32_t p01 = prmt(v[0], v[1], 0x5140), p23 = prmt(v[2], v[3], 0x5140);
                 const uint32_t q01 = prmt(v[0], v[1], 0x7362), q23 = prmt(v[2], v[3], 0x7362);
@@ -562,87 +583,55 @@ __global__ void __launch_bounds__(32, 8) decode_tc_kernel(const TcParams p) {
         if (lane == 0 && i + kStages < total_stages) issue(i + kStages);
     }
 
-    // ---------------- CTA partials -> cluster reduction ----------------
-    // All stages consumed and no copy in flight: the ring becomes the publication area.
-    // Raw u32 digit-plane accumulators are published as is; plane combination, the 2^-sh
-    // slot scale, the V step / zero-point and the division happen once per output in the
-    // cluster reduction below.
-    uint4* pubv = reinterpret_cast<uint4*>(sm.ring);  // [NT][16 nc][32 lanes]
-#pragma unroll
-    for (int mt = 0; mt < NT; ++mt)
-#pragma unroll
-        for (int nc = 0; nc < 16; ++nc)
-            pubv[(mt * 16 + nc) * 32 + lane] =
-                make_uint4((uint32_t)vacc[mt][nc][0], (uint32_t)vacc[mt][nc][1], (uint32_t)vacc[mt][nc][2],
-                           (uint32_t)vacc[mt][nc][3]);
-    float* pubt = reinterpret_cast<float*>(pubv + NT * 16 * 32);  // [G][128] tail numerators (if ntl)
+    // ---------------- push partials into rank 0 (exact integer reductions) ----------------
 #pragma unroll
     for (int mt = 0; mt < NT; ++mt) {
-        float ws = wsum[mt];  // u22 weight sum of head 4mt + ph over this chunk
+        uint32_t ws = wacc[mt];
 #pragma unroll
         for (int o : {1, 2, 4}) ws += __shfl_xor_sync(0xffffffffu, ws, o);
-        if (pj == 0 && 4 * mt + ph < G) sm.pub_den[4 * mt + ph] = ws;
-    }
-    if (ntl > 0) {
-        // fp32 tail rows of this CTA, on the same 2^22 - 1 weight scale.
-        for (int h = 0; h < G; ++h) {
-            float wt = 0.f;
-            float4 tn = make_float4(0.f, 0.f, 0.f, 0.f);
-            for (int j = 0; j < ntl; ++j) {
-                const float pt = ex2(__fmaf_rn(sm.tail_s[h * kTailMax + j], kLog2e, sm.gpar[h * 4 + 2])) * kPScale;
-                const float4 vv = *reinterpret_cast<const float4*>(
-                    a.v_tail + ((size_t)unit * a.tail_cap + tt0 + j) * kDim + 4 * lane);
-                tn.x = __fmaf_rn(pt, vv.x, tn.x);
-                tn.y = __fmaf_rn(pt, vv.y, tn.y);
-                tn.z = __fmaf_rn(pt, vv.z, tn.z);
-                tn.w = __fmaf_rn(pt, vv.w, tn.w);
-                wt += pt;
+        if (pj == 0 && 4 * mt + ph < G) red_cluster_u64(sm.wsum + 4 * mt + ph, 0, ws);
+        const int h = 4 * mt + (g & 3);
+        if (h < G) {
+#pragma unroll
+            for (int nc = 0; nc < 16; ++nc) {
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    // row g (+8 for r >= 2): plane 0/2 for g < 4, plane 1 (row g) for g >= 4
+                    if (!lowlane && r >= 2) continue;
+                    const int plane = lowlane ? (r >= 2 ? 2 : 0) : 1;
+                    int sh;
+                    const int ch = v_channel<BITS>(2 * t + (r & 1), nc, sh);
+                    red_cluster_u32(sm.vsum + (plane * G + h) * kDim + ch, 0, (uint32_t)vacc[mt][nc][r]);
+                }
             }
-            reinterpret_cast<float4*>(pubt + h * kDim)[lane] = tn;
-            if (lane == 0) sm.pub_den[8 + h] = wt;
         }
     }
-    if (lane == 0) sm.part->has_tail = ntl > 0;  // tail flag for the reducers
-    cluster_arrive();  // #2: partials published
+    cluster_arrive();  // #2: every CTA's accumulators are in rank 0
     cluster_wait();
-    // Each CTA finalizes a slice of the G x 128 outputs: exact u32 plane sums over the
-    // cluster, then out = (s_c V_c / 2^sh + alpha_c W_vis + T_c) / (W_vis + W_tail).
+    if (rank != 0) return;
+
+    // ---------------- rank 0: finalize the unit ----------------
+    // out = (s_c V_c / 2^sh + alpha_c W_vis + sum_t p_t v_tc) / (W_vis + sum_t p_t),
+    // every weight on the same (2^22 - 1) scale; tail weights recomputed in fp32.
     constexpr float kInvLevels = 1.0f / (float)((1u << BITS) - 1u);
-    const int per = (G * kDim + S - 1) / S;
-    for (int idx = rank * per + lane; idx < min(G * kDim, (rank + 1) * per); idx += 32) {
+    for (int idx = lane; idx < G * kDim; idx += 32) {
         const int h = idx / kDim, ch = idx % kDim;
-        // locate (plane rows, column) of (h, ch) in the MMA accumulator layout
         constexpr int cpb = Gm::kCpb;
-        const int byte = ch / cpb, s = cpb - 1 - ch % cpb;
-        const int gcol = byte / (2 * BITS), q = byte % (2 * BITS);
-        const int nc = q * cpb + s, sh = s * BITS;
-        const int mt = h >> 2, hl = h & 3;
-        const int lane0 = 4 * hl + (gcol >> 1);        // rows hl (plane 0) / hl+8 (plane 2)
-        const int lane1 = 4 * (hl + 4) + (gcol >> 1);  // row hl+4 (plane 1)
-        const int odd = gcol & 1;
-        uint32_t p0 = 0, p1 = 0, p2 = 0;
-        float wv = 0.f, wt = 0.f, tn = 0.f;
-        for (int r = 0; r < S; ++r) {
-            const uint32_t* pv = reinterpret_cast<const uint32_t*>(cluster.map_shared_rank(pubv, r) + (mt * 16 + nc) * 32);
-            p0 += pv[lane0 * 4 + odd];
-            p2 += pv[lane0 * 4 + 2 + odd];
-            p1 += pv[lane1 * 4 + odd];
-            const float* pd = cluster.map_shared_rank(sm.pub_den, r);
-            wv += pd[h];
-            if (cluster.map_shared_rank(sm.part, r)->has_tail) {
-                wt += pd[8 + h];
-                tn += reinterpret_cast<const float*>(cluster.map_shared_rank(pubv, r) + NT * 16 * 32)[h * kDim + ch];
-            }
-        }
-        const float V = __fmaf_rn((float)p2, 65536.0f, __fmaf_rn((float)p1, 256.0f, (float)p0)) *
+        const int sh = (cpb - 1 - ch % cpb) * BITS;
+        const float V = __fmaf_rn((float)sm.vsum[(2 * G + h) * kDim + ch], 65536.0f,
+                                  __fmaf_rn((float)sm.vsum[(G + h) * kDim + ch], 256.0f, (float)sm.vsum[h * kDim + ch])) *
                         __int_as_float((127 - sh) << 23);
+        const float wv = (float)sm.wsum[h];
+        float wt = 0.f, tn = 0.f;
+        for (int j = 0; j < ntl; ++j) {
+            const float pt = ex2(__fmaf_rn(sm.tail_s[h * kTailMax + j], kLog2e, sm.gpar[h * 4 + 2])) * kPScale;
+            wt += pt;
+            tn = __fmaf_rn(pt, a.v_tail[((size_t)unit * a.tail_cap + j) * kDim + ch], tn);
+        }
         const float va = __ldg(a.v_alpha + unit * kDim + ch);
         const float step = __fsub_rn(__ldg(a.v_beta + unit * kDim + ch), va) * kInvLevels;
-        a.out[((size_t)unit * G + h) * kDim + ch] =
-            __fmaf_rn(step > 0.0f ? step : 0.0f, V, __fmaf_rn(va, wv, tn)) / (wv + wt);
+        a.out[((size_t)unit * G + h) * kDim + ch] = __fmaf_rn(step > 0.0f ? step : 0.0f, V, __fmaf_rn(va, wv, tn)) / (wv + wt);
     }
-    cluster_arrive();  // #3: keep shared memory alive until every peer has read it
-    cluster_wait();
 }
 
 void plan(const DecodeArgs& a, int& S, int& T) {
@@ -667,7 +656,7 @@ cudaError_t launch_bits(const DecodeArgs& a, cudaStream_t s) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     TcParams p{a, a.tc_frag, a.tc_qconst, S, T};
-    const size_t smem = tc_smem_bytes((int)a.group, T, NT);
+    const size_t smem = tc_smem_bytes((int)a.group, T, NT, S);
     auto kern = decode_tc_kernel<BITS, NT>;
     static bool attr_done = false;  // per instantiation
     if (!attr_done) {
@@ -708,9 +697,9 @@ bool decode_tc_supported(const DecodeArgs& a) {
     int S, T;
     plan(a, S, T);
     if (T > kMaxT) return false;
-    // fp32 tail split over the cluster: at most kTailMax rows per CTA.
-    if (a.tail_cap > (size_t)kTailMax * S) return false;
-    return tc_smem_bytes((int)a.group, T, a.group > 4 ? 2 : 1) <= 200 * 1024;
+    // the fp32 tail lives in rank 0: at most kTailMax rows
+    if (a.tail_cap > (size_t)kTailMax) return false;
+    return tc_smem_bytes((int)a.group, T, a.group > 4 ? 2 : 1, S) <= 200 * 1024;
 }
 
 cudaError_t launch_decode_tc(const DecodeArgs& a, cudaStream_t s) {
