@@ -86,10 +86,14 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
+// The .aligned forms require a converged warp: every call site is preceded by a
+// __syncwarp() inside these helpers.
 __device__ __forceinline__ void cluster_arrive() {
+    __syncwarp();
     asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void cluster_wait() {
+    __syncwarp();
     asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
@@ -316,6 +320,7 @@ __global__ void __launch_bounds__(32, 8) decode_tc_kernel(const TcParams p) {
     }
     // #0: peers may push into this CTA's shared memory only once every CTA of the
     // cluster is running; arrive now, wait just before the first push.
+    __syncwarp();
     asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
     if (rank == 0) {  // cluster-wide accumulators, zeroed before barrier #1 lets peers in
         for (int i = lane; i < 3 * G * kDim; i += 32) sm.vsum[i] = 0u;
