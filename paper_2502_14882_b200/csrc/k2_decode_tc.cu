@@ -71,13 +71,19 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// Bounded wait: a TMA completion that never arrives traps (an error the host sees)
+// instead of hanging the device.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n .reg .pred p;\n"
-        "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
+    uint32_t done = 0;
+    for (uint32_t spin = 0;; ++spin) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+        if (done) return;
+        if (spin > (1u << 24)) __trap();
+    }
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile(
@@ -442,7 +448,8 @@ __global__ void __launch_bounds__(32, 8) decode_tc_kernel(const TcParams p) {
     }
     if (lane >= 4 * NT && lane < 8) mine = INFINITY;   // min of absent heads
     if (lane >= 8 + 4 * NT && lane < 16) mine = -INFINITY;
-    if (lane >= 16 && lane < 24) mine = __shfl_sync(0xffffffffu, tmax, lane - 16);
+    const float tm8 = __shfl_sync(0xffffffffu, tmax, lane & 7);  // all lanes: full-mask shuffle
+    if (lane >= 16 && lane < 24) mine = tm8;
     cluster_wait();  // #0
     if (lane < 24)
         for (int r = 0; r < S; ++r) st_cluster_f32(sm.allpart + rank * 24 + lane, r, mine);
