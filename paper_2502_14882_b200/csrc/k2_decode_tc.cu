@@ -33,9 +33,8 @@ namespace {
 
 constexpr int kDim = 128;
 constexpr int kStages = 2;
-constexpr int kStageBytes = 4096;
+constexpr int kStageBytes = 2048;
 constexpr int kTailMax = 64;   // fp32 tail tokens per CTA
-constexpr int kMaxT = 2048;    // visual tokens per CTA
 constexpr int kMaxCluster = 16;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: float -> int rounding trick
@@ -45,7 +44,7 @@ constexpr int kPRow = 12;              // words per p-plane smem row (stride avo
 template <int BITS>
 struct Geo {
     static constexpr int kRowBytes = 16 * BITS;
-    static constexpr int kStageTokens = kStageBytes / kRowBytes;  // 256 / BITS
+    static constexpr int kStageTokens = kStageBytes / kRowBytes;  // 128 / BITS
     static constexpr int kCpb = 8 / BITS;  // codes per byte
     static constexpr uint32_t kMask = 0x01010101u * ((1u << BITS) - 1u);
 };
@@ -222,44 +221,50 @@ __global__ void __launch_bounds__(kDim) prep_kernel(DecodeArgs a, int NT, uint32
 }
 
 // ---- decode ------------------------------------------------------------------------------
+constexpr int kWarps = 8;             // consumer warps per CTA
+constexpr int kWarpTokens = 512;      // visual tokens per warp (contiguous)
+constexpr int kCtaTokens = kWarps * kWarpTokens;
+
 struct Smem {  // carve-up of the dynamic shared memory of one decode CTA
-    uint8_t* ring;       // kStages x kStageBytes: TMA landing zone
-    float* scores;       // [G][T + 4] calibrated-softmax inputs of the visual chunk
-    float* tail_s;       // [G][kTailMax] fp32 tail scores (rank 0 only)
-    uint32_t* pw;        // [NT][12][kPRow] p digit planes of the current 32-token block
-    float* allpart;      // [S][24] (min[8], max[8], tail max[8]) pushed by every CTA
+    uint8_t* ring;       // [kWarps][kStages][kStageBytes]: per-warp TMA landing zones
+    float* scores;       // [kWarps][4 NT][kWarpTokens + 4]; reused for the accumulators
+    uint32_t* pw;        // [kWarps][NT][12][kPRow] p digit planes of a warp's current block
+    float* tail_s;       // [8][kTailMax] fp32 tail scores (rank 0)
+    float* wpart;        // [kWarps][24] per-warp (min, max, tail max) per head
+    float* allpart;      // [S][24] per-CTA partials (pushed by every CTA of the cluster)
     float* gpar;         // [8][4] softmax parameters per head
-    uint32_t* vsum;      // [3][G][128] rank 0: cluster-wide u32 digit-plane sums
-    unsigned long long* wsum;  // [8] rank 0: cluster-wide u22 weight sums per head
-    uint64_t* full;      // [kStages] TMA completion barriers
+    uint32_t* wsum;      // [kWarps][8] per-warp u22 weight sums per head
+    float* recv;         // [S][8 * 128 + 8] rank 0: partial numerators / denominators
+    uint64_t* full;      // [kWarps][kStages] TMA completion barriers
 };
 
-__host__ __device__ inline size_t tc_smem_bytes(int G, int T, int NT, int S, Smem* out = nullptr,
-                                                uint8_t* base = nullptr) {
+__host__ __device__ inline size_t tc_smem_bytes(int NT, int S, Smem* out = nullptr, uint8_t* base = nullptr) {
     size_t off = 0;
     auto take = [&](size_t bytes) {
         size_t o = off;
         off += (bytes + 15) & ~size_t(15);
         return base + o;
     };
-    uint8_t* ring = take(kStages * kStageBytes);
-    uint8_t* scores = take((size_t)G * (T + 4) * 4);
-    uint8_t* tail_s = take((size_t)G * kTailMax * 4);
-    uint8_t* pw = take((size_t)NT * 12 * kPRow * 4);
+    uint8_t* ring = take((size_t)kWarps * kStages * kStageBytes);
+    uint8_t* scores = take((size_t)kWarps * 4 * NT * (kWarpTokens + 4) * 4);
+    uint8_t* pw = take((size_t)kWarps * NT * 12 * kPRow * 4);
+    uint8_t* tail_s = take((size_t)8 * kTailMax * 4);
+    uint8_t* wpart = take((size_t)kWarps * 24 * 4);
     uint8_t* allpart = take((size_t)S * 24 * 4);
     uint8_t* gpar = take(32 * 4);
-    uint8_t* vsum = take((size_t)3 * G * kDim * 4);
-    uint8_t* wsum = take(8 * 8);
-    uint8_t* full = take(kStages * 8);
+    uint8_t* wsum = take((size_t)kWarps * 8 * 4);
+    uint8_t* recv = take(S > 1 ? (size_t)S * (8 * kDim + 8) * 4 : 16);
+    uint8_t* full = take((size_t)kWarps * kStages * 8);
     if (out) {
         out->ring = ring;
         out->scores = reinterpret_cast<float*>(scores);
-        out->tail_s = reinterpret_cast<float*>(tail_s);
         out->pw = reinterpret_cast<uint32_t*>(pw);
+        out->tail_s = reinterpret_cast<float*>(tail_s);
+        out->wpart = reinterpret_cast<float*>(wpart);
         out->allpart = reinterpret_cast<float*>(allpart);
         out->gpar = reinterpret_cast<float*>(gpar);
-        out->vsum = reinterpret_cast<uint32_t*>(vsum);
-        out->wsum = reinterpret_cast<unsigned long long*>(wsum);
+        out->wsum = reinterpret_cast<uint32_t*>(wsum);
+        out->recv = reinterpret_cast<float*>(recv);
         out->full = reinterpret_cast<uint64_t*>(full);
     }
     return off;
@@ -270,69 +275,55 @@ __device__ __forceinline__ void st_cluster_f32(float* local_ptr, int rank, float
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(addr) : "r"(smem_u32(local_ptr)), "r"(rank));
     asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
 }
-__device__ __forceinline__ void red_cluster_u32(uint32_t* local_ptr, int rank, uint32_t v) {
-    uint32_t addr;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(addr) : "r"(smem_u32(local_ptr)), "r"(rank));
-    asm volatile("red.shared::cluster.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
-}
-__device__ __forceinline__ void red_cluster_u64(unsigned long long* local_ptr, int rank, unsigned long long v) {
-    uint32_t addr;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(addr) : "r"(smem_u32(local_ptr)), "r"(rank));
-    asm volatile("red.shared::cluster.add.u64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
-}
 
-// One warp per CTA, one contiguous chunk of T visual tokens per CTA, a cluster of S
-// CTAs per unit. The warp streams its chunk through a 2-slot TMA ring (lane 0 re-arms a
-// slot once the warp has consumed it). Cross-CTA traffic is push-only: softmax stats
-// are stored into every peer before barrier #1, integer accumulators are reduced into
-// rank 0 (red.shared::cluster) before barrier #2; no CTA ever waits on a remote load.
+// CTA = 8 warps; warp w owns visual tokens [w*512, w*512+512) of the CTA's chunk and
+// streams them (K codes, then V codes) through its own 2-slot TMA ring, re-armed by its
+// lane 0. A unit of n visual tokens takes S = ceil(n / 4096) CTAs (a cluster); for
+// n <= 4096 there is no cluster traffic at all. Cross-warp reductions go through shared
+// memory (exact integer sums for the p.V accumulators); cross-CTA traffic is push-only.
 template <int BITS, int NT>
-__global__ void __launch_bounds__(32, 8) decode_tc_kernel(const TcParams p) {
+__global__ void __launch_bounds__(kWarps * 32, 1) decode_tc_kernel(const TcParams p) {
     using Gm = Geo<BITS>;
     const DecodeArgs& a = p.a;
     const int G = (int)a.group;
-    const int S = p.S, T = p.T, TS = T + 4;
-    const int rank = (int)cg::this_cluster().block_rank();
+    const int S = p.S;
+    constexpr int TS = kWarpTokens + 4;
+    const int rank = S > 1 ? (int)cg::this_cluster().block_rank() : 0;
     const int unit = blockIdx.x / S;
-    const int lane = threadIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, t = lane & 3;
 
     extern __shared__ __align__(128) uint8_t smem_raw[];
     Smem sm;
-    tc_smem_bytes(G, T, NT, S, &sm, smem_raw);
-    float* scores = sm.scores;
+    tc_smem_bytes(NT, S, &sm, smem_raw);
+    float* scores = sm.scores + warp * 4 * NT * TS;  // this warp's [4 NT][TS]
+    uint8_t* ring = sm.ring + warp * kStages * kStageBytes;
+    uint64_t* full = sm.full + warp * kStages;
 
     const int n = (int)a.n_vis;
-    const int tok0 = rank * T;
-    const int nv = max(0, min(T, n - tok0));
+    const int tok0 = rank * kCtaTokens + warp * kWarpTokens;  // this warp's first token
+    const int nv = max(0, min(kWarpTokens, n - tok0));
     const int ntl = rank == 0 ? a.tail_len[unit / a.kv_heads] : 0;  // fp32 tail: rank 0
     const uint8_t* kcodes = a.k_codes + ((size_t)unit * n + tok0) * Gm::kRowBytes;
     const uint8_t* vcodes = a.v_codes + ((size_t)unit * n + tok0) * Gm::kRowBytes;
     const int nstage = (nv + Gm::kStageTokens - 1) / Gm::kStageTokens;
     const int total_stages = 2 * nstage;
 
-    auto issue = [&](int i) {  // lane 0 only: stage i (K stages, then V stages) into slot i % kStages
+    auto issue = [&](int i) {  // lane 0: stage i (K stages, then V stages) into slot i % kStages
         const int slot = i % kStages;
         const int si = i < nstage ? i : i - nstage;
         const uint8_t* src = (i < nstage ? kcodes : vcodes) + (size_t)si * kStageBytes;
         const uint32_t bytes = (uint32_t)(min(Gm::kStageTokens, nv - si * Gm::kStageTokens) * Gm::kRowBytes);
-        mbar_expect_tx(&sm.full[slot], bytes);
-        bulk_g2s(sm.ring + slot * kStageBytes, src, bytes, &sm.full[slot]);
+        mbar_expect_tx(&full[slot], bytes);
+        bulk_g2s(ring + slot * kStageBytes, src, bytes, &full[slot]);
     };
     if (lane == 0) {
-        for (int i = 0; i < kStages; ++i) mbar_init(&sm.full[i], 1);
+        for (int i = 0; i < kStages; ++i) mbar_init(&full[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         for (int i = 0; i < min(kStages, total_stages); ++i) issue(i);
     }
-    // #0: peers may push into this CTA's shared memory only once every CTA of the
-    // cluster is running; arrive now, wait just before the first push.
     __syncwarp();
-    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-    if (rank == 0) {  // cluster-wide accumulators, zeroed before barrier #1 lets peers in
-        for (int i = lane; i < 3 * G * kDim; i += 32) sm.vsum[i] = 0u;
-        if (lane < 8) sm.wsum[lane] = 0ull;
-    }
-    __syncwarp();
+    if (S > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");  // #0
 
     griddep_wait();  // prep kernel's q planes are visible from here on
     uint32_t afrag[NT][4][4];
@@ -354,11 +345,11 @@ __global__ void __launch_bounds__(32, 8) decode_tc_kernel(const TcParams p) {
         lo[nt] = INFINITY, hi[nt] = -INFINITY;
     }
 
-    // ---------------- phase A: scores of the visual chunk ----------------
+    // ---------------- phase A: scores of this warp's tokens ----------------
     for (int st = 0; st < nstage; ++st) {
         const int slot = st % kStages;
-        mbar_wait(&sm.full[slot], (st / kStages) & 1);
-        const uint8_t* buf = sm.ring + slot * kStageBytes;
+        mbar_wait(&full[slot], (st / kStages) & 1);
+        const uint8_t* buf = ring + slot * kStageBytes;
         const int ns = min(Gm::kStageTokens, nv - st * Gm::kStageTokens);
         const int ntiles = (ns + 7) >> 3;
         const int tbase = st * Gm::kStageTokens + 2 * t + (lowlane ? 0 : 1);
@@ -393,7 +384,7 @@ __global__ void __launch_bounds__(32, 8) decode_tc_kernel(const TcParams p) {
                     imma_s8u8(acc[0], afrag[nt][kb], breg[0][2 * kb], breg[0][2 * kb + 1]);
                     imma_s8u8(acc[1], afrag[nt][kb], breg[1][2 * kb], breg[1][2 * kb + 1]);
                 }
-                const int h = 4 * nt + (g & 3);
+                const int hrow = 4 * nt + (g & 3);
 #pragma unroll
                 for (int u2 = 0; u2 < 2; ++u2) {
                     // rows g / g+8 hold digit planes (0,2) [g<4] or (1,3) [g>=4] of head g%4;
@@ -403,9 +394,9 @@ __global__ void __launch_bounds__(32, 8) decode_tc_kernel(const TcParams p) {
                     const int recv = __shfl_xor_sync(0xffffffffu, lowlane ? p1 : p0, 16);
                     const int total = (lowlane ? p0 : p1) + recv;
                     const int tok = tbase + (tile + u2) * 8;
-                    if (h < G && tok < nv) {
+                    if (hrow < G && tok < nv) {
                         const float sc = __fmaf_rn((float)total, cA[nt], cB[nt]);
-                        scores[h * TS + tok] = sc;
+                        scores[hrow * TS + tok] = sc;
                         lo[nt] = fminf(lo[nt], sc);
                         hi[nt] = fmaxf(hi[nt], sc);
                     }
@@ -416,23 +407,25 @@ __global__ void __launch_bounds__(32, 8) decode_tc_kernel(const TcParams p) {
         if (lane == 0 && st + kStages < total_stages) issue(st + kStages);
     }
 
-    // fp32 tail rows (rank 0): lanes split the 128 channels.
+    // fp32 tail rows (rank 0, warp 0): lanes split the 128 channels.
     const float isd = __fdiv_rn(1.0f, sqrtf((float)kDim));
     float tmax = -INFINITY;  // for head (lane & 7)
-    for (int j = 0; j < ntl; ++j) {
-        const float4 kv = *reinterpret_cast<const float4*>(a.k_tail + ((size_t)unit * a.tail_cap + j) * kDim + 4 * lane);
-        for (int h = 0; h < G; ++h) {
-            const float4 qv = *reinterpret_cast<const float4*>(a.q + ((size_t)unit * G + h) * kDim + 4 * lane);
-            float d = kv.x * qv.x + kv.y * qv.y + kv.z * qv.z + kv.w * qv.w;
+    if (warp == 0) {
+        for (int j = 0; j < ntl; ++j) {
+            const float4 kv = *reinterpret_cast<const float4*>(a.k_tail + ((size_t)unit * a.tail_cap + j) * kDim + 4 * lane);
+            for (int h = 0; h < G; ++h) {
+                const float4 qv = *reinterpret_cast<const float4*>(a.q + ((size_t)unit * G + h) * kDim + 4 * lane);
+                float d = kv.x * qv.x + kv.y * qv.y + kv.z * qv.z + kv.w * qv.w;
 #pragma unroll
-            for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-            d *= isd;
-            if (lane == 0) sm.tail_s[h * kTailMax + j] = d;
-            if ((lane & 7) == h) tmax = fmaxf(tmax, d);
+                for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+                d *= isd;
+                if (lane == 0) sm.tail_s[h * kTailMax + j] = d;
+                if ((lane & 7) == h) tmax = fmaxf(tmax, d);
+            }
         }
     }
-    // CTA partial (min, max, tail max) per head -> pushed into every peer.
-    float mine = -INFINITY;  // lane k < 24 owns value k of the partial record
+    // Per-warp partial record (min[8], max[8], tail max[8]); lane k < 24 owns entry k.
+    float mine = -INFINITY;
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
 #pragma unroll
@@ -442,23 +435,37 @@ __global__ void __launch_bounds__(32, 8) decode_tc_kernel(const TcParams p) {
         }
         // lane (g, 0), g < 4 holds head 4nt + g
         const float l8 = __shfl_sync(0xffffffffu, lo[nt], 4 * (lane & 3));
-        const float h8 = __shfl_sync(0xffffffffu, hi[nt], 4 * ((lane - 8) & 3));
-        if (lane >> 2 == nt) mine = l8;                 // lanes 4nt .. 4nt+3: min of head lane&3 (+4nt)
-        if ((lane - 8) >> 2 == nt && lane >= 8 && lane < 16) mine = h8;
+        const float h8 = __shfl_sync(0xffffffffu, hi[nt], 4 * (lane & 3));
+        if ((lane >> 2) == nt) mine = l8;              // lanes 4nt..4nt+3: min
+        if (lane >= 8 && lane < 16 && ((lane - 8) >> 2) == nt) mine = h8;  // lanes 8+4nt..: max
     }
-    if (lane >= 4 * NT && lane < 8) mine = INFINITY;   // min of absent heads
-    if (lane >= 8 + 4 * NT && lane < 16) mine = -INFINITY;
-    const float tm8 = __shfl_sync(0xffffffffu, tmax, lane & 7);  // all lanes: full-mask shuffle
+    if (lane >= 4 * NT && lane < 8) mine = INFINITY;  // absent heads
+    const float tm8 = __shfl_sync(0xffffffffu, tmax, lane & 7);
     if (lane >= 16 && lane < 24) mine = tm8;
-    cluster_wait();  // #0
-    if (lane < 24)
-        for (int r = 0; r < S; ++r) st_cluster_f32(sm.allpart + rank * 24 + lane, r, mine);
-    cluster_arrive();  // #1: partials pushed everywhere, rank 0 accumulators zeroed
-    cluster_wait();
-
-    // Global softmax parameters per head (identical in every CTA of the cluster).
-    if (lane < 8) {
-        const int h = lane;
+    if (lane < 24) sm.wpart[warp * 24 + lane] = mine;
+    __syncthreads();
+    if (threadIdx.x < 24) {  // CTA partial
+        const int k = threadIdx.x;
+        float v = sm.wpart[k];
+        for (int w2 = 1; w2 < kWarps; ++w2) v = k < 8 ? fminf(v, sm.wpart[w2 * 24 + k]) : fmaxf(v, sm.wpart[w2 * 24 + k]);
+        if (S > 1) {
+            asm volatile("barrier.cluster.wait.acquire;" ::: "memory");  // #0 (non-aligned: one warp)
+            for (int r = 0; r < S; ++r) st_cluster_f32(sm.allpart + rank * 24 + k, r, v);
+        } else {
+            sm.allpart[k] = v;
+        }
+    }
+    if (S > 1) {
+        if (threadIdx.x >= 24) asm volatile("barrier.cluster.wait.acquire;" ::: "memory");  // #0, the rest
+        __syncwarp();
+        cluster_arrive();  // #1: partials pushed everywhere
+        cluster_wait();
+    } else {
+        __syncthreads();
+    }
+    // Global softmax parameters per head.
+    if (threadIdx.x < 8) {
+        const int h = threadIdx.x;
         float gamma = INFINITY, delta = -INFINITY, tm = -INFINITY;
         for (int r = 0; r < S; ++r) {
             gamma = fminf(gamma, sm.allpart[r * 24 + h]);
@@ -481,9 +488,9 @@ __global__ void __launch_bounds__(32, 8) decode_tc_kernel(const TcParams p) {
         sm.gpar[h * 4 + 1] = (B - m) * kLog2e;
         sm.gpar[h * 4 + 2] = -m * kLog2e;
     }
-    __syncwarp();
+    __syncthreads();
 
-    // ---------------- phase B: p . V over the visual chunk ----------------
+    // ---------------- phase B: p . V over this warp's tokens ----------------
     // D[16 head-planes x 8 ch] += P[16 head-planes x 32 tok] * V[32 tok x 8 ch], 16 channel
     // tiles per 32-token block. p = exp(g(s) - m) in [0, 1] is a 22-bit integer split in
     // three u8 planes (A rows plane*4 + head), written once per (head, token) to a smem
@@ -506,16 +513,16 @@ __global__ void __launch_bounds__(32, 8) decode_tc_kernel(const TcParams p) {
         pa[mt] = sm.gpar[(4 * mt + ph) * 4 + 0];
         pb[mt] = sm.gpar[(4 * mt + ph) * 4 + 1];
     }
-    uint32_t* pw = sm.pw;
+    uint32_t* pw = sm.pw + warp * NT * 12 * kPRow;
     for (int st = 0; st < nstage; ++st) {
         const int i = nstage + st;
         const int slot = i % kStages;
-        mbar_wait(&sm.full[slot], (i / kStages) & 1);
-        const uint8_t* buf = sm.ring + slot * kStageBytes;
+        mbar_wait(&full[slot], (i / kStages) & 1);
+        const uint8_t* buf = ring + slot * kStageBytes;
         const int ns = min(Gm::kStageTokens, nv - st * Gm::kStageTokens);
         const int nblk = (ns + 31) >> 5;
         for (int blk = 0; blk < nblk; ++blk) {
-            const int btok = st * Gm::kStageTokens + blk * 32;  // chunk-local first token
+            const int btok = st * Gm::kStageTokens + blk * 32;  // warp-local first token
 #pragma unroll
             for (int mt = 0; mt < NT; ++mt) {
                 const int h = 4 * mt + ph;
@@ -595,68 +602,82 @@ __global__ void __launch_bounds__(32, 8) decode_tc_kernel(const TcParams p) {
         if (lane == 0 && i + kStages < total_stages) issue(i + kStages);
     }
 
-    // ---------------- push partials into rank 0 (exact integer reductions) ----------------
+    // ---------------- CTA reduction (exact integer sums through shared memory) ----------------
+    // This warp's scores are dead now: its region takes the warp's accumulators
+    // [NT][16 nc][32 lanes] uint4 (rows g / g+8 x columns 2t / 2t+1).
+    uint4* accs = reinterpret_cast<uint4*>(sm.scores + warp * 4 * NT * TS);
 #pragma unroll
     for (int mt = 0; mt < NT; ++mt) {
+#pragma unroll
+        for (int nc = 0; nc < 16; ++nc)
+            accs[(mt * 16 + nc) * 32 + lane] = make_uint4((uint32_t)vacc[mt][nc][0], (uint32_t)vacc[mt][nc][1],
+                                                          (uint32_t)vacc[mt][nc][2], (uint32_t)vacc[mt][nc][3]);
         uint32_t ws = wacc[mt];
 #pragma unroll
         for (int o : {1, 2, 4}) ws += __shfl_xor_sync(0xffffffffu, ws, o);
-        if (pj == 0 && 4 * mt + ph < G) red_cluster_u64(sm.wsum + 4 * mt + ph, 0, ws);
-        const int h = 4 * mt + (g & 3);
-        if (h < G) {
-#pragma unroll
-            for (int nc = 0; nc < 16; ++nc) {
-#pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    // row g (+8 for r >= 2): plane 0/2 for g < 4, plane 1 (row g) for g >= 4
-                    if (!lowlane && r >= 2) continue;
-                    const int plane = lowlane ? (r >= 2 ? 2 : 0) : 1;
-                    int sh;
-                    const int ch = v_channel<BITS>(2 * t + (r & 1), nc, sh);
-                    red_cluster_u32(sm.vsum + (plane * G + h) * kDim + ch, 0, (uint32_t)vacc[mt][nc][r]);
-                }
-            }
-        }
+        if (pj == 0) sm.wsum[warp * 8 + 4 * mt + ph] = ws;
     }
-    cluster_arrive();  // #2: every CTA's accumulators are in rank 0
-    cluster_wait();
-    if (rank != 0) return;
-
-    // ---------------- rank 0: finalize the unit ----------------
-    // out = (s_c V_c / 2^sh + alpha_c W_vis + sum_t p_t v_tc) / (W_vis + sum_t p_t),
-    // every weight on the same (2^22 - 1) scale; tail weights recomputed in fp32.
+    __syncthreads();
+    // Thread per (head, channel): u32 digit-plane sums over warps, then
+    //   out = (s_c V / 2^sh + alpha_c W_vis + sum_t p_t v_tc) / (W_vis + sum_t p_t)
+    // on the common (2^22 - 1) weight scale; tail weights recomputed in fp32 (rank 0).
     constexpr float kInvLevels = 1.0f / (float)((1u << BITS) - 1u);
-    for (int idx = lane; idx < G * kDim; idx += 32) {
+    for (int idx = threadIdx.x; idx < G * kDim; idx += kWarps * 32) {
         const int h = idx / kDim, ch = idx % kDim;
         constexpr int cpb = Gm::kCpb;
-        const int sh = (cpb - 1 - ch % cpb) * BITS;
-        const float V = __fmaf_rn((float)sm.vsum[(2 * G + h) * kDim + ch], 65536.0f,
-                                  __fmaf_rn((float)sm.vsum[(G + h) * kDim + ch], 256.0f, (float)sm.vsum[h * kDim + ch])) *
+        const int byte = ch / cpb, s = cpb - 1 - ch % cpb;
+        const int gcol = byte / (2 * BITS), q = byte % (2 * BITS);
+        const int nc = q * cpb + s, sh = s * BITS;
+        const int mt = h >> 2, hl = h & 3;
+        const int lane0 = 4 * hl + (gcol >> 1);        // rows hl (plane 0) / hl+8 (plane 2)
+        const int lane1 = 4 * (hl + 4) + (gcol >> 1);  // row hl+4 (plane 1)
+        const int odd = gcol & 1;
+        uint32_t s0 = 0, s1 = 0, s2 = 0, wv = 0;
+        for (int w2 = 0; w2 < kWarps; ++w2) {
+            const uint32_t* base = reinterpret_cast<const uint32_t*>(
+                reinterpret_cast<const uint4*>(sm.scores + w2 * 4 * NT * TS) + (mt * 16 + nc) * 32);
+            s0 += base[lane0 * 4 + odd];
+            s2 += base[lane0 * 4 + 2 + odd];
+            s1 += base[lane1 * 4 + odd];
+            wv += sm.wsum[w2 * 8 + h];
+        }
+        const float V = __fmaf_rn((float)s2, 65536.0f, __fmaf_rn((float)s1, 256.0f, (float)s0)) *
                         __int_as_float((127 - sh) << 23);
-        const float wv = (float)sm.wsum[h];
-        float wt = 0.f, tn = 0.f;
+        const float va = __ldg(a.v_alpha + unit * kDim + ch);
+        const float step = fmaxf(__fsub_rn(__ldg(a.v_beta + unit * kDim + ch), va) * kInvLevels, 0.0f);
+        float num = __fmaf_rn(step, V, va * (float)wv), den = (float)wv;
         for (int j = 0; j < ntl; ++j) {
             const float pt = ex2(__fmaf_rn(sm.tail_s[h * kTailMax + j], kLog2e, sm.gpar[h * 4 + 2])) * kPScale;
-            wt += pt;
-            tn = __fmaf_rn(pt, a.v_tail[((size_t)unit * a.tail_cap + j) * kDim + ch], tn);
+            den += pt;
+            num = __fmaf_rn(pt, a.v_tail[((size_t)unit * a.tail_cap + j) * kDim + ch], num);
         }
-        const float va = __ldg(a.v_alpha + unit * kDim + ch);
-        const float step = __fsub_rn(__ldg(a.v_beta + unit * kDim + ch), va) * kInvLevels;
-        a.out[((size_t)unit * G + h) * kDim + ch] = __fmaf_rn(step > 0.0f ? step : 0.0f, V, __fmaf_rn(va, wv, tn)) / (wv + wt);
+        if (S == 1) {
+            a.out[((size_t)unit * G + h) * kDim + ch] = num / den;
+        } else {
+            st_cluster_f32(sm.recv + rank * (8 * kDim + 8) + idx, 0, num);
+            if (ch == 0) st_cluster_f32(sm.recv + rank * (8 * kDim + 8) + 8 * kDim + h, 0, den);
+        }
+    }
+    if (S > 1) {
+        __syncwarp();
+        cluster_arrive();  // #2: partial numerators / denominators are in rank 0
+        cluster_wait();
+        if (rank != 0) return;
+        for (int idx = threadIdx.x; idx < G * kDim; idx += kWarps * 32) {
+            const int h = idx / kDim;
+            float num = 0.f, den = 0.f;
+            for (int r = 0; r < S; ++r) {
+                num += sm.recv[r * (8 * kDim + 8) + idx];
+                den += sm.recv[r * (8 * kDim + 8) + 8 * kDim + h];
+            }
+            a.out[((size_t)unit * G + (idx / kDim)) * kDim + (idx % kDim)] = num / den;
+        }
     }
 }
 
 void plan(const DecodeArgs& a, int& S, int& T) {
-    const int n = (int)a.n_vis;
-    const int units = (int)a.units;
-    const int s_min = (n + kMaxT - 1) / kMaxT;  // smem cap on tokens per CTA
-    int s_pref = (n + 511) / 512;               // ~512 tokens per (one-warp) CTA
-    const int want_ctas = 4 * 148;
-    if (units * s_pref < want_ctas) s_pref = (want_ctas + units - 1) / units;
-    S = std::max(1, std::min(kMaxCluster, std::max(s_min, s_pref)));
-    S = std::min(S, std::max(1, (n + 31) / 32));  // >= 32 tokens per CTA
-    T = ((n + S - 1) / S + 31) / 32 * 32;
-    S = (n + T - 1) / T;
+    S = std::max(1, (int)((a.n_vis + kCtaTokens - 1) / kCtaTokens));
+    T = kCtaTokens;
 }
 
 template <int BITS, int NT>
@@ -668,7 +689,7 @@ cudaError_t launch_bits(const DecodeArgs& a, cudaStream_t s) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     TcParams p{a, a.tc_frag, a.tc_qconst, S, T};
-    const size_t smem = tc_smem_bytes((int)a.group, T, NT, S);
+    const size_t smem = tc_smem_bytes(NT, S);
     auto kern = decode_tc_kernel<BITS, NT>;
     static bool attr_done = false;  // per instantiation
     if (!attr_done) {
@@ -680,7 +701,7 @@ cudaError_t launch_bits(const DecodeArgs& a, cudaStream_t s) {
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(a.units * S));
-    cfg.blockDim = dim3(32);
+    cfg.blockDim = dim3(kWarps * 32);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attrs[2];
@@ -708,10 +729,11 @@ bool decode_tc_supported(const DecodeArgs& a) {
     if (a.units == 0) return false;
     int S, T;
     plan(a, S, T);
-    if (T > kMaxT) return false;
+    if (S > kMaxCluster) return false;
     // the fp32 tail lives in rank 0: at most kTailMax rows
     if (a.tail_cap > (size_t)kTailMax) return false;
-    return tc_smem_bytes((int)a.group, T, a.group > 4 ? 2 : 1, S) <= 200 * 1024;
+    (void)T;
+    return tc_smem_bytes(a.group > 4 ? 2 : 1, S) <= 200 * 1024;
 }
 
 cudaError_t launch_decode_tc(const DecodeArgs& a, cudaStream_t s) {
