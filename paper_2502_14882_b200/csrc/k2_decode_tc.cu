@@ -38,13 +38,15 @@ constexpr int kTailMax = 64;   // fp32 tail tokens per CTA
 constexpr int kMaxCluster = 16;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: float -> int rounding trick
-constexpr float kPScale = 4194303.0f;  // 2^22 - 1: probabilities as 22-bit integers
+constexpr float kPScale = 4190000.0f;  // p in [0, 1(+eps)] -> integer < 2^22 (22-bit digits)
 constexpr int kPRow = 12;              // words per p-plane smem row (stride avoids bank conflicts)
 
 template <int BITS>
 struct Geo {
     static constexpr int kRowBytes = 16 * BITS;
-    static constexpr int kStageTokens = kStageBytes / kRowBytes;  // 128 / BITS
+    // >= 32 tokens per stage: a stage holds whole 32-token phase-B blocks
+    static constexpr int kStageBytesB = kStageBytes / kRowBytes >= 32 ? kStageBytes : 32 * kRowBytes;
+    static constexpr int kStageTokens = kStageBytesB / kRowBytes;
     static constexpr int kCpb = 8 / BITS;  // codes per byte
     static constexpr uint32_t kMask = 0x01010101u * ((1u << BITS) - 1u);
 };
@@ -113,11 +115,12 @@ __device__ __forceinline__ float ex2(float x) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
     return r;
 }
-// D += A(16x32, s8) * B(32x8, u8)
-__device__ __forceinline__ void imma_s8u8(int (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-    asm("mma.sync.aligned.m16n8k32.row.col.s32.s8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+// D += A(16x32, u8) * B(32x8, s8)
+__device__ __forceinline__ void imma_u8s8(int (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                          uint32_t b0, uint32_t b1) {
+    asm("mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
         : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
-        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 // D += A(16x32, u8) * B(32x8, u8)
 __device__ __forceinline__ void imma_u8u8(int (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
@@ -190,20 +193,19 @@ __global__ void __launch_bounds__(kDim) prep_kernel(DecodeArgs a, int NT, uint32
         if (h < G) qconst[unit * G + h] = make_float2(S > 0.0f ? isd / S : 0.0f, qdota * isd);
     }
     __syncthreads();
-    // A fragments: entry (nt, kb, reg, lane) packs bytes j = 0..3 of row r, k = 4t+j(+16).
-    const int total = NT * 4 * 4 * 32;
+    // B fragments of the q.K MMA: entry (hg, pp, kb, r, lane) packs bytes j = 0..3 of
+    // column n = g (head 4hg + g/2, digit plane 2pp + g%2) at k = 4t + j (+16 for r = 1).
+    const int total = NT * 2 * 4 * 2 * 32;
     for (int e = c; e < total; e += kDim) {
-        const int ln = e & 31, reg = (e >> 5) & 3, kb = (e >> 7) & 3, nt = e >> 9;
+        const int ln = e & 31, r = (e >> 5) & 1, kb = (e >> 6) & 3, pp = (e >> 8) & 1, hg = e >> 9;
         const int g = ln >> 2, t = ln & 3;
-        const int row = (reg & 1) ? g + 8 : g;
-        const int half = reg >> 1;
-        const int plane = ((row >> 2) & 1) + 2 * (row >> 3);
-        const int h = 4 * nt + (row & 3);
+        const int plane = 2 * pp + (g & 1);
+        const int h = 4 * hg + (g >> 1);
         uint32_t word = 0;
         if (h < G) {
             for (int j = 0; j < 4; ++j) {
                 int sh;
-                const int ch = k_channel<BITS>(t, 2 * kb + half, j, sh);
+                const int ch = k_channel<BITS>(t, 2 * kb + r, j, sh);
                 const int Q = __float2int_rn(__fmul_rn(s_qs[h][ch], s_scale[h]) * __int_as_float((127 - sh) << 23));
                 // balanced base-256 digits: Q = d0 + 2^8 d1 + 2^16 d2 + 2^24 d3
                 int d0 = ((Q + 128) & 255) - 128;
@@ -224,6 +226,7 @@ __global__ void __launch_bounds__(kDim) prep_kernel(DecodeArgs a, int NT, uint32
 constexpr int kWarps = 8;             // consumer warps per CTA
 constexpr int kWarpTokens = 512;      // visual tokens per warp (contiguous)
 constexpr int kCtaTokens = kWarps * kWarpTokens;
+constexpr int kTS = kWarpTokens + 36;  // score row stride (also holds 17 x 32 uint4 accumulators)
 
 struct Smem {  // carve-up of the dynamic shared memory of one decode CTA
     uint8_t* ring;       // [kWarps][kStages][kStageBytes]: per-warp TMA landing zones
@@ -238,15 +241,18 @@ struct Smem {  // carve-up of the dynamic shared memory of one decode CTA
     uint64_t* full;      // [kWarps][kStages] TMA completion barriers
 };
 
-__host__ __device__ inline size_t tc_smem_bytes(int NT, int S, Smem* out = nullptr, uint8_t* base = nullptr) {
+__host__ __device__ inline size_t tc_smem_bytes(int BITS, int NT, int S, Smem* out = nullptr, uint8_t* base = nullptr) {
     size_t off = 0;
     auto take = [&](size_t bytes) {
         size_t o = off;
         off += (bytes + 15) & ~size_t(15);
         return base + o;
     };
-    uint8_t* ring = take((size_t)kWarps * kStages * kStageBytes);
-    uint8_t* scores = take((size_t)kWarps * 4 * NT * (kWarpTokens + 4) * 4);
+    const int stage = kStageBytes / (16 * BITS) >= 32 ? kStageBytes : 32 * 16 * BITS;
+    const size_t planes_bytes = (size_t)3 * 4 * NT * (kDim + 1) * 4;
+    const size_t ring_bytes = (size_t)kWarps * kStages * stage;
+    uint8_t* ring = take(ring_bytes > planes_bytes ? ring_bytes : planes_bytes);
+    uint8_t* scores = take((size_t)kWarps * 4 * NT * kTS * 4);
     uint8_t* pw = take((size_t)kWarps * NT * 12 * kPRow * 4);
     uint8_t* tail_s = take((size_t)8 * kTailMax * 4);
     uint8_t* wpart = take((size_t)kWarps * 24 * 4);
@@ -287,7 +293,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_tc_kernel(const TcParam
     const DecodeArgs& a = p.a;
     const int G = (int)a.group;
     const int S = p.S;
-    constexpr int TS = kWarpTokens + 4;
+    constexpr int TS = kTS;
     const int rank = S > 1 ? (int)cg::this_cluster().block_rank() : 0;
     const int unit = blockIdx.x / S;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -295,9 +301,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_tc_kernel(const TcParam
 
     extern __shared__ __align__(128) uint8_t smem_raw[];
     Smem sm;
-    tc_smem_bytes(NT, S, &sm, smem_raw);
+    tc_smem_bytes(BITS, NT, S, &sm, smem_raw);
     float* scores = sm.scores + warp * 4 * NT * TS;  // this warp's [4 NT][TS]
-    uint8_t* ring = sm.ring + warp * kStages * kStageBytes;
+    uint8_t* ring = sm.ring + warp * kStages * Gm::kStageBytesB;
     uint64_t* full = sm.full + warp * kStages;
 
     const int n = (int)a.n_vis;
@@ -312,10 +318,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_tc_kernel(const TcParam
     auto issue = [&](int i) {  // lane 0: stage i (K stages, then V stages) into slot i % kStages
         const int slot = i % kStages;
         const int si = i < nstage ? i : i - nstage;
-        const uint8_t* src = (i < nstage ? kcodes : vcodes) + (size_t)si * kStageBytes;
+        const uint8_t* src = (i < nstage ? kcodes : vcodes) + (size_t)si * Gm::kStageBytesB;
         const uint32_t bytes = (uint32_t)(min(Gm::kStageTokens, nv - si * Gm::kStageTokens) * Gm::kRowBytes);
         mbar_expect_tx(&full[slot], bytes);
-        bulk_g2s(ring + slot * kStageBytes, src, bytes, &full[slot]);
+        bulk_g2s(ring + slot * Gm::kStageBytesB, src, bytes, &full[slot]);
     };
     if (lane == 0) {
         for (int i = 0; i < kStages; ++i) mbar_init(&full[i], 1);
@@ -326,79 +332,89 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_tc_kernel(const TcParam
     if (S > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");  // #0
 
     griddep_wait();  // prep kernel's q planes are visible from here on
-    uint32_t afrag[NT][4][4];
+    uint32_t bq[NT][2][4][2];  // [head group][digit-plane pair][k-block][reg]
     const uint32_t* fr = p.frag + (size_t)unit * NT * 512;
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
+    for (int hg = 0; hg < NT; ++hg)
 #pragma unroll
-        for (int kb = 0; kb < 4; ++kb)
+        for (int pp = 0; pp < 2; ++pp)
 #pragma unroll
-            for (int r = 0; r < 4; ++r) afrag[nt][kb][r] = __ldg(fr + ((nt * 4 + kb) * 4 + r) * 32 + lane);
-    const bool lowlane = g < 4;
-    const int wl = lowlane ? 1 : 256, wh = lowlane ? 65536 : (1 << 24);
+            for (int kb = 0; kb < 4; ++kb)
+#pragma unroll
+                for (int r = 0; r < 2; ++r) bq[hg][pp][kb][r] = __ldg(fr + (((hg * 2 + pp) * 4 + kb) * 2 + r) * 32 + lane);
     float cA[NT], cB[NT], lo[NT], hi[NT];
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-        const int h = 4 * nt + (g & 3);
+    for (int hg = 0; hg < NT; ++hg) {
+        const int h = 4 * hg + t;  // this lane's head in C columns 2t, 2t+1
         const float2 qc = h < G ? p.qconst[(size_t)unit * G + h] : make_float2(0.f, 0.f);
-        cA[nt] = qc.x, cB[nt] = qc.y;
-        lo[nt] = INFINITY, hi[nt] = -INFINITY;
+        cA[hg] = qc.x, cB[hg] = qc.y;
+        lo[hg] = INFINITY, hi[hg] = -INFINITY;
     }
 
     // ---------------- phase A: scores of this warp's tokens ----------------
+    // D[16 tokens x 8 (head, plane)] += K[16 tokens x 32 ch] * Q[32 ch x 8]: A = raw code
+    // bytes (one LOP3 selects 4 codes x 2^sh), B = the q digit planes (registers). Lane
+    // (g, t) ends with all four digit planes of head t for tokens g and g + 8.
     for (int st = 0; st < nstage; ++st) {
         const int slot = st % kStages;
         mbar_wait(&full[slot], (st / kStages) & 1);
-        const uint8_t* buf = ring + slot * kStageBytes;
+        const uint8_t* buf = ring + slot * Gm::kStageBytesB;
         const int ns = min(Gm::kStageTokens, nv - st * Gm::kStageTokens);
-        const int ntiles = (ns + 7) >> 3;
-        const int tbase = st * Gm::kStageTokens + 2 * t + (lowlane ? 0 : 1);
-        // Two tiles per iteration: two independent IMMA accumulator chains in flight.
-        for (int tile = 0; tile < ntiles; tile += 2) {
-            uint32_t breg[2][8];
+        for (int tile = 0; tile < ns; tile += 32) {  // two 16-token MMA tiles per iteration
+            uint32_t areg[2][2][8];  // [tile][token g / g+8][slot register rho]
 #pragma unroll
             for (int u2 = 0; u2 < 2; ++u2) {
-                const uint8_t* rowp = buf + ((tile + u2) * 8 + g) * Gm::kRowBytes + t * 4 * BITS;
-                uint32_t w[BITS];
-                if (BITS == 1) {
-                    w[0] = *reinterpret_cast<const uint32_t*>(rowp);
-                } else if (BITS == 2) {
-                    const uint2 v = *reinterpret_cast<const uint2*>(rowp);
-                    w[0] = v.x, w[1 % BITS] = v.y;
-                } else {
 #pragma unroll
-                    for (int u = 0; u < BITS; u += 4) {
-                        const uint4 v = *reinterpret_cast<const uint4*>(rowp + 4 * u);
-                        w[u] = v.x, w[(u + 1) % BITS] = v.y, w[(u + 2) % BITS] = v.z, w[(u + 3) % BITS] = v.w;
+                for (int hf = 0; hf < 2; ++hf) {
+                    const uint8_t* rowp = buf + (tile + 16 * u2 + 8 * hf + g) * Gm::kRowBytes + t * 4 * BITS;
+                    uint32_t w[BITS];
+                    if (BITS == 1) {
+                        w[0] = *reinterpret_cast<const uint32_t*>(rowp);
+                    } else if (BITS == 2) {
+                        const uint2 v = *reinterpret_cast<const uint2*>(rowp);
+                        w[0] = v.x, w[1 % BITS] = v.y;
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < BITS; u += 4) {
+                            const uint4 v = *reinterpret_cast<const uint4*>(rowp + 4 * u);
+                            w[u] = v.x, w[(u + 1) % BITS] = v.y, w[(u + 2) % BITS] = v.z, w[(u + 3) % BITS] = v.w;
+                        }
                     }
-                }
 #pragma unroll
-                for (int rho = 0; rho < 8; ++rho)
-                    breg[u2][rho] = w[rho / Gm::kCpb] & (Gm::kMask << ((rho % Gm::kCpb) * BITS));
+                    for (int rho = 0; rho < 8; ++rho)
+                        areg[u2][hf][rho] = w[rho / Gm::kCpb] & (Gm::kMask << ((rho % Gm::kCpb) * BITS));
+                }
             }
 #pragma unroll
-            for (int nt = 0; nt < NT; ++nt) {
-                int acc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+            for (int hg = 0; hg < NT; ++hg) {
+                int acc[2][2][4];  // [tile][plane pair]
 #pragma unroll
-                for (int kb = 0; kb < 4; ++kb) {
-                    imma_s8u8(acc[0], afrag[nt][kb], breg[0][2 * kb], breg[0][2 * kb + 1]);
-                    imma_s8u8(acc[1], afrag[nt][kb], breg[1][2 * kb], breg[1][2 * kb + 1]);
-                }
-                const int hrow = 4 * nt + (g & 3);
+                for (int u2 = 0; u2 < 2; ++u2)
+#pragma unroll
+                    for (int pp = 0; pp < 2; ++pp) acc[u2][pp][0] = acc[u2][pp][1] = acc[u2][pp][2] = acc[u2][pp][3] = 0;
+#pragma unroll
+                for (int kb = 0; kb < 4; ++kb)
+#pragma unroll
+                    for (int u2 = 0; u2 < 2; ++u2)
+#pragma unroll
+                        for (int pp = 0; pp < 2; ++pp)
+                            imma_u8s8(acc[u2][pp], areg[u2][0][2 * kb], areg[u2][1][2 * kb], areg[u2][0][2 * kb + 1],
+                                      areg[u2][1][2 * kb + 1], bq[hg][pp][kb][0], bq[hg][pp][kb][1]);
+                const int h = 4 * hg + t;
 #pragma unroll
                 for (int u2 = 0; u2 < 2; ++u2) {
-                    // rows g / g+8 hold digit planes (0,2) [g<4] or (1,3) [g>=4] of head g%4;
-                    // the int32 sums wrap mod 2^32 but the total is exact (|score| < 2^31).
-                    const int p0 = acc[u2][0] * wl + acc[u2][2] * wh;  // token 2t
-                    const int p1 = acc[u2][1] * wl + acc[u2][3] * wh;  // token 2t+1
-                    const int recv = __shfl_xor_sync(0xffffffffu, lowlane ? p1 : p0, 16);
-                    const int total = (lowlane ? p0 : p1) + recv;
-                    const int tok = tbase + (tile + u2) * 8;
-                    if (hrow < G && tok < nv) {
-                        const float sc = __fmaf_rn((float)total, cA[nt], cB[nt]);
-                        scores[hrow * TS + tok] = sc;
-                        lo[nt] = fminf(lo[nt], sc);
-                        hi[nt] = fmaxf(hi[nt], sc);
+#pragma unroll
+                    for (int hf = 0; hf < 2; ++hf) {
+                        // digit planes 0..3 of head t, token g (+8): wrapping int32 sum, exact total
+                        const int total = acc[u2][0][2 * hf] + acc[u2][0][2 * hf + 1] * 256 +
+                                          acc[u2][1][2 * hf] * 65536 + acc[u2][1][2 * hf + 1] * (1 << 24);
+                        const int tok = st * Gm::kStageTokens + tile + 16 * u2 + 8 * hf + g;
+                        if (h < G && tok < nv) {
+                            const float sc = __fmaf_rn((float)total, cA[hg], cB[hg]);
+                            scores[h * TS + tok] = sc;
+                            lo[hg] = fminf(lo[hg], sc);
+                            hi[hg] = fmaxf(hi[hg], sc);
+                        }
                     }
                 }
             }
@@ -406,6 +422,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_tc_kernel(const TcParam
         __syncwarp();
         if (lane == 0 && st + kStages < total_stages) issue(st + kStages);
     }
+    // Head rows beyond G: finite scores (their softmax offset is -inf, so p = 0).
+    for (int h = G; h < 4 * NT; ++h)
+        for (int tk = lane; tk < ((nv + 31) & ~31); tk += 32) scores[h * TS + tk] = 0.0f;
 
     // fp32 tail rows (rank 0, warp 0): lanes split the 128 channels.
     const float isd = __fdiv_rn(1.0f, sqrtf((float)kDim));
@@ -429,13 +448,13 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_tc_kernel(const TcParam
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
 #pragma unroll
-        for (int o : {1, 2, 16}) {
+        for (int o : {4, 8, 16}) {
             lo[nt] = fminf(lo[nt], __shfl_xor_sync(0xffffffffu, lo[nt], o));
             hi[nt] = fmaxf(hi[nt], __shfl_xor_sync(0xffffffffu, hi[nt], o));
         }
-        // lane (g, 0), g < 4 holds head 4nt + g
-        const float l8 = __shfl_sync(0xffffffffu, lo[nt], 4 * (lane & 3));
-        const float h8 = __shfl_sync(0xffffffffu, hi[nt], 4 * (lane & 3));
+        // lane t (< 4) holds head 4nt + t
+        const float l8 = __shfl_sync(0xffffffffu, lo[nt], lane & 3);
+        const float h8 = __shfl_sync(0xffffffffu, hi[nt], lane & 3);
         if ((lane >> 2) == nt) mine = l8;              // lanes 4nt..4nt+3: min
         if (lane >= 8 && lane < 16 && ((lane - 8) >> 2) == nt) mine = h8;  // lanes 8+4nt..: max
     }
@@ -503,13 +522,13 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_tc_kernel(const TcParam
         for (int nc = 0; nc < 16; ++nc)
 #pragma unroll
             for (int r = 0; r < 4; ++r) vacc[mt][nc][r] = 0;
-    uint32_t wacc[NT];
+    int wacc[NT][4];  // sum_j p_j per digit plane: IMMA against an all-ones operand
     const int pj = lane & 7, ph = lane >> 3;      // p-writer: k-word pj of head ph
     const int ptok = (pj & 3) + 16 * (pj >> 2);  // token of k = 4*pj (+4i for byte i)
     float pa[NT], pb[NT];
 #pragma unroll
     for (int mt = 0; mt < NT; ++mt) {
-        wacc[mt] = 0u;
+        wacc[mt][0] = wacc[mt][1] = wacc[mt][2] = wacc[mt][3] = 0;
         pa[mt] = sm.gpar[(4 * mt + ph) * 4 + 0];
         pb[mt] = sm.gpar[(4 * mt + ph) * 4 + 1];
     }
@@ -518,7 +537,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_tc_kernel(const TcParam
         const int i = nstage + st;
         const int slot = i % kStages;
         mbar_wait(&full[slot], (i / kStages) & 1);
-        const uint8_t* buf = ring + slot * kStageBytes;
+        const uint8_t* buf = ring + slot * Gm::kStageBytesB;
         const int ns = min(Gm::kStageTokens, nv - st * Gm::kStageTokens);
         const int nblk = (ns + 31) >> 5;
         for (int blk = 0; blk < nblk; ++blk) {
@@ -528,12 +547,19 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_tc_kernel(const TcParam
                 const int h = 4 * mt + ph;
                 uint32_t v[4];
 #pragma unroll
-                for (int ii = 0; ii < 4; ++ii) {
-                    const int tok = btok + ptok + 4 * ii;
-                    float pr = 0.0f;
-                    if (h < G && tok < nv) pr = fminf(ex2(__fmaf_rn(scores[h * TS + tok], pa[mt], pb[mt])), 1.0f);
-                    v[ii] = __float_as_uint(__fmaf_rn(pr, kPScale, kMagic));  // round(p (2^22-1)) in low bits
-                    wacc[mt] += v[ii] & 0x3FFFFFu;
+                if (btok + 32 <= nv) {  // full block (warp-uniform): no bounds checks
+#pragma unroll
+                    for (int ii = 0; ii < 4; ++ii) {
+                        const float pr = ex2(__fmaf_rn(scores[h * TS + btok + ptok + 4 * ii], pa[mt], pb[mt]));
+                        v[ii] = __float_as_uint(__fmaf_rn(pr, kPScale, kMagic));  // round(p * kPScale) in low bits
+                    }
+                } else {
+#pragma unroll
+                    for (int ii = 0; ii < 4; ++ii) {
+                        const int tok = btok + ptok + 4 * ii;
+                        const float pr = tok < nv ? ex2(__fmaf_rn(scores[h * TS + tok], pa[mt], pb[mt])) : 0.0f;
+                        v[ii] = __float_as_uint(__fmaf_rn(pr, kPScale, kMagic));
+                    }
                 }
                 const uint32_t p01 = prmt(v[0], v[1], 0x5140), p23 = prmt(v[2], v[3], 0x5140);
                 const uint32_t q01 = prmt(v[0], v[1], 0x7362), q23 = prmt(v[2], v[3], 0x7362);
@@ -549,8 +575,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_tc_kernel(const TcParam
                 const uint32_t* r0 = pw + (mt * 12 + g) * kPRow;
                 afr[mt][0] = r0[t];
                 afr[mt][2] = r0[4 + t];
-                afr[mt][1] = lowlane ? r0[8 * kPRow + t] : 0u;
-                afr[mt][3] = lowlane ? r0[8 * kPRow + 4 + t] : 0u;
+                afr[mt][1] = g < 4 ? r0[8 * kPRow + t] : 0u;
+                afr[mt][3] = g < 4 ? r0[8 * kPRow + 4 + t] : 0u;
             }
             __syncwarp();
             // B operand: V codes of this lane's 2*BITS bytes for 8 tokens, byte-transposed.
@@ -597,6 +623,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_tc_kernel(const TcParam
                 for (int mt = 0; mt < NT; ++mt)
                     imma_u8u8(vacc[mt][nc], afr[mt][0], afr[mt][1], afr[mt][2], afr[mt][3], b0, b1);
             }
+#pragma unroll
+            for (int mt = 0; mt < NT; ++mt)
+                imma_u8u8(wacc[mt], afr[mt][0], afr[mt][1], afr[mt][2], afr[mt][3], 0x01010101u, 0x01010101u);
         }
         __syncwarp();
         if (lane == 0 && i + kStages < total_stages) issue(i + kStages);
@@ -604,48 +633,58 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_tc_kernel(const TcParam
 
     // ---------------- CTA reduction (exact integer sums through shared memory) ----------------
     // This warp's scores are dead now: its region takes the warp's accumulators
-    // [NT][16 nc][32 lanes] uint4 (rows g / g+8 x columns 2t / 2t+1).
+    // [NT][16 nc + 1 (weights)][32 lanes] uint4 (rows g / g+8 x columns 2t / 2t+1).
     uint4* accs = reinterpret_cast<uint4*>(sm.scores + warp * 4 * NT * TS);
 #pragma unroll
     for (int mt = 0; mt < NT; ++mt) {
 #pragma unroll
         for (int nc = 0; nc < 16; ++nc)
-            accs[(mt * 16 + nc) * 32 + lane] = make_uint4((uint32_t)vacc[mt][nc][0], (uint32_t)vacc[mt][nc][1],
+            accs[(mt * 17 + nc) * 32 + lane] = make_uint4((uint32_t)vacc[mt][nc][0], (uint32_t)vacc[mt][nc][1],
                                                           (uint32_t)vacc[mt][nc][2], (uint32_t)vacc[mt][nc][3]);
-        uint32_t ws = wacc[mt];
-#pragma unroll
-        for (int o : {1, 2, 4}) ws += __shfl_xor_sync(0xffffffffu, ws, o);
-        if (pj == 0) sm.wsum[warp * 8 + 4 * mt + ph] = ws;
+        accs[(mt * 17 + 16) * 32 + lane] =
+            make_uint4((uint32_t)wacc[mt][0], (uint32_t)wacc[mt][1], (uint32_t)wacc[mt][2], (uint32_t)wacc[mt][3]);
     }
     __syncthreads();
-    // Thread per (head, channel): u32 digit-plane sums over warps, then
+    // Pass 1: element e of the accumulator image, summed over warps (consecutive threads
+    // read consecutive words: conflict-free), scattered into planes[plane][head][ch].
+    uint32_t* planes = reinterpret_cast<uint32_t*>(sm.ring);  // [3][4 NT][128 + 1] (ring is idle)
+    constexpr int PS = kDim + 1;
+    for (int e = threadIdx.x; e < NT * 17 * 128; e += kWarps * 32) {
+        const int mt = e / (17 * 128), rem = e % (17 * 128);
+        const int nc = rem >> 7, ln = (rem >> 2) & 31, r = rem & 3;
+        const int gg = ln >> 2, tt = ln & 3;
+        const int row = gg + 8 * (r >> 1);
+        if (row >= 12) continue;  // rows 12..15 are empty (3 digit planes)
+        uint32_t sum = 0;
+        for (int w2 = 0; w2 < kWarps; ++w2)
+            sum += reinterpret_cast<const uint32_t*>(sm.scores + w2 * 4 * NT * TS)[(mt * 17 * 32) * 4 + rem];
+        const int plane = row >> 2, head = 4 * mt + (row & 3);
+        if (nc == 16) {  // weights: identical in every column; keep column 0
+            if ((tt == 0) && (r & 1) == 0) planes[(plane * 4 * NT + head) * PS + kDim] = sum;
+            continue;
+        }
+        int sh;
+        const int ch = v_channel<BITS>(2 * tt + (r & 1), nc, sh);
+        planes[(plane * 4 * NT + head) * PS + ch] = sum;
+    }
+    __syncthreads();
+    // Pass 2, thread per (head, channel):
     //   out = (s_c V / 2^sh + alpha_c W_vis + sum_t p_t v_tc) / (W_vis + sum_t p_t)
-    // on the common (2^22 - 1) weight scale; tail weights recomputed in fp32 (rank 0).
+    // on the common kPScale weight scale; tail weights recomputed in fp32 (rank 0).
     constexpr float kInvLevels = 1.0f / (float)((1u << BITS) - 1u);
     for (int idx = threadIdx.x; idx < G * kDim; idx += kWarps * 32) {
         const int h = idx / kDim, ch = idx % kDim;
         constexpr int cpb = Gm::kCpb;
-        const int byte = ch / cpb, s = cpb - 1 - ch % cpb;
-        const int gcol = byte / (2 * BITS), q = byte % (2 * BITS);
-        const int nc = q * cpb + s, sh = s * BITS;
-        const int mt = h >> 2, hl = h & 3;
-        const int lane0 = 4 * hl + (gcol >> 1);        // rows hl (plane 0) / hl+8 (plane 2)
-        const int lane1 = 4 * (hl + 4) + (gcol >> 1);  // row hl+4 (plane 1)
-        const int odd = gcol & 1;
-        uint32_t s0 = 0, s1 = 0, s2 = 0, wv = 0;
-        for (int w2 = 0; w2 < kWarps; ++w2) {
-            const uint32_t* base = reinterpret_cast<const uint32_t*>(
-                reinterpret_cast<const uint4*>(sm.scores + w2 * 4 * NT * TS) + (mt * 16 + nc) * 32);
-            s0 += base[lane0 * 4 + odd];
-            s2 += base[lane0 * 4 + 2 + odd];
-            s1 += base[lane1 * 4 + odd];
-            wv += sm.wsum[w2 * 8 + h];
-        }
-        const float V = __fmaf_rn((float)s2, 65536.0f, __fmaf_rn((float)s1, 256.0f, (float)s0)) *
+        const int sh = (cpb - 1 - ch % cpb) * BITS;
+        const uint32_t* pl = planes + h * PS;
+        const float V = __fmaf_rn((float)pl[2 * 4 * NT * PS + ch], 65536.0f,
+                                  __fmaf_rn((float)pl[4 * NT * PS + ch], 256.0f, (float)pl[ch])) *
                         __int_as_float((127 - sh) << 23);
+        const float wv = __fmaf_rn((float)pl[2 * 4 * NT * PS + kDim], 65536.0f,
+                                   __fmaf_rn((float)pl[4 * NT * PS + kDim], 256.0f, (float)pl[kDim]));
         const float va = __ldg(a.v_alpha + unit * kDim + ch);
         const float step = fmaxf(__fsub_rn(__ldg(a.v_beta + unit * kDim + ch), va) * kInvLevels, 0.0f);
-        float num = __fmaf_rn(step, V, va * (float)wv), den = (float)wv;
+        float num = __fmaf_rn(step, V, va * wv), den = wv;
         for (int j = 0; j < ntl; ++j) {
             const float pt = ex2(__fmaf_rn(sm.tail_s[h * kTailMax + j], kLog2e, sm.gpar[h * 4 + 2])) * kPScale;
             den += pt;
@@ -689,7 +728,7 @@ cudaError_t launch_bits(const DecodeArgs& a, cudaStream_t s) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     TcParams p{a, a.tc_frag, a.tc_qconst, S, T};
-    const size_t smem = tc_smem_bytes(NT, S);
+    const size_t smem = tc_smem_bytes(BITS, NT, S);
     auto kern = decode_tc_kernel<BITS, NT>;
     static bool attr_done = false;  // per instantiation
     if (!attr_done) {
@@ -733,7 +772,7 @@ bool decode_tc_supported(const DecodeArgs& a) {
     // the fp32 tail lives in rank 0: at most kTailMax rows
     if (a.tail_cap > (size_t)kTailMax) return false;
     (void)T;
-    return tc_smem_bytes(a.group > 4 ? 2 : 1, S) <= 200 * 1024;
+    return tc_smem_bytes(a.bits, a.group > 4 ? 2 : 1, S) <= 200 * 1024;
 }
 
 cudaError_t launch_decode_tc(const DecodeArgs& a, cudaStream_t s) {
