@@ -253,7 +253,7 @@ __host__ __device__ inline size_t tc_smem_bytes(int BITS, int NT, int S, Smem* o
     const size_t ring_bytes = (size_t)kWarps * kStages * stage;
     uint8_t* ring = take(ring_bytes > planes_bytes ? ring_bytes : planes_bytes);
     uint8_t* scores = take((size_t)kWarps * 4 * NT * kTS * 4);
-    uint8_t* pw = take((size_t)kWarps * NT * 12 * kPRow * 4);
+    uint8_t* pw = take((size_t)kWarps * 2 * NT * 12 * kPRow * 4);
     uint8_t* tail_s = take((size_t)8 * kTailMax * 4);
     uint8_t* wpart = take((size_t)kWarps * 24 * 4);
     uint8_t* allpart = take((size_t)S * 24 * 4);
@@ -360,7 +360,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_tc_kernel(const TcParam
         mbar_wait(&full[slot], (st / kStages) & 1);
         const uint8_t* buf = ring + slot * Gm::kStageBytesB;
         const int ns = min(Gm::kStageTokens, nv - st * Gm::kStageTokens);
-        for (int tile = 0; tile < ns; tile += 32) {  // two 16-token MMA tiles per iteration
+        // Two 16-token MMA tiles per step; the epilogue of step k runs after the IMMAs of
+        // step k+1 are issued (software pipelining of the IMMA latency).
+        int accA[NT][2][2][4], accB[NT][2][2][4];  // two pipeline slots: [head group][tile][plane pair]
+        auto mma_step = [&](int tile, int (&ac)[NT][2][2][4]) {
             uint32_t areg[2][2][8];  // [tile][token g / g+8][slot register rho]
 #pragma unroll
             for (int u2 = 0; u2 < 2; ++u2) {
@@ -386,28 +389,34 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_tc_kernel(const TcParam
                 }
             }
 #pragma unroll
-            for (int hg = 0; hg < NT; ++hg) {
-                int acc[2][2][4];  // [tile][plane pair]
+            for (int hg = 0; hg < NT; ++hg)
 #pragma unroll
                 for (int u2 = 0; u2 < 2; ++u2)
 #pragma unroll
-                    for (int pp = 0; pp < 2; ++pp) acc[u2][pp][0] = acc[u2][pp][1] = acc[u2][pp][2] = acc[u2][pp][3] = 0;
+                    for (int pp = 0; pp < 2; ++pp)
+                        ac[hg][u2][pp][0] = ac[hg][u2][pp][1] = ac[hg][u2][pp][2] = ac[hg][u2][pp][3] = 0;
 #pragma unroll
-                for (int kb = 0; kb < 4; ++kb)
+            for (int kb = 0; kb < 4; ++kb)
+#pragma unroll
+                for (int hg = 0; hg < NT; ++hg)
 #pragma unroll
                     for (int u2 = 0; u2 < 2; ++u2)
 #pragma unroll
                         for (int pp = 0; pp < 2; ++pp)
-                            imma_u8s8(acc[u2][pp], areg[u2][0][2 * kb], areg[u2][1][2 * kb], areg[u2][0][2 * kb + 1],
+                            imma_u8s8(ac[hg][u2][pp], areg[u2][0][2 * kb], areg[u2][1][2 * kb], areg[u2][0][2 * kb + 1],
                                       areg[u2][1][2 * kb + 1], bq[hg][pp][kb][0], bq[hg][pp][kb][1]);
+        };
+        auto epilogue = [&](int tile, const int (&ac)[NT][2][2][4]) {
+#pragma unroll
+            for (int hg = 0; hg < NT; ++hg) {
                 const int h = 4 * hg + t;
 #pragma unroll
                 for (int u2 = 0; u2 < 2; ++u2) {
 #pragma unroll
                     for (int hf = 0; hf < 2; ++hf) {
                         // digit planes 0..3 of head t, token g (+8): wrapping int32 sum, exact total
-                        const int total = acc[u2][0][2 * hf] + acc[u2][0][2 * hf + 1] * 256 +
-                                          acc[u2][1][2 * hf] * 65536 + acc[u2][1][2 * hf + 1] * (1 << 24);
+                        const int total = ac[hg][u2][0][2 * hf] + ac[hg][u2][0][2 * hf + 1] * 256 +
+                                          ac[hg][u2][1][2 * hf] * 65536 + ac[hg][u2][1][2 * hf + 1] * (1 << 24);
                         const int tok = st * Gm::kStageTokens + tile + 16 * u2 + 8 * hf + g;
                         if (h < G && tok < nv) {
                             const float sc = __fmaf_rn((float)total, cA[hg], cB[hg]);
@@ -418,6 +427,22 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_tc_kernel(const TcParam
                     }
                 }
             }
+        };
+        const int nsteps = (ns + 31) >> 5;  // >= 1
+        mma_step(0, accA);
+        int k = 1;
+        for (; k + 1 < nsteps; k += 2) {  // unrolled by two: register-resident pipeline slots
+            mma_step(32 * k, accB);
+            epilogue(32 * (k - 1), accA);
+            mma_step(32 * (k + 1), accA);
+            epilogue(32 * k, accB);
+        }
+        if (k < nsteps) {
+            mma_step(32 * k, accB);
+            epilogue(32 * (k - 1), accA);
+            epilogue(32 * k, accB);
+        } else {
+            epilogue(32 * (k - 1), accA);
         }
         __syncwarp();
         if (lane == 0 && st + kStages < total_stages) issue(st + kStages);
@@ -532,103 +557,107 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_tc_kernel(const TcParam
         pa[mt] = sm.gpar[(4 * mt + ph) * 4 + 0];
         pb[mt] = sm.gpar[(4 * mt + ph) * 4 + 1];
     }
-    uint32_t* pw = sm.pw + warp * NT * 12 * kPRow;
-    for (int st = 0; st < nstage; ++st) {
-        const int i = nstage + st;
-        const int slot = i % kStages;
-        mbar_wait(&full[slot], (i / kStages) & 1);
-        const uint8_t* buf = ring + slot * Gm::kStageBytesB;
-        const int ns = min(Gm::kStageTokens, nv - st * Gm::kStageTokens);
-        const int nblk = (ns + 31) >> 5;
-        for (int blk = 0; blk < nblk; ++blk) {
-            const int btok = st * Gm::kStageTokens + blk * 32;  // warp-local first token
+    // p tiles are double-buffered: block b+1's probabilities are produced while block
+    // b's IMMAs issue (software pipelining hides the LDS -> FFMA -> MUFU latency chain).
+    uint32_t* pw = sm.pw + warp * 2 * NT * 12 * kPRow;
+    auto p_write = [&](int blk, uint32_t* tile) {
+        const int btok = blk * 32;  // warp-local first token of the block
 #pragma unroll
-            for (int mt = 0; mt < NT; ++mt) {
-                const int h = 4 * mt + ph;
-                uint32_t v[4];
-#pragma unroll
-                if (btok + 32 <= nv) {  // full block (warp-uniform): no bounds checks
-#pragma unroll
-                    for (int ii = 0; ii < 4; ++ii) {
-                        const float pr = ex2(__fmaf_rn(scores[h * TS + btok + ptok + 4 * ii], pa[mt], pb[mt]));
-                        v[ii] = __float_as_uint(__fmaf_rn(pr, kPScale, kMagic));  // round(p * kPScale) in low bits
-                    }
-                } else {
-#pragma unroll
-                    for (int ii = 0; ii < 4; ++ii) {
-                        const int tok = btok + ptok + 4 * ii;
-                        const float pr = tok < nv ? ex2(__fmaf_rn(scores[h * TS + tok], pa[mt], pb[mt])) : 0.0f;
-                        v[ii] = __float_as_uint(__fmaf_rn(pr, kPScale, kMagic));
-                    }
-                }
-                const uint32_t p01 = prmt(v[0], v[1], 0x5140), p23 = prmt(v[2], v[3], 0x5140);
-                const uint32_t q01 = prmt(v[0], v[1], 0x7362), q23 = prmt(v[2], v[3], 0x7362);
-                uint32_t* rowp = pw + (mt * 12 + ph) * kPRow + pj;
-                rowp[0 * 4 * kPRow] = prmt(p01, p23, 0x5410);                // bits 0-7
-                rowp[1 * 4 * kPRow] = prmt(p01, p23, 0x7632);                // bits 8-15
-                rowp[2 * 4 * kPRow] = prmt(q01, q23, 0x5410) & 0x3F3F3F3Fu;  // bits 16-21
-            }
-            __syncwarp();
-            uint32_t afr[NT][4];
-#pragma unroll
-            for (int mt = 0; mt < NT; ++mt) {
-                const uint32_t* r0 = pw + (mt * 12 + g) * kPRow;
-                afr[mt][0] = r0[t];
-                afr[mt][2] = r0[4 + t];
-                afr[mt][1] = g < 4 ? r0[8 * kPRow + t] : 0u;
-                afr[mt][3] = g < 4 ? r0[8 * kPRow + 4 + t] : 0u;
-            }
-            __syncwarp();
-            // B operand: V codes of this lane's 2*BITS bytes for 8 tokens, byte-transposed.
-            constexpr int NW = (2 * BITS + 3) / 4;  // 32-bit words per token slice
-            uint32_t X[2][2 * BITS];
-#pragma unroll
-            for (int grp = 0; grp < 2; ++grp) {
-                uint32_t raw[4][NW];
+        for (int mt = 0; mt < NT; ++mt) {
+            const int h = 4 * mt + ph;
+            uint32_t v[4];
+            if (btok + 32 <= nv) {  // full block (warp-uniform): no bounds checks
 #pragma unroll
                 for (int ii = 0; ii < 4; ++ii) {
-                    const uint8_t* rp = buf + (blk * 32 + 16 * grp + t + 4 * ii) * Gm::kRowBytes + 2 * BITS * g;
-                    if (BITS == 1) {
-                        raw[ii][0] = *reinterpret_cast<const uint16_t*>(rp);
-                    } else if (BITS == 2) {
-                        raw[ii][0] = *reinterpret_cast<const uint32_t*>(rp);
-                    } else if (BITS == 4) {
-                        const uint2 vv = *reinterpret_cast<const uint2*>(rp);
-                        raw[ii][0] = vv.x, raw[ii][NW - 1] = vv.y;
-                    } else {
-                        const uint4 vv = *reinterpret_cast<const uint4*>(rp);
-                        raw[ii][0] = vv.x, raw[ii][1 % NW] = vv.y, raw[ii][2 % NW] = vv.z, raw[ii][3 % NW] = vv.w;
-                    }
+                    const float pr = ex2(__fmaf_rn(scores[h * TS + btok + ptok + 4 * ii], pa[mt], pb[mt]));
+                    v[ii] = __float_as_uint(__fmaf_rn(pr, kPScale, kMagic));  // round(p * kPScale) in low bits
                 }
+            } else {
 #pragma unroll
-                for (int wi = 0; wi < NW; ++wi) {
-                    const uint32_t P0 = prmt(raw[0][wi], raw[1][wi], 0x5140);
-                    const uint32_t P2 = prmt(raw[2][wi], raw[3][wi], 0x5140);
-                    X[grp][(4 * wi + 0) % (2 * BITS)] = prmt(P0, P2, 0x5410);
-                    X[grp][(4 * wi + 1) % (2 * BITS)] = prmt(P0, P2, 0x7632);
-                    if (2 * BITS > 2) {
-                        const uint32_t P1 = prmt(raw[0][wi], raw[1][wi], 0x7362);
-                        const uint32_t P3 = prmt(raw[2][wi], raw[3][wi], 0x7362);
-                        X[grp][(4 * wi + 2) % (2 * BITS)] = prmt(P1, P3, 0x5410);
-                        X[grp][(4 * wi + 3) % (2 * BITS)] = prmt(P1, P3, 0x7632);
-                    }
+                for (int ii = 0; ii < 4; ++ii) {
+                    const int tok = btok + ptok + 4 * ii;
+                    const float pr = tok < nv ? ex2(__fmaf_rn(scores[h * TS + tok], pa[mt], pb[mt])) : 0.0f;
+                    v[ii] = __float_as_uint(__fmaf_rn(pr, kPScale, kMagic));
+                }
+            }
+            const uint32_t p01 = prmt(v[0], v[1], 0x5140), p23 = prmt(v[2], v[3], 0x5140);
+            const uint32_t q01 = prmt(v[0], v[1], 0x7362), q23 = prmt(v[2], v[3], 0x7362);
+            uint32_t* rowp = tile + (mt * 12 + ph) * kPRow + pj;
+            rowp[0 * 4 * kPRow] = prmt(p01, p23, 0x5410);                // bits 0-7
+            rowp[1 * 4 * kPRow] = prmt(p01, p23, 0x7632);                // bits 8-15
+            rowp[2 * 4 * kPRow] = prmt(q01, q23, 0x5410) & 0x3F3F3F3Fu;  // bits 16-21
+        }
+    };
+    constexpr int kBps = Gm::kStageTokens / 32;  // 32-token blocks per stage
+    const int nblk_all = (nv + 31) >> 5;
+    if (nblk_all > 0) p_write(0, pw);
+    __syncwarp();
+    for (int b = 0; b < nblk_all; ++b) {
+        const int st = b / kBps, blk = b % kBps;
+        const int i = nstage + st;
+        const int slot = i % kStages;
+        if (blk == 0) mbar_wait(&full[slot], (i / kStages) & 1);
+        const uint8_t* buf = ring + slot * Gm::kStageBytesB;
+        uint32_t* cur = pw + (b & 1) * NT * 12 * kPRow;
+        uint32_t afr[NT][4];
+#pragma unroll
+        for (int mt = 0; mt < NT; ++mt) {
+            const uint32_t* r0 = cur + (mt * 12 + g) * kPRow;
+            afr[mt][0] = r0[t];
+            afr[mt][2] = r0[4 + t];
+            afr[mt][1] = g < 4 ? r0[8 * kPRow + t] : 0u;
+            afr[mt][3] = g < 4 ? r0[8 * kPRow + 4 + t] : 0u;
+        }
+        if (b + 1 < nblk_all) p_write(b + 1, pw + ((b + 1) & 1) * NT * 12 * kPRow);
+        // B operand: V codes of this lane's 2*BITS bytes for 8 tokens, byte-transposed.
+        constexpr int NW = (2 * BITS + 3) / 4;  // 32-bit words per token slice
+        uint32_t X[2][2 * BITS];
+#pragma unroll
+        for (int grp = 0; grp < 2; ++grp) {
+            uint32_t raw[4][NW];
+#pragma unroll
+            for (int ii = 0; ii < 4; ++ii) {
+                const uint8_t* rp = buf + (blk * 32 + 16 * grp + t + 4 * ii) * Gm::kRowBytes + 2 * BITS * g;
+                if (BITS == 1) {
+                    raw[ii][0] = *reinterpret_cast<const uint16_t*>(rp);
+                } else if (BITS == 2) {
+                    raw[ii][0] = *reinterpret_cast<const uint32_t*>(rp);
+                } else if (BITS == 4) {
+                    const uint2 vv = *reinterpret_cast<const uint2*>(rp);
+                    raw[ii][0] = vv.x, raw[ii][NW - 1] = vv.y;
+                } else {
+                    const uint4 vv = *reinterpret_cast<const uint4*>(rp);
+                    raw[ii][0] = vv.x, raw[ii][1 % NW] = vv.y, raw[ii][2 % NW] = vv.z, raw[ii][3 % NW] = vv.w;
                 }
             }
 #pragma unroll
-            for (int nc = 0; nc < 16; ++nc) {
-                constexpr int cpb = Gm::kCpb;
-                const uint32_t m = Gm::kMask << ((nc % cpb) * BITS);
-                const uint32_t b0 = X[0][nc / cpb] & m, b1 = X[1][nc / cpb] & m;
-#pragma unroll
-                for (int mt = 0; mt < NT; ++mt)
-                    imma_u8u8(vacc[mt][nc], afr[mt][0], afr[mt][1], afr[mt][2], afr[mt][3], b0, b1);
+            for (int wi = 0; wi < NW; ++wi) {
+                const uint32_t P0 = prmt(raw[0][wi], raw[1][wi], 0x5140);
+                const uint32_t P2 = prmt(raw[2][wi], raw[3][wi], 0x5140);
+                X[grp][(4 * wi + 0) % (2 * BITS)] = prmt(P0, P2, 0x5410);
+                X[grp][(4 * wi + 1) % (2 * BITS)] = prmt(P0, P2, 0x7632);
+                if (2 * BITS > 2) {
+                    const uint32_t P1 = prmt(raw[0][wi], raw[1][wi], 0x7362);
+                    const uint32_t P3 = prmt(raw[2][wi], raw[3][wi], 0x7362);
+                    X[grp][(4 * wi + 2) % (2 * BITS)] = prmt(P1, P3, 0x5410);
+                    X[grp][(4 * wi + 3) % (2 * BITS)] = prmt(P1, P3, 0x7632);
+                }
             }
+        }
+#pragma unroll
+        for (int nc = 0; nc < 16; ++nc) {
+            constexpr int cpb = Gm::kCpb;
+            const uint32_t m = Gm::kMask << ((nc % cpb) * BITS);
+            const uint32_t b0 = X[0][nc / cpb] & m, b1 = X[1][nc / cpb] & m;
 #pragma unroll
             for (int mt = 0; mt < NT; ++mt)
-                imma_u8u8(wacc[mt], afr[mt][0], afr[mt][1], afr[mt][2], afr[mt][3], 0x01010101u, 0x01010101u);
+                imma_u8u8(vacc[mt][nc], afr[mt][0], afr[mt][1], afr[mt][2], afr[mt][3], b0, b1);
         }
+#pragma unroll
+        for (int mt = 0; mt < NT; ++mt)
+            imma_u8u8(wacc[mt], afr[mt][0], afr[mt][1], afr[mt][2], afr[mt][3], 0x01010101u, 0x01010101u);
         __syncwarp();
-        if (lane == 0 && i + kStages < total_stages) issue(i + kStages);
+        if (lane == 0 && (blk == kBps - 1 || b == nblk_all - 1) && i + kStages < total_stages) issue(i + kStages);
     }
 
     // ---------------- CTA reduction (exact integer sums through shared memory) ----------------
