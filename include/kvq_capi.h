@@ -2,7 +2,7 @@
  * kvq_capi.h — C-ABI of the B200-native CalibQuant decode hot path.
  *
  * This is the drop-in boundary. Every entry point replaces one function of the
- * reference's header-only C++ API (`kvq`, /root/reference/proj/include/kvq/*.hpp;
+ * reference's header-only C++ API (`kvq`, headers under /root/reference/proj/include/kvq/;
  * cited per function below) and is what the C++ drop-in headers in include/kvq/ and
  * the Python binding (paper_2502_14882_b200/kvq.py) bind. Plain pointers and sizes
  * only: no CUDA, torch or C++ types cross this boundary.
@@ -95,6 +95,11 @@ int kvq_qk_scores(const float* queries, const uint8_t* codes, const float* alpha
 int kvq_wv_output(const float* weights, const uint8_t* codes, const float* alpha,
                   const float* beta, size_t heads, size_t tokens, size_t dim, int bitwidth,
                   int word_bits, float* out);
+
+/* kvq::naive_qk (kernels.hpp:401-413): dense q . k_j for every row of k [rows][cols]. */
+int kvq_naive_qk(const float* q, const float* k, size_t rows, size_t cols, float* out);
+/* kvq::naive_wv (kernels.hpp:415-426): sum_j w_j v_j over the rows of v [rows][cols]. */
+int kvq_naive_wv(const float* w, const float* v, size_t rows, size_t cols, float* out);
 
 /* ---- calibrate.hpp ----------------------------------------------------------- */
 /* kvq::calibrated_softmax_concat (calibrate.hpp:100-114) over `rows` rows:

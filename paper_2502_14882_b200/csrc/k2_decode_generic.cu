@@ -242,7 +242,37 @@ __global__ void calibrated_softmax_kernel(const float* __restrict__ vis, size_t 
     for (size_t j = threadIdx.x; j < n_vis + n_tail; j += blockDim.x) o[j] = __fdiv_rn(o[j], sum);
 }
 
+__global__ void naive_qk_kernel(const float* __restrict__ q, const float* __restrict__ k, size_t rows,
+                                size_t cols, float* __restrict__ out) {
+    for (size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x; j < rows; j += (size_t)gridDim.x * blockDim.x) {
+        float acc = 0.0f;
+        for (size_t c = 0; c < cols; ++c) acc = __fmaf_rn(q[c], k[j * cols + c], acc);
+        out[j] = acc;
+    }
+}
+
+__global__ void naive_wv_kernel(const float* __restrict__ w, const float* __restrict__ v, size_t rows,
+                                size_t cols, float* __restrict__ out) {
+    for (size_t c = (size_t)blockIdx.x * blockDim.x + threadIdx.x; c < cols; c += (size_t)gridDim.x * blockDim.x) {
+        float acc = 0.0f;
+        for (size_t j = 0; j < rows; ++j) acc = __fmaf_rn(w[j], v[j * cols + c], acc);
+        out[c] = acc;
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_naive_qk(const float* q, const float* k, size_t rows, size_t cols, float* out, cudaStream_t s) {
+    naive_qk_kernel<<<(unsigned)((rows + 255) / 256 ? (rows + 255) / 256 : 1), 256, 0, s>>>(q, k, rows, cols, out);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_naive_wv(const float* w, const float* v, size_t rows, size_t cols, float* out, cudaStream_t s) {
+    naive_wv_kernel<<<(unsigned)((cols + 127) / 128 ? (cols + 127) / 128 : 1), 128, 0, s>>>(w, v, rows, cols, out);
+    note_launch();
+    return cudaGetLastError();
+}
 
 cudaError_t launch_decode_generic(const DecodeArgs& a, cudaStream_t s) {
     const size_t cpr = codes_per_row(a.dim, a.bits, a.word_bits);

@@ -483,6 +483,32 @@ int kvq_wv_output(const float* weights, const uint8_t* codes, const float* alpha
     });
 }
 
+int kvq_naive_qk(const float* q, const float* k, size_t rows, size_t cols, float* out) {
+    return guarded([&] {
+        if (rows == 0) return;
+        require_device();
+        DevBuf<float> dq(cols ? cols : 1), dk(rows * cols ? rows * cols : 1), dout(rows);
+        dq.upload(q, cols);
+        dk.upload(k, rows * cols);
+        ck(kvqb::launch_naive_qk(dq.p, dk.p, rows, cols, dout.p, 0), "naive_qk");
+        dout.download(out, rows);
+        sync(0);
+    });
+}
+
+int kvq_naive_wv(const float* w, const float* v, size_t rows, size_t cols, float* out) {
+    return guarded([&] {
+        if (cols == 0) return;
+        require_device();
+        DevBuf<float> dw(rows ? rows : 1), dv(rows * cols ? rows * cols : 1), dout(cols);
+        dw.upload(w, rows);
+        dv.upload(v, rows * cols);
+        ck(kvqb::launch_naive_wv(dw.p, dv.p, rows, cols, dout.p, 0), "naive_wv");
+        dout.download(out, cols);
+        sync(0);
+    });
+}
+
 int kvq_calibrated_softmax_concat(const float* vis, size_t n_vis, const float* tail, size_t n_tail,
                                   size_t rows, float tau1, float tau2, float* out,
                                   size_t* slope_violations) {

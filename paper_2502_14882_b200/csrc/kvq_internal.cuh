@@ -84,6 +84,9 @@ cudaError_t launch_qk_scores(const float* q, const uint8_t* codes, const float* 
 cudaError_t launch_wv_output(const float* w, const uint8_t* codes, const float* alpha,
                              const float* beta, size_t heads, size_t tokens, size_t dim,
                              int bits, int word_bits, float* out, cudaStream_t s);
+// Dense fp32 products of the tail / full-precision baseline (kernels.hpp:401-426).
+cudaError_t launch_naive_qk(const float* q, const float* k, size_t rows, size_t cols, float* out, cudaStream_t s);
+cudaError_t launch_naive_wv(const float* w, const float* v, size_t rows, size_t cols, float* out, cudaStream_t s);
 // calibrated_softmax_concat (calibrate.hpp:100-114) over `rows` independent rows.
 cudaError_t launch_calibrated_softmax(const float* vis, size_t n_vis, const float* tail,
                                       size_t n_tail, size_t rows, float tau1, float tau2,

@@ -1,0 +1,183 @@
+// test_dropin.cpp — the reference's own known-answer tests, re-run against the B200
+// drop-in headers (include/kvq/*.hpp -> libkvq_b200.so). Plain asserts (Catch2 is not
+// available); exit 0 = pass. Cited per case: /root/reference/proj/tests/*.cpp.
+#include <cmath>
+#include <cstdio>
+#include <random>
+#include <vector>
+
+#include "kvq/kvq.hpp"
+
+using namespace kvq;
+
+static int g_fail = 0;
+#define CHECK(cond)                                                        \
+    do {                                                                   \
+        if (!(cond)) {                                                     \
+            std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond);    \
+            ++g_fail;                                                      \
+        }                                                                  \
+    } while (0)
+#define CHECK_THROWS(expr, type)                                           \
+    do {                                                                   \
+        bool caught = false;                                               \
+        try { (void)(expr); } catch (const type&) { caught = true; }       \
+        if (!caught) { std::printf("FAIL %s:%d: no " #type "\n", __FILE__, __LINE__); ++g_fail; } \
+    } while (0)
+
+static DenseMatrix random_matrix(std::mt19937_64& eng, std::size_t r, std::size_t c, float lo, float hi) {
+    std::uniform_real_distribution<float> d(lo, hi);
+    DenseMatrix m(r, c);
+    for (float& v : m.data) v = d(eng);
+    return m;
+}
+
+// double-precision attention (reference.hpp:26-54 restated)
+static std::vector<double> attention(std::span<const float> q, const DenseMatrix& k, const DenseMatrix& v) {
+    std::vector<double> s(k.rows);
+    double m = -1e300;
+    for (std::size_t j = 0; j < k.rows; ++j) {
+        double a = 0;
+        for (std::size_t c = 0; c < k.cols; ++c) a += (double)q[c] * k.at(j, c);
+        s[j] = a / std::sqrt((double)k.cols);
+        m = std::max(m, s[j]);
+    }
+    double sum = 0;
+    for (double& x : s) sum += (x = std::exp(x - m));
+    std::vector<double> out(v.cols, 0.0);
+    for (std::size_t c = 0; c < v.cols; ++c)
+        for (std::size_t j = 0; j < k.rows; ++j) out[c] += s[j] / sum * v.at(j, c);
+    return out;
+}
+
+int main() {
+    // test_bitpack.cpp:12-52, 126-140
+    CHECK(pack(std::vector<std::uint32_t>{3, 1, 0, 2}, 2, 8).bytes == std::vector<std::uint8_t>{210});
+    CHECK(pack(std::vector<std::uint32_t>{1, 0, 1, 1, 0, 0, 1, 0}, 1, 8).bytes[0] == 178);
+    {
+        PackedBuffer b = pack(std::vector<std::uint32_t>{1, 2, 3}, 4, 16);
+        CHECK(b.word_at(0) == 0x1230u && b.bytes[0] == 0x30 && b.bytes[1] == 0x12);
+        CHECK((unpack(b) == std::vector<std::uint32_t>{1, 2, 3}));
+    }
+    CHECK_THROWS(pack(std::vector<std::uint32_t>{4}, 2, 8), domain_error);
+    CHECK_THROWS(pack(std::vector<std::uint32_t>{1}, 3, 8), config_error);
+
+    // test_quantize.cpp:34-67
+    {
+        DenseMatrix m(2, 2, {1, 5, 3, 2});
+        ChannelStats s = compute_stats(m, QuantMode::channel_wise);
+        CHECK((s.alpha == std::vector<float>{1, 2}) && (s.beta == std::vector<float>{3, 5}));
+        ChannelStats gs = compute_stats(m, QuantMode::global);
+        CHECK((gs.alpha == std::vector<float>{1, 1}) && (gs.beta == std::vector<float>{5, 5}));
+        CHECK_THROWS(compute_stats(DenseMatrix(0, 3), QuantMode::channel_wise), domain_error);
+        auto q1 = [](float x, float a, float b, int bits) {
+            return unpack(quantize(DenseMatrix(1, 1, {x}), ChannelStats{{a}, {b}}, bits).codes)[0];
+        };
+        CHECK(q1(1.4f, 0, 3, 2) == 1 && q1(0.1f, -2, 2, 1) == 1);
+        CHECK(q1(0.5f, 0, 3, 2) == 1 && q1(1.5f, 0, 3, 2) == 2 && q1(2.5f, 0, 3, 2) == 3);
+        CHECK(q1(99.f, -1.5f, 2.5f, 4) == 15 && q1(-99.f, -1.5f, 2.5f, 4) == 0);
+    }
+
+    // test_kernels.cpp:37-46, 111-121
+    {
+        QuantizedSegment seg = quantize(DenseMatrix(1, 2, {1, 0}), ChannelStats{{0, 0}, {1, 1}}, 1);
+        std::vector<float> q = {2, 3};
+        CHECK(qk_scores(q, seg, KernelConfig{})[0] == 2.0f);
+        std::mt19937_64 rng(6);
+        DenseMatrix m = random_matrix(rng, 9, 11, -2, 2);
+        QuantizedSegment s4 = quantize(m, compute_stats(m, QuantMode::channel_wise), 4);
+        DenseMatrix deq = dequantize(s4);
+        std::vector<float> w(9, 0.0f);
+        w[4] = 1.0f;
+        std::vector<float> out = wv_output(w, s4, KernelConfig{});
+        for (std::size_t c = 0; c < 11; ++c) CHECK(out[c] == deq.at(4, c));
+        CHECK_THROWS(qk_scores(std::vector<float>(3), s4, KernelConfig{}), domain_error);
+        CHECK_THROWS(qk_scores(std::vector<float>(11), s4, KernelConfig{0, 1, 1}), config_error);
+    }
+
+    // test_calibrate.cpp:60-66, 134-147
+    {
+        ScoreRange r{0.0f, 10.0f};
+        CalibrationParams p{2.0f, 1.0f};
+        CHECK(g_apply(0.0f, r, p) == -2.0f && g_apply(10.0f, r, p) == 9.0f && g_apply(5.0f, r, p) == 3.5f);
+        std::vector<float> got = calibrated_softmax_concat(std::vector<float>{0, 10}, std::vector<float>{9}, p);
+        std::vector<float> want = softmax_row(std::vector<float>{-2, 9, 9});
+        for (int i = 0; i < 3; ++i) CHECK(std::abs(got[i] - want[i]) <= 1e-6f);
+        std::size_t viol = 0;
+        calibrated_softmax_concat(std::vector<float>{0.0f, 1e-4f}, {}, CalibrationParams{0, 3}, &viol);
+        CHECK(viol == 1);
+    }
+
+    // test_kvcache.cpp:82-110 (8-bit decode tracks the oracle through appends), 112-140
+    // (append never touches codes), 161-182 (weights sum to 1), 272-293 (memory law)
+    {
+        std::mt19937_64 rng(2);
+        const std::size_t h = 2, n = 48, d = 12;
+        std::vector<DenseMatrix> ks, vs;
+        for (std::size_t i = 0; i < h; ++i) {
+            ks.push_back(random_matrix(rng, n, d, 4, 12));
+            vs.push_back(random_matrix(rng, n, d, 4, 12));
+        }
+        HybridKVCache cache = HybridKVCache::build(ks, vs, QuantizationConfig{8, QuantMode::channel_wise, 8},
+                                                   CalibrationParams{});
+        std::vector<std::uint8_t> before = cache.key_segment(0).codes.bytes;
+        std::vector<DenseMatrix> fk = ks, fv = vs;
+        for (int step = 0; step < 6; ++step) {
+            DenseMatrix kn = random_matrix(rng, h, d, 4, 12), vn = random_matrix(rng, h, d, 4, 12);
+            cache.append(kn, vn);
+            for (std::size_t i = 0; i < h; ++i) {
+                fk[i].append_row(kn.row_span(i));
+                fv[i].append_row(vn.row_span(i));
+            }
+            DenseMatrix q = random_matrix(rng, h, d, -0.5f, 0.5f);
+            DenseMatrix out = cache.decode_step(q);
+            for (std::size_t i = 0; i < h; ++i) {
+                std::vector<double> want = attention(q.row_span(i), fk[i], fv[i]);
+                for (std::size_t c = 0; c < d; ++c)
+                    CHECK(std::abs(out.at(i, c) - want[c]) <= 1e-3 * std::max(std::abs(want[c]), 1e-6));
+            }
+            DecodeDetail det = cache.decode_step_detailed(q);
+            for (std::size_t i = 0; i < h; ++i) {
+                double sum = 0;
+                for (float w : det.weights.row_span(i)) sum += w;
+                CHECK(std::abs(sum - 1.0) <= 1e-5);
+            }
+        }
+        CHECK(cache.key_segment(0).codes.bytes == before);
+        CHECK(cache.vis_tokens() == n && cache.tail_tokens() == 6);
+        CHECK_THROWS(cache.append(DenseMatrix(h, d + 1), DenseMatrix(h, d + 1)), domain_error);
+    }
+    {
+        std::mt19937_64 rng(9);
+        DenseMatrix k = random_matrix(rng, 1024, 64, -1, 1);
+        HybridKVCache cache = HybridKVCache::build(std::vector<DenseMatrix>{k}, std::vector<DenseMatrix>{k},
+                                                   QuantizationConfig{1, QuantMode::channel_wise, 8}, CalibrationParams{});
+        CHECK(cache.memory().quantized_bytes == 17408);
+        CHECK_THROWS(HybridKVCache::build(std::vector<DenseMatrix>{k}, std::vector<DenseMatrix>{k},
+                                          QuantizationConfig{3, QuantMode::channel_wise, 8}, CalibrationParams{}),
+                     config_error);
+    }
+    // d = 128 tensor-core path through the drop-in: 1-bit, calibration, vs a generic-path
+    // twin of the same cache (same codes, different kernels).
+    {
+        std::mt19937_64 rng(12);
+        std::vector<DenseMatrix> ks, vs;
+        for (int i = 0; i < 2; ++i) {
+            ks.push_back(random_matrix(rng, 700, 128, -2, 2));
+            vs.push_back(random_matrix(rng, 700, 128, -2, 2));
+        }
+        HybridKVCache a = HybridKVCache::build(ks, vs, QuantizationConfig{1, QuantMode::channel_wise, 8},
+                                               CalibrationParams{1, 0});
+        DenseMatrix q = random_matrix(rng, 2, 128, -1, 1);
+        DenseMatrix fast = a.decode_step(q);
+        DenseMatrix slow = a.decode_step_detailed(q).outputs;  // generic path (weights export)
+        double err = 0, norm = 0;
+        for (std::size_t i = 0; i < fast.data.size(); ++i) {
+            err += (fast.data[i] - slow.data[i]) * (double)(fast.data[i] - slow.data[i]);
+            norm += (double)slow.data[i] * slow.data[i];
+        }
+        CHECK(std::sqrt(err / norm) <= 1e-4);
+    }
+    std::printf(g_fail ? "test_dropin: %d failures\n" : "test_dropin: all passed%.0d\n", g_fail);
+    return g_fail ? 1 : 0;
+}
