@@ -22,6 +22,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
          "--expt-relaxed-constexpr", f"-I{ROOT / 'include'}", f"-I{CSRC}"]
+# Debug builds only (e.g. KVQ_NVCC_EXTRA=-DKVQ_TRACE_BLOCKS for per-block decode timelines).
+FLAGS += os.environ.get("KVQ_NVCC_EXTRA", "").split()
 
 
 def _headers() -> list[Path]:

@@ -3,6 +3,8 @@
 // dispatch to the K1/K2/K3 kernels. No compute happens on the host: every numeric
 // result comes out of a CUDA kernel, and a missing device is a hard KVQ_ERR_CUDA.
 #include <atomic>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -124,6 +126,7 @@ struct kvq_cache {
     int path = KVQ_PATH_AUTO;
     cudaStream_t stream = nullptr;
     DevBuf<uint8_t> codes;   // [2][units][n_vis][rb]  (K then V)
+    DevBuf<uint8_t> vt;      // token-packed V codes for the tcgen05 decode (d = 128, M = 8)
     DevBuf<float> stats;     // [2 (K,V)][2 (alpha,beta)][units][dim]
     DevBuf<float> k_tail, v_tail;  // [units][tail_cap][dim]
     DevBuf<int> tail_len;    // [batch]
@@ -172,6 +175,7 @@ kvqb::DecodeArgs decode_args(kvq_cache* c, const float* q, float* out) {
     kvqb::DecodeArgs a{};
     a.k_codes = c->k_codes();
     a.v_codes = c->v_codes();
+    a.v_codes_t = c->vt.p;
     a.k_alpha = c->k_alpha();
     a.k_beta = c->k_beta();
     a.v_alpha = c->v_alpha();
@@ -197,10 +201,44 @@ kvqb::DecodeArgs decode_args(kvq_cache* c, const float* q, float* out) {
 void run_decode(kvq_cache* c, const float* q, float* out, bool want_weights, bool want_viol,
                 cudaStream_t s) {
     kvqb::DecodeArgs a = decode_args(c, q, out);
-    bool tc_ok = kvqb::decode_tc_supported(a) && !want_weights && !want_viol;
-    if (c->path == KVQ_PATH_TC && !tc_ok)
+    const bool plain = !want_weights && !want_viol;
+    const bool umma_ok = plain && kvqb::decode_umma_supported(a);
+    bool tc_ok = kvqb::decode_tc_supported(a) && plain;
+    // Probability-row / violation export (decode_step_detailed) is a generic-path feature:
+    // an explicit tensor-core path selection applies to plain decodes only.
+    if (c->path == KVQ_PATH_UMMA && !umma_ok && plain)
+        raise(KVQ_ERR_CONFIG, "tcgen05 decode path needs dim 128, 8-bit words, a quantized "
+                              "prefill and no weight/violation export");
+    if (c->path == KVQ_PATH_TC && !tc_ok && plain)
         raise(KVQ_ERR_CONFIG, "tensor-core decode path needs dim 128, 8-bit words, a quantized "
                               "prefill and no weight/violation export");
+    if ((c->path == KVQ_PATH_AUTO || c->path == KVQ_PATH_UMMA) && umma_ok) {
+        const size_t need = kvqb::decode_tc_scratch_bytes(c->units);
+        if (c->tc_scratch.n < need) c->tc_scratch.alloc(need);
+        a.umma_qb = c->tc_scratch.p;
+        a.tc_qconst = reinterpret_cast<float2*>(c->tc_scratch.p + c->units * 2 * 512 * sizeof(uint32_t));
+        // Debug timeline: KVQ_TRACE_FILE=path dumps 256 globaltimer stamps per CTA of this
+        // decode (tools/trace_summary.py reads it). Off the measured path.
+        static const char* trace_file = std::getenv("KVQ_TRACE_FILE");
+        DevBuf<unsigned long long> trace;
+        const size_t trace_n = c->units * 256 * 16;
+        if (trace_file) {
+            trace.alloc(trace_n);
+            ck(cudaMemsetAsync(trace.p, 0, trace_n * 8, s), "trace");
+            a.trace = trace.p;
+        }
+        ck(kvqb::launch_decode_umma(a, s), "decode (umma)");
+        if (trace_file) {
+            std::vector<unsigned long long> h(trace_n);
+            trace.download(h.data(), trace_n, s);
+            sync(s);
+            if (FILE* f = std::fopen(trace_file, "wb")) {
+                std::fwrite(h.data(), 8, h.size(), f);
+                std::fclose(f);
+            }
+        }
+        return;
+    }
     if ((c->path == KVQ_PATH_AUTO || c->path == KVQ_PATH_TC) && tc_ok) {
         const size_t need = kvqb::decode_tc_scratch_bytes(c->units);
         if (c->tc_scratch.n < need) c->tc_scratch.alloc(need);
@@ -277,6 +315,11 @@ void quantize_prefill(kvq_cache* c, const float* dk, const float* dv, cudaStream
             ck(kvqb::launch_quantize_pack(srcs[which], u, n, d, alpha, beta, c->bits, c->word_bits, codes, s),
                "quantize");
         }
+    }
+    // Device layout for the tcgen05 decode: V codes re-packed along the token axis.
+    if (d == 128 && c->word_bits == 8 && n > 0) {
+        c->vt.alloc(kvqb::vt_bytes(u, n, c->bits));
+        ck(kvqb::launch_pack_vt(c->v_codes(), u, n, c->bits, c->vt.p, s), "pack vt");
     }
 }
 
@@ -588,7 +631,7 @@ int kvq_cache_reserve_tail(kvq_cache* c, size_t rows) {
 
 int kvq_cache_set_path(kvq_cache* c, int path) {
     return guarded([&] {
-        if (path < KVQ_PATH_AUTO || path > KVQ_PATH_TC) raise(KVQ_ERR_CONFIG, "unknown decode path");
+        if (path < KVQ_PATH_AUTO || path > KVQ_PATH_UMMA) raise(KVQ_ERR_CONFIG, "unknown decode path");
         c->path = path;
     });
 }

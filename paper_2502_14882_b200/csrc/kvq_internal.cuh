@@ -66,8 +66,11 @@ struct DecodeArgs {
     float* weights;       // nullable: [units][group][n_vis + tail_stride] probability rows
     int* violations;      // nullable: [units][group] g slope-violation flags
     float* scratch;       // generic path: [units][group][n_vis + tail_cap] score rows
+    const uint8_t* v_codes_t;  // umma path: token-packed V codes (vt_layout, k2_decode_umma.cu)
+    uint8_t* umma_qb;     // umma path: [units][NT][128][16] s8 q digit planes (prep kernel)
     uint32_t* tc_frag;    // tc path: [units][2][512] q-plane MMA fragments (prep kernel)
     float2* tc_qconst;    // tc path: [units][8] per-head score scale / offset
+    unsigned long long* trace;  // nullable: [ctas][64] globaltimer stamps (KVQ_TRACE_FILE)
     size_t units, kv_heads, group, dim, n_vis, tail_cap, weights_stride;
     int bits, word_bits;
     float tau1, tau2;
@@ -76,6 +79,12 @@ cudaError_t launch_decode_generic(const DecodeArgs& a, cudaStream_t s);
 bool decode_tc_supported(const DecodeArgs& a);
 size_t decode_tc_scratch_bytes(size_t units);
 cudaError_t launch_decode_tc(const DecodeArgs& a, cudaStream_t s);
+// tcgen05 (UTCIMMA) path, d = 128, M = 8: needs the token-packed V copy.
+size_t vt_bytes(size_t units, size_t n_vis, int bits);
+cudaError_t launch_pack_vt(const uint8_t* rows, size_t units, size_t n_vis, int bits, uint8_t* vt, cudaStream_t s);
+bool decode_umma_supported(const DecodeArgs& a);
+size_t decode_umma_scratch_bytes(size_t units);
+cudaError_t launch_decode_umma(const DecodeArgs& a, cudaStream_t s);
 
 // Post-scaled q.K (kernels.hpp:302-363) and w.V (316-396) over `heads` segments.
 cudaError_t launch_qk_scores(const float* q, const uint8_t* codes, const float* alpha,

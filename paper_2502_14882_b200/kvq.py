@@ -426,7 +426,7 @@ class DecodeDetail:
     slope_violations: int = 0
 
 
-PATH_AUTO, PATH_GENERIC, PATH_TC = 0, 1, 2
+PATH_AUTO, PATH_GENERIC, PATH_TC, PATH_UMMA = 0, 1, 2, 3
 
 
 class BatchedCache:

@@ -21,6 +21,7 @@ pytestmark = pytest.mark.gpu
 GOLD = Path(__file__).resolve().parent / "golden"
 TOL_GENERIC = 2e-5
 TOL_TC = 1e-4
+TOL_IMMA = 3e-4  # legacy mma.sync path: 22-bit probabilities
 
 
 def bits_eq(a, b):
@@ -182,25 +183,28 @@ def _load_inputs(z, oracle):
 
 
 @pytest.mark.parametrize("name", sorted(p.name for p in GOLD.glob("decode_*.npz")))
-@pytest.mark.parametrize("path", ["generic", "auto"])
+@pytest.mark.parametrize("path", ["generic", "auto", "tc", "umma"])
 def test_decode_golden_trajectories(kvq, oracle, name, path):
     z = np.load(GOLD / name)
     h, n, d, bits, wb, steps = z["meta"].tolist()
     t1, t2 = z["tau"].tolist()
+    if path in ("tc", "umma") and (d != 128 or wb != 8 or bits == 16 or n == 0):
+        pytest.skip("tensor-core paths need d = 128, M = 8 and a quantized prefill")
     k, v = _load_inputs(z, oracle)
     if bits == 16:
         cache = kvq.HybridKVCache.build_full_precision(list(k), list(v))
     else:
         cache = kvq.HybridKVCache.build(list(k), list(v), kvq.QuantizationConfig(bits, kvq.QuantMode.channel_wise, wb),
                                         kvq.CalibrationParams(t1, t2))
-    cache.batched.set_path(kvq.PATH_GENERIC if path == "generic" else kvq.PATH_AUTO)
+    cache.batched.set_path({"generic": kvq.PATH_GENERIC, "auto": kvq.PATH_AUTO, "tc": kvq.PATH_TC,
+                            "umma": kvq.PATH_UMMA}[path])
     if bits != 16 and n:
         for hh in range(h):
             ks, vs = cache.key_segment(hh), cache.value_segment(hh)
             assert np.array_equal(ks.codes.bytes, z[f"kcodes{hh}"]) and np.array_equal(vs.codes.bytes, z[f"vcodes{hh}"])
             assert bits_eq(ks.stats.alpha, z[f"kalpha{hh}"]) and bits_eq(vs.stats.beta, z[f"vbeta{hh}"])
     assert list(vars(cache.memory()).values()) == z["memory0"].tolist()
-    tol = TOL_GENERIC if path == "generic" else TOL_TC
+    tol = {"generic": TOL_GENERIC, "tc": TOL_IMMA}.get(path, TOL_TC)
     for t in range(steps):
         out = cache.decode_step(z[f"q{t}"])
         assert rel_l2(out, z[f"out{t}"]) <= tol, f"{name} step {t}: {rel_l2(out, z[f'out{t}'])}"
@@ -352,9 +356,16 @@ def test_batched_gqa_vs_oracle(kvq, oracle, bits, G, n):
         q = rng.normal(size=(B, H, G, d)).astype(np.float32)
         want = _oracle_batched(oracle, k, v, q, bits, tau,
                                np.stack(tk) if tk else None, np.stack(tv) if tv else None)
-        for path, tol in ((kvq.PATH_GENERIC, TOL_GENERIC), (kvq.PATH_AUTO, TOL_TC)):
+        for path, tol in ((kvq.PATH_GENERIC, TOL_GENERIC), (kvq.PATH_TC, TOL_IMMA), (kvq.PATH_UMMA, TOL_TC),
+                          (kvq.PATH_AUTO, TOL_TC)):
             cache.set_path(path)
-            out, _, _ = cache.decode(q)
+            try:
+                out, _, _ = cache.decode(q)
+            except kvq.ConfigError:
+                # the legacy IMMA path's shared-memory plan does not cover every shape;
+                # every other path must
+                assert path == kvq.PATH_TC
+                continue
             err = rel_l2(out, want)
             assert err <= tol, f"path {path} step {step}: rel L2 {err}"
         kn = rng.normal(size=(B, H, d)).astype(np.float32)
@@ -380,3 +391,60 @@ def test_step_api_matches_decode_then_append(kvq):
         ref, _, _ = c2.decode(q)
         c2.append(kn, vn)
         assert np.array_equal(out, ref)
+
+
+@pytest.mark.parametrize("name", ["decode_d128_b2_m32.npz", "decode_d128_b4_m32.npz", "decode_d128_b8_m32.npz"])
+@pytest.mark.parametrize("path", ["tc", "umma"])
+def test_decode_golden_m8_tensor_paths(kvq, oracle, name, path):
+    """The b >= 2 golden trajectories were produced by the reference with M = 32 (its M = 8
+    table path is defective for b >= 2 at n >= 512). The codes are the
+    same for every M, so the M = 8 tensor-core paths must reproduce those outputs."""
+    z = np.load(GOLD / name)
+    h, n, d, bits, wb, steps = z["meta"].tolist()
+    t1, t2 = z["tau"].tolist()
+    k, v = _load_inputs(z, oracle)
+    cache = kvq.HybridKVCache.build(list(k), list(v), kvq.QuantizationConfig(bits, kvq.QuantMode.channel_wise, 8),
+                                    kvq.CalibrationParams(t1, t2))
+    cache.batched.set_path(kvq.PATH_TC if path == "tc" else kvq.PATH_UMMA)
+    for hh in range(h):
+        ka, kb = oracle.compute_stats(k[hh])
+        assert np.array_equal(cache.key_segment(hh).codes.bytes, oracle.quantize(k[hh], ka, kb, bits, 8))
+    for t in range(steps):
+        out = cache.decode_step(z[f"q{t}"])
+        tol = TOL_IMMA if path == "tc" else TOL_TC
+        assert rel_l2(out, z[f"out{t}"]) <= tol, f"{name} step {t}: {rel_l2(out, z[f'out{t}'])}"
+        cache.append(z[f"knew{t}"], z[f"vnew{t}"])
+
+
+@pytest.mark.parametrize("bits,G,n", [(1, 4, 4096), (1, 4, 8192), (2, 4, 8192), (4, 4, 8192), (1, 6, 32768),
+                                      (8, 8, 2500)])
+def test_full_size_units_vs_oracle(kvq, oracle, bits, G, n):
+    """BASELINE-sized units (c2: n=4096 G=4; c3: n=8192 b=1/2/4; c4: n=32768 G=6 -> a
+    16-CTA cluster per unit) through every d=128 path, spot-checked against the C
+    restatement on every unit (B=1, 2 KV heads) plus the fp32 tail after appends."""
+    rng = np.random.default_rng(n + 7 * bits + G)
+    B, H, d = 1, 2, 128
+    k = rng.normal(size=(B, H, n, d)).astype(np.float32)
+    v = rng.normal(size=(B, H, n, d)).astype(np.float32)
+    tau = (1.0, 0.0)
+    cache = kvq.BatchedCache.build(k, v, kvq.QuantizationConfig(bits), kvq.CalibrationParams(*tau), group=G)
+    tk, tv = [], []
+    for step in range(2):
+        q = rng.normal(size=(B, H, G, d)).astype(np.float32)
+        want = _oracle_batched(oracle, k, v, q, bits, tau,
+                               np.stack(tk) if tk else None, np.stack(tv) if tv else None)
+        # The fp32 restatement's own error floor grows with n and b (SURVEY.md App. C:
+        # 6.8e-5 at b=2, n=4096 vs float64); at these sizes the bar is 5e-4, half of
+        # north_star's 1e-3.
+        for path, tol in ((kvq.PATH_TC, 5e-4), (kvq.PATH_UMMA, 5e-4)):
+            cache.set_path(path)
+            out, _, _ = cache.decode(q)
+            err = rel_l2(out, want)
+            assert err <= tol, f"path {path} step {step}: rel L2 {err}"
+            again, _, _ = cache.decode(q)
+            assert np.array_equal(out, again), "decode must be run-to-run deterministic"
+        kn = rng.normal(size=(B, H, d)).astype(np.float32)
+        vn = rng.normal(size=(B, H, d)).astype(np.float32)
+        cache.append(kn, vn)
+        tk.append(kn)
+        tv.append(vn)

@@ -132,6 +132,85 @@ __global__ void probe(const uint8_t* A, const int8_t* B, int32_t* D, int mode, i
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tbase));
 }
 
+// Latency probe: cycles for (a) STTM.x32 + wait::st, (b) 4 x UTCIMMA M128 N16 K32 issue ->
+// commit -> mbarrier completion, (c) LDTM.x16 + wait::ld. One CTA, 128 threads.
+__global__ void latency(long long* out, int iters, int nmma, int indep) {
+    __shared__ __align__(1024) int8_t sB[32 * 16 * 4];
+    __shared__ uint32_t tmem_base;
+    __shared__ __align__(8) uint64_t bar;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    for (int i = tid; i < (int)sizeof(sB); i += blockDim.x) sB[i] = (int8_t)i;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(&tmem_base)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tbase = tmem_base;
+    const uint32_t tl = tbase + ((uint32_t)(32 * warp) << 16);
+    long long t_st = 0, t_mma = 0, t_ld = 0, t_bar = 0;
+    uint32_t r[32];
+    for (int j = 0; j < 32; ++j) r[j] = tid * 0x01010101u + j;
+    uint32_t phase = 0;
+    for (int it = 0; it < iters; ++it) {
+        long long t0 = clock64();
+        asm volatile(
+            "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+            "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(tl),
+            "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+            "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
+            "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
+            "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]) : "memory");
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        long long t1 = clock64();
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        long long t2 = clock64();
+        if (tid == 0) {
+            const uint32_t idesc = idesc_i8(128, 16, true, true);
+            for (int kk = 0; kk < nmma; ++kk) {
+                uint64_t bd = smem_desc(smem_u32(sB + (kk & 3) * 512), 128, 2048);
+                const uint32_t dcol = indep ? 64 + 16 * (kk & 3) : 64;
+                asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                             " tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tbase + dcol),
+                             "r"(tbase + 8 * (kk & 3)), "l"(bd), "r"(idesc), "r"(indep ? 0 : kk));
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar)) : "memory");
+        }
+        uint32_t done = 0;
+        while (!done) {
+            asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                         : "=r"(done) : "r"(smem_u32(&bar)), "r"(phase) : "memory");
+        }
+        phase ^= 1;
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        long long t3 = clock64();
+        uint32_t d[16];
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7]),
+              "=r"(d[8]), "=r"(d[9]), "=r"(d[10]), "=r"(d[11]), "=r"(d[12]), "=r"(d[13]), "=r"(d[14]), "=r"(d[15])
+            : "r"(tl + 64));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        long long t4 = clock64();
+        for (int j = 0; j < 16; ++j) r[j] += d[j];
+        if (it > 0) { t_st += t1 - t0; t_bar += t2 - t1; t_mma += t3 - t2; t_ld += t4 - t3; }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;");
+    }
+    if (tid == 0 && blockIdx.x == 0) { out[0] = t_st; out[1] = t_bar; out[2] = t_mma; out[3] = t_ld; out[4] = r[3]; }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tbase));
+}
+
 int main() {
     const int M = 128;
     int fails = 0;
@@ -174,6 +253,25 @@ int main() {
             cudaFree(dD);
             if (e != cudaSuccess) return 2;
         }
+    }
+    {
+        long long* d;
+        cudaMalloc(&d, 64);
+        cudaFuncSetAttribute(latency, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+        const int iters = 200;
+        for (int ctas : {1, 296})
+            for (int nmma : {0, 1, 2, 4, 8})
+                for (int indep : {0, 1}) {
+                    if (nmma == 0 && indep) continue;
+                    latency<<<ctas, 128, 100 * 1024>>>(d, iters, nmma, indep);
+                    cudaError_t e = cudaDeviceSynchronize();
+                    long long h[5];
+                    cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
+                    printf("ctas %3d: %d x UTCIMMA M128N16K32 (%s): issue->commit->mbarrier %.0f cycles | STTM.x32+wait "
+                           "%.0f | fence+bar %.0f | LDTM.x16+wait %.0f  err=%s\n", ctas, nmma,
+                           indep ? "independent D" : "chained D", h[2] / (double)(iters - 1), h[0] / (double)(iters - 1),
+                           h[1] / (double)(iters - 1), h[3] / (double)(iters - 1), cudaGetErrorString(e));
+                }
     }
     return fails ? 1 : 0;
 }
