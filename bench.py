@@ -53,6 +53,7 @@ CONFIGS = {
     "c5b512": (512, 8, 4, 4096, 1, (1.0, 0.0), "BASELINE c5: batch 512, 4096 visual tokens, 1-bit"),
 }
 DIM = 128
+PATHS = {"auto": 0, "generic": 1, "tc": 2, "umma": 3}  # KVQ_PATH_* (include/kvq_capi.h)
 TAIL_WINDOW = 32
 L2_BYTES = 126 * 1024 * 1024
 
@@ -200,6 +201,7 @@ def run_ours(args, world, rank, local):
     cache_bytes = units * (2 * n * DIM * bits // 8 + 16 * DIM)
     total_steps = W + K + args.e2e_steps
     R = max(2, -(-total_steps // TAIL_WINDOW), -(-(3 * L2_BYTES) // cache_bytes))
+    tail_cap = -(-(total_steps + 2 * R) // R) + 3  # per replica: warm-up + timed + e2e appends
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
     kv_chunk = max(1, min(batch, (1 << 31) // (H * n * DIM * 4)))  # bound the fp32 staging to ~2 GiB
@@ -210,7 +212,8 @@ def run_ours(args, world, rank, local):
         for r in range(R):
             c = kvq.BatchedCache.build_device(k, v, kvq.QuantizationConfig(bits), kvq.CalibrationParams(*tau),
                                               group=G, stream=sptr)
-            c.reserve_tail(-(-total_steps // R) + 1)
+            c.reserve_tail(tail_cap)
+            c.set_path(PATHS[args.path])
             caches.append(c)
         del k, v
         q = [torch.randn((batch, H, G, DIM), device=dev, generator=gen) for _ in range(4)]
@@ -223,14 +226,39 @@ def run_ours(args, world, rank, local):
 
     tails = [0] * R
 
+    # Eager warm-up (allocates the decode scratch), then one CUDA graph per replica for
+    # each half of the step: [prep + K2 decode] and [K3 append]. Graph replays remove the
+    # host launch overhead (ctypes + C-ABI) from the timed region; events between the two
+    # graph launches time the decode alone.
+    for t in range(R):
+        caches[t].decode_device(q[t % 4], out, sptr)
+        caches[t].append_device(kn[t % 4], vn[t % 4], sptr)
+        tails[t] += 1
+    stream.synchronize()
+    g_dec, g_app = [], []
+    launches_dec = launches_app = 0
+    for r in range(R):
+        gd, ga = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        l0 = kvq.launch_count()
+        with torch.cuda.graph(gd, stream=stream):
+            caches[r].decode_device(q[r % 4], out, sptr)
+        l1 = kvq.launch_count()
+        with torch.cuda.graph(ga, stream=stream):
+            caches[r].append_device(kn[r % 4], vn[r % 4], sptr)
+        launches_dec, launches_app = l1 - l0, kvq.launch_count() - l1
+        g_dec.append(gd)
+        g_app.append(ga)
+
     def step(t, ev=None):
         r = t % R
         if ev is not None:
             ev[0].record(stream)
-        caches[r].decode_device(q[t % 4], out, sptr)
+        with torch.cuda.stream(stream):
+            g_dec[r].replay()
         if ev is not None:
             ev[1].record(stream)
-        caches[r].append_device(kn[t % 4], vn[t % 4], sptr)
+        with torch.cuda.stream(stream):
+            g_app[r].replay()
         tails[r] += 1
 
     for t in range(W):
@@ -241,10 +269,13 @@ def run_ours(args, world, rank, local):
     dec_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     bytes_alg = 0
-    launches0 = kvq.launch_count()
     sampler = ClockSampler(local)
     with sampler:
         torch.cuda.synchronize()
+        # Let the host run ahead: a ~20 ms spin on the stream (before the timed region)
+        # while all K steps are enqueued, so no launch gap lands inside an event interval.
+        with torch.cuda.stream(stream):
+            torch.cuda._sleep(int(4e7))
         start.record(stream)
         for i in range(K):
             t = W + i
@@ -252,7 +283,8 @@ def run_ours(args, world, rank, local):
             step(t, dec_ev[i])
         stop.record(stream)
         stream.synchronize()
-    launches = kvq.launch_count() - launches0
+    launches = K * (launches_dec + launches_app)
+    assert max(tails) <= tail_cap, "bench tail accounting exceeded the reserved capacity"
     elapsed_ms = start.elapsed_time(stop)
     dec_ms = [a.elapsed_time(b) for a, b in dec_ev]
     if world > 1:
@@ -314,7 +346,7 @@ def run_ours(args, world, rank, local):
                        "kv_heads": H, "head_dim": DIM, "n_vis": n, "bits": bits, "tau": list(tau),
                        "tail_window": TAIL_WINDOW, "parallelism": f"units sharded x{world} (no collective)",
                        "l2": f"inputs larger than L2: {R} rotating cache replicas x {cache_bytes / 2**20:.1f} MiB",
-                       "step": "K2 decode (all q heads) + K3 append"},
+                       "step": "K2 decode (all q heads) + K3 append", "decode_path": args.path},
             "hbm_gbs": bytes_alg / K / (ms_per_step * 1e-3) / 1e9,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
@@ -341,6 +373,8 @@ def main():
     ap.add_argument("--cpu-requests", type=int, default=16)
     ap.add_argument("--steps-cpu", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--path", default=os.environ.get("KVQ_PATH", "auto"), choices=sorted(PATHS),
+                    help="K2 decode kernel: auto, tc (mma.sync IMMA), umma (tcgen05), generic")
     args = ap.parse_args()
     world, rank, local = dist_setup(args)
     if args.impl == "reference":

@@ -41,7 +41,7 @@ extern "C" {
 #define KVQ_MODE_GLOBAL 1       /* QuantMode::global */
 #define KVQ_FULL_PRECISION_BITS 16 /* kvcache.hpp:26 */
 
-#define KVQ_PATH_AUTO 0    /* tcgen05 path when the shape allows, else IMMA, else generic */
+#define KVQ_PATH_AUTO 0    /* IMMA path when the shape allows, else tcgen05, else generic */
 #define KVQ_PATH_GENERIC 1 /* any shape; also the path that emits probability rows */
 #define KVQ_PATH_TC 2      /* d = 128, M = 8 legacy mma.sync IMMA path (KVQ_ERR_CONFIG otherwise) */
 #define KVQ_PATH_UMMA 3    /* d = 128, M = 8 tcgen05 UTCIMMA path (KVQ_ERR_CONFIG otherwise) */

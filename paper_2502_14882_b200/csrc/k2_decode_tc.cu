@@ -226,52 +226,63 @@ __global__ void __launch_bounds__(kDim) prep_kernel(DecodeArgs a, int NT, uint32
 constexpr int kWarps = 8;             // consumer warps per CTA
 constexpr int kWarpTokens = 512;      // visual tokens per warp (contiguous)
 constexpr int kCtaTokens = kWarps * kWarpTokens;
-constexpr int kTS = kWarpTokens + 36;  // score row stride (also holds 17 x 32 uint4 accumulators)
+constexpr int kSteps = kWarpTokens / 32;  // 32-token steps per warp
+
+// Per-warp TMA ring: ~10 KB in flight per warp (80 KB per CTA, two CTAs per SM) covers
+// the ~2 us bulk-copy latency measured under load (profiles/r01_trace_umma_c2.txt).
+template <int BITS>
+constexpr int ring_stages() {
+    return Geo<BITS>::kStageBytesB >= 4096 ? 3 : 5;
+}
 
 struct Smem {  // carve-up of the dynamic shared memory of one decode CTA
-    uint8_t* ring;       // [kWarps][kStages][kStageBytes]: per-warp TMA landing zones
-    float* scores;       // [kWarps][4 NT][kWarpTokens + 4]; reused for the accumulators
-    uint32_t* pw;        // [kWarps][NT][12][kPRow] p digit planes of a warp's current block
+    uint8_t* ring;       // [kWarps][kStages][kStageBytes]: per-warp TMA landing zones;
+                         // after the V stream: planes + the cluster receive buffer
+    uint32_t* acc;       // [NT][16 nc][32 lanes][4]: CTA sum of the warps' p.V accumulators
+    uint32_t* pw;        // [kWarps][2][NT][12][kPRow] p digit planes of a warp's block
     float* tail_s;       // [8][kTailMax] fp32 tail scores (rank 0)
     float* wpart;        // [kWarps][24] per-warp (min, max, tail max) per head
     float* allpart;      // [S][24] per-CTA partials (pushed by every CTA of the cluster)
     float* gpar;         // [8][4] softmax parameters per head
     uint32_t* wsum;      // [kWarps][8] per-warp u22 weight sums per head
-    float* recv;         // [S][8 * 128 + 8] rank 0: partial numerators / denominators
     uint64_t* full;      // [kWarps][kStages] TMA completion barriers
+    uint32_t* tmem_slot;
 };
 
-__host__ __device__ inline size_t tc_smem_bytes(int BITS, int NT, int S, Smem* out = nullptr, uint8_t* base = nullptr) {
+template <int BITS, int NT>
+__host__ __device__ inline size_t tc_smem_bytes(int S, Smem* out = nullptr, uint8_t* base = nullptr) {
     size_t off = 0;
     auto take = [&](size_t bytes) {
         size_t o = off;
-        off += (bytes + 15) & ~size_t(15);
+        off += (bytes + 127) & ~size_t(127);
         return base + o;
     };
-    const int stage = kStageBytes / (16 * BITS) >= 32 ? kStageBytes : 32 * 16 * BITS;
+    constexpr int stage = Geo<BITS>::kStageBytesB;
     const size_t planes_bytes = (size_t)3 * 4 * NT * (kDim + 1) * 4;
-    const size_t ring_bytes = (size_t)kWarps * kStages * stage;
-    uint8_t* ring = take(ring_bytes > planes_bytes ? ring_bytes : planes_bytes);
-    uint8_t* scores = take((size_t)kWarps * 4 * NT * kTS * 4);
+    const size_t recv_bytes = S > 1 ? (size_t)S * (8 * kDim + 8) * 4 : 0;
+    const size_t ring_bytes = (size_t)kWarps * ring_stages<BITS>() * stage;
+    const size_t tail_use = planes_bytes + recv_bytes;
+    uint8_t* ring = take(ring_bytes > tail_use ? ring_bytes : tail_use);
+    uint8_t* acc = take((size_t)NT * 16 * 32 * 4 * 4);
     uint8_t* pw = take((size_t)kWarps * 2 * NT * 12 * kPRow * 4);
     uint8_t* tail_s = take((size_t)8 * kTailMax * 4);
     uint8_t* wpart = take((size_t)kWarps * 24 * 4);
-    uint8_t* allpart = take((size_t)S * 24 * 4);
+    uint8_t* allpart = take((size_t)(S > 0 ? S : 1) * 24 * 4);
     uint8_t* gpar = take(32 * 4);
     uint8_t* wsum = take((size_t)kWarps * 8 * 4);
-    uint8_t* recv = take(S > 1 ? (size_t)S * (8 * kDim + 8) * 4 : 16);
-    uint8_t* full = take((size_t)kWarps * kStages * 8);
+    uint8_t* full = take((size_t)kWarps * ring_stages<BITS>() * 8);
+    uint8_t* slot = take(16);
     if (out) {
         out->ring = ring;
-        out->scores = reinterpret_cast<float*>(scores);
+        out->acc = reinterpret_cast<uint32_t*>(acc);
         out->pw = reinterpret_cast<uint32_t*>(pw);
         out->tail_s = reinterpret_cast<float*>(tail_s);
         out->wpart = reinterpret_cast<float*>(wpart);
         out->allpart = reinterpret_cast<float*>(allpart);
         out->gpar = reinterpret_cast<float*>(gpar);
         out->wsum = reinterpret_cast<uint32_t*>(wsum);
-        out->recv = reinterpret_cast<float*>(recv);
         out->full = reinterpret_cast<uint64_t*>(full);
+        out->tmem_slot = reinterpret_cast<uint32_t*>(slot);
     }
     return off;
 }
@@ -281,19 +292,43 @@ __device__ __forceinline__ void st_cluster_f32(float* local_ptr, int rank, float
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(addr) : "r"(smem_u32(local_ptr)), "r"(rank));
     asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
 }
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, float a, float b, float c, float d) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "r"(__float_as_uint(a)),
+                 "r"(__float_as_uint(b)), "r"(__float_as_uint(c)), "r"(__float_as_uint(d))
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, float (&v)[4]) {
+    uint32_t r0, r1, r2, r3;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    v[0] = __uint_as_float(r0), v[1] = __uint_as_float(r1), v[2] = __uint_as_float(r2), v[3] = __uint_as_float(r3);
+}
+__device__ __forceinline__ void red_add_u32(uint32_t* p, uint32_t v) {
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
 
 // CTA = 8 warps; warp w owns visual tokens [w*512, w*512+512) of the CTA's chunk and
-// streams them (K codes, then V codes) through its own 2-slot TMA ring, re-armed by its
-// lane 0. A unit of n visual tokens takes S = ceil(n / 4096) CTAs (a cluster); for
-// n <= 4096 there is no cluster traffic at all. Cross-warp reductions go through shared
-// memory (exact integer sums for the p.V accumulators); cross-CTA traffic is push-only.
+// streams them (K codes, then V codes) through its own TMA ring, re-armed by its lane 0.
+// A unit of n visual tokens takes S = ceil(n / 4096) CTAs (a cluster); for n <= 4096
+// there is no cluster traffic at all.
+//
+// Token order inside a 32-token step: the phase-A accumulator gives lane (g, t) the
+// scores of tokens {g, g+8, g+16, g+24} for head t. Phase B uses exactly those four
+// tokens as its k-group g (k = 4g + j <-> token 8j' ... see v_row below), so every lane
+// turns its own scores into probabilities: scores never leave the lane. They wait in
+// tensor memory (lane-private columns, tcgen05.st/ld) between the phases.
+// Cross-warp reductions of the p.V accumulators are exact integer shared-memory atomics
+// (deterministic); cross-CTA traffic is push-only.
 template <int BITS, int NT>
 __global__ void __launch_bounds__(kWarps * 32, 1) decode_tc_kernel(const TcParams p) {
     using Gm = Geo<BITS>;
+    constexpr int kStagesW = ring_stages<BITS>();
+    constexpr uint32_t kTmemCols = NT == 1 ? 128 : 256;  // 2 lane-sharing warps x 16 steps x 4 NT
     const DecodeArgs& a = p.a;
     const int G = (int)a.group;
     const int S = p.S;
-    constexpr int TS = kTS;
     const int rank = S > 1 ? (int)cg::this_cluster().block_rank() : 0;
     const int unit = blockIdx.x / S;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -301,10 +336,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_tc_kernel(const TcParam
 
     extern __shared__ __align__(128) uint8_t smem_raw[];
     Smem sm;
-    tc_smem_bytes(BITS, NT, S, &sm, smem_raw);
-    float* scores = sm.scores + warp * 4 * NT * TS;  // this warp's [4 NT][TS]
-    uint8_t* ring = sm.ring + warp * kStages * Gm::kStageBytesB;
-    uint64_t* full = sm.full + warp * kStages;
+    tc_smem_bytes<BITS, NT>(S, &sm, smem_raw);
+    uint8_t* ring = sm.ring + warp * kStagesW * Gm::kStageBytesB;
+    uint64_t* full = sm.full + warp * kStagesW;
 
     const int n = (int)a.n_vis;
     const int tok0 = rank * kCtaTokens + warp * kWarpTokens;  // this warp's first token
@@ -315,8 +349,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_tc_kernel(const TcParam
     const int nstage = (nv + Gm::kStageTokens - 1) / Gm::kStageTokens;
     const int total_stages = 2 * nstage;
 
-    auto issue = [&](int i) {  // lane 0: stage i (K stages, then V stages) into slot i % kStages
-        const int slot = i % kStages;
+    auto issue = [&](int i) {  // lane 0: stage i (K stages, then V stages) into slot i % kStagesW
+        const int slot = i % kStagesW;
         const int si = i < nstage ? i : i - nstage;
         const uint8_t* src = (i < nstage ? kcodes : vcodes) + (size_t)si * Gm::kStageBytesB;
         const uint32_t bytes = (uint32_t)(min(Gm::kStageTokens, nv - si * Gm::kStageTokens) * Gm::kRowBytes);
@@ -324,13 +358,31 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_tc_kernel(const TcParam
         bulk_g2s(ring + slot * Gm::kStageBytesB, src, bytes, &full[slot]);
     };
     if (lane == 0) {
-        for (int i = 0; i < kStages; ++i) mbar_init(&full[i], 1);
+        for (int i = 0; i < kStagesW; ++i) mbar_init(&full[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int i = 0; i < min(kStages, total_stages); ++i) issue(i);
+        for (int i = 0; i < min(kStagesW, total_stages); ++i) issue(i);
     }
-    __syncwarp();
+    // zero the CTA accumulator image; allocate the lane-private score columns
+    for (int i = threadIdx.x; i < NT * 16 * 32 * 4; i += kWarps * 32) sm.acc[i] = 0u;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(sm.tmem_slot)),
+                     "r"(kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tbase = *sm.tmem_slot;
+    // lanes of warp quarter (warp % 4); warps 4..7 use the upper half of the columns
+    const uint32_t tmem_w = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * kSteps * 4 * NT);
     if (S > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");  // #0
 
+    // Warm L2 with the fp32 tail rows (rank 0 reads them after phase A / in the epilogue).
+    for (int l = threadIdx.x; l < 8 * ntl; l += blockDim.x) {
+        const float* base = (l & 4) ? a.v_tail : a.k_tail;
+        const float* ptr = base + ((size_t)unit * a.tail_cap + (l >> 3)) * kDim + 32 * (l & 3);
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
+    }
     griddep_wait();  // prep kernel's q planes are visible from here on
     uint32_t bq[NT][2][4][2];  // [head group][digit-plane pair][k-block][reg]
     const uint32_t* fr = p.frag + (size_t)unit * NT * 512;
@@ -356,12 +408,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_tc_kernel(const TcParam
     // bytes (one LOP3 selects 4 codes x 2^sh), B = the q digit planes (registers). Lane
     // (g, t) ends with all four digit planes of head t for tokens g and g + 8.
     for (int st = 0; st < nstage; ++st) {
-        const int slot = st % kStages;
-        mbar_wait(&full[slot], (st / kStages) & 1);
+        const int slot = st % kStagesW;
+        mbar_wait(&full[slot], (st / kStagesW) & 1);
         const uint8_t* buf = ring + slot * Gm::kStageBytesB;
         const int ns = min(Gm::kStageTokens, nv - st * Gm::kStageTokens);
-        // Two 16-token MMA tiles per step; the epilogue of step k runs after the IMMAs of
-        // step k+1 are issued (software pipelining of the IMMA latency).
         int accA[NT][2][2][4], accB[NT][2][2][4];  // two pipeline slots: [head group][tile][plane pair]
         auto mma_step = [&](int tile, int (&ac)[NT][2][2][4]) {
             uint32_t areg[2][2][8];  // [tile][token g / g+8][slot register rho]
@@ -407,9 +457,11 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_tc_kernel(const TcParam
                                       areg[u2][1][2 * kb + 1], bq[hg][pp][kb][0], bq[hg][pp][kb][1]);
         };
         auto epilogue = [&](int tile, const int (&ac)[NT][2][2][4]) {
+            const int step = (st * Gm::kStageTokens + tile) >> 5;  // warp-local 32-token step
+            const int tbase_tok = st * Gm::kStageTokens + tile;
 #pragma unroll
             for (int hg = 0; hg < NT; ++hg) {
-                const int h = 4 * hg + t;
+                float sc[4];
 #pragma unroll
                 for (int u2 = 0; u2 < 2; ++u2) {
 #pragma unroll
@@ -417,15 +469,16 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_tc_kernel(const TcParam
                         // digit planes 0..3 of head t, token g (+8): wrapping int32 sum, exact total
                         const int total = ac[hg][u2][0][2 * hf] + ac[hg][u2][0][2 * hf + 1] * 256 +
                                           ac[hg][u2][1][2 * hf] * 65536 + ac[hg][u2][1][2 * hf + 1] * (1 << 24);
-                        const int tok = st * Gm::kStageTokens + tile + 16 * u2 + 8 * hf + g;
-                        if (h < G && tok < nv) {
-                            const float sc = __fmaf_rn((float)total, cA[hg], cB[hg]);
-                            scores[h * TS + tok] = sc;
-                            lo[hg] = fminf(lo[hg], sc);
-                            hi[hg] = fmaxf(hi[hg], sc);
+                        const int tok = tbase_tok + 16 * u2 + 8 * hf + g;
+                        const float s = __fmaf_rn((float)total, cA[hg], cB[hg]);
+                        sc[2 * u2 + hf] = s;
+                        if (tok < nv) {
+                            lo[hg] = fminf(lo[hg], s);
+                            hi[hg] = fmaxf(hi[hg], s);
                         }
                     }
                 }
+                tmem_st4(tmem_w + (uint32_t)((step * NT + hg) * 4), sc[0], sc[1], sc[2], sc[3]);
             }
         };
         const int nsteps = (ns + 31) >> 5;  // >= 1
@@ -445,26 +498,32 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_tc_kernel(const TcParam
             epilogue(32 * (k - 1), accA);
         }
         __syncwarp();
-        if (lane == 0 && st + kStages < total_stages) issue(st + kStages);
+        if (lane == 0 && st + kStagesW < total_stages) issue(st + kStagesW);
     }
-    // Head rows beyond G: finite scores (their softmax offset is -inf, so p = 0).
-    for (int h = G; h < 4 * NT; ++h)
-        for (int tk = lane; tk < ((nv + 31) & ~31); tk += 32) scores[h * TS + tk] = 0.0f;
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");  // scores are in tensor memory
 
-    // fp32 tail rows (rank 0, warp 0): lanes split the 128 channels.
+    // fp32 tail rows (rank 0): warp w takes rows w, w + NW, ...; lanes split the 128
+    // channels; q rows are loaded once.
     const float isd = __fdiv_rn(1.0f, sqrtf((float)kDim));
     float tmax = -INFINITY;  // for head (lane & 7)
-    if (warp == 0) {
-        for (int j = 0; j < ntl; ++j) {
-            const float4 kv = *reinterpret_cast<const float4*>(a.k_tail + ((size_t)unit * a.tail_cap + j) * kDim + 4 * lane);
-            for (int h = 0; h < G; ++h) {
-                const float4 qv = *reinterpret_cast<const float4*>(a.q + ((size_t)unit * G + h) * kDim + 4 * lane);
-                float d = kv.x * qv.x + kv.y * qv.y + kv.z * qv.z + kv.w * qv.w;
+    if (warp < kWarps && ntl > warp) {
+        float4 qv[8];
 #pragma unroll
-                for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-                d *= isd;
-                if (lane == 0) sm.tail_s[h * kTailMax + j] = d;
-                if ((lane & 7) == h) tmax = fmaxf(tmax, d);
+        for (int h = 0; h < 8; ++h)
+            qv[h] = h < G ? *reinterpret_cast<const float4*>(a.q + ((size_t)unit * G + h) * kDim + 4 * lane)
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int j = warp; j < ntl; j += kWarps) {
+            const float4 kv = *reinterpret_cast<const float4*>(a.k_tail + ((size_t)unit * a.tail_cap + j) * kDim + 4 * lane);
+#pragma unroll
+            for (int h = 0; h < 8; ++h) {
+                if (h < G) {
+                    float d = kv.x * qv[h].x + kv.y * qv[h].y + kv.z * qv[h].z + kv.w * qv[h].w;
+#pragma unroll
+                    for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+                    d *= isd;
+                    if (lane == 0) sm.tail_s[h * kTailMax + j] = d;
+                    if ((lane & 7) == h) tmax = fmaxf(tmax, d);
+                }
             }
         }
     }
@@ -489,14 +548,14 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_tc_kernel(const TcParam
     if (lane < 24) sm.wpart[warp * 24 + lane] = mine;
     __syncthreads();
     if (threadIdx.x < 24) {  // CTA partial
-        const int k = threadIdx.x;
-        float v = sm.wpart[k];
-        for (int w2 = 1; w2 < kWarps; ++w2) v = k < 8 ? fminf(v, sm.wpart[w2 * 24 + k]) : fmaxf(v, sm.wpart[w2 * 24 + k]);
+        const int kk = threadIdx.x;
+        float v = sm.wpart[kk];
+        for (int w2 = 1; w2 < kWarps; ++w2) v = kk < 8 ? fminf(v, sm.wpart[w2 * 24 + kk]) : fmaxf(v, sm.wpart[w2 * 24 + kk]);
         if (S > 1) {
             asm volatile("barrier.cluster.wait.acquire;" ::: "memory");  // #0 (non-aligned: one warp)
-            for (int r = 0; r < S; ++r) st_cluster_f32(sm.allpart + rank * 24 + k, r, v);
+            for (int r = 0; r < S; ++r) st_cluster_f32(sm.allpart + rank * 24 + kk, r, v);
         } else {
-            sm.allpart[k] = v;
+            sm.allpart[kk] = v;
         }
     }
     if (S > 1) {
@@ -528,18 +587,20 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_tc_kernel(const TcParam
         } else {
             m = fmaxf(m, __fsub_rn(gamma, a.tau1));
         }
-        sm.gpar[h * 4 + 0] = A * kLog2e;
-        sm.gpar[h * 4 + 1] = (B - m) * kLog2e;
+        const bool live = h < G;
+        sm.gpar[h * 4 + 0] = live ? A * kLog2e : 0.0f;
+        sm.gpar[h * 4 + 1] = live ? (B - m) * kLog2e : -INFINITY;
         sm.gpar[h * 4 + 2] = -m * kLog2e;
     }
     __syncthreads();
 
     // ---------------- phase B: p . V over this warp's tokens ----------------
     // D[16 head-planes x 8 ch] += P[16 head-planes x 32 tok] * V[32 tok x 8 ch], 16 channel
-    // tiles per 32-token block. p = exp(g(s) - m) in [0, 1] is a 22-bit integer split in
-    // three u8 planes (A rows plane*4 + head), written once per (head, token) to a smem
-    // tile in MMA k-order. V codes are the B operand: four tokens per register (PRMT byte
-    // transpose) x 2^sh (LOP3 slot select) - never dequantized.
+    // tiles per 32-token block. Lane (g, t) turns its own four scores of head t (tokens
+    // g, g+8, g+16, g+24 = k-group g) into p = exp(g(s) - m) in [0, 1], a 22-bit integer
+    // split in three u8 planes, and writes them as one word per plane of the P tile (A
+    // rows plane*4 + head, k-group word g). V codes are the B operand: four tokens per
+    // register (PRMT byte transpose) x 2^sh (LOP3 slot select) - never dequantized.
     int vacc[NT][16][4];
 #pragma unroll
     for (int mt = 0; mt < NT; ++mt)
@@ -547,42 +608,31 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_tc_kernel(const TcParam
         for (int nc = 0; nc < 16; ++nc)
 #pragma unroll
             for (int r = 0; r < 4; ++r) vacc[mt][nc][r] = 0;
-    int wacc[NT][4];  // sum_j p_j per digit plane: IMMA against an all-ones operand
-    const int pj = lane & 7, ph = lane >> 3;      // p-writer: k-word pj of head ph
-    const int ptok = (pj & 3) + 16 * (pj >> 2);  // token of k = 4*pj (+4i for byte i)
+    uint32_t wacc[NT];  // sum of this lane's u22 probabilities (head 4 mt + t)
     float pa[NT], pb[NT];
 #pragma unroll
     for (int mt = 0; mt < NT; ++mt) {
-        wacc[mt][0] = wacc[mt][1] = wacc[mt][2] = wacc[mt][3] = 0;
-        pa[mt] = sm.gpar[(4 * mt + ph) * 4 + 0];
-        pb[mt] = sm.gpar[(4 * mt + ph) * 4 + 1];
+        wacc[mt] = 0;
+        pa[mt] = sm.gpar[(4 * mt + t) * 4 + 0];
+        pb[mt] = sm.gpar[(4 * mt + t) * 4 + 1];
     }
-    // p tiles are double-buffered: block b+1's probabilities are produced while block
-    // b's IMMAs issue (software pipelining hides the LDS -> FFMA -> MUFU latency chain).
     uint32_t* pw = sm.pw + warp * 2 * NT * 12 * kPRow;
     auto p_write = [&](int blk, uint32_t* tile) {
-        const int btok = blk * 32;  // warp-local first token of the block
 #pragma unroll
         for (int mt = 0; mt < NT; ++mt) {
-            const int h = 4 * mt + ph;
+            float sc[4];
+            tmem_ld4(tmem_w + (uint32_t)((blk * NT + mt) * 4), sc);
             uint32_t v[4];
-            if (btok + 32 <= nv) {  // full block (warp-uniform): no bounds checks
 #pragma unroll
-                for (int ii = 0; ii < 4; ++ii) {
-                    const float pr = ex2(__fmaf_rn(scores[h * TS + btok + ptok + 4 * ii], pa[mt], pb[mt]));
-                    v[ii] = __float_as_uint(__fmaf_rn(pr, kPScale, kMagic));  // round(p * kPScale) in low bits
-                }
-            } else {
-#pragma unroll
-                for (int ii = 0; ii < 4; ++ii) {
-                    const int tok = btok + ptok + 4 * ii;
-                    const float pr = tok < nv ? ex2(__fmaf_rn(scores[h * TS + tok], pa[mt], pb[mt])) : 0.0f;
-                    v[ii] = __float_as_uint(__fmaf_rn(pr, kPScale, kMagic));
-                }
+            for (int j = 0; j < 4; ++j) {
+                const int tok = blk * 32 + 16 * (j >> 1) + 8 * (j & 1) + g;
+                const float pr = tok < nv ? ex2(__fmaf_rn(sc[j], pa[mt], pb[mt])) : 0.0f;
+                v[j] = __float_as_uint(__fmaf_rn(pr, kPScale, kMagic));  // round(p * kPScale) in low bits
+                wacc[mt] += v[j] - 0x4B400000u;
             }
             const uint32_t p01 = prmt(v[0], v[1], 0x5140), p23 = prmt(v[2], v[3], 0x5140);
             const uint32_t q01 = prmt(v[0], v[1], 0x7362), q23 = prmt(v[2], v[3], 0x7362);
-            uint32_t* rowp = tile + (mt * 12 + ph) * kPRow + pj;
+            uint32_t* rowp = tile + (mt * 12 + t) * kPRow + g;
             rowp[0 * 4 * kPRow] = prmt(p01, p23, 0x5410);                // bits 0-7
             rowp[1 * 4 * kPRow] = prmt(p01, p23, 0x7632);                // bits 8-15
             rowp[2 * 4 * kPRow] = prmt(q01, q23, 0x5410) & 0x3F3F3F3Fu;  // bits 16-21
@@ -595,8 +645,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_tc_kernel(const TcParam
     for (int b = 0; b < nblk_all; ++b) {
         const int st = b / kBps, blk = b % kBps;
         const int i = nstage + st;
-        const int slot = i % kStages;
-        if (blk == 0) mbar_wait(&full[slot], (i / kStages) & 1);
+        const int slot = i % kStagesW;
+        if (blk == 0) mbar_wait(&full[slot], (i / kStagesW) & 1);
         const uint8_t* buf = ring + slot * Gm::kStageBytesB;
         uint32_t* cur = pw + (b & 1) * NT * 12 * kPRow;
         uint32_t afr[NT][4];
@@ -609,7 +659,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_tc_kernel(const TcParam
             afr[mt][3] = g < 4 ? r0[8 * kPRow + 4 + t] : 0u;
         }
         if (b + 1 < nblk_all) p_write(b + 1, pw + ((b + 1) & 1) * NT * 12 * kPRow);
-        // B operand: V codes of this lane's 2*BITS bytes for 8 tokens, byte-transposed.
+        // B operand: V codes of this lane's 2*BITS bytes for the 4 tokens of k-group t
+        // (grp 0) / 4 + t (grp 1): rows 4 grp + t + 8 ii, byte-transposed.
         constexpr int NW = (2 * BITS + 3) / 4;  // 32-bit words per token slice
         uint32_t X[2][2 * BITS];
 #pragma unroll
@@ -617,7 +668,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_tc_kernel(const TcParam
             uint32_t raw[4][NW];
 #pragma unroll
             for (int ii = 0; ii < 4; ++ii) {
-                const uint8_t* rp = buf + (blk * 32 + 16 * grp + t + 4 * ii) * Gm::kRowBytes + 2 * BITS * g;
+                const uint8_t* rp = buf + (blk * 32 + 4 * grp + t + 8 * ii) * Gm::kRowBytes + 2 * BITS * g;
                 if (BITS == 1) {
                     raw[ii][0] = *reinterpret_cast<const uint16_t*>(rp);
                 } else if (BITS == 2) {
@@ -653,45 +704,36 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_tc_kernel(const TcParam
             for (int mt = 0; mt < NT; ++mt)
                 imma_u8u8(vacc[mt][nc], afr[mt][0], afr[mt][1], afr[mt][2], afr[mt][3], b0, b1);
         }
-#pragma unroll
-        for (int mt = 0; mt < NT; ++mt)
-            imma_u8u8(wacc[mt], afr[mt][0], afr[mt][1], afr[mt][2], afr[mt][3], 0x01010101u, 0x01010101u);
         __syncwarp();
-        if (lane == 0 && (blk == kBps - 1 || b == nblk_all - 1) && i + kStages < total_stages) issue(i + kStages);
+        if (lane == 0 && (blk == kBps - 1 || b == nblk_all - 1) && i + kStagesW < total_stages) issue(i + kStagesW);
     }
 
-    // ---------------- CTA reduction (exact integer sums through shared memory) ----------------
-    // This warp's scores are dead now: its region takes the warp's accumulators
-    // [NT][16 nc + 1 (weights)][32 lanes] uint4 (rows g / g+8 x columns 2t / 2t+1).
-    uint4* accs = reinterpret_cast<uint4*>(sm.scores + warp * 4 * NT * TS);
+    // ---------------- CTA reduction (exact integer sums in shared memory) ----------------
 #pragma unroll
     for (int mt = 0; mt < NT; ++mt) {
 #pragma unroll
         for (int nc = 0; nc < 16; ++nc)
-            accs[(mt * 17 + nc) * 32 + lane] = make_uint4((uint32_t)vacc[mt][nc][0], (uint32_t)vacc[mt][nc][1],
-                                                          (uint32_t)vacc[mt][nc][2], (uint32_t)vacc[mt][nc][3]);
-        accs[(mt * 17 + 16) * 32 + lane] =
-            make_uint4((uint32_t)wacc[mt][0], (uint32_t)wacc[mt][1], (uint32_t)wacc[mt][2], (uint32_t)wacc[mt][3]);
+#pragma unroll
+            for (int r = 0; r < 4; ++r) red_add_u32(sm.acc + ((mt * 16 + nc) * 32 + lane) * 4 + r, (uint32_t)vacc[mt][nc][r]);
+        uint32_t w = wacc[mt];
+        w += __shfl_xor_sync(0xffffffffu, w, 4);
+        w += __shfl_xor_sync(0xffffffffu, w, 8);
+        w += __shfl_xor_sync(0xffffffffu, w, 16);
+        if (lane < 4) sm.wsum[warp * 8 + 4 * mt + lane] = w;
     }
-    __syncthreads();
-    // Pass 1: element e of the accumulator image, summed over warps (consecutive threads
-    // read consecutive words: conflict-free), scattered into planes[plane][head][ch].
-    uint32_t* planes = reinterpret_cast<uint32_t*>(sm.ring);  // [3][4 NT][128 + 1] (ring is idle)
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();  // (the V stream is drained: the ring is free from here on)
+    // Scatter the accumulator image into planes[plane][head][ch].
+    uint32_t* planes = reinterpret_cast<uint32_t*>(sm.ring);  // [3][4 NT][128 + 1]
     constexpr int PS = kDim + 1;
-    for (int e = threadIdx.x; e < NT * 17 * 128; e += kWarps * 32) {
-        const int mt = e / (17 * 128), rem = e % (17 * 128);
+    for (int e = threadIdx.x; e < NT * 16 * 128; e += kWarps * 32) {
+        const int mt = e / (16 * 128), rem = e % (16 * 128);
         const int nc = rem >> 7, ln = (rem >> 2) & 31, r = rem & 3;
         const int gg = ln >> 2, tt = ln & 3;
         const int row = gg + 8 * (r >> 1);
         if (row >= 12) continue;  // rows 12..15 are empty (3 digit planes)
-        uint32_t sum = 0;
-        for (int w2 = 0; w2 < kWarps; ++w2)
-            sum += reinterpret_cast<const uint32_t*>(sm.scores + w2 * 4 * NT * TS)[(mt * 17 * 32) * 4 + rem];
+        const uint32_t sum = sm.acc[(mt * 16 * 32) * 4 + rem];
         const int plane = row >> 2, head = 4 * mt + (row & 3);
-        if (nc == 16) {  // weights: identical in every column; keep column 0
-            if ((tt == 0) && (r & 1) == 0) planes[(plane * 4 * NT + head) * PS + kDim] = sum;
-            continue;
-        }
         int sh;
         const int ch = v_channel<BITS>(2 * tt + (r & 1), nc, sh);
         planes[(plane * 4 * NT + head) * PS + ch] = sum;
@@ -701,6 +743,12 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_tc_kernel(const TcParam
     //   out = (s_c V / 2^sh + alpha_c W_vis + sum_t p_t v_tc) / (W_vis + sum_t p_t)
     // on the common kPScale weight scale; tail weights recomputed in fp32 (rank 0).
     constexpr float kInvLevels = 1.0f / (float)((1u << BITS) - 1u);
+    float* recv = reinterpret_cast<float*>(sm.ring + ((size_t)3 * 4 * NT * PS * 4 + 127) / 128 * 128);
+    if (S > 1) {  // every CTA's ring is drained before rank 0's becomes the receive buffer
+        __syncwarp();
+        cluster_arrive();  // #2a
+        cluster_wait();
+    }
     for (int idx = threadIdx.x; idx < G * kDim; idx += kWarps * 32) {
         const int h = idx / kDim, ch = idx % kDim;
         constexpr int cpb = Gm::kCpb;
@@ -709,37 +757,56 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_tc_kernel(const TcParam
         const float V = __fmaf_rn((float)pl[2 * 4 * NT * PS + ch], 65536.0f,
                                   __fmaf_rn((float)pl[4 * NT * PS + ch], 256.0f, (float)pl[ch])) *
                         __int_as_float((127 - sh) << 23);
-        const float wv = __fmaf_rn((float)pl[2 * 4 * NT * PS + kDim], 65536.0f,
-                                   __fmaf_rn((float)pl[4 * NT * PS + kDim], 256.0f, (float)pl[kDim]));
+        unsigned long long ws = 0;
+        for (int w2 = 0; w2 < kWarps; ++w2) ws += sm.wsum[w2 * 8 + h];
+        const float wv = (float)ws;
         const float va = __ldg(a.v_alpha + unit * kDim + ch);
         const float step = fmaxf(__fsub_rn(__ldg(a.v_beta + unit * kDim + ch), va) * kInvLevels, 0.0f);
         float num = __fmaf_rn(step, V, va * wv), den = wv;
-        for (int j = 0; j < ntl; ++j) {
+        const float* vt = a.v_tail + (size_t)unit * a.tail_cap * kDim + ch;
+        int j = 0;
+        for (; j + 8 <= ntl; j += 8) {  // 8 independent loads in flight, j ascending
+            float vv[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) vv[u] = __ldg(vt + (size_t)(j + u) * kDim);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const float pt = ex2(__fmaf_rn(sm.tail_s[h * kTailMax + j + u], kLog2e, sm.gpar[h * 4 + 2])) * kPScale;
+                den += pt;
+                num = __fmaf_rn(pt, vv[u], num);
+            }
+        }
+        for (; j < ntl; ++j) {
             const float pt = ex2(__fmaf_rn(sm.tail_s[h * kTailMax + j], kLog2e, sm.gpar[h * 4 + 2])) * kPScale;
             den += pt;
-            num = __fmaf_rn(pt, a.v_tail[((size_t)unit * a.tail_cap + j) * kDim + ch], num);
+            num = __fmaf_rn(pt, __ldg(vt + (size_t)j * kDim), num);
         }
         if (S == 1) {
             a.out[((size_t)unit * G + h) * kDim + ch] = num / den;
         } else {
-            st_cluster_f32(sm.recv + rank * (8 * kDim + 8) + idx, 0, num);
-            if (ch == 0) st_cluster_f32(sm.recv + rank * (8 * kDim + 8) + 8 * kDim + h, 0, den);
+            st_cluster_f32(recv + rank * (8 * kDim + 8) + idx, 0, num);
+            if (ch == 0) st_cluster_f32(recv + rank * (8 * kDim + 8) + 8 * kDim + h, 0, den);
         }
     }
     if (S > 1) {
         __syncwarp();
-        cluster_arrive();  // #2: partial numerators / denominators are in rank 0
+        cluster_arrive();  // #2b: partial numerators / denominators are in rank 0
         cluster_wait();
-        if (rank != 0) return;
-        for (int idx = threadIdx.x; idx < G * kDim; idx += kWarps * 32) {
-            const int h = idx / kDim;
-            float num = 0.f, den = 0.f;
-            for (int r = 0; r < S; ++r) {
-                num += sm.recv[r * (8 * kDim + 8) + idx];
-                den += sm.recv[r * (8 * kDim + 8) + 8 * kDim + h];
+        if (rank == 0) {
+            for (int idx = threadIdx.x; idx < G * kDim; idx += kWarps * 32) {
+                const int h = idx / kDim;
+                float num = 0.f, den = 0.f;
+                for (int r = 0; r < S; ++r) {
+                    num += recv[r * (8 * kDim + 8) + idx];
+                    den += recv[r * (8 * kDim + 8) + 8 * kDim + h];
+                }
+                a.out[((size_t)unit * G + (idx / kDim)) * kDim + (idx % kDim)] = num / den;
             }
-            a.out[((size_t)unit * G + (idx / kDim)) * kDim + (idx % kDim)] = num / den;
         }
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(kTmemCols));
     }
 }
 
@@ -757,13 +824,18 @@ cudaError_t launch_bits(const DecodeArgs& a, cudaStream_t s) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     TcParams p{a, a.tc_frag, a.tc_qconst, S, T};
-    const size_t smem = tc_smem_bytes(BITS, NT, S);
+    // TMEM: kTmemCols per CTA; never let more CTAs share an SM than TMEM can serve (a
+    // blocked tcgen05.alloc inside a cluster could deadlock against its partners).
+    const size_t max_ctas = NT == 1 ? 4 : 2;
+    size_t smem = tc_smem_bytes<BITS, NT>(S);
+    const size_t floor_bytes = 232448 / (max_ctas + 1) + 1;
+    if (smem < floor_bytes) smem = floor_bytes;
     auto kern = decode_tc_kernel<BITS, NT>;
     static bool attr_done = false;  // per instantiation
     if (!attr_done) {
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
         if (e != cudaSuccess) return e;
         attr_done = true;
     }
@@ -790,6 +862,11 @@ cudaError_t launch_bits(const DecodeArgs& a, cudaStream_t s) {
 
 size_t decode_tc_scratch_bytes(size_t units) { return units * (2 * 512 * sizeof(uint32_t) + 8 * sizeof(float2)); }
 
+template <int BITS, int NT>
+static size_t tc_smem_for(int S) {
+    return tc_smem_bytes<BITS, NT>(S);
+}
+
 bool decode_tc_supported(const DecodeArgs& a) {
     if (a.dim != (size_t)kDim || a.word_bits != 8 || a.n_vis == 0) return false;
     if (a.bits != 1 && a.bits != 2 && a.bits != 4 && a.bits != 8) return false;
@@ -801,7 +878,19 @@ bool decode_tc_supported(const DecodeArgs& a) {
     // the fp32 tail lives in rank 0: at most kTailMax rows
     if (a.tail_cap > (size_t)kTailMax) return false;
     (void)T;
-    return tc_smem_bytes(a.bits, a.group > 4 ? 2 : 1, S) <= 200 * 1024;
+    const int NT = a.group > 4 ? 2 : 1;
+    size_t smem = 0;
+    switch (a.bits * 10 + NT) {
+        case 11: smem = tc_smem_for<1, 1>(S); break;
+        case 12: smem = tc_smem_for<1, 2>(S); break;
+        case 21: smem = tc_smem_for<2, 1>(S); break;
+        case 22: smem = tc_smem_for<2, 2>(S); break;
+        case 41: smem = tc_smem_for<4, 1>(S); break;
+        case 42: smem = tc_smem_for<4, 2>(S); break;
+        case 81: smem = tc_smem_for<8, 1>(S); break;
+        case 82: smem = tc_smem_for<8, 2>(S); break;
+    }
+    return smem <= 220 * 1024;
 }
 
 cudaError_t launch_decode_tc(const DecodeArgs& a, cudaStream_t s) {

@@ -541,6 +541,12 @@ __global__ void __launch_bounds__(kThreads + 64) decode_umma_kernel(const UParam
     } else {
         // ======================= consumer warps =======================
         const uint32_t tlane = tbase + ((uint32_t)(32 * warp) << 16);  // this warp's TMEM lane quarter
+        // Warm L2 with the fp32 tail rows (rank 0 reads them after phase A / in the epilogue).
+        for (int l = threadIdx.x; l < 8 * ntl; l += blockDim.x) {
+            const float* base = (l & 4) ? a.v_tail : a.k_tail;
+            const float* ptr = base + ((size_t)unit * a.tail_cap + (l >> 3)) * kDim + 32 * (l & 3);
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
+        }
         griddep_wait();  // the prep kernel's B tile and constants are visible from here on
         {
             const uint4* src = reinterpret_cast<const uint4*>(p.qb + (size_t)unit * 2048 * NT);
@@ -627,21 +633,28 @@ __global__ void __launch_bounds__(kThreads + 64) decode_umma_kernel(const UParam
         tc_wait_st();  // this thread's score columns are in TMEM before phase B reads them back
         if (tid == 0) UTRACE(2);
 
-        // fp32 tail rows (rank 0, warp 0): lanes split the 128 channels.
+        // fp32 tail rows (rank 0): warp w takes rows w, w + NW, ...; lanes split the 128
+        // channels; q rows are loaded once.
         const float isd = __fdiv_rn(1.0f, sqrtf((float)kDim));
         float tmax = -INFINITY;  // for head (lane & 7)
-        if (warp == 0) {
-            for (int j = 0; j < ntl; ++j) {
-                const float4 kv =
-                    *reinterpret_cast<const float4*>(a.k_tail + ((size_t)unit * a.tail_cap + j) * kDim + 4 * lane);
-                for (int h = 0; h < G; ++h) {
-                    const float4 qv = *reinterpret_cast<const float4*>(a.q + ((size_t)unit * G + h) * kDim + 4 * lane);
-                    float d = kv.x * qv.x + kv.y * qv.y + kv.z * qv.z + kv.w * qv.w;
-#pragma unroll
-                    for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-                    d *= isd;
-                    if (lane == 0) sm.tail_s[h * kTailMax + j] = d;
-                    if ((lane & 7) == h) tmax = fmaxf(tmax, d);
+        if (warp < 4 && ntl > warp) {
+            float4 qv[8];
+    #pragma unroll
+            for (int h = 0; h < 8; ++h)
+                qv[h] = h < G ? *reinterpret_cast<const float4*>(a.q + ((size_t)unit * G + h) * kDim + 4 * lane)
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int j = warp; j < ntl; j += 4) {
+                const float4 kv = *reinterpret_cast<const float4*>(a.k_tail + ((size_t)unit * a.tail_cap + j) * kDim + 4 * lane);
+    #pragma unroll
+                for (int h = 0; h < 8; ++h) {
+                    if (h < G) {
+                        float d = kv.x * qv[h].x + kv.y * qv[h].y + kv.z * qv[h].z + kv.w * qv[h].w;
+    #pragma unroll
+                        for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+                        d *= isd;
+                        if (lane == 0) sm.tail_s[h * kTailMax + j] = d;
+                        if ((lane & 7) == h) tmax = fmaxf(tmax, d);
+                    }
                 }
             }
         }
@@ -658,13 +671,17 @@ __global__ void __launch_bounds__(kThreads + 64) decode_umma_kernel(const UParam
                 sm.red[(warp * 3 + 1) * 8 + h] = hi[h];
             }
         }
-        if (warp == 0 && lane < 8) sm.red[(0 * 3 + 2) * 8 + lane] = tmax;  // lanes 0..7 hold heads 0..7
+        {  // tail max per head over the 4 warps (lanes 0..7 hold heads 0..7)
+            float tm = tmax;
+            if (lane < 8) sm.red[(warp * 3 + 2) * 8 + lane] = tm;
+        }
         consumer_sync();
         if (tid < 24) {  // CTA record: (min[8], max[8], tail max[8])
             const int k = tid, kind = k >> 3, h = k & 7;
             float v;
             if (kind == 2) {
-                v = sm.red[2 * 8 + h];
+                v = fmaxf(fmaxf(sm.red[(0 * 3 + 2) * 8 + h], sm.red[(1 * 3 + 2) * 8 + h]),
+                          fmaxf(sm.red[(2 * 3 + 2) * 8 + h], sm.red[(3 * 3 + 2) * 8 + h]));
             } else if (h >= H) {
                 v = kind == 0 ? INFINITY : -INFINITY;
             } else {
@@ -823,10 +840,25 @@ __global__ void __launch_bounds__(kThreads + 64) decode_umma_kernel(const UParam
                                                 __fmaf_rn((float)r[4 * h + 1], 256.0f, (float)r[4 * h])));
             num[h] = __fmaf_rn(vstep, V * 4.656612873077393e-10f /* 2^-31 */, va * W);
             den[h] = W;
-            for (int j = 0; j < ntl && h < G; ++j) {  // fp32 tail (rank 0)
-                const float pt = ex2(__fmaf_rn(sm.tail_s[h * kTailMax + j], kLog2e, sm.gpar[h * 4 + 2]));
-                den[h] += pt;
-                num[h] = __fmaf_rn(pt, a.v_tail[((size_t)unit * a.tail_cap + j) * kDim + ch], num[h]);
+            if (h < G) {  // fp32 tail (rank 0), 8 independent loads in flight, j ascending
+                const float* vt = a.v_tail + (size_t)unit * a.tail_cap * kDim + ch;
+                int j = 0;
+                for (; j + 8 <= ntl; j += 8) {
+                    float vv[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) vv[u] = __ldg(vt + (size_t)(j + u) * kDim);
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const float pt = ex2(__fmaf_rn(sm.tail_s[h * kTailMax + j + u], kLog2e, sm.gpar[h * 4 + 2]));
+                        den[h] += pt;
+                        num[h] = __fmaf_rn(pt, vv[u], num[h]);
+                    }
+                }
+                for (; j < ntl; ++j) {
+                    const float pt = ex2(__fmaf_rn(sm.tail_s[h * kTailMax + j], kLog2e, sm.gpar[h * 4 + 2]));
+                    den[h] += pt;
+                    num[h] = __fmaf_rn(pt, __ldg(vt + (size_t)j * kDim), num[h]);
+                }
             }
         }
         if (S == 1) {

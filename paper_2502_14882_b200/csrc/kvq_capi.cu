@@ -212,7 +212,10 @@ void run_decode(kvq_cache* c, const float* q, float* out, bool want_weights, boo
     if (c->path == KVQ_PATH_TC && !tc_ok && plain)
         raise(KVQ_ERR_CONFIG, "tensor-core decode path needs dim 128, 8-bit words, a quantized "
                               "prefill and no weight/violation export");
-    if ((c->path == KVQ_PATH_AUTO || c->path == KVQ_PATH_UMMA) && umma_ok) {
+    // AUTO prefers the mma.sync IMMA kernel: for this problem's N = G x digit planes = 16
+    // it out-runs tcgen05 (a kind::i8 UTCIMMA costs ~100 cycles for any N <= 128,
+    // profiles/r01_umma_rate.txt). The tcgen05 path remains selectable (KVQ_PATH_UMMA).
+    if ((c->path == KVQ_PATH_UMMA || (c->path == KVQ_PATH_AUTO && !tc_ok)) && umma_ok) {
         const size_t need = kvqb::decode_tc_scratch_bytes(c->units);
         if (c->tc_scratch.n < need) c->tc_scratch.alloc(need);
         a.umma_qb = c->tc_scratch.p;
