@@ -542,7 +542,7 @@ __global__ void __launch_bounds__(kThreads + 64) decode_umma_kernel(const UParam
         // ======================= consumer warps =======================
         const uint32_t tlane = tbase + ((uint32_t)(32 * warp) << 16);  // this warp's TMEM lane quarter
         // Warm L2 with the fp32 tail rows (rank 0 reads them after phase A / in the epilogue).
-        for (int l = threadIdx.x; l < 8 * ntl; l += blockDim.x) {
+        for (int l = tid; l < 8 * ntl; l += kThreads) {
             const float* base = (l & 4) ? a.v_tail : a.k_tail;
             const float* ptr = base + ((size_t)unit * a.tail_cap + (l >> 3)) * kDim + 32 * (l & 3);
             asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
