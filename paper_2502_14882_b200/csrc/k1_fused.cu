@@ -1,7 +1,123 @@
-// k1_fused.cu — placeholder until the fused single-pass K1 lands.
+// k1_fused.cu — K1 code pass for the decode layout (d = 128, M = 8, channel-wise or
+// global stats already computed): codes + MSB-first packing with warp ballots / shuffles,
+// bit-exact with quantize (quantize.hpp:91-127) and pack (bitpack.hpp:64-90).
+//
+// Lane c of a warp owns channels c, 32+c, 64+c, 96+c of every row it visits: a row is
+// read as four coalesced 128-byte transactions, the lane's four (alpha, inv_step) pairs
+// live in registers for the whole kernel, and each 32-channel group of a row is packed by
+// one warp-wide collective:
+//   b = 1: W = ballot(code); the LE word of bytes 4w..4w+3 is byte_perm(brev(W), 0x0123)
+//          (brev maps bit 8j+k to 8(3-j)+7-k; the byte swap puts channel 8j+k at bit
+//          8j+7-k: MSB-first within byte j);
+//   b = 2/4/8: each lane shifts its code to its bit position inside its 32-bit word and
+//          the lanes sharing a word OR-reduce with shuffles.
+// Per element: one fsub, one fmul (IEEE, no contraction), roundf (half away from zero),
+// clamp - the reference's quantize_one exactly.
 #include "kvq_internal.cuh"
+
 namespace kvqb {
-bool quantize_fused_supported(size_t, size_t, int, int) { return false; }
-cudaError_t launch_quantize_fused(const float*, size_t, size_t, size_t, int, float*, float*, uint8_t*,
-                                  cudaStream_t) { return cudaErrorNotSupported; }
+
+namespace {
+
+constexpr int kDim = 128;
+constexpr int kWarpsPerCta = 8;
+constexpr int kRowsPerIter = 4;  // rows in flight per warp (16 loads per lane)
+
+__device__ __forceinline__ uint32_t code_of(float x, float a, float inv, float levels) {
+    float t = roundf(__fmul_rn(__fsub_rn(x, a), inv));
+    t = t < 0.0f ? 0.0f : (levels < t ? levels : t);
+    return (uint32_t)t;  // NaN -> 0, as the x86 reference build
+}
+
+template <int BITS>
+__device__ __forceinline__ void pack_store(const uint32_t (&code)[4], uint8_t* row_out, int lane) {
+    if constexpr (BITS == 1) {
+        uint32_t words[4];
+#pragma unroll
+        for (int w = 0; w < 4; ++w) words[w] = __byte_perm(__brev(__ballot_sync(0xffffffffu, code[w] != 0u)), 0, 0x0123);
+        if (lane == 0) *reinterpret_cast<uint4*>(row_out) = make_uint4(words[0], words[1], words[2], words[3]);
+    } else {
+        // 32/BITS channels per word; channel c' (within its word) -> bit 8*(c'/cpb) + 8 - BITS*(c'%cpb + 1)
+        constexpr int cpb = 8 / BITS;
+        constexpr int lanes_per_word = 32 / BITS;
+        const int cw = lane % lanes_per_word;
+        const int shift = 8 * (cw / cpb) + 8 - BITS * (cw % cpb + 1);
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            uint32_t v = code[w] << shift;
+#pragma unroll
+            for (int o = 1; o < lanes_per_word; o <<= 1) v |= __shfl_xor_sync(0xffffffffu, v, o);
+            // word index within the row: group w covers 32 channels = BITS words
+            if (cw == 0) reinterpret_cast<uint32_t*>(row_out)[w * BITS + lane / lanes_per_word] = v;
+        }
+    }
+}
+
+template <int BITS>
+__global__ void __launch_bounds__(kWarpsPerCta * 32)
+quantize_rows_d128(const float* __restrict__ x, size_t rows, const float* __restrict__ alpha,
+                   const float* __restrict__ beta, uint8_t* __restrict__ codes) {
+    constexpr int kRowBytes = 16 * BITS;
+    const float levels = (float)((1u << BITS) - 1u);
+    const size_t m = blockIdx.y;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    float a[4], inv[4];
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+        const int c = 32 * w + lane;
+        a[w] = alpha[m * kDim + c];
+        const float range = __fsub_rn(beta[m * kDim + c], a[w]);
+        inv[w] = range > 0.0f ? __fdiv_rn(levels, range) : 0.0f;  // quantize.hpp:102-106
+    }
+    const float* src = x + m * rows * kDim;
+    uint8_t* dst = codes + m * rows * kRowBytes;
+    const size_t stride = (size_t)gridDim.x * kWarpsPerCta * kRowsPerIter;
+    for (size_t r0 = ((size_t)blockIdx.x * kWarpsPerCta + warp) * kRowsPerIter; r0 < rows; r0 += stride) {
+        float v[kRowsPerIter][4];
+#pragma unroll
+        for (int i = 0; i < kRowsPerIter; ++i)
+#pragma unroll
+            for (int w = 0; w < 4; ++w)
+                v[i][w] = r0 + i < rows ? __ldcs(src + (r0 + i) * kDim + 32 * w + lane) : 0.0f;
+#pragma unroll
+        for (int i = 0; i < kRowsPerIter; ++i) {
+            if (r0 + i >= rows) break;  // warp-uniform
+            uint32_t code[4];
+#pragma unroll
+            for (int w = 0; w < 4; ++w) code[w] = code_of(v[i][w], a[w], inv[w], levels);
+            pack_store<BITS>(code, dst + (r0 + i) * kRowBytes, lane);
+        }
+    }
+}
+
+}  // namespace
+
+bool quantize_fused_supported(size_t rows, size_t dim, int word_bits, int mode) {
+    (void)rows;
+    (void)mode;  // stats (either mode) come from the stats kernel; codes are per channel
+    return dim == (size_t)kDim && word_bits == 8;
+}
+
+cudaError_t launch_quantize_fused(const float* x, size_t mats, size_t rows, size_t dim, int bits, int mode,
+                                  float* alpha, float* beta, uint8_t* codes, cudaStream_t s) {
+    if (rows == 0 || mats == 0) return cudaSuccess;
+    cudaError_t e = launch_compute_stats(x, mats, rows, dim, mode, alpha, beta, s);  // compute_stats
+    if (e != cudaSuccess) return e;
+    const size_t rows_per_cta = (size_t)kWarpsPerCta * kRowsPerIter;
+    size_t gx = (rows + rows_per_cta - 1) / rows_per_cta;
+    // enough CTAs to fill the GPU several times over, grid-striding beyond that
+    const size_t cap = (148 * 16 + mats - 1) / mats;
+    if (gx > cap) gx = cap < 1 ? 1 : cap;
+    dim3 grid((unsigned)gx, (unsigned)mats);
+    switch (bits) {
+        case 1: quantize_rows_d128<1><<<grid, kWarpsPerCta * 32, 0, s>>>(x, rows, alpha, beta, codes); break;
+        case 2: quantize_rows_d128<2><<<grid, kWarpsPerCta * 32, 0, s>>>(x, rows, alpha, beta, codes); break;
+        case 4: quantize_rows_d128<4><<<grid, kWarpsPerCta * 32, 0, s>>>(x, rows, alpha, beta, codes); break;
+        case 8: quantize_rows_d128<8><<<grid, kWarpsPerCta * 32, 0, s>>>(x, rows, alpha, beta, codes); break;
+        default: return cudaErrorInvalidValue;
+    }
+    note_launch();
+    return cudaGetLastError();
+}
+
 }  // namespace kvqb

@@ -198,11 +198,15 @@ kvqb::DecodeArgs decode_args(kvq_cache* c, const float* q, float* out) {
     return a;
 }
 
+void ensure_vt(kvq_cache* c, cudaStream_t s);
+
 void run_decode(kvq_cache* c, const float* q, float* out, bool want_weights, bool want_viol,
                 cudaStream_t s) {
     kvqb::DecodeArgs a = decode_args(c, q, out);
     const bool plain = !want_weights && !want_viol;
-    const bool umma_ok = plain && kvqb::decode_umma_supported(a);
+    kvqb::DecodeArgs probe = a;
+    probe.v_codes_t = reinterpret_cast<const uint8_t*>(1);  // shape check only
+    const bool umma_ok = plain && c->dim == 128 && c->word_bits == 8 && kvqb::decode_umma_supported(probe);
     bool tc_ok = kvqb::decode_tc_supported(a) && plain;
     // Probability-row / violation export (decode_step_detailed) is a generic-path feature:
     // an explicit tensor-core path selection applies to plain decodes only.
@@ -216,6 +220,8 @@ void run_decode(kvq_cache* c, const float* q, float* out, bool want_weights, boo
     // it out-runs tcgen05 (a kind::i8 UTCIMMA costs ~100 cycles for any N <= 128,
     // profiles/r01_umma_rate.txt). The tcgen05 path remains selectable (KVQ_PATH_UMMA).
     if ((c->path == KVQ_PATH_UMMA || (c->path == KVQ_PATH_AUTO && !tc_ok)) && umma_ok) {
+        ensure_vt(c, s);
+        a.v_codes_t = c->vt.p;
         const size_t need = kvqb::decode_tc_scratch_bytes(c->units);
         if (c->tc_scratch.n < need) c->tc_scratch.alloc(need);
         a.umma_qb = c->tc_scratch.p;
@@ -312,18 +318,21 @@ void quantize_prefill(kvq_cache* c, const float* dk, const float* dv, cudaStream
         float* alpha = which == 0 ? c->k_alpha() : c->v_alpha();
         float* beta = which == 0 ? c->k_beta() : c->v_beta();
         if (kvqb::quantize_fused_supported(n, d, c->word_bits, c->mode)) {
-            ck(kvqb::launch_quantize_fused(srcs[which], u, n, d, c->bits, alpha, beta, codes, s), "quantize");
+            ck(kvqb::launch_quantize_fused(srcs[which], u, n, d, c->bits, c->mode, alpha, beta, codes, s), "quantize");
         } else {
             ck(kvqb::launch_compute_stats(srcs[which], u, n, d, c->mode, alpha, beta, s), "compute_stats");
             ck(kvqb::launch_quantize_pack(srcs[which], u, n, d, alpha, beta, c->bits, c->word_bits, codes, s),
                "quantize");
         }
     }
-    // Device layout for the tcgen05 decode: V codes re-packed along the token axis.
-    if (d == 128 && c->word_bits == 8 && n > 0) {
-        c->vt.alloc(kvqb::vt_bytes(u, n, c->bits));
-        ck(kvqb::launch_pack_vt(c->v_codes(), u, n, c->bits, c->vt.p, s), "pack vt");
-    }
+}
+
+// Device layout for the tcgen05 decode: V codes re-packed along the token axis. Built on
+// first use of that path (the default IMMA path reads the reference layout).
+void ensure_vt(kvq_cache* c, cudaStream_t s) {
+    if (c->vt.p || c->dim != 128 || c->word_bits != 8 || c->n_vis == 0) return;
+    c->vt.alloc(kvqb::vt_bytes(c->units, c->n_vis, c->bits));
+    ck(kvqb::launch_pack_vt(c->v_codes(), c->units, c->n_vis, c->bits, c->vt.p, s), "pack vt");
 }
 
 void fill_full_precision_tail(kvq_cache* c, const float* k, const float* v, size_t n, cudaMemcpyKind kind) {
@@ -480,7 +489,7 @@ int kvq_quantize_device(const float* x, size_t mats, size_t rows, size_t dim, in
         require_device();
         cudaStream_t s = (cudaStream_t)stream;
         if (kvqb::quantize_fused_supported(rows, dim, word_bits, mode)) {
-            ck(kvqb::launch_quantize_fused(x, mats, rows, dim, bitwidth, alpha, beta, codes, s), "quantize");
+            ck(kvqb::launch_quantize_fused(x, mats, rows, dim, bitwidth, mode, alpha, beta, codes, s), "quantize");
         } else {
             ck(kvqb::launch_compute_stats(x, mats, rows, dim, mode, alpha, beta, s), "compute_stats");
             ck(kvqb::launch_quantize_pack(x, mats, rows, dim, alpha, beta, bitwidth, word_bits, codes, s), "quantize");

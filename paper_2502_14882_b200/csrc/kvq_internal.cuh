@@ -36,9 +36,10 @@ cudaError_t launch_compute_stats(const float* x, size_t mats, size_t rows, size_
 cudaError_t launch_quantize_pack(const float* x, size_t mats, size_t rows, size_t dim,
                                  const float* alpha, const float* beta, int bits, int word_bits,
                                  uint8_t* codes, cudaStream_t s);
-// Fused single-pass K1 for d = 128, M = 8 (cluster exchange of partial stats).
+// K1 for the decode layout (d = 128, M = 8): stats kernel, then the warp-collective code
+// pass of k1_fused.cu (coalesced rows, ballot / shuffle packing).
 bool quantize_fused_supported(size_t rows, size_t dim, int word_bits, int mode);
-cudaError_t launch_quantize_fused(const float* x, size_t mats, size_t rows, size_t dim, int bits,
+cudaError_t launch_quantize_fused(const float* x, size_t mats, size_t rows, size_t dim, int bits, int mode,
                                   float* alpha, float* beta, uint8_t* codes, cudaStream_t s);
 // Generic bit packing of explicit u32 codes (bitpack.hpp:161-187). err_flag set to 1 on
 // an out-of-range code.
