@@ -23,6 +23,8 @@
 // Packed K/V are never dequantized; the only fp32 math per token is the softmax.
 #include <cooperative_groups.h>
 
+#include <cstdlib>
+
 #include "kvq_internal.cuh"
 
 namespace cg = cooperative_groups;
@@ -110,6 +112,16 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
     asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
     return r;
 }
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+// Debug timeline (KVQ_TRACE_FILE): slot k of this CTA's 256-entry record.
+#define TTRACE(k)                                                                          \
+    do {                                                                                   \
+        if (a.trace) a.trace[(size_t)blockIdx.x * 256 + (k)] = gtimer();                   \
+    } while (0)
 __device__ __forceinline__ float ex2(float x) {
     float r;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
@@ -230,14 +242,14 @@ constexpr int kSteps = kWarpTokens / 32;  // 32-token steps per warp
 
 // Per-warp TMA ring: ~10 KB in flight per warp (80 KB per CTA, two CTAs per SM) covers
 // the ~2 us bulk-copy latency measured under load (profiles/r01_trace_umma_c2.txt).
-template <int BITS>
+template <int BITS, int OCC>
 constexpr int ring_stages() {
-    return Geo<BITS>::kStageBytesB >= 4096 ? 3 : 5;
+    return OCC >= 3 ? (Geo<BITS>::kStageBytesB >= 4096 ? 2 : 3) : (Geo<BITS>::kStageBytesB >= 4096 ? 3 : 5);
 }
 
 struct Smem {  // carve-up of the dynamic shared memory of one decode CTA
     uint8_t* ring;       // [kWarps][kStages][kStageBytes]: per-warp TMA landing zones;
-                         // after the V stream: planes + the cluster receive buffer
+                         // after the V stream: the cluster receive buffer
     uint32_t* acc;       // [NT][16 nc][32 lanes][4]: CTA sum of the warps' p.V accumulators
     uint32_t* pw;        // [kWarps][2][NT][12][kPRow] p digit planes of a warp's block
     float* tail_s;       // [8][kTailMax] fp32 tail scores (rank 0)
@@ -249,7 +261,7 @@ struct Smem {  // carve-up of the dynamic shared memory of one decode CTA
     uint32_t* tmem_slot;
 };
 
-template <int BITS, int NT>
+template <int BITS, int NT, int OCC>
 __host__ __device__ inline size_t tc_smem_bytes(int S, Smem* out = nullptr, uint8_t* base = nullptr) {
     size_t off = 0;
     auto take = [&](size_t bytes) {
@@ -258,10 +270,9 @@ __host__ __device__ inline size_t tc_smem_bytes(int S, Smem* out = nullptr, uint
         return base + o;
     };
     constexpr int stage = Geo<BITS>::kStageBytesB;
-    const size_t planes_bytes = (size_t)3 * 4 * NT * (kDim + 1) * 4;
     const size_t recv_bytes = S > 1 ? (size_t)S * (8 * kDim + 8) * 4 : 0;
-    const size_t ring_bytes = (size_t)kWarps * ring_stages<BITS>() * stage;
-    const size_t tail_use = planes_bytes + recv_bytes;
+    const size_t ring_bytes = (size_t)kWarps * ring_stages<BITS, OCC>() * stage;
+    const size_t tail_use = recv_bytes;
     uint8_t* ring = take(ring_bytes > tail_use ? ring_bytes : tail_use);
     uint8_t* acc = take((size_t)NT * 16 * 32 * 4 * 4);
     uint8_t* pw = take((size_t)kWarps * 2 * NT * 12 * kPRow * 4);
@@ -270,7 +281,7 @@ __host__ __device__ inline size_t tc_smem_bytes(int S, Smem* out = nullptr, uint
     uint8_t* allpart = take((size_t)(S > 0 ? S : 1) * 24 * 4);
     uint8_t* gpar = take(32 * 4);
     uint8_t* wsum = take((size_t)kWarps * 8 * 4);
-    uint8_t* full = take((size_t)kWarps * ring_stages<BITS>() * 8);
+    uint8_t* full = take((size_t)kWarps * ring_stages<BITS, OCC>() * 8);
     uint8_t* slot = take(16);
     if (out) {
         out->ring = ring;
@@ -321,10 +332,10 @@ __device__ __forceinline__ void red_add_u32(uint32_t* p, uint32_t v) {
 // tensor memory (lane-private columns, tcgen05.st/ld) between the phases.
 // Cross-warp reductions of the p.V accumulators are exact integer shared-memory atomics
 // (deterministic); cross-CTA traffic is push-only.
-template <int BITS, int NT>
-__global__ void __launch_bounds__(kWarps * 32, 1) decode_tc_kernel(const TcParams p) {
+template <int BITS, int NT, int OCC>
+__global__ void __launch_bounds__(kWarps * 32, OCC) decode_tc_kernel(const TcParams p) {
     using Gm = Geo<BITS>;
-    constexpr int kStagesW = ring_stages<BITS>();
+    constexpr int kStagesW = ring_stages<BITS, OCC>();
     constexpr uint32_t kTmemCols = NT == 1 ? 128 : 256;  // 2 lane-sharing warps x 16 steps x 4 NT
     const DecodeArgs& a = p.a;
     const int G = (int)a.group;
@@ -336,7 +347,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_tc_kernel(const TcParam
 
     extern __shared__ __align__(128) uint8_t smem_raw[];
     Smem sm;
-    tc_smem_bytes<BITS, NT>(S, &sm, smem_raw);
+    tc_smem_bytes<BITS, NT, OCC>(S, &sm, smem_raw);
+    if (threadIdx.x == 0) TTRACE(0);
     uint8_t* ring = sm.ring + warp * kStagesW * Gm::kStageBytesB;
     uint64_t* full = sm.full + warp * kStagesW;
 
@@ -383,9 +395,92 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_tc_kernel(const TcParam
         const float* ptr = base + ((size_t)unit * a.tail_cap + (l >> 3)) * kDim + 32 * (l & 3);
         asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
     }
-    griddep_wait();  // prep kernel's q planes are visible from here on
+    // V scale / zero-point of this thread's output channel (threadIdx.x % 128), loaded early.
+    constexpr float kInvLevelsV = 1.0f / (float)((1u << BITS) - 1u);
+    const float v_a = __ldg(a.v_alpha + unit * kDim + (threadIdx.x & (kDim - 1)));
+    const float v_step =
+        fmaxf(__fsub_rn(__ldg(a.v_beta + unit * kDim + (threadIdx.x & (kDim - 1))), v_a) * kInvLevelsV, 0.0f);
+    griddep_wait();  // the previous step's append (tail rows, tail_len) and q are visible from here on
+
+    // ---- fold the K scales into the query (scale_query, kernels.hpp:183-194) ----
+    // Q'_c = round(S_h qs_c / 2^sh_c) in 4 balanced int8 digit planes, S_h bounding the
+    // int32 score so IMMA accumulation is exact; computed by every CTA for its own unit
+    // while its TMA ring fills (the pw tiles are idle until phase B). Two barriers.
+    float* s_qs = reinterpret_cast<float*>(sm.pw);  // [8][128]
+    float* s_red = s_qs + 8 * kDim;                  // [2][8][4]: per-warp sum|qs|, sum q.alpha
+    uint32_t* s_frag = reinterpret_cast<uint32_t*>(s_red + 64);  // [NT][512]
+    const float levels = (float)((1u << BITS) - 1u);
+    const float isd0 = __fdiv_rn(1.0f, sqrtf((float)kDim));
+    if (threadIdx.x < kDim) {
+        const int c = threadIdx.x;
+        const float ka = a.k_alpha[unit * kDim + c];
+        const float kbeta = a.k_beta[unit * kDim + c];
+        float qv[8];
+#pragma unroll
+        for (int h = 0; h < 8; ++h) qv[h] = h < G ? a.q[(unit * G + h) * kDim + c] : 0.0f;
+        const float range = __fsub_rn(kbeta, ka);
+        const float stp = range > 0.0f ? __fdiv_rn(range, levels) : 0.0f;
+        float ab[8], sa[8];
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+            const float qs = range > 0.0f ? __fmul_rn(qv[h], stp) : 0.0f;
+            s_qs[h * kDim + c] = qs;
+            ab[h] = fabsf(qs);
+            sa[h] = __fmul_rn(qv[h], ka);
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1)
+#pragma unroll
+            for (int h = 0; h < 8; ++h) {
+                ab[h] += __shfl_xor_sync(0xffffffffu, ab[h], o);
+                sa[h] += __shfl_xor_sync(0xffffffffu, sa[h], o);
+            }
+        if (lane < 8) {
+            float x = ab[0], y = sa[0];
+#pragma unroll
+            for (int h = 1; h < 8; ++h)
+                if (lane == h) x = ab[h], y = sa[h];
+            s_red[(0 * 8 + lane) * 4 + warp] = x;
+            s_red[(1 * 8 + lane) * 4 + warp] = y;
+        }
+    }
+    __syncthreads();
+    // S_h: |score_int| <= (2^b - 1) * sum|Q_c| <= 2^30 (exact int32 accumulation).
+    auto scale_of = [&](int h) {
+        const float sum_abs = (s_red[h * 4 + 0] + s_red[h * 4 + 1]) + (s_red[h * 4 + 2] + s_red[h * 4 + 3]);
+        return sum_abs > 0.0f ? 1073741824.0f / (levels * sum_abs) : 0.0f;
+    };
+    // B fragments: entry (hg, pp, kb, r, lane) packs bytes j = 0..3 of column n = g
+    // (head 4hg + g/2, digit plane 2pp + g%2) at k = 4t + j (+16 for r = 1).
+    for (int e = threadIdx.x; e < NT * 512; e += kWarps * 32) {
+        const int ln = e & 31, r = (e >> 5) & 1, kb = (e >> 6) & 3, pp = (e >> 8) & 1, hg = e >> 9;
+        const int gg = ln >> 2, tt = ln & 3;
+        const int plane = 2 * pp + (gg & 1);
+        const int h = 4 * hg + (gg >> 1);
+        uint32_t word = 0;
+        if (h < G) {
+            const float S_h = scale_of(h);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                int sh;
+                const int ch = k_channel<BITS>(tt, 2 * kb + r, j, sh);
+                const int Q = __float2int_rn(__fmul_rn(s_qs[h * kDim + ch], S_h) * __int_as_float((127 - sh) << 23));
+                // balanced base-256 digits: Q = d0 + 2^8 d1 + 2^16 d2 + 2^24 d3
+                const int d0 = ((Q + 128) & 255) - 128;
+                const int q1 = (Q - d0) >> 8;
+                const int d1 = ((q1 + 128) & 255) - 128;
+                const int q2 = (q1 - d1) >> 8;
+                const int d2 = ((q2 + 128) & 255) - 128;
+                const int d3 = (q2 - d2) >> 8;
+                const int d = plane == 0 ? d0 : plane == 1 ? d1 : plane == 2 ? d2 : d3;
+                word |= (uint32_t)(d & 255) << (8 * j);
+            }
+        }
+        s_frag[e] = word;
+    }
+    __syncthreads();
     uint32_t bq[NT][2][4][2];  // [head group][digit-plane pair][k-block][reg]
-    const uint32_t* fr = p.frag + (size_t)unit * NT * 512;
+    float cA[NT], cB[NT], lo[NT], hi[NT];
 #pragma unroll
     for (int hg = 0; hg < NT; ++hg)
 #pragma unroll
@@ -393,13 +488,19 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_tc_kernel(const TcParam
 #pragma unroll
             for (int kb = 0; kb < 4; ++kb)
 #pragma unroll
-                for (int r = 0; r < 2; ++r) bq[hg][pp][kb][r] = __ldg(fr + (((hg * 2 + pp) * 4 + kb) * 2 + r) * 32 + lane);
-    float cA[NT], cB[NT], lo[NT], hi[NT];
+                for (int r = 0; r < 2; ++r) bq[hg][pp][kb][r] = s_frag[(((hg * 2 + pp) * 4 + kb) * 2 + r) * 32 + lane];
 #pragma unroll
     for (int hg = 0; hg < NT; ++hg) {
         const int h = 4 * hg + t;  // this lane's head in C columns 2t, 2t+1
-        const float2 qc = h < G ? p.qconst[(size_t)unit * G + h] : make_float2(0.f, 0.f);
-        cA[hg] = qc.x, cB[hg] = qc.y;
+        float ca = 0.f, cb = 0.f;
+        if (h < G) {
+            const float S_h = scale_of(h);
+            const float qdota = (s_red[(8 + h) * 4 + 0] + s_red[(8 + h) * 4 + 1]) +
+                                (s_red[(8 + h) * 4 + 2] + s_red[(8 + h) * 4 + 3]);
+            ca = S_h > 0.0f ? isd0 / S_h : 0.0f;
+            cb = qdota * isd0;
+        }
+        cA[hg] = ca, cB[hg] = cb;
         lo[hg] = INFINITY, hi[hg] = -INFINITY;
     }
 
@@ -501,6 +602,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_tc_kernel(const TcParam
         if (lane == 0 && st + kStagesW < total_stages) issue(st + kStagesW);
     }
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");  // scores are in tensor memory
+    if (lane == 0) TTRACE(8 + warp);  // phase A done, per warp
 
     // fp32 tail rows (rank 0): warp w takes rows w, w + NW, ...; lanes split the 128
     // channels; q rows are loaded once.
@@ -594,6 +696,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_tc_kernel(const TcParam
     }
     __syncthreads();
 
+    if (threadIdx.x == 0) TTRACE(1);  // softmax parameters known
     // ---------------- phase B: p . V over this warp's tokens ----------------
     // D[16 head-planes x 8 ch] += P[16 head-planes x 32 tok] * V[32 tok x 8 ch], 16 channel
     // tiles per 32-token block. Lane (g, t) turns its own four scores of head t (tokens
@@ -708,13 +811,15 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_tc_kernel(const TcParam
         if (lane == 0 && (blk == kBps - 1 || b == nblk_all - 1) && i + kStagesW < total_stages) issue(i + kStagesW);
     }
 
+    if (lane == 0) TTRACE(16 + warp);  // phase B done, per warp
     // ---------------- CTA reduction (exact integer sums in shared memory) ----------------
+    // Image layout [mt][nc][r][lane]: consecutive lanes hit consecutive banks.
 #pragma unroll
     for (int mt = 0; mt < NT; ++mt) {
 #pragma unroll
         for (int nc = 0; nc < 16; ++nc)
 #pragma unroll
-            for (int r = 0; r < 4; ++r) red_add_u32(sm.acc + ((mt * 16 + nc) * 32 + lane) * 4 + r, (uint32_t)vacc[mt][nc][r]);
+            for (int r = 0; r < 4; ++r) red_add_u32(sm.acc + ((mt * 16 + nc) * 4 + r) * 32 + lane, (uint32_t)vacc[mt][nc][r]);
         uint32_t w = wacc[mt];
         w += __shfl_xor_sync(0xffffffffu, w, 4);
         w += __shfl_xor_sync(0xffffffffu, w, 8);
@@ -723,27 +828,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_tc_kernel(const TcParam
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();  // (the V stream is drained: the ring is free from here on)
-    // Scatter the accumulator image into planes[plane][head][ch].
-    uint32_t* planes = reinterpret_cast<uint32_t*>(sm.ring);  // [3][4 NT][128 + 1]
-    constexpr int PS = kDim + 1;
-    for (int e = threadIdx.x; e < NT * 16 * 128; e += kWarps * 32) {
-        const int mt = e / (16 * 128), rem = e % (16 * 128);
-        const int nc = rem >> 7, ln = (rem >> 2) & 31, r = rem & 3;
-        const int gg = ln >> 2, tt = ln & 3;
-        const int row = gg + 8 * (r >> 1);
-        if (row >= 12) continue;  // rows 12..15 are empty (3 digit planes)
-        const uint32_t sum = sm.acc[(mt * 16 * 32) * 4 + rem];
-        const int plane = row >> 2, head = 4 * mt + (row & 3);
-        int sh;
-        const int ch = v_channel<BITS>(2 * tt + (r & 1), nc, sh);
-        planes[(plane * 4 * NT + head) * PS + ch] = sum;
-    }
-    __syncthreads();
-    // Pass 2, thread per (head, channel):
+    // Output, thread per (head, channel), straight from the accumulator image:
     //   out = (s_c V / 2^sh + alpha_c W_vis + sum_t p_t v_tc) / (W_vis + sum_t p_t)
     // on the common kPScale weight scale; tail weights recomputed in fp32 (rank 0).
-    constexpr float kInvLevels = 1.0f / (float)((1u << BITS) - 1u);
-    float* recv = reinterpret_cast<float*>(sm.ring + ((size_t)3 * 4 * NT * PS * 4 + 127) / 128 * 128);
+    float* recv = reinterpret_cast<float*>(sm.ring);
     if (S > 1) {  // every CTA's ring is drained before rank 0's becomes the receive buffer
         __syncwarp();
         cluster_arrive();  // #2a
@@ -752,17 +840,25 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_tc_kernel(const TcParam
     for (int idx = threadIdx.x; idx < G * kDim; idx += kWarps * 32) {
         const int h = idx / kDim, ch = idx % kDim;
         constexpr int cpb = Gm::kCpb;
-        const int sh = (cpb - 1 - ch % cpb) * BITS;
-        const uint32_t* pl = planes + h * PS;
-        const float V = __fmaf_rn((float)pl[2 * 4 * NT * PS + ch], 65536.0f,
-                                  __fmaf_rn((float)pl[4 * NT * PS + ch], 256.0f, (float)pl[ch])) *
-                        __int_as_float((127 - sh) << 23);
+        // invert v_channel: ch = (2 BITS g' + q) cpb + (cpb - 1 - s), nc = q cpb + s, and
+        // accumulator column g' = 2 tt + (r & 1), row = plane*4 + head%4 = gg + 8 (r >> 1)
+        const int s_slot = cpb - 1 - ch % cpb, rem = ch / cpb;
+        const int gcol = rem / (2 * BITS), qq = rem % (2 * BITS);
+        const int nc = qq * cpb + s_slot, tt = gcol >> 1, rlo = gcol & 1;
+        const int mt = h >> 2, hh = h & 3;
+        uint32_t pl[3];
+#pragma unroll
+        for (int plane = 0; plane < 3; ++plane) {
+            const int row = plane * 4 + hh;
+            const int gg = row & 7, r = ((row >> 3) << 1) | rlo;
+            pl[plane] = sm.acc[((mt * 16 + nc) * 4 + r) * 32 + gg * 4 + tt];
+        }
+        const float V = __fmaf_rn((float)pl[2], 65536.0f, __fmaf_rn((float)pl[1], 256.0f, (float)pl[0])) *
+                        __int_as_float((127 - s_slot * BITS) << 23);
         unsigned long long ws = 0;
         for (int w2 = 0; w2 < kWarps; ++w2) ws += sm.wsum[w2 * 8 + h];
         const float wv = (float)ws;
-        const float va = __ldg(a.v_alpha + unit * kDim + ch);
-        const float step = fmaxf(__fsub_rn(__ldg(a.v_beta + unit * kDim + ch), va) * kInvLevels, 0.0f);
-        float num = __fmaf_rn(step, V, va * wv), den = wv;
+        float num = __fmaf_rn(v_step, V, v_a * wv), den = wv;
         const float* vt = a.v_tail + (size_t)unit * a.tail_cap * kDim + ch;
         int j = 0;
         for (; j + 8 <= ntl; j += 8) {  // 8 independent loads in flight, j ascending
@@ -804,6 +900,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_tc_kernel(const TcParam
             }
         }
     }
+    if (threadIdx.x == 0) TTRACE(5);
     if (warp == 0) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(kTmemCols));
@@ -815,22 +912,19 @@ void plan(const DecodeArgs& a, int& S, int& T) {
     T = kCtaTokens;
 }
 
-template <int BITS, int NT>
-cudaError_t launch_bits(const DecodeArgs& a, cudaStream_t s) {
+template <int BITS, int NT, int OCC>
+cudaError_t launch_occ(const DecodeArgs& a, cudaStream_t s) {
     int S, T;
     plan(a, S, T);
-    prep_kernel<BITS><<<(unsigned)a.units, kDim, 0, s>>>(a, NT, a.tc_frag, a.tc_qconst);
-    note_launch();
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
+    cudaError_t e = cudaSuccess;
     TcParams p{a, a.tc_frag, a.tc_qconst, S, T};
     // TMEM: kTmemCols per CTA; never let more CTAs share an SM than TMEM can serve (a
     // blocked tcgen05.alloc inside a cluster could deadlock against its partners).
     const size_t max_ctas = NT == 1 ? 4 : 2;
-    size_t smem = tc_smem_bytes<BITS, NT>(S);
+    size_t smem = tc_smem_bytes<BITS, NT, OCC>(S);
     const size_t floor_bytes = 232448 / (max_ctas + 1) + 1;
     if (smem < floor_bytes) smem = floor_bytes;
-    auto kern = decode_tc_kernel<BITS, NT>;
+    auto kern = decode_tc_kernel<BITS, NT, OCC>;
     static bool attr_done = false;  // per instantiation
     if (!attr_done) {
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -862,9 +956,24 @@ cudaError_t launch_bits(const DecodeArgs& a, cudaStream_t s) {
 
 size_t decode_tc_scratch_bytes(size_t units) { return units * (2 * 512 * sizeof(uint32_t) + 8 * sizeof(float2)); }
 
+// CTAs per SM the kernel is built for (register bound + ring depth): 2 by default,
+// KVQ_TC_OCC=3 selects the 3-CTA variant (fewer registers, shallower ring).
+static int tc_occ() {
+    static int occ = [] {
+        const char* e = std::getenv("KVQ_TC_OCC");
+        return e && e[0] == '3' ? 3 : 2;
+    }();
+    return occ;
+}
+
+template <int BITS, int NT>
+cudaError_t launch_bits(const DecodeArgs& a, cudaStream_t s) {
+    return tc_occ() == 3 ? launch_occ<BITS, NT, 3>(a, s) : launch_occ<BITS, NT, 2>(a, s);
+}
+
 template <int BITS, int NT>
 static size_t tc_smem_for(int S) {
-    return tc_smem_bytes<BITS, NT>(S);
+    return tc_occ() == 3 ? tc_smem_bytes<BITS, NT, 3>(S) : tc_smem_bytes<BITS, NT, 2>(S);
 }
 
 bool decode_tc_supported(const DecodeArgs& a) {

@@ -198,6 +198,30 @@ kvqb::DecodeArgs decode_args(kvq_cache* c, const float* q, float* out) {
     return a;
 }
 
+// Debug timeline: KVQ_TRACE_FILE=path dumps 256 globaltimer stamps per CTA of each
+// tensor-core decode (tools/trace_decode.py reads it). Off the measured path.
+template <typename F>
+void traced(kvq_cache* c, kvqb::DecodeArgs& a, cudaStream_t s, F&& launch) {
+    static const char* trace_file = std::getenv("KVQ_TRACE_FILE");
+    if (!trace_file) {
+        launch();
+        return;
+    }
+    const size_t trace_n = c->units * 256 * 16;
+    DevBuf<unsigned long long> trace(trace_n);
+    ck(cudaMemsetAsync(trace.p, 0, trace_n * 8, s), "trace");
+    a.trace = trace.p;
+    launch();
+    std::vector<unsigned long long> h(trace_n);
+    trace.download(h.data(), trace_n, s);
+    sync(s);
+    if (FILE* f = std::fopen(trace_file, "wb")) {
+        std::fwrite(h.data(), 8, h.size(), f);
+        std::fclose(f);
+    }
+    a.trace = nullptr;
+}
+
 void ensure_vt(kvq_cache* c, cudaStream_t s);
 
 void run_decode(kvq_cache* c, const float* q, float* out, bool want_weights, bool want_viol,
@@ -226,26 +250,7 @@ void run_decode(kvq_cache* c, const float* q, float* out, bool want_weights, boo
         if (c->tc_scratch.n < need) c->tc_scratch.alloc(need);
         a.umma_qb = c->tc_scratch.p;
         a.tc_qconst = reinterpret_cast<float2*>(c->tc_scratch.p + c->units * 2 * 512 * sizeof(uint32_t));
-        // Debug timeline: KVQ_TRACE_FILE=path dumps 256 globaltimer stamps per CTA of this
-        // decode (tools/trace_summary.py reads it). Off the measured path.
-        static const char* trace_file = std::getenv("KVQ_TRACE_FILE");
-        DevBuf<unsigned long long> trace;
-        const size_t trace_n = c->units * 256 * 16;
-        if (trace_file) {
-            trace.alloc(trace_n);
-            ck(cudaMemsetAsync(trace.p, 0, trace_n * 8, s), "trace");
-            a.trace = trace.p;
-        }
-        ck(kvqb::launch_decode_umma(a, s), "decode (umma)");
-        if (trace_file) {
-            std::vector<unsigned long long> h(trace_n);
-            trace.download(h.data(), trace_n, s);
-            sync(s);
-            if (FILE* f = std::fopen(trace_file, "wb")) {
-                std::fwrite(h.data(), 8, h.size(), f);
-                std::fclose(f);
-            }
-        }
+        traced(c, a, s, [&] { ck(kvqb::launch_decode_umma(a, s), "decode (umma)"); });
         return;
     }
     if ((c->path == KVQ_PATH_AUTO || c->path == KVQ_PATH_TC) && tc_ok) {
@@ -253,7 +258,7 @@ void run_decode(kvq_cache* c, const float* q, float* out, bool want_weights, boo
         if (c->tc_scratch.n < need) c->tc_scratch.alloc(need);
         a.tc_frag = reinterpret_cast<uint32_t*>(c->tc_scratch.p);
         a.tc_qconst = reinterpret_cast<float2*>(c->tc_scratch.p + c->units * 2 * 512 * sizeof(uint32_t));
-        ck(kvqb::launch_decode_tc(a, s), "decode (tc)");
+        traced(c, a, s, [&] { ck(kvqb::launch_decode_tc(a, s), "decode (tc)"); });
         return;
     }
     size_t need = c->units * c->group * (c->n_vis + c->tail_cap);

@@ -42,6 +42,10 @@ __global__ void mma_loop(int iters, float* sink) {
         asm volatile("mma.sync.aligned.m16n8k16.row.col.f16.f16.f16.f16 {%0,%1}, {%2,%3,%4,%5}, {%6,%7}, {%0,%1};"
                      : "+r"(cc[0]), "+r"(cc[1])
                      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+      } else if (KIND == 7) {
+        asm volatile("mma.sync.aligned.m16n8k64.row.col.s32.u4.s4.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+                     : "+r"(ci[j][0]), "+r"(ci[j][1]), "+r"(ci[j][2]), "+r"(ci[j][3])
+                     : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
       } else if (KIND == 6) {
         // 1-bit and.popc (emulated?)
         asm volatile("mma.sync.aligned.m16n8k256.row.col.s32.b1.b1.s32.and.popc {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
@@ -77,11 +81,11 @@ int main() {
   float* sink; cudaMalloc(&sink, 4096);
   const char* names[] = {"HMMA m16n8k16 f16->f32", "IMMA m16n8k32 s8", "IMMA m16n8k32 u8.s8",
                          "FP8 m16n8k32 e4m3->f32", "HMMA m16n8k16 bf16->f32", "HMMA m16n8k16 f16->f16",
-                         "BMMA m16n8k256 and.popc"};
-  const double macs[] = {16*8*16, 16*8*32, 16*8*32, 16*8*32, 16*8*16, 16*8*16, 16*8*256};
+                         "BMMA m16n8k256 and.popc", "IMMA m16n8k64 u4.s4"};
+  const double macs[] = {16*8*16, 16*8*32, 16*8*32, 16*8*32, 16*8*16, 16*8*16, 16*8*256, 16*8*64};
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   for (int warps = 4; warps <= 16; warps *= 2) {
-    for (int k = 0; k < 7; ++k) {
+    for (int k = 0; k < 8; ++k) {
       int iters = 2000;
       int blocks = p.multiProcessorCount * 2;
       auto launch = [&]() {
@@ -93,6 +97,7 @@ int main() {
           case 4: mma_loop<4><<<blocks, warps * 32>>>(iters, sink); break;
           case 5: mma_loop<5><<<blocks, warps * 32>>>(iters, sink); break;
           case 6: mma_loop<6><<<blocks, warps * 32>>>(iters, sink); break;
+          case 7: mma_loop<7><<<blocks, warps * 32>>>(iters, sink); break;
         }
       };
       launch(); cudaDeviceSynchronize();
