@@ -244,7 +244,9 @@ constexpr int kSteps = kWarpTokens / 32;  // 32-token steps per warp
 // the ~2 us bulk-copy latency measured under load (profiles/r01_trace_umma_c2.txt).
 template <int BITS, int OCC>
 constexpr int ring_stages() {
-    return OCC >= 3 ? (Geo<BITS>::kStageBytesB >= 4096 ? 2 : 3) : (Geo<BITS>::kStageBytesB >= 4096 ? 3 : 5);
+    return OCC >= 3   ? (Geo<BITS>::kStageBytesB >= 4096 ? 2 : 3)
+           : OCC == 2 ? (Geo<BITS>::kStageBytesB >= 4096 ? 3 : 5)
+                      : (Geo<BITS>::kStageBytesB >= 4096 ? 4 : 8);  // one CTA per SM (G > 4)
 }
 
 struct Smem {  // carve-up of the dynamic shared memory of one decode CTA
@@ -361,8 +363,9 @@ __global__ void __launch_bounds__(kWarps * 32, OCC) decode_tc_kernel(const TcPar
     uint64_t* full = sm.full + warp * kStagesW;
 
     const int n = (int)a.n_vis;
-    const int tok0 = rank * kCtaTokens + warp * kWarpTokens;  // this warp's first token
-    const int nv = max(0, min(kWarpTokens, n - tok0));
+    const int wt = p.T / kWarps;                        // tokens per warp (multiple of 32, <= 512)
+    const int tok0 = rank * p.T + warp * wt;              // this warp's first token
+    const int nv = max(0, min(wt, n - tok0));
     const int ntl = rank == 0 ? a.tail_len[unit / a.kv_heads] : 0;  // fp32 tail: rank 0
     const uint8_t* kcodes = a.k_codes + ((size_t)unit * n + tok0) * Gm::kRowBytes;
     const uint8_t* vcodes = a.v_codes + ((size_t)unit * n + tok0) * Gm::kRowBytes;
@@ -915,9 +918,17 @@ __global__ void __launch_bounds__(kWarps * 32, OCC) decode_tc_kernel(const TcPar
     }
 }
 
+// Token split: at most 4096 tokens per CTA; small batches split units further (down to
+// 256 tokens per CTA) so that units x S fills ~2 CTAs per SM - a single unit otherwise
+// runs on one SM for its full latency.
 void plan(const DecodeArgs& a, int& S, int& T) {
-    S = std::max(1, (int)((a.n_vis + kCtaTokens - 1) / kCtaTokens));
-    T = kCtaTokens;
+    const int n = (int)a.n_vis;
+    int s_min = std::max(1, (n + kCtaTokens - 1) / kCtaTokens);
+    const int want = (int)((2 * 148 + a.units - 1) / a.units);
+    int s = std::max(s_min, std::min(want, kMaxCluster));
+    s = std::min(s, std::max(1, (n + 255) / 256));
+    T = ((n + s - 1) / s + 255) / 256 * 256;  // multiple of 8 warps x 32 tokens
+    S = (n + T - 1) / T;
 }
 
 template <int BITS, int NT, int OCC>
@@ -928,7 +939,7 @@ cudaError_t launch_occ(const DecodeArgs& a, cudaStream_t s) {
     TcParams p{a, a.tc_frag, a.tc_qconst, S, T};
     // TMEM: kTmemCols per CTA; never let more CTAs share an SM than TMEM can serve (a
     // blocked tcgen05.alloc inside a cluster could deadlock against its partners).
-    const size_t max_ctas = NT == 1 ? 4 : 2;
+    const size_t max_ctas = OCC == 1 ? 1 : (NT == 1 ? 4 : 2);
     size_t smem = tc_smem_bytes<BITS, NT, OCC>(S);
     const size_t floor_bytes = 232448 / (max_ctas + 1) + 1;
     if (smem < floor_bytes) smem = floor_bytes;
@@ -974,14 +985,23 @@ static int tc_occ() {
     return occ;
 }
 
+// G > 4 (two head groups) needs ~180 registers: one CTA per SM, no spills.
 template <int BITS, int NT>
 cudaError_t launch_bits(const DecodeArgs& a, cudaStream_t s) {
-    return tc_occ() == 3 ? launch_occ<BITS, NT, 3>(a, s) : launch_occ<BITS, NT, 2>(a, s);
+    if constexpr (NT == 2) {
+        return launch_occ<BITS, NT, 1>(a, s);
+    } else {
+        return tc_occ() == 3 ? launch_occ<BITS, NT, 3>(a, s) : launch_occ<BITS, NT, 2>(a, s);
+    }
 }
 
 template <int BITS, int NT>
 static size_t tc_smem_for(int S) {
-    return tc_occ() == 3 ? tc_smem_bytes<BITS, NT, 3>(S) : tc_smem_bytes<BITS, NT, 2>(S);
+    if constexpr (NT == 2) {
+        return tc_smem_bytes<BITS, NT, 1>(S);
+    } else {
+        return tc_occ() == 3 ? tc_smem_bytes<BITS, NT, 3>(S) : tc_smem_bytes<BITS, NT, 2>(S);
+    }
 }
 
 bool decode_tc_supported(const DecodeArgs& a) {
