@@ -125,6 +125,8 @@ struct kvq_cache {
     size_t n_tail = 0, tail_cap = 0;
     int path = KVQ_PATH_AUTO;
     cudaStream_t stream = nullptr;
+    cudaStream_t side = nullptr;       // kvq_cache_step: new K/V rows upload + append
+    cudaEvent_t decoded = nullptr;     // kvq_cache_step: decode retired -> append may run
     DevBuf<uint8_t> codes;   // [2][units][n_vis][rb]  (K then V)
     DevBuf<uint8_t> vt;      // token-packed V codes for the tcgen05 decode (d = 128, M = 8)
     DevBuf<float> stats;     // [2 (K,V)][2 (alpha,beta)][units][dim]
@@ -143,6 +145,8 @@ struct kvq_cache {
     size_t q_elems() const { return units * group * dim; }
     ~kvq_cache() {
         if (stream) cudaStreamDestroy(stream);
+        if (side) cudaStreamDestroy(side);
+        if (decoded) cudaEventDestroy(decoded);
     }
 };
 
@@ -704,15 +708,25 @@ int kvq_cache_decode_device(kvq_cache* c, const float* queries, float* out, void
 int kvq_cache_step(kvq_cache* c, const float* queries, const float* k_new, const float* v_new, float* out) {
     return guarded([&] {
         grow_tail(c, c->n_tail + 1);
-        cudaStream_t s = c->stream;
+        if (!c->side) {
+            ck(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking), "stream");
+            ck(cudaEventCreateWithFlags(&c->decoded, cudaEventDisableTiming), "event");
+        }
+        // Two streams: the queries upload feeds the decode; the new K/V rows upload overlaps
+        // it and the append waits for the decode (which must not see the new row); the
+        // output download overlaps the append.
+        cudaStream_t s = c->stream, s2 = c->side;
         c->d_q.upload(queries, c->q_elems(), s);
-        c->d_knew.upload(k_new, c->units * c->dim, s);
-        c->d_vnew.upload(v_new, c->units * c->dim, s);
+        c->d_knew.upload(k_new, c->units * c->dim, s2);
+        c->d_vnew.upload(v_new, c->units * c->dim, s2);
         run_decode(c, c->d_q.p, c->d_out.p, false, false, s);
-        ck(kvqb::launch_append(c->d_knew.p, c->d_vnew.p, c->batch, c->kv_heads, c->dim, c->tail_cap,
-                               c->k_tail.p, c->v_tail.p, c->tail_len.p, s), "append");
+        ck(cudaEventRecord(c->decoded, s), "event");
         c->d_out.download(out, c->q_elems(), s);
+        ck(cudaStreamWaitEvent(s2, c->decoded, 0), "event");
+        ck(kvqb::launch_append(c->d_knew.p, c->d_vnew.p, c->batch, c->kv_heads, c->dim, c->tail_cap,
+                               c->k_tail.p, c->v_tail.p, c->tail_len.p, s2), "append");
         sync(s);
+        sync(s2);
         c->n_tail += 1;
     });
 }
