@@ -368,7 +368,8 @@ __global__ void __launch_bounds__(kWarps * 32, OCC) decode_tc_kernel(const TcPar
     const int nv = max(0, min(wt, n - tok0));
     const int ntl = rank == 0 ? a.tail_len[unit / a.kv_heads] : 0;  // fp32 tail: rank 0
     const uint8_t* kcodes = a.k_codes + ((size_t)unit * n + tok0) * Gm::kRowBytes;
-    const uint8_t* vcodes = a.v_codes + ((size_t)unit * n + tok0) * Gm::kRowBytes;
+    const int nb32 = (n + 31) >> 5;  // 32-token blocks of the unit (vx_layout)
+    const uint8_t* vcodes = a.v_codes_x + ((size_t)unit * nb32 + (tok0 >> 5)) * (size_t)(32 * Gm::kRowBytes);
     const int nstage = (nv + Gm::kStageTokens - 1) / Gm::kStageTokens;
     const int total_stages = 2 * nstage;
 
@@ -376,7 +377,9 @@ __global__ void __launch_bounds__(kWarps * 32, OCC) decode_tc_kernel(const TcPar
         const int slot = i % kStagesW;
         const int si = i < nstage ? i : i - nstage;
         const uint8_t* src = (i < nstage ? kcodes : vcodes) + (size_t)si * Gm::kStageBytesB;
-        const uint32_t bytes = (uint32_t)(min(Gm::kStageTokens, nv - si * Gm::kStageTokens) * Gm::kRowBytes);
+        const int rows_left = min(Gm::kStageTokens, nv - si * Gm::kStageTokens);
+        // K: exact rows; V (vx_layout): whole 32-token blocks (zero-padded past n)
+        const uint32_t bytes = (uint32_t)((i < nstage ? rows_left : (rows_left + 31) / 32 * 32) * Gm::kRowBytes);
         mbar_expect_tx(&full[slot], bytes);
         bulk_g2s(ring + slot * Gm::kStageBytesB, src, bytes, &full[slot]);
     };
@@ -774,38 +777,19 @@ __global__ void __launch_bounds__(kWarps * 32, OCC) decode_tc_kernel(const TcPar
         }
         if (b + 1 < nblk_all) p_write(b + 1, pw + ((b + 1) & 1) * NT * 12 * kPRow);
         // B operand: V codes of this lane's 2*BITS bytes for the 4 tokens of k-group t
-        // (grp 0) / 4 + t (grp 1): rows 4 grp + t + 8 ii, byte-transposed.
-        constexpr int NW = (2 * BITS + 3) / 4;  // 32-bit words per token slice
+        // (grp 0) / 4 + t (grp 1), byte-transposed ahead of time (vx_layout): one
+        // conflict-free 16*BITS-byte load per lane.
         uint32_t X[2][2 * BITS];
+        {
+            const uint4* xp = reinterpret_cast<const uint4*>(buf + (size_t)(blk * 32 + lane) * 16 * BITS);
 #pragma unroll
-        for (int grp = 0; grp < 2; ++grp) {
-            uint32_t raw[4][NW];
+            for (int u = 0; u < BITS; ++u) {
+                const uint4 v4 = xp[u];
+                const uint32_t w4[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
-            for (int ii = 0; ii < 4; ++ii) {
-                const uint8_t* rp = buf + (blk * 32 + 4 * grp + t + 8 * ii) * Gm::kRowBytes + 2 * BITS * g;
-                if (BITS == 1) {
-                    raw[ii][0] = *reinterpret_cast<const uint16_t*>(rp);
-                } else if (BITS == 2) {
-                    raw[ii][0] = *reinterpret_cast<const uint32_t*>(rp);
-                } else if (BITS == 4) {
-                    const uint2 vv = *reinterpret_cast<const uint2*>(rp);
-                    raw[ii][0] = vv.x, raw[ii][NW - 1] = vv.y;
-                } else {
-                    const uint4 vv = *reinterpret_cast<const uint4*>(rp);
-                    raw[ii][0] = vv.x, raw[ii][1 % NW] = vv.y, raw[ii][2 % NW] = vv.z, raw[ii][3 % NW] = vv.w;
-                }
-            }
-#pragma unroll
-            for (int wi = 0; wi < NW; ++wi) {
-                const uint32_t P0 = prmt(raw[0][wi], raw[1][wi], 0x5140);
-                const uint32_t P2 = prmt(raw[2][wi], raw[3][wi], 0x5140);
-                X[grp][(4 * wi + 0) % (2 * BITS)] = prmt(P0, P2, 0x5410);
-                X[grp][(4 * wi + 1) % (2 * BITS)] = prmt(P0, P2, 0x7632);
-                if (2 * BITS > 2) {
-                    const uint32_t P1 = prmt(raw[0][wi], raw[1][wi], 0x7362);
-                    const uint32_t P3 = prmt(raw[2][wi], raw[3][wi], 0x7362);
-                    X[grp][(4 * wi + 2) % (2 * BITS)] = prmt(P1, P3, 0x5410);
-                    X[grp][(4 * wi + 3) % (2 * BITS)] = prmt(P1, P3, 0x7632);
+                for (int k = 0; k < 4; ++k) {
+                    const int idx = 4 * u + k;
+                    X[idx / (2 * BITS)][idx % (2 * BITS)] = w4[k];
                 }
             }
         }
@@ -973,6 +957,76 @@ cudaError_t launch_occ(const DecodeArgs& a, cudaStream_t s) {
 
 }  // namespace
 
+// ---- vx_layout: V codes pre-arranged as the phase-B B operand ---------------------------
+// [unit][32-token block][lane 32][2 grp][2*BITS words]: word w of group grp of lane (g, t)
+// holds, byte-transposed, the 2*BITS code bytes of channel group g of the four tokens
+// 4 grp + t + 8 ii (ii = 0..3) of the block - exactly the registers the decode used to
+// build from token-major rows with PRMT. Tokens past n are zero codes. Built once per
+// cache (pack_vx_kernel); the reference-layout V copy stays for read-back.
+namespace {
+template <int BITS>
+__global__ void __launch_bounds__(32) pack_vx_kernel(const uint8_t* __restrict__ rows, size_t n, size_t nb32,
+                                                     uint8_t* __restrict__ vx) {
+    constexpr int kRowBytes = 16 * BITS;
+    constexpr int NW = (2 * BITS + 3) / 4;
+    const size_t unit = blockIdx.y, blk = blockIdx.x;
+    const int lane = threadIdx.x, g = lane >> 2, t = lane & 3;
+    uint32_t X[2][2 * BITS];
+#pragma unroll
+    for (int grp = 0; grp < 2; ++grp) {
+        uint32_t raw[4][NW];
+#pragma unroll
+        for (int ii = 0; ii < 4; ++ii) {
+            const size_t tok = blk * 32 + 4 * grp + t + 8 * ii;
+            const uint8_t* rp = rows + (unit * n + tok) * kRowBytes + 2 * BITS * g;
+#pragma unroll
+            for (int wi = 0; wi < NW; ++wi) {
+                uint32_t w = 0;
+                for (int by = 0; by < 4 && 4 * wi + by < 2 * BITS; ++by)
+                    w |= (tok < n ? (uint32_t)rp[4 * wi + by] : 0u) << (8 * by);
+                raw[ii][wi] = w;
+            }
+        }
+#pragma unroll
+        for (int wi = 0; wi < NW; ++wi) {
+            const uint32_t P0 = prmt(raw[0][wi], raw[1][wi], 0x5140);
+            const uint32_t P2 = prmt(raw[2][wi], raw[3][wi], 0x5140);
+            X[grp][(4 * wi + 0) % (2 * BITS)] = prmt(P0, P2, 0x5410);
+            X[grp][(4 * wi + 1) % (2 * BITS)] = prmt(P0, P2, 0x7632);
+            if (2 * BITS > 2) {
+                const uint32_t P1 = prmt(raw[0][wi], raw[1][wi], 0x7362);
+                const uint32_t P3 = prmt(raw[2][wi], raw[3][wi], 0x7362);
+                X[grp][(4 * wi + 2) % (2 * BITS)] = prmt(P1, P3, 0x5410);
+                X[grp][(4 * wi + 3) % (2 * BITS)] = prmt(P1, P3, 0x7632);
+            }
+        }
+    }
+    uint32_t* dst = reinterpret_cast<uint32_t*>(vx + ((unit * nb32 + blk) * 32 + lane) * (size_t)(16 * BITS));
+#pragma unroll
+    for (int grp = 0; grp < 2; ++grp)
+#pragma unroll
+        for (int w = 0; w < 2 * BITS; ++w) dst[grp * 2 * BITS + w] = X[grp][w];
+}
+
+}  // namespace
+
+size_t vx_bytes(size_t units, size_t n_vis, int bits) { return units * ((n_vis + 31) / 32) * 32 * 16 * (size_t)bits; }
+
+cudaError_t launch_pack_vx(const uint8_t* rows, size_t units, size_t n_vis, int bits, uint8_t* vx, cudaStream_t s) {
+    if (n_vis == 0 || units == 0) return cudaSuccess;
+    const size_t nb32 = (n_vis + 31) / 32;
+    dim3 grid((unsigned)nb32, (unsigned)units);
+    switch (bits) {
+        case 1: pack_vx_kernel<1><<<grid, 32, 0, s>>>(rows, n_vis, nb32, vx); break;
+        case 2: pack_vx_kernel<2><<<grid, 32, 0, s>>>(rows, n_vis, nb32, vx); break;
+        case 4: pack_vx_kernel<4><<<grid, 32, 0, s>>>(rows, n_vis, nb32, vx); break;
+        case 8: pack_vx_kernel<8><<<grid, 32, 0, s>>>(rows, n_vis, nb32, vx); break;
+        default: return cudaErrorInvalidValue;
+    }
+    note_launch();
+    return cudaGetLastError();
+}
+
 size_t decode_tc_scratch_bytes(size_t units) { return units * (2 * 512 * sizeof(uint32_t) + 8 * sizeof(float2)); }
 
 // CTAs per SM the kernel is built for (register bound + ring depth): 2 by default,
@@ -1005,7 +1059,7 @@ static size_t tc_smem_for(int S) {
 }
 
 bool decode_tc_supported(const DecodeArgs& a) {
-    if (a.dim != (size_t)kDim || a.word_bits != 8 || a.n_vis == 0) return false;
+    if (a.dim != (size_t)kDim || a.word_bits != 8 || a.n_vis == 0 || !a.v_codes_x) return false;
     if (a.bits != 1 && a.bits != 2 && a.bits != 4 && a.bits != 8) return false;
     if (a.group < 1 || a.group > 8) return false;
     if (a.units == 0) return false;

@@ -129,6 +129,7 @@ struct kvq_cache {
     cudaEvent_t decoded = nullptr;     // kvq_cache_step: decode retired -> append may run
     DevBuf<uint8_t> codes;   // [2][units][n_vis][rb]  (K then V)
     DevBuf<uint8_t> vt;      // token-packed V codes for the tcgen05 decode (d = 128, M = 8)
+    DevBuf<uint8_t> vx;      // V codes pre-arranged as IMMA operands for the default decode
     DevBuf<float> stats;     // [2 (K,V)][2 (alpha,beta)][units][dim]
     DevBuf<float> k_tail, v_tail;  // [units][tail_cap][dim]
     DevBuf<int> tail_len;    // [batch]
@@ -180,6 +181,7 @@ kvqb::DecodeArgs decode_args(kvq_cache* c, const float* q, float* out) {
     a.k_codes = c->k_codes();
     a.v_codes = c->v_codes();
     a.v_codes_t = c->vt.p;
+    a.v_codes_x = c->vx.p;
     a.k_alpha = c->k_alpha();
     a.k_beta = c->k_beta();
     a.v_alpha = c->v_alpha();
@@ -227,11 +229,16 @@ void traced(kvq_cache* c, kvqb::DecodeArgs& a, cudaStream_t s, F&& launch) {
 }
 
 void ensure_vt(kvq_cache* c, cudaStream_t s);
+void ensure_vx(kvq_cache* c, cudaStream_t s);
 
 void run_decode(kvq_cache* c, const float* q, float* out, bool want_weights, bool want_viol,
                 cudaStream_t s) {
     kvqb::DecodeArgs a = decode_args(c, q, out);
     const bool plain = !want_weights && !want_viol;
+    if (plain && c->path != KVQ_PATH_GENERIC && c->path != KVQ_PATH_UMMA) {
+        ensure_vx(c, s);
+        a.v_codes_x = c->vx.p;
+    }
     kvqb::DecodeArgs probe = a;
     probe.v_codes_t = reinterpret_cast<const uint8_t*>(1);  // shape check only
     const bool umma_ok = plain && c->dim == 128 && c->word_bits == 8 && kvqb::decode_umma_supported(probe);
@@ -250,6 +257,7 @@ void run_decode(kvq_cache* c, const float* q, float* out, bool want_weights, boo
     if ((c->path == KVQ_PATH_UMMA || (c->path == KVQ_PATH_AUTO && !tc_ok)) && umma_ok) {
         ensure_vt(c, s);
         a.v_codes_t = c->vt.p;
+    a.v_codes_x = c->vx.p;
         const size_t need = kvqb::decode_tc_scratch_bytes(c->units);
         if (c->tc_scratch.n < need) c->tc_scratch.alloc(need);
         a.umma_qb = c->tc_scratch.p;
@@ -305,6 +313,8 @@ kvq_cache* build_common(size_t batch, size_t kv_heads, size_t group, size_t n_vi
     c->n_vis = full ? 0 : n_vis;
     c->rb = row_bytes(dim, full ? 8 : bitwidth, c->word_bits);
     ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+    ck(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking), "stream");
+    ck(cudaEventCreateWithFlags(&c->decoded, cudaEventDisableTiming), "event");
     c->stats.alloc(4 * c->units * dim);
     ck(cudaMemsetAsync(c->stats.p, 0, sizeof(float) * c->stats.n, c->stream), "memset");
     c->codes.alloc(2 * c->units * c->n_vis * c->rb);
@@ -338,6 +348,12 @@ void quantize_prefill(kvq_cache* c, const float* dk, const float* dv, cudaStream
 
 // Device layout for the tcgen05 decode: V codes re-packed along the token axis. Built on
 // first use of that path (the default IMMA path reads the reference layout).
+void ensure_vx(kvq_cache* c, cudaStream_t s) {
+    if (c->vx.p || c->dim != 128 || c->word_bits != 8 || c->n_vis == 0) return;
+    c->vx.alloc(kvqb::vx_bytes(c->units, c->n_vis, c->bits));
+    ck(kvqb::launch_pack_vx(c->v_codes(), c->units, c->n_vis, c->bits, c->vx.p, s), "pack vx");
+}
+
 void ensure_vt(kvq_cache* c, cudaStream_t s) {
     if (c->vt.p || c->dim != 128 || c->word_bits != 8 || c->n_vis == 0) return;
     c->vt.alloc(kvqb::vt_bytes(c->units, c->n_vis, c->bits));
@@ -708,10 +724,6 @@ int kvq_cache_decode_device(kvq_cache* c, const float* queries, float* out, void
 int kvq_cache_step(kvq_cache* c, const float* queries, const float* k_new, const float* v_new, float* out) {
     return guarded([&] {
         grow_tail(c, c->n_tail + 1);
-        if (!c->side) {
-            ck(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking), "stream");
-            ck(cudaEventCreateWithFlags(&c->decoded, cudaEventDisableTiming), "event");
-        }
         // Two streams: the queries upload feeds the decode; the new K/V rows upload overlaps
         // it and the append waits for the decode (which must not see the new row); the
         // output download overlaps the append.

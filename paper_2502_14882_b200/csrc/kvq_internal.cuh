@@ -68,6 +68,7 @@ struct DecodeArgs {
     int* violations;      // nullable: [units][group] g slope-violation flags
     float* scratch;       // generic path: [units][group][n_vis + tail_cap] score rows
     const uint8_t* v_codes_t;  // umma path: token-packed V codes (vt_layout, k2_decode_umma.cu)
+    const uint8_t* v_codes_x;  // tc path: V codes as phase-B MMA operands (vx_layout, k2_decode_tc.cu)
     uint8_t* umma_qb;     // umma path: [units][NT][128][16] s8 q digit planes (prep kernel)
     uint32_t* tc_frag;    // tc path: [units][2][512] q-plane MMA fragments (prep kernel)
     float2* tc_qconst;    // tc path: [units][8] per-head score scale / offset
@@ -80,6 +81,8 @@ cudaError_t launch_decode_generic(const DecodeArgs& a, cudaStream_t s);
 bool decode_tc_supported(const DecodeArgs& a);
 size_t decode_tc_scratch_bytes(size_t units);
 cudaError_t launch_decode_tc(const DecodeArgs& a, cudaStream_t s);
+size_t vx_bytes(size_t units, size_t n_vis, int bits);
+cudaError_t launch_pack_vx(const uint8_t* rows, size_t units, size_t n_vis, int bits, uint8_t* vx, cudaStream_t s);
 // tcgen05 (UTCIMMA) path, d = 128, M = 8: needs the token-packed V copy.
 size_t vt_bytes(size_t units, size_t n_vis, int bits);
 cudaError_t launch_pack_vt(const uint8_t* rows, size_t units, size_t n_vis, int bits, uint8_t* vt, cudaStream_t s);
