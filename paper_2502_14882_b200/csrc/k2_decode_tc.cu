@@ -740,13 +740,21 @@ __global__ void __launch_bounds__(kWarps * 32, OCC) decode_tc_kernel(const TcPar
             float sc[4];
             tmem_ld4(tmem_w + (uint32_t)((blk * NT + mt) * 4), sc);
             uint32_t v[4];
+            if (blk * 32 + 32 <= nv) {  // full block (warp-uniform): no per-token checks
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int tok = blk * 32 + 16 * (j >> 1) + 8 * (j & 1) + g;
-                const float pr = tok < nv ? ex2(__fmaf_rn(sc[j], pa[mt], pb[mt])) : 0.0f;
-                v[j] = __float_as_uint(__fmaf_rn(pr, kPScale, kMagic));  // round(p * kPScale) in low bits
-                wacc[mt] += v[j] - 0x4B400000u;
+                for (int j = 0; j < 4; ++j) {
+                    const float pr = ex2(__fmaf_rn(sc[j], pa[mt], pb[mt]));
+                    v[j] = __float_as_uint(__fmaf_rn(pr, kPScale, kMagic));  // round(p * kPScale) in low bits
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int tok = blk * 32 + 16 * (j >> 1) + 8 * (j & 1) + g;
+                    const float pr = tok < nv ? ex2(__fmaf_rn(sc[j], pa[mt], pb[mt])) : 0.0f;
+                    v[j] = __float_as_uint(__fmaf_rn(pr, kPScale, kMagic));
+                }
             }
+            wacc[mt] += (v[0] + v[1]) + (v[2] + v[3]) - 4u * 0x4B400000u;
             const uint32_t p01 = prmt(v[0], v[1], 0x5140), p23 = prmt(v[2], v[3], 0x5140);
             const uint32_t q01 = prmt(v[0], v[1], 0x7362), q23 = prmt(v[2], v[3], 0x7362);
             uint32_t* rowp = tile + (mt * 12 + t) * kPRow + g;
@@ -759,51 +767,56 @@ __global__ void __launch_bounds__(kWarps * 32, OCC) decode_tc_kernel(const TcPar
     const int nblk_all = (nv + 31) >> 5;
     if (nblk_all > 0) p_write(0, pw);
     __syncwarp();
-    for (int b = 0; b < nblk_all; ++b) {
-        const int st = b / kBps, blk = b % kBps;
+    for (int st = 0; st < nstage; ++st) {
         const int i = nstage + st;
         const int slot = i % kStagesW;
-        if (blk == 0) mbar_wait(&full[slot], (i / kStagesW) & 1);
+        mbar_wait(&full[slot], (i / kStagesW) & 1);
         const uint8_t* buf = ring + slot * Gm::kStageBytesB;
-        uint32_t* cur = pw + (b & 1) * NT * 12 * kPRow;
-        uint32_t afr[NT][4];
+        const int nb = min(kBps, nblk_all - st * kBps);
 #pragma unroll
-        for (int mt = 0; mt < NT; ++mt) {
-            const uint32_t* r0 = cur + (mt * 12 + g) * kPRow;
-            afr[mt][0] = r0[t];
-            afr[mt][2] = r0[4 + t];
-            afr[mt][1] = g < 4 ? r0[8 * kPRow + t] : 0u;
-            afr[mt][3] = g < 4 ? r0[8 * kPRow + 4 + t] : 0u;
-        }
-        if (b + 1 < nblk_all) p_write(b + 1, pw + ((b + 1) & 1) * NT * 12 * kPRow);
-        // B operand: V codes of this lane's 2*BITS bytes for the 4 tokens of k-group t
-        // (grp 0) / 4 + t (grp 1), byte-transposed ahead of time (vx_layout): one
-        // conflict-free 16*BITS-byte load per lane.
-        uint32_t X[2][2 * BITS];
-        {
-            const uint4* xp = reinterpret_cast<const uint4*>(buf + (size_t)(blk * 32 + lane) * 16 * BITS);
+        for (int blk = 0; blk < kBps; ++blk) {
+            if (blk >= nb) break;  // warp-uniform
+            const int b = st * kBps + blk;
+            uint32_t* cur = pw + (b & 1) * NT * 12 * kPRow;
+            uint32_t afr[NT][4];
 #pragma unroll
-            for (int u = 0; u < BITS; ++u) {
-                const uint4 v4 = xp[u];
-                const uint32_t w4[4] = {v4.x, v4.y, v4.z, v4.w};
+            for (int mt = 0; mt < NT; ++mt) {
+                const uint32_t* r0 = cur + (mt * 12 + g) * kPRow;
+                afr[mt][0] = r0[t];
+                afr[mt][2] = r0[4 + t];
+                afr[mt][1] = g < 4 ? r0[8 * kPRow + t] : 0u;
+                afr[mt][3] = g < 4 ? r0[8 * kPRow + 4 + t] : 0u;
+            }
+            if (b + 1 < nblk_all) p_write(b + 1, pw + ((b + 1) & 1) * NT * 12 * kPRow);
+            // B operand: V codes of this lane's 2*BITS bytes for the 4 tokens of k-group t
+            // (grp 0) / 4 + t (grp 1), byte-transposed ahead of time (vx_layout): one
+            // conflict-free 16*BITS-byte load per lane.
+            uint32_t X[2][2 * BITS];
+            {
+                const uint4* xp = reinterpret_cast<const uint4*>(buf + (size_t)(blk * 32 + lane) * 16 * BITS);
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int idx = 4 * u + k;
-                    X[idx / (2 * BITS)][idx % (2 * BITS)] = w4[k];
+                for (int u = 0; u < BITS; ++u) {
+                    const uint4 v4 = xp[u];
+                    const uint32_t w4[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int idx = 4 * u + k;
+                        X[idx / (2 * BITS)][idx % (2 * BITS)] = w4[k];
+                    }
                 }
             }
-        }
 #pragma unroll
-        for (int nc = 0; nc < 16; ++nc) {
-            constexpr int cpb = Gm::kCpb;
-            const uint32_t m = Gm::kMask << ((nc % cpb) * BITS);
-            const uint32_t b0 = X[0][nc / cpb] & m, b1 = X[1][nc / cpb] & m;
+            for (int nc = 0; nc < 16; ++nc) {
+                constexpr int cpb = Gm::kCpb;
+                const uint32_t m = Gm::kMask << ((nc % cpb) * BITS);
+                const uint32_t b0 = X[0][nc / cpb] & m, b1 = X[1][nc / cpb] & m;
 #pragma unroll
-            for (int mt = 0; mt < NT; ++mt)
-                imma_u8u8(vacc[mt][nc], afr[mt][0], afr[mt][1], afr[mt][2], afr[mt][3], b0, b1);
+                for (int mt = 0; mt < NT; ++mt)
+                    imma_u8u8(vacc[mt][nc], afr[mt][0], afr[mt][1], afr[mt][2], afr[mt][3], b0, b1);
+            }
+            __syncwarp();
         }
-        __syncwarp();
-        if (lane == 0 && (blk == kBps - 1 || b == nblk_all - 1) && i + kStagesW < total_stages) issue(i + kStagesW);
+        if (lane == 0 && i + kStagesW < total_stages) issue(i + kStagesW);
     }
 
     if (lane == 0) TTRACE(16 + warp);  // phase B done, per warp
