@@ -395,12 +395,8 @@ __global__ void __launch_bounds__(kWarps * 32, OCC) decode_tc_kernel(const TcPar
                      "r"(kTmemCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t tbase = *sm.tmem_slot;
-    // lanes of warp quarter (warp % 4); warps 4..7 use the upper half of the columns
-    const uint32_t tmem_w = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * kSteps * 4 * NT);
+    // (the allocation is published by the first prologue barrier below)
+    if (threadIdx.x == 0) TTRACE(6);
     if (S > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");  // #0
 
     // Warm L2 with the fp32 tail rows (rank 0 reads them after phase A / in the epilogue).
@@ -409,12 +405,15 @@ __global__ void __launch_bounds__(kWarps * 32, OCC) decode_tc_kernel(const TcPar
         const float* ptr = base + ((size_t)unit * a.tail_cap + (l >> 3)) * kDim + 32 * (l & 3);
         asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
     }
-    // V scale / zero-point of this thread's output channel (threadIdx.x % 128), loaded early.
-    constexpr float kInvLevelsV = 1.0f / (float)((1u << BITS) - 1u);
-    const float v_a = __ldg(a.v_alpha + unit * kDim + (threadIdx.x & (kDim - 1)));
-    const float v_step =
-        fmaxf(__fsub_rn(__ldg(a.v_beta + unit * kDim + (threadIdx.x & (kDim - 1))), v_a) * kInvLevelsV, 0.0f);
+    // Cache-build data (stats: stable since the build synchronized) is loaded before the
+    // grid dependency resolves; only q and the tail come from the preceding kernel.
+    const float v_a = __ldg(a.v_alpha + unit * kDim + (threadIdx.x & (kDim - 1)));   // output channel
+    const float v_b = __ldg(a.v_beta + unit * kDim + (threadIdx.x & (kDim - 1)));
+    const float k_a = __ldg(a.k_alpha + unit * kDim + (threadIdx.x & (kDim - 1)));   // prologue channel
+    const float k_b = __ldg(a.k_beta + unit * kDim + (threadIdx.x & (kDim - 1)));
+    if (threadIdx.x == 0) TTRACE(7);
     griddep_wait();  // the previous step's append (tail rows, tail_len) and q are visible from here on
+    if (threadIdx.x == 0) TTRACE(3);
 
     // ---- fold the K scales into the query (scale_query, kernels.hpp:183-194) ----
     // Q'_c = round(S_h qs_c / 2^sh_c) in 4 balanced int8 digit planes, S_h bounding the
@@ -427,8 +426,7 @@ __global__ void __launch_bounds__(kWarps * 32, OCC) decode_tc_kernel(const TcPar
     const float isd0 = __fdiv_rn(1.0f, sqrtf((float)kDim));
     if (threadIdx.x < kDim) {
         const int c = threadIdx.x;
-        const float ka = a.k_alpha[unit * kDim + c];
-        const float kbeta = a.k_beta[unit * kDim + c];
+        const float ka = k_a, kbeta = k_b;
         float qv[8];
 #pragma unroll
         for (int h = 0; h < 8; ++h) qv[h] = h < G ? a.q[(unit * G + h) * kDim + c] : 0.0f;
@@ -458,7 +456,12 @@ __global__ void __launch_bounds__(kWarps * 32, OCC) decode_tc_kernel(const TcPar
             s_red[(1 * 8 + lane) * 4 + warp] = y;
         }
     }
-    __syncthreads();
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();  // also publishes the TMEM allocation
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tbase = *sm.tmem_slot;
+    // lanes of warp quarter (warp % 4); warps 4..7 use the upper half of the columns
+    const uint32_t tmem_w = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * kSteps * 4 * NT);
     // S_h: |score_int| <= (2^b - 1) * sum|Q_c| <= 2^30 (exact int32 accumulation).
     auto scale_of = [&](int h) {
         const float sum_abs = (s_red[h * 4 + 0] + s_red[h * 4 + 1]) + (s_red[h * 4 + 2] + s_red[h * 4 + 3]);
@@ -518,6 +521,7 @@ __global__ void __launch_bounds__(kWarps * 32, OCC) decode_tc_kernel(const TcPar
         lo[hg] = INFINITY, hi[hg] = -INFINITY;
     }
 
+    if (threadIdx.x == 0) TTRACE(2);  // prologue done (q planes in registers)
     // ---------------- phase A: scores of this warp's tokens ----------------
     // D[16 tokens x 8 (head, plane)] += K[16 tokens x 32 ch] * Q[32 ch x 8]: A = raw code
     // bytes (one LOP3 selects 4 codes x 2^sh), B = the q digit planes (registers). Lane
@@ -584,12 +588,19 @@ __global__ void __launch_bounds__(kWarps * 32, OCC) decode_tc_kernel(const TcPar
                         // digit planes 0..3 of head t, token g (+8): wrapping int32 sum, exact total
                         const int total = ac[hg][u2][0][2 * hf] + ac[hg][u2][0][2 * hf + 1] * 256 +
                                           ac[hg][u2][1][2 * hf] * 65536 + ac[hg][u2][1][2 * hf + 1] * (1 << 24);
-                        const int tok = tbase_tok + 16 * u2 + 8 * hf + g;
-                        const float s = __fmaf_rn((float)total, cA[hg], cB[hg]);
-                        sc[2 * u2 + hf] = s;
+                        sc[2 * u2 + hf] = __fmaf_rn((float)total, cA[hg], cB[hg]);
+                    }
+                }
+                if (tbase_tok + 32 <= nv) {  // full step (warp-uniform): min/max trees, no checks
+                    lo[hg] = fminf(lo[hg], fminf(fminf(sc[0], sc[1]), fminf(sc[2], sc[3])));
+                    hi[hg] = fmaxf(hi[hg], fmaxf(fmaxf(sc[0], sc[1]), fmaxf(sc[2], sc[3])));
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int tok = tbase_tok + 16 * (j >> 1) + 8 * (j & 1) + g;
                         if (tok < nv) {
-                            lo[hg] = fminf(lo[hg], s);
-                            hi[hg] = fmaxf(hi[hg], s);
+                            lo[hg] = fminf(lo[hg], sc[j]);
+                            hi[hg] = fmaxf(hi[hg], sc[j]);
                         }
                     }
                 }
@@ -866,6 +877,8 @@ __global__ void __launch_bounds__(kWarps * 32, OCC) decode_tc_kernel(const TcPar
         unsigned long long ws = 0;
         for (int w2 = 0; w2 < kWarps; ++w2) ws += sm.wsum[w2 * 8 + h];
         const float wv = (float)ws;
+        constexpr float kInvLevelsV = 1.0f / (float)((1u << BITS) - 1u);
+        const float v_step = fmaxf(__fsub_rn(v_b, v_a) * kInvLevelsV, 0.0f);
         float num = __fmaf_rn(v_step, V, v_a * wv), den = wv;
         const float* vt = a.v_tail + (size_t)unit * a.tail_cap * kDim + ch;
         int j = 0;

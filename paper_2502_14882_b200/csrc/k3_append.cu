@@ -13,6 +13,9 @@ __global__ void append_kernel(const float* __restrict__ k_new, const float* __re
                               size_t kv_heads, size_t dim, size_t tail_cap,
                               float* __restrict__ k_tail, float* __restrict__ v_tail,
                               int* __restrict__ tail_len) {
+    // The next decode (launched with programmatic stream serialization) may start its
+    // prologue now; it reads the tail only after griddepcontrol.wait (= this grid done).
+    asm volatile("griddepcontrol.launch_dependents;");
     const size_t b = blockIdx.x;
     const size_t slot = (size_t)tail_len[b];
     const size_t n = kv_heads * dim;
