@@ -135,11 +135,13 @@ def dist_setup(args):
     return world, rank, local
 
 
-def cpu_reference(cfg_name: str, requests: int, steps: int, threads: int):
+def cpu_reference(cfg_name: str, requests: int, steps: int, threads: int, warmup: int = 1, budget_s: float = 0.0):
     """The reference's own HybridKVCache::decode_step (oracle/_ref/libkvq_ref.so, compiled
     unmodified from /root/reference) on a bounded sample of the workload: `requests` of the
-    config's requests, all KV heads, G decode_step calls per request (GQA emulated),
-    outer thread pool over requests, 1 warm-up step. Returns (tokens/s, detail)."""
+    config's requests, all KV heads, G decode_step calls per request (GQA emulated), outer
+    thread pool over requests; `warmup` untimed steps, median of `steps` timed steps (capped
+    so the timed steps take about `budget_s` seconds when budget_s > 0). Returns
+    (tokens/s, detail)."""
     from oracle.oracle import Ref
     batch, H, G, n, bits, tau, _ = CONFIGS[cfg_name]
     requests = min(requests, batch)
@@ -152,26 +154,36 @@ def cpu_reference(cfg_name: str, requests: int, steps: int, threads: int):
     # b >= 2 needs the reference's M = 32 path for correct output at n >= 512
     # (kernels.hpp:220 defect); b = 1 runs as shipped (M = 8).
     word_bits = 8 if bits == 1 else 32
-    secs, _ = Ref().bench_decode(k, v, requests, H, G, n, DIM, bits, word_bits, tau[0], tau[1], q, kn, vn, threads,
-                                 steps + 1)
-    step_s = statistics.median(secs[1:])
+    ref = Ref()
+    if budget_s > 0:  # size the run: one probe step
+        probe, _ = ref.bench_decode(k, v, requests, H, G, n, DIM, bits, word_bits, tau[0], tau[1], q, kn, vn,
+                                    threads, 2)
+        steps = max(3, min(steps, int(budget_s / max(min(probe), 1e-6))))
+    secs, _ = ref.bench_decode(k, v, requests, H, G, n, DIM, bits, word_bits, tau[0], tau[1], q, kn, vn, threads,
+                               steps + warmup)
+    step_s = statistics.median(secs[warmup:])
     return requests / step_s, {
         "sample": f"{requests} of {batch} requests x {H} KV heads x G={G}, n_vis={n}, b={bits}, M={word_bits}; "
-                  f"median of {steps} steps after 1 warm-up; reference HybridKVCache::decode_step + append",
+                  f"median of {steps} steps after {warmup} warm-up; reference HybridKVCache::decode_step + append",
         "step_seconds": step_s,
+        "steps": steps,
     }
 
 
 def run_reference(args, world, rank):
+    """Reference arm: the reference's CPU path on this host's cores (rank 0 only), same
+    config / metric / unit as our arm, `--steps K --warmup W` honoured (K capped so the
+    timed part stays around a minute)."""
     if rank != 0:
         return
     threads = os.cpu_count() or 1
     batch, H, G, n, bits, tau, desc = CONFIGS[args.config]
     t0 = time.time()
-    value, det = cpu_reference(args.config, args.cpu_requests, args.steps_cpu, threads)
+    warm = max(1, args.warmup)
+    value, det = cpu_reference(args.config, args.cpu_requests, args.steps, threads, warmup=warm, budget_s=60.0)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
-        "steps": args.steps_cpu, "warmup": 1, "ms_per_step": det["step_seconds"] * 1e3, "higher_is_better": True,
+        "steps": det["steps"], "warmup": warm, "ms_per_step": det["step_seconds"] * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": f"u{bits}", "data": "synthetic (gaussian)",
         "config": {"workload": desc, "batch": batch, "q_heads": H * G, "kv_heads": H, "n_vis": n, "bits": bits,
                    "tau": list(tau)},
