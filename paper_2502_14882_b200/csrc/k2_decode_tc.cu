@@ -419,11 +419,18 @@ __global__ void __launch_bounds__(kWarps * 32, OCC) decode_tc_kernel(const TcPar
     // Q'_c = round(S_h qs_c / 2^sh_c) in 4 balanced int8 digit planes, S_h bounding the
     // int32 score so IMMA accumulation is exact; computed by every CTA for its own unit
     // while its TMA ring fills (the pw tiles are idle until phase B). Two barriers.
-    float* s_qs = reinterpret_cast<float*>(sm.pw);  // [8][128]
-    float* s_red = s_qs + 8 * kDim;                  // [2][8][4]: per-warp sum|qs|, sum q.alpha
-    uint32_t* s_frag = reinterpret_cast<uint32_t*>(s_red + 64);  // [NT][512]
+    float* s_red = reinterpret_cast<float*>(sm.pw);  // [2][8][4]: per-warp sum|qs|, sum q.alpha
+    uint32_t* s_frag = reinterpret_cast<uint32_t*>(s_red + 64);  // [NT][512] B fragments
     const float levels = (float)((1u << BITS) - 1u);
     const float isd0 = __fdiv_rn(1.0f, sqrtf((float)kDim));
+    // S_h: |score_int| <= (2^b - 1) * sum|Q_c| <= 2^30 (exact int32 accumulation). Any S_h
+    // with that bound is exact; the same value scales Q and the score back (cA).
+    auto scale_of = [&](int h) {
+        const float sum_abs = (s_red[h * 4 + 0] + s_red[h * 4 + 1]) + (s_red[h * 4 + 2] + s_red[h * 4 + 3]);
+        return sum_abs > 0.0f ? 1073741824.0f * __frcp_rn(levels * sum_abs) : 0.0f;
+    };
+    for (int e = threadIdx.x; e < NT * 512; e += kWarps * 32) s_frag[e] = 0u;  // heads >= G stay 0
+    float qsv[8];
     if (threadIdx.x < kDim) {
         const int c = threadIdx.x;
         const float ka = k_a, kbeta = k_b;
@@ -435,9 +442,8 @@ __global__ void __launch_bounds__(kWarps * 32, OCC) decode_tc_kernel(const TcPar
         float ab[8], sa[8];
 #pragma unroll
         for (int h = 0; h < 8; ++h) {
-            const float qs = range > 0.0f ? __fmul_rn(qv[h], stp) : 0.0f;
-            s_qs[h * kDim + c] = qs;
-            ab[h] = fabsf(qs);
+            qsv[h] = range > 0.0f ? __fmul_rn(qv[h], stp) : 0.0f;
+            ab[h] = fabsf(qsv[h]);
             sa[h] = __fmul_rn(qv[h], ka);
         }
 #pragma unroll
@@ -456,45 +462,48 @@ __global__ void __launch_bounds__(kWarps * 32, OCC) decode_tc_kernel(const TcPar
             s_red[(1 * 8 + lane) * 4 + warp] = y;
         }
     }
+    if (threadIdx.x == 0) TTRACE(24);
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();  // also publishes the TMEM allocation
+    if (threadIdx.x == 0) TTRACE(25);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tbase = *sm.tmem_slot;
     // lanes of warp quarter (warp % 4); warps 4..7 use the upper half of the columns
     const uint32_t tmem_w = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * kSteps * 4 * NT);
-    // S_h: |score_int| <= (2^b - 1) * sum|Q_c| <= 2^30 (exact int32 accumulation).
-    auto scale_of = [&](int h) {
-        const float sum_abs = (s_red[h * 4 + 0] + s_red[h * 4 + 1]) + (s_red[h * 4 + 2] + s_red[h * 4 + 3]);
-        return sum_abs > 0.0f ? 1073741824.0f / (levels * sum_abs) : 0.0f;
-    };
-    // B fragments: entry (hg, pp, kb, r, lane) packs bytes j = 0..3 of column n = g
-    // (head 4hg + g/2, digit plane 2pp + g%2) at k = 4t + j (+16 for r = 1).
-    for (int e = threadIdx.x; e < NT * 512; e += kWarps * 32) {
-        const int ln = e & 31, r = (e >> 5) & 1, kb = (e >> 6) & 3, pp = (e >> 8) & 1, hg = e >> 9;
-        const int gg = ln >> 2, tt = ln & 3;
-        const int plane = 2 * pp + (gg & 1);
-        const int h = 4 * hg + (gg >> 1);
-        uint32_t word = 0;
-        if (h < G) {
-            const float S_h = scale_of(h);
+    // B fragments: entry (hg, pp, kb, r, lane(gg, tt)) byte j = digit plane 2pp + gg%2 of
+    // head 4hg + gg/2 at channel k_channel(tt, 2kb + r, j). Thread c scatters its channel's
+    // digits: invert k_channel (ch = (4 (t BITS + u) + j) cpb + cpb - 1 - s, rho = u cpb + s).
+    if (threadIdx.x < kDim) {
+        constexpr int cpb = Gm::kCpb;
+        const int c = threadIdx.x;
+        const int s_slot = cpb - 1 - c % cpb, qidx = c / cpb;
+        const int j = qidx & 3, tb = qidx >> 2;
+        const int tt = tb / BITS, u = tb % BITS;
+        const int rho = u * cpb + s_slot, kb = rho >> 1, r = rho & 1;
+        const int sh = s_slot * BITS;
+        uint8_t* fb = reinterpret_cast<uint8_t*>(s_frag);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                int sh;
-                const int ch = k_channel<BITS>(tt, 2 * kb + r, j, sh);
-                const int Q = __float2int_rn(__fmul_rn(s_qs[h * kDim + ch], S_h) * __int_as_float((127 - sh) << 23));
-                // balanced base-256 digits: Q = d0 + 2^8 d1 + 2^16 d2 + 2^24 d3
-                const int d0 = ((Q + 128) & 255) - 128;
-                const int q1 = (Q - d0) >> 8;
-                const int d1 = ((q1 + 128) & 255) - 128;
-                const int q2 = (q1 - d1) >> 8;
-                const int d2 = ((q2 + 128) & 255) - 128;
-                const int d3 = (q2 - d2) >> 8;
-                const int d = plane == 0 ? d0 : plane == 1 ? d1 : plane == 2 ? d2 : d3;
-                word |= (uint32_t)(d & 255) << (8 * j);
+        for (int h = 0; h < 8; ++h) {
+            if (h >= G) break;
+            const int Q = __float2int_rn(__fmul_rn(qsv[h], scale_of(h)) * __int_as_float((127 - sh) << 23));
+            // balanced base-256 digits: Q = d0 + 2^8 d1 + 2^16 d2 + 2^24 d3
+            const int d0 = ((Q + 128) & 255) - 128;
+            const int q1 = (Q - d0) >> 8;
+            const int d1 = ((q1 + 128) & 255) - 128;
+            const int q2 = (q1 - d1) >> 8;
+            const int d2 = ((q2 + 128) & 255) - 128;
+            const int d3 = (q2 - d2) >> 8;
+            const int dg[4] = {d0, d1, d2, d3};
+            const int hg = h >> 2;
+#pragma unroll
+            for (int plane = 0; plane < 4; ++plane) {
+                const int gg = 2 * (h & 3) + (plane & 1), pp = plane >> 1;
+                const int e = ((((hg * 2 + pp) * 4 + kb) * 2 + r) * 32) + gg * 4 + tt;
+                fb[4 * e + j] = (uint8_t)(dg[plane] & 255);
             }
         }
-        s_frag[e] = word;
     }
+    if (threadIdx.x == 0) TTRACE(26);
     __syncthreads();
     uint32_t bq[NT][2][4][2];  // [head group][digit-plane pair][k-block][reg]
     float cA[NT], cB[NT], lo[NT], hi[NT];

@@ -35,6 +35,8 @@ pa = t[:, 8:16].max(1)
 pb = t[:, 16:24].max(1)
 for name, d in [("start->TMA issued + TMEM alloc", t[:, 6] - t[:, 0]), ("alloc->before griddep", t[:, 7] - t[:, 6]),
                 ("griddep wait", t[:, 3] - t[:, 7]), ("start->griddep released", t[:, 3] - t[:, 0]), ("griddep->prologue done", t[:, 2] - t[:, 3]),
+                ("  q loads+reductions", t[:, 24] - t[:, 3]), ("  sync 1", t[:, 25] - t[:, 24]), ("  frag build", t[:, 26] - t[:, 25]),
+                ("  sync 2 + bq", t[:, 2] - t[:, 26]),
                 ("prologue->phase A done", pa - t[:, 2]), ("start->phase A done (slowest warp)", pa - t[:, 0]), ("phase A warp spread", t[:, 8:16].max(1) - t[:, 8:16].min(1)),
                 ("phaseA done->params", t[:, 1] - pa), ("phase B (params->slowest warp)", pb - t[:, 1]),
                 ("epilogue", t[:, 5] - pb), ("CTA total", t[:, 5] - t[:, 0])]:
