@@ -8,18 +8,20 @@
 //   row     = [g(score_vis) | score_tail],  g affine from (gamma, delta) of the vis part
 //   out_c   = (s_c sum_j p_j code_jc + alpha_c sum_j p_j + sum_t p_t v_tc) / sum p
 //
-// Kernel 1 (prep, one CTA per unit): folds the K scale into the query: Q'_c =
-//   round(S_h qs_c / 2^sh_c) split into 4 balanced int8 digit planes; S_h bounds the
-//   int32 score so IMMA accumulation is exact. Emits the A-fragments of the q.K MMA.
-// Kernel 2 (decode, cluster of S CTAs per unit, each a contiguous token chunk):
-//   one warp/CTA  : cp.async.bulk (TMA) ring of 4 KB stages, K chunk then V chunk
-//   phase A       : IMMA  [16 head-planes x 32 ch] x [32 ch x 8 tokens]; B operand is
-//                   the raw code bytes: one LOP3 extracts 4 codes (x 2^sh) per register
-//   cluster #1    : DSMEM exchange of per-CTA (min, max, tail max) -> gamma, delta, m
-//   phase B       : p = exp(g(s) - m) as a 22-bit integer (three u8 planes) -> IMMA
-//                   [16 head-planes x 32 tok] x [32 tok x 8 ch]; V codes byte-transposed
-//                   with PRMT, slot-selected with LOP3
-//   cluster #2/#3 : DSMEM reduction of partial numerators/denominators -> out
+// One kernel, a cluster of S CTAs per unit (each CTA a contiguous token chunk, 8 warps,
+// each warp a contiguous slice streamed through its own cp.async.bulk ring):
+//   prologue  : fold the K scale into the query: Q'_c = round(S_h qs_c / 2^sh_c) in 4
+//               balanced int8 digit planes (S_h keeps the int32 score exact) -> the B
+//               fragments of the q.K MMA, built in shared memory while the ring fills
+//   phase A   : IMMA [16 tokens x 32 ch] x [32 ch x 8 (head, plane)]; A operand = the raw
+//               code bytes, one LOP3 selects 4 codes (x 2^sh) per register; scores parked
+//               in lane-private tensor-memory columns
+//   cluster #1: DSMEM exchange of per-CTA (min, max, tail max) -> gamma, delta, m
+//   phase B   : p = exp(g(s) - m) as a 22-bit integer (three u8 planes), computed by the
+//               lane that owns the score -> IMMA [16 head-planes x 32 tok] x [32 tok x 8
+//               ch]; V codes pre-arranged as B registers (vx layout), slot-selected by LOP3
+//   epilogue  : exact integer CTA reduction (shared-memory atomics), DSMEM push of partial
+//               numerators / denominators to rank 0 (cluster #2)
 // Packed K/V are never dequantized; the only fp32 math per token is the softmax.
 #include <cooperative_groups.h>
 
@@ -55,9 +57,7 @@ struct Geo {
 
 struct TcParams {
     DecodeArgs a;
-    const uint32_t* frag;  // [units][NT][4 kb][4 reg][32 lanes] A fragments (q planes)
-    const float2* qconst;  // [units][G] (isd / S_h, qdota_h * isd)
-    int S, T;              // cluster size, visual tokens per CTA (multiple of 32)
+    int S, T;  // cluster size, visual tokens per CTA (multiple of 8 warps x 32)
 };
 
 // ---- PTX helpers ---------------------------------------------------------------------
@@ -158,80 +158,6 @@ __device__ __forceinline__ int v_channel(int g, int iota, int& shift) {
     const int q = iota / cpb, s = iota % cpb;
     shift = s * BITS;
     return (2 * BITS * g + q) * cpb + (cpb - 1 - s);
-}
-
-// ---- prep: fold the K scales into the query -------------------------------------------
-template <int BITS>
-__global__ void __launch_bounds__(kDim) prep_kernel(DecodeArgs a, int NT, uint32_t* __restrict__ frag,
-                                                    float2* __restrict__ qconst) {
-    griddep_launch();  // the decode grid may start streaming codes right away
-    __shared__ float s_qs[8][kDim];
-    __shared__ float s_red[2][8][4];
-    __shared__ float s_scale[8];
-    const int unit = blockIdx.x, c = threadIdx.x, G = (int)a.group;
-    const int lane = c & 31, wid = c >> 5;
-    const float levels = (float)((1u << BITS) - 1u);
-    const float isd = __fdiv_rn(1.0f, sqrtf((float)kDim));
-    const float ka = a.k_alpha[unit * kDim + c];
-    const float range = __fsub_rn(a.k_beta[unit * kDim + c], ka);
-    const float step = range > 0.0f ? __fdiv_rn(range, levels) : 0.0f;
-    for (int h = 0; h < 8; ++h) {
-        float qs = 0.f, qa = 0.f;
-        if (h < G) {
-            const float q = a.q[(unit * G + h) * kDim + c];
-            qs = range > 0.0f ? __fmul_rn(q, step) : 0.0f;  // detail::scale_query
-            qa = __fmul_rn(q, ka);
-        }
-        s_qs[h][c] = qs;
-        float ab = fabsf(qs), sa = qa;
-#pragma unroll
-        for (int o = 16; o; o >>= 1) {
-            ab += __shfl_xor_sync(0xffffffffu, ab, o);
-            sa += __shfl_xor_sync(0xffffffffu, sa, o);
-        }
-        if (lane == 0) {
-            s_red[0][h][wid] = ab;
-            s_red[1][h][wid] = sa;
-        }
-    }
-    __syncthreads();
-    if (c < 8) {
-        const int h = c;
-        float sum_abs = (s_red[0][h][0] + s_red[0][h][1]) + (s_red[0][h][2] + s_red[0][h][3]);
-        float qdota = (s_red[1][h][0] + s_red[1][h][1]) + (s_red[1][h][2] + s_red[1][h][3]);
-        // |score_int| <= (2^b - 1) * sum|Q_c| <= 2^30: exact int32 accumulation.
-        float S = sum_abs > 0.0f ? 1073741824.0f / (levels * sum_abs) : 0.0f;
-        s_scale[h] = S;
-        if (h < G) qconst[unit * G + h] = make_float2(S > 0.0f ? isd / S : 0.0f, qdota * isd);
-    }
-    __syncthreads();
-    // B fragments of the q.K MMA: entry (hg, pp, kb, r, lane) packs bytes j = 0..3 of
-    // column n = g (head 4hg + g/2, digit plane 2pp + g%2) at k = 4t + j (+16 for r = 1).
-    const int total = NT * 2 * 4 * 2 * 32;
-    for (int e = c; e < total; e += kDim) {
-        const int ln = e & 31, r = (e >> 5) & 1, kb = (e >> 6) & 3, pp = (e >> 8) & 1, hg = e >> 9;
-        const int g = ln >> 2, t = ln & 3;
-        const int plane = 2 * pp + (g & 1);
-        const int h = 4 * hg + (g >> 1);
-        uint32_t word = 0;
-        if (h < G) {
-            for (int j = 0; j < 4; ++j) {
-                int sh;
-                const int ch = k_channel<BITS>(t, 2 * kb + r, j, sh);
-                const int Q = __float2int_rn(__fmul_rn(s_qs[h][ch], s_scale[h]) * __int_as_float((127 - sh) << 23));
-                // balanced base-256 digits: Q = d0 + 2^8 d1 + 2^16 d2 + 2^24 d3
-                int d0 = ((Q + 128) & 255) - 128;
-                int q1 = (Q - d0) >> 8;
-                int d1 = ((q1 + 128) & 255) - 128;
-                int q2 = (q1 - d1) >> 8;
-                int d2 = ((q2 + 128) & 255) - 128;
-                int d3 = (q2 - d2) >> 8;
-                const int d = plane == 0 ? d0 : plane == 1 ? d1 : plane == 2 ? d2 : d3;
-                word |= (uint32_t)(d & 255) << (8 * j);
-            }
-        }
-        frag[(size_t)unit * total + e] = word;
-    }
 }
 
 // ---- decode ------------------------------------------------------------------------------
@@ -955,7 +881,7 @@ cudaError_t launch_occ(const DecodeArgs& a, cudaStream_t s) {
     int S, T;
     plan(a, S, T);
     cudaError_t e = cudaSuccess;
-    TcParams p{a, a.tc_frag, a.tc_qconst, S, T};
+    TcParams p{a, S, T};
     // TMEM: kTmemCols per CTA; never let more CTAs share an SM than TMEM can serve (a
     // blocked tcgen05.alloc inside a cluster could deadlock against its partners).
     const size_t max_ctas = OCC == 1 ? 1 : (NT == 1 ? 4 : 2);
@@ -1120,7 +1046,6 @@ bool decode_tc_supported(const DecodeArgs& a) {
 }
 
 cudaError_t launch_decode_tc(const DecodeArgs& a, cudaStream_t s) {
-    if (!a.tc_frag || !a.tc_qconst) return cudaErrorInvalidValue;
     const int NT = a.group > 4 ? 2 : 1;
     switch (a.bits * 10 + NT) {
         case 11: return launch_bits<1, 1>(a, s);

@@ -134,7 +134,7 @@ struct kvq_cache {
     DevBuf<float> k_tail, v_tail;  // [units][tail_cap][dim]
     DevBuf<int> tail_len;    // [batch]
     DevBuf<float> d_q, d_out, d_knew, d_vnew, scratch, weights;
-    DevBuf<uint8_t> tc_scratch;  // prep-kernel outputs of the tensor-core decode path
+    DevBuf<uint8_t> tc_scratch;  // prep-kernel outputs of the tcgen05 decode path
     DevBuf<int> viol;
 
     uint8_t* k_codes() const { return codes.p; }
@@ -266,10 +266,6 @@ void run_decode(kvq_cache* c, const float* q, float* out, bool want_weights, boo
         return;
     }
     if ((c->path == KVQ_PATH_AUTO || c->path == KVQ_PATH_TC) && tc_ok) {
-        const size_t need = kvqb::decode_tc_scratch_bytes(c->units);
-        if (c->tc_scratch.n < need) c->tc_scratch.alloc(need);
-        a.tc_frag = reinterpret_cast<uint32_t*>(c->tc_scratch.p);
-        a.tc_qconst = reinterpret_cast<float2*>(c->tc_scratch.p + c->units * 2 * 512 * sizeof(uint32_t));
         traced(c, a, s, [&] { ck(kvqb::launch_decode_tc(a, s), "decode (tc)"); });
         return;
     }

@@ -70,8 +70,7 @@ struct DecodeArgs {
     const uint8_t* v_codes_t;  // umma path: token-packed V codes (vt_layout, k2_decode_umma.cu)
     const uint8_t* v_codes_x;  // tc path: V codes as phase-B MMA operands (vx_layout, k2_decode_tc.cu)
     uint8_t* umma_qb;     // umma path: [units][NT][128][16] s8 q digit planes (prep kernel)
-    uint32_t* tc_frag;    // tc path: [units][2][512] q-plane MMA fragments (prep kernel)
-    float2* tc_qconst;    // tc path: [units][8] per-head score scale / offset
+    float2* tc_qconst;    // umma path: [units][8] per-head score scale / offset (prep kernel)
     unsigned long long* trace;  // nullable: [ctas][64] globaltimer stamps (KVQ_TRACE_FILE)
     size_t units, kv_heads, group, dim, n_vis, tail_cap, weights_stride;
     int bits, word_bits;
