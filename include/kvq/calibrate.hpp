@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <span>
+#include <string>
 #include <vector>
 
 #include "kvq/kernels.hpp"
@@ -63,6 +64,85 @@ inline std::vector<float> calibrated_scores(std::span<const float> q, const Quan
     const float inv_sqrt_d = 1.0f / std::sqrt(static_cast<float>(keys.dim));
     for (float& v : s) v *= inv_sqrt_d;
     return calibrated_softmax_concat(s, {}, p);
+}
+
+// ---- offline tau search (calibrate.hpp:127-234), scored on the GPU ---------------------
+
+struct CalibrationSample {
+    std::vector<float> query;
+    DenseMatrix keys_exact;       // n x d full-precision keys
+    QuantizedSegment keys_quant;  // same tokens, packed
+};
+
+struct GridCell {
+    CalibrationParams params;
+    double mse = 0.0;
+};
+
+inline std::vector<CalibrationParams> make_grid(std::vector<float> values) {
+    if (values.empty()) throw domain_error("make_grid: empty value list");
+    std::sort(values.begin(), values.end());
+    std::vector<CalibrationParams> cells;
+    cells.reserve(values.size() * values.size());
+    for (float t1 : values)
+        for (float t2 : values) cells.push_back({t1, t2});
+    return cells;
+}
+
+inline std::vector<CalibrationParams> default_grid() { return make_grid({0.0f, 1.0f, 2.0f, 3.0f}); }
+
+namespace detail {
+// One C-ABI call: the mean MSE per cell and the argmin (ties: smaller tau1, then tau2).
+inline std::vector<double> grid_call(std::span<const CalibrationSample> set, std::span<const CalibrationParams> cells,
+                                     CalibrationParams* best) {
+    if (set.empty()) throw domain_error("grid_mse_table: empty calibration set");
+    if (cells.empty()) throw domain_error("grid_mse_table: empty grid");
+    const std::size_t n = set[0].keys_exact.rows, d = set[0].keys_exact.cols;
+    const int bits = set[0].keys_quant.bitwidth, wb = set[0].keys_quant.codes.word_bits;
+    std::vector<float> q, ke, alpha, beta;
+    std::vector<std::uint8_t> codes;
+    for (std::size_t i = 0; i < set.size(); ++i) {
+        const CalibrationSample& s = set[i];
+        if (s.query.size() != d || s.keys_exact.rows != n || s.keys_exact.cols != d || s.keys_quant.dim != d ||
+            s.keys_quant.tokens != n || s.keys_quant.bitwidth != bits || s.keys_quant.codes.word_bits != wb)
+            throw domain_error("calibration sample " + std::to_string(i) + " has inconsistent shapes");
+        q.insert(q.end(), s.query.begin(), s.query.end());
+        ke.insert(ke.end(), s.keys_exact.data.begin(), s.keys_exact.data.end());
+        codes.insert(codes.end(), s.keys_quant.codes.bytes.begin(), s.keys_quant.codes.bytes.end());
+        alpha.insert(alpha.end(), s.keys_quant.stats.alpha.begin(), s.keys_quant.stats.alpha.end());
+        beta.insert(beta.end(), s.keys_quant.stats.beta.begin(), s.keys_quant.stats.beta.end());
+    }
+    std::vector<float> t1, t2;
+    for (const auto& c : cells) t1.push_back(c.tau1), t2.push_back(c.tau2);
+    std::vector<double> mse(cells.size());
+    float b[2] = {0.0f, 0.0f};
+    capi::check(kvq_grid_mse_table(q.data(), ke.data(), codes.data(), alpha.data(), beta.data(), set.size(), n, d,
+                                   bits, wb, t1.data(), t2.data(), cells.size(), mse.data(), b));
+    if (best) *best = CalibrationParams{b[0], b[1]};
+    return mse;
+}
+}  // namespace detail
+
+inline std::vector<GridCell> grid_mse_table(std::span<const CalibrationSample> set,
+                                            std::span<const CalibrationParams> cells, const KernelConfig& cfg = {}) {
+    cfg.validate();
+    std::vector<double> mse = detail::grid_call(set, cells, nullptr);
+    std::vector<GridCell> table(cells.size());
+    for (std::size_t c = 0; c < cells.size(); ++c) table[c] = {cells[c], mse[c]};
+    return table;
+}
+
+inline CalibrationParams grid_search(std::span<const CalibrationSample> set, std::span<const CalibrationParams> cells,
+                                     const KernelConfig& cfg = {}) {
+    cfg.validate();
+    CalibrationParams best;
+    detail::grid_call(set, cells, &best);
+    return best;
+}
+
+inline CalibrationParams grid_search(std::span<const CalibrationSample> set, const KernelConfig& cfg = {}) {
+    std::vector<CalibrationParams> cells = default_grid();
+    return grid_search(set, cells, cfg);
 }
 
 }  // namespace kvq

@@ -110,6 +110,17 @@ int kvq_calibrated_softmax_concat(const float* vis, size_t n_vis, const float* t
                                   size_t n_tail, size_t rows, float tau1, float tau2, float* out,
                                   size_t* slope_violations);
 
+/* kvq::grid_mse_table + kvq::grid_search (calibrate.hpp:160-234), offline tau search on
+ * the device: `samples` calibration samples (queries [S][dim], exact keys [S][tokens][dim],
+ * packed keys [S][tokens][row_bytes] with stats alpha/beta [S][dim]) scored against `cells`
+ * candidate (tau1[c], tau2[c]) pairs. mse[c] (nullable) receives the mean softmax MSE per
+ * cell; best_tau (nullable) the argmin, ties to the smaller tau1, then tau2. DOMAIN on an
+ * empty set or grid. */
+int kvq_grid_mse_table(const float* queries, const float* keys_exact, const uint8_t* codes,
+                       const float* alpha, const float* beta, size_t samples, size_t tokens,
+                       size_t dim, int bitwidth, int word_bits, const float* tau1, const float* tau2,
+                       size_t cells, double* mse, float* best_tau);
+
 /* ---- kvcache.hpp: HybridKVCache ---------------------------------------------- */
 /* A device-resident hybrid cache for `batch` independent sequences of `kv_heads` KV
  * heads each; every KV head serves `group` query heads (GQA). batch = 1, group = 1 is

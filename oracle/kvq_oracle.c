@@ -345,6 +345,55 @@ void kvqo_calibrated_softmax_concat(const float* vis, size_t n_vis, const float*
     kvqo_softmax_inplace(out, n_vis + n_tail);
 }
 
+/* Offline tau search (calibrate.hpp:160-234): grid_mse_table / grid_search over `samples`
+ * calibration samples (query [S][d], exact keys [S][n][d], packed keys [S][n][row bytes]
+ * with stats [S][d]); mse[c] = mean over samples of the mean squared difference between
+ * calibrated_softmax_concat(quant / sqrt(d), {}, cell) and softmax(exact / sqrt(d)), in
+ * double (sample_mse, 180-188). best = argmin, ties to the smaller tau1, then tau2. */
+void kvqo_grid_mse_table(const float* queries, const float* keys_exact, const uint8_t* codes,
+                         const float* alpha, const float* beta, size_t samples, size_t n,
+                         size_t d, int bits, int word_bits, const float* tau1, const float* tau2,
+                         size_t cells, double* mse, float* best) {
+    const size_t g = (size_t)(word_bits / bits);
+    const size_t rb = (d + g - 1) / g * g / g * (size_t)(word_bits / 8);
+    const float inv_sqrt_d = 1.0f / sqrtf((float)d);
+    float* quant = (float*)malloc(sizeof(float) * (samples * n + 1));
+    float* exact = (float*)malloc(sizeof(float) * (samples * n + 1));
+    float* prob = (float*)malloc(sizeof(float) * (n + 1));
+    for (size_t s = 0; s < samples; ++s) { /* prepare_samples, 160-178 */
+        kvqo_qk_scores(queries + s * d, codes + s * n * rb, n, d, alpha + s * d, beta + s * d, bits,
+                       word_bits, quant + s * n);
+        for (size_t j = 0; j < n; ++j) quant[s * n + j] *= inv_sqrt_d;
+        kvqo_naive_qk(queries + s * d, keys_exact + s * n * d, n, d, exact + s * n);
+        for (size_t j = 0; j < n; ++j) exact[s * n + j] *= inv_sqrt_d;
+        kvqo_softmax_inplace(exact + s * n, n);
+    }
+    size_t bi = 0;
+    for (size_t c = 0; c < cells; ++c) {
+        double acc = 0.0;
+        for (size_t s = 0; s < samples; ++s) {
+            kvqo_calibrated_softmax_concat(quant + s * n, n, NULL, 0, tau1[c], tau2[c], prob, NULL);
+            double a2 = 0.0;
+            for (size_t j = 0; j < n; ++j) {
+                double diff = (double)prob[j] - (double)exact[s * n + j];
+                a2 += diff * diff;
+            }
+            acc += a2 / (double)n;
+        }
+        mse[c] = acc / (double)samples;
+        if (c > 0 && (mse[c] < mse[bi] ||
+                      (mse[c] == mse[bi] && (tau1[c] < tau1[bi] || (tau1[c] == tau1[bi] && tau2[c] < tau2[bi])))))
+            bi = c;
+    }
+    if (best && cells) {
+        best[0] = tau1[bi];
+        best[1] = tau2[bi];
+    }
+    free(quant);
+    free(exact);
+    free(prob);
+}
+
 /* ---- kvcache.hpp ----------------------------------------------------------- */
 
 void kvqo_decode_head(const float* q, size_t dim, size_t n_vis, int bits, int word_bits,

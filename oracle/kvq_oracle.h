@@ -97,6 +97,12 @@ void kvqo_generate_step_head(uint64_t seed, uint64_t head, uint64_t step, size_t
 void kvqo_oracle_attention(const float* q, const float* k, const float* v, size_t n,
                            size_t dim, float* out);
 
+/* grid_mse_table / grid_search (calibrate.hpp:160-234). */
+void kvqo_grid_mse_table(const float* queries, const float* keys_exact, const uint8_t* codes,
+                         const float* alpha, const float* beta, size_t samples, size_t n,
+                         size_t d, int bits, int word_bits, const float* tau1, const float* tau2,
+                         size_t cells, double* mse, float* best);
+
 #ifdef __cplusplus
 }
 #endif

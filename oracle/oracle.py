@@ -78,6 +78,8 @@ class C_Oracle:
             "kvqo_generate_step_head": (None, [C.c_uint64, C.c_uint64, C.c_uint64, _SZ, C.c_double, C.c_double,
                                                _F, _F, _F]),
             "kvqo_oracle_attention": (None, [_F, _F, _F, _SZ, _SZ, _F]),
+            "kvqo_grid_mse_table": (None, [_F, _F, _U8, _F, _F, _SZ, _SZ, _SZ, C.c_int, C.c_int, _F, _F, _SZ,
+                                           C.POINTER(C.c_double), _F]),
         }
         for n, (r, a) in sigs.items():
             f = getattr(L, n)
@@ -185,6 +187,20 @@ class C_Oracle:
         return out
 
 
+    def grid_mse_table(self, queries, keys_exact, codes, alpha, beta, bits, word_bits, tau1, tau2):
+        """calibrate.hpp:195-234 -> (mse[cells] float64, best (tau1, tau2))."""
+        q, ke = _f32(queries), _f32(keys_exact)
+        S, n, d = ke.shape
+        cb = np.ascontiguousarray(codes, np.uint8)
+        t1, t2 = _f32(tau1), _f32(tau2)
+        mse = np.zeros(t1.size, np.float64)
+        best = np.zeros(2, np.float32)
+        self.L.kvqo_grid_mse_table(_fp(q), _fp(ke), _u8(cb), _fp(_f32(alpha)), _fp(_f32(beta)), S, n, d, bits,
+                                   word_bits, _fp(t1), _fp(t2), t1.size, mse.ctypes.data_as(C.POINTER(C.c_double)),
+                                   _fp(best))
+        return mse, (float(best[0]), float(best[1]))
+
+
 class Ref:
     """The unmodified reference behind oracle/ref_shim.cpp."""
 
@@ -220,6 +236,8 @@ class Ref:
             "kvqr_cache_memory": (C.c_int, [_VP, _SZP]),
             "kvqr_bench_decode": (C.c_int, [_F, _F, _SZ, _SZ, _SZ, _SZ, _SZ, C.c_int, C.c_int, C.c_float, C.c_float,
                                             _F, _F, _F, C.c_int, C.c_int, C.POINTER(C.c_double), _F]),
+            "kvqr_grid_mse_table": (C.c_int, [_F, _F, _U8, _F, _F, _SZ, _SZ, _SZ, C.c_int, C.c_int, _F, _F, _SZ,
+                                              C.POINTER(C.c_double), _F]),
         }
         for n, (r, a) in sigs.items():
             f = getattr(L, n)
@@ -330,6 +348,19 @@ class Ref:
                                           threads, steps, secs, _fp(out)))
         return list(secs), out
 
+
+    def grid_mse_table(self, queries, keys_exact, codes, alpha, beta, bits, word_bits, tau1, tau2):
+        """calibrate.hpp:195-234 -> (mse[cells] float64, best (tau1, tau2))."""
+        q, ke = _f32(queries), _f32(keys_exact)
+        S, n, d = ke.shape
+        cb = np.ascontiguousarray(codes, np.uint8)
+        t1, t2 = _f32(tau1), _f32(tau2)
+        mse = np.zeros(t1.size, np.float64)
+        best = np.zeros(2, np.float32)
+        self._ok(self.L.kvqr_grid_mse_table(_fp(q), _fp(ke), _u8(cb), _fp(_f32(alpha)), _fp(_f32(beta)), S, n, d, bits,
+                                   word_bits, _fp(t1), _fp(t2), t1.size, mse.ctypes.data_as(C.POINTER(C.c_double)),
+                                   _fp(best)))
+        return mse, (float(best[0]), float(best[1]))
 
 class RefCache:
     def __init__(self, ref: Ref, handle, heads, dim):

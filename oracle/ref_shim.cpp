@@ -143,6 +143,32 @@ int kvqr_wv_output(const float* w, const std::uint8_t* bytes, std::size_t tokens
     } catch (const std::exception& e) { return fail(e); }
 }
 
+// grid_mse_table / grid_search (calibrate.hpp:195-234) over `samples` calibration samples:
+// queries [S][d], keys_exact [S][n][d], packed keys [S][n][row_bytes] + alpha/beta [S][d].
+int kvqr_grid_mse_table(const float* queries, const float* keys_exact, const std::uint8_t* codes,
+                        const float* alpha, const float* beta, std::size_t samples, std::size_t n,
+                        std::size_t d, int bits, int word_bits, const float* tau1, const float* tau2,
+                        std::size_t cells, double* mse, float* best) {
+    try {
+        std::vector<kvq::CalibrationSample> set(samples);
+        std::size_t g = static_cast<std::size_t>(word_bits / bits);
+        std::size_t rb = (d + g - 1) / g * g / g * static_cast<std::size_t>(word_bits / 8);
+        for (std::size_t s = 0; s < samples; ++s) {
+            set[s].query.assign(queries + s * d, queries + (s + 1) * d);
+            set[s].keys_exact = mat(keys_exact + s * n * d, n, d);
+            set[s].keys_quant = seg_from(codes + s * n * rb, n, d, alpha + s * d, beta + s * d, bits, word_bits);
+        }
+        std::vector<kvq::CalibrationParams> grid(cells);
+        for (std::size_t c = 0; c < cells; ++c) grid[c] = {tau1[c], tau2[c]};
+        std::vector<kvq::GridCell> table = kvq::grid_mse_table(set, grid);
+        for (std::size_t c = 0; c < cells; ++c) mse[c] = table[c].mse;
+        kvq::CalibrationParams b = kvq::grid_search(set, grid);
+        best[0] = b.tau1;
+        best[1] = b.tau2;
+        return 0;
+    } catch (const std::exception& e) { return fail(e); }
+}
+
 int kvqr_calibrated_softmax_concat(const float* vis, std::size_t n_vis, const float* tail,
                                    std::size_t n_tail, float tau1, float tau2, float* out,
                                    std::size_t* violations) {

@@ -2,6 +2,7 @@
 // reference's error classes, device memory management for the hybrid cache, and
 // dispatch to the K1/K2/K3 kernels. No compute happens on the host: every numeric
 // result comes out of a CUDA kernel, and a missing device is a hard KVQ_ERR_CUDA.
+#include <algorithm>
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
@@ -603,6 +604,54 @@ int kvq_calibrated_softmax_concat(const float* vis, size_t n_vis, const float* t
         sync(0);
         if (slope_violations)
             for (int x : v) *slope_violations += (size_t)x;
+    });
+}
+
+int kvq_grid_mse_table(const float* queries, const float* keys_exact, const uint8_t* codes, const float* alpha,
+                       const float* beta, size_t samples, size_t tokens, size_t dim, int bitwidth, int word_bits,
+                       const float* tau1, const float* tau2, size_t cells, double* mse, float* best_tau) {
+    return guarded([&] {
+        // grid_mse_table (calibrate.hpp:195-200) argument checks, then shapes (165-169)
+        if (samples == 0) raise(KVQ_ERR_DOMAIN, "grid_mse_table: empty calibration set");
+        if (cells == 0) raise(KVQ_ERR_DOMAIN, "grid_mse_table: empty grid");
+        validate_config(bitwidth, word_bits);
+        if (dim == 0 || tokens == 0) raise(KVQ_ERR_DOMAIN, "calibration sample 0 has inconsistent shapes");
+        require_device();
+        const size_t rb = row_bytes(dim, bitwidth, word_bits);
+        DevBuf<float> dq(samples * dim), dk(samples * tokens * dim), da(samples * dim), dbt(samples * dim);
+        DevBuf<uint8_t> dc(samples * tokens * rb);
+        DevBuf<float> t1(cells), t2(cells), quant(samples * tokens), exact(samples * tokens),
+            prob(samples * tokens);
+        DevBuf<double> mse_cs(cells * samples);
+        dq.upload(queries, dq.n);
+        dk.upload(keys_exact, dk.n);
+        dc.upload(codes, dc.n);
+        da.upload(alpha, da.n);
+        dbt.upload(beta, dbt.n);
+        t1.upload(tau1, cells);
+        t2.upload(tau2, cells);
+        ck(kvqb::launch_grid_mse(dq.p, dk.p, dc.p, da.p, dbt.p, samples, tokens, dim, bitwidth, word_bits, t1.p, t2.p,
+                                 cells, quant.p, exact.p, prob.p, mse_cs.p, 0),
+           "grid_mse_table");
+        std::vector<double> h(cells * samples);
+        mse_cs.download(h.data(), h.size());
+        sync(0);
+        // per-cell mean in sample order; argmin with the reference's tie-break (213-228)
+        size_t best = 0;
+        std::vector<double> m(cells);
+        for (size_t c = 0; c < cells; ++c) {
+            double acc = 0.0;
+            for (size_t s = 0; s < samples; ++s) acc += h[c * samples + s];
+            m[c] = acc / (double)samples;
+            if (c > 0 && (m[c] < m[best] || (m[c] == m[best] && (tau1[c] < tau1[best] ||
+                                                                 (tau1[c] == tau1[best] && tau2[c] < tau2[best])))))
+                best = c;
+        }
+        if (mse) std::copy(m.begin(), m.end(), mse);
+        if (best_tau) {
+            best_tau[0] = tau1[best];
+            best_tau[1] = tau2[best];
+        }
     });
 }
 

@@ -104,6 +104,12 @@ cudaError_t launch_calibrated_softmax(const float* vis, size_t n_vis, const floa
                                       size_t n_tail, size_t rows, float tau1, float tau2,
                                       float* out, int* violations, cudaStream_t s);
 
+// Offline tau search (k_grid.cu, calibrate.hpp:160-234): per (cell, sample) softmax MSE.
+cudaError_t launch_grid_mse(const float* queries, const float* keys_exact, const uint8_t* codes, const float* alpha,
+                            const float* beta, size_t samples, size_t n, size_t d, int bits, int word_bits,
+                            const float* tau1, const float* tau2, size_t cells, float* quant, float* exact,
+                            float* exact_prob, double* mse_cs, cudaStream_t s);
+
 // ---- K3: append --------------------------------------------------------------
 cudaError_t launch_append(const float* k_new, const float* v_new, size_t batch, size_t kv_heads,
                           size_t dim, size_t tail_cap, float* k_tail, float* v_tail,

@@ -77,6 +77,8 @@ def lib() -> C.CDLL:
             "kvq_qk_scores": (C.c_int, [_F, _U8, _F, _F, _SZ, _SZ, _SZ, C.c_int, C.c_int, _F]),
             "kvq_wv_output": (C.c_int, [_F, _U8, _F, _F, _SZ, _SZ, _SZ, C.c_int, C.c_int, _F]),
             "kvq_calibrated_softmax_concat": (C.c_int, [_F, _SZ, _F, _SZ, _SZ, C.c_float, C.c_float, _F, _SZP]),
+            "kvq_grid_mse_table": (C.c_int, [_F, _F, _U8, _F, _F, _SZ, _SZ, _SZ, C.c_int, C.c_int, _F, _F, _SZ,
+                                             C.POINTER(C.c_double), _F]),
             "kvq_cache_build": (C.c_int, [_F, _F, _SZ, _SZ, _SZ, _SZ, _SZ, C.c_int, C.c_int, C.c_int,
                                           C.c_float, C.c_float, C.POINTER(_VP)]),
             "kvq_cache_build_device": (C.c_int, [_VP, _VP, _SZ, _SZ, _SZ, _SZ, _SZ, C.c_int, C.c_int, C.c_int,
@@ -398,6 +400,76 @@ def g_apply(x: float, gamma: float, delta: float, p: CalibrationParams) -> float
         return float(f(x - f(p.tau1)))
     t = f(f(x - gamma) / width)
     return float(f(x - f(f(f(p.tau1) * f(f(1) - t)) + f(f(p.tau2) * t))))
+
+
+@dataclass
+class CalibrationSample:
+    """calibrate.hpp:127-131: one query, its exact keys and the same keys quantized."""
+
+    query: np.ndarray              # [d]
+    keys_exact: np.ndarray         # [n][d] fp32
+    keys_quant: QuantizedSegment   # same tokens, packed
+
+
+@dataclass
+class GridCell:
+    """calibrate.hpp:148-151."""
+
+    params: CalibrationParams
+    mse: float = 0.0
+
+
+def make_grid(values) -> list[CalibrationParams]:
+    """calibrate.hpp:133-142: the sorted cartesian square of `values`."""
+    vals = sorted(float(v) for v in values)
+    if not vals:
+        raise DomainError("make_grid: empty value list")
+    return [CalibrationParams(t1, t2) for t1 in vals for t2 in vals]
+
+
+def default_grid() -> list[CalibrationParams]:
+    """calibrate.hpp:144-146: {0, 1, 2, 3}^2."""
+    return make_grid([0.0, 1.0, 2.0, 3.0])
+
+
+def _grid_call(samples: Sequence[CalibrationSample], cells: Sequence[CalibrationParams]):
+    if not samples:
+        raise DomainError("grid_mse_table: empty calibration set")
+    if not cells:
+        raise DomainError("grid_mse_table: empty grid")
+    s0 = samples[0]
+    n, d = s0.keys_exact.shape
+    bits, wb = s0.keys_quant.bitwidth, s0.keys_quant.codes.word_bits
+    for i, s in enumerate(samples):
+        if (np.asarray(s.query).size != d or s.keys_exact.shape != (n, d) or s.keys_quant.dim != d
+                or s.keys_quant.tokens != n or s.keys_quant.bitwidth != bits or s.keys_quant.codes.word_bits != wb):
+            raise DomainError(f"calibration sample {i} has inconsistent shapes")
+    q = np.stack([_f32(s.query) for s in samples])
+    ke = np.stack([_f32(s.keys_exact) for s in samples])
+    codes = np.stack([np.ascontiguousarray(s.keys_quant.codes.bytes, np.uint8) for s in samples])
+    alpha = np.stack([_f32(s.keys_quant.stats.alpha) for s in samples])
+    beta = np.stack([_f32(s.keys_quant.stats.beta) for s in samples])
+    t1 = _f32([c.tau1 for c in cells])
+    t2 = _f32([c.tau2 for c in cells])
+    mse = np.zeros(len(cells), np.float64)
+    best = np.zeros(2, np.float32)
+    _check(lib().kvq_grid_mse_table(_fp(q), _fp(ke), codes.ctypes.data_as(_U8), _fp(alpha), _fp(beta), len(samples),
+                                    n, d, bits, wb, _fp(t1), _fp(t2), len(cells),
+                                    mse.ctypes.data_as(C.POINTER(C.c_double)), _fp(best)))
+    return mse, CalibrationParams(float(best[0]), float(best[1]))
+
+
+def grid_mse_table(samples: Sequence[CalibrationSample], cells: Sequence[CalibrationParams]) -> list[GridCell]:
+    """kvq::grid_mse_table (calibrate.hpp:195-210) on the GPU: mean softmax MSE per cell."""
+    mse, _ = _grid_call(samples, cells)
+    return [GridCell(c, float(m)) for c, m in zip(cells, mse)]
+
+
+def grid_search(samples: Sequence[CalibrationSample], cells: Sequence[CalibrationParams] | None = None
+                ) -> CalibrationParams:
+    """kvq::grid_search (calibrate.hpp:213-234): argmin, ties to the smaller tau1, then tau2."""
+    _, best = _grid_call(samples, default_grid() if cells is None else cells)
+    return best
 
 
 # ---- kvcache.hpp -----------------------------------------------------------------------

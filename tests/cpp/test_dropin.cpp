@@ -178,6 +178,28 @@ int main() {
         }
         CHECK(std::sqrt(err / norm) <= 1e-4);
     }
+    // Offline tau search (test_calibrate.cpp:212-263 analogue): outlier-channel keys at 1 bit
+    // prefer a non-identity calibration; the table's argmin is grid_search's answer.
+    {
+        std::mt19937_64 rng(31);
+        std::vector<CalibrationSample> set;
+        for (int s = 0; s < 2; ++s) {
+            DenseMatrix k = random_matrix(rng, 384, 64, -1, 1);
+            for (std::size_t r = 0; r < k.rows; ++r)
+                for (std::size_t c = 0; c < 3; ++c) k.at(r, c) *= 8.0f;
+            ChannelStats st = compute_stats(k, QuantMode::channel_wise);
+            DenseMatrix qm = random_matrix(rng, 1, 64, -1, 1);
+            set.push_back({qm.data, k, quantize(k, st, 1, 8)});
+        }
+        std::vector<GridCell> table = grid_mse_table(set, default_grid());
+        CHECK(table.size() == 16);
+        CalibrationParams best = grid_search(set);
+        std::size_t arg = 0;
+        for (std::size_t i = 1; i < table.size(); ++i)
+            if (table[i].mse < table[arg].mse) arg = i;
+        CHECK(table[arg].params == best);
+        CHECK_THROWS(grid_search(std::span<const CalibrationSample>{}), domain_error);
+    }
     std::printf(g_fail ? "test_dropin: %d failures\n" : "test_dropin: all passed%.0d\n", g_fail);
     return g_fail ? 1 : 0;
 }

@@ -185,7 +185,40 @@ def decode_cases():
                extra={"seed": np.array(seed), "sha256": np.array(digest)})
 
 
+def grid_cases():
+    """grid_mse_table / grid_search (calibrate.hpp:195-234) from the reference: 2 samples
+    of 384 tokens (the CLI calibrates on <= 512 tokens x 2 samples, kvq_main.cpp:281-287;
+    384 < 512 keeps the reference off its defective b >= 2 byte-LUT qK path)
+    at b = 1, 2, 4 on gaussian keys with outlier channels, the default grid."""
+    R = Ref()
+    rng = np.random.default_rng(2508)
+    t1 = np.repeat(np.arange(4, dtype=np.float32), 4)
+    t2 = np.tile(np.arange(4, dtype=np.float32), 4)
+    out = {"tau1": t1, "tau2": t2}
+    for bits in (1, 2, 4):
+        S, n, d = 2, 384, 128
+        q = rng.normal(size=(S, d)).astype(np.float32)
+        ke = rng.normal(size=(S, n, d)).astype(np.float32)
+        ke[:, :, :4] *= 8.0  # outlier channels
+        codes, al, be = [], [], []
+        for s_ in range(S):
+            a, b = R.compute_stats(ke[s_])
+            codes.append(R.quantize(ke[s_], a, b, bits, 8))
+            al.append(a)
+            be.append(b)
+        mse, best = R.grid_mse_table(q, ke, np.stack(codes), np.stack(al), np.stack(be), bits, 8, t1, t2)
+        out.update({f"b{bits}_q": q, f"b{bits}_keys": ke, f"b{bits}_codes": np.stack(codes),
+                    f"b{bits}_alpha": np.stack(al), f"b{bits}_beta": np.stack(be), f"b{bits}_mse": mse,
+                    f"b{bits}_best": np.array(best, np.float32)})
+    np.savez_compressed(HERE / "grid_search.npz", **out)
+
+
 if __name__ == "__main__":
-    quant_cases()
-    kernel_cases()
-    decode_cases()
+    import sys as _sys
+    if len(_sys.argv) > 1 and _sys.argv[1] == "grid":
+        grid_cases()
+    else:
+        quant_cases()
+        kernel_cases()
+        decode_cases()
+        grid_cases()

@@ -448,3 +448,39 @@ def test_full_size_units_vs_oracle(kvq, oracle, bits, G, n):
         cache.append(kn, vn)
         tk.append(kn)
         tv.append(vn)
+
+
+# ---- offline tau search -------------------------------------------------------
+
+@pytest.mark.parametrize("bits", [1, 2, 4])
+def test_grid_search_matches_reference(kvq, oracle, bits):
+    """Device grid_mse_table / grid_search vs the reference's table (golden) and the C
+    restatement: same argmin (with the tie-break), MSE within float-reordering noise."""
+    z = np.load(GOLD / "grid_search.npz")
+    q, ke = z[f"b{bits}_q"], z[f"b{bits}_keys"]
+    samples = []
+    for s in range(q.shape[0]):
+        seg = kvq.QuantizedSegment(kvq.PackedBuffer(z[f"b{bits}_codes"][s], bits, 8, ke.shape[1] * ke.shape[2]),
+                                   kvq.ChannelStats(z[f"b{bits}_alpha"][s], z[f"b{bits}_beta"][s]),
+                                   ke.shape[1], ke.shape[2], bits)
+        samples.append(kvq.CalibrationSample(q[s], ke[s], seg))
+    cells = [kvq.CalibrationParams(float(a), float(b)) for a, b in zip(z["tau1"], z["tau2"])]
+    table = kvq.grid_mse_table(samples, cells)
+    got = np.array([c.mse for c in table])
+    np.testing.assert_allclose(got, z[f"b{bits}_mse"], rtol=1e-4)
+    best = kvq.grid_search(samples, cells)
+    # Cells with equal tau1 - tau2 shift every score of a row by the same constant
+    # (g = x - tau1 + (tau1 - tau2) t), so their softmaxes are identical and their MSEs
+    # differ only by rounding (~1e-7 relative): among such exact-math ties the reference's
+    # argmin is decided by its libm's last bit. Require the device's pick to be the device
+    # table's argmin (first-minimum tie-break) and to lie in the reference winner's class.
+    arg = int(np.argmin(got))
+    assert (best.tau1, best.tau2) == (table[arg].params.tau1, table[arg].params.tau2)
+    ref_best = z[f"b{bits}_best"].tolist()
+    assert best.tau1 - best.tau2 == ref_best[0] - ref_best[1]
+    assert z[f"b{bits}_mse"][arg] <= z[f"b{bits}_mse"].min() * (1 + 1e-6)
+    assert kvq.grid_search(samples) == best  # default grid = the same {0,1,2,3}^2
+    with pytest.raises(kvq.DomainError):
+        kvq.grid_search([], cells)
+    with pytest.raises(kvq.DomainError):
+        kvq.grid_mse_table(samples, [])

@@ -284,3 +284,14 @@ def test_decode_matches_reference_cache(oracle, ref):
             for hh in range(h):
                 kt[hh].append(kn[hh])
                 vt[hh].append(vn[hh])
+
+
+def test_grid_search_oracle_matches_reference_fixture(oracle):
+    """The C restatement of grid_mse_table / grid_search against the unmodified reference's
+    outputs (tests/golden/grid_search.npz, calibrate.hpp:195-234)."""
+    z = np.load(GOLD / "grid_search.npz")
+    for bits in (1, 2, 4):
+        mse, best = oracle.grid_mse_table(z[f"b{bits}_q"], z[f"b{bits}_keys"], z[f"b{bits}_codes"],
+                                          z[f"b{bits}_alpha"], z[f"b{bits}_beta"], bits, 8, z["tau1"], z["tau2"])
+        np.testing.assert_allclose(mse, z[f"b{bits}_mse"], rtol=1e-6)
+        assert best == tuple(z[f"b{bits}_best"].tolist())
