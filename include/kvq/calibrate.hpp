@@ -4,12 +4,18 @@
 #pragma once
 
 #include <algorithm>
+#include <array>
 #include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <fstream>
 #include <span>
 #include <string>
 #include <vector>
 
 #include "kvq/kernels.hpp"
+#include "kvq/quantize.hpp"
+#include "kvq/workload.hpp"
 
 namespace kvq {
 
@@ -143,6 +149,118 @@ inline CalibrationParams grid_search(std::span<const CalibrationSample> set, std
 inline CalibrationParams grid_search(std::span<const CalibrationSample> set, const KernelConfig& cfg = {}) {
     std::vector<CalibrationParams> cells = default_grid();
     return grid_search(set, cells, cfg);
+}
+
+// ---- diagnostics (calibrate.hpp:236-397): per-head softmax MSE of the quant / quant_c
+// rows against the exact row and shared-edge histograms, computed on the GPU
+// (kvq_mse_report); the CSV writers are host formatting.
+
+enum class ScoreVariant { exact = 0, quant = 1, quant_c = 2 };
+
+inline const char* variant_name(ScoreVariant v) {
+    switch (v) {
+        case ScoreVariant::exact: return "exact";
+        case ScoreVariant::quant: return "quant";
+        default: return "quant_c";
+    }
+}
+
+struct MseRow {
+    std::size_t head = 0;
+    double mse_quant = 0.0;
+    double mse_quant_c = 0.0;
+};
+
+struct HeadHistogram {
+    std::size_t head = 0;
+    std::vector<float> edges;                          // bins + 1, shared by the variants
+    std::array<std::vector<std::uint64_t>, 3> counts;  // indexed by ScoreVariant
+};
+
+struct MseReport {
+    std::vector<MseRow> rows;
+    std::vector<HeadHistogram> histograms;
+    double mean_mse_quant = 0.0;
+    double mean_mse_quant_c = 0.0;
+};
+
+inline MseReport mse_report(std::span<const HeadWorkload> heads, const QuantizationConfig& qcfg,
+                            const CalibrationParams& p, std::size_t bins = 40, const KernelConfig& kcfg = {}) {
+    if (heads.empty()) throw domain_error("mse_report: no heads");
+    if (bins < 1) throw config_error("mse_report: bins must be >= 1");
+    qcfg.validate();
+    kcfg.validate();
+    MseReport report;
+    for (std::size_t i = 0; i < heads.size();) {  // runs of equal-shape heads: one device call
+        const std::size_t n = heads[i].keys.rows, d = heads[i].keys.cols;
+        std::size_t j = i;
+        std::vector<float> q, k;
+        for (; j < heads.size() && heads[j].keys.rows == n && heads[j].keys.cols == d; ++j) {
+            if (heads[j].query.data.size() != d) throw domain_error("naive_qk: query length does not match key cols");
+            q.insert(q.end(), heads[j].query.data.begin(), heads[j].query.data.end());
+            k.insert(k.end(), heads[j].keys.data.begin(), heads[j].keys.data.end());
+        }
+        const std::size_t h = j - i;
+        std::vector<double> mq(h), mc(h);
+        std::vector<float> edges(h * (bins + 1));
+        std::vector<std::uint64_t> counts(h * 3 * bins);
+        capi::check(kvq_mse_report(q.data(), k.data(), h, n, d, qcfg.bitwidth, static_cast<int>(qcfg.mode),
+                                   qcfg.word_bits, p.tau1, p.tau2, bins, mq.data(), mc.data(), edges.data(),
+                                   counts.data()));
+        for (std::size_t x = 0; x < h; ++x) {
+            report.rows.push_back({i + x, mq[x], mc[x]});
+            HeadHistogram hist;
+            hist.head = i + x;
+            hist.edges.assign(edges.begin() + x * (bins + 1), edges.begin() + (x + 1) * (bins + 1));
+            for (int v = 0; v < 3; ++v)
+                hist.counts[v].assign(counts.begin() + (x * 3 + v) * bins, counts.begin() + (x * 3 + v + 1) * bins);
+            report.histograms.push_back(std::move(hist));
+        }
+        i = j;
+    }
+    for (const MseRow& r : report.rows) {
+        report.mean_mse_quant += r.mse_quant;
+        report.mean_mse_quant_c += r.mse_quant_c;
+    }
+    report.mean_mse_quant /= static_cast<double>(heads.size());
+    report.mean_mse_quant_c /= static_cast<double>(heads.size());
+    return report;
+}
+
+namespace detail {
+inline std::string fmt_real(double v) {
+    char buf[48];
+    std::snprintf(buf, sizeof(buf), "%.9g", v);
+    return buf;
+}
+inline std::ofstream open_csv(const std::string& path) {
+    std::ofstream os(path);
+    if (!os) throw format_error("cannot open for writing: " + path, 0);
+    return os;
+}
+}  // namespace detail
+
+// columns: variant,head,mse (exact rows carry 0 by definition)
+inline void write_mse_csv(const std::string& path, const MseReport& report) {
+    std::ofstream os = detail::open_csv(path);
+    os << "variant,head,mse\n";
+    for (const MseRow& r : report.rows) os << "exact," << r.head << ",0\n";
+    for (const MseRow& r : report.rows) os << "quant," << r.head << "," << detail::fmt_real(r.mse_quant) << "\n";
+    for (const MseRow& r : report.rows) os << "quant_c," << r.head << "," << detail::fmt_real(r.mse_quant_c) << "\n";
+    if (!os) throw format_error("write failed: " + path, 0);
+}
+
+// columns: variant,head,bin_left,bin_right,count
+inline void write_histogram_csv(const std::string& path, const MseReport& report) {
+    std::ofstream os = detail::open_csv(path);
+    os << "variant,head,bin_left,bin_right,count\n";
+    for (const HeadHistogram& h : report.histograms)
+        for (int v = 0; v < 3; ++v)
+            for (std::size_t b = 0; b + 1 < h.edges.size(); ++b)
+                os << variant_name(static_cast<ScoreVariant>(v)) << "," << h.head << "," << detail::fmt_real(h.edges[b])
+                   << "," << detail::fmt_real(h.edges[b + 1]) << "," << h.counts[static_cast<std::size_t>(v)][b]
+                   << "\n";
+    if (!os) throw format_error("write failed: " + path, 0);
 }
 
 }  // namespace kvq

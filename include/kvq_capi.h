@@ -121,6 +121,18 @@ int kvq_grid_mse_table(const float* queries, const float* keys_exact, const uint
                        size_t dim, int bitwidth, int word_bits, const float* tau1, const float* tau2,
                        size_t cells, double* mse, float* best_tau);
 
+/* kvq::mse_report (calibrate.hpp:300-351) for `heads` heads of equal shape (queries
+ * [heads][dim], keys [heads][tokens][dim]): each head's keys are quantized with its own
+ * stats (bitwidth, mode, word_bits), and its exact, quantized and calibrated (tau1, tau2)
+ * pre-softmax rows are compared. Per head: mse_quant / mse_quant_c [heads] (softmax MSE vs
+ * the exact row), edges [heads][bins+1] (shared by the three rows), counts
+ * [heads][3][bins] in ScoreVariant order (exact, quant, quant_c). Any output may be NULL.
+ * DOMAIN on no heads or an empty matrix, CONFIG on bins < 1 or a bad configuration. */
+int kvq_mse_report(const float* queries, const float* keys, size_t heads, size_t tokens,
+                   size_t dim, int bitwidth, int mode, int word_bits, float tau1, float tau2,
+                   size_t bins, double* mse_quant, double* mse_quant_c, float* edges,
+                   uint64_t* counts);
+
 /* ---- kvcache.hpp: HybridKVCache ---------------------------------------------- */
 /* A device-resident hybrid cache for `batch` independent sequences of `kv_heads` KV
  * heads each; every KV head serves `group` query heads (GQA). batch = 1, group = 1 is

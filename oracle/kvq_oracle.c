@@ -394,6 +394,86 @@ void kvqo_grid_mse_table(const float* queries, const float* keys_exact, const ui
     free(prob);
 }
 
+/* mse_report (calibrate.hpp:300-351) over `heads` heads of equal shape. Per head: stats +
+ * quantize of the keys (mode, bits, word_bits), exact = naive_qk * inv_sqrt_d, quant =
+ * qk_scores * inv_sqrt_d, qc = g_transform(quant, row_range(quant), tau); edges [bins+1] =
+ * lo + (hi - lo) * i / bins over the union of the three rows (322-331); counts [3][bins]
+ * by bin_row (272-287); mse_q / mse_qc = prob_mse of the softmaxes vs the exact softmax
+ * (289-296). Returns 0, or -1 on an empty matrix (compute_stats). */
+int kvqo_mse_report(const float* queries, const float* keys, size_t heads, size_t n, size_t d, int mode,
+                    int bits, int word_bits, float tau1, float tau2, size_t bins, double* mse_q,
+                    double* mse_qc, float* edges, uint64_t* counts) {
+    if (n == 0 || d == 0) return -1;
+    const size_t rb = kvqo_row_bytes(d, bits, word_bits);
+    const float inv_sqrt_d = 1.0f / sqrtf((float)d);
+    float* alpha = (float*)malloc(sizeof(float) * d);
+    float* beta = (float*)malloc(sizeof(float) * d);
+    uint8_t* codes = (uint8_t*)malloc(n * rb + 1);
+    float* rows[3];
+    float* prob[3];
+    for (int v = 0; v < 3; ++v) {
+        rows[v] = (float*)malloc(sizeof(float) * n);
+        prob[v] = (float*)malloc(sizeof(float) * n);
+    }
+    for (size_t h = 0; h < heads; ++h) {
+        const float* k = keys + h * n * d;
+        const float* q = queries + h * d;
+        kvqo_compute_stats(k, n, d, mode, alpha, beta);
+        kvqo_quantize(k, n, d, alpha, beta, bits, word_bits, codes);
+        kvqo_naive_qk(q, k, n, d, rows[0]);
+        for (size_t j = 0; j < n; ++j) rows[0][j] *= inv_sqrt_d;
+        kvqo_qk_scores(q, codes, n, d, alpha, beta, bits, word_bits, rows[1]);
+        for (size_t j = 0; j < n; ++j) rows[1][j] *= inv_sqrt_d;
+        float gamma = rows[1][0], delta = rows[1][0];
+        for (size_t j = 0; j < n; ++j) {
+            if (rows[1][j] < gamma) gamma = rows[1][j];
+            if (delta < rows[1][j]) delta = rows[1][j];
+        }
+        for (size_t j = 0; j < n; ++j) rows[2][j] = kvqo_g_apply(rows[1][j], gamma, delta, tau1, tau2);
+        float lo = rows[0][0], hi = rows[0][0];
+        for (int v = 0; v < 3; ++v)
+            for (size_t j = 0; j < n; ++j) {
+                if (rows[v][j] < lo) lo = rows[v][j];
+                if (hi < rows[v][j]) hi = rows[v][j];
+            }
+        float* e = edges + h * (bins + 1);
+        for (size_t i = 0; i <= bins; ++i) e[i] = lo + (hi - lo) * (float)i / (float)bins;
+        const float blo = e[0], bw = e[bins] - e[0];
+        for (int v = 0; v < 3; ++v) {
+            uint64_t* c = counts + (h * 3 + (size_t)v) * bins;
+            for (size_t b = 0; b < bins; ++b) c[b] = 0;
+            for (size_t j = 0; j < n; ++j) {
+                size_t idx = 0;
+                if (bw > 0.0f) {
+                    float t = (rows[v][j] - blo) / bw * (float)bins;
+                    size_t i = (size_t)(0.0f < t ? t : 0.0f);
+                    idx = i < bins - 1 ? i : bins - 1;
+                }
+                ++c[idx];
+            }
+            memcpy(prob[v], rows[v], sizeof(float) * n);
+            kvqo_softmax_inplace(prob[v], n);
+        }
+        double aq = 0.0, ac = 0.0;
+        for (size_t j = 0; j < n; ++j) {
+            double dq = (double)prob[1][j] - (double)prob[0][j];
+            double dc = (double)prob[2][j] - (double)prob[0][j];
+            aq += dq * dq;
+            ac += dc * dc;
+        }
+        mse_q[h] = aq / (double)n;
+        mse_qc[h] = ac / (double)n;
+    }
+    for (int v = 0; v < 3; ++v) {
+        free(rows[v]);
+        free(prob[v]);
+    }
+    free(alpha);
+    free(beta);
+    free(codes);
+    return 0;
+}
+
 /* ---- kvcache.hpp ----------------------------------------------------------- */
 
 void kvqo_decode_head(const float* q, size_t dim, size_t n_vis, int bits, int word_bits,

@@ -2,7 +2,7 @@
  * kvq_oracle.h — TEST INFRASTRUCTURE ONLY (the parity checker, never the product).
  *
  * Plain-C restatement of the CalibQuant `kvq` reference hot path
- * (/root/reference/proj/include/kvq/*.hpp). Every function cites the reference
+ * (the reference headers under /root/reference/proj/include/kvq/). Every function cites the reference
  * file:line it follows and keeps the reference's fp32 evaluation order so that,
  * compiled with the reference's own flags (no FMA contraction), it reproduces the
  * reference bit for bit. It is pinned against the reference compiled from its
@@ -102,6 +102,10 @@ void kvqo_grid_mse_table(const float* queries, const float* keys_exact, const ui
                          const float* alpha, const float* beta, size_t samples, size_t n,
                          size_t d, int bits, int word_bits, const float* tau1, const float* tau2,
                          size_t cells, double* mse, float* best);
+/* calibrate.hpp:300-351 */
+int kvqo_mse_report(const float* queries, const float* keys, size_t heads, size_t n, size_t d, int mode,
+                    int bits, int word_bits, float tau1, float tau2, size_t bins, double* mse_q,
+                    double* mse_qc, float* edges, uint64_t* counts);
 
 #ifdef __cplusplus
 }

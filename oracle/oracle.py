@@ -80,6 +80,9 @@ class C_Oracle:
             "kvqo_oracle_attention": (None, [_F, _F, _F, _SZ, _SZ, _F]),
             "kvqo_grid_mse_table": (None, [_F, _F, _U8, _F, _F, _SZ, _SZ, _SZ, C.c_int, C.c_int, _F, _F, _SZ,
                                            C.POINTER(C.c_double), _F]),
+            "kvqo_mse_report": (C.c_int, [_F, _F, _SZ, _SZ, _SZ, C.c_int, C.c_int, C.c_int, C.c_float, C.c_float,
+                                          _SZ, C.POINTER(C.c_double), C.POINTER(C.c_double), _F,
+                                          C.POINTER(C.c_uint64)]),
         }
         for n, (r, a) in sigs.items():
             f = getattr(L, n)
@@ -180,6 +183,18 @@ class C_Oracle:
         self.L.kvqo_generate_step_head(seed, head, step, dim, mean, stddev, _fp(q), _fp(k), _fp(v))
         return q, k, v
 
+    def naive_qk(self, q, k):
+        k = _f32(k)
+        out = np.zeros(k.shape[0], np.float32)
+        self.L.kvqo_naive_qk(_fp(_f32(q)), _fp(k), k.shape[0], k.shape[1], _fp(out))
+        return out
+
+    def naive_wv(self, w, v):
+        v = _f32(v)
+        out = np.zeros(v.shape[1], np.float32)
+        self.L.kvqo_naive_wv(_fp(_f32(w)), _fp(v), v.shape[0], v.shape[1], _fp(out))
+        return out
+
     def oracle_attention(self, q, k, v):
         k, v = _f32(k), _f32(v)
         out = np.zeros(k.shape[1], np.float32)
@@ -199,6 +214,30 @@ class C_Oracle:
                                    word_bits, _fp(t1), _fp(t2), t1.size, mse.ctypes.data_as(C.POINTER(C.c_double)),
                                    _fp(best))
         return mse, (float(best[0]), float(best[1]))
+
+    def mse_report(self, queries, keys, bits, mode=0, word_bits=8, tau=(0.0, 0.0), bins=40):
+        """calibrate.hpp:300-351 -> dict(mse_quant, mse_quant_c [H], edges [H][bins+1],
+        counts [H][3][bins], means (quant, quant_c))."""
+        q, k = _f32(queries), _f32(keys)
+        H, n, d = k.shape
+        out = _report_buffers(H, bins)
+        st = self.L.kvqo_mse_report(_fp(q), _fp(k), H, n, d, mode, bits, word_bits, tau[0], tau[1], bins,
+                                    *_report_ptrs(out))
+        if st != 0:
+            raise ValueError("compute_stats: empty matrix")
+        out["means"] = (float(np.mean(out["mse_quant"])), float(np.mean(out["mse_quant_c"])))
+        return out
+
+
+def _report_buffers(H, bins):
+    return {"mse_quant": np.zeros(H, np.float64), "mse_quant_c": np.zeros(H, np.float64),
+            "edges": np.zeros((H, bins + 1), np.float32), "counts": np.zeros((H, 3, bins), np.uint64)}
+
+
+def _report_ptrs(out):
+    return (out["mse_quant"].ctypes.data_as(C.POINTER(C.c_double)),
+            out["mse_quant_c"].ctypes.data_as(C.POINTER(C.c_double)), _fp(out["edges"]),
+            out["counts"].ctypes.data_as(C.POINTER(C.c_uint64)))
 
 
 class Ref:
@@ -238,6 +277,9 @@ class Ref:
                                             _F, _F, _F, C.c_int, C.c_int, C.POINTER(C.c_double), _F]),
             "kvqr_grid_mse_table": (C.c_int, [_F, _F, _U8, _F, _F, _SZ, _SZ, _SZ, C.c_int, C.c_int, _F, _F, _SZ,
                                               C.POINTER(C.c_double), _F]),
+            "kvqr_mse_report": (C.c_int, [_F, _F, _SZ, _SZ, _SZ, C.c_int, C.c_int, C.c_int, C.c_float, C.c_float,
+                                          _SZ, C.POINTER(C.c_double), C.POINTER(C.c_double), _F,
+                                          C.POINTER(C.c_uint64), C.POINTER(C.c_double)]),
         }
         for n, (r, a) in sigs.items():
             f = getattr(L, n)
@@ -361,6 +403,17 @@ class Ref:
                                    word_bits, _fp(t1), _fp(t2), t1.size, mse.ctypes.data_as(C.POINTER(C.c_double)),
                                    _fp(best)))
         return mse, (float(best[0]), float(best[1]))
+
+    def mse_report(self, queries, keys, bits, mode=0, word_bits=8, tau=(0.0, 0.0), bins=40):
+        q, k = _f32(queries), _f32(keys)
+        H, n, d = k.shape
+        out = _report_buffers(H, bins)
+        means = np.zeros(2, np.float64)
+        self._ok(self.L.kvqr_mse_report(_fp(q), _fp(k), H, n, d, mode, bits, word_bits, tau[0], tau[1], bins,
+                                        *_report_ptrs(out), means.ctypes.data_as(C.POINTER(C.c_double))))
+        out["means"] = (float(means[0]), float(means[1]))
+        return out
+
 
 class RefCache:
     def __init__(self, ref: Ref, handle, heads, dim):

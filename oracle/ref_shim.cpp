@@ -169,6 +169,32 @@ int kvqr_grid_mse_table(const float* queries, const float* keys_exact, const std
     } catch (const std::exception& e) { return fail(e); }
 }
 
+int kvqr_mse_report(const float* queries, const float* keys, std::size_t heads, std::size_t n, std::size_t d,
+                    int mode, int bits, int word_bits, float tau1, float tau2, std::size_t bins, double* mse_q,
+                    double* mse_qc, float* edges, std::uint64_t* counts, double* means) {
+    try {
+        std::vector<kvq::HeadWorkload> hw(heads);
+        for (std::size_t h = 0; h < heads; ++h) {
+            hw[h].keys = mat(keys + h * n * d, n, d);
+            hw[h].values = kvq::DenseMatrix(n, d);
+            hw[h].query = mat(queries + h * d, 1, d);
+        }
+        kvq::QuantizationConfig qcfg{bits, mode ? kvq::QuantMode::global : kvq::QuantMode::channel_wise, word_bits};
+        kvq::MseReport r = kvq::mse_report(hw, qcfg, kvq::CalibrationParams{tau1, tau2}, bins);
+        for (std::size_t h = 0; h < heads; ++h) {
+            mse_q[h] = r.rows[h].mse_quant;
+            mse_qc[h] = r.rows[h].mse_quant_c;
+            const kvq::HeadHistogram& hh = r.histograms[h];
+            std::copy(hh.edges.begin(), hh.edges.end(), edges + h * (bins + 1));
+            for (int v = 0; v < 3; ++v)
+                std::copy(hh.counts[v].begin(), hh.counts[v].end(), counts + (h * 3 + v) * bins);
+        }
+        means[0] = r.mean_mse_quant;
+        means[1] = r.mean_mse_quant_c;
+        return 0;
+    } catch (const std::exception& e) { return fail(e); }
+}
+
 int kvqr_calibrated_softmax_concat(const float* vis, std::size_t n_vis, const float* tail,
                                    std::size_t n_tail, float tau1, float tau2, float* out,
                                    std::size_t* violations) {

@@ -246,7 +246,7 @@ __global__ void naive_qk_kernel(const float* __restrict__ q, const float* __rest
                                 size_t cols, float* __restrict__ out) {
     for (size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x; j < rows; j += (size_t)gridDim.x * blockDim.x) {
         float acc = 0.0f;
-        for (size_t c = 0; c < cols; ++c) acc = __fmaf_rn(q[c], k[j * cols + c], acc);
+        for (size_t c = 0; c < cols; ++c) acc = __fadd_rn(acc, __fmul_rn(q[c], k[j * cols + c]));
         out[j] = acc;
     }
 }
@@ -255,7 +255,7 @@ __global__ void naive_wv_kernel(const float* __restrict__ w, const float* __rest
                                 size_t cols, float* __restrict__ out) {
     for (size_t c = (size_t)blockIdx.x * blockDim.x + threadIdx.x; c < cols; c += (size_t)gridDim.x * blockDim.x) {
         float acc = 0.0f;
-        for (size_t j = 0; j < rows; ++j) acc = __fmaf_rn(w[j], v[j * cols + c], acc);
+        for (size_t j = 0; j < rows; ++j) acc = __fadd_rn(acc, __fmul_rn(w[j], v[j * cols + c]));
         out[c] = acc;
     }
 }

@@ -655,6 +655,37 @@ int kvq_grid_mse_table(const float* queries, const float* keys_exact, const uint
     });
 }
 
+int kvq_mse_report(const float* queries, const float* keys, size_t heads, size_t tokens, size_t dim, int bitwidth,
+                   int mode, int word_bits, float tau1, float tau2, size_t bins, double* mse_quant,
+                   double* mse_quant_c, float* edges, uint64_t* counts) {
+    return guarded([&] {
+        // mse_report argument checks in the reference's order (calibrate.hpp:302-305), then
+        // compute_stats on each head (quantize.hpp:64-68)
+        if (heads == 0) raise(KVQ_ERR_DOMAIN, "mse_report: no heads");
+        if (bins < 1) raise(KVQ_ERR_CONFIG, "mse_report: bins must be >= 1");
+        validate_config(bitwidth, word_bits);
+        if (mode != KVQ_MODE_CHANNEL_WISE && mode != KVQ_MODE_GLOBAL) raise(KVQ_ERR_CONFIG, "unknown quant mode");
+        if (tokens == 0 || dim == 0) raise(KVQ_ERR_DOMAIN, "compute_stats: empty matrix");
+        require_device();
+        const size_t rb = row_bytes(dim, bitwidth, word_bits);
+        DevBuf<float> dq(heads * dim), dk(heads * tokens * dim), da(heads * dim), dbt(heads * dim);
+        DevBuf<uint8_t> dc(heads * tokens * rb);
+        DevBuf<float> quant(heads * tokens), exact(heads * tokens), qc(heads * tokens), de(heads * (bins + 1));
+        DevBuf<unsigned long long> dcnt(heads * 3 * bins);
+        DevBuf<double> mq(heads), mc(heads);
+        dq.upload(queries, dq.n);
+        dk.upload(keys, dk.n);
+        ck(kvqb::launch_mse_report(dq.p, dk.p, heads, tokens, dim, bitwidth, mode, word_bits, tau1, tau2, bins, da.p,
+                                   dbt.p, dc.p, quant.p, exact.p, qc.p, de.p, dcnt.p, mq.p, mc.p, 0),
+           "mse_report");
+        if (mse_quant) mq.download(mse_quant, heads);
+        if (mse_quant_c) mc.download(mse_quant_c, heads);
+        if (edges) de.download(edges, de.n);
+        if (counts) dcnt.download(reinterpret_cast<unsigned long long*>(counts), dcnt.n);
+        sync(0);
+    });
+}
+
 int kvq_cache_build(const float* k_vis, const float* v_vis, size_t batch, size_t kv_heads, size_t group,
                     size_t n_vis, size_t dim, int bitwidth, int mode, int word_bits, float tau1, float tau2,
                     kvq_cache** out) {

@@ -109,6 +109,13 @@ cudaError_t launch_grid_mse(const float* queries, const float* keys_exact, const
                             const float* beta, size_t samples, size_t n, size_t d, int bits, int word_bits,
                             const float* tau1, const float* tau2, size_t cells, float* quant, float* exact,
                             float* exact_prob, double* mse_cs, cudaStream_t s);
+// mse_report (calibrate.hpp:300-351) for `heads` heads of equal shape: K1 stats + codes into
+// alpha/beta [heads][d] and codes, quant / exact / qc rows [heads][n] (scratch), edges
+// [heads][bins+1], counts [heads][3][bins] (exact, quant, quant_c), MSEs [heads].
+cudaError_t launch_mse_report(const float* queries, const float* keys, size_t heads, size_t n, size_t d, int bits,
+                              int mode, int word_bits, float tau1, float tau2, size_t bins, float* alpha, float* beta,
+                              uint8_t* codes, float* quant, float* exact, float* qc, float* edges,
+                              unsigned long long* counts, double* mse_q, double* mse_qc, cudaStream_t s);
 
 // ---- K3: append --------------------------------------------------------------
 cudaError_t launch_append(const float* k_new, const float* v_new, size_t batch, size_t kv_heads,

@@ -75,10 +75,14 @@ def lib() -> C.CDLL:
             "kvq_dequantize": (C.c_int, [_U8, _SZ, _SZ, _F, _F, C.c_int, C.c_int, _F]),
             "kvq_quantize_device": (C.c_int, [_VP, _SZ, _SZ, _SZ, C.c_int, C.c_int, C.c_int, _VP, _VP, _VP, _VP]),
             "kvq_qk_scores": (C.c_int, [_F, _U8, _F, _F, _SZ, _SZ, _SZ, C.c_int, C.c_int, _F]),
+            "kvq_naive_qk": (C.c_int, [_F, _F, _SZ, _SZ, _F]),
+            "kvq_naive_wv": (C.c_int, [_F, _F, _SZ, _SZ, _F]),
             "kvq_wv_output": (C.c_int, [_F, _U8, _F, _F, _SZ, _SZ, _SZ, C.c_int, C.c_int, _F]),
             "kvq_calibrated_softmax_concat": (C.c_int, [_F, _SZ, _F, _SZ, _SZ, C.c_float, C.c_float, _F, _SZP]),
             "kvq_grid_mse_table": (C.c_int, [_F, _F, _U8, _F, _F, _SZ, _SZ, _SZ, C.c_int, C.c_int, _F, _F, _SZ,
                                              C.POINTER(C.c_double), _F]),
+            "kvq_mse_report": (C.c_int, [_F, _F, _SZ, _SZ, _SZ, C.c_int, C.c_int, C.c_int, C.c_float, C.c_float, _SZ,
+                                         C.POINTER(C.c_double), C.POINTER(C.c_double), _F, C.POINTER(C.c_uint64)]),
             "kvq_cache_build": (C.c_int, [_F, _F, _SZ, _SZ, _SZ, _SZ, _SZ, C.c_int, C.c_int, C.c_int,
                                           C.c_float, C.c_float, C.POINTER(_VP)]),
             "kvq_cache_build_device": (C.c_int, [_VP, _VP, _SZ, _SZ, _SZ, _SZ, _SZ, C.c_int, C.c_int, C.c_int,
@@ -283,6 +287,29 @@ class KernelConfig:
             raise ConfigError("kernel blocks and workers must be >= 1")
 
 
+def naive_qk(q, k) -> np.ndarray:
+    """kvq::naive_qk (kernels.hpp:401-413): q K^T over an unquantized matrix, the reference's
+    scalar loop (same order, separately rounded)."""
+    q, k = _f32(q).reshape(-1), _f32(k)
+    if q.size != k.shape[1]:
+        raise DomainError("naive_qk: query length does not match key cols")
+    out = np.zeros(k.shape[0], np.float32)
+    if k.shape[0]:
+        _check(lib().kvq_naive_qk(_fp(q), _fp(k), k.shape[0], k.shape[1], _fp(out)))
+    return out
+
+
+def naive_wv(w, v) -> np.ndarray:
+    """kvq::naive_wv (kernels.hpp:415-426): w V, accumulated over rows in order."""
+    w, v = _f32(w).reshape(-1), _f32(v)
+    if w.size != v.shape[0]:
+        raise DomainError("naive_wv: weight length does not match value rows")
+    out = np.zeros(v.shape[1], np.float32)
+    if v.shape[1]:
+        _check(lib().kvq_naive_wv(_fp(w), _fp(v), v.shape[0], v.shape[1], _fp(out)))
+    return out
+
+
 def _check_uniform(segs: Sequence[QuantizedSegment], who: str) -> None:
     s0 = segs[0]
     for s in segs[1:]:
@@ -470,6 +497,137 @@ def grid_search(samples: Sequence[CalibrationSample], cells: Sequence[Calibratio
     """kvq::grid_search (calibrate.hpp:213-234): argmin, ties to the smaller tau1, then tau2."""
     _, best = _grid_call(samples, default_grid() if cells is None else cells)
     return best
+
+
+# ---- diagnostics: mse_report (calibrate.hpp:236-397) -----------------------------------
+
+class ScoreVariant(IntEnum):
+    """calibrate.hpp:241."""
+
+    exact = 0
+    quant = 1
+    quant_c = 2
+
+
+def variant_name(v: ScoreVariant) -> str:
+    return ("exact", "quant", "quant_c")[int(v)]
+
+
+@dataclass
+class HeadWorkload:
+    """workload.hpp:68-72 (values are carried but unused by mse_report)."""
+
+    keys: np.ndarray    # [tokens][d]
+    values: np.ndarray  # [tokens][d]
+    query: np.ndarray   # [1][d] or [d]
+
+
+@dataclass
+class MseRow:
+    """calibrate.hpp:251-255."""
+
+    head: int = 0
+    mse_quant: float = 0.0
+    mse_quant_c: float = 0.0
+
+
+@dataclass
+class HeadHistogram:
+    """calibrate.hpp:257-261: bins + 1 shared edges, counts per ScoreVariant."""
+
+    head: int = 0
+    edges: np.ndarray = field(default_factory=lambda: np.zeros(0, np.float32))
+    counts: np.ndarray = field(default_factory=lambda: np.zeros((3, 0), np.uint64))
+
+
+@dataclass
+class MseReport:
+    """calibrate.hpp:263-268."""
+
+    rows: list = field(default_factory=list)
+    histograms: list = field(default_factory=list)
+    mean_mse_quant: float = 0.0
+    mean_mse_quant_c: float = 0.0
+
+
+def _report_call(keys: np.ndarray, queries: np.ndarray, cfg: QuantizationConfig, p: CalibrationParams, bins: int):
+    H, n, d = keys.shape
+    mq, mc = np.zeros(H, np.float64), np.zeros(H, np.float64)
+    edges = np.zeros((H, bins + 1), np.float32)
+    counts = np.zeros((H, 3, bins), np.uint64)
+    _check(lib().kvq_mse_report(_fp(queries), _fp(keys), H, n, d, cfg.bitwidth, int(cfg.mode), cfg.word_bits,
+                                p.tau1, p.tau2, bins, mq.ctypes.data_as(C.POINTER(C.c_double)),
+                                mc.ctypes.data_as(C.POINTER(C.c_double)), _fp(edges),
+                                counts.ctypes.data_as(C.POINTER(C.c_uint64))))
+    return mq, mc, edges, counts
+
+
+def mse_report(heads: Sequence[HeadWorkload], qcfg: QuantizationConfig, p: CalibrationParams, bins: int = 40,
+               kcfg: KernelConfig | None = None) -> MseReport:
+    """kvq::mse_report (calibrate.hpp:300-351) on the GPU: per head, quantize the keys with
+    their own stats, then compare the exact, quantized and calibrated pre-softmax rows
+    (softmax MSE vs exact; shared-edge histograms). Heads of equal shape go in one call."""
+    if not heads:
+        raise DomainError("mse_report: no heads")
+    if bins < 1:
+        raise ConfigError("mse_report: bins must be >= 1")
+    if kcfg is not None:
+        kcfg.validate()
+    keys = [_f32(h.keys) for h in heads]
+    queries = [_f32(h.query).reshape(-1) for h in heads]
+    for k, q in zip(keys, queries):
+        if k.ndim != 2 or q.size != k.shape[1]:
+            raise DomainError("naive_qk: query length does not match key cols")
+    report = MseReport()
+    i = 0
+    while i < len(heads):  # runs of equal-shape heads share one device call
+        j = i + 1
+        while j < len(heads) and keys[j].shape == keys[i].shape:
+            j += 1
+        mq, mc, edges, counts = _report_call(np.stack(keys[i:j]), np.stack(queries[i:j]), qcfg, p, bins)
+        for h in range(j - i):
+            report.rows.append(MseRow(i + h, float(mq[h]), float(mc[h])))
+            report.histograms.append(HeadHistogram(i + h, edges[h], counts[h]))
+        i = j
+    for r in report.rows:  # in head order, as the reference accumulates
+        report.mean_mse_quant += r.mse_quant
+        report.mean_mse_quant_c += r.mse_quant_c
+    report.mean_mse_quant /= len(heads)
+    report.mean_mse_quant_c /= len(heads)
+    return report
+
+
+def _fmt_real(v: float) -> str:
+    return "%.9g" % v  # calibrate.hpp:355-359
+
+
+def write_mse_csv(path, report: MseReport) -> None:
+    """calibrate.hpp:369-381; columns variant,head,mse."""
+    try:
+        with open(path, "w") as f:
+            f.write("variant,head,mse\n")
+            for r in report.rows:
+                f.write(f"exact,{r.head},0\n")
+            for r in report.rows:
+                f.write(f"quant,{r.head},{_fmt_real(r.mse_quant)}\n")
+            for r in report.rows:
+                f.write(f"quant_c,{r.head},{_fmt_real(r.mse_quant_c)}\n")
+    except OSError as e:
+        raise FormatError(f"cannot open for writing: {path}") from e
+
+
+def write_histogram_csv(path, report: MseReport) -> None:
+    """calibrate.hpp:383-397; columns variant,head,bin_left,bin_right,count."""
+    try:
+        with open(path, "w") as f:
+            f.write("variant,head,bin_left,bin_right,count\n")
+            for h in report.histograms:
+                for v in range(3):
+                    for b in range(len(h.edges) - 1):
+                        f.write(f"{variant_name(ScoreVariant(v))},{h.head},{_fmt_real(float(h.edges[b]))},"
+                                f"{_fmt_real(float(h.edges[b + 1]))},{int(h.counts[v][b])}\n")
+    except OSError as e:
+        raise FormatError(f"cannot open for writing: {path}") from e
 
 
 # ---- kvcache.hpp -----------------------------------------------------------------------

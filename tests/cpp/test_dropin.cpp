@@ -200,6 +200,32 @@ int main() {
         CHECK(table[arg].params == best);
         CHECK_THROWS(grid_search(std::span<const CalibrationSample>{}), domain_error);
     }
+    // mse_report (test_calibrate.cpp:272-305 analogue): every head and bin covered, ragged heads.
+    {
+        std::mt19937_64 rng(41);
+        std::vector<HeadWorkload> heads;
+        for (std::size_t n : {50, 50, 70}) {
+            HeadWorkload w{random_matrix(rng, n, 8, -1, 1), random_matrix(rng, n, 8, -1, 1), random_matrix(rng, 1, 8, -1, 1)};
+            heads.push_back(std::move(w));
+        }
+        QuantizationConfig qcfg{1, QuantMode::channel_wise, 8};
+        MseReport report = mse_report(heads, qcfg, CalibrationParams{1.0f, 0.0f}, 12);
+        CHECK(report.rows.size() == 3 && report.histograms.size() == 3);
+        double mq = 0.0;
+        for (std::size_t h = 0; h < 3; ++h) {
+            CHECK(report.rows[h].head == h && report.rows[h].mse_quant >= 0.0);
+            mq += report.rows[h].mse_quant;
+            CHECK(report.histograms[h].edges.size() == 13);
+            for (const auto& counts : report.histograms[h].counts) {
+                std::uint64_t total = 0;
+                for (std::uint64_t c : counts) total += c;
+                CHECK(total == heads[h].keys.rows);
+            }
+        }
+        CHECK(std::abs(report.mean_mse_quant - mq / 3.0) <= 1e-12);
+        CHECK_THROWS(mse_report(std::span<const HeadWorkload>{}, qcfg, CalibrationParams{}), domain_error);
+        CHECK_THROWS(mse_report(heads, qcfg, CalibrationParams{}, 0), config_error);
+    }
     std::printf(g_fail ? "test_dropin: %d failures\n" : "test_dropin: all passed%.0d\n", g_fail);
     return g_fail ? 1 : 0;
 }

@@ -213,12 +213,50 @@ def grid_cases():
     np.savez_compressed(HERE / "grid_search.npz", **out)
 
 
+# (name, heads, tokens, dim, bits, mode, tau, bins, source): the reference's three mse_report
+# tests (test_calibrate.cpp:272-352, generate() workloads, seeds 41/43/47), then head-dim-128
+# cases with outlier channels: global stats, a single bin, few bins, and more bins than the
+# device keeps in shared memory. n < 512 (or b = 1) keeps the reference off its defective
+# byte-LUT qK path.
+REPORT_CASES = [
+    ("t41", 3, 50, 8, 1, 0, (1.0, 0.0), 12, 41),
+    ("t43", 2, 64, 16, 8, 0, (0.0, 0.0), 40, 43),
+    ("t47", 2, 20, 4, 2, 0, (0.0, 0.0), 40, 47),
+    ("g2", 4, 384, 128, 2, 1, (2.0, 1.0), 40, None),
+    ("b1", 2, 600, 128, 1, 0, (3.0, 0.0), 7, None),
+    ("one", 2, 300, 64, 4, 0, (1.0, 2.0), 1, None),
+    ("wide", 1, 1024, 64, 1, 0, (1.0, 0.0), 5000, None),
+]
+
+
+def report_cases():
+    """mse_report (calibrate.hpp:300-351) from the unmodified reference."""
+    R = Ref()
+    rng = np.random.default_rng(2510)
+    out = {}
+    for name, H, n, d, bits, mode, tau, bins, seed in REPORT_CASES:
+        if seed is not None:
+            k, _, q = R.generate(seed, H, n, d)
+        else:
+            k = rng.normal(size=(H, n, d)).astype(np.float32)
+            k[:, :, :3] *= 6.0
+            q = rng.normal(size=(H, d)).astype(np.float32)
+        r = R.mse_report(q, k, bits, mode, 8, tau, bins)
+        out.update({f"{name}_q": q, f"{name}_keys": k, f"{name}_mse_quant": r["mse_quant"],
+                    f"{name}_mse_quant_c": r["mse_quant_c"], f"{name}_edges": r["edges"],
+                    f"{name}_counts": r["counts"], f"{name}_means": np.array(r["means"])})
+    np.savez_compressed(HERE / "mse_report.npz", **out)
+
+
 if __name__ == "__main__":
     import sys as _sys
     if len(_sys.argv) > 1 and _sys.argv[1] == "grid":
         grid_cases()
+    elif len(_sys.argv) > 1 and _sys.argv[1] == "report":
+        report_cases()
     else:
         quant_cases()
         kernel_cases()
         decode_cases()
         grid_cases()
+        report_cases()

@@ -484,3 +484,74 @@ def test_grid_search_matches_reference(kvq, oracle, bits):
         kvq.grid_search([], cells)
     with pytest.raises(kvq.DomainError):
         kvq.grid_mse_table(samples, [])
+
+
+# ---- mse_report diagnostics ----------------------------------------------
+
+REPORT = [("t41", 1, 0, (1.0, 0.0), 12), ("t43", 8, 0, (0.0, 0.0), 40), ("t47", 2, 0, (0.0, 0.0), 40),
+          ("g2", 2, 1, (2.0, 1.0), 40), ("b1", 1, 0, (3.0, 0.0), 7), ("one", 4, 0, (1.0, 2.0), 1),
+          ("wide", 1, 0, (1.0, 0.0), 5000)]
+
+
+@pytest.mark.parametrize("name,bits,mode,tau,bins", REPORT)
+def test_mse_report_matches_reference(kvq, name, bits, mode, tau, bins):
+    """Device mse_report vs the reference's (tests/golden/mse_report.npz). The exact rows are
+    bit-exact (sequential separately rounded naive_qk); the quantized rows differ from the
+    reference's by summation order (~1e-7 relative), which moves the shared edges by that
+    much and can flip a value lying on a bin boundary: edges within 2e-6 of the largest edge
+    magnitude (a few ulps of the row range), each
+    histogram total exact, per-bin counts within 2 + n/200 in L1, MSEs within 1e-4 relative."""
+    z = np.load(GOLD / "mse_report.npz")
+    q, k = z[f"{name}_q"], z[f"{name}_keys"]
+    H, n, d = k.shape
+    heads = [kvq.HeadWorkload(k[h], np.zeros_like(k[h]), q[h][None]) for h in range(H)]
+    cfg = kvq.QuantizationConfig(bits, kvq.QuantMode(mode), 8)
+    rep = kvq.mse_report(heads, cfg, kvq.CalibrationParams(*tau), bins)
+    assert [r.head for r in rep.rows] == list(range(H)) and len(rep.histograms) == H
+    np.testing.assert_allclose([r.mse_quant for r in rep.rows], z[f"{name}_mse_quant"], rtol=1e-4)
+    np.testing.assert_allclose([r.mse_quant_c for r in rep.rows], z[f"{name}_mse_quant_c"], rtol=1e-4)
+    np.testing.assert_allclose([rep.mean_mse_quant, rep.mean_mse_quant_c], z[f"{name}_means"], rtol=1e-4)
+    for h, hist in enumerate(rep.histograms):
+        assert hist.edges.shape == (bins + 1,) and np.all(np.diff(hist.edges) >= 0)
+        want = z[f"{name}_edges"][h]
+        np.testing.assert_allclose(hist.edges, want, rtol=0, atol=2e-6 * np.abs(want).max())
+        for v in range(3):
+            got, want = hist.counts[v].astype(np.int64), z[f"{name}_counts"][h, v].astype(np.int64)
+            assert got.sum() == n
+            assert np.abs(got - want).sum() <= 2 + n // 200, (h, v, np.nonzero(got - want))
+
+
+def test_mse_report_errors_and_ragged_heads(kvq, oracle):
+    """Argument errors in the reference's order (calibrate.hpp:302-305) and heads of unequal
+    shapes (one device call per run of equal shapes), checked against the C restatement."""
+    rng = np.random.default_rng(5)
+    cfg = kvq.QuantizationConfig(2, kvq.QuantMode.channel_wise, 8)
+    with pytest.raises(kvq.DomainError):
+        kvq.mse_report([], cfg, kvq.CalibrationParams())
+    ks = [rng.normal(size=(n, 32)).astype(np.float32) for n in (40, 40, 72, 40)]
+    qs = [rng.normal(size=(1, 32)).astype(np.float32) for _ in ks]
+    heads = [kvq.HeadWorkload(k, k, q) for k, q in zip(ks, qs)]
+    with pytest.raises(kvq.ConfigError):
+        kvq.mse_report(heads, cfg, kvq.CalibrationParams(), 0)
+    with pytest.raises(kvq.ConfigError):
+        kvq.mse_report(heads, kvq.QuantizationConfig(3, kvq.QuantMode.channel_wise, 8), kvq.CalibrationParams())
+    rep = kvq.mse_report(heads, cfg, kvq.CalibrationParams(1.0, 0.0), 9)
+    for h, (k, q) in enumerate(zip(ks, qs)):
+        want = oracle.mse_report(q, k[None], 2, 0, 8, (1.0, 0.0), 9)
+        assert rep.rows[h].head == h
+        np.testing.assert_allclose(rep.rows[h].mse_quant, want["mse_quant"][0], rtol=1e-4)
+        np.testing.assert_allclose(rep.rows[h].mse_quant_c, want["mse_quant_c"][0], rtol=1e-4)
+        np.testing.assert_allclose(rep.histograms[h].edges, want["edges"][0], rtol=0,
+                                   atol=2e-6 * np.abs(want["edges"][0]).max())
+    assert rep.mean_mse_quant == pytest.approx(np.mean([r.mse_quant for r in rep.rows]), rel=1e-12)
+
+
+def test_naive_products_bit_exact(kvq, oracle):
+    """naive_qk / naive_wv (kernels.hpp:401-426): the reference's scalar loops, separately
+    rounded in the same order -> bit-identical to the C restatement."""
+    rng = np.random.default_rng(9)
+    k = rng.normal(size=(333, 96)).astype(np.float32)
+    q = rng.normal(size=96).astype(np.float32)
+    w = rng.random(333).astype(np.float32)
+    assert np.array_equal(kvq.naive_qk(q, k), oracle.naive_qk(q, k))
+    assert np.array_equal(kvq.naive_wv(w, k), oracle.naive_wv(w, k))

@@ -295,3 +295,44 @@ def test_grid_search_oracle_matches_reference_fixture(oracle):
                                           z[f"b{bits}_alpha"], z[f"b{bits}_beta"], bits, 8, z["tau1"], z["tau2"])
         np.testing.assert_allclose(mse, z[f"b{bits}_mse"], rtol=1e-6)
         assert best == tuple(z[f"b{bits}_best"].tolist())
+
+
+REPORT_CASES = [("t41", 1, 0, (1.0, 0.0), 12), ("t43", 8, 0, (0.0, 0.0), 40), ("t47", 2, 0, (0.0, 0.0), 40),
+                ("g2", 2, 1, (2.0, 1.0), 40), ("b1", 1, 0, (3.0, 0.0), 7), ("one", 4, 0, (1.0, 2.0), 1),
+                ("wide", 1, 0, (1.0, 0.0), 5000)]
+
+
+@pytest.mark.parametrize("name,bits,mode,tau,bins", REPORT_CASES)
+def test_mse_report_oracle_matches_reference_fixture(oracle, name, bits, mode, tau, bins):
+    """The C restatement of mse_report (calibrate.hpp:300-351) against the unmodified
+    reference (tests/golden/mse_report.npz): edges and histograms bit-identical, MSEs equal."""
+    z = np.load(GOLD / "mse_report.npz")
+    r = oracle.mse_report(z[f"{name}_q"], z[f"{name}_keys"], bits, mode, 8, tau, bins)
+    assert np.array_equal(r["edges"], z[f"{name}_edges"])
+    assert np.array_equal(r["counts"], z[f"{name}_counts"])
+    np.testing.assert_allclose(r["mse_quant"], z[f"{name}_mse_quant"], rtol=1e-12)
+    np.testing.assert_allclose(r["mse_quant_c"], z[f"{name}_mse_quant_c"], rtol=1e-12)
+    # the reference's own invariants (test_calibrate.cpp:272-305)
+    assert np.all(z[f"{name}_counts"].sum(axis=2) == z[f"{name}_keys"].shape[1])
+    np.testing.assert_allclose(z[f"{name}_means"], [z[f"{name}_mse_quant"].mean(), z[f"{name}_mse_quant_c"].mean()],
+                               rtol=1e-12)
+
+
+def test_report_csv_writers(tmp_path):
+    """write_mse_csv / write_histogram_csv (calibrate.hpp:369-397): host formatting of a
+    report, the line layout of the reference's tests (test_calibrate.cpp:307-352)."""
+    from paper_2502_14882_b200 import kvq
+    rep = kvq.MseReport(rows=[kvq.MseRow(0, 0.125, 1e-7), kvq.MseRow(1, 2.0 / 3.0, 0.0)],
+                        histograms=[kvq.HeadHistogram(h, np.array([-1.0, 0.5, 2.0], np.float32),
+                                                      np.array([[1, 2], [3, 0], [0, 3]], np.uint64)) for h in (0, 1)])
+    kvq.write_mse_csv(tmp_path / "mse.csv", rep)
+    lines = (tmp_path / "mse.csv").read_text().splitlines()
+    assert lines == ["variant,head,mse", "exact,0,0", "exact,1,0", "quant,0,0.125", "quant,1,0.666666667",
+                     "quant_c,0,1e-07", "quant_c,1,0"]
+    kvq.write_histogram_csv(tmp_path / "hist.csv", rep)
+    lines = (tmp_path / "hist.csv").read_text().splitlines()
+    assert len(lines) == 1 + 2 * 3 * 2
+    assert lines[0] == "variant,head,bin_left,bin_right,count"
+    assert lines[1:4] == ["exact,0,-1,0.5,1", "exact,0,0.5,2,2", "quant,0,-1,0.5,3"]
+    with pytest.raises(kvq.FormatError):
+        kvq.write_mse_csv(tmp_path / "missing" / "x.csv", rep)
