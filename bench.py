@@ -135,7 +135,8 @@ def dist_setup(args):
     return world, rank, local
 
 
-def cpu_reference(cfg_name: str, requests: int, steps: int, threads: int, warmup: int = 1, budget_s: float = 0.0):
+def cpu_reference(cfg_name: str, requests: int, steps: int, threads: int, warmup: int = 1, budget_s: float = 0.0,
+                  tail: int = 0):
     """The reference's own HybridKVCache::decode_step (oracle/_ref/libkvq_ref.so, compiled
     unmodified from /root/reference) on a bounded sample of the workload: `requests` of the
     config's requests, all KV heads, G decode_step calls per request (GQA emulated), outer
@@ -157,13 +158,14 @@ def cpu_reference(cfg_name: str, requests: int, steps: int, threads: int, warmup
     ref = Ref()
     if budget_s > 0:  # size the run: one probe step
         probe, _ = ref.bench_decode(k, v, requests, H, G, n, DIM, bits, word_bits, tau[0], tau[1], q, kn, vn,
-                                    threads, 2)
+                                    threads, 2, tail)
         steps = max(3, min(steps, int(budget_s / max(min(probe), 1e-6))))
     secs, _ = ref.bench_decode(k, v, requests, H, G, n, DIM, bits, word_bits, tau[0], tau[1], q, kn, vn, threads,
-                               steps + warmup)
+                               steps + warmup, tail)
     step_s = statistics.median(secs[warmup:])
     return requests / step_s, {
-        "sample": f"{requests} of {batch} requests x {H} KV heads x G={G}, n_vis={n}, b={bits}, M={word_bits}; "
+        "sample": f"{requests} of {batch} requests x {H} KV heads x G={G}, n_vis={n}, b={bits}, M={word_bits}, "
+                  f"fp32 tail {tail}+; "
                   f"median of {steps} steps after {warmup} warm-up; reference HybridKVCache::decode_step + append",
         "step_seconds": step_s,
         "steps": steps,
@@ -178,9 +180,12 @@ def run_reference(args, world, rank):
         return
     threads = os.cpu_count() or 1
     batch, H, G, n, bits, tau, desc = CONFIGS[args.config]
+    if args.tail:
+        desc += f", {args.tail} generated tokens in the fp32 tail"
     t0 = time.time()
     warm = max(1, args.warmup)
-    value, det = cpu_reference(args.config, args.cpu_requests, args.steps, threads, warmup=warm, budget_s=60.0)
+    value, det = cpu_reference(args.config, args.cpu_requests, args.steps, threads, warmup=warm, budget_s=60.0,
+                               tail=args.tail)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
         "steps": det["steps"], "warmup": warm, "ms_per_step": det["step_seconds"] * 1e3, "higher_is_better": True,
@@ -202,6 +207,8 @@ def run_ours(args, world, rank, local):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     batch, H, G, n, bits, tau, desc = CONFIGS[args.config]
+    if args.tail:
+        desc += f", {args.tail} generated tokens in the fp32 tail"
     if args.batch:
         batch = args.batch
     units = batch * H
@@ -224,7 +231,7 @@ def run_ours(args, world, rank, local):
         for r in range(R):
             c = kvq.BatchedCache.build_device(k, v, kvq.QuantizationConfig(bits), kvq.CalibrationParams(*tau),
                                               group=G, stream=sptr)
-            c.reserve_tail(tail_cap)
+            c.reserve_tail(tail_cap + args.tail)
             c.set_path(PATHS[args.path])
             caches.append(c)
         del k, v
@@ -237,6 +244,13 @@ def run_ours(args, world, rank, local):
     del kv_chunk
 
     tails = [0] * R
+    # --tail N: every request already generated N tokens (fp32 tail rows) before the timed
+    # steps - the long-generation regime where the dense tail is a second bandwidth term.
+    for r in range(R):
+        for i in range(args.tail):
+            caches[r].append_device(kn[i % 4], vn[i % 4], sptr)
+        tails[r] += args.tail
+    stream.synchronize()
 
     # Eager warm-up (allocates the decode scratch), then one CUDA graph per replica for
     # each half of the step: [prep + K2 decode] and [K3 append]. Graph replays remove the
@@ -296,7 +310,7 @@ def run_ours(args, world, rank, local):
         stop.record(stream)
         stream.synchronize()
     launches = K * (launches_dec + launches_app)
-    assert max(tails) <= tail_cap, "bench tail accounting exceeded the reserved capacity"
+    assert max(tails) <= tail_cap + args.tail, "bench tail accounting exceeded the reserved capacity"
     elapsed_ms = start.elapsed_time(stop)
     dec_ms = [a.elapsed_time(b) for a, b in dec_ev]
     if world > 1:
@@ -315,7 +329,8 @@ def run_ours(args, world, rank, local):
     traffic = None
     if prof.exists():
         try:
-            traffic = json.loads(prof.read_text()).get(args.config, {}).get("dram_bytes_per_launch")
+            key = args.config + (f"+tail{args.tail}" if args.tail else "")
+            traffic = json.loads(prof.read_text()).get(key, {}).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
 
@@ -342,7 +357,8 @@ def run_ours(args, world, rank, local):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            cv, det = cpu_reference(args.config, args.cpu_requests, args.steps_cpu, os.cpu_count() or 1)
+            cv, det = cpu_reference(args.config, args.cpu_requests, args.steps_cpu, os.cpu_count() or 1,
+                                    tail=args.tail)
             cpu = {"value": cv, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": det["sample"]}
         except Exception as e:  # keep the GPU line even if the checker is missing
@@ -358,11 +374,13 @@ def run_ours(args, world, rank, local):
                        "kv_heads": H, "head_dim": DIM, "n_vis": n, "bits": bits, "tau": list(tau),
                        "tail_window": TAIL_WINDOW, "parallelism": f"units sharded x{world} (no collective)",
                        "l2": f"inputs larger than L2: {R} rotating cache replicas x {cache_bytes / 2**20:.1f} MiB",
-                       "step": "K2 decode (all q heads) + K3 append", "decode_path": args.path},
+                       "step": "K2 decode (all q heads) + K3 append", "decode_path": args.path,
+                       "tail_prefill": args.tail},
             "hbm_gbs": bytes_alg / K / (ms_per_step * 1e-3) / 1e9,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                         "kernel": "K2 decode", "alg_bytes_per_launch": bytes_alg / K,
+                         "kernel": "K2 decode" + (" + fp32 tail pass" if args.tail + tail_cap > 64 else ""),
+                         "alg_bytes_per_launch": bytes_alg / K,
                          "launch_us": dec_mean_s * 1e6},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": int(hq.nbytes + hk.nbytes + hv.nbytes),
@@ -382,6 +400,8 @@ def main():
     ap.add_argument("--batch", type=int, default=0, help="override the config's per-GPU batch")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=100)
+    ap.add_argument("--tail", type=int, default=0,
+                    help="generated tokens already in every request's fp32 tail (SURVEY §8 f2 long-tail runs)")
     ap.add_argument("--cpu-requests", type=int, default=16)
     ap.add_argument("--steps-cpu", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")

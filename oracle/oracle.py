@@ -274,7 +274,7 @@ class Ref:
             "kvqr_cache_segment": (C.c_int, [_VP, _SZ, C.c_int, _U8, _F, _F]),
             "kvqr_cache_memory": (C.c_int, [_VP, _SZP]),
             "kvqr_bench_decode": (C.c_int, [_F, _F, _SZ, _SZ, _SZ, _SZ, _SZ, C.c_int, C.c_int, C.c_float, C.c_float,
-                                            _F, _F, _F, C.c_int, C.c_int, C.POINTER(C.c_double), _F]),
+                                            _F, _F, _F, C.c_int, C.c_int, _SZ, C.POINTER(C.c_double), _F]),
             "kvqr_grid_mse_table": (C.c_int, [_F, _F, _U8, _F, _F, _SZ, _SZ, _SZ, C.c_int, C.c_int, _F, _F, _SZ,
                                               C.POINTER(C.c_double), _F]),
             "kvqr_mse_report": (C.c_int, [_F, _F, _SZ, _SZ, _SZ, C.c_int, C.c_int, C.c_int, C.c_float, C.c_float,
@@ -382,12 +382,12 @@ class Ref:
         return RefCache(self, out.value, h, d)
 
     def bench_decode(self, k, v, requests, kv_heads, group, n, dim, bits, word_bits, tau1, tau2, q, k_new, v_new,
-                     threads, steps):
+                     threads, steps, prefill_tail=0):
         secs = (C.c_double * steps)()
         out = np.zeros_like(_f32(q))
         self._ok(self.L.kvqr_bench_decode(_fp(_f32(k)), _fp(_f32(v)), requests, kv_heads, group, n, dim, bits,
                                           word_bits, tau1, tau2, _fp(_f32(q)), _fp(_f32(k_new)), _fp(_f32(v_new)),
-                                          threads, steps, secs, _fp(out)))
+                                          threads, steps, prefill_tail, secs, _fp(out)))
         return list(secs), out
 
 

@@ -342,7 +342,7 @@ int kvqr_bench_decode(const float* k_vis, const float* v_vis, std::size_t reques
                       std::size_t kv_heads, std::size_t group, std::size_t n, std::size_t dim,
                       int bits, int word_bits, float tau1, float tau2, const float* queries,
                       const float* k_new, const float* v_new, int threads, int steps,
-                      double* step_seconds, float* out_last) {
+                      std::size_t prefill_tail, double* step_seconds, float* out_last) {
     try {
         std::vector<kvq::HybridKVCache> caches(requests);
         {
@@ -360,6 +360,10 @@ int kvqr_bench_decode(const float* k_vis, const float* v_vis, std::size_t reques
                         caches[r] = kvq::HybridKVCache::build(
                             ks, vs, kvq::QuantizationConfig{bits, kvq::QuantMode::channel_wise, word_bits},
                             kvq::CalibrationParams{tau1, tau2});
+                        // generated tokens already in the fp32 tail before the timed steps
+                        for (std::size_t t = 0; t < prefill_tail; ++t)
+                            caches[r].append(mat(k_new + r * kv_heads * dim, kv_heads, dim),
+                                             mat(v_new + r * kv_heads * dim, kv_heads, dim));
                     }
                 });
             }

@@ -43,6 +43,7 @@ constexpr int kMaxCluster = 16;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: float -> int rounding trick
 constexpr float kPScale = 4190000.0f;  // p in [0, 1(+eps)] -> integer < 2^22 (22-bit digits)
+constexpr float kLog2PScale = 21.9985188f;  // log2(kPScale): weights are on the kPScale scale
 constexpr int kPRow = 12;              // words per p-plane smem row (stride avoids bank conflicts)
 
 template <int BITS>
@@ -292,7 +293,10 @@ __global__ void __launch_bounds__(kWarps * 32, OCC) decode_tc_kernel(const TcPar
     const int wt = p.T / kWarps;                        // tokens per warp (multiple of 32, <= 512)
     const int tok0 = rank * p.T + warp * wt;              // this warp's first token
     const int nv = max(0, min(wt, n - tok0));
-    const int ntl = rank == 0 ? a.tail_len[unit / a.kv_heads] : 0;  // fp32 tail: rank 0
+    // fp32 tail: rank 0, unless a separate tail pass owns it (a.tail_lse). tail_len is written
+    // by the previous step's append: the pre-dependency read is an L2 prefetch hint only.
+    const bool own_tail = rank == 0 && a.tail_lse == nullptr;
+    const int ntl_hint = own_tail ? __ldcg(a.tail_len + unit / a.kv_heads) : 0;
     const uint8_t* kcodes = a.k_codes + ((size_t)unit * n + tok0) * Gm::kRowBytes;
     const int nb32 = (n + 31) >> 5;  // 32-token blocks of the unit (vx_layout)
     const uint8_t* vcodes = a.v_codes_x + ((size_t)unit * nb32 + (tok0 >> 5)) * (size_t)(32 * Gm::kRowBytes);
@@ -326,7 +330,7 @@ __global__ void __launch_bounds__(kWarps * 32, OCC) decode_tc_kernel(const TcPar
     if (S > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");  // #0
 
     // Warm L2 with the fp32 tail rows (rank 0 reads them after phase A / in the epilogue).
-    for (int l = threadIdx.x; l < 8 * ntl; l += blockDim.x) {
+    for (int l = threadIdx.x; l < 8 * min(ntl_hint, kTailMax); l += blockDim.x) {
         const float* base = (l & 4) ? a.v_tail : a.k_tail;
         const float* ptr = base + ((size_t)unit * a.tail_cap + (l >> 3)) * kDim + 32 * (l & 3);
         asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
@@ -339,6 +343,8 @@ __global__ void __launch_bounds__(kWarps * 32, OCC) decode_tc_kernel(const TcPar
     const float k_b = __ldg(a.k_beta + unit * kDim + (threadIdx.x & (kDim - 1)));
     if (threadIdx.x == 0) TTRACE(7);
     griddep_wait();  // the previous step's append (tail rows, tail_len) and q are visible from here on
+    const int ntl = own_tail ? __ldcg(a.tail_len + unit / a.kv_heads) : 0;
+    if (a.tail_lse) griddep_launch();  // the tail pass may start streaming the fp32 tail
     if (threadIdx.x == 0) TTRACE(3);
 
     // ---- fold the K scales into the query (scale_query, kernels.hpp:183-194) ----
@@ -835,6 +841,7 @@ __global__ void __launch_bounds__(kWarps * 32, OCC) decode_tc_kernel(const TcPar
         }
         if (S == 1) {
             a.out[((size_t)unit * G + h) * kDim + ch] = num / den;
+            if (a.tail_lse && ch == 0) a.tail_lse[(size_t)unit * G + h] = log2f(den) - kLog2PScale - sm.gpar[h * 4 + 2];
         } else {
             st_cluster_f32(recv + rank * (8 * kDim + 8) + idx, 0, num);
             if (ch == 0) st_cluster_f32(recv + rank * (8 * kDim + 8) + 8 * kDim + h, 0, den);
@@ -853,6 +860,8 @@ __global__ void __launch_bounds__(kWarps * 32, OCC) decode_tc_kernel(const TcPar
                     den += recv[r * (8 * kDim + 8) + 8 * kDim + h];
                 }
                 a.out[((size_t)unit * G + (idx / kDim)) * kDim + (idx % kDim)] = num / den;
+                if (a.tail_lse && idx % kDim == 0)
+                    a.tail_lse[(size_t)unit * G + h] = log2f(den) - kLog2PScale - sm.gpar[h * 4 + 2];
             }
         }
     }
@@ -1027,8 +1036,8 @@ bool decode_tc_supported(const DecodeArgs& a) {
     int S, T;
     plan(a, S, T);
     if (S > kMaxCluster) return false;
-    // the fp32 tail lives in rank 0: at most kTailMax rows
-    if (a.tail_cap > (size_t)kTailMax) return false;
+    // the fp32 tail lives in rank 0 (at most kTailMax rows) unless the tail pass owns it
+    if (a.tail_cap > (size_t)kTailMax && a.tail_lse == nullptr) return false;
     (void)T;
     const int NT = a.group > 4 ? 2 : 1;
     size_t smem = 0;

@@ -133,6 +133,7 @@ struct kvq_cache {
     DevBuf<uint8_t> vx;      // V codes pre-arranged as IMMA operands for the default decode
     DevBuf<float> stats;     // [2 (K,V)][2 (alpha,beta)][units][dim]
     DevBuf<float> k_tail, v_tail;  // [units][tail_cap][dim]
+    DevBuf<float> lse;             // [units][group] decode log-sum-exp for the tail pass
     DevBuf<int> tail_len;    // [batch]
     DevBuf<float> d_q, d_out, d_knew, d_vnew, scratch, weights;
     DevBuf<uint8_t> tc_scratch;  // prep-kernel outputs of the tcgen05 decode path
@@ -243,6 +244,12 @@ void run_decode(kvq_cache* c, const float* q, float* out, bool want_weights, boo
     kvqb::DecodeArgs probe = a;
     probe.v_codes_t = reinterpret_cast<const uint8_t*>(1);  // shape check only
     const bool umma_ok = plain && c->dim == 128 && c->word_bits == 8 && kvqb::decode_umma_supported(probe);
+    // Long fp32 tails leave the in-kernel tail of the tensor-core decode for the tail pass
+    // (k2_tail.cu), which streams them at HBM rate and merges by log-sum-exp.
+    if (plain && c->tail_cap > kvqb::kTcTailMax && kvqb::decode_tail_supported(a)) {
+        if (c->lse.n < c->units * c->group) c->lse.alloc(c->units * c->group);
+        a.tail_lse = c->lse.p;
+    }
     bool tc_ok = kvqb::decode_tc_supported(a) && plain;
     // Probability-row / violation export (decode_step_detailed) is a generic-path feature:
     // an explicit tensor-core path selection applies to plain decodes only.
@@ -258,7 +265,8 @@ void run_decode(kvq_cache* c, const float* q, float* out, bool want_weights, boo
     if ((c->path == KVQ_PATH_UMMA || (c->path == KVQ_PATH_AUTO && !tc_ok)) && umma_ok) {
         ensure_vt(c, s);
         a.v_codes_t = c->vt.p;
-    a.v_codes_x = c->vx.p;
+        a.v_codes_x = c->vx.p;
+        a.tail_lse = nullptr;
         const size_t need = kvqb::decode_tc_scratch_bytes(c->units);
         if (c->tc_scratch.n < need) c->tc_scratch.alloc(need);
         a.umma_qb = c->tc_scratch.p;
@@ -268,6 +276,12 @@ void run_decode(kvq_cache* c, const float* q, float* out, bool want_weights, boo
     }
     if ((c->path == KVQ_PATH_AUTO || c->path == KVQ_PATH_TC) && tc_ok) {
         traced(c, a, s, [&] { ck(kvqb::launch_decode_tc(a, s), "decode (tc)"); });
+        if (a.tail_lse) ck(kvqb::launch_decode_tail(a, true, s), "decode (tail)");
+        return;
+    }
+    // A pure fp32 cache (build_full_precision): the tail pass is the whole decode.
+    if (plain && c->n_vis == 0 && c->path != KVQ_PATH_GENERIC && kvqb::decode_tail_supported(a)) {
+        ck(kvqb::launch_decode_tail(a, false, s), "decode (tail)");
         return;
     }
     size_t need = c->units * c->group * (c->n_vis + c->tail_cap);

@@ -72,6 +72,8 @@ struct DecodeArgs {
     uint8_t* umma_qb;     // umma path: [units][NT][128][16] s8 q digit planes (prep kernel)
     float2* tc_qconst;    // umma path: [units][8] per-head score scale / offset (prep kernel)
     unsigned long long* trace;  // nullable: [ctas][64] globaltimer stamps (KVQ_TRACE_FILE)
+    float* tail_lse;      // nullable: the fp32 tail is left to the tail pass (k2_tail.cu); the
+                          // decode writes its base-2 log-sum-exp per (unit, head) here
     size_t units, kv_heads, group, dim, n_vis, tail_cap, weights_stride;
     int bits, word_bits;
     float tau1, tau2;
@@ -80,6 +82,11 @@ cudaError_t launch_decode_generic(const DecodeArgs& a, cudaStream_t s);
 bool decode_tc_supported(const DecodeArgs& a);
 size_t decode_tc_scratch_bytes(size_t units);
 cudaError_t launch_decode_tc(const DecodeArgs& a, cudaStream_t s);
+// fp32 tail pass (k2_tail.cu): attention over the dense tail rows, merged by log-sum-exp
+// with the decode's output when `after_decode` (a.tail_lse set, launched right after it).
+bool decode_tail_supported(const DecodeArgs& a);
+cudaError_t launch_decode_tail(const DecodeArgs& a, bool after_decode, cudaStream_t s);
+constexpr size_t kTcTailMax = 64;  // tail rows the tensor-core decodes keep in-kernel
 size_t vx_bytes(size_t units, size_t n_vis, int bits);
 cudaError_t launch_pack_vx(const uint8_t* rows, size_t units, size_t n_vis, int bits, uint8_t* vx, cudaStream_t s);
 // tcgen05 (UTCIMMA) path, d = 128, M = 8: needs the token-packed V copy.

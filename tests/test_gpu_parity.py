@@ -555,3 +555,75 @@ def test_naive_products_bit_exact(kvq, oracle):
     w = rng.random(333).astype(np.float32)
     assert np.array_equal(kvq.naive_qk(q, k), oracle.naive_qk(q, k))
     assert np.array_equal(kvq.naive_wv(w, k), oracle.naive_wv(w, k))
+
+
+# ---- long fp32 tails: the tail pass ---------------------------------------
+
+@pytest.mark.parametrize("bits,G,n,n_tail", [(1, 4, 4096, 200), (2, 8, 1000, 130), (4, 1, 300, 65),
+                                             (1, 6, 512, 1000), (8, 3, 64, 96)])
+def test_long_tail_pass_vs_oracle(kvq, oracle, bits, G, n, n_tail):
+    """Tails beyond the tensor-core decode's in-kernel capacity (64 rows) go to the tail pass
+    (k2_tail.cu), merged with the quantized part by log-sum-exp: same result as the
+    reference's single softmax over [g(vis) | tail] (C restatement)."""
+    rng = np.random.default_rng(n_tail + 11 * bits + G)
+    B, H, d = 2, 2, 128
+    k = rng.normal(size=(B, H, n, d)).astype(np.float32)
+    v = rng.normal(size=(B, H, n, d)).astype(np.float32)
+    tau = (1.0, 0.0)
+    cache = kvq.BatchedCache.build(k, v, kvq.QuantizationConfig(bits), kvq.CalibrationParams(*tau), group=G)
+    tk, tv = [], []
+    for _ in range(n_tail):
+        kn = rng.normal(size=(B, H, d)).astype(np.float32)
+        vn = rng.normal(size=(B, H, d)).astype(np.float32)
+        cache.append(kn, vn)
+        tk.append(kn)
+        tv.append(vn)
+    q = rng.normal(size=(B, H, G, d)).astype(np.float32)
+    want = _oracle_batched(oracle, k, v, q, bits, tau, np.stack(tk), np.stack(tv))
+    cache.set_path(kvq.PATH_AUTO)
+    out, _, _ = cache.decode(q)
+    assert rel_l2(out, want) <= 5e-4, rel_l2(out, want)
+    again, _, _ = cache.decode(q)
+    assert np.array_equal(out, again), "decode must be run-to-run deterministic"
+    cache.set_path(kvq.PATH_GENERIC)
+    gen, _, _ = cache.decode(q)
+    assert rel_l2(out, gen) <= 5e-4
+
+
+def test_long_tail_decisive_token(kvq):
+    """A decisive generated token deep in a long tail dominates the merged softmax
+    (test_kvcache.cpp:142-159 at tail length 150)."""
+    rng = np.random.default_rng(12)
+    B, H, G, n, d = 1, 2, 4, 256, 128
+    k = rng.uniform(-1, 1, (B, H, n, d)).astype(np.float32)
+    v = rng.uniform(-1, 1, (B, H, n, d)).astype(np.float32)
+    cache = kvq.BatchedCache.build(k, v, kvq.QuantizationConfig(2), kvq.CalibrationParams(), group=G)
+    for t in range(150):
+        kn = rng.uniform(-0.1, 0.1, (B, H, d)).astype(np.float32)
+        vn = rng.uniform(-1, 1, (B, H, d)).astype(np.float32)
+        if t == 97:
+            kn[..., 0] = 30.0
+            vn = np.broadcast_to(np.arange(d, dtype=np.float32) - 3, (B, H, d)).copy()
+        cache.append(kn, vn)
+    q = np.zeros((B, H, G, d), np.float32)
+    q[..., 0] = 30.0
+    out, _, _ = cache.decode(q)
+    assert np.all(np.abs(out - (np.arange(d, dtype=np.float32) - 3)) <= 1e-3)
+
+
+@pytest.mark.parametrize("n_tail", [1, 40, 300])
+def test_full_precision_cache_tail_pass(kvq, oracle, n_tail):
+    """build_full_precision (kvcache.hpp:69-91): no quantized part, the tail pass is the
+    whole decode (plain fp32 attention, kvcache.hpp:286-304)."""
+    rng = np.random.default_rng(n_tail)
+    h, d = 3, 128
+    k = rng.normal(size=(h, n_tail, d)).astype(np.float32)
+    v = rng.normal(size=(h, n_tail, d)).astype(np.float32)
+    cache = kvq.HybridKVCache.build_full_precision(list(k), list(v))
+    q = rng.normal(size=(h, d)).astype(np.float32)
+    out = cache.decode_step(q)
+    for hh in range(h):
+        want, _, _ = oracle.decode_head(q[hh], 0, 8, 8, np.zeros(0, np.uint8), np.zeros(d, np.float32),
+                                        np.zeros(d, np.float32), np.zeros(0, np.uint8), np.zeros(d, np.float32),
+                                        np.zeros(d, np.float32), k[hh], v[hh], 0.0, 0.0)
+        assert rel_l2(out[hh], want) <= 1e-5
