@@ -4,48 +4,56 @@
 //
 // The reference runs ONE softmax over [g(vis) | tail] (calibrate.hpp:100-114). Split in
 // two passes this is exact algebra: with the decode's normalised output o_v and base-2
-// log-sum-exp l_v of its (calibrated) vis weights, and this pass's running max M_t, sum
+// log-sum-exp l_v of its (calibrated) vis weights, and this pass's reference max M_t, sum
 // D_t = sum_j 2^(t_j - M_t) and numerator N_t = sum_j 2^(t_j - M_t) v_j (t_j = score_j log2 e):
 //   out = (o_v 2^(l_v - X) + N_t 2^(M_t - X)) / (2^(l_v - X) + D_t 2^(M_t - X)),
 //   X = max(l_v, M_t + log2 D_t).
 // Without a quantized prefill (build_full_precision) l_v = -inf and this pass is the whole
 // decode.
 //
-// Layout and work split. A unit's tail is [tail_cap][128] fp32 for K and for V (rows
-// appended by K3). The rows of a unit are split over a cluster of S CTAs (S sized so the
-// grid covers the SMs); inside a CTA warp w takes rows w, w + 8, ...; lane l owns channels
-// 4l..4l+3 of every row (one coalesced 512-byte row read per warp and tensor). A warp keeps
-// its own online softmax (running max, sum, 4 numerators per head and lane); warps merge in
-// shared memory, ranks through DSMEM into rank 0, which alone waits for the decode grid
-// (programmatic dependent launch: everything before the merge overlaps the decode's tail
+// Data movement. A unit's tail is [tail_cap][128] fp32 for K and for V (rows appended by
+// K3). The unit's rows are split over a cluster of S CTAs; a CTA's rows are cut in 4-row
+// stages (2 KB of K + 2 KB of V, contiguous) dealt round-robin to its 8 warps, and every
+// warp streams its stages through its own ring of cp.async.bulk copies (kStages deep,
+// mbarrier completion) - the loads never wait on the math, so HBM sees a steady stream.
+//
+// Math per stage, per warp (lane l owns channels 4l..4l+3):
+//   scores  4 rows x GP heads partial dots, then ONE butterfly reduce-scatter across the
+//           warp (4 GP values -> one complete score per lane, 16 or 31 shuffles instead of
+//           5 per score); lane L holds (row i, head h) = idx / GP, idx % GP, idx = L >> 1
+//           (GP = 4) or L (GP = 8);
+//   softmax lazy running max per head (warp-uniform): a score is exponentiated against
+//           the current reference m as long as it stays below m + kSlack (so weights stay
+//           <= 2^kSlack); one vote detects the rare stage that raises it and rescales;
+//   values  each lane exponentiates its own score once; the weights are broadcast back
+//           (one shuffle per (row, head)) into 4 FMAs per head and row.
+// Warps merge in shared memory, ranks through DSMEM into rank 0, which alone waits for the
+// decode grid (programmatic dependent launch: the streaming overlaps the decode's tail
 // end) and writes the output. HBM-bound: 1024 algorithmic bytes per tail row and unit.
-#include <cooperative_groups.h>
-
 #include "kvq_internal.cuh"
-
-namespace cg = cooperative_groups;
+#include "kvq_ptx.cuh"
 
 namespace kvqb {
 
 namespace {
 
+using namespace ptx;
+
 constexpr int kDim = 128;
-constexpr int kWarps = 8;
-constexpr int kRows = 4;  // rows in flight per warp (4 K + 4 V float4 loads per lane)
+#ifndef KVQ_TAIL_WARPS  // (tuning builds only: tools/gpu_tail_tune.sh)
+#define KVQ_TAIL_WARPS 8
+#endif
+#ifndef KVQ_TAIL_STAGES
+#define KVQ_TAIL_STAGES 3
+#endif
+constexpr int kWarps = KVQ_TAIL_WARPS;
+constexpr int kStageRows = 4;
+constexpr int kRowBytes = kDim * 4;
+constexpr int kStageBytes = 2 * kStageRows * kRowBytes;  // K rows then V rows
+constexpr int kStages = KVQ_TAIL_STAGES;                 // ring depth per warp
 constexpr int kMaxCluster = 8;
 constexpr float kLog2e = 1.4426950408889634f;
-
-__device__ __forceinline__ float ex2(float x) {
-    float r;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return r;
-}
-__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void cluster_sync_all() {
-    __syncwarp();
-    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
+constexpr float kSlack = 8.0f;  // weights stay <= 2^8 against a stale reference max
 
 struct TailParams {
     const float* q;         // [units][G][128]
@@ -55,175 +63,242 @@ struct TailParams {
     const float* lse;       // [units][G] decode's base-2 log-sum-exp; nullptr: no quantized part
     float* out;             // [units][G][128]: the decode's output in, the merged output out
     size_t kv_heads, tail_cap;
-    int S, rows_per_cta;
+    int G, S;
     float scale;            // log2(e) / sqrt(d)
 };
 
-// Per CTA: warp partials, then the CTA's merged (max, sum, 128 numerators) per head, which
-// rank 0 reads from every rank through DSMEM.
-template <int G>
+template <int GP>
 struct TailSmem {
-    float wm[kWarps][G];
-    float wd[kWarps][G];
-    float wn[kWarps][G][kDim];
-    float pm[G];
-    float pd[G];
-    float pn[G][kDim];
+    static constexpr int kRing = kWarps * kStages * kStageBytes;
+    // the ring; after the stream drains, the warp partials alias it
+    alignas(128) uint8_t ring[kRing];
+    uint64_t full[kWarps][kStages];
+    float wm[kWarps][GP];
+    float wd[kWarps][GP];
+    float pm[GP];
+    float pd[GP];
+    float pn[GP][kDim];
+    __device__ float* wn() { return reinterpret_cast<float*>(ring); }  // [kWarps][GP][kDim]
 };
+static_assert(kWarps * 8 * kDim * 4 <= kWarps * kStages * kStageBytes, "warp partials must fit in the ring");
 
-__device__ __forceinline__ float ld_cluster(const float* local_ptr, int rank) {
-    uint32_t addr;
-    float v;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(addr) : "r"(smem_addr(local_ptr)), "r"(rank));
-    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
-    return v;
+// Reduce-scatter of N = 4 GP per-lane partial sums: afterwards lane L holds the complete
+// warp sum of value idx(L) (idx = L >> 1 for N = 16, L for N = 32).
+template <int N>
+__device__ __forceinline__ float reduce_scatter(float (&a)[N], int lane) {
+    static_assert(N == 16 || N == 32, "4 rows x 4 or 8 heads");
+    // N = 32: lane bits 4..0 select halves; N = 16: lane bits 4..1, then bit 0 sums the pair
+    constexpr int kSteps = N == 32 ? 5 : 4;
+#pragma unroll
+    for (int st = 0; st < kSteps; ++st) {
+        const int o = 16 >> st, half = N >> (st + 1);
+        const bool b = (lane & o) != 0;
+#pragma unroll
+        for (int k = 0; k < half; ++k) {
+            const float keep = b ? a[k + half] : a[k];
+            const float send = b ? a[k] : a[k + half];
+            a[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+    }
+    float r = a[0];
+    if (N == 16) r += __shfl_xor_sync(0xffffffffu, r, 1);
+    return r;
 }
 
-template <int G>
+template <int GP>
 __global__ void __launch_bounds__(kWarps * 32) tail_kernel(const TailParams p) {
-    __shared__ TailSmem<G> sm;
-    const int S = p.S;
-    const int rank = S > 1 ? (int)cg::this_cluster().block_rank() : 0;
+    constexpr int N = kStageRows * GP;
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    TailSmem<GP>& sm = *reinterpret_cast<TailSmem<GP>*>(smem_raw);
+    const int S = p.S, G = p.G;
+    const int rank = S > 1 ? (int)cluster_rank() : 0;
     const size_t unit = blockIdx.x / S;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // tail_len was final before the decode grid passed its own dependency wait, and this
     // grid starts only after every decode CTA did (griddepcontrol.launch_dependents).
     const int len = __ldcg(p.tail_len + unit / p.kv_heads);
-    const int r0 = rank * p.rows_per_cta, r1 = min(len, r0 + p.rows_per_cta);
+    // the request's rows (not its capacity) split evenly over the ranks, in whole stages
+    const int rpc = ((len + S - 1) / S + kStageRows - 1) / kStageRows * kStageRows;
+    const int r0 = rank * rpc, r1 = min(len, r0 + rpc);
+    const int nst = r1 > r0 ? (r1 - r0 + kStageRows - 1) / kStageRows : 0;  // CTA stages
+    const int my = nst > warp ? (nst - warp + kWarps - 1) / kWarps : 0;      // this warp's
 
-    float4 q[G];
-#pragma unroll
-    for (int h = 0; h < G; ++h)
-        q[h] = __ldg(reinterpret_cast<const float4*>(p.q + (unit * G + h) * kDim) + lane);
-    float m[G], d[G];
-    float4 acc[G];
-#pragma unroll
-    for (int h = 0; h < G; ++h) m[h] = -INFINITY, d[h] = 0.0f, acc[h] = make_float4(0.f, 0.f, 0.f, 0.f);
-
-    const float4* kt = reinterpret_cast<const float4*>(p.k_tail + unit * p.tail_cap * kDim) + lane;
-    const float4* vt = reinterpret_cast<const float4*>(p.v_tail + unit * p.tail_cap * kDim) + lane;
-    for (int j0 = r0 + warp; j0 < r1; j0 += kWarps * kRows) {
-        float4 kv[kRows], vv[kRows];
-#pragma unroll
-        for (int i = 0; i < kRows; ++i) {
-            const int j = j0 + i * kWarps;
-            kv[i] = j < r1 ? __ldcs(kt + (size_t)j * (kDim / 4)) : make_float4(0.f, 0.f, 0.f, 0.f);
-            vv[i] = j < r1 ? __ldcs(vt + (size_t)j * (kDim / 4)) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-#pragma unroll
-        for (int h = 0; h < G; ++h) {
-            float t[kRows];
-#pragma unroll
-            for (int i = 0; i < kRows; ++i) {
-                float s = kv[i].x * q[h].x;
-                s = __fmaf_rn(kv[i].y, q[h].y, s);
-                s = __fmaf_rn(kv[i].z, q[h].z, s);
-                s = __fmaf_rn(kv[i].w, q[h].w, s);
-                t[i] = s;
-            }
-#pragma unroll
-            for (int o = 16; o; o >>= 1)
-#pragma unroll
-                for (int i = 0; i < kRows; ++i) t[i] += __shfl_xor_sync(0xffffffffu, t[i], o);
-            float mx = m[h];
-#pragma unroll
-            for (int i = 0; i < kRows; ++i) {
-                t[i] = j0 + i * kWarps < r1 ? t[i] * p.scale : -INFINITY;
-                mx = fmaxf(mx, t[i]);
-            }
-            if (mx > m[h]) {  // warp-uniform: rescale the running sums
-                const float c = ex2(m[h] - mx);
-                d[h] *= c;
-                acc[h].x *= c, acc[h].y *= c, acc[h].z *= c, acc[h].w *= c;
-                m[h] = mx;
-            }
-#pragma unroll
-            for (int i = 0; i < kRows; ++i) {
-                const float w = ex2(t[i] - mx);
-                d[h] += w;
-                acc[h].x = __fmaf_rn(w, vv[i].x, acc[h].x);
-                acc[h].y = __fmaf_rn(w, vv[i].y, acc[h].y);
-                acc[h].z = __fmaf_rn(w, vv[i].z, acc[h].z);
-                acc[h].w = __fmaf_rn(w, vv[i].w, acc[h].w);
-            }
-        }
+    uint8_t* ring = sm.ring + warp * kStages * kStageBytes;
+    uint64_t* full = sm.full[warp];
+    const float* kbase = p.k_tail + unit * p.tail_cap * kDim;
+    const float* vbase = p.v_tail + unit * p.tail_cap * kDim;
+    auto issue = [&](int k) {  // lane 0: this warp's k-th stage (CTA stage warp + 8k)
+        const int row = r0 + (warp + kWarps * k) * kStageRows;
+        const uint32_t bytes = (uint32_t)(min(kStageRows, r1 - row) * kRowBytes);
+        uint8_t* dst = ring + (k % kStages) * kStageBytes;
+        mbar_expect_tx(&full[k % kStages], 2 * bytes);
+        bulk_g2s(dst, kbase + (size_t)row * kDim, bytes, &full[k % kStages]);
+        bulk_g2s(dst + kStageRows * kRowBytes, vbase + (size_t)row * kDim, bytes, &full[k % kStages]);
+    };
+    if (lane == 0) {
+        for (int i = 0; i < kStages; ++i) mbar_init(&full[i], 1);
+        mbar_init_fence();
+        for (int k = 0; k < min(kStages, my); ++k) issue(k);
     }
+    __syncwarp();
+
+    float4 q[GP];
 #pragma unroll
-    for (int h = 0; h < G; ++h) {
-        if (lane == 0) sm.wm[warp][h] = m[h], sm.wd[warp][h] = d[h];
-        *reinterpret_cast<float4*>(&sm.wn[warp][h][4 * lane]) = acc[h];
+    for (int h = 0; h < GP; ++h)
+        q[h] = h < G ? __ldg(reinterpret_cast<const float4*>(p.q + (unit * G + h) * kDim) + lane)
+                     : make_float4(0.f, 0.f, 0.f, 0.f);
+    const int my_idx = N == 32 ? lane : lane >> 1;  // (row, head) of this lane's score
+    const int my_row = my_idx / GP, my_head = my_idx % GP;
+    float m[GP];
+    float4 acc[GP];
+#pragma unroll
+    for (int h = 0; h < GP; ++h) m[h] = -INFINITY, acc[h] = make_float4(0.f, 0.f, 0.f, 0.f);
+    float mh = -INFINITY;  // m[my_head]
+    float dsum = 0.0f;     // sum of this lane's own weights (head my_head)
+
+    for (int k = 0; k < my; ++k) {
+        mbar_wait(&full[k % kStages], (uint32_t)((k / kStages) & 1));
+        const float* kr = reinterpret_cast<const float*>(ring + (k % kStages) * kStageBytes);
+        const float* vr = kr + kStageRows * kDim;
+        const int rows = min(kStageRows, r1 - (r0 + (warp + kWarps * k) * kStageRows));
+        float part[N];
+#pragma unroll
+        for (int i = 0; i < kStageRows; ++i) {
+            const float4 kv = *reinterpret_cast<const float4*>(kr + i * kDim + 4 * lane);
+#pragma unroll
+            for (int h = 0; h < GP; ++h) {
+                float s = kv.x * q[h].x;
+                s = __fmaf_rn(kv.y, q[h].y, s);
+                s = __fmaf_rn(kv.z, q[h].z, s);
+                part[i * GP + h] = __fmaf_rn(kv.w, q[h].w, s);
+            }
+        }
+        float t = reduce_scatter<N>(part, lane) * p.scale;
+        if (my_row >= rows) t = -INFINITY;  // rows past the tail (stale shared memory)
+        // lazy max: rescale only when a score passes its head's reference by kSlack
+        if (__any_sync(0xffffffffu, my_head < G && t > mh + kSlack)) {
+            float nm = fmaxf(mh, t);  // new max of my head over the stage's rows (lane bits 3, 4)
+            nm = fmaxf(nm, __shfl_xor_sync(0xffffffffu, nm, 8));
+            nm = fmaxf(nm, __shfl_xor_sync(0xffffffffu, nm, 16));
+            dsum *= ex2(mh - nm);
+#pragma unroll
+            for (int h = 0; h < GP; ++h) {
+                const float nmh = __shfl_sync(0xffffffffu, nm, N == 32 ? h : 2 * h);
+                const float c = ex2(m[h] - nmh);  // 0 on the first stage (m = -inf)
+                acc[h].x *= c, acc[h].y *= c, acc[h].z *= c, acc[h].w *= c;
+                m[h] = nmh;
+            }
+            mh = nm;
+        }
+        const float w = ex2(t - mh);
+        dsum += w;
+#pragma unroll
+        for (int i = 0; i < kStageRows; ++i) {
+            if (i >= rows) break;  // warp-uniform: no stale (possibly NaN) rows past the tail
+            const float4 vv = *reinterpret_cast<const float4*>(vr + i * kDim + 4 * lane);
+#pragma unroll
+            for (int h = 0; h < GP; ++h) {
+                const float wh = __shfl_sync(0xffffffffu, w, N == 32 ? i * GP + h : 2 * (i * GP + h));
+                acc[h].x = __fmaf_rn(wh, vv.x, acc[h].x);
+                acc[h].y = __fmaf_rn(wh, vv.y, acc[h].y);
+                acc[h].z = __fmaf_rn(wh, vv.z, acc[h].z);
+                acc[h].w = __fmaf_rn(wh, vv.w, acc[h].w);
+            }
+        }
+        __syncwarp();  // every lane is done with this slot
+        if (lane == 0 && k + kStages < my) issue(k + kStages);
+    }
+    // warp partials: per-head sum over the lanes that own the head (one copy of each score)
+    if (N == 16 && (lane & 1)) dsum = 0.0f;
+    dsum += __shfl_xor_sync(0xffffffffu, dsum, 8);
+    dsum += __shfl_xor_sync(0xffffffffu, dsum, 16);
+    __syncthreads();  // every warp's stream is drained: the ring becomes the partials
+    float* wn = sm.wn();
+#pragma unroll
+    for (int h = 0; h < GP; ++h) {
+        if (lane == (N == 32 ? h : 2 * h)) sm.wm[warp][h] = m[h], sm.wd[warp][h] = dsum;
+        *reinterpret_cast<float4*>(wn + (warp * GP + h) * kDim + 4 * lane) = acc[h];
     }
     __syncthreads();
     // CTA merge: thread per (head, channel) item.
-    constexpr int kItems = (G * kDim + kWarps * 32 - 1) / (kWarps * 32);
+    constexpr int kItems = (GP * kDim + kWarps * 32 - 1) / (kWarps * 32);
 #pragma unroll
     for (int it = 0; it < kItems; ++it) {
         const int idx = threadIdx.x + it * kWarps * 32;
-        if (idx >= G * kDim) break;
         const int h = idx / kDim, ch = idx % kDim;
+        if (h >= G) break;
         float M = -INFINITY;
         for (int w = 0; w < kWarps; ++w) M = fmaxf(M, sm.wm[w][h]);
-        float D = 0.0f, N = 0.0f;
+        float D = 0.0f, Nn = 0.0f;
         if (M != -INFINITY)
             for (int w = 0; w < kWarps; ++w) {
                 const float c = ex2(sm.wm[w][h] - M);  // 0 for an empty warp (-inf)
                 D = __fmaf_rn(sm.wd[w][h], c, D);
-                N = __fmaf_rn(sm.wn[w][h][ch], c, N);
+                Nn = __fmaf_rn(wn[(w * GP + h) * kDim + ch], c, Nn);
             }
-        sm.pn[h][ch] = N;
+        sm.pn[h][ch] = Nn;
         if (ch == 0) sm.pm[h] = M, sm.pd[h] = D;
     }
-    if (S > 1) cluster_sync_all();  // every rank's partial is readable
+    if (S > 1) cluster_sync();  // every rank's partial is readable
     else __syncthreads();
     // Rank 0 folds the ranks in order (registers), then lets them go.
     float RM[kItems], RD[kItems], RN[kItems];
+#pragma unroll
+    for (int it = 0; it < kItems; ++it) RM[it] = -INFINITY, RD[it] = 0.0f, RN[it] = 0.0f;
     if (rank == 0) {
 #pragma unroll
         for (int it = 0; it < kItems; ++it) {
             const int idx = threadIdx.x + it * kWarps * 32;
-            RM[it] = -INFINITY, RD[it] = 0.0f, RN[it] = 0.0f;
-            if (idx >= G * kDim) continue;
             const int h = idx / kDim, ch = idx % kDim;
+            if (h >= G) break;
             float mr[kMaxCluster];
             for (int r = 0; r < S; ++r) {
-                mr[r] = S > 1 ? ld_cluster(&sm.pm[h], r) : sm.pm[h];
+                mr[r] = S > 1 ? ld_cluster_f32(&sm.pm[h], r) : sm.pm[h];
                 RM[it] = fmaxf(RM[it], mr[r]);
             }
             if (RM[it] == -INFINITY) continue;
             for (int r = 0; r < S; ++r) {
                 const float c = ex2(mr[r] - RM[it]);
-                RD[it] = __fmaf_rn(S > 1 ? ld_cluster(&sm.pd[h], r) : sm.pd[h], c, RD[it]);
-                RN[it] = __fmaf_rn(S > 1 ? ld_cluster(&sm.pn[h][ch], r) : sm.pn[h][ch], c, RN[it]);
+                RD[it] = __fmaf_rn(S > 1 ? ld_cluster_f32(&sm.pd[h], r) : sm.pd[h], c, RD[it]);
+                RN[it] = __fmaf_rn(S > 1 ? ld_cluster_f32(&sm.pn[h][ch], r) : sm.pn[h][ch], c, RN[it]);
             }
         }
     }
-    if (S > 1) cluster_sync_all();  // remote shared memory stays valid until rank 0 has read it
+    if (S > 1) cluster_sync();  // remote shared memory stays valid until rank 0 has read it
     if (rank != 0) return;
-    // The decode's output and log-sum-exp are complete from here on.
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+    griddep_wait();  // the decode's output and log-sum-exp are complete from here on
 #pragma unroll
     for (int it = 0; it < kItems; ++it) {
         const int idx = threadIdx.x + it * kWarps * 32;
-        if (idx >= G * kDim || RM[it] == -INFINITY) continue;  // no tail rows: the decode's output stands
         const int h = idx / kDim, ch = idx % kDim;
-        const float M = RM[it], D = RD[it], N = RN[it];
+        if (h >= G || RM[it] == -INFINITY) continue;  // no tail rows: the decode's output stands
+        const float M = RM[it], D = RD[it], Nn = RN[it];
         float* o = p.out + (unit * G + h) * kDim + ch;
         const float lv = p.lse ? p.lse[unit * G + h] : -INFINITY;
         if (lv == -INFINITY) {
-            *o = N / D;
+            *o = Nn / D;
         } else {
             const float X = fmaxf(lv, M + __log2f(D));
             const float wv = ex2(lv - X), wt = ex2(M - X);  // tail weight in total: D 2^(M - X)
-            *o = __fmaf_rn(*o, wv, N * wt) / __fmaf_rn(D, wt, wv);
+            *o = __fmaf_rn(*o, wv, Nn * wt) / __fmaf_rn(D, wt, wv);
         }
     }
 }
 
-template <int G>
-cudaError_t launch_g(const TailParams& p, size_t units, cudaStream_t s, bool pdl) {
+template <int GP>
+cudaError_t launch_gp(const TailParams& p, size_t units, cudaStream_t s, bool pdl) {
+    auto kern = tail_kernel<GP>;
+    const size_t smem = sizeof(TailSmem<GP>);
+    static bool attr_done = false;  // per instantiation
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr_done = true;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(units * p.S));
     cfg.blockDim = dim3(kWarps * 32);
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attrs[2];
     attrs[0].id = cudaLaunchAttributeClusterDimension;
@@ -234,7 +309,7 @@ cudaError_t launch_g(const TailParams& p, size_t units, cudaStream_t s, bool pdl
     attrs[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attrs;
     cfg.numAttrs = pdl ? 2 : 1;
-    return cudaLaunchKernelEx(&cfg, tail_kernel<G>, p);
+    return cudaLaunchKernelEx(&cfg, kern, p);
 }
 
 }  // namespace
@@ -243,9 +318,14 @@ bool decode_tail_supported(const DecodeArgs& a) {
     return a.dim == (size_t)kDim && a.group >= 1 && a.group <= 8 && a.tail_cap > 0 && a.units > 0;
 }
 
-// Cluster size: enough CTAs for ~4 per SM, at least 64 rows per CTA, at most 8 ranks.
+#ifndef KVQ_TAIL_CTAS_PER_SM
+#define KVQ_TAIL_CTAS_PER_SM 2
+#endif
+// Cluster size: split a unit only when the units alone leave SMs idle (~2 CTAs per SM;
+// splitting further costs more in per-CTA setup and merges than it gains, r01 sweep in
+// profiles/r01_tail_tune.txt), at least 64 rows per CTA, at most 8 ranks.
 int tail_split(size_t units, size_t tail_cap) {
-    const size_t want = (4 * 148 + units - 1) / units;
+    const size_t want = (KVQ_TAIL_CTAS_PER_SM * 148 + units - 1) / units;
     size_t s = std::min<size_t>(want, (tail_cap + 63) / 64);
     return (int)std::max<size_t>(1, std::min<size_t>(s, kMaxCluster));
 }
@@ -260,21 +340,11 @@ cudaError_t launch_decode_tail(const DecodeArgs& a, bool after_decode, cudaStrea
     p.out = a.out;
     p.kv_heads = a.kv_heads;
     p.tail_cap = a.tail_cap;
+    p.G = (int)a.group;
     p.S = tail_split(a.units, a.tail_cap);
-    p.rows_per_cta = (int)((a.tail_cap + p.S - 1) / p.S);
     p.scale = kLog2e / sqrtf((float)kDim);
-    cudaError_t e;
-    switch (a.group) {
-        case 1: e = launch_g<1>(p, a.units, s, after_decode); break;
-        case 2: e = launch_g<2>(p, a.units, s, after_decode); break;
-        case 3: e = launch_g<3>(p, a.units, s, after_decode); break;
-        case 4: e = launch_g<4>(p, a.units, s, after_decode); break;
-        case 5: e = launch_g<5>(p, a.units, s, after_decode); break;
-        case 6: e = launch_g<6>(p, a.units, s, after_decode); break;
-        case 7: e = launch_g<7>(p, a.units, s, after_decode); break;
-        case 8: e = launch_g<8>(p, a.units, s, after_decode); break;
-        default: return cudaErrorInvalidValue;
-    }
+    const cudaError_t e = a.group <= 4 ? launch_gp<4>(p, a.units, s, after_decode)
+                                       : launch_gp<8>(p, a.units, s, after_decode);
     note_launch();
     return e;
 }

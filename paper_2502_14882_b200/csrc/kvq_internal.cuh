@@ -86,7 +86,10 @@ cudaError_t launch_decode_tc(const DecodeArgs& a, cudaStream_t s);
 // with the decode's output when `after_decode` (a.tail_lse set, launched right after it).
 bool decode_tail_supported(const DecodeArgs& a);
 cudaError_t launch_decode_tail(const DecodeArgs& a, bool after_decode, cudaStream_t s);
-constexpr size_t kTcTailMax = 64;  // tail rows the tensor-core decodes keep in-kernel
+#ifndef KVQ_TC_TAIL_MAX
+#define KVQ_TC_TAIL_MAX 64
+#endif
+constexpr size_t kTcTailMax = KVQ_TC_TAIL_MAX;  // tail capacity the tensor-core decodes keep in-kernel
 size_t vx_bytes(size_t units, size_t n_vis, int bits);
 cudaError_t launch_pack_vx(const uint8_t* rows, size_t units, size_t n_vis, int bits, uint8_t* vx, cudaStream_t s);
 // tcgen05 (UTCIMMA) path, d = 128, M = 8: needs the token-packed V copy.
