@@ -51,7 +51,7 @@ inline void check(int status) {
         case KVQ_OK: return;
         case KVQ_ERR_CONFIG: throw config_error(last_error());
         case KVQ_ERR_DOMAIN: throw domain_error(last_error());
-        case KVQ_ERR_FORMAT: throw format_error(last_error(), 0);
+        case KVQ_ERR_FORMAT: throw format_error(last_error(), kvq_last_error_offset());
         default: throw device_error(last_error());
     }
 }

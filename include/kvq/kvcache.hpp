@@ -8,7 +8,11 @@
 // host copies instead of references into host vectors.
 #pragma once
 
+#include <fstream>
+#include <istream>
+#include <iterator>
 #include <memory>
+#include <ostream>
 #include <span>
 #include <string>
 #include <vector>
@@ -95,6 +99,46 @@ public:
         return CacheMemory{m[0], m[1], m[2], m[3], m[4], m[5]};
     }
 
+    // ---- snapshots (kvcache.hpp:137-218): the reference's KVQC bytes; the device cache
+    // is gathered into the image by strided device->host copies (kvq_cache_save_image).
+    void save(std::ostream& os) const {
+        std::size_t n = 0;
+        capi::check(kvq_cache_image_bytes(handle_.get(), &n));
+        std::vector<char> img(n);
+        capi::check(kvq_cache_save_image(handle_.get(), img.data(), n, 0, nullptr));
+        os.write(img.data(), static_cast<std::streamsize>(n));
+    }
+
+    void save(const std::string& path) const {
+        std::ofstream os(path, std::ios::binary);
+        if (!os) throw format_error("cannot open for writing: " + path, 0);
+        save(os);
+        if (!os) throw format_error("write failed: " + path, 0);
+    }
+
+    // Reads the stream's remaining bytes, parses one cache image from them and leaves the
+    // stream just past it (seekable streams); `off` advances like the reference's.
+    static HybridKVCache load(std::istream& is, std::uint64_t& off) {
+        const std::istream::pos_type start = is.tellg();
+        std::string img((std::istreambuf_iterator<char>(is)), std::istreambuf_iterator<char>());
+        std::size_t used = 0;
+        HybridKVCache out = from_image(img, off, &used);
+        is.clear();
+        if (start != std::istream::pos_type(-1)) is.seekg(start + static_cast<std::streamoff>(used));
+        return out;
+    }
+
+    static HybridKVCache load(const std::string& path) {
+        std::ifstream is(path, std::ios::binary);
+        if (!is) throw format_error("cannot open for reading: " + path, 0);
+        std::string img((std::istreambuf_iterator<char>(is)), std::istreambuf_iterator<char>());
+        std::uint64_t off = 0;
+        std::size_t used = 0;
+        HybridKVCache out = from_image(img, off, &used);
+        if (used != img.size()) throw format_error("trailing bytes after cache data", used);
+        return out;
+    }
+
     kvq_cache* native() const { return handle_.get(); }
 
 private:
@@ -125,6 +169,17 @@ private:
         kvq_cache* c = nullptr;
         capi::check(kvq_cache_build(kf.data(), vf.data(), 1, k.size(), 1, n, d, bits, mode, word_bits, cal.tau1,
                                     cal.tau2, &c));
+        HybridKVCache out;
+        out.handle_.reset(c);
+        return out;
+    }
+
+    static HybridKVCache from_image(const std::string& img, std::uint64_t& off, std::size_t* used) {
+        kvq_cache* c = nullptr;
+        const int st = kvq_cache_load_image(img.data(), img.size(), 1, 1, used, &c);
+        if (st == KVQ_ERR_FORMAT) throw format_error(capi::last_error(), off + kvq_last_error_offset());
+        capi::check(st);
+        off += *used;
         HybridKVCache out;
         out.handle_.reset(c);
         return out;

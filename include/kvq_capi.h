@@ -50,6 +50,9 @@ extern "C" {
 /* Copies the calling thread's last error message (NUL-terminated, truncated to cap);
  * returns its full length. */
 size_t kvq_last_error(char* buf, size_t cap);
+/* Byte offset carried by the calling thread's last KVQ_ERR_FORMAT (format_error::offset,
+ * errors.hpp:23-33). */
+unsigned long long kvq_last_error_offset(void);
 /* Number of CUDA kernels this library has launched in this process. */
 unsigned long long kvq_launch_count(void);
 /* 1 if a CUDA device is usable (the library never falls back to the CPU). */
@@ -188,6 +191,22 @@ int kvq_cache_read_tail(const kvq_cache* c, size_t unit, int which, float* out);
 /* Raw device pointers (k_codes, v_codes, k_alpha, k_beta, v_alpha, v_beta, k_tail, v_tail,
  * tail_len) for zero-copy integration with a serving engine. */
 int kvq_cache_device_pointers(const kvq_cache* c, void* ptrs[9]);
+
+/* ---- cache snapshots (HybridKVCache::save / load, kvcache.hpp:137-218) -------------
+ * The image is the reference's KVQC byte stream: manifest, then per unit ("head") a KVQP
+ * K segment, a KVQP V segment, a KVQT K tail and a KVQT V tail (quantize.hpp:148-230,
+ * tensor_io.hpp:11-128), little-endian, byte-identical to the reference's save(). */
+int kvq_cache_image_bytes(const kvq_cache* c, size_t* bytes);
+/* Writes the image into `image` (host memory, or device memory when image_on_device) of
+ * `capacity` bytes; stream NULL = the cache's stream. DOMAIN if the buffer is too small. */
+int kvq_cache_save_image(const kvq_cache* c, void* image, size_t capacity, int image_on_device,
+                         void* stream);
+/* Parses and validates an image in host memory (the reference's format_error messages and
+ * byte offsets, kvq_last_error_offset) and builds a device cache of `batch` requests
+ * (heads / batch KV heads each) with query group `group`. *consumed (nullable) = the
+ * image's length; bytes beyond it are left to the caller (file loads reject them). */
+int kvq_cache_load_image(const void* image, size_t bytes, size_t batch, size_t group,
+                         size_t* consumed, kvq_cache** out);
 
 #ifdef __cplusplus
 }

@@ -275,6 +275,8 @@ class Ref:
             "kvqr_cache_memory": (C.c_int, [_VP, _SZP]),
             "kvqr_bench_decode": (C.c_int, [_F, _F, _SZ, _SZ, _SZ, _SZ, _SZ, C.c_int, C.c_int, C.c_float, C.c_float,
                                             _F, _F, _F, C.c_int, C.c_int, _SZ, C.POINTER(C.c_double), _F]),
+            "kvqr_cache_save": (C.c_int, [C.c_void_p, C.c_void_p, _SZ, _SZP]),
+            "kvqr_cache_load": (C.c_int, [C.c_void_p, _SZ, C.POINTER(C.c_void_p), C.POINTER(C.c_uint64)]),
             "kvqr_grid_mse_table": (C.c_int, [_F, _F, _U8, _F, _F, _SZ, _SZ, _SZ, C.c_int, C.c_int, _F, _F, _SZ,
                                               C.POINTER(C.c_double), _F]),
             "kvqr_mse_report": (C.c_int, [_F, _F, _SZ, _SZ, _SZ, C.c_int, C.c_int, C.c_int, C.c_float, C.c_float,
@@ -370,6 +372,16 @@ class Ref:
         return out
 
     # -- HybridKVCache
+    def cache_load(self, image: bytes, heads: int, dim: int):
+        """HybridKVCache::load -> (RefCache, None) or (None, (status, message, offset))."""
+        out = C.c_void_p()
+        off = C.c_uint64(0)
+        buf = (C.c_uint8 * max(len(image), 1)).from_buffer_copy(image or b"\0")
+        st = self.L.kvqr_cache_load(buf, len(image), C.byref(out), C.byref(off))
+        if st != 0:
+            return None, (st, self.L.kvqr_last_error().decode(), int(off.value))
+        return RefCache(self, out.value, heads, dim), None
+
     def cache_build(self, k, v, bits, word_bits=8, tau1=0.0, tau2=0.0, mode=0):
         """k, v: [heads][n][dim]."""
         k, v = _f32(k), _f32(v)
@@ -446,3 +458,10 @@ class RefCache:
         m = (C.c_size_t * 6)()
         self.ref.L.kvqr_cache_memory(self.h, m)
         return [int(x) for x in m]
+
+    def save(self) -> bytes:
+        n = C.c_size_t(0)
+        self.ref._ok(self.ref.L.kvqr_cache_save(self.h, None, 0, C.byref(n)))
+        buf = (C.c_uint8 * n.value)()
+        self.ref._ok(self.ref.L.kvqr_cache_save(self.h, buf, n.value, C.byref(n)))
+        return bytes(buf)

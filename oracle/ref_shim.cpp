@@ -15,6 +15,7 @@
 #include <cstring>
 #include <exception>
 #include <span>
+#include <sstream>
 #include <string>
 #include <thread>
 #include <vector>
@@ -316,6 +317,38 @@ int kvqr_cache_segment(const kvqr_cache* c, std::size_t h, int which, std::uint8
     std::copy(s.stats.alpha.begin(), s.stats.alpha.end(), alpha);
     std::copy(s.stats.beta.begin(), s.stats.beta.end(), beta);
     return 0;
+}
+
+// HybridKVCache::save into a caller buffer (*len = bytes needed; copies only if it fits).
+int kvqr_cache_save(const kvqr_cache* c, std::uint8_t* buf, std::size_t cap, std::size_t* len) {
+    try {
+        std::stringstream ss;
+        c->cache.save(ss);
+        const std::string b = ss.str();
+        *len = b.size();
+        if (b.size() <= cap) std::memcpy(buf, b.data(), b.size());
+        return 0;
+    } catch (const std::exception& e) { return fail(e); }
+}
+
+// HybridKVCache::load from a byte image; *err_off = format_error::offset() on failure.
+int kvqr_cache_load(const std::uint8_t* buf, std::size_t len, kvqr_cache** out, std::uint64_t* err_off) {
+    try {
+        std::stringstream ss(std::string(reinterpret_cast<const char*>(buf), len));
+        std::uint64_t off = 0;
+        auto* c = new kvqr_cache;
+        try {
+            c->cache = kvq::HybridKVCache::load(ss, off);
+        } catch (...) {
+            delete c;
+            throw;
+        }
+        *out = c;
+        return 0;
+    } catch (const kvq::format_error& e) {
+        *err_off = e.offset();
+        return fail(e);
+    } catch (const std::exception& e) { return fail(e); }
 }
 
 int kvqr_cache_memory(const kvqr_cache* c, std::size_t* out6) {

@@ -38,7 +38,11 @@ class DomainError(KvqError):
 
 
 class FormatError(KvqError):
-    """kvq::format_error: malformed serialized data."""
+    """kvq::format_error: malformed serialized data; `offset` = the byte where parsing failed."""
+
+    def __init__(self, msg: str, offset: int = 0):
+        super().__init__(f"{msg} (byte offset {offset})")
+        self.message, self.offset = msg, offset
 
 
 class CudaError(KvqError):
@@ -101,6 +105,10 @@ def lib() -> C.CDLL:
             "kvq_cache_read_segment": (C.c_int, [_VP, _SZ, C.c_int, _U8, _F, _F]),
             "kvq_cache_read_tail": (C.c_int, [_VP, _SZ, C.c_int, _F]),
             "kvq_cache_device_pointers": (C.c_int, [_VP, C.POINTER(_VP)]),
+            "kvq_last_error_offset": (C.c_ulonglong, []),
+            "kvq_cache_image_bytes": (C.c_int, [_VP, _SZP]),
+            "kvq_cache_save_image": (C.c_int, [_VP, _VP, _SZ, C.c_int, _VP]),
+            "kvq_cache_load_image": (C.c_int, [_VP, _SZ, _SZ, _SZ, _SZP, C.POINTER(_VP)]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -114,7 +122,10 @@ def _check(status: int) -> None:
     if status != 0:
         buf = C.create_string_buffer(1024)
         lib().kvq_last_error(buf, 1024)
-        raise _ERRS.get(status, KvqError)(buf.value.decode(errors="replace"))
+        msg = buf.value.decode(errors="replace")
+        if status == 3:
+            raise FormatError(msg, int(lib().kvq_last_error_offset()))
+        raise _ERRS.get(status, KvqError)(msg)
 
 
 def _f32(a) -> np.ndarray:
@@ -700,6 +711,34 @@ class BatchedCache:
                                             cal.tau2, stream, C.byref(out)))
         return cls(out.value)
 
+    # -- snapshots: the reference's KVQC bytes (kvcache.hpp:137-218), every unit a "head"
+    def image_bytes(self) -> int:
+        n = C.c_size_t(0)
+        _check(lib().kvq_cache_image_bytes(self._h, C.byref(n)))
+        return n.value
+
+    def save_image(self) -> bytes:
+        """The cache as one KVQC image (host bytes)."""
+        n = self.image_bytes()
+        buf = (C.c_uint8 * n)()
+        _check(lib().kvq_cache_save_image(self._h, C.cast(buf, _VP), n, 0, None))
+        return bytes(buf)
+
+    def save_image_device(self, out, stream: int = 0) -> None:
+        """The image into a torch CUDA uint8 tensor of image_bytes() (checkpoint or migrate
+        a cache without a host round trip)."""
+        _check(lib().kvq_cache_save_image(self._h, out.data_ptr(), out.numel(), 1, stream or None))
+
+    @classmethod
+    def load_image(cls, image: bytes, batch: int = 1, group: int = 1) -> tuple["BatchedCache", int]:
+        """Parse a KVQC image (heads = batch x kv_heads units); returns (cache, bytes used)."""
+        data = bytes(image)
+        buf = (C.c_uint8 * max(len(data), 1)).from_buffer_copy(data or b"\0")
+        used = C.c_size_t(0)
+        out = C.c_void_p()
+        _check(lib().kvq_cache_load_image(C.cast(buf, _VP), len(data), batch, group, C.byref(used), C.byref(out)))
+        return cls(out.value), used.value
+
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value and _lib is not None:
@@ -896,6 +935,36 @@ class HybridKVCache:
 
     def memory(self) -> CacheMemory:
         return self._c.memory()
+
+    def save(self, path) -> None:
+        """HybridKVCache::save (kvcache.hpp:137-161): the reference's KVQC bytes."""
+        data = self._c.save_image()
+        try:
+            with open(path, "wb") as f:
+                f.write(data)
+        except OSError as e:
+            raise FormatError(f"cannot open for writing: {path}") from e
+
+    @classmethod
+    def load(cls, path) -> "HybridKVCache":
+        """HybridKVCache::load (kvcache.hpp:163-218); trailing bytes are a format error."""
+        try:
+            with open(path, "rb") as f:
+                data = f.read()
+        except OSError as e:
+            raise FormatError(f"cannot open for reading: {path}") from e
+        c, used = BatchedCache.load_image(data)
+        if used != len(data):
+            raise FormatError("trailing bytes after cache data", used)
+        return cls(c)
+
+    @classmethod
+    def from_bytes(cls, image: bytes) -> tuple["HybridKVCache", int]:
+        c, used = BatchedCache.load_image(image)
+        return cls(c), used
+
+    def to_bytes(self) -> bytes:
+        return self._c.save_image()
 
     @property
     def batched(self) -> BatchedCache:

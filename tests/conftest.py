@@ -45,3 +45,12 @@ def kvq():
     if not k.device_available():
         pytest.fail("no CUDA device: gpu tests must run on a B200 (no CPU fallback exists)")
     return k
+
+
+@pytest.fixture(scope="session")
+def kvq_host():
+    """The product library without requiring a device: host-side paths only (argument and
+    file-format validation, which run before any device work)."""
+    from paper_2502_14882_b200 import kvq as k
+    k.lib()
+    return k

@@ -4,6 +4,8 @@
 #include <cmath>
 #include <cstdio>
 #include <random>
+#include <sstream>
+#include <fstream>
 #include <vector>
 
 #include "kvq/kvq.hpp"
@@ -225,6 +227,58 @@ int main() {
         CHECK(std::abs(report.mean_mse_quant - mq / 3.0) <= 1e-12);
         CHECK_THROWS(mse_report(std::span<const HeadWorkload>{}, qcfg, CalibrationParams{}), domain_error);
         CHECK_THROWS(mse_report(heads, qcfg, CalibrationParams{}, 0), config_error);
+    }
+    // Snapshots (test_kvcache.cpp:307-395, test_quantize.cpp:233-290, test_tensor.cpp:69-141).
+    {
+        std::mt19937_64 rng(11);
+        std::vector<DenseMatrix> ks, vs;
+        for (int h = 0; h < 2; ++h) ks.push_back(random_matrix(rng, 24, 8, -2, 2)), vs.push_back(random_matrix(rng, 24, 8, -2, 2));
+        HybridKVCache cache = HybridKVCache::build(ks, vs, QuantizationConfig{4, QuantMode::channel_wise, 8},
+                                                   CalibrationParams{2.0f, 1.0f});
+        DenseMatrix kn = random_matrix(rng, 2, 8, -2, 2);
+        cache.append(kn, kn);
+        DenseMatrix q = random_matrix(rng, 2, 8, -1, 1);
+        std::stringstream ss;
+        cache.save(ss);
+        ss << "after";  // data following the image stays in the stream
+        std::uint64_t off = 0;
+        HybridKVCache back = HybridKVCache::load(ss, off);
+        std::string rest;
+        ss >> rest;
+        CHECK(rest == "after");
+        CHECK(off == ss.str().size() - 5);
+        CHECK(back.heads() == 2 && back.dim() == 8 && back.bitwidth() == 4 && back.tail_tokens() == 1);
+        CHECK(back.calibration() == (CalibrationParams{2.0f, 1.0f}));
+        CHECK(back.decode_step(q).data == cache.decode_step(q).data);
+        CHECK(back.memory().total_bytes == cache.memory().total_bytes);
+        const std::string path = "/tmp/kvq_dropin_cache.kvqc";
+        cache.save(path);
+        CHECK(HybridKVCache::load(path).decode_step(q).data == cache.decode_step(q).data);
+        { std::ofstream os(path, std::ios::binary | std::ios::app); os << "x"; }
+        CHECK_THROWS(HybridKVCache::load(path), format_error);
+        std::string bytes = ss.str().substr(0, ss.str().size() - 5);
+        bytes[0] = 'Z';
+        std::stringstream bad(bytes);
+        off = 0;
+        try {
+            HybridKVCache::load(bad, off);
+            CHECK(false);
+        } catch (const format_error& e) {
+            CHECK(e.offset() == 0);
+        }
+        // KVQP + KVQT records
+        QuantizedSegment seg = cache.key_segment(0);
+        std::stringstream s2;
+        write_segment(s2, seg);
+        off = 0;
+        QuantizedSegment seg2 = read_segment(s2, off);
+        CHECK(seg2.codes.bytes == seg.codes.bytes && seg2.stats.alpha == seg.stats.alpha && seg2.tokens == 24);
+        DenseMatrix t = cache.key_tail(1);
+        std::stringstream s3;
+        write_tensor(s3, t);
+        off = 0;
+        CHECK(read_tensor(s3, off) == t);
+        CHECK(off == 24 + 4 * 8);
     }
     std::printf(g_fail ? "test_dropin: %d failures\n" : "test_dropin: all passed%.0d\n", g_fail);
     return g_fail ? 1 : 0;

@@ -248,15 +248,77 @@ def report_cases():
     np.savez_compressed(HERE / "mse_report.npz", **out)
 
 
+# (name, heads, n_vis, dim, bits (16 = full precision), word_bits, tau, appends)
+CACHE_IO_CASES = [
+    ("q4", 2, 24, 8, 4, 8, (2.0, 1.0), 1),      # test_kvcache.cpp:307-335
+    ("fp", 2, 12, 6, 16, 8, (0.0, 0.0), 0),     # test_kvcache.cpp:337-351
+    ("d128", 3, 300, 128, 1, 8, (1.0, 0.0), 5),
+    ("m16", 2, 10, 5, 2, 16, (0.0, 0.0), 2),    # padded rows, 16-bit words
+    ("empty", 2, 0, 8, 2, 8, (1.0, 0.0), 3),    # quantized cache with no prefill
+]
+# byte mutations of the q4 image (test_kvcache.cpp:353-395 and the record readers):
+# (label, offset or -1 = truncate to `value` bytes, value)
+CACHE_IO_MUTATIONS = [
+    ("magic", 0, ord("Z")), ("version", 4, 9), ("bitwidth", 24, 5), ("manifest_tokens", 28, 7),
+    ("trunc_half", -1, 514), ("trunc_head", -1, 100), ("seg_magic", 52, ord("X")), ("seg_widths", 60, 3),
+    ("seg_logical", 64, 191), ("tail_nan", -2, 0), ("trunc_alpha", -1, 52 + 20 + 96 + 8 + 10),
+]
+
+
+def cache_io_cases():
+    """HybridKVCache::save images (kvcache.hpp:137-161) and load errors (163-211) from the
+    unmodified reference."""
+    R = Ref()
+    rng = np.random.default_rng(2511)
+    out = {}
+    for name, h, n, d, bits, wb, tau, appends in CACHE_IO_CASES:
+        k = rng.uniform(-2, 2, (h, n, d)).astype(np.float32)
+        v = rng.uniform(-2, 2, (h, n, d)).astype(np.float32)
+        c = R.cache_build(k, v, bits, wb, tau[0], tau[1])
+        kn = rng.uniform(-2, 2, (appends, h, d)).astype(np.float32)
+        vn = rng.uniform(-2, 2, (appends, h, d)).astype(np.float32)
+        for t in range(appends):
+            c.append(kn[t], vn[t])
+        q = rng.uniform(-1, 1, (h, d)).astype(np.float32)
+        o, _, _ = c.decode(q, n + appends)
+        img = np.frombuffer(c.save(), np.uint8)
+        out.update({f"{name}_k": k, f"{name}_v": v, f"{name}_kn": kn, f"{name}_vn": vn, f"{name}_q": q,
+                    f"{name}_out": o, f"{name}_image": img})
+    base = bytes(out["q4_image"])
+    msgs, offs = [], []
+    for label, at, val in CACHE_IO_MUTATIONS:
+        b = bytearray(base)
+        if at == -1:
+            b = b[:val]
+        elif at == -2:  # a NaN in the first head's K tail data
+            seg = 20 + 24 * 8 * 4 // 8 + 8 + 2 * 4 * 8  # q4 segment: 24 rows x 8 dims x 4 bits, dim 8
+            b[52 + 2 * seg + 24: 52 + 2 * seg + 28] = np.array([np.nan], np.float32).tobytes()
+        else:
+            b[at] = val
+        c, err = R.cache_load(bytes(b), 2, 8)
+        assert err is not None and err[0] == 3, (label, err)
+        msgs.append(err[1])
+        offs.append(err[2])
+    out["mut_labels"] = np.array([m[0] for m in CACHE_IO_MUTATIONS])
+    out["mut_at"] = np.array([m[1] for m in CACHE_IO_MUTATIONS])
+    out["mut_val"] = np.array([m[2] for m in CACHE_IO_MUTATIONS])
+    out["mut_msg"] = np.array(msgs)
+    out["mut_off"] = np.array(offs, np.uint64)
+    np.savez_compressed(HERE / "cache_io.npz", **out)
+
+
 if __name__ == "__main__":
     import sys as _sys
     if len(_sys.argv) > 1 and _sys.argv[1] == "grid":
         grid_cases()
     elif len(_sys.argv) > 1 and _sys.argv[1] == "report":
         report_cases()
+    elif len(_sys.argv) > 1 and _sys.argv[1] == "cache_io":
+        cache_io_cases()
     else:
         quant_cases()
         kernel_cases()
         decode_cases()
         grid_cases()
         report_cases()
+        cache_io_cases()
