@@ -408,7 +408,9 @@ __global__ void __launch_bounds__(kWarps * 32, OCC) decode_tc_kernel(const TcPar
     if (threadIdx.x < kDim) {
         constexpr int cpb = Gm::kCpb;
         const int c = threadIdx.x;
-        const int s_slot = cpb - 1 - c % cpb, qidx = c / cpb;
+        // raw row byte of channel c: c / cpb for M = 8, the same byte of the reversed LE word
+        // for M = 16 / 32 (bitpack.hpp:85)
+        const int s_slot = cpb - 1 - c % cpb, qidx = (c / cpb) ^ (a.word_bits / 8 - 1);
         const int j = qidx & 3, tb = qidx >> 2;
         const int tt = tb / BITS, u = tb % BITS;
         const int rho = u * cpb + s_slot, kb = rho >> 1, r = rho & 1;
@@ -936,7 +938,7 @@ cudaError_t launch_occ(const DecodeArgs& a, cudaStream_t s) {
 namespace {
 template <int BITS>
 __global__ void __launch_bounds__(32) pack_vx_kernel(const uint8_t* __restrict__ rows, size_t n, size_t nb32,
-                                                     uint8_t* __restrict__ vx) {
+                                                     int bx, uint8_t* __restrict__ vx) {
     constexpr int kRowBytes = 16 * BITS;
     constexpr int NW = (2 * BITS + 3) / 4;
     const size_t unit = blockIdx.y, blk = blockIdx.x;
@@ -948,12 +950,12 @@ __global__ void __launch_bounds__(32) pack_vx_kernel(const uint8_t* __restrict__
 #pragma unroll
         for (int ii = 0; ii < 4; ++ii) {
             const size_t tok = blk * 32 + 4 * grp + t + 8 * ii;
-            const uint8_t* rp = rows + (unit * n + tok) * kRowBytes + 2 * BITS * g;
+            const uint8_t* rp = rows + (unit * n + tok) * kRowBytes;  // byte (2 BITS g + k) ^ bx
 #pragma unroll
             for (int wi = 0; wi < NW; ++wi) {
                 uint32_t w = 0;
                 for (int by = 0; by < 4 && 4 * wi + by < 2 * BITS; ++by)
-                    w |= (tok < n ? (uint32_t)rp[4 * wi + by] : 0u) << (8 * by);
+                    w |= (tok < n ? (uint32_t)rp[(2 * BITS * g + 4 * wi + by) ^ bx] : 0u) << (8 * by);
                 raw[ii][wi] = w;
             }
         }
@@ -982,15 +984,19 @@ __global__ void __launch_bounds__(32) pack_vx_kernel(const uint8_t* __restrict__
 
 size_t vx_bytes(size_t units, size_t n_vis, int bits) { return units * ((n_vis + 31) / 32) * 32 * 16 * (size_t)bits; }
 
-cudaError_t launch_pack_vx(const uint8_t* rows, size_t units, size_t n_vis, int bits, uint8_t* vx, cudaStream_t s) {
+cudaError_t launch_pack_vx(const uint8_t* rows, size_t units, size_t n_vis, int bits, int word_bits, uint8_t* vx,
+                           cudaStream_t s) {
     if (n_vis == 0 || units == 0) return cudaSuccess;
     const size_t nb32 = (n_vis + 31) / 32;
     dim3 grid((unsigned)nb32, (unsigned)units);
+    // M = 16 / 32 rows are M = 8 rows with the bytes of each LE word reversed
+    // (bitpack.hpp:85: code i of a word at bit M - N(i+1)): read byte k ^ (M/8 - 1).
+    const int bx = word_bits / 8 - 1;
     switch (bits) {
-        case 1: pack_vx_kernel<1><<<grid, 32, 0, s>>>(rows, n_vis, nb32, vx); break;
-        case 2: pack_vx_kernel<2><<<grid, 32, 0, s>>>(rows, n_vis, nb32, vx); break;
-        case 4: pack_vx_kernel<4><<<grid, 32, 0, s>>>(rows, n_vis, nb32, vx); break;
-        case 8: pack_vx_kernel<8><<<grid, 32, 0, s>>>(rows, n_vis, nb32, vx); break;
+        case 1: pack_vx_kernel<1><<<grid, 32, 0, s>>>(rows, n_vis, nb32, bx, vx); break;
+        case 2: pack_vx_kernel<2><<<grid, 32, 0, s>>>(rows, n_vis, nb32, bx, vx); break;
+        case 4: pack_vx_kernel<4><<<grid, 32, 0, s>>>(rows, n_vis, nb32, bx, vx); break;
+        case 8: pack_vx_kernel<8><<<grid, 32, 0, s>>>(rows, n_vis, nb32, bx, vx); break;
         default: return cudaErrorInvalidValue;
     }
     note_launch();
@@ -1029,7 +1035,8 @@ static size_t tc_smem_for(int S) {
 }
 
 bool decode_tc_supported(const DecodeArgs& a) {
-    if (a.dim != (size_t)kDim || a.word_bits != 8 || a.n_vis == 0 || !a.v_codes_x) return false;
+    if (a.dim != (size_t)kDim || a.n_vis == 0 || !a.v_codes_x) return false;
+    if (a.word_bits != 8 && a.word_bits != 16 && a.word_bits != 32) return false;
     if (a.bits != 1 && a.bits != 2 && a.bits != 4 && a.bits != 8) return false;
     if (a.group < 1 || a.group > 8) return false;
     if (a.units == 0) return false;

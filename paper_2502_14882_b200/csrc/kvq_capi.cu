@@ -366,9 +366,9 @@ void quantize_prefill(kvq_cache* c, const float* dk, const float* dv, cudaStream
 // Device layout for the tcgen05 decode: V codes re-packed along the token axis. Built on
 // first use of that path (the default IMMA path reads the reference layout).
 void ensure_vx(kvq_cache* c, cudaStream_t s) {
-    if (c->vx.p || c->dim != 128 || c->word_bits != 8 || c->n_vis == 0) return;
+    if (c->vx.p || c->dim != 128 || c->n_vis == 0 || c->bits == KVQ_FULL_PRECISION_BITS) return;
     c->vx.alloc(kvqb::vx_bytes(c->units, c->n_vis, c->bits));
-    ck(kvqb::launch_pack_vx(c->v_codes(), c->units, c->n_vis, c->bits, c->vx.p, s), "pack vx");
+    ck(kvqb::launch_pack_vx(c->v_codes(), c->units, c->n_vis, c->bits, c->word_bits, c->vx.p, s), "pack vx");
 }
 
 void ensure_vt(kvq_cache* c, cudaStream_t s) {

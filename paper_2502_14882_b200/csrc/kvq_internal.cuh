@@ -91,7 +91,8 @@ cudaError_t launch_decode_tail(const DecodeArgs& a, bool after_decode, cudaStrea
 #endif
 constexpr size_t kTcTailMax = KVQ_TC_TAIL_MAX;  // tail capacity the tensor-core decodes keep in-kernel
 size_t vx_bytes(size_t units, size_t n_vis, int bits);
-cudaError_t launch_pack_vx(const uint8_t* rows, size_t units, size_t n_vis, int bits, uint8_t* vx, cudaStream_t s);
+cudaError_t launch_pack_vx(const uint8_t* rows, size_t units, size_t n_vis, int bits, int word_bits, uint8_t* vx,
+                           cudaStream_t s);
 // tcgen05 (UTCIMMA) path, d = 128, M = 8: needs the token-packed V copy.
 size_t vt_bytes(size_t units, size_t n_vis, int bits);
 cudaError_t launch_pack_vt(const uint8_t* rows, size_t units, size_t n_vis, int bits, uint8_t* vt, cudaStream_t s);

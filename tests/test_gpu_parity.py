@@ -188,8 +188,8 @@ def test_decode_golden_trajectories(kvq, oracle, name, path):
     z = np.load(GOLD / name)
     h, n, d, bits, wb, steps = z["meta"].tolist()
     t1, t2 = z["tau"].tolist()
-    if path in ("tc", "umma") and (d != 128 or wb != 8 or bits == 16 or n == 0):
-        pytest.skip("tensor-core paths need d = 128, M = 8 and a quantized prefill")
+    if path in ("tc", "umma") and (d != 128 or bits == 16 or n == 0 or (path == "umma" and wb != 8)):
+        pytest.skip("tensor-core paths need d = 128 and a quantized prefill (tcgen05: M = 8)")
     k, v = _load_inputs(z, oracle)
     if bits == 16:
         cache = kvq.HybridKVCache.build_full_precision(list(k), list(v))
@@ -394,21 +394,21 @@ def test_step_api_matches_decode_then_append(kvq):
 
 
 @pytest.mark.parametrize("name", ["decode_d128_b2_m32.npz", "decode_d128_b4_m32.npz", "decode_d128_b8_m32.npz"])
-@pytest.mark.parametrize("path", ["tc", "umma"])
-def test_decode_golden_m8_tensor_paths(kvq, oracle, name, path):
+@pytest.mark.parametrize("path,wb", [("tc", 8), ("umma", 8), ("tc", 16)])
+def test_decode_golden_m8_tensor_paths(kvq, oracle, name, path, wb):
     """The b >= 2 golden trajectories were produced by the reference with M = 32 (its M = 8
     table path is defective for b >= 2 at n >= 512). The codes are the
     same for every M, so the M = 8 tensor-core paths must reproduce those outputs."""
     z = np.load(GOLD / name)
-    h, n, d, bits, wb, steps = z["meta"].tolist()
+    h, n, d, bits, _, steps = z["meta"].tolist()  # made with M = 32
     t1, t2 = z["tau"].tolist()
     k, v = _load_inputs(z, oracle)
-    cache = kvq.HybridKVCache.build(list(k), list(v), kvq.QuantizationConfig(bits, kvq.QuantMode.channel_wise, 8),
+    cache = kvq.HybridKVCache.build(list(k), list(v), kvq.QuantizationConfig(bits, kvq.QuantMode.channel_wise, wb),
                                     kvq.CalibrationParams(t1, t2))
     cache.batched.set_path(kvq.PATH_TC if path == "tc" else kvq.PATH_UMMA)
     for hh in range(h):
         ka, kb = oracle.compute_stats(k[hh])
-        assert np.array_equal(cache.key_segment(hh).codes.bytes, oracle.quantize(k[hh], ka, kb, bits, 8))
+        assert np.array_equal(cache.key_segment(hh).codes.bytes, oracle.quantize(k[hh], ka, kb, bits, wb))
     for t in range(steps):
         out = cache.decode_step(z[f"q{t}"])
         tol = TOL_IMMA if path == "tc" else TOL_TC
