@@ -880,7 +880,8 @@ __global__ void __launch_bounds__(kWarps * 32, OCC) decode_tc_kernel(const TcPar
 void plan(const DecodeArgs& a, int& S, int& T) {
     const int n = (int)a.n_vis;
     int s_min = std::max(1, (n + kCtaTokens - 1) / kCtaTokens);
-    const int want = (int)((2 * 148 + a.units - 1) / a.units);
+    const size_t pu = a.plan_units ? a.plan_units : a.units;  // a chunk plans as its whole batch
+    const int want = (int)((2 * 148 + pu - 1) / pu);
     int s = std::max(s_min, std::min(want, kMaxCluster));
     s = std::min(s, std::max(1, (n + 255) / 256));
     T = ((n + s - 1) / s + 255) / 256 * 256;  // multiple of 8 warps x 32 tokens

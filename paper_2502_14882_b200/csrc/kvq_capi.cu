@@ -4,6 +4,7 @@
 // result comes out of a CUDA kernel, and a missing device is a hard KVQ_ERR_CUDA.
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -134,6 +135,8 @@ struct kvq_cache {
     cudaStream_t stream = nullptr;
     cudaStream_t side = nullptr;       // kvq_cache_step: new K/V rows upload + append
     cudaEvent_t decoded = nullptr;     // kvq_cache_step: decode retired -> append may run
+    cudaStream_t d2h = nullptr;        // kvq_cache_step (chunked): output downloads
+    std::vector<cudaEvent_t> ev_q, ev_dec;  // kvq_cache_step (chunked): per-chunk hand-offs
     DevBuf<uint8_t> codes;   // [2][units][n_vis][rb]  (K then V)
     DevBuf<uint8_t> vt;      // token-packed V codes for the tcgen05 decode (d = 128, M = 8)
     DevBuf<uint8_t> vx;      // V codes pre-arranged as IMMA operands for the default decode
@@ -156,6 +159,9 @@ struct kvq_cache {
         if (stream) cudaStreamDestroy(stream);
         if (side) cudaStreamDestroy(side);
         if (decoded) cudaEventDestroy(decoded);
+        if (d2h) cudaStreamDestroy(d2h);
+        for (cudaEvent_t e : ev_q) cudaEventDestroy(e);
+        for (cudaEvent_t e : ev_dec) cudaEventDestroy(e);
     }
 };
 
@@ -819,6 +825,48 @@ int kvq_cache_decode_device(kvq_cache* c, const float* queries, float* out, void
     return guarded([&] { run_decode(c, queries, out, false, false, (cudaStream_t)stream); });
 }
 
+}  // extern "C"
+
+namespace {
+
+// Requests [b0, b1) of the cache as DecodeArgs: every per-unit array is unit-major and
+// tail_len request-major, so a request range is a pointer offset.
+kvqb::DecodeArgs range_args(const kvqb::DecodeArgs& a, const kvq_cache* c, size_t b0, size_t b1) {
+    kvqb::DecodeArgs r = a;
+    const size_t u0 = b0 * c->kv_heads, d = c->dim, G = c->group;
+    r.k_codes += u0 * c->n_vis * c->rb;
+    r.v_codes += u0 * c->n_vis * c->rb;
+    if (r.v_codes_x) r.v_codes_x += kvqb::vx_bytes(u0, c->n_vis, c->bits);
+    r.k_alpha += u0 * d;
+    r.k_beta += u0 * d;
+    r.v_alpha += u0 * d;
+    r.v_beta += u0 * d;
+    r.k_tail += u0 * c->tail_cap * d;
+    r.v_tail += u0 * c->tail_cap * d;
+    r.tail_len += b0;
+    r.q += u0 * G * d;
+    r.out += u0 * G * d;
+    if (r.tail_lse) r.tail_lse += u0 * G;
+    r.units = (b1 - b0) * c->kv_heads;
+    r.plan_units = c->units;  // chunked results are bit-identical to the whole-batch decode
+    return r;
+}
+
+// How many request chunks one host-buffer step is cut into: each chunk's query upload,
+// decode and output download run on their own streams, so chunk i's decode overlaps chunk
+// i+1's upload and chunk i-1's download. KVQ_STEP_CHUNKS overrides (tuning).
+size_t step_chunks(const kvq_cache* c) {
+    static const char* env = std::getenv("KVQ_STEP_CHUNKS");
+    // measured (profiles/r01_e2e_chunks.txt): c5 B=512 706 -> 519 us/step with 4 chunks,
+    // c2 B=64 unchanged at 2 (its uploads are short next to the decode)
+    size_t k = env ? (size_t)std::max(1, std::atoi(env)) : (c->batch >= 256 ? 4 : c->batch >= 32 ? 2 : 1);
+    return std::min(k, c->batch);
+}
+
+}  // namespace
+
+extern "C" {
+
 int kvq_cache_step(kvq_cache* c, const float* queries, const float* k_new, const float* v_new, float* out) {
     return guarded([&] {
         grow_tail(c, c->n_tail + 1);
@@ -826,18 +874,123 @@ int kvq_cache_step(kvq_cache* c, const float* queries, const float* k_new, const
         // it and the append waits for the decode (which must not see the new row); the
         // output download overlaps the append.
         cudaStream_t s = c->stream, s2 = c->side;
+        const size_t chunks = step_chunks(c);
+        kvqb::DecodeArgs a = decode_args(c, c->d_q.p, c->d_out.p);
+        if (chunks > 1 && c->path != KVQ_PATH_GENERIC && c->path != KVQ_PATH_UMMA) {
+            ensure_vx(c, s);
+            a.v_codes_x = c->vx.p;
+            if (c->tail_cap > kvqb::kTcTailMax && kvqb::decode_tail_supported(a)) {
+                if (c->lse.n < c->units * c->group) c->lse.alloc(c->units * c->group);
+                a.tail_lse = c->lse.p;
+            }
+        }
+        if (chunks > 1 && c->path != KVQ_PATH_GENERIC && c->path != KVQ_PATH_UMMA && kvqb::decode_tc_supported(a)) {
+            // pipelined: [upload q_i] -> [decode_i] -> [download out_i] on three streams
+            if (!c->d2h) ck(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking), "stream");
+            while (c->ev_q.size() < chunks) {
+                cudaEvent_t e1, e2;
+                ck(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming), "event");
+                ck(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming), "event");
+                c->ev_q.push_back(e1);
+                c->ev_dec.push_back(e2);
+            }
+            const size_t per_req = c->kv_heads * c->group * c->dim;
+            auto bounds = [&](size_t i) { return c->batch * i / chunks; };
+            // Debug timeline (KVQ_STEP_TRACE): per-chunk device times on stderr.
+            static const bool trace = std::getenv("KVQ_STEP_TRACE") != nullptr;
+            std::vector<cudaEvent_t> tq, td, to;
+            cudaEvent_t t0 = nullptr;
+            if (trace) {
+                cudaEventCreate(&t0);
+                tq.resize(chunks), td.resize(chunks), to.resize(chunks);
+                for (size_t i = 0; i < chunks; ++i)
+                    cudaEventCreate(&tq[i]), cudaEventCreate(&td[i]), cudaEventCreate(&to[i]);
+                cudaEventRecord(t0, s2);
+            }
+            for (size_t i = 0; i < chunks; ++i) {
+                const size_t b0 = bounds(i), b1 = bounds(i + 1);
+                ck(cudaMemcpyAsync(c->d_q.p + b0 * per_req, queries + b0 * per_req, (b1 - b0) * per_req * 4,
+                                   cudaMemcpyHostToDevice, s2), "H2D");
+                ck(cudaEventRecord(c->ev_q[i], s2), "event");
+                if (trace) cudaEventRecord(tq[i], s2);
+            }
+            c->d_knew.upload(k_new, c->units * c->dim, s2);
+            c->d_vnew.upload(v_new, c->units * c->dim, s2);
+            for (size_t i = 0; i < chunks; ++i) {
+                const size_t b0 = bounds(i), b1 = bounds(i + 1);
+                ck(cudaStreamWaitEvent(s, c->ev_q[i], 0), "event");
+                const kvqb::DecodeArgs r = range_args(a, c, b0, b1);
+                ck(kvqb::launch_decode_tc(r, s), "decode (tc)");
+                if (r.tail_lse) ck(kvqb::launch_decode_tail(r, true, s), "decode (tail)");
+                ck(cudaEventRecord(c->ev_dec[i], s), "event");
+                if (trace) cudaEventRecord(td[i], s);
+                ck(cudaStreamWaitEvent(c->d2h, c->ev_dec[i], 0), "event");
+                ck(cudaMemcpyAsync(out + b0 * per_req, c->d_out.p + b0 * per_req, (b1 - b0) * per_req * 4,
+                                   cudaMemcpyDeviceToHost, c->d2h), "D2H");
+                if (trace) cudaEventRecord(to[i], c->d2h);
+            }
+            ck(cudaEventRecord(c->decoded, s2), "event");  // new K/V rows are on the device
+            ck(cudaStreamWaitEvent(s, c->decoded, 0), "event");
+            ck(kvqb::launch_append(c->d_knew.p, c->d_vnew.p, c->batch, c->kv_heads, c->dim, c->tail_cap,
+                                   c->k_tail.p, c->v_tail.p, c->tail_len.p, s), "append");
+            sync(c->d2h);
+            sync(s);
+            c->n_tail += 1;
+            if (trace) {
+                std::string line = "[step x" + std::to_string(chunks) + "]";
+                for (size_t i = 0; i < chunks; ++i) {
+                    float a1, a2, a3;
+                    cudaEventElapsedTime(&a1, t0, tq[i]);
+                    cudaEventElapsedTime(&a2, t0, td[i]);
+                    cudaEventElapsedTime(&a3, t0, to[i]);
+                    char b[96];
+                    std::snprintf(b, sizeof(b), " | q %.1f dec %.1f out %.1f", 1e3 * a1, 1e3 * a2, 1e3 * a3);
+                    line += b;
+                    cudaEventDestroy(tq[i]), cudaEventDestroy(td[i]), cudaEventDestroy(to[i]);
+                }
+                cudaEventDestroy(t0);
+                std::fprintf(stderr, "%s us\n", line.c_str());
+            }
+            return;
+        }
+        // Debug timeline (KVQ_STEP_TRACE): device intervals of one step on stderr.
+        static const bool trace = std::getenv("KVQ_STEP_TRACE") != nullptr;
+        cudaEvent_t ev[5] = {};
+        const auto h0 = std::chrono::steady_clock::now();
+        if (trace)
+            for (auto& e : ev) cudaEventCreate(&e);
+        if (trace) cudaEventRecord(ev[0], s);
         c->d_q.upload(queries, c->q_elems(), s);
+        if (trace) cudaEventRecord(ev[1], s);
+        // the new K/V rows only feed the append: upload them behind the queries (one copy
+        // engine direction), overlapped with the decode
+        ck(cudaEventRecord(c->decoded, s), "event");
+        ck(cudaStreamWaitEvent(s2, c->decoded, 0), "event");
         c->d_knew.upload(k_new, c->units * c->dim, s2);
         c->d_vnew.upload(v_new, c->units * c->dim, s2);
         run_decode(c, c->d_q.p, c->d_out.p, false, false, s);
+        if (trace) cudaEventRecord(ev[2], s);
         ck(cudaEventRecord(c->decoded, s), "event");
         c->d_out.download(out, c->q_elems(), s);
+        if (trace) cudaEventRecord(ev[3], s);
         ck(cudaStreamWaitEvent(s2, c->decoded, 0), "event");
         ck(kvqb::launch_append(c->d_knew.p, c->d_vnew.p, c->batch, c->kv_heads, c->dim, c->tail_cap,
                                c->k_tail.p, c->v_tail.p, c->tail_len.p, s2), "append");
+        if (trace) cudaEventRecord(ev[4], s2);
+        const auto h1 = std::chrono::steady_clock::now();
         sync(s);
         sync(s2);
         c->n_tail += 1;
+        if (trace) {
+            float t[4];
+            for (int i = 0; i < 4; ++i) cudaEventElapsedTime(&t[i], ev[0], ev[i + 1]);
+            const double issue = std::chrono::duration<double, std::micro>(h1 - h0).count();
+            const double wall =
+                std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count();
+            std::fprintf(stderr, "[step] q %.1f dec %.1f out %.1f app %.1f us (device); issue %.1f wall %.1f us\n",
+                         1e3 * t[0], 1e3 * t[1], 1e3 * t[2], 1e3 * t[3], issue, wall);
+            for (auto& e : ev) cudaEventDestroy(e);
+        }
     });
 }
 

@@ -75,6 +75,8 @@ struct DecodeArgs {
     float* tail_lse;      // nullable: the fp32 tail is left to the tail pass (k2_tail.cu); the
                           // decode writes its base-2 log-sum-exp per (unit, head) here
     size_t units, kv_heads, group, dim, n_vis, tail_cap, weights_stride;
+    size_t plan_units;    // 0, or the whole batch's units when `units` is one chunk of it: the
+                          // split (and so the summation order) is the whole batch's
     int bits, word_bits;
     float tau1, tau2;
 };

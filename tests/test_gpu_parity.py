@@ -375,9 +375,12 @@ def test_batched_gqa_vs_oracle(kvq, oracle, bits, G, n):
         tv.append(vn)
 
 
-def test_step_api_matches_decode_then_append(kvq):
+@pytest.mark.parametrize("B", [3, 40])
+def test_step_api_matches_decode_then_append(kvq, B):
+    """kvq_cache_step == decode + append, bit for bit; B = 40 takes the pipelined step
+    (request chunks: upload / decode / download overlapped on three streams)."""
     rng = np.random.default_rng(12)
-    B, H, G, n, d = 3, 2, 4, 200, 128
+    H, G, n, d = 2, 4, 200, 128
     k = rng.normal(size=(B, H, n, d)).astype(np.float32)
     v = rng.normal(size=(B, H, n, d)).astype(np.float32)
     c1 = kvq.BatchedCache.build(k, v, kvq.QuantizationConfig(1), kvq.CalibrationParams(1, 0), group=G)
