@@ -883,6 +883,8 @@ void plan(const DecodeArgs& a, int& S, int& T) {
     const size_t pu = a.plan_units ? a.plan_units : a.units;  // a chunk plans as its whole batch
     const int want = (int)((2 * 148 + pu - 1) / pu);
     int s = std::max(s_min, std::min(want, kMaxCluster));
+    static const int force = std::getenv("KVQ_TC_SPLIT") ? std::atoi(std::getenv("KVQ_TC_SPLIT")) : 0;  // tuning
+    if (force > 0) s = std::max(s_min, std::min(force, kMaxCluster));
     s = std::min(s, std::max(1, (n + 255) / 256));
     T = ((n + s - 1) / s + 255) / 256 * 256;  // multiple of 8 warps x 32 tokens
     S = (n + T - 1) / T;
