@@ -137,6 +137,7 @@ struct kvq_cache {
     cudaEvent_t decoded = nullptr;     // kvq_cache_step: decode retired -> append may run
     cudaStream_t d2h = nullptr;        // kvq_cache_step (chunked): output downloads
     std::vector<cudaEvent_t> ev_q, ev_dec;  // kvq_cache_step (chunked): per-chunk hand-offs
+    std::vector<cudaStream_t> chunk_streams;  // kvq_cache_step (chunked): one decode stream per chunk
     DevBuf<uint8_t> codes;   // [2][units][n_vis][rb]  (K then V)
     DevBuf<uint8_t> vt;      // token-packed V codes for the tcgen05 decode (d = 128, M = 8)
     DevBuf<uint8_t> vx;      // V codes pre-arranged as IMMA operands for the default decode
@@ -162,6 +163,7 @@ struct kvq_cache {
         if (d2h) cudaStreamDestroy(d2h);
         for (cudaEvent_t e : ev_q) cudaEventDestroy(e);
         for (cudaEvent_t e : ev_dec) cudaEventDestroy(e);
+        for (cudaStream_t x : chunk_streams) cudaStreamDestroy(x);
     }
 };
 
@@ -889,22 +891,28 @@ int kvq_cache_step(kvq_cache* c, const float* queries, const float* k_new, const
             if (!c->d2h) ck(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking), "stream");
             while (c->ev_q.size() < chunks) {
                 cudaEvent_t e1, e2;
+                cudaStream_t cs;
                 ck(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming), "event");
                 ck(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming), "event");
+                ck(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "stream");
                 c->ev_q.push_back(e1);
                 c->ev_dec.push_back(e2);
+                c->chunk_streams.push_back(cs);
             }
+            // every chunk decodes on its own stream as soon as its queries are on the device:
+            // a chunk alone does not fill the GPU (a CTA's latency, not its count, sets the
+            // time), so the chunks' decodes must overlap, not queue
             const size_t per_req = c->kv_heads * c->group * c->dim;
             auto bounds = [&](size_t i) { return c->batch * i / chunks; };
             // Debug timeline (KVQ_STEP_TRACE): per-chunk device times on stderr.
             static const bool trace = std::getenv("KVQ_STEP_TRACE") != nullptr;
-            std::vector<cudaEvent_t> tq, td, to;
+            std::vector<cudaEvent_t> tq, td, to, tb;
             cudaEvent_t t0 = nullptr;
             if (trace) {
                 cudaEventCreate(&t0);
-                tq.resize(chunks), td.resize(chunks), to.resize(chunks);
+                tq.resize(chunks), td.resize(chunks), to.resize(chunks), tb.resize(chunks);
                 for (size_t i = 0; i < chunks; ++i)
-                    cudaEventCreate(&tq[i]), cudaEventCreate(&td[i]), cudaEventCreate(&to[i]);
+                    cudaEventCreate(&tq[i]), cudaEventCreate(&td[i]), cudaEventCreate(&to[i]), cudaEventCreate(&tb[i]);
                 cudaEventRecord(t0, s2);
             }
             for (size_t i = 0; i < chunks; ++i) {
@@ -918,12 +926,14 @@ int kvq_cache_step(kvq_cache* c, const float* queries, const float* k_new, const
             c->d_vnew.upload(v_new, c->units * c->dim, s2);
             for (size_t i = 0; i < chunks; ++i) {
                 const size_t b0 = bounds(i), b1 = bounds(i + 1);
-                ck(cudaStreamWaitEvent(s, c->ev_q[i], 0), "event");
+                cudaStream_t cs = c->chunk_streams[i];
+                ck(cudaStreamWaitEvent(cs, c->ev_q[i], 0), "event");
+                if (trace) cudaEventRecord(tb[i], cs);
                 const kvqb::DecodeArgs r = range_args(a, c, b0, b1);
-                ck(kvqb::launch_decode_tc(r, s), "decode (tc)");
-                if (r.tail_lse) ck(kvqb::launch_decode_tail(r, true, s), "decode (tail)");
-                ck(cudaEventRecord(c->ev_dec[i], s), "event");
-                if (trace) cudaEventRecord(td[i], s);
+                ck(kvqb::launch_decode_tc(r, cs), "decode (tc)");
+                if (r.tail_lse) ck(kvqb::launch_decode_tail(r, true, cs), "decode (tail)");
+                ck(cudaEventRecord(c->ev_dec[i], cs), "event");
+                if (trace) cudaEventRecord(td[i], cs);
                 ck(cudaStreamWaitEvent(c->d2h, c->ev_dec[i], 0), "event");
                 ck(cudaMemcpyAsync(out + b0 * per_req, c->d_out.p + b0 * per_req, (b1 - b0) * per_req * 4,
                                    cudaMemcpyDeviceToHost, c->d2h), "D2H");
@@ -931,6 +941,7 @@ int kvq_cache_step(kvq_cache* c, const float* queries, const float* k_new, const
             }
             ck(cudaEventRecord(c->decoded, s2), "event");  // new K/V rows are on the device
             ck(cudaStreamWaitEvent(s, c->decoded, 0), "event");
+            for (size_t i = 0; i < chunks; ++i) ck(cudaStreamWaitEvent(s, c->ev_dec[i], 0), "event");
             ck(kvqb::launch_append(c->d_knew.p, c->d_vnew.p, c->batch, c->kv_heads, c->dim, c->tail_cap,
                                    c->k_tail.p, c->v_tail.p, c->tail_len.p, s), "append");
             sync(c->d2h);
@@ -939,14 +950,16 @@ int kvq_cache_step(kvq_cache* c, const float* queries, const float* k_new, const
             if (trace) {
                 std::string line = "[step x" + std::to_string(chunks) + "]";
                 for (size_t i = 0; i < chunks; ++i) {
-                    float a1, a2, a3;
+                    float a1, a2, a3, a0;
                     cudaEventElapsedTime(&a1, t0, tq[i]);
+                    cudaEventElapsedTime(&a0, t0, tb[i]);
                     cudaEventElapsedTime(&a2, t0, td[i]);
                     cudaEventElapsedTime(&a3, t0, to[i]);
-                    char b[96];
-                    std::snprintf(b, sizeof(b), " | q %.1f dec %.1f out %.1f", 1e3 * a1, 1e3 * a2, 1e3 * a3);
+                    char b[128];
+                    std::snprintf(b, sizeof(b), " | q %.1f dec %.1f-%.1f out %.1f", 1e3 * a1, 1e3 * a0, 1e3 * a2,
+                                  1e3 * a3);
                     line += b;
-                    cudaEventDestroy(tq[i]), cudaEventDestroy(td[i]), cudaEventDestroy(to[i]);
+                    cudaEventDestroy(tq[i]), cudaEventDestroy(td[i]), cudaEventDestroy(to[i]), cudaEventDestroy(tb[i]);
                 }
                 cudaEventDestroy(t0);
                 std::fprintf(stderr, "%s us\n", line.c_str());
