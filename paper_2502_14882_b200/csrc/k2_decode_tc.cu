@@ -344,7 +344,9 @@ __global__ void __launch_bounds__(kWarps * 32, OCC) decode_tc_kernel(const TcPar
     if (threadIdx.x == 0) TTRACE(7);
     griddep_wait();  // the previous step's append (tail rows, tail_len) and q are visible from here on
     const int ntl = own_tail ? __ldcg(a.tail_len + unit / a.kv_heads) : 0;
-    if (a.tail_lse) griddep_launch();  // the tail pass may start streaming the fp32 tail
+    // Dependents (the tail pass, or the append) may launch now: this grid is fully resident
+    // once every CTA has passed here, and they wait for its completion before writing.
+    griddep_launch();
     if (threadIdx.x == 0) TTRACE(3);
 
     // ---- fold the K scales into the query (scale_query, kernels.hpp:183-194) ----

@@ -17,9 +17,38 @@ __global__ void append_kernel(const float* __restrict__ k_new, const float* __re
     // prologue now; it reads the tail only after griddepcontrol.wait (= this grid done).
     asm volatile("griddepcontrol.launch_dependents;");
     const size_t b = blockIdx.x;
-    const size_t slot = (size_t)tail_len[b];
     const size_t n = kv_heads * dim;
     const bool vec = (dim % 4) == 0;
+    if (vec && n <= 4 * 4 * blockDim.x) {
+        // Launched right behind the decode (programmatic dependent launch): the new rows
+        // are read while the decode finishes; the tail is written once it has retired.
+        float4 kr[4], vr[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const size_t i = threadIdx.x + (size_t)r * blockDim.x;
+            if (4 * i < n) {
+                kr[r] = *reinterpret_cast<const float4*>(k_new + b * n + 4 * i);
+                vr[r] = *reinterpret_cast<const float4*>(v_new + b * n + 4 * i);
+            }
+        }
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        const size_t slot = (size_t)tail_len[b];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const size_t i = threadIdx.x + (size_t)r * blockDim.x;
+            if (4 * i < n) {
+                const size_t h = (4 * i) / dim, c = (4 * i) % dim;
+                const size_t dst = ((b * kv_heads + h) * tail_cap + slot) * dim + c;
+                *reinterpret_cast<float4*>(k_tail + dst) = kr[r];
+                *reinterpret_cast<float4*>(v_tail + dst) = vr[r];
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) tail_len[b] = (int)(slot + 1);
+        return;
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const size_t slot = (size_t)tail_len[b];
     for (size_t i = threadIdx.x; i < (vec ? n / 4 : n); i += blockDim.x) {
         if (vec) {
             size_t h = (i * 4) / dim, c = (i * 4) % dim;
@@ -43,10 +72,17 @@ __global__ void append_kernel(const float* __restrict__ k_new, const float* __re
 cudaError_t launch_append(const float* k_new, const float* v_new, size_t batch, size_t kv_heads,
                           size_t dim, size_t tail_cap, float* k_tail, float* v_tail,
                           int* tail_len, cudaStream_t s) {
-    append_kernel<<<(unsigned)batch, 256, 0, s>>>(k_new, v_new, kv_heads, dim, tail_cap, k_tail, v_tail,
-                                                  tail_len);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)batch);
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
     note_launch();
-    return cudaGetLastError();
+    return cudaLaunchKernelEx(&cfg, append_kernel, k_new, v_new, kv_heads, dim, tail_cap, k_tail, v_tail, tail_len);
 }
 
 }  // namespace kvqb
