@@ -124,6 +124,19 @@ void sync(cudaStream_t s) { ck(cudaStreamSynchronize(s), "kernel execution"); }
 
 }  // namespace
 
+// The host buffers and cache state a captured step graph is valid for.
+struct StepKey {
+    const void *q = nullptr, *k = nullptr, *v = nullptr;
+    void* out = nullptr;
+    size_t tail_cap = 0;
+    int path = -1;
+    size_t chunks = 0;
+    bool operator==(const StepKey& o) const {
+        return q == o.q && k == o.k && v == o.v && out == o.out && tail_cap == o.tail_cap && path == o.path &&
+               chunks == o.chunks;
+    }
+};
+
 // ------------------------------------------------------------------------------------
 struct kvq_cache {
     size_t batch = 0, kv_heads = 0, group = 0, n_vis = 0, dim = 0, units = 0;
@@ -138,6 +151,9 @@ struct kvq_cache {
     cudaStream_t d2h = nullptr;        // kvq_cache_step (chunked): output downloads
     std::vector<cudaEvent_t> ev_q, ev_dec;  // kvq_cache_step (chunked): per-chunk hand-offs
     std::vector<cudaStream_t> chunk_streams;  // kvq_cache_step (chunked): one decode stream per chunk
+    cudaEvent_t ev_fork = nullptr, ev_kv = nullptr, ev_join = nullptr;  // kvq_cache_step fork / join
+    cudaGraphExec_t step_exec = nullptr;  // kvq_cache_step replay for the buffers in step_key
+    StepKey step_key;
     DevBuf<uint8_t> codes;   // [2][units][n_vis][rb]  (K then V)
     DevBuf<uint8_t> vt;      // token-packed V codes for the tcgen05 decode (d = 128, M = 8)
     DevBuf<uint8_t> vx;      // V codes pre-arranged as IMMA operands for the default decode
@@ -164,6 +180,9 @@ struct kvq_cache {
         for (cudaEvent_t e : ev_q) cudaEventDestroy(e);
         for (cudaEvent_t e : ev_dec) cudaEventDestroy(e);
         for (cudaStream_t x : chunk_streams) cudaStreamDestroy(x);
+        for (cudaEvent_t e : {ev_fork, ev_kv, ev_join})
+            if (e) cudaEventDestroy(e);
+        if (step_exec) cudaGraphExecDestroy(step_exec);
     }
 };
 
@@ -857,6 +876,137 @@ kvqb::DecodeArgs range_args(const kvqb::DecodeArgs& a, const kvq_cache* c, size_
 // How many request chunks one host-buffer step is cut into: each chunk's query upload,
 // decode and output download run on their own streams, so chunk i's decode overlaps chunk
 // i+1's upload and chunk i-1's download. KVQ_STEP_CHUNKS overrides (tuning).
+size_t step_chunks(const kvq_cache* c);
+
+// The chunk count a step will actually use: chunking needs the tensor-core decode.
+size_t step_chunks_for(kvq_cache* c) {
+    size_t chunks = step_chunks(c);
+    if (chunks <= 1 || c->path == KVQ_PATH_GENERIC || c->path == KVQ_PATH_UMMA) return 1;
+    kvqb::DecodeArgs a = decode_args(c, c->d_q.p, c->d_out.p);
+    ensure_vx(c, c->stream);
+    a.v_codes_x = c->vx.p;
+    if (c->tail_cap > kvqb::kTcTailMax && kvqb::decode_tail_supported(a)) {
+        if (c->lse.n < c->units * c->group) c->lse.alloc(c->units * c->group);
+        a.tail_lse = c->lse.p;
+    }
+    return kvqb::decode_tc_supported(a) ? chunks : 1;
+}
+
+// Streams and events of the host-buffer step, created before any graph capture.
+void step_resources(kvq_cache* c, size_t chunks) {
+    auto event = [](cudaEvent_t& e) {
+        if (!e) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    };
+    if (!c->d2h) ck(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking), "stream");
+    event(c->ev_fork);
+    event(c->ev_kv);
+    event(c->ev_join);
+    while (c->ev_q.size() < chunks) {
+        cudaEvent_t e1 = nullptr, e2 = nullptr;
+        cudaStream_t cs;
+        event(e1);
+        event(e2);
+        ck(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "stream");
+        c->ev_q.push_back(e1);
+        c->ev_dec.push_back(e2);
+        c->chunk_streams.push_back(cs);
+    }
+}
+
+// One decode + append step from host buffers (kvq_main.cpp:313-321 order). Streams it
+// forks from c->stream all rejoin it, so one wait on c->stream (or one graph launch)
+// covers the step:
+//   side    : query upload(s) ... new K/V rows upload (one copy-engine queue, queries first)
+//   chunk i : decode of requests [b_i, b_{i+1}) as soon as their queries are on the device
+//             (chunk decodes overlap: one chunk alone is latency-, not throughput-bound)
+//   d2h     : output download of each chunk once it is decoded
+//   stream  : the append, after every decode read the tail and the new rows are uploaded
+void issue_step(kvq_cache* c, const float* queries, const float* k_new, const float* v_new, float* out,
+                size_t chunks) {
+    cudaStream_t s = c->stream, s2 = c->side, d2h = c->d2h;
+    ck(cudaEventRecord(c->ev_fork, s), "event");
+    ck(cudaStreamWaitEvent(s2, c->ev_fork, 0), "event");
+    ck(cudaStreamWaitEvent(d2h, c->ev_fork, 0), "event");
+    const size_t per_req = c->kv_heads * c->group * c->dim;
+    auto bounds = [&](size_t i) { return c->batch * i / chunks; };
+    for (size_t i = 0; i < chunks; ++i) {
+        const size_t b0 = bounds(i), b1 = bounds(i + 1);
+        ck(cudaMemcpyAsync(c->d_q.p + b0 * per_req, queries + b0 * per_req, (b1 - b0) * per_req * 4,
+                           cudaMemcpyHostToDevice, s2), "H2D");
+        ck(cudaEventRecord(c->ev_q[i], s2), "event");
+    }
+    c->d_knew.upload(k_new, c->units * c->dim, s2);
+    c->d_vnew.upload(v_new, c->units * c->dim, s2);
+    ck(cudaEventRecord(c->ev_kv, s2), "event");
+    if (chunks == 1) {
+        ck(cudaStreamWaitEvent(s, c->ev_q[0], 0), "event");
+        run_decode(c, c->d_q.p, c->d_out.p, false, false, s);
+        ck(cudaEventRecord(c->ev_dec[0], s), "event");
+    } else {
+        kvqb::DecodeArgs a = decode_args(c, c->d_q.p, c->d_out.p);
+        a.v_codes_x = c->vx.p;
+        if (c->tail_cap > kvqb::kTcTailMax && kvqb::decode_tail_supported(a)) a.tail_lse = c->lse.p;
+        for (size_t i = 0; i < chunks; ++i) {
+            cudaStream_t cs = c->chunk_streams[i];
+            ck(cudaStreamWaitEvent(cs, c->ev_q[i], 0), "event");
+            const kvqb::DecodeArgs r = range_args(a, c, bounds(i), bounds(i + 1));
+            ck(kvqb::launch_decode_tc(r, cs), "decode (tc)");
+            if (r.tail_lse) ck(kvqb::launch_decode_tail(r, true, cs), "decode (tail)");
+            ck(cudaEventRecord(c->ev_dec[i], cs), "event");
+            ck(cudaStreamWaitEvent(s, c->ev_dec[i], 0), "event");
+        }
+    }
+    for (size_t i = 0; i < chunks; ++i) {
+        const size_t b0 = bounds(i), b1 = bounds(i + 1);
+        ck(cudaStreamWaitEvent(d2h, c->ev_dec[i], 0), "event");
+        ck(cudaMemcpyAsync(out + b0 * per_req, c->d_out.p + b0 * per_req, (b1 - b0) * per_req * 4,
+                           cudaMemcpyDeviceToHost, d2h), "D2H");
+    }
+    ck(cudaEventRecord(c->ev_join, d2h), "event");
+    ck(cudaStreamWaitEvent(s, c->ev_kv, 0), "event");
+    ck(kvqb::launch_append(c->d_knew.p, c->d_vnew.p, c->batch, c->kv_heads, c->dim, c->tail_cap, c->k_tail.p,
+                           c->v_tail.p, c->tail_len.p, s), "append");
+    ck(cudaStreamWaitEvent(s, c->ev_join, 0), "event");
+}
+
+// Records the step just issued for these host buffers as a CUDA graph (memcpy and kernel
+// nodes on the same streams), replayed while the buffers, the tail capacity and the path
+// stay the same. KVQ_STEP_GRAPH=0 disables (and debug tracing does).
+void capture_step(kvq_cache* c, const StepKey& key) {
+    static const bool off = (std::getenv("KVQ_STEP_GRAPH") && std::atoi(std::getenv("KVQ_STEP_GRAPH")) == 0) ||
+                            std::getenv("KVQ_TRACE_FILE");
+    if (off) return;
+    if (c->step_exec) cudaGraphExecDestroy(c->step_exec);
+    c->step_exec = nullptr;
+    cudaGraph_t g = nullptr;
+    cudaStream_t s = c->stream;
+    if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    try {
+        issue_step(c, static_cast<const float*>(key.q), static_cast<const float*>(key.k),
+                   static_cast<const float*>(key.v), static_cast<float*>(key.out), key.chunks);
+    } catch (const Error&) {
+        cudaStreamEndCapture(s, &g);
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();
+        return;
+    }
+    if (cudaStreamEndCapture(s, &g) != cudaSuccess || !g) {
+        cudaGetLastError();
+        return;
+    }
+    cudaGraphExec_t exec = nullptr;
+    if (cudaGraphInstantiate(&exec, g, 0) == cudaSuccess) {
+        c->step_exec = exec;
+        c->step_key = key;
+    } else {
+        cudaGetLastError();
+    }
+    cudaGraphDestroy(g);
+}
+
 size_t step_chunks(const kvq_cache* c) {
     static const char* env = std::getenv("KVQ_STEP_CHUNKS");
     // measured (profiles/r01_e2e_chunks.txt): c5 B=512 706 -> 519 us/step with 4 chunks,
@@ -872,138 +1022,20 @@ extern "C" {
 int kvq_cache_step(kvq_cache* c, const float* queries, const float* k_new, const float* v_new, float* out) {
     return guarded([&] {
         grow_tail(c, c->n_tail + 1);
-        // Two streams: the queries upload feeds the decode; the new K/V rows upload overlaps
-        // it and the append waits for the decode (which must not see the new row); the
-        // output download overlaps the append.
-        cudaStream_t s = c->stream, s2 = c->side;
-        const size_t chunks = step_chunks(c);
-        kvqb::DecodeArgs a = decode_args(c, c->d_q.p, c->d_out.p);
-        if (chunks > 1 && c->path != KVQ_PATH_GENERIC && c->path != KVQ_PATH_UMMA) {
-            ensure_vx(c, s);
-            a.v_codes_x = c->vx.p;
-            if (c->tail_cap > kvqb::kTcTailMax && kvqb::decode_tail_supported(a)) {
-                if (c->lse.n < c->units * c->group) c->lse.alloc(c->units * c->group);
-                a.tail_lse = c->lse.p;
-            }
-        }
-        if (chunks > 1 && c->path != KVQ_PATH_GENERIC && c->path != KVQ_PATH_UMMA && kvqb::decode_tc_supported(a)) {
-            // pipelined: [upload q_i] -> [decode_i] -> [download out_i] on three streams
-            if (!c->d2h) ck(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking), "stream");
-            while (c->ev_q.size() < chunks) {
-                cudaEvent_t e1, e2;
-                cudaStream_t cs;
-                ck(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming), "event");
-                ck(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming), "event");
-                ck(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "stream");
-                c->ev_q.push_back(e1);
-                c->ev_dec.push_back(e2);
-                c->chunk_streams.push_back(cs);
-            }
-            // every chunk decodes on its own stream as soon as its queries are on the device:
-            // a chunk alone does not fill the GPU (a CTA's latency, not its count, sets the
-            // time), so the chunks' decodes must overlap, not queue
-            const size_t per_req = c->kv_heads * c->group * c->dim;
-            auto bounds = [&](size_t i) { return c->batch * i / chunks; };
-            // Debug timeline (KVQ_STEP_TRACE): per-chunk device times on stderr.
-            static const bool trace = std::getenv("KVQ_STEP_TRACE") != nullptr;
-            std::vector<cudaEvent_t> tq, td, to, tb;
-            cudaEvent_t t0 = nullptr;
-            if (trace) {
-                cudaEventCreate(&t0);
-                tq.resize(chunks), td.resize(chunks), to.resize(chunks), tb.resize(chunks);
-                for (size_t i = 0; i < chunks; ++i)
-                    cudaEventCreate(&tq[i]), cudaEventCreate(&td[i]), cudaEventCreate(&to[i]), cudaEventCreate(&tb[i]);
-                cudaEventRecord(t0, s2);
-            }
-            for (size_t i = 0; i < chunks; ++i) {
-                const size_t b0 = bounds(i), b1 = bounds(i + 1);
-                ck(cudaMemcpyAsync(c->d_q.p + b0 * per_req, queries + b0 * per_req, (b1 - b0) * per_req * 4,
-                                   cudaMemcpyHostToDevice, s2), "H2D");
-                ck(cudaEventRecord(c->ev_q[i], s2), "event");
-                if (trace) cudaEventRecord(tq[i], s2);
-            }
-            c->d_knew.upload(k_new, c->units * c->dim, s2);
-            c->d_vnew.upload(v_new, c->units * c->dim, s2);
-            for (size_t i = 0; i < chunks; ++i) {
-                const size_t b0 = bounds(i), b1 = bounds(i + 1);
-                cudaStream_t cs = c->chunk_streams[i];
-                ck(cudaStreamWaitEvent(cs, c->ev_q[i], 0), "event");
-                if (trace) cudaEventRecord(tb[i], cs);
-                const kvqb::DecodeArgs r = range_args(a, c, b0, b1);
-                ck(kvqb::launch_decode_tc(r, cs), "decode (tc)");
-                if (r.tail_lse) ck(kvqb::launch_decode_tail(r, true, cs), "decode (tail)");
-                ck(cudaEventRecord(c->ev_dec[i], cs), "event");
-                if (trace) cudaEventRecord(td[i], cs);
-                ck(cudaStreamWaitEvent(c->d2h, c->ev_dec[i], 0), "event");
-                ck(cudaMemcpyAsync(out + b0 * per_req, c->d_out.p + b0 * per_req, (b1 - b0) * per_req * 4,
-                                   cudaMemcpyDeviceToHost, c->d2h), "D2H");
-                if (trace) cudaEventRecord(to[i], c->d2h);
-            }
-            ck(cudaEventRecord(c->decoded, s2), "event");  // new K/V rows are on the device
-            ck(cudaStreamWaitEvent(s, c->decoded, 0), "event");
-            for (size_t i = 0; i < chunks; ++i) ck(cudaStreamWaitEvent(s, c->ev_dec[i], 0), "event");
-            ck(kvqb::launch_append(c->d_knew.p, c->d_vnew.p, c->batch, c->kv_heads, c->dim, c->tail_cap,
-                                   c->k_tail.p, c->v_tail.p, c->tail_len.p, s), "append");
-            sync(c->d2h);
+        cudaStream_t s = c->stream;
+        const size_t chunks = step_chunks_for(c);
+        step_resources(c, chunks);
+        const StepKey key{queries, k_new, v_new, out, c->tail_cap, c->path, chunks};
+        if (c->step_exec && c->step_key == key) {  // replay: one launch, one wait
+            ck(cudaGraphLaunch(c->step_exec, s), "step graph");
             sync(s);
             c->n_tail += 1;
-            if (trace) {
-                std::string line = "[step x" + std::to_string(chunks) + "]";
-                for (size_t i = 0; i < chunks; ++i) {
-                    float a1, a2, a3, a0;
-                    cudaEventElapsedTime(&a1, t0, tq[i]);
-                    cudaEventElapsedTime(&a0, t0, tb[i]);
-                    cudaEventElapsedTime(&a2, t0, td[i]);
-                    cudaEventElapsedTime(&a3, t0, to[i]);
-                    char b[128];
-                    std::snprintf(b, sizeof(b), " | q %.1f dec %.1f-%.1f out %.1f", 1e3 * a1, 1e3 * a0, 1e3 * a2,
-                                  1e3 * a3);
-                    line += b;
-                    cudaEventDestroy(tq[i]), cudaEventDestroy(td[i]), cudaEventDestroy(to[i]), cudaEventDestroy(tb[i]);
-                }
-                cudaEventDestroy(t0);
-                std::fprintf(stderr, "%s us\n", line.c_str());
-            }
             return;
         }
-        // Debug timeline (KVQ_STEP_TRACE): device intervals of one step on stderr.
-        static const bool trace = std::getenv("KVQ_STEP_TRACE") != nullptr;
-        cudaEvent_t ev[5] = {};
-        const auto h0 = std::chrono::steady_clock::now();
-        if (trace)
-            for (auto& e : ev) cudaEventCreate(&e);
-        if (trace) cudaEventRecord(ev[0], s);
-        c->d_q.upload(queries, c->q_elems(), s);
-        if (trace) cudaEventRecord(ev[1], s);
-        // the new K/V rows only feed the append: upload them behind the queries (one copy
-        // engine direction), overlapped with the decode
-        ck(cudaEventRecord(c->decoded, s), "event");
-        ck(cudaStreamWaitEvent(s2, c->decoded, 0), "event");
-        c->d_knew.upload(k_new, c->units * c->dim, s2);
-        c->d_vnew.upload(v_new, c->units * c->dim, s2);
-        run_decode(c, c->d_q.p, c->d_out.p, false, false, s);
-        if (trace) cudaEventRecord(ev[2], s);
-        ck(cudaEventRecord(c->decoded, s), "event");
-        c->d_out.download(out, c->q_elems(), s);
-        if (trace) cudaEventRecord(ev[3], s);
-        ck(cudaStreamWaitEvent(s2, c->decoded, 0), "event");
-        ck(kvqb::launch_append(c->d_knew.p, c->d_vnew.p, c->batch, c->kv_heads, c->dim, c->tail_cap,
-                               c->k_tail.p, c->v_tail.p, c->tail_len.p, s2), "append");
-        if (trace) cudaEventRecord(ev[4], s2);
-        const auto h1 = std::chrono::steady_clock::now();
+        issue_step(c, queries, k_new, v_new, out, chunks);
         sync(s);
-        sync(s2);
         c->n_tail += 1;
-        if (trace) {
-            float t[4];
-            for (int i = 0; i < 4; ++i) cudaEventElapsedTime(&t[i], ev[0], ev[i + 1]);
-            const double issue = std::chrono::duration<double, std::micro>(h1 - h0).count();
-            const double wall =
-                std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count();
-            std::fprintf(stderr, "[step] q %.1f dec %.1f out %.1f app %.1f us (device); issue %.1f wall %.1f us\n",
-                         1e3 * t[0], 1e3 * t[1], 1e3 * t[2], 1e3 * t[3], issue, wall);
-            for (auto& e : ev) cudaEventDestroy(e);
-        }
+        capture_step(c, key);  // for the next call with the same buffers
     });
 }
 
