@@ -28,6 +28,7 @@
 #include <cstdlib>
 
 #include "kvq_internal.cuh"
+#include "kvq_ptx.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -61,73 +62,18 @@ struct TcParams {
     int S, T;  // cluster size, visual tokens per CTA (multiple of 8 warps x 32)
 };
 
-// ---- PTX helpers ---------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-// Bounded wait: a TMA completion that never arrives traps (an error the host sees)
-// instead of hanging the device.
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    uint32_t done = 0;
-    for (uint32_t spin = 0;; ++spin) {
-        asm volatile(
-            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-            : "=r"(done)
-            : "r"(smem_u32(bar)), "r"(parity)
-            : "memory");
-        if (done) return;
-        if (spin > (1u << 24)) __trap();
-    }
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-// The .aligned forms require a converged warp: every call site is preceded by a
-// __syncwarp() inside these helpers.
-__device__ __forceinline__ void cluster_arrive() {
-    __syncwarp();
-    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void cluster_wait() {
-    __syncwarp();
-    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;"); }
+// ---- PTX helpers (mbarriers, bulk copies, cluster barriers, PDL: kvq_ptx.cuh) ---------
+using namespace ptx;
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
     uint32_t r;
     asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
     return r;
-}
-__device__ __forceinline__ unsigned long long gtimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
 }
 // Debug timeline (KVQ_TRACE_FILE): slot k of this CTA's 256-entry record.
 #define TTRACE(k)                                                                          \
     do {                                                                                   \
         if (a.trace) a.trace[(size_t)blockIdx.x * 256 + (k)] = gtimer();                   \
     } while (0)
-__device__ __forceinline__ float ex2(float x) {
-    float r;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return r;
-}
 // D += A(16x32, u8) * B(32x8, s8)
 __device__ __forceinline__ void imma_u8s8(int (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                                           uint32_t b0, uint32_t b1) {
@@ -227,11 +173,6 @@ __host__ __device__ inline size_t tc_smem_bytes(int S, Smem* out = nullptr, uint
     return off;
 }
 
-__device__ __forceinline__ void st_cluster_f32(float* local_ptr, int rank, float v) {
-    uint32_t addr;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(addr) : "r"(smem_u32(local_ptr)), "r"(rank));
-    asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
-}
 // Tensor-memory traffic here touches no generic memory: no "memory" clobbers, so the
 // compiler may overlap shared-memory work with it; the wait carries the loaded registers
 // as operands so no use of them can be scheduled above it.

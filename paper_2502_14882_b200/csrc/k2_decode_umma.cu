@@ -34,6 +34,7 @@
 #include <cooperative_groups.h>
 
 #include "kvq_internal.cuh"
+#include "kvq_ptx.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -80,34 +81,12 @@ struct UParams {
     int S, T;              // cluster size, tokens per CTA (multiple of 128)
 };
 
-// ---- PTX helpers ---------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-// Bounded wait: a completion that never arrives traps (an error the host sees) instead
-// of hanging the device.
-// try_wait (no time hint): the hardware's short default suspend, then re-check; a
-// lost arrival traps after ~2^28 polls instead of hanging the device.
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    uint32_t done = 0;
-    for (uint32_t spin = 0;; ++spin) {
-        asm volatile(
-            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-            " selp.u32 %0, 1, 0, p;\n}\n"
-            : "=r"(done)
-            : "r"(smem_u32(bar)), "r"(parity)
-            : "memory");
-        if (done) return;
-        if (spin > (1u << 28)) __trap();
-    }
-}
+// ---- PTX helpers (mbarriers, bulk copies, cluster barriers, PDL: kvq_ptx.cuh) ---------
+// Waits here may legitimately be long (the MMA warp waits on whole stages): mbarrier polls
+// trap after 2^28 instead of 2^24.
+using namespace ptx;
+template <typename... A>
+__device__ __forceinline__ void mbar_wait_long(A... a) { ptx::mbar_wait<28>(a...); }
 __device__ __forceinline__ bool elect_one() {
     uint32_t pred = 0;
     asm volatile(
@@ -115,39 +94,7 @@ __device__ __forceinline__ bool elect_one() {
         : "=r"(pred));
     return pred != 0;
 }
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void cluster_arrive() {
-    __syncwarp();
-    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void cluster_wait() {
-    __syncwarp();
-    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;"); }
-__device__ __forceinline__ float ex2(float x) {
-    float r;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return r;
-}
-__device__ __forceinline__ void st_cluster_f32(float* local_ptr, int rank, float v) {
-    uint32_t addr;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(addr) : "r"(smem_u32(local_ptr)), "r"(rank));
-    asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
-}
 
-__device__ __forceinline__ unsigned long long gtimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
 // Debug timeline (KVQ_TRACE_FILE): slot k of this CTA's 256-entry record. Per-block
 // stamps (BTRACE) only exist in a -DKVQ_TRACE_BLOCKS build.
 #define UTRACE(k)                                                                          \
@@ -388,9 +335,6 @@ __host__ __device__ inline size_t umma_smem_bytes(int T, int S, USmem* out = nul
     return off;
 }
 
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 // Named barrier over the 4 consumer warps only (the issuer warp never joins it).
 __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
@@ -460,7 +404,7 @@ __global__ void __launch_bounds__(kThreads + 64) decode_umma_kernel(const UParam
             const uint8_t* vcodes = a.v_codes_t + ((size_t)unit * nvb + tok0 / kBlk) * Gm::kBlockBytes;
             for (int i = 0; i < total_stages; ++i) {
                 const int slot = i % Gm::kStages;
-                if (i >= Gm::kStages) mbar_wait(&sm.empty[slot], ((i / Gm::kStages) - 1) & 1);
+                if (i >= Gm::kStages) mbar_wait_long(&sm.empty[slot], ((i / Gm::kStages) - 1) & 1);
                 if (lane == 0 && i < 64) BTRACE(192 + i);
                 uint32_t bytes;
                 const uint8_t* src;
@@ -492,9 +436,9 @@ __global__ void __launch_bounds__(kThreads + 64) decode_umma_kernel(const UParam
             const uint32_t qb_addr = smem_u32(sm.qb);
             for (int blk = 0; blk < nblk; ++blk) {
                 const int x = blk % Gm::kNA, y = blk % Gm::kND;
-                mbar_wait(&sm.afull[x], (blk / Gm::kNA) & 1);
+                mbar_wait_long(&sm.afull[x], (blk / Gm::kNA) & 1);
                 if (lane == 0 && blk < 16) BTRACE(128 + 4 * blk);
-                if (blk >= Gm::kND) mbar_wait(&sm.dempty[y], (blk / Gm::kND - 1) & 1);
+                if (blk >= Gm::kND) mbar_wait_long(&sm.dempty[y], (blk / Gm::kND - 1) & 1);
                 if (lane == 0 && blk < 16) BTRACE(128 + 4 * blk + 1);
                 tc_fence_after();
                 const uint32_t d = tbase + Gm::kColDA + Gm::kN * y;
@@ -519,7 +463,7 @@ __global__ void __launch_bounds__(kThreads + 64) decode_umma_kernel(const UParam
             const uint32_t ptile_addr = smem_u32(sm.ptile);
             for (int blk = 0; blk < nblk; ++blk) {
                 const int x = blk % Gm::kNA;
-                mbar_wait(&sm.afull[4 + x], (blk / Gm::kNA) & 1);
+                mbar_wait_long(&sm.afull[4 + x], (blk / Gm::kNA) & 1);
                 tc_fence_after();
                 const uint32_t pt = ptile_addr + x * NT * 2048;
                 if (elect_one()) {
@@ -566,7 +510,7 @@ __global__ void __launch_bounds__(kThreads + 64) decode_umma_kernel(const UParam
         // ---------------- phase A: scores ----------------
         auto epilogue_a = [&](int blk) {
             const int y = blk % Gm::kND;
-            mbar_wait(&sm.dfull[y], (blk / Gm::kND) & 1);
+            mbar_wait_long(&sm.dfull[y], (blk / Gm::kND) & 1);
             if (tid == 0 && blk < 16) BTRACE(64 + 4 * blk + 2);
             tc_fence_after();
             uint32_t r[16 * NT];
@@ -604,7 +548,7 @@ __global__ void __launch_bounds__(kThreads + 64) decode_umma_kernel(const UParam
         if (tid == 0) UTRACE(1);
         for (int blk = 0; blk < nblk; ++blk) {
             const int slot = blk % Gm::kStages;
-            mbar_wait(&sm.full[slot], (blk / Gm::kStages) & 1);
+            mbar_wait_long(&sm.full[slot], (blk / Gm::kStages) & 1);
             if (tid == 0 && blk < 16) BTRACE(64 + 4 * blk);
             const uint8_t* row = sm.ring + slot * Gm::kBlockBytes + tid * Gm::kRowBytes;
             uint32_t w[4 * BITS];
@@ -748,7 +692,7 @@ __global__ void __launch_bounds__(kThreads + 64) decode_umma_kernel(const UParam
             const int slot = i % Gm::kStages;
             const int x = blk % Gm::kNA;
             if (blk >= Gm::kNA) {  // A buffer / p tile of block blk - NA are free once its MMAs retired
-                mbar_wait(&sm.dfull[4 + x], (blk / Gm::kNA - 1) & 1);
+                mbar_wait_long(&sm.dfull[4 + x], (blk / Gm::kNA - 1) & 1);
                 tc_fence_after();
             }
             // p side first (independent of the TMA): thread m = token m of the block.
@@ -772,7 +716,7 @@ __global__ void __launch_bounds__(kThreads + 64) decode_umma_kernel(const UParam
                         make_uint4(P[4 * hg], P[4 * hg + 1], P[4 * hg + 2], P[4 * hg + 3]);
             }
             // V side: thread c = channel c, 4b words = 128 tokens of codes.
-            mbar_wait(&sm.full[slot], (i / Gm::kStages) & 1);
+            mbar_wait_long(&sm.full[slot], (i / Gm::kStages) & 1);
             {
                 const uint8_t* src = sm.ring + slot * Gm::kBlockBytes + tid * Gm::kRowBytes;
                 uint32_t w[4 * BITS];
@@ -805,7 +749,7 @@ __global__ void __launch_bounds__(kThreads + 64) decode_umma_kernel(const UParam
         if (lane == 0)
             for (int h = 0; h < H; ++h) sm.red[(warp * 3 + 2) * 8 + h] = wsum[h];
         if (nblk > 0) {
-            mbar_wait(&sm.dfull[4 + (nblk - 1) % Gm::kNA], ((nblk - 1) / Gm::kNA) & 1);
+            mbar_wait_long(&sm.dfull[4 + (nblk - 1) % Gm::kNA], ((nblk - 1) / Gm::kNA) & 1);
             tc_fence_after();
         }
         consumer_sync();

@@ -20,8 +20,13 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
 }
-// Bounded wait: a bulk copy that never completes traps (an error the host sees) instead
-// of hanging the device.
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// Bounded wait: an arrival that never comes traps after 2^kSpinLog2 polls (an error the
+// host sees) instead of hanging the device. try_wait without a time hint suspends for the
+// hardware's short default between polls.
+template <int kSpinLog2 = 24>
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     uint32_t done = 0;
     for (uint32_t spin = 0;; ++spin) {
@@ -31,7 +36,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
             : "r"(smem_u32(bar)), "r"(parity)
             : "memory");
         if (done) return;
-        if (spin > (1u << 24)) __trap();
+        if (spin > (1u << kSpinLog2)) __trap();
     }
 }
 // global -> shared bulk copy (16-byte aligned, multiple of 16 bytes), completion counted
@@ -49,6 +54,21 @@ __device__ __forceinline__ float ld_cluster_f32(const float* local_ptr, int rank
     asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
     return v;
 }
+__device__ __forceinline__ void st_cluster_f32(float* local_ptr, int rank, float v) {
+    uint32_t addr;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(addr) : "r"(smem_u32(local_ptr)), "r"(rank));
+    asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+// Cluster barrier halves (release / acquire). The .aligned forms need a converged warp:
+// each helper reconverges first.
+__device__ __forceinline__ void cluster_arrive() {
+    __syncwarp();
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+    __syncwarp();
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 // Full cluster barrier (release / acquire). The .aligned form needs a converged warp.
 __device__ __forceinline__ void cluster_sync() {
     __syncwarp();
@@ -62,6 +82,11 @@ __device__ __forceinline__ uint32_t cluster_rank() {
 }
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;"); }
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 __device__ __forceinline__ float ex2(float x) {
     float r;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
