@@ -638,3 +638,66 @@ def test_full_precision_cache_tail_pass(kvq, oracle, n_tail):
                                         np.zeros(d, np.float32), np.zeros(0, np.uint8), np.zeros(d, np.float32),
                                         np.zeros(d, np.float32), k[hh], v[hh], 0.0, 0.0)
         assert rel_l2(out[hh], want) <= 1e-5
+
+
+# ---- randomized sweep over shapes, widths, tails and paths --------------------------------
+
+def _sweep_cases(seed=2024, count=24):
+    rng = np.random.default_rng(seed)
+    cases = []
+    for i in range(count):
+        bits = int(rng.choice([1, 2, 4, 8]))
+        cases.append(dict(
+            B=int(rng.integers(1, 4)), H=int(rng.integers(1, 4)), G=int(rng.integers(1, 9)),
+            n=int(rng.choice([1, 31, 33, 255, 257, 1000, 2049])), bits=bits,
+            wb=int(rng.choice([w for w in (8, 16, 32) if w % bits == 0])),
+            tail=int(rng.choice([0, 1, 7, 64, 65, 130])),
+            tau=(float(rng.choice([0.0, 1.0, 3.0])), float(rng.choice([0.0, 1.0, 2.0]))),
+            seed=int(rng.integers(1 << 30))))
+    return cases
+
+
+@pytest.mark.parametrize("case", _sweep_cases(), ids=lambda c: "b{bits}m{wb}_B{B}H{H}G{G}_n{n}_t{tail}".format(**c))
+def test_randomized_paths_vs_oracle(kvq, oracle, case):
+    """Random (batch, KV heads, group, n, b, M, tail length, tau) through every path that
+    accepts the shape (AUTO picks the tensor-core decode + tail pass where it can), against
+    the C restatement. Ragged n (not a multiple of 32), tails around the in-kernel limit
+    (64) and every pack width are covered."""
+    c = case
+    rng = np.random.default_rng(c["seed"])
+    B, H, G, n, d = c["B"], c["H"], c["G"], c["n"], 128
+    k = rng.normal(size=(B, H, n, d)).astype(np.float32)
+    v = rng.normal(size=(B, H, n, d)).astype(np.float32)
+    cache = kvq.BatchedCache.build(k, v, kvq.QuantizationConfig(c["bits"], kvq.QuantMode.channel_wise, c["wb"]),
+                                   kvq.CalibrationParams(*c["tau"]), group=G)
+    tk, tv = [], []
+    for _ in range(c["tail"]):
+        kn = rng.normal(size=(B, H, d)).astype(np.float32)
+        vn = rng.normal(size=(B, H, d)).astype(np.float32)
+        cache.append(kn, vn)
+        tk.append(kn)
+        tv.append(vn)
+    q = rng.normal(size=(B, H, G, d)).astype(np.float32)
+    want = np.zeros_like(q)
+    for b in range(B):
+        for h in range(H):
+            ka, kb = oracle.compute_stats(k[b, h])
+            va, vb = oracle.compute_stats(v[b, h])
+            kc = oracle.quantize(k[b, h], ka, kb, c["bits"], c["wb"])
+            vc = oracle.quantize(v[b, h], va, vb, c["bits"], c["wb"])
+            ktail = np.stack([x[b, h] for x in tk]) if tk else np.zeros((0, d), np.float32)
+            vtail = np.stack([x[b, h] for x in tv]) if tv else np.zeros((0, d), np.float32)
+            for g in range(G):
+                want[b, h, g] = oracle.decode_head(q[b, h, g], n, c["bits"], c["wb"], kc, ka, kb, vc, va, vb, ktail,
+                                                   vtail, *c["tau"])[0]
+    for path in (kvq.PATH_AUTO, kvq.PATH_TC, kvq.PATH_UMMA, kvq.PATH_GENERIC):
+        cache.set_path(path)
+        try:
+            out, _, _ = cache.decode(q)
+        except kvq.ConfigError:
+            assert path in (kvq.PATH_TC, kvq.PATH_UMMA), "AUTO and GENERIC accept every shape"
+            continue
+        # fp32 reduction-order noise grows with n + tail: 1e-4 for the generic path at these
+        # sizes (2e-5 on the small golden trajectories), 5e-4 for the tensor-core paths
+        tol = 1e-4 if path == kvq.PATH_GENERIC else 5e-4
+        assert rel_l2(out, want) <= tol, (path, rel_l2(out, want))
