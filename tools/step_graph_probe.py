@@ -58,5 +58,18 @@ def run(kind, steps=24):
     return e0.elapsed_time(e1) / steps * 1e3
 
 
+def run_dec(steps=24):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(st):
+        torch.cuda._sleep(int(2e7))
+        e0.record(st)
+        for i in range(steps):
+            split[i % R][0].replay()
+        e1.record(st)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps * 1e3
+
+
 for rep in range(2):
-    print("split %.1f us/step, fused %.1f us/step" % (run("split"), run("fused")))
+    print("split %.1f us/step, fused %.1f us/step, decode only %.1f us" % (run("split"), run("fused"), run_dec()))
