@@ -12,6 +12,7 @@ tensors (torch is only plumbing for device memory and streams).
 from __future__ import annotations
 
 import ctypes as C
+import struct
 from dataclasses import dataclass, field
 from enum import IntEnum
 from pathlib import Path
@@ -243,6 +244,100 @@ class QuantizedSegment:
 
     def row_bytes(self) -> int:
         return self.words_per_row() * self.codes.word_bits // 8
+
+
+# ---- file records: KVQP segments (quantize.hpp:148-230), KVQT tensors (tensor_io.hpp) -------
+# Host formatting; byte-identical to the reference's writers. Readers raise FormatError with
+# the reference's messages and byte offsets (relative to the start of the record + `off`).
+
+def _read(buf: bytes, off: int, n: int, what: str) -> bytes:
+    if len(buf) - off < n:
+        raise FormatError(f"truncated while reading {what}", off)
+    return buf[off:off + n]
+
+
+def _magic(buf: bytes, off: int, magic: bytes, name: str) -> int:
+    if len(buf) - off < 4:
+        raise FormatError(f"truncated before {name} magic", off)
+    if buf[off:off + 4] != magic:
+        raise FormatError(f"bad {name} magic", off)
+    return off + 4
+
+
+def write_segment(seg: QuantizedSegment) -> bytes:
+    """write_segment (quantize.hpp:155-168): the KVQP record of `seg`."""
+    c = seg.codes
+    return (b"KVQP" + struct.pack("<IBBHQ", 1, c.code_bits, c.word_bits, 0, c.logical_count)
+            + np.ascontiguousarray(c.bytes, np.uint8).tobytes() + struct.pack("<Q", seg.dim)
+            + _f32(seg.stats.alpha).astype("<f4").tobytes() + _f32(seg.stats.beta).astype("<f4").tobytes())
+
+
+def read_segment(buf: bytes, off: int = 0) -> tuple[QuantizedSegment, int]:
+    """read_segment (quantize.hpp:177-222) -> (segment, offset after it)."""
+    off = _magic(buf, off, b"KVQP", "packed segment")
+    (version,) = struct.unpack("<I", _read(buf, off, 4, "version"))
+    off += 4
+    if version != 1:
+        raise FormatError(f"unsupported segment version {version}", off - 4)
+    if len(buf) - off < 4:
+        raise FormatError("truncated while reading width header", off)
+    n, m = buf[off], buf[off + 1]
+    off += 4
+    if n < 1 or m < 8 or m > 32 or m % 8:
+        raise FormatError("stored widths invalid: word bits must be 8, 16, or 32 and code bits >= 1", off - 4)
+    if m % n:
+        raise FormatError(f"stored widths invalid: code bits {n} must divide word bits {m}", off - 4)
+    (logical,) = struct.unpack("<Q", _read(buf, off, 8, "logical_count"))
+    off += 8
+    g = m // n
+    nbytes = (logical + g - 1) // g * (m // 8)
+    if len(buf) - off < nbytes:
+        raise FormatError("truncated packed words", off)
+    codes = np.frombuffer(buf, np.uint8, nbytes, off).copy()
+    off += nbytes
+    (dim,) = struct.unpack("<Q", _read(buf, off, 8, "dim"))
+    off += 8
+    stats = []
+    for what in ("alpha", "beta"):
+        have = min(dim, (len(buf) - off) // 4)
+        if have < dim:
+            raise FormatError(f"truncated while reading {what}", off + 4 * have)
+        stats.append(np.frombuffer(buf, "<f4", dim, off).astype(np.float32))
+        off += 4 * dim
+    stride = (dim + g - 1) // g * g
+    if (logical != 0) if stride == 0 else (logical % stride != 0):
+        raise FormatError("logical_count does not cover whole rows", off)
+    seg = QuantizedSegment(PackedBuffer(codes, n, m, logical), ChannelStats(stats[0], stats[1]),
+                           0 if stride == 0 else logical // stride, dim, n)
+    return seg, off
+
+
+def write_tensor(m) -> bytes:
+    """write_tensor (tensor_io.hpp:66-72): the KVQT record of a [rows][cols] fp32 matrix."""
+    a = _f32(m)
+    a = a.reshape(a.shape[0], -1) if a.ndim != 2 else a
+    return b"KVQT" + struct.pack("<IQQ", 1, a.shape[0], a.shape[1]) + a.astype("<f4").tobytes()
+
+
+def read_tensor(buf: bytes, off: int = 0) -> tuple[np.ndarray, int]:
+    """read_tensor (tensor_io.hpp:84-107) -> (matrix, offset after it)."""
+    off = _magic(buf, off, b"KVQT", "tensor")
+    (version,) = struct.unpack("<I", _read(buf, off, 4, "version"))
+    off += 4
+    if version != 1:
+        raise FormatError(f"unsupported tensor version {version}", off - 4)
+    (rows,) = struct.unpack("<Q", _read(buf, off, 8, "rows"))
+    off += 8
+    (cols,) = struct.unpack("<Q", _read(buf, off, 8, "cols"))
+    off += 8
+    count = rows * cols
+    if len(buf) - off < 4 * count:
+        raise FormatError("truncated while reading tensor data", off + (len(buf) - off) // 4 * 4)
+    a = np.frombuffer(buf, "<f4", count, off).astype(np.float32).reshape(rows, cols)
+    off += 4 * count
+    if not np.all(np.isfinite(a)):
+        raise FormatError("tensor contains non-finite values", off)
+    return a, off
 
 
 def compute_stats(m, mode: QuantMode = QuantMode.channel_wise) -> ChannelStats:

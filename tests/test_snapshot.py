@@ -107,3 +107,31 @@ def test_device_image_and_batched_load(kvq):
     assert (g.batch, g.kv_heads, g.group) == (1, 3, 2)
     with pytest.raises(kvq.DomainError):
         kvq.BatchedCache.load_image(img, batch=2)
+
+
+def test_segment_and_tensor_records_roundtrip_reference_bytes(kvq_host):
+    """The KVQP / KVQT records inside a reference KVQC image read back and re-serialize to
+    the same bytes (quantize.hpp:148-230, tensor_io.hpp:66-107); short reads raise the
+    reference's messages."""
+    k = kvq_host
+    for name in CASES:
+        img = np.load(GOLD / "cache_io.npz")[f"{name}_image"].tobytes()
+        off = 52
+        heads = int.from_bytes(img[8:16], "little")
+        for _ in range(heads):
+            for _ in range(2):
+                seg, end = k.read_segment(img, off)
+                assert k.write_segment(seg) == img[off:end]
+                off = end
+            for _ in range(2):
+                t, end = k.read_tensor(img, off)
+                assert k.write_tensor(t) == img[off:end]
+                off = end
+        assert off == len(img)
+    img = np.load(GOLD / "cache_io.npz")["q4_image"].tobytes()
+    with pytest.raises(k.FormatError) as e:
+        k.read_segment(img[:52 + 20 + 96 + 8 + 10], 52)
+    assert e.value.message == "truncated while reading alpha" and e.value.offset == 184
+    with pytest.raises(k.FormatError) as e:
+        k.read_segment(img[:100], 52)
+    assert e.value.message == "truncated packed words" and e.value.offset == 72
