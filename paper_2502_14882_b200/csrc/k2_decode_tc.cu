@@ -59,7 +59,8 @@ struct Geo {
 
 struct TcParams {
     DecodeArgs a;
-    int S, T;  // cluster size, visual tokens per CTA (multiple of 8 warps x 32)
+    int S, T;    // cluster size, visual tokens per CTA (multiple of 8 warps x 32)
+    int groups;  // head groups per unit handled by separate CTAs (1, or 2 for G > 4 at NT = 1)
 };
 
 // ---- PTX helpers (mbarriers, bulk copies, cluster barriers, PDL: kvq_ptx.cuh) ---------
@@ -216,10 +217,17 @@ __global__ void __launch_bounds__(kWarps * 32, OCC) decode_tc_kernel(const TcPar
     constexpr int kStagesW = ring_stages<BITS, OCC>();
     constexpr uint32_t kTmemCols = NT == 1 ? 128 : 256;  // 2 lane-sharing warps x 16 steps x 4 NT
     const DecodeArgs& a = p.a;
-    const int G = (int)a.group;
     const int S = p.S;
     const int rank = S > 1 ? (int)cg::this_cluster().block_rank() : 0;
-    const int unit = blockIdx.x / S;
+    // Grid: (head group, unit, rank). With two head groups a CTA serves query heads
+    // [4 grp, 4 grp + G) of its unit (softmax rows are per head, so the split is exact).
+    const int unit_g = blockIdx.x / S;
+    const int grp = unit_g / (int)a.units;
+    const int unit = unit_g % (int)a.units;
+    const int G_all = (int)a.group;
+    const int h0 = 4 * grp;
+    const int G = p.groups > 1 ? min(4, G_all - h0) : G_all;
+    auto qrow = [&](int h) { return (size_t)unit * G_all + h0 + h; };  // row of head h in q / out
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, t = lane & 3;
 
@@ -311,7 +319,7 @@ __global__ void __launch_bounds__(kWarps * 32, OCC) decode_tc_kernel(const TcPar
         const float ka = k_a, kbeta = k_b;
         float qv[8];
 #pragma unroll
-        for (int h = 0; h < 8; ++h) qv[h] = h < G ? a.q[(unit * G + h) * kDim + c] : 0.0f;
+        for (int h = 0; h < 8; ++h) qv[h] = h < G ? a.q[qrow(h) * kDim + c] : 0.0f;
         const float range = __fsub_rn(kbeta, ka);
         const float stp = range > 0.0f ? __fdiv_rn(range, levels) : 0.0f;
         float ab[8], sa[8];
@@ -523,7 +531,7 @@ __global__ void __launch_bounds__(kWarps * 32, OCC) decode_tc_kernel(const TcPar
         float4 qv[8];
 #pragma unroll
         for (int h = 0; h < 8; ++h)
-            qv[h] = h < G ? *reinterpret_cast<const float4*>(a.q + ((size_t)unit * G + h) * kDim + 4 * lane)
+            qv[h] = h < G ? *reinterpret_cast<const float4*>(a.q + qrow(h) * kDim + 4 * lane)
                           : make_float4(0.f, 0.f, 0.f, 0.f);
         for (int j = warp; j < ntl; j += kWarps) {
             const float4 kv = *reinterpret_cast<const float4*>(a.k_tail + ((size_t)unit * a.tail_cap + j) * kDim + 4 * lane);
@@ -785,8 +793,8 @@ __global__ void __launch_bounds__(kWarps * 32, OCC) decode_tc_kernel(const TcPar
             num = __fmaf_rn(pt, __ldg(vt + (size_t)j * kDim), num);
         }
         if (S == 1) {
-            a.out[((size_t)unit * G + h) * kDim + ch] = num / den;
-            if (a.tail_lse && ch == 0) a.tail_lse[(size_t)unit * G + h] = log2f(den) - kLog2PScale - sm.gpar[h * 4 + 2];
+            a.out[qrow(h) * kDim + ch] = num / den;
+            if (a.tail_lse && ch == 0) a.tail_lse[qrow(h)] = log2f(den) - kLog2PScale - sm.gpar[h * 4 + 2];
         } else {
             st_cluster_f32(recv + rank * (8 * kDim + 8) + idx, 0, num);
             if (ch == 0) st_cluster_f32(recv + rank * (8 * kDim + 8) + 8 * kDim + h, 0, den);
@@ -804,9 +812,9 @@ __global__ void __launch_bounds__(kWarps * 32, OCC) decode_tc_kernel(const TcPar
                     num += recv[r * (8 * kDim + 8) + idx];
                     den += recv[r * (8 * kDim + 8) + 8 * kDim + h];
                 }
-                a.out[((size_t)unit * G + (idx / kDim)) * kDim + (idx % kDim)] = num / den;
+                a.out[qrow(idx / kDim) * kDim + (idx % kDim)] = num / den;
                 if (a.tail_lse && idx % kDim == 0)
-                    a.tail_lse[(size_t)unit * G + h] = log2f(den) - kLog2PScale - sm.gpar[h * 4 + 2];
+                    a.tail_lse[qrow(h)] = log2f(den) - kLog2PScale - sm.gpar[h * 4 + 2];
             }
         }
     }
@@ -834,11 +842,11 @@ void plan(const DecodeArgs& a, int& S, int& T) {
 }
 
 template <int BITS, int NT, int OCC>
-cudaError_t launch_occ(const DecodeArgs& a, cudaStream_t s) {
+cudaError_t launch_occ(const DecodeArgs& a, cudaStream_t s, int groups = 1) {
     int S, T;
     plan(a, S, T);
     cudaError_t e = cudaSuccess;
-    TcParams p{a, S, T};
+    TcParams p{a, S, T, groups};
     // TMEM: kTmemCols per CTA; never let more CTAs share an SM than TMEM can serve (a
     // blocked tcgen05.alloc inside a cluster could deadlock against its partners).
     const size_t max_ctas = OCC == 1 ? 1 : (NT == 1 ? 4 : 2);
@@ -855,7 +863,7 @@ cudaError_t launch_occ(const DecodeArgs& a, cudaStream_t s) {
         attr_done = true;
     }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(a.units * S));
+    cfg.gridDim = dim3((unsigned)(a.units * S * groups));
     cfg.blockDim = dim3(kWarps * 32);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
@@ -967,8 +975,21 @@ cudaError_t launch_bits(const DecodeArgs& a, cudaStream_t s) {
     if constexpr (NT == 2) {
         return launch_occ<BITS, NT, 1>(a, s);
     } else {
-        return tc_occ() == 3 ? launch_occ<BITS, NT, 3>(a, s) : launch_occ<BITS, NT, 2>(a, s);
+        // G > 4 at NT = 1: two head groups as separate CTAs (two CTAs per SM each)
+        const int groups = a.group > 4 ? 2 : 1;
+        return tc_occ() == 3 ? launch_occ<BITS, NT, 3>(a, s, groups) : launch_occ<BITS, NT, 2>(a, s, groups);
     }
+}
+
+// G > 4: two CTAs of one head group each (NT = 1, two CTAs per SM, codes streamed twice)
+// beat one CTA holding both groups (NT = 2, ~226 registers, one CTA per SM, codes streamed
+// once): C4 (G = 6) 246 -> 202 us per step, G = 8 at C2 shape 90 -> 77 us
+// (profiles/r01_tc_headsplit.txt). KVQ_TC_HEADSPLIT=0 selects NT = 2 (tuning).
+int tc_nt(const DecodeArgs& a) {
+    if (a.group <= 4) return 1;
+    static const char* env = std::getenv("KVQ_TC_HEADSPLIT");
+    const bool split = env ? std::atoi(env) != 0 : true;
+    return split ? 1 : 2;
 }
 
 template <int BITS, int NT>
@@ -992,7 +1013,7 @@ bool decode_tc_supported(const DecodeArgs& a) {
     // the fp32 tail lives in rank 0 (at most kTailMax rows) unless the tail pass owns it
     if (a.tail_cap > (size_t)kTailMax && a.tail_lse == nullptr) return false;
     (void)T;
-    const int NT = a.group > 4 ? 2 : 1;
+    const int NT = tc_nt(a);
     size_t smem = 0;
     switch (a.bits * 10 + NT) {
         case 11: smem = tc_smem_for<1, 1>(S); break;
@@ -1008,7 +1029,7 @@ bool decode_tc_supported(const DecodeArgs& a) {
 }
 
 cudaError_t launch_decode_tc(const DecodeArgs& a, cudaStream_t s) {
-    const int NT = a.group > 4 ? 2 : 1;
+    const int NT = tc_nt(a);
     switch (a.bits * 10 + NT) {
         case 11: return launch_bits<1, 1>(a, s);
         case 12: return launch_bits<1, 2>(a, s);
