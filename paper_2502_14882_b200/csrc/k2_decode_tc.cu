@@ -110,9 +110,14 @@ __device__ __forceinline__ int v_channel(int g, int iota, int& shift) {
 
 // ---- decode ------------------------------------------------------------------------------
 constexpr int kWarps = 8;             // consumer warps per CTA
-constexpr int kWarpTokens = 512;      // visual tokens per warp (contiguous)
-constexpr int kCtaTokens = kWarps * kWarpTokens;
-constexpr int kSteps = kWarpTokens / 32;  // 32-token steps per warp
+// Visual tokens per warp (contiguous), at most: the warp's scores wait in TMEM (4 columns
+// per 32-token step and head group), 256 columns per CTA, two CTAs per SM = all 512.
+template <int NT>
+constexpr int warp_tokens() { return NT == 1 ? 1024 : 512; }
+#ifndef KVQ_TC_WARP_TOKENS_CAP  // (tuning builds: cap the per-warp token count)
+#define KVQ_TC_WARP_TOKENS_CAP 1024
+#endif
+inline int cta_tokens(int NT) { return kWarps * std::min(NT == 1 ? 1024 : 512, KVQ_TC_WARP_TOKENS_CAP); }
 
 // Per-warp TMA ring: ~10 KB in flight per warp (80 KB per CTA, two CTAs per SM) covers
 // the ~2 us bulk-copy latency measured under load (profiles/r01_trace_umma_c2.txt).
@@ -215,7 +220,8 @@ template <int BITS, int NT, int OCC>
 __global__ void __launch_bounds__(kWarps * 32, OCC) decode_tc_kernel(const TcParams p) {
     using Gm = Geo<BITS>;
     constexpr int kStagesW = ring_stages<BITS, OCC>();
-    constexpr uint32_t kTmemCols = NT == 1 ? 128 : 256;  // 2 lane-sharing warps x 16 steps x 4 NT
+    constexpr int kSteps = warp_tokens<NT>() / 32;                 // 32-token steps per warp, at most
+    constexpr uint32_t kTmemCols = 2 * kSteps * 4 * NT;              // 2 lane-sharing warps; 256
     const DecodeArgs& a = p.a;
     const int S = p.S;
     const int rank = S > 1 ? (int)cg::this_cluster().block_rank() : 0;
@@ -825,14 +831,19 @@ __global__ void __launch_bounds__(kWarps * 32, OCC) decode_tc_kernel(const TcPar
     }
 }
 
-// Token split: at most 4096 tokens per CTA; small batches split units further (down to
-// 256 tokens per CTA) so that units x S fills ~2 CTAs per SM - a single unit otherwise
-// runs on one SM for its full latency.
-void plan(const DecodeArgs& a, int& S, int& T) {
+// Token split: at most 8192 (NT = 1) / 4096 tokens per CTA; small batches split units further (down to
+// 256 tokens per CTA) so that units x S covers the SMs - a single unit otherwise runs on
+// one SM for its full latency.
+void plan(const DecodeArgs& a, int NT, int& S, int& T) {
     const int n = (int)a.n_vis;
-    int s_min = std::max(1, (n + kCtaTokens - 1) / kCtaTokens);
-    const size_t pu = a.plan_units ? a.plan_units : a.units;  // a chunk plans as its whole batch
-    const int want = (int)((2 * 148 + pu - 1) / pu);
+    const int ct = cta_tokens(NT);
+    int s_min = std::max(1, (n + ct - 1) / ct);
+    size_t pu = a.plan_units ? a.plan_units : a.units;  // a chunk plans as its whole batch
+    if (NT == 1 && a.group > 4) pu *= 2;                 // two head-group CTAs per unit
+    // split a unit only while the units leave SMs without a CTA: about one CTA per SM is the
+    // sweet spot (profiles/r01_tc_split2.txt: >= 128 units S = 1, 64 units S = 2; splitting
+    // further pays per-CTA prologues and cluster merges for no occupancy gain)
+    const int want = (int)((128 + pu - 1) / pu);
     int s = std::max(s_min, std::min(want, kMaxCluster));
     static const int force = std::getenv("KVQ_TC_SPLIT") ? std::atoi(std::getenv("KVQ_TC_SPLIT")) : 0;  // tuning
     if (force > 0) s = std::max(s_min, std::min(force, kMaxCluster));
@@ -844,7 +855,7 @@ void plan(const DecodeArgs& a, int& S, int& T) {
 template <int BITS, int NT, int OCC>
 cudaError_t launch_occ(const DecodeArgs& a, cudaStream_t s, int groups = 1) {
     int S, T;
-    plan(a, S, T);
+    plan(a, NT, S, T);
     cudaError_t e = cudaSuccess;
     TcParams p{a, S, T, groups};
     // TMEM: kTmemCols per CTA; never let more CTAs share an SM than TMEM can serve (a
@@ -1008,12 +1019,12 @@ bool decode_tc_supported(const DecodeArgs& a) {
     if (a.group < 1 || a.group > 8) return false;
     if (a.units == 0) return false;
     int S, T;
-    plan(a, S, T);
+    const int NT = tc_nt(a);
+    plan(a, NT, S, T);
     if (S > kMaxCluster) return false;
     // the fp32 tail lives in rank 0 (at most kTailMax rows) unless the tail pass owns it
     if (a.tail_cap > (size_t)kTailMax && a.tail_lse == nullptr) return false;
     (void)T;
-    const int NT = tc_nt(a);
     size_t smem = 0;
     switch (a.bits * 10 + NT) {
         case 11: smem = tc_smem_for<1, 1>(S); break;
