@@ -117,7 +117,7 @@ constexpr int warp_tokens() { return NT == 1 ? 1024 : 512; }
 #ifndef KVQ_TC_WARP_TOKENS_CAP  // (tuning builds: cap the per-warp token count)
 #define KVQ_TC_WARP_TOKENS_CAP 1024
 #endif
-inline int cta_tokens(int NT) { return kWarps * std::min(NT == 1 ? 1024 : 512, KVQ_TC_WARP_TOKENS_CAP); }
+inline int cta_tokens(int NT, int W = kWarps) { return W * std::min(NT == 1 ? 1024 : 512, KVQ_TC_WARP_TOKENS_CAP); }
 
 // Per-warp TMA ring: ~10 KB in flight per warp (80 KB per CTA, two CTAs per SM) covers
 // the ~2 us bulk-copy latency measured under load (profiles/r01_trace_umma_c2.txt).
@@ -142,7 +142,7 @@ struct Smem {  // carve-up of the dynamic shared memory of one decode CTA
     uint32_t* tmem_slot;
 };
 
-template <int BITS, int NT, int OCC>
+template <int BITS, int NT, int OCC, int W = kWarps>
 __host__ __device__ inline size_t tc_smem_bytes(int S, Smem* out = nullptr, uint8_t* base = nullptr) {
     size_t off = 0;
     auto take = [&](size_t bytes) {
@@ -152,17 +152,17 @@ __host__ __device__ inline size_t tc_smem_bytes(int S, Smem* out = nullptr, uint
     };
     constexpr int stage = Geo<BITS>::kStageBytesB;
     const size_t recv_bytes = S > 1 ? (size_t)S * (8 * kDim + 8) * 4 : 0;
-    const size_t ring_bytes = (size_t)kWarps * ring_stages<BITS, OCC>() * stage;
+    const size_t ring_bytes = (size_t)W * ring_stages<BITS, OCC>() * stage;
     const size_t tail_use = recv_bytes;
     uint8_t* ring = take(ring_bytes > tail_use ? ring_bytes : tail_use);
     uint8_t* acc = take((size_t)NT * 16 * 32 * 4 * 4);
-    uint8_t* pw = take((size_t)kWarps * 2 * NT * 12 * kPRow * 4);
+    uint8_t* pw = take((size_t)W * 2 * NT * 12 * kPRow * 4);
     uint8_t* tail_s = take((size_t)8 * kTailMax * 4);
-    uint8_t* wpart = take((size_t)kWarps * 24 * 4);
+    uint8_t* wpart = take((size_t)W * 24 * 4);
     uint8_t* allpart = take((size_t)(S > 0 ? S : 1) * 24 * 4);
     uint8_t* gpar = take(32 * 4);
-    uint8_t* wsum = take((size_t)kWarps * 8 * 4);
-    uint8_t* full = take((size_t)kWarps * ring_stages<BITS, OCC>() * 8);
+    uint8_t* wsum = take((size_t)W * 8 * 4);
+    uint8_t* full = take((size_t)W * ring_stages<BITS, OCC>() * 8);
     uint8_t* slot = take(16);
     if (out) {
         out->ring = ring;
@@ -216,12 +216,12 @@ __device__ __forceinline__ void red_add_u32(uint32_t* p, uint32_t v) {
 // tensor memory (lane-private columns, tcgen05.st/ld) between the phases.
 // Cross-warp reductions of the p.V accumulators are exact integer shared-memory atomics
 // (deterministic); cross-CTA traffic is push-only.
-template <int BITS, int NT, int OCC>
-__global__ void __launch_bounds__(kWarps * 32, OCC) decode_tc_kernel(const TcParams p) {
+template <int BITS, int NT, int OCC, int W = kWarps>
+__global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p) {
     using Gm = Geo<BITS>;
     constexpr int kStagesW = ring_stages<BITS, OCC>();
     constexpr int kSteps = warp_tokens<NT>() / 32;                 // 32-token steps per warp, at most
-    constexpr uint32_t kTmemCols = 2 * kSteps * 4 * NT;              // 2 lane-sharing warps; 256
+    constexpr uint32_t kTmemCols = (W / 4) * kSteps * 4 * NT;        // lane-sharing warps; 256 / 128
     const DecodeArgs& a = p.a;
     const int S = p.S;
     const int rank = S > 1 ? (int)cg::this_cluster().block_rank() : 0;
@@ -239,13 +239,13 @@ __global__ void __launch_bounds__(kWarps * 32, OCC) decode_tc_kernel(const TcPar
 
     extern __shared__ __align__(128) uint8_t smem_raw[];
     Smem sm;
-    tc_smem_bytes<BITS, NT, OCC>(S, &sm, smem_raw);
+    tc_smem_bytes<BITS, NT, OCC, W>(S, &sm, smem_raw);
     if (threadIdx.x == 0) TTRACE(0);
     uint8_t* ring = sm.ring + warp * kStagesW * Gm::kStageBytesB;
     uint64_t* full = sm.full + warp * kStagesW;
 
     const int n = (int)a.n_vis;
-    const int wt = p.T / kWarps;                        // tokens per warp (multiple of 32, <= 512)
+    const int wt = p.T / W;                        // tokens per warp (multiple of 32, <= 512)
     const int tok0 = rank * p.T + warp * wt;              // this warp's first token
     const int nv = max(0, min(wt, n - tok0));
     // fp32 tail: rank 0, unless a separate tail pass owns it (a.tail_lse). tail_len is written
@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(kWarps * 32, OCC) decode_tc_kernel(const TcPar
         for (int i = 0; i < min(kStagesW, total_stages); ++i) issue(i);
     }
     // zero the CTA accumulator image; allocate the lane-private score columns
-    for (int i = threadIdx.x; i < NT * 16 * 32 * 4; i += kWarps * 32) sm.acc[i] = 0u;
+    for (int i = threadIdx.x; i < NT * 16 * 32 * 4; i += W * 32) sm.acc[i] = 0u;
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(sm.tmem_slot)),
                      "r"(kTmemCols));
@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(kWarps * 32, OCC) decode_tc_kernel(const TcPar
         const float sum_abs = (s_red[h * 4 + 0] + s_red[h * 4 + 1]) + (s_red[h * 4 + 2] + s_red[h * 4 + 3]);
         return sum_abs > 0.0f ? 1073741824.0f * __frcp_rn(levels * sum_abs) : 0.0f;
     };
-    for (int e = threadIdx.x; e < NT * 512; e += kWarps * 32) s_frag[e] = 0u;  // heads >= G stay 0
+    for (int e = threadIdx.x; e < NT * 512; e += W * 32) s_frag[e] = 0u;  // heads >= G stay 0
     float qsv[8];
     if (threadIdx.x < kDim) {
         const int c = threadIdx.x;
@@ -533,13 +533,13 @@ __global__ void __launch_bounds__(kWarps * 32, OCC) decode_tc_kernel(const TcPar
     // channels; q rows are loaded once.
     const float isd = __fdiv_rn(1.0f, sqrtf((float)kDim));
     float tmax = -INFINITY;  // for head (lane & 7)
-    if (warp < kWarps && ntl > warp) {
+    if (warp < W && ntl > warp) {
         float4 qv[8];
 #pragma unroll
         for (int h = 0; h < 8; ++h)
             qv[h] = h < G ? *reinterpret_cast<const float4*>(a.q + qrow(h) * kDim + 4 * lane)
                           : make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int j = warp; j < ntl; j += kWarps) {
+        for (int j = warp; j < ntl; j += W) {
             const float4 kv = *reinterpret_cast<const float4*>(a.k_tail + ((size_t)unit * a.tail_cap + j) * kDim + 4 * lane);
 #pragma unroll
             for (int h = 0; h < 8; ++h) {
@@ -577,7 +577,7 @@ __global__ void __launch_bounds__(kWarps * 32, OCC) decode_tc_kernel(const TcPar
     if (threadIdx.x < 24) {  // CTA partial
         const int kk = threadIdx.x;
         float v = sm.wpart[kk];
-        for (int w2 = 1; w2 < kWarps; ++w2) v = kk < 8 ? fminf(v, sm.wpart[w2 * 24 + kk]) : fmaxf(v, sm.wpart[w2 * 24 + kk]);
+        for (int w2 = 1; w2 < W; ++w2) v = kk < 8 ? fminf(v, sm.wpart[w2 * 24 + kk]) : fmaxf(v, sm.wpart[w2 * 24 + kk]);
         if (S > 1) {
             asm volatile("barrier.cluster.wait.acquire;" ::: "memory");  // #0 (non-aligned: one warp)
             for (int r = 0; r < S; ++r) st_cluster_f32(sm.allpart + rank * 24 + kk, r, v);
@@ -756,7 +756,7 @@ __global__ void __launch_bounds__(kWarps * 32, OCC) decode_tc_kernel(const TcPar
         cluster_arrive();  // #2a
         cluster_wait();
     }
-    for (int idx = threadIdx.x; idx < G * kDim; idx += kWarps * 32) {
+    for (int idx = threadIdx.x; idx < G * kDim; idx += W * 32) {
         const int h = idx / kDim, ch = idx % kDim;
         constexpr int cpb = Gm::kCpb;
         // invert v_channel: ch = (2 BITS g' + q) cpb + (cpb - 1 - s), nc = q cpb + s, and
@@ -775,7 +775,7 @@ __global__ void __launch_bounds__(kWarps * 32, OCC) decode_tc_kernel(const TcPar
         const float V = __fmaf_rn((float)pl[2], 65536.0f, __fmaf_rn((float)pl[1], 256.0f, (float)pl[0])) *
                         __int_as_float((127 - s_slot * BITS) << 23);
         unsigned long long ws = 0;
-        for (int w2 = 0; w2 < kWarps; ++w2) ws += sm.wsum[w2 * 8 + h];
+        for (int w2 = 0; w2 < W; ++w2) ws += sm.wsum[w2 * 8 + h];
         const float wv = (float)ws;
         constexpr float kInvLevelsV = 1.0f / (float)((1u << BITS) - 1u);
         const float v_step = fmaxf(__fsub_rn(v_b, v_a) * kInvLevelsV, 0.0f);
@@ -811,7 +811,7 @@ __global__ void __launch_bounds__(kWarps * 32, OCC) decode_tc_kernel(const TcPar
         cluster_arrive();  // #2b: partial numerators / denominators are in rank 0
         cluster_wait();
         if (rank == 0) {
-            for (int idx = threadIdx.x; idx < G * kDim; idx += kWarps * 32) {
+            for (int idx = threadIdx.x; idx < G * kDim; idx += W * 32) {
                 const int h = idx / kDim;
                 float num = 0.f, den = 0.f;
                 for (int r = 0; r < S; ++r) {
@@ -834,9 +834,9 @@ __global__ void __launch_bounds__(kWarps * 32, OCC) decode_tc_kernel(const TcPar
 // Token split: at most 8192 (NT = 1) / 4096 tokens per CTA; small batches split units further (down to
 // 256 tokens per CTA) so that units x S covers the SMs - a single unit otherwise runs on
 // one SM for its full latency.
-void plan(const DecodeArgs& a, int NT, int& S, int& T) {
+void plan(const DecodeArgs& a, int NT, int& S, int& T, int W = kWarps) {
     const int n = (int)a.n_vis;
-    const int ct = cta_tokens(NT);
+    const int ct = cta_tokens(NT, W);
     int s_min = std::max(1, (n + ct - 1) / ct);
     size_t pu = a.plan_units ? a.plan_units : a.units;  // a chunk plans as its whole batch
     if (NT == 1 && a.group > 4) pu *= 2;                 // two head-group CTAs per unit
@@ -852,19 +852,19 @@ void plan(const DecodeArgs& a, int NT, int& S, int& T) {
     S = (n + T - 1) / T;
 }
 
-template <int BITS, int NT, int OCC>
+template <int BITS, int NT, int OCC, int W = kWarps>
 cudaError_t launch_occ(const DecodeArgs& a, cudaStream_t s, int groups = 1) {
     int S, T;
-    plan(a, NT, S, T);
+    plan(a, NT, S, T, W);
     cudaError_t e = cudaSuccess;
     TcParams p{a, S, T, groups};
-    // TMEM: kTmemCols per CTA; never let more CTAs share an SM than TMEM can serve (a
+    // TMEM: 512 columns per SM; never let more CTAs share an SM than TMEM can serve (a
     // blocked tcgen05.alloc inside a cluster could deadlock against its partners).
-    const size_t max_ctas = OCC == 1 ? 1 : (NT == 1 ? 4 : 2);
-    size_t smem = tc_smem_bytes<BITS, NT, OCC>(S);
+    const size_t max_ctas = W == 4 ? 4 : (OCC == 1 ? 1 : 2);
+    size_t smem = tc_smem_bytes<BITS, NT, OCC, W>(S);
     const size_t floor_bytes = 232448 / (max_ctas + 1) + 1;
     if (smem < floor_bytes) smem = floor_bytes;
-    auto kern = decode_tc_kernel<BITS, NT, OCC>;
+    auto kern = decode_tc_kernel<BITS, NT, OCC, W>;
     static bool attr_done = false;  // per instantiation
     if (!attr_done) {
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -875,7 +875,7 @@ cudaError_t launch_occ(const DecodeArgs& a, cudaStream_t s, int groups = 1) {
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(a.units * S * groups));
-    cfg.blockDim = dim3(kWarps * 32);
+    cfg.blockDim = dim3(W * 32);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attrs[2];
@@ -972,6 +972,19 @@ size_t decode_tc_scratch_bytes(size_t units) { return units * (2 * 512 * sizeof(
 
 // CTAs per SM the kernel is built for (register bound + ring depth): 2 by default,
 // KVQ_TC_OCC=3 selects the 3-CTA variant (fewer registers, shallower ring).
+// CTA shape: 8 warps, two CTAs per SM; or 4 warps, four per SM (up to 1024 tokens per warp,
+// 128 TMEM columns per CTA). Many short units favour 4-warp CTAs - all of C2's 512 units are
+// resident at once instead of in 1.73 waves (56.0 -> 50.4 us; C5 B=512 342 -> 287 us) -
+// while fewer or longer units favour 8 warps (C3: a 4-warp CTA would need a 2-CTA cluster,
+// 48 -> 52 us; profiles/r01_tc_w4.txt). KVQ_TC_W4=0/1 forces either (tuning).
+static bool tc_w4(const DecodeArgs& a) {
+    static const char* env = std::getenv("KVQ_TC_W4");
+    if (env) return std::atoi(env) != 0;
+    size_t pu = a.plan_units ? a.plan_units : a.units;
+    if (a.group > 4) pu *= 2;
+    return pu > 2 * 148 && a.n_vis <= (size_t)cta_tokens(1, 4);
+}
+
 static int tc_occ() {
     static int occ = [] {
         const char* e = std::getenv("KVQ_TC_OCC");
@@ -988,6 +1001,7 @@ cudaError_t launch_bits(const DecodeArgs& a, cudaStream_t s) {
     } else {
         // G > 4 at NT = 1: two head groups as separate CTAs (two CTAs per SM each)
         const int groups = a.group > 4 ? 2 : 1;
+        if (tc_w4(a)) return launch_occ<BITS, NT, 4, 4>(a, s, groups);
         return tc_occ() == 3 ? launch_occ<BITS, NT, 3>(a, s, groups) : launch_occ<BITS, NT, 2>(a, s, groups);
     }
 }
@@ -1004,9 +1018,11 @@ int tc_nt(const DecodeArgs& a) {
 }
 
 template <int BITS, int NT>
-static size_t tc_smem_for(int S) {
+static size_t tc_smem_for(const DecodeArgs& a, int S) {
     if constexpr (NT == 2) {
         return tc_smem_bytes<BITS, NT, 1>(S);
+    } else if (tc_w4(a)) {
+        return tc_smem_bytes<BITS, NT, 4, 4>(S);
     } else {
         return tc_occ() == 3 ? tc_smem_bytes<BITS, NT, 3>(S) : tc_smem_bytes<BITS, NT, 2>(S);
     }
@@ -1020,21 +1036,21 @@ bool decode_tc_supported(const DecodeArgs& a) {
     if (a.units == 0) return false;
     int S, T;
     const int NT = tc_nt(a);
-    plan(a, NT, S, T);
+    plan(a, NT, S, T, NT == 1 && tc_w4(a) ? 4 : kWarps);
     if (S > kMaxCluster) return false;
     // the fp32 tail lives in rank 0 (at most kTailMax rows) unless the tail pass owns it
     if (a.tail_cap > (size_t)kTailMax && a.tail_lse == nullptr) return false;
     (void)T;
     size_t smem = 0;
     switch (a.bits * 10 + NT) {
-        case 11: smem = tc_smem_for<1, 1>(S); break;
-        case 12: smem = tc_smem_for<1, 2>(S); break;
-        case 21: smem = tc_smem_for<2, 1>(S); break;
-        case 22: smem = tc_smem_for<2, 2>(S); break;
-        case 41: smem = tc_smem_for<4, 1>(S); break;
-        case 42: smem = tc_smem_for<4, 2>(S); break;
-        case 81: smem = tc_smem_for<8, 1>(S); break;
-        case 82: smem = tc_smem_for<8, 2>(S); break;
+        case 11: smem = tc_smem_for<1, 1>(a, S); break;
+        case 12: smem = tc_smem_for<1, 2>(a, S); break;
+        case 21: smem = tc_smem_for<2, 1>(a, S); break;
+        case 22: smem = tc_smem_for<2, 2>(a, S); break;
+        case 41: smem = tc_smem_for<4, 1>(a, S); break;
+        case 42: smem = tc_smem_for<4, 2>(a, S); break;
+        case 81: smem = tc_smem_for<8, 1>(a, S); break;
+        case 82: smem = tc_smem_for<8, 2>(a, S); break;
     }
     return smem <= 220 * 1024;
 }
