@@ -121,9 +121,13 @@ inline int cta_tokens(int NT, int W = kWarps) { return W * std::min(NT == 1 ? 10
 
 // Per-warp TMA ring: ~10 KB in flight per warp (80 KB per CTA, two CTAs per SM) covers
 // the ~2 us bulk-copy latency measured under load (profiles/r01_trace_umma_c2.txt).
+#ifndef KVQ_TC_W4_STAGES  // (tuning builds)
+#define KVQ_TC_W4_STAGES 3
+#endif
 template <int BITS, int OCC>
 constexpr int ring_stages() {
-    return OCC >= 3   ? (Geo<BITS>::kStageBytesB >= 4096 ? 2 : 3)
+    return OCC == 4   ? (Geo<BITS>::kStageBytesB >= 4096 ? 2 : KVQ_TC_W4_STAGES)  // 4-warp CTAs
+           : OCC >= 3 ? (Geo<BITS>::kStageBytesB >= 4096 ? 2 : 3)
            : OCC == 2 ? (Geo<BITS>::kStageBytesB >= 4096 ? 3 : 5)
                       : (Geo<BITS>::kStageBytesB >= 4096 ? 4 : 8);  // one CTA per SM (G > 4)
 }
