@@ -8,8 +8,9 @@
 //   row     = [g(score_vis) | score_tail],  g affine from (gamma, delta) of the vis part
 //   out_c   = (s_c sum_j p_j code_jc + alpha_c sum_j p_j + sum_t p_t v_tc) / sum p
 //
-// One kernel, a cluster of S CTAs per unit (each CTA a contiguous token chunk, 8 warps,
-// each warp a contiguous slice streamed through its own cp.async.bulk ring):
+// One kernel, a cluster of S CTAs per unit and head group (each CTA a contiguous token
+// chunk, 8 or 4 warps, each warp a contiguous slice streamed through its own cp.async.bulk
+// ring):
 //   prologue  : fold the K scale into the query: Q'_c = round(S_h qs_c / 2^sh_c) in 4
 //               balanced int8 digit planes (S_h keeps the int32 score exact) -> the B
 //               fragments of the q.K MMA, built in shared memory while the ring fills
@@ -59,7 +60,7 @@ struct Geo {
 
 struct TcParams {
     DecodeArgs a;
-    int S, T;    // cluster size, visual tokens per CTA (multiple of 8 warps x 32)
+    int S, T;    // cluster size, visual tokens per CTA (multiple of 256)
     int groups;  // head groups per unit handled by separate CTAs (1, or 2 for G > 4 at NT = 1)
 };
 
@@ -111,7 +112,8 @@ __device__ __forceinline__ int v_channel(int g, int iota, int& shift) {
 // ---- decode ------------------------------------------------------------------------------
 constexpr int kWarps = 8;             // consumer warps per CTA
 // Visual tokens per warp (contiguous), at most: the warp's scores wait in TMEM (4 columns
-// per 32-token step and head group), 256 columns per CTA, two CTAs per SM = all 512.
+// per 32-token step and head group): 256 columns per 8-warp CTA x 2 per SM, or 128 per
+// 4-warp CTA x 4 per SM = all 512.
 template <int NT>
 constexpr int warp_tokens() { return NT == 1 ? 1024 : 512; }
 #ifndef KVQ_TC_WARP_TOKENS_CAP  // (tuning builds: cap the per-warp token count)
@@ -208,10 +210,10 @@ __device__ __forceinline__ void red_add_u32(uint32_t* p, uint32_t v) {
     asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
 }
 
-// CTA = 8 warps; warp w owns visual tokens [w*512, w*512+512) of the CTA's chunk and
-// streams them (K codes, then V codes) through its own TMA ring, re-armed by its lane 0.
-// A unit of n visual tokens takes S = ceil(n / 4096) CTAs (a cluster); for n <= 4096
-// there is no cluster traffic at all.
+// CTA = W warps (8, or 4 for many short units); warp w owns visual tokens [w T/W, (w+1) T/W)
+// of the CTA's chunk (at most 1024) and streams them (K codes, then V codes) through its own
+// TMA ring, re-armed by its lane 0. A unit of n visual tokens takes S CTAs (a cluster, see
+// plan()); with S = 1 there is no cluster traffic at all.
 //
 // Token order inside a 32-token step: the phase-A accumulator gives lane (g, t) the
 // scores of tokens {g, g+8, g+16, g+24} for head t. Phase B uses exactly those four
@@ -249,7 +251,7 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
     uint64_t* full = sm.full + warp * kStagesW;
 
     const int n = (int)a.n_vis;
-    const int wt = p.T / W;                        // tokens per warp (multiple of 32, <= 512)
+    const int wt = p.T / W;                        // tokens per warp (multiple of 32, <= 1024)
     const int tok0 = rank * p.T + warp * wt;              // this warp's first token
     const int nv = max(0, min(wt, n - tok0));
     // fp32 tail: rank 0, unless a separate tail pass owns it (a.tail_lse). tail_len is written
@@ -852,7 +854,7 @@ void plan(const DecodeArgs& a, int NT, int& S, int& T, int W = kWarps) {
     static const int force = std::getenv("KVQ_TC_SPLIT") ? std::atoi(std::getenv("KVQ_TC_SPLIT")) : 0;  // tuning
     if (force > 0) s = std::max(s_min, std::min(force, kMaxCluster));
     s = std::min(s, std::max(1, (n + 255) / 256));
-    T = ((n + s - 1) / s + 255) / 256 * 256;  // multiple of 8 warps x 32 tokens
+    T = ((n + s - 1) / s + 255) / 256 * 256;  // multiple of 8 warps x 32 tokens (and of 4 x 32)
     S = (n + T - 1) / T;
 }
 
