@@ -701,3 +701,35 @@ def test_randomized_paths_vs_oracle(kvq, oracle, case):
         # sizes (2e-5 on the small golden trajectories), 5e-4 for the tensor-core paths
         tol = 1e-4 if path == kvq.PATH_GENERIC else 5e-4
         assert rel_l2(out, want) <= tol, (path, rel_l2(out, want))
+
+
+@pytest.mark.parametrize("bits,G,n,tail", [(1, 4, 300, 0), (2, 2, 1100, 70), (4, 6, 64, 5)])
+def test_many_units_four_warp_ctas(kvq, oracle, bits, G, n, tail):
+    """More than 296 units of n <= 4096 tokens select 4-warp CTAs (four per SM): checked
+    against the C restatement on a spread of units, plus determinism."""
+    rng = np.random.default_rng(bits * 1000 + n)
+    B, H, d = 40, 8, 128  # 320 units
+    k = rng.normal(size=(B, H, n, d)).astype(np.float32)
+    v = rng.normal(size=(B, H, n, d)).astype(np.float32)
+    tau = (1.0, 0.0)
+    cache = kvq.BatchedCache.build(k, v, kvq.QuantizationConfig(bits), kvq.CalibrationParams(*tau), group=G)
+    tk, tv = [], []
+    for _ in range(tail):
+        kn = rng.normal(size=(B, H, d)).astype(np.float32)
+        vn = rng.normal(size=(B, H, d)).astype(np.float32)
+        cache.append(kn, vn)
+        tk.append(kn)
+        tv.append(vn)
+    q = rng.normal(size=(B, H, G, d)).astype(np.float32)
+    out, _, _ = cache.decode(q)
+    again, _, _ = cache.decode(q)
+    assert np.array_equal(out, again)
+    for b, h in [(0, 0), (7, 3), (19, 7), (39, 5)]:
+        ka, kb = oracle.compute_stats(k[b, h])
+        va, vb = oracle.compute_stats(v[b, h])
+        kc, vc = oracle.quantize(k[b, h], ka, kb, bits), oracle.quantize(v[b, h], va, vb, bits)
+        kt = np.stack([x[b, h] for x in tk]) if tk else np.zeros((0, d), np.float32)
+        vt = np.stack([x[b, h] for x in tv]) if tv else np.zeros((0, d), np.float32)
+        for g in range(G):
+            want = oracle.decode_head(q[b, h, g], n, bits, 8, kc, ka, kb, vc, va, vb, kt, vt, *tau)[0]
+            assert rel_l2(out[b, h, g], want) <= 5e-4, (b, h, g, rel_l2(out[b, h, g], want))
