@@ -33,6 +33,10 @@ decode_generic_kernel(DecodeArgs a) {
     float* qs = smem;            // [cpr]
     float* red = smem + cpr;     // [32]
     float* scal = red + 32;      // qdota
+    // channel c's code: byte cbyte[c] of the row, bits [cshift[c], cshift[c] + b) - codes
+    // never straddle a byte (b | 8), so no per-code division or word assembly
+    uint16_t* cbyte = reinterpret_cast<uint16_t*>(scal + 8);  // [d]
+    uint8_t* cshift = reinterpret_cast<uint8_t*>(cbyte + d);   // [d]
     const size_t unit = blockIdx.x / a.group;
     const size_t g = blockIdx.x % a.group;
     const size_t b = unit / a.kv_heads;
@@ -64,15 +68,23 @@ decode_generic_kernel(DecodeArgs a) {
         for (size_t c = 0; c < d; ++c) qa = __fadd_rn(qa, __fmul_rn(q[c], ka[c]));
         scal[0] = qa;
     }
+    for (size_t c = threadIdx.x; c < d; c += blockDim.x) {
+        uint32_t by, sh;
+        code_pos(c, a.bits, a.word_bits, by, sh);
+        cbyte[c] = (uint16_t)by;
+        cshift[c] = (uint8_t)sh;
+    }
     __syncthreads();
     const float qdota = scal[0];
+    const uint32_t cmask = (1u << a.bits) - 1u;
+    auto code = [&](const uint8_t* r, size_t c) { return (float)(((uint32_t)r[cbyte[c]] >> cshift[c]) & cmask); };
 
     // Scores. Local min/max of the visual part.
     float lo = INFINITY, hi = -INFINITY;
     for (size_t j = threadIdx.x; j < n; j += blockDim.x) {
         const uint8_t* r = kc + j * rb;
         float acc = 0.0f;
-        for (size_t c = 0; c < d; ++c) acc = __fmaf_rn(qs[c], (float)code_at(r, c, a.bits, a.word_bits), acc);
+        for (size_t c = 0; c < d; ++c) acc = __fmaf_rn(qs[c], code(r, c), acc);
         float s = __fmul_rn(__fadd_rn(acc, qdota), inv_sqrt_d);
         row[j] = s;
         lo = fminf(lo, s);
@@ -129,7 +141,7 @@ decode_generic_kernel(DecodeArgs a) {
         for (size_t j = 0; j < n; ++j) {
             float w = row[j];
             wsum = __fadd_rn(wsum, w);
-            acc = __fmaf_rn(w, (float)code_at(vc + j * rb, c, a.bits, a.word_bits), acc);
+            acc = __fmaf_rn(w, code(vc + j * rb, c), acc);
         }
         float o = 0.0f;
         if (n > 0) {
@@ -171,14 +183,24 @@ __global__ void qk_scores_kernel(const float* __restrict__ q, const uint8_t* __r
         for (size_t c = 0; c < dim; ++c) qa = __fadd_rn(qa, __fmul_rn(qh[c], a[c]));
         smem[cpr] = qa;
     }
+    uint16_t* cbyte = reinterpret_cast<uint16_t*>(smem + cpr + 1);  // [dim] code positions
+    uint8_t* cshift = reinterpret_cast<uint8_t*>(cbyte + dim);
+    for (size_t c = threadIdx.x; c < dim; c += blockDim.x) {
+        uint32_t by, sh;
+        code_pos(c, bits, word_bits, by, sh);
+        cbyte[c] = (uint16_t)by;
+        cshift[c] = (uint8_t)sh;
+    }
     __syncthreads();
     const float qdota = smem[cpr];
+    const uint32_t cmask = bits >= 32 ? 0xffffffffu : (1u << bits) - 1u;
     const uint8_t* seg = codes + h * tokens * rb;
     for (size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x; j < tokens;
          j += (size_t)gridDim.x * blockDim.x) {
         const uint8_t* r = seg + j * rb;
         float acc = 0.0f;
-        for (size_t c = 0; c < dim; ++c) acc = __fmaf_rn(qs[c], (float)code_at(r, c, bits, word_bits), acc);
+        for (size_t c = 0; c < dim; ++c)
+            acc = __fmaf_rn(qs[c], (float)code_load(r, cbyte[c], cshift[c], bits, cmask), acc);
         scores[h * tokens + j] = __fadd_rn(acc, qdota);
     }
 }
@@ -195,9 +217,12 @@ __global__ void wv_output_kernel(const float* __restrict__ w, const uint8_t* __r
     for (size_t c = (size_t)blockIdx.x * blockDim.x + threadIdx.x; c < dim;
          c += (size_t)gridDim.x * blockDim.x) {
         float acc = 0.0f, wsum = 0.0f;
+        uint32_t by, sh;
+        code_pos(c, bits, word_bits, by, sh);
+        const uint32_t cmask = bits >= 32 ? 0xffffffffu : (1u << bits) - 1u;
         for (size_t j = 0; j < tokens; ++j) {
             wsum = __fadd_rn(wsum, wh[j]);
-            acc = __fmaf_rn(wh[j], (float)code_at(seg + j * rb, c, bits, word_bits), acc);
+            acc = __fmaf_rn(wh[j], (float)code_load(seg + j * rb, by, sh, bits, cmask), acc);
         }
         float a = alpha[h * dim + c];
         float range = __fsub_rn(beta[h * dim + c], a);
@@ -276,7 +301,7 @@ cudaError_t launch_naive_wv(const float* w, const float* v, size_t rows, size_t 
 
 cudaError_t launch_decode_generic(const DecodeArgs& a, cudaStream_t s) {
     const size_t cpr = codes_per_row(a.dim, a.bits, a.word_bits);
-    const size_t smem = sizeof(float) * (cpr + 40);
+    const size_t smem = sizeof(float) * (cpr + 40) + 3 * a.dim + 16;  // + per-channel byte / shift
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(decode_generic_kernel,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -292,7 +317,7 @@ cudaError_t launch_qk_scores(const float* q, const uint8_t* codes, const float* 
                              int bits, int word_bits, float* scores, cudaStream_t s) {
     const size_t cpr = codes_per_row(dim, bits, word_bits);
     dim3 grid((unsigned)((tokens + 255) / 256 > 0 ? (tokens + 255) / 256 : 1), (unsigned)heads);
-    qk_scores_kernel<<<grid, 256, sizeof(float) * (cpr + 1), s>>>(q, codes, alpha, beta, tokens, dim,
+    qk_scores_kernel<<<grid, 256, sizeof(float) * (cpr + 1) + 3 * dim + 8, s>>>(q, codes, alpha, beta, tokens, dim,
                                                                    bits, word_bits, scores);
     note_launch();
     return cudaGetLastError();

@@ -16,6 +16,24 @@ __device__ __forceinline__ uint32_t code_at(const uint8_t* row, size_t c, int bi
     return (w >> (word_bits - bits * ((int)(c % (size_t)g) + 1))) & (bits >= 32 ? 0xffffffffu : (1u << bits) - 1u);
 }
 
+// Byte of a packed row where channel c's code starts, and its bit shift there: the code
+// sits at bit M - N(k+1) of its LE word (k = c mod codes-per-word); for N <= 8 (N | 8) it
+// never straddles a byte. Hoisting this out of token loops removes per-code divisions.
+__device__ __forceinline__ void code_pos(size_t c, int bits, int word_bits, uint32_t& byte, uint32_t& shift) {
+    const size_t cpw = (size_t)(word_bits / bits);
+    const int bitpos = word_bits - bits * ((int)(c % cpw) + 1);
+    byte = (uint32_t)((c / cpw) * (size_t)(word_bits / 8) + (size_t)(bitpos / 8));
+    shift = (uint32_t)(bitpos % 8);  // 0 for N = 16 (half-word aligned)
+}
+
+// The code at (byte, shift) of a row: one byte for N <= 8; a 16-bit code (the standalone
+// quantizer API allows N = 16) spans the two LE bytes of its half word.
+__device__ __forceinline__ uint32_t code_load(const uint8_t* row, uint32_t byte, uint32_t shift, int bits,
+                                              uint32_t mask) {
+    const uint32_t v = bits <= 8 ? (uint32_t)row[byte] : (uint32_t)row[byte] | ((uint32_t)row[byte + 1] << 8);
+    return (v >> shift) & mask;
+}
+
 // g (calibrate.hpp:62-67), evaluated with the reference's exact op order.
 __device__ __forceinline__ float g_apply_dev(float x, float gamma, float width, float tau1, float tau2) {
     if (width <= 0.0f) return __fsub_rn(x, tau1);

@@ -733,3 +733,22 @@ def test_many_units_four_warp_ctas(kvq, oracle, bits, G, n, tail):
         for g in range(G):
             want = oracle.decode_head(q[b, h, g], n, bits, 8, kc, ka, kb, vc, va, vb, kt, vt, *tau)[0]
             assert rel_l2(out[b, h, g], want) <= 5e-4, (b, h, g, rel_l2(out[b, h, g], want))
+
+
+@pytest.mark.parametrize("word_bits", [16, 32])
+def test_sixteen_bit_codes_standalone_kernels(kvq, oracle, word_bits):
+    """The standalone quantizer accepts 16-bit codes (quantize.hpp:98 with N = 16): qk_scores
+    and wv_output read them across the two bytes of their half word (C restatement)."""
+    rng = np.random.default_rng(16 + word_bits)
+    n, d = 37, 24
+    m = rng.normal(size=(n, d)).astype(np.float32)
+    st = kvq.compute_stats(m)
+    seg = kvq.quantize(m, st, 16, word_bits)
+    q = rng.normal(size=d).astype(np.float32)
+    w = rng.random(n).astype(np.float32)
+    got_s = kvq.qk_scores(q, seg)
+    want_s = oracle.qk_scores(q, seg.codes.bytes, n, d, st.alpha, st.beta, 16, word_bits)
+    assert rel_l2(got_s, want_s) <= 1e-6
+    got_o = kvq.wv_output(w, seg)
+    want_o = oracle.wv_output(w, seg.codes.bytes, n, d, st.alpha, st.beta, 16, word_bits)
+    assert rel_l2(got_o, want_o) <= 1e-6
