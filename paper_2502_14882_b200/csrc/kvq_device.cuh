@@ -5,17 +5,6 @@
 
 namespace kvqb {
 
-// Code of channel c in one packed row (reference layout: LE M-bit words, MSB-first
-// codes; bitpack.hpp:182, 199-200).
-__device__ __forceinline__ uint32_t code_at(const uint8_t* row, size_t c, int bits, int word_bits) {
-    const int g = word_bits / bits;
-    const size_t wi = c / (size_t)g;
-    const int nb = word_bits / 8;
-    uint32_t w = 0;
-    for (int b = 0; b < nb; ++b) w |= (uint32_t)row[wi * nb + b] << (8 * b);
-    return (w >> (word_bits - bits * ((int)(c % (size_t)g) + 1))) & (bits >= 32 ? 0xffffffffu : (1u << bits) - 1u);
-}
-
 // Byte of a packed row where channel c's code starts, and its bit shift there: the code
 // sits at bit M - N(k+1) of its LE word (k = c mod codes-per-word); for N <= 8 (N | 8) it
 // never straddles a byte. Hoisting this out of token loops removes per-code divisions.
