@@ -39,7 +39,10 @@ namespace {
 
 constexpr int kDim = 128;
 constexpr int kStages = 2;
-constexpr int kStageBytes = 2048;
+#ifndef KVQ_TC_STAGE_BYTES  // (tuning builds)
+#define KVQ_TC_STAGE_BYTES 2048
+#endif
+constexpr int kStageBytes = KVQ_TC_STAGE_BYTES;
 constexpr int kTailMax = 64;   // fp32 tail tokens per CTA
 constexpr int kMaxCluster = 16;
 constexpr float kLog2e = 1.4426950408889634f;
@@ -48,11 +51,11 @@ constexpr float kPScale = 4190000.0f;  // p in [0, 1(+eps)] -> integer < 2^22 (2
 constexpr float kLog2PScale = 21.9985188f;  // log2(kPScale): weights are on the kPScale scale
 constexpr int kPRow = 12;              // words per p-plane smem row (stride avoids bank conflicts)
 
-template <int BITS>
+template <int BITS, int SB = kStageBytes>
 struct Geo {
     static constexpr int kRowBytes = 16 * BITS;
     // >= 32 tokens per stage: a stage holds whole 32-token phase-B blocks
-    static constexpr int kStageBytesB = kStageBytes / kRowBytes >= 32 ? kStageBytes : 32 * kRowBytes;
+    static constexpr int kStageBytesB = SB / kRowBytes >= 32 ? SB : 32 * kRowBytes;
     static constexpr int kStageTokens = kStageBytesB / kRowBytes;
     static constexpr int kCpb = 8 / BITS;  // codes per byte
     static constexpr uint32_t kMask = 0x01010101u * ((1u << BITS) - 1u);
@@ -126,12 +129,21 @@ inline int cta_tokens(int NT, int W = kWarps) { return W * std::min(NT == 1 ? 10
 #ifndef KVQ_TC_W4_STAGES  // (tuning builds)
 #define KVQ_TC_W4_STAGES 3
 #endif
-template <int BITS, int OCC>
+#ifndef KVQ_TC_W4_STAGE_BYTES
+#define KVQ_TC_W4_STAGE_BYTES 4096
+#endif
+// Stage size per CTA shape: 4-warp CTAs stream 4 KB stages, two deep (fewer barrier rounds
+// per token; C2 50.0 -> 47.8 us), 8-warp CTAs 2 KB stages five deep (4 KB stages cost C3
+// 48 -> 60 us; profiles/r01_tc_stage.txt).
+template <int W>
+constexpr int stage_bytes() { return W == 4 ? KVQ_TC_W4_STAGE_BYTES : kStageBytes; }
+template <int BITS, int OCC, int W = kWarps>
 constexpr int ring_stages() {
-    return OCC == 4   ? (Geo<BITS>::kStageBytesB >= 4096 ? 2 : KVQ_TC_W4_STAGES)  // 4-warp CTAs
-           : OCC >= 3 ? (Geo<BITS>::kStageBytesB >= 4096 ? 2 : 3)
-           : OCC == 2 ? (Geo<BITS>::kStageBytesB >= 4096 ? 3 : 5)
-                      : (Geo<BITS>::kStageBytesB >= 4096 ? 4 : 8);  // one CTA per SM (G > 4)
+    constexpr int sb = Geo<BITS, stage_bytes<W>()>::kStageBytesB;
+    return OCC == 4   ? (sb >= 4096 ? 2 : KVQ_TC_W4_STAGES)  // 4-warp CTAs
+           : OCC >= 3 ? (sb >= 4096 ? 2 : 3)
+           : OCC == 2 ? (sb >= 4096 ? 3 : 5)
+                      : (sb >= 4096 ? 4 : 8);  // one CTA per SM (G > 4)
 }
 
 struct Smem {  // carve-up of the dynamic shared memory of one decode CTA
@@ -156,9 +168,9 @@ __host__ __device__ inline size_t tc_smem_bytes(int S, Smem* out = nullptr, uint
         off += (bytes + 127) & ~size_t(127);
         return base + o;
     };
-    constexpr int stage = Geo<BITS>::kStageBytesB;
+    constexpr int stage = Geo<BITS, stage_bytes<W>()>::kStageBytesB;
     const size_t recv_bytes = S > 1 ? (size_t)S * (8 * kDim + 8) * 4 : 0;
-    const size_t ring_bytes = (size_t)W * ring_stages<BITS, OCC>() * stage;
+    const size_t ring_bytes = (size_t)W * ring_stages<BITS, OCC, W>() * stage;
     const size_t tail_use = recv_bytes;
     uint8_t* ring = take(ring_bytes > tail_use ? ring_bytes : tail_use);
     uint8_t* acc = take((size_t)NT * 16 * 32 * 4 * 4);
@@ -168,7 +180,7 @@ __host__ __device__ inline size_t tc_smem_bytes(int S, Smem* out = nullptr, uint
     uint8_t* allpart = take((size_t)(S > 0 ? S : 1) * 24 * 4);
     uint8_t* gpar = take(32 * 4);
     uint8_t* wsum = take((size_t)W * 8 * 4);
-    uint8_t* full = take((size_t)W * ring_stages<BITS, OCC>() * 8);
+    uint8_t* full = take((size_t)W * ring_stages<BITS, OCC, W>() * 8);
     uint8_t* slot = take(16);
     if (out) {
         out->ring = ring;
@@ -224,8 +236,8 @@ __device__ __forceinline__ void red_add_u32(uint32_t* p, uint32_t v) {
 // (deterministic); cross-CTA traffic is push-only.
 template <int BITS, int NT, int OCC, int W = kWarps>
 __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p) {
-    using Gm = Geo<BITS>;
-    constexpr int kStagesW = ring_stages<BITS, OCC>();
+    using Gm = Geo<BITS, stage_bytes<W>()>;
+    constexpr int kStagesW = ring_stages<BITS, OCC, W>();
     constexpr int kSteps = warp_tokens<NT>() / 32;                 // 32-token steps per warp, at most
     constexpr uint32_t kTmemCols = (W / 4) * kSteps * 4 * NT;        // lane-sharing warps; 256 / 128
     const DecodeArgs& a = p.a;
