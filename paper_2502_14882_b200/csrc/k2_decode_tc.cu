@@ -40,7 +40,7 @@ namespace {
 constexpr int kDim = 128;
 constexpr int kStages = 2;
 #ifndef KVQ_TC_STAGE_BYTES  // (tuning builds)
-#define KVQ_TC_STAGE_BYTES 2048
+#define KVQ_TC_STAGE_BYTES 4096
 #endif
 constexpr int kStageBytes = KVQ_TC_STAGE_BYTES;
 constexpr int kTailMax = 64;   // fp32 tail tokens per CTA
@@ -126,24 +126,21 @@ inline int cta_tokens(int NT, int W = kWarps) { return W * std::min(NT == 1 ? 10
 
 // Per-warp TMA ring: ~10 KB in flight per warp (80 KB per CTA, two CTAs per SM) covers
 // the ~2 us bulk-copy latency measured under load (profiles/r01_trace_umma_c2.txt).
-#ifndef KVQ_TC_W4_STAGES  // (tuning builds)
-#define KVQ_TC_W4_STAGES 3
+#ifndef KVQ_TC_STAGES  // (tuning builds; 0 = by stage size and occupancy)
+#define KVQ_TC_STAGES 0
 #endif
-#ifndef KVQ_TC_W4_STAGE_BYTES
-#define KVQ_TC_W4_STAGE_BYTES 4096
-#endif
-// Stage size per CTA shape: 4-warp CTAs stream 4 KB stages, two deep (fewer barrier rounds
-// per token; C2 50.0 -> 47.8 us), 8-warp CTAs 2 KB stages five deep (4 KB stages cost C3
-// 48 -> 60 us; profiles/r01_tc_stage.txt).
+// Ring geometry: 4 KB stages two deep per warp, for both CTA shapes - fewer barrier rounds
+// per token than 2 KB x 5 and still two (8-warp) or four (4-warp) CTAs per SM
+// (profiles/r01_tc_stage.txt, r01_tc_stage8.txt: C2 50.0 -> 47.8 us, C3 48.0 -> 45.5 us,
+// C4 164.5 -> 154.7 us; a third 4 KB stage would drop 8-warp CTAs to one per SM).
 template <int W>
-constexpr int stage_bytes() { return W == 4 ? KVQ_TC_W4_STAGE_BYTES : kStageBytes; }
+constexpr int stage_bytes() { return kStageBytes; }
 template <int BITS, int OCC, int W = kWarps>
 constexpr int ring_stages() {
     constexpr int sb = Geo<BITS, stage_bytes<W>()>::kStageBytesB;
-    return OCC == 4   ? (sb >= 4096 ? 2 : KVQ_TC_W4_STAGES)  // 4-warp CTAs
-           : OCC >= 3 ? (sb >= 4096 ? 2 : 3)
-           : OCC == 2 ? (sb >= 4096 ? 3 : 5)
-                      : (sb >= 4096 ? 4 : 8);  // one CTA per SM (G > 4)
+    return KVQ_TC_STAGES > 0 ? KVQ_TC_STAGES
+           : OCC >= 2        ? (sb >= 4096 ? 2 : (OCC == 2 ? 5 : 3))
+                             : (sb >= 4096 ? 4 : 8);  // one CTA per SM (G > 4, NT = 2)
 }
 
 struct Smem {  // carve-up of the dynamic shared memory of one decode CTA
