@@ -3,7 +3,7 @@
 mkdir -p gpurun_out; rm -f gpurun_out/e2e2.txt
 PYTHONPATH=. python tools/e2e_probe3.py >> gpurun_out/e2e2.txt 2>&1
 for rep in 1 2; do
-  for k in 1 2 4; do
+  for k in 1 2 4 8; do
     for cfg in c2 c5b512; do
       KVQ_STEP_CHUNKS=$k timeout 300 python bench.py --config $cfg --steps 50 --warmup 5 --e2e-steps 200 --no-cpu > gpurun_out/e.json 2>/dev/null
       python -c "
