@@ -29,19 +29,23 @@ __device__ __forceinline__ uint32_t code_of(float x, float a, float inv, float l
     return (uint32_t)t;  // NaN -> 0, as the x86 reference build
 }
 
+// M-bit pack words (M = 8, 16, 32), each 32-bit register holding 32/M of them LE: the
+// channel cw-th in the register sits at bit (cw / cpM) M + M - N (cw mod cpM + 1), cpM = M/N
+// (bitpack.hpp:85). For N = 1 the warp ballot's brev puts channel i at bit 31 - i, which is
+// M = 32 directly, M = 16 after swapping the half words, M = 8 after reversing the bytes.
 template <int BITS>
-__device__ __forceinline__ void pack_store(const uint32_t (&code)[4], uint8_t* row_out, int lane) {
+__device__ __forceinline__ void pack_store(const uint32_t (&code)[4], uint8_t* row_out, int lane, int word_bits) {
     if constexpr (BITS == 1) {
+        const uint32_t sel = word_bits == 8 ? 0x0123u : (word_bits == 16 ? 0x1032u : 0x3210u);
         uint32_t words[4];
 #pragma unroll
-        for (int w = 0; w < 4; ++w) words[w] = __byte_perm(__brev(__ballot_sync(0xffffffffu, code[w] != 0u)), 0, 0x0123);
+        for (int w = 0; w < 4; ++w) words[w] = __byte_perm(__brev(__ballot_sync(0xffffffffu, code[w] != 0u)), 0, sel);
         if (lane == 0) *reinterpret_cast<uint4*>(row_out) = make_uint4(words[0], words[1], words[2], words[3]);
     } else {
-        // 32/BITS channels per word; channel c' (within its word) -> bit 8*(c'/cpb) + 8 - BITS*(c'%cpb + 1)
-        constexpr int cpb = 8 / BITS;
         constexpr int lanes_per_word = 32 / BITS;
+        const int cpm = word_bits / BITS;
         const int cw = lane % lanes_per_word;
-        const int shift = 8 * (cw / cpb) + 8 - BITS * (cw % cpb + 1);
+        const int shift = (cw / cpm) * word_bits + word_bits - BITS * (cw % cpm + 1);
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
             uint32_t v = code[w] << shift;
@@ -56,7 +60,7 @@ __device__ __forceinline__ void pack_store(const uint32_t (&code)[4], uint8_t* r
 template <int BITS>
 __global__ void __launch_bounds__(kWarpsPerCta * 32)
 quantize_rows_d128(const float* __restrict__ x, size_t rows, const float* __restrict__ alpha,
-                   const float* __restrict__ beta, uint8_t* __restrict__ codes) {
+                   const float* __restrict__ beta, uint8_t* __restrict__ codes, int word_bits) {
     constexpr int kRowBytes = 16 * BITS;
     const float levels = (float)((1u << BITS) - 1u);
     const size_t m = blockIdx.y;
@@ -85,7 +89,7 @@ quantize_rows_d128(const float* __restrict__ x, size_t rows, const float* __rest
             uint32_t code[4];
 #pragma unroll
             for (int w = 0; w < 4; ++w) code[w] = code_of(v[i][w], a[w], inv[w], levels);
-            pack_store<BITS>(code, dst + (r0 + i) * kRowBytes, lane);
+            pack_store<BITS>(code, dst + (r0 + i) * kRowBytes, lane, word_bits);
         }
     }
 }
@@ -95,11 +99,11 @@ quantize_rows_d128(const float* __restrict__ x, size_t rows, const float* __rest
 bool quantize_fused_supported(size_t rows, size_t dim, int word_bits, int mode) {
     (void)rows;
     (void)mode;  // stats (either mode) come from the stats kernel; codes are per channel
-    return dim == (size_t)kDim && word_bits == 8;
+    return dim == (size_t)kDim && (word_bits == 8 || word_bits == 16 || word_bits == 32);
 }
 
-cudaError_t launch_quantize_fused(const float* x, size_t mats, size_t rows, size_t dim, int bits, int mode,
-                                  float* alpha, float* beta, uint8_t* codes, cudaStream_t s) {
+cudaError_t launch_quantize_fused(const float* x, size_t mats, size_t rows, size_t dim, int bits, int word_bits,
+                                  int mode, float* alpha, float* beta, uint8_t* codes, cudaStream_t s) {
     if (rows == 0 || mats == 0) return cudaSuccess;
     cudaError_t e = launch_compute_stats(x, mats, rows, dim, mode, alpha, beta, s);  // compute_stats
     if (e != cudaSuccess) return e;
@@ -110,10 +114,10 @@ cudaError_t launch_quantize_fused(const float* x, size_t mats, size_t rows, size
     if (gx > cap) gx = cap < 1 ? 1 : cap;
     dim3 grid((unsigned)gx, (unsigned)mats);
     switch (bits) {
-        case 1: quantize_rows_d128<1><<<grid, kWarpsPerCta * 32, 0, s>>>(x, rows, alpha, beta, codes); break;
-        case 2: quantize_rows_d128<2><<<grid, kWarpsPerCta * 32, 0, s>>>(x, rows, alpha, beta, codes); break;
-        case 4: quantize_rows_d128<4><<<grid, kWarpsPerCta * 32, 0, s>>>(x, rows, alpha, beta, codes); break;
-        case 8: quantize_rows_d128<8><<<grid, kWarpsPerCta * 32, 0, s>>>(x, rows, alpha, beta, codes); break;
+        case 1: quantize_rows_d128<1><<<grid, kWarpsPerCta * 32, 0, s>>>(x, rows, alpha, beta, codes, word_bits); break;
+        case 2: quantize_rows_d128<2><<<grid, kWarpsPerCta * 32, 0, s>>>(x, rows, alpha, beta, codes, word_bits); break;
+        case 4: quantize_rows_d128<4><<<grid, kWarpsPerCta * 32, 0, s>>>(x, rows, alpha, beta, codes, word_bits); break;
+        case 8: quantize_rows_d128<8><<<grid, kWarpsPerCta * 32, 0, s>>>(x, rows, alpha, beta, codes, word_bits); break;
         default: return cudaErrorInvalidValue;
     }
     note_launch();

@@ -201,7 +201,8 @@ void quantize_prefill(kvq_cache* c, const float* dk, const float* dv, cudaStream
         float* alpha = which == 0 ? c->k_alpha() : c->v_alpha();
         float* beta = which == 0 ? c->k_beta() : c->v_beta();
         if (kvqb::quantize_fused_supported(n, d, c->word_bits, c->mode)) {
-            ck(kvqb::launch_quantize_fused(srcs[which], u, n, d, c->bits, c->mode, alpha, beta, codes, s), "quantize");
+            ck(kvqb::launch_quantize_fused(srcs[which], u, n, d, c->bits, c->word_bits, c->mode, alpha, beta, codes, s),
+               "quantize");
         } else {
             ck(kvqb::launch_compute_stats(srcs[which], u, n, d, c->mode, alpha, beta, s), "compute_stats");
             ck(kvqb::launch_quantize_pack(srcs[which], u, n, d, alpha, beta, c->bits, c->word_bits, codes, s),

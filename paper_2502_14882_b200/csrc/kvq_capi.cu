@@ -155,7 +155,8 @@ int kvq_quantize_device(const float* x, size_t mats, size_t rows, size_t dim, in
         require_device();
         cudaStream_t s = (cudaStream_t)stream;
         if (kvqb::quantize_fused_supported(rows, dim, word_bits, mode)) {
-            ck(kvqb::launch_quantize_fused(x, mats, rows, dim, bitwidth, mode, alpha, beta, codes, s), "quantize");
+            ck(kvqb::launch_quantize_fused(x, mats, rows, dim, bitwidth, word_bits, mode, alpha, beta, codes, s),
+               "quantize");
         } else {
             ck(kvqb::launch_compute_stats(x, mats, rows, dim, mode, alpha, beta, s), "compute_stats");
             ck(kvqb::launch_quantize_pack(x, mats, rows, dim, alpha, beta, bitwidth, word_bits, codes, s), "quantize");

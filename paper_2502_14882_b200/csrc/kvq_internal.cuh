@@ -39,8 +39,8 @@ cudaError_t launch_quantize_pack(const float* x, size_t mats, size_t rows, size_
 // K1 for the decode layout (d = 128, M = 8): stats kernel, then the warp-collective code
 // pass of k1_fused.cu (coalesced rows, ballot / shuffle packing).
 bool quantize_fused_supported(size_t rows, size_t dim, int word_bits, int mode);
-cudaError_t launch_quantize_fused(const float* x, size_t mats, size_t rows, size_t dim, int bits, int mode,
-                                  float* alpha, float* beta, uint8_t* codes, cudaStream_t s);
+cudaError_t launch_quantize_fused(const float* x, size_t mats, size_t rows, size_t dim, int bits, int word_bits,
+                                  int mode, float* alpha, float* beta, uint8_t* codes, cudaStream_t s);
 // Generic bit packing of explicit u32 codes (bitpack.hpp:161-187). err_flag set to 1 on
 // an out-of-range code.
 cudaError_t launch_pack_codes(const uint32_t* codes, size_t count, int bits, int word_bits,

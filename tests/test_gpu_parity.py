@@ -102,11 +102,12 @@ def test_quantize_hand_values(kvq):
 
 
 @pytest.mark.parametrize("bits", [1, 2, 4, 8])
-def test_quantize_device_matches_oracle_d128(kvq, oracle, bits):
-    """Batched device K1 (the cache build path, incl. the fused d = 128 kernel) is
-    bit-exact against the oracle on every unit."""
+@pytest.mark.parametrize("word_bits", [8, 16, 32])
+def test_quantize_device_matches_oracle_d128(kvq, oracle, bits, word_bits):
+    """Batched device K1 (the cache build path, incl. the fused d = 128 kernel for every
+    pack width) is bit-exact against the oracle on every unit."""
     import torch
-    rng = np.random.default_rng(bits)
+    rng = np.random.default_rng(bits + word_bits)
     mats, n, d = 6, 777, 128
     x = rng.normal(size=(mats, n, d)).astype(np.float32)
     x[0, :, 3] = 0.5  # degenerate channel
@@ -116,7 +117,7 @@ def test_quantize_device_matches_oracle_d128(kvq, oracle, bits):
     codes = torch.zeros(mats * n * rb, dtype=torch.uint8, device="cuda")
     alpha = torch.zeros(mats * d, dtype=torch.float32, device="cuda")
     beta = torch.zeros_like(alpha)
-    kvq._check(kvq.lib().kvq_quantize_device(xd.data_ptr(), mats, n, d, bits, 0, 8, codes.data_ptr(),
+    kvq._check(kvq.lib().kvq_quantize_device(xd.data_ptr(), mats, n, d, bits, 0, word_bits, codes.data_ptr(),
                                              alpha.data_ptr(), beta.data_ptr(), 0))
     torch.cuda.synchronize()
     codes, alpha, beta = codes.cpu().numpy().reshape(mats, -1), alpha.cpu().numpy().reshape(mats, d), \
@@ -124,7 +125,7 @@ def test_quantize_device_matches_oracle_d128(kvq, oracle, bits):
     for m in range(mats):
         a, b = oracle.compute_stats(x[m])
         assert bits_eq(alpha[m], a) and bits_eq(beta[m], b)
-        assert np.array_equal(codes[m], oracle.quantize(x[m], a, b, bits, 8)), f"unit {m}"
+        assert np.array_equal(codes[m], oracle.quantize(x[m], a, b, bits, word_bits)), f"unit {m}"
 
 
 # ---- standalone kernels.hpp / calibrate.hpp -------------------------------------------------
