@@ -160,6 +160,9 @@ struct kvq_cache {
     DevBuf<float> stats;     // [2 (K,V)][2 (alpha,beta)][units][dim]
     DevBuf<float> k_tail, v_tail;  // [units][tail_cap][dim]
     DevBuf<float> lse;             // [units][group] decode log-sum-exp for the tail pass
+    DevBuf<float> tail_part;       // [units][group][130] tail-pass partials (concurrent schedule)
+    cudaStream_t tstream = nullptr;  // the tail pass, concurrent with the decode
+    cudaEvent_t ev_tfork = nullptr, ev_tjoin = nullptr;
     DevBuf<int> tail_len;    // [batch]
     DevBuf<float> d_q, d_out, d_knew, d_vnew, scratch, weights;
     DevBuf<uint8_t> tc_scratch;  // prep-kernel outputs of the tcgen05 decode path
@@ -177,6 +180,9 @@ struct kvq_cache {
         if (side) cudaStreamDestroy(side);
         if (decoded) cudaEventDestroy(decoded);
         if (d2h) cudaStreamDestroy(d2h);
+        if (tstream) cudaStreamDestroy(tstream);
+        if (ev_tfork) cudaEventDestroy(ev_tfork);
+        if (ev_tjoin) cudaEventDestroy(ev_tjoin);
         for (cudaEvent_t e : ev_q) cudaEventDestroy(e);
         for (cudaEvent_t e : ev_dec) cudaEventDestroy(e);
         for (cudaStream_t x : chunk_streams) cudaStreamDestroy(x);

@@ -62,6 +62,8 @@ struct TailParams {
     const int* tail_len;    // [batch]
     const float* lse;       // [units][G] decode's base-2 log-sum-exp; nullptr: no quantized part
     float* out;             // [units][G][128]: the decode's output in, the merged output out
+    float* part;            // nullable: write (M, D, N[128]) per (unit, head) here instead of
+                            // merging (the concurrent schedule; tail_merge_kernel merges)
     size_t kv_heads, tail_cap;
     int G, S;
     float scale;            // log2(e) / sqrt(d)
@@ -266,6 +268,18 @@ __global__ void __launch_bounds__(kWarps * 32) tail_kernel(const TailParams p) {
     }
     if (S > 1) cluster_sync();  // remote shared memory stays valid until rank 0 has read it
     if (rank != 0) return;
+    if (p.part) {  // concurrent schedule: hand the partials to tail_merge_kernel
+#pragma unroll
+        for (int it = 0; it < kItems; ++it) {
+            const int idx = threadIdx.x + it * kWarps * 32;
+            const int h = idx / kDim, ch = idx % kDim;
+            if (h >= G) break;
+            float* rec = p.part + (unit * G + h) * (kDim + 2);
+            rec[2 + ch] = RN[it];
+            if (ch == 0) rec[0] = RM[it], rec[1] = RD[it];
+        }
+        return;
+    }
     griddep_wait();  // the decode's output and log-sum-exp are complete from here on
 #pragma unroll
     for (int it = 0; it < kItems; ++it) {
@@ -282,6 +296,27 @@ __global__ void __launch_bounds__(kWarps * 32) tail_kernel(const TailParams p) {
             const float wv = ex2(lv - X), wt = ex2(M - X);  // tail weight in total: D 2^(M - X)
             *o = __fmaf_rn(*o, wv, Nn * wt) / __fmaf_rn(D, wt, wv);
         }
+    }
+}
+
+// Concurrent schedule, last step: merge the tail pass's partials into the decode's output
+// (one thread per (unit, head, channel); the same log-sum-exp algebra as the in-pass merge).
+__global__ void __launch_bounds__(256) tail_merge_kernel(const float* __restrict__ part, const float* __restrict__ lse,
+                                                         float* __restrict__ out, size_t rows) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;  // (unit * G + h) * 128 + ch
+    if (i >= rows * kDim) return;
+    const size_t row = i / kDim, ch = i % kDim;
+    const float* rec = part + row * (kDim + 2);
+    const float M = rec[0];
+    if (M == -INFINITY) return;  // no tail rows: the decode's output stands
+    const float D = rec[1], Nn = rec[2 + ch];
+    const float lv = lse ? lse[row] : -INFINITY;
+    if (lv == -INFINITY) {
+        out[i] = Nn / D;
+    } else {
+        const float X = fmaxf(lv, M + __log2f(D));
+        const float wv = ex2(lv - X), wt = ex2(M - X);
+        out[i] = __fmaf_rn(out[i], wv, Nn * wt) / __fmaf_rn(D, wt, wv);
     }
 }
 
@@ -328,6 +363,32 @@ int tail_split(size_t units, size_t tail_cap) {
     const size_t want = (KVQ_TAIL_CTAS_PER_SM * 148 + units - 1) / units;
     size_t s = std::min<size_t>(want, (tail_cap + 63) / 64);
     return (int)std::max<size_t>(1, std::min<size_t>(s, kMaxCluster));
+}
+
+cudaError_t launch_decode_tail_partials(const DecodeArgs& a, float* part, cudaStream_t s) {
+    TailParams p{};
+    p.q = a.q;
+    p.k_tail = a.k_tail;
+    p.v_tail = a.v_tail;
+    p.tail_len = a.tail_len;
+    p.out = a.out;
+    p.part = part;
+    p.kv_heads = a.kv_heads;
+    p.tail_cap = a.tail_cap;
+    p.G = (int)a.group;
+    p.S = tail_split(a.units, a.tail_cap);
+    p.scale = kLog2e / sqrtf((float)kDim);
+    // every row's M starts at -inf: rows past a request's tail length are skipped by the merge
+    const cudaError_t e = a.group <= 4 ? launch_gp<4>(p, a.units, s, false) : launch_gp<8>(p, a.units, s, false);
+    note_launch();
+    return e;
+}
+
+cudaError_t launch_tail_merge(const DecodeArgs& a, const float* part, cudaStream_t s) {
+    const size_t rows = a.units * a.group;
+    tail_merge_kernel<<<(unsigned)((rows * kDim + 255) / 256), 256, 0, s>>>(part, a.tail_lse, a.out, rows);
+    note_launch();
+    return cudaGetLastError();
 }
 
 cudaError_t launch_decode_tail(const DecodeArgs& a, bool after_decode, cudaStream_t s) {

@@ -86,6 +86,15 @@ void traced(kvq_cache* c, kvqb::DecodeArgs& a, cudaStream_t s, F&& launch) {
 void ensure_vt(kvq_cache* c, cudaStream_t s);
 void ensure_vx(kvq_cache* c, cudaStream_t s);
 
+// Long tails: the tail pass chained behind the decode (programmatic dependent launch) is
+// the default; KVQ_TAIL_CONCURRENT=1 runs it on its own stream beside the decode with a
+// separate merge - measured 3-4 us slower per step (the decode's CTAs already fill the SMs,
+// profiles/r01_tail_concurrent.txt), kept as an option.
+static bool tail_concurrent() {
+    static const char* env = std::getenv("KVQ_TAIL_CONCURRENT");
+    return env ? std::atoi(env) != 0 : false;
+}
+
 void run_decode(kvq_cache* c, const float* q, float* out, bool want_weights, bool want_viol,
                 cudaStream_t s) {
     kvqb::DecodeArgs a = decode_args(c, q, out);
@@ -101,6 +110,7 @@ void run_decode(kvq_cache* c, const float* q, float* out, bool want_weights, boo
     // (k2_tail.cu), which streams them at HBM rate and merges by log-sum-exp.
     if (plain && c->tail_cap > kvqb::kTcTailMax && kvqb::decode_tail_supported(a)) {
         if (c->lse.n < c->units * c->group) c->lse.alloc(c->units * c->group);
+        if (c->tail_part.n < c->units * c->group * 130) c->tail_part.alloc(c->units * c->group * 130);
         a.tail_lse = c->lse.p;
     }
     bool tc_ok = kvqb::decode_tc_supported(a) && plain;
@@ -128,6 +138,18 @@ void run_decode(kvq_cache* c, const float* q, float* out, bool want_weights, boo
         return;
     }
     if ((c->path == KVQ_PATH_AUTO || c->path == KVQ_PATH_TC) && tc_ok) {
+        if (a.tail_lse && tail_concurrent()) {
+            // the HBM-bound tail pass runs beside the issue-bound decode (its own stream,
+            // partials to scratch), then one merge - instead of queueing behind it
+            ck(cudaEventRecord(c->ev_tfork, s), "event");
+            ck(cudaStreamWaitEvent(c->tstream, c->ev_tfork, 0), "event");
+            ck(kvqb::launch_decode_tail_partials(a, c->tail_part.p, c->tstream), "decode (tail)");
+            ck(cudaEventRecord(c->ev_tjoin, c->tstream), "event");
+            traced(c, a, s, [&] { ck(kvqb::launch_decode_tc(a, s), "decode (tc)"); });
+            ck(cudaStreamWaitEvent(s, c->ev_tjoin, 0), "event");
+            ck(kvqb::launch_tail_merge(a, c->tail_part.p, s), "decode (tail merge)");
+            return;
+        }
         traced(c, a, s, [&] { ck(kvqb::launch_decode_tc(a, s), "decode (tc)"); });
         if (a.tail_lse) ck(kvqb::launch_decode_tail(a, true, s), "decode (tail)");
         return;
@@ -179,6 +201,9 @@ kvq_cache* build_common(size_t batch, size_t kv_heads, size_t group, size_t n_vi
     ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
     ck(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking), "stream");
     ck(cudaEventCreateWithFlags(&c->decoded, cudaEventDisableTiming), "event");
+    ck(cudaStreamCreateWithFlags(&c->tstream, cudaStreamNonBlocking), "stream");
+    ck(cudaEventCreateWithFlags(&c->ev_tfork, cudaEventDisableTiming), "event");
+    ck(cudaEventCreateWithFlags(&c->ev_tjoin, cudaEventDisableTiming), "event");
     c->stats.alloc(4 * c->units * dim);
     ck(cudaMemsetAsync(c->stats.p, 0, sizeof(float) * c->stats.n, c->stream), "memset");
     c->codes.alloc(2 * c->units * c->n_vis * c->rb);

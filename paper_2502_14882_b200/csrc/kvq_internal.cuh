@@ -88,6 +88,10 @@ cudaError_t launch_decode_tc(const DecodeArgs& a, cudaStream_t s);
 // with the decode's output when `after_decode` (a.tail_lse set, launched right after it).
 bool decode_tail_supported(const DecodeArgs& a);
 cudaError_t launch_decode_tail(const DecodeArgs& a, bool after_decode, cudaStream_t s);
+// Concurrent schedule: the tail pass writes (M, D, N[128]) per (unit, head) to `part`
+// ([units][G][130]) on its own stream while the decode runs; launch_tail_merge combines.
+cudaError_t launch_decode_tail_partials(const DecodeArgs& a, float* part, cudaStream_t s);
+cudaError_t launch_tail_merge(const DecodeArgs& a, const float* part, cudaStream_t s);
 #ifndef KVQ_TC_TAIL_MAX
 #define KVQ_TC_TAIL_MAX 64
 #endif
