@@ -86,11 +86,23 @@ class ClockSampler:
         try:
             import pynvml
             pynvml.nvmlInit()
-            self.nv, self.h = pynvml, pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.nv, self.h = pynvml, self._handle(pynvml, index)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
         except Exception:
             self.nv = None
             self.max_mhz = None
+
+    @staticmethod
+    def _handle(pynvml, index: int):
+        """NVML handle of CUDA device `index`: by PCI address (CUDA and NVML may enumerate
+        differently, e.g. under CUDA_VISIBLE_DEVICES), else by index."""
+        try:
+            import torch
+            pr = torch.cuda.get_device_properties(index)
+            bus = "%08x:%02x:%02x.0" % (pr.pci_domain_id, pr.pci_bus_id, pr.pci_device_id)
+            return pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode())
+        except Exception:
+            return pynvml.nvmlDeviceGetHandleByIndex(index)
 
     def _sample(self):
         self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
