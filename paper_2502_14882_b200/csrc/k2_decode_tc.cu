@@ -312,7 +312,11 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
     const float k_a = __ldg(a.k_alpha + unit * kDim + (threadIdx.x & (kDim - 1)));   // prologue channel
     const float k_b = __ldg(a.k_beta + unit * kDim + (threadIdx.x & (kDim - 1)));
     if (threadIdx.x == 0) TTRACE(7);
-    griddep_wait();  // the previous step's append (tail rows, tail_len) and q are visible from here on
+    // The previous step's append (tail rows, tail_len) and q are visible from here on. A
+    // balancing sibling launch (dep_wait_at_end) starts only once every CTA of the first
+    // launch has passed this wait, so it may skip it; it waits at exit instead, keeping
+    // "this grid done" = "both launches done" for the kernel that follows.
+    if (!a.dep_wait_at_end) griddep_wait();
     const int ntl = own_tail ? __ldcg(a.tail_len + unit / a.kv_heads) : 0;
     // Dependents (the tail pass, or the append) may launch now: this grid is fully resident
     // once every CTA has passed here, and they wait for its completion before writing.
@@ -844,6 +848,7 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(kTmemCols));
     }
+    if (a.dep_wait_at_end) griddep_wait();
 }
 
 // Token split: at most 8192 (NT = 1) / 4096 tokens per CTA; small batches split units further (down to
@@ -862,6 +867,7 @@ void plan(const DecodeArgs& a, int NT, int& S, int& T, int W = kWarps) {
     int s = std::max(s_min, std::min(want, kMaxCluster));
     static const int force = std::getenv("KVQ_TC_SPLIT") ? std::atoi(std::getenv("KVQ_TC_SPLIT")) : 0;  // tuning
     if (force > 0) s = std::max(s_min, std::min(force, kMaxCluster));
+    if (a.split_override > 0) s = std::max(s_min, std::min(a.split_override, kMaxCluster));
     s = std::min(s, std::max(1, (n + 255) / 256));
     T = ((n + s - 1) / s + 255) / 256 * 256;  // multiple of 8 warps x 32 tokens (and of 4 x 32)
     S = (n + T - 1) / T;
@@ -1070,8 +1076,53 @@ bool decode_tc_supported(const DecodeArgs& a) {
     return smem <= 220 * 1024;
 }
 
+// Units [u0, u1) of `a` (every per-unit array is unit-major; u0 on a request boundary).
+static DecodeArgs unit_range(const DecodeArgs& a, size_t u0, size_t u1) {
+    DecodeArgs r = a;
+    const size_t rb = row_bytes(a.dim, a.bits, a.word_bits), d = a.dim, G = a.group;
+    r.k_codes += u0 * a.n_vis * rb;
+    r.v_codes += u0 * a.n_vis * rb;
+    if (r.v_codes_x) r.v_codes_x += vx_bytes(u0, a.n_vis, a.bits);
+    r.k_alpha += u0 * d, r.k_beta += u0 * d, r.v_alpha += u0 * d, r.v_beta += u0 * d;
+    r.k_tail += u0 * a.tail_cap * d, r.v_tail += u0 * a.tail_cap * d;
+    r.tail_len += u0 / a.kv_heads;
+    r.q += u0 * G * d, r.out += u0 * G * d;
+    if (r.tail_lse) r.tail_lse += u0 * G;
+    r.units = u1 - u0;
+    return r;
+}
+
+static cudaError_t launch_nt(const DecodeArgs& a, int NT, cudaStream_t s);
+
+// 4-warp CTAs, more than three but at most four units per SM: SMs holding four whole units
+// set the makespan while others hold three. The units beyond three per SM are instead cut
+// in halves (2-CTA clusters) and launched right behind (programmatic dependent launch),
+// filling the free fourth slots: every SM then carries at most 3.5 units of work.
+static bool balance_w4(const DecodeArgs& a) {
+    static const char* env = std::getenv("KVQ_TC_BALANCE");
+    if (env && std::atoi(env) == 0) return false;
+    const bool whole = a.plan_units == 0 || a.plan_units == a.units;
+    return whole && a.group <= 4 && !a.split_override && a.units > 3 * 148 && a.units <= 4 * 148 &&
+           a.n_vis >= 2 * 256 && tc_w4(a);
+}
+
 cudaError_t launch_decode_tc(const DecodeArgs& a, cudaStream_t s) {
-    const int NT = tc_nt(a);
+    if (balance_w4(a)) {
+        size_t nsplit = a.units - 3 * 148;
+        nsplit = (nsplit + a.kv_heads - 1) / a.kv_heads * a.kv_heads;  // whole requests
+        const size_t u1 = a.units - nsplit;
+        DecodeArgs A = unit_range(a, 0, u1), B = unit_range(a, u1, a.units);
+        A.plan_units = B.plan_units = a.units;  // same CTA shape for both
+        B.split_override = 2;
+        B.dep_wait_at_end = 1;
+        cudaError_t e = launch_nt(A, 1, s);
+        if (e != cudaSuccess) return e;
+        return launch_nt(B, 1, s);
+    }
+    return launch_nt(a, tc_nt(a), s);
+}
+
+static cudaError_t launch_nt(const DecodeArgs& a, int NT, cudaStream_t s) {
     switch (a.bits * 10 + NT) {
         case 11: return launch_bits<1, 1>(a, s);
         case 12: return launch_bits<1, 2>(a, s);

@@ -704,12 +704,15 @@ def test_randomized_paths_vs_oracle(kvq, oracle, case):
         assert rel_l2(out, want) <= tol, (path, rel_l2(out, want))
 
 
-@pytest.mark.parametrize("bits,G,n,tail", [(1, 4, 300, 0), (2, 2, 1100, 70), (4, 6, 64, 5)])
-def test_many_units_four_warp_ctas(kvq, oracle, bits, G, n, tail):
-    """More than 296 units of n <= 4096 tokens select 4-warp CTAs (four per SM): checked
-    against the C restatement on a spread of units, plus determinism."""
+@pytest.mark.parametrize("bits,G,n,tail,B", [(1, 4, 300, 0, 40), (2, 2, 1100, 70, 40), (4, 6, 64, 5, 40),
+                                             (1, 4, 700, 3, 64), (2, 3, 1024, 80, 64)])
+def test_many_units_four_warp_ctas(kvq, oracle, bits, G, n, tail, B):
+    """More than 296 units of n <= 4096 tokens select 4-warp CTAs (four per SM); 512 units
+    also take the balanced launch (the units beyond three per SM as 2-CTA clusters behind
+    the first grid): checked against the C restatement on a spread of units (both launches),
+    plus determinism."""
     rng = np.random.default_rng(bits * 1000 + n)
-    B, H, d = 40, 8, 128  # 320 units
+    H, d = 8, 128
     k = rng.normal(size=(B, H, n, d)).astype(np.float32)
     v = rng.normal(size=(B, H, n, d)).astype(np.float32)
     tau = (1.0, 0.0)
@@ -725,7 +728,7 @@ def test_many_units_four_warp_ctas(kvq, oracle, bits, G, n, tail):
     out, _, _ = cache.decode(q)
     again, _, _ = cache.decode(q)
     assert np.array_equal(out, again)
-    for b, h in [(0, 0), (7, 3), (19, 7), (39, 5)]:
+    for b, h in [(0, 0), (7, 3), (19, 7), (39, 5), (B - 1, 7), (B - 4, 2)]:
         ka, kb = oracle.compute_stats(k[b, h])
         va, vb = oracle.compute_stats(v[b, h])
         kc, vc = oracle.quantize(k[b, h], ka, kb, bits), oracle.quantize(v[b, h], va, vb, bits)
