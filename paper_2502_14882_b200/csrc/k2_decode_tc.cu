@@ -1094,22 +1094,27 @@ static DecodeArgs unit_range(const DecodeArgs& a, size_t u0, size_t u1) {
 
 static cudaError_t launch_nt(const DecodeArgs& a, int NT, cudaStream_t s);
 
-// 4-warp CTAs, more than three but at most four units per SM: SMs holding four whole units
-// set the makespan while others hold three. The units beyond three per SM are instead cut
-// in halves (2-CTA clusters) and launched right behind (programmatic dependent launch),
-// filling the free fourth slots: every SM then carries at most 3.5 units of work.
-static bool balance_w4(const DecodeArgs& a) {
+// 4-warp CTAs (four slots per SM) with k whole units per SM plus a remainder r: the SMs
+// holding k + 1 whole units set the makespan. The r remainder units are instead cut in
+// halves (2-CTA clusters) and launched right behind (programmatic dependent launch) into
+// the free slots, when they fit (148 k + 2 r <= 592): every SM carries at most k + 1/2.
+static size_t balance_w4(const DecodeArgs& a) {
     static const char* env = std::getenv("KVQ_TC_BALANCE");
-    if (env && std::atoi(env) == 0) return false;
+    if (env && std::atoi(env) == 0) return 0;
     const bool whole = a.plan_units == 0 || a.plan_units == a.units;
-    return whole && a.group <= 4 && !a.split_override && a.units > 3 * 148 && a.units <= 4 * 148 &&
-           a.n_vis >= 2 * 256 && tc_w4(a);
+    if (!whole || a.group > 4 || a.split_override || a.n_vis < 2 * 256 || !tc_w4(a)) return 0;
+    const size_t k = a.units / 148;
+    size_t r = a.units - 148 * k;
+    r = (r + a.kv_heads - 1) / a.kv_heads * a.kv_heads;  // whole requests
+    // measured (profiles/r01_tc_balance.txt): a gain while the remainder is at most half an
+    // SM row (r <= 74: 320 units 40.6 -> 38.4 us, 512 units 48.1 -> 45.2 us), a loss beyond
+    // (384 and 432 units), where the extra launch and cluster merges outweigh the rebalance
+    if (k < 2 || r == 0 || 2 * r > 148 || 148 * k + 2 * r > 4 * 148) return 0;
+    return r;
 }
 
 cudaError_t launch_decode_tc(const DecodeArgs& a, cudaStream_t s) {
-    if (balance_w4(a)) {
-        size_t nsplit = a.units - 3 * 148;
-        nsplit = (nsplit + a.kv_heads - 1) / a.kv_heads * a.kv_heads;  // whole requests
+    if (const size_t nsplit = balance_w4(a)) {
         const size_t u1 = a.units - nsplit;
         DecodeArgs A = unit_range(a, 0, u1), B = unit_range(a, u1, a.units);
         A.plan_units = B.plan_units = a.units;  // same CTA shape for both
