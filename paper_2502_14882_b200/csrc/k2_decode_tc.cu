@@ -1098,13 +1098,15 @@ static cudaError_t launch_nt(const DecodeArgs& a, int NT, cudaStream_t s);
 // holding k + 1 whole units set the makespan. The r remainder units are instead cut in
 // halves (2-CTA clusters) and launched right behind (programmatic dependent launch) into
 // the free slots, when they fit (148 k + 2 r <= 592): every SM carries at most k + 1/2.
+// Returns how many of the batch's last units are split (0: no balancing). Decided on the
+// whole batch (plan_units), so chunked launches split exactly the same units.
 static size_t balance_w4(const DecodeArgs& a) {
     static const char* env = std::getenv("KVQ_TC_BALANCE");
     if (env && std::atoi(env) == 0) return 0;
-    const bool whole = a.plan_units == 0 || a.plan_units == a.units;
-    if (!whole || a.group > 4 || a.split_override || a.n_vis < 2 * 256 || !tc_w4(a)) return 0;
-    const size_t k = a.units / 148;
-    size_t r = a.units - 148 * k;
+    const size_t units = a.plan_units ? a.plan_units : a.units;
+    if (a.group > 4 || a.split_override || a.n_vis < 2 * 256 || !tc_w4(a)) return 0;
+    const size_t k = units / 148;
+    size_t r = units - 148 * k;
     r = (r + a.kv_heads - 1) / a.kv_heads * a.kv_heads;  // whole requests
     // measured (profiles/r01_tc_balance.txt): a gain while the remainder is at most half an
     // SM row (r <= 74: 320 units 40.6 -> 38.4 us, 512 units 48.1 -> 45.2 us), a loss beyond
@@ -1115,13 +1117,19 @@ static size_t balance_w4(const DecodeArgs& a) {
 
 cudaError_t launch_decode_tc(const DecodeArgs& a, cudaStream_t s) {
     if (const size_t nsplit = balance_w4(a)) {
-        const size_t u1 = a.units - nsplit;
-        DecodeArgs A = unit_range(a, 0, u1), B = unit_range(a, u1, a.units);
-        A.plan_units = B.plan_units = a.units;  // same CTA shape for both
+        const size_t total = a.plan_units ? a.plan_units : a.units;
+        // this launch covers batch units [unit_base, unit_base + units); split from `first`
+        const size_t first = total - nsplit;
+        const size_t cut = first <= a.unit_base ? 0 : std::min(a.units, first - a.unit_base);
+        DecodeArgs A = unit_range(a, 0, cut), B = unit_range(a, cut, a.units);
+        A.plan_units = B.plan_units = total;  // same CTA shape for both
+        B.unit_base = a.unit_base + cut;
         B.split_override = 2;
-        B.dep_wait_at_end = 1;
-        cudaError_t e = launch_nt(A, 1, s);
-        if (e != cudaSuccess) return e;
+        if (cut > 0) {
+            cudaError_t e = launch_nt(A, 1, s);
+            if (e != cudaSuccess || cut == a.units) return e;
+            B.dep_wait_at_end = 1;  // launched behind A (see the kernel's dependency wait)
+        }
         return launch_nt(B, 1, s);
     }
     return launch_nt(a, tc_nt(a), s);

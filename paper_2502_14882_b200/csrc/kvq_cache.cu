@@ -292,6 +292,7 @@ kvqb::DecodeArgs range_args(const kvqb::DecodeArgs& a, const kvq_cache* c, size_
     if (r.tail_lse) r.tail_lse += u0 * G;
     r.units = (b1 - b0) * c->kv_heads;
     r.plan_units = c->units;  // chunked results are bit-identical to the whole-batch decode
+    r.unit_base = u0;
     return r;
 }
 

@@ -77,6 +77,7 @@ struct DecodeArgs {
     size_t units, kv_heads, group, dim, n_vis, tail_cap, weights_stride;
     size_t plan_units;    // 0, or the whole batch's units when `units` is one chunk of it: the
                           // split (and so the summation order) is the whole batch's
+    size_t unit_base;     // first unit of this launch within the plan_units batch (chunks)
     int split_override;   // tensor-core decode: force this cluster size (0 = plan)
     int dep_wait_at_end;  // tensor-core decode launched behind a sibling grid: skip the early
                           // dependency wait (the sibling did it), wait at exit instead

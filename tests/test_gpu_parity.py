@@ -376,12 +376,13 @@ def test_batched_gqa_vs_oracle(kvq, oracle, bits, G, n):
         tv.append(vn)
 
 
-@pytest.mark.parametrize("B", [3, 40])
-def test_step_api_matches_decode_then_append(kvq, B):
-    """kvq_cache_step == decode + append, bit for bit; B = 40 takes the pipelined step
-    (request chunks: upload / decode / download overlapped on three streams)."""
+@pytest.mark.parametrize("B,H,n", [(3, 2, 200), (40, 2, 200), (64, 8, 600)])
+def test_step_api_matches_decode_then_append(kvq, B, H, n):
+    """kvq_cache_step == decode + append, bit for bit; B >= 32 takes the pipelined step
+    (request chunks: upload / decode / download overlapped on three streams); 512 units
+    also take the balanced 4-warp launch, whose split units the chunks must reproduce."""
     rng = np.random.default_rng(12)
-    H, G, n, d = 2, 4, 200, 128
+    G, d = 4, 128
     k = rng.normal(size=(B, H, n, d)).astype(np.float32)
     v = rng.normal(size=(B, H, n, d)).astype(np.float32)
     c1 = kvq.BatchedCache.build(k, v, kvq.QuantizationConfig(1), kvq.CalibrationParams(1, 0), group=G)
