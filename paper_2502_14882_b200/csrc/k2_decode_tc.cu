@@ -1115,6 +1115,9 @@ static size_t balance_w4(const DecodeArgs& a) {
     return r;
 }
 
+// (Tried and dropped: the analogous mixed launch for 8-warp batches of 149-296 units -
+// 8-warp whole units plus 4-warp half-unit clusters sharing SMs - was 5-18 % slower,
+// profiles/r01_tc_balance.txt.)
 cudaError_t launch_decode_tc(const DecodeArgs& a, cudaStream_t s) {
     if (const size_t nsplit = balance_w4(a)) {
         const size_t total = a.plan_units ? a.plan_units : a.units;
