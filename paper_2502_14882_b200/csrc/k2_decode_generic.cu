@@ -84,7 +84,17 @@ decode_generic_kernel(DecodeArgs a) {
     for (size_t j = threadIdx.x; j < n; j += blockDim.x) {
         const uint8_t* r = kc + j * rb;
         float acc = 0.0f;
-        for (size_t c = 0; c < d; ++c) acc = __fmaf_rn(qs[c], code(r, c), acc);
+        if ((rb & 3) == 0 && a.bits <= 8) {  // 32-bit row words: one load per word, codes in order
+            const uint32_t* r32 = reinterpret_cast<const uint32_t*>(r);
+            uint32_t w = 0, cur = 0xffffffffu;
+            for (size_t c = 0; c < d; ++c) {
+                const uint32_t wi = cbyte[c] >> 2;
+                if (wi != cur) w = __ldg(r32 + wi), cur = wi;
+                acc = __fmaf_rn(qs[c], (float)((w >> (8 * (cbyte[c] & 3) + cshift[c])) & cmask), acc);
+            }
+        } else {
+            for (size_t c = 0; c < d; ++c) acc = __fmaf_rn(qs[c], code(r, c), acc);
+        }
         float s = __fmul_rn(__fadd_rn(acc, qdota), inv_sqrt_d);
         row[j] = s;
         lo = fminf(lo, s);
@@ -199,8 +209,18 @@ __global__ void qk_scores_kernel(const float* __restrict__ q, const uint8_t* __r
          j += (size_t)gridDim.x * blockDim.x) {
         const uint8_t* r = seg + j * rb;
         float acc = 0.0f;
-        for (size_t c = 0; c < dim; ++c)
-            acc = __fmaf_rn(qs[c], (float)code_load(r, cbyte[c], cshift[c], bits, cmask), acc);
+        if ((rb & 3) == 0) {  // 32-bit row words: one load per word, codes in channel order
+            const uint32_t* r32 = reinterpret_cast<const uint32_t*>(r);
+            uint32_t w = 0, cur = 0xffffffffu;
+            for (size_t c = 0; c < dim; ++c) {
+                const uint32_t wi = cbyte[c] >> 2;
+                if (wi != cur) w = __ldg(r32 + wi), cur = wi;
+                acc = __fmaf_rn(qs[c], (float)((w >> (8 * (cbyte[c] & 3) + cshift[c])) & cmask), acc);
+            }
+        } else {
+            for (size_t c = 0; c < dim; ++c)
+                acc = __fmaf_rn(qs[c], (float)code_load(r, cbyte[c], cshift[c], bits, cmask), acc);
+        }
         scores[h * tokens + j] = __fadd_rn(acc, qdota);
     }
 }
