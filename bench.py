@@ -55,7 +55,7 @@ CONFIGS = {
     "c5b512": (512, 8, 4, 4096, 1, (1.0, 0.0), "BASELINE c5: batch 512, 4096 visual tokens, 1-bit"),
 }
 DIM = 128
-PATHS = {"auto": 0, "generic": 1, "tc": 2, "umma": 3}  # KVQ_PATH_* (include/kvq_capi.h)
+PATHS = {"auto": 0, "generic": 1, "tc": 2, "umma": 3, "hc": 4, "ws": 5}  # KVQ_PATH_* (include/kvq_capi.h)
 TAIL_WINDOW = 32
 L2_BYTES = 126 * 1024 * 1024
 

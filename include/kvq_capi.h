@@ -41,10 +41,12 @@ extern "C" {
 #define KVQ_MODE_GLOBAL 1       /* QuantMode::global */
 #define KVQ_FULL_PRECISION_BITS 16 /* kvcache.hpp:26 */
 
-#define KVQ_PATH_AUTO 0    /* IMMA path when the shape allows, else tcgen05, else generic */
+#define KVQ_PATH_AUTO 0    /* per-CTA IMMA path when the shape allows, else tcgen05, else generic */
 #define KVQ_PATH_GENERIC 1 /* any shape; also the path that emits probability rows */
 #define KVQ_PATH_TC 2      /* d = 128, M = 8 legacy mma.sync IMMA path (KVQ_ERR_CONFIG otherwise) */
 #define KVQ_PATH_UMMA 3    /* d = 128, M = 8 tcgen05 UTCIMMA path (KVQ_ERR_CONFIG otherwise) */
+#define KVQ_PATH_HC 4      /* d = 128, b <= 4, G <= 4 8-warp channel-split IMMA path (KVQ_ERR_CONFIG otherwise) */
+#define KVQ_PATH_WS 5      /* d = 128, b <= 4, G <= 4, n <= 8192, >= 296 units: persistent warp-specialized IMMA path */
 
 /* ---- diagnostics ------------------------------------------------------------ */
 /* Copies the calling thread's last error message (NUL-terminated, truncated to cap);

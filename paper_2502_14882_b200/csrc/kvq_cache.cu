@@ -85,6 +85,7 @@ void traced(kvq_cache* c, kvqb::DecodeArgs& a, cudaStream_t s, F&& launch) {
 
 void ensure_vt(kvq_cache* c, cudaStream_t s);
 void ensure_vx(kvq_cache* c, cudaStream_t s);
+void ensure_vx2(kvq_cache* c, cudaStream_t s);
 
 // Long tails: the tail pass chained behind the decode (programmatic dependent launch) is
 // the default; KVQ_TAIL_CONCURRENT=1 runs it on its own stream beside the decode with a
@@ -95,14 +96,63 @@ static bool tail_concurrent() {
     return env ? std::atoi(env) != 0 : false;
 }
 
+// The tensor-core decode kernel a plain decode of this cache runs: KVQ_PATH_TC (the per-CTA
+// IMMA kernel, k2_decode_tc.cu), KVQ_PATH_WS (persistent warp-specialized, k2_decode_ws.cu),
+// KVQ_PATH_HC (8-warp channel-split, k2_decode_hc.cu), or -1 (none applies). Builds the V
+// operand layout the chosen kernel reads (vx / vx2) on first use.
+int pick_tensor_decode(kvq_cache* c, kvqb::DecodeArgs& a, cudaStream_t s) {
+    // AUTO runs the per-CTA IMMA kernel: the ws and hc kernels are correct but measured
+    // slower at every BASELINE shape (profiles/r02_ws_trace_c2.txt, r02_hc_*), so they are
+    // selected explicitly only.
+    if (c->path == KVQ_PATH_WS) {
+        kvqb::DecodeArgs probe = a;
+        probe.v_codes_x = reinterpret_cast<const uint8_t*>(1);  // shape check only
+        if (kvqb::decode_ws_supported(probe)) {
+            ensure_vx(c, s);
+            a.v_codes_x = c->vx.p;
+            const size_t need = kvqb::decode_ws_scratch_bytes(c->units);
+            if (c->tc_scratch.n < need) c->tc_scratch.alloc(need);
+            a.q_frag = reinterpret_cast<uint32_t*>(c->tc_scratch.p);
+            a.q_const = reinterpret_cast<float2*>(c->tc_scratch.p + c->units * 512 * sizeof(uint32_t));
+            return KVQ_PATH_WS;
+        }
+        if (c->path == KVQ_PATH_WS)
+            raise(KVQ_ERR_CONFIG, "ws decode path needs dim 128, 1/2/4-bit codes, at most 4 query heads per KV "
+                                  "head, n <= 8192, >= 296 units, a quantized prefill and no weight/violation export");
+    }
+    if (c->path == KVQ_PATH_HC) {
+        kvqb::DecodeArgs probe = a;
+        probe.v_codes_x2 = reinterpret_cast<const uint8_t*>(1);
+        if (kvqb::decode_hc_supported(probe)) {
+            ensure_vx2(c, s);
+            a.v_codes_x2 = c->vx2.p;
+            return KVQ_PATH_HC;
+        }
+        raise(KVQ_ERR_CONFIG, "hc decode path needs dim 128, 1/2/4-bit codes, at most 4 query heads per KV "
+                              "head, a quantized prefill and no weight/violation export");
+    }
+    if (c->path == KVQ_PATH_AUTO || c->path == KVQ_PATH_TC) {
+        kvqb::DecodeArgs probe = a;
+        probe.v_codes_x = reinterpret_cast<const uint8_t*>(1);
+        if (kvqb::decode_tc_supported(probe)) {
+            ensure_vx(c, s);
+            a.v_codes_x = c->vx.p;
+            return KVQ_PATH_TC;
+        }
+    }
+    return -1;
+}
+
+void launch_tensor_decode(int kind, const kvqb::DecodeArgs& a, cudaStream_t s) {
+    if (kind == KVQ_PATH_WS) ck(kvqb::launch_decode_ws(a, s), "decode (ws)");
+    else if (kind == KVQ_PATH_HC) ck(kvqb::launch_decode_hc(a, s), "decode (hc)");
+    else ck(kvqb::launch_decode_tc(a, s), "decode (tc)");
+}
+
 void run_decode(kvq_cache* c, const float* q, float* out, bool want_weights, bool want_viol,
                 cudaStream_t s) {
     kvqb::DecodeArgs a = decode_args(c, q, out);
     const bool plain = !want_weights && !want_viol;
-    if (plain && c->path != KVQ_PATH_GENERIC && c->path != KVQ_PATH_UMMA) {
-        ensure_vx(c, s);
-        a.v_codes_x = c->vx.p;
-    }
     kvqb::DecodeArgs probe = a;
     probe.v_codes_t = reinterpret_cast<const uint8_t*>(1);  // shape check only
     const bool umma_ok = plain && c->dim == 128 && c->word_bits == 8 && kvqb::decode_umma_supported(probe);
@@ -113,19 +163,21 @@ void run_decode(kvq_cache* c, const float* q, float* out, bool want_weights, boo
         if (c->tail_part.n < c->units * c->group * 130) c->tail_part.alloc(c->units * c->group * 130);
         a.tail_lse = c->lse.p;
     }
-    bool tc_ok = kvqb::decode_tc_supported(a) && plain;
+    const int tc_kind = plain && c->path != KVQ_PATH_GENERIC && c->path != KVQ_PATH_UMMA ? pick_tensor_decode(c, a, s)
+                                                                                        : -1;
     // Probability-row / violation export (decode_step_detailed) is a generic-path feature:
     // an explicit tensor-core path selection applies to plain decodes only.
     if (c->path == KVQ_PATH_UMMA && !umma_ok && plain)
         raise(KVQ_ERR_CONFIG, "tcgen05 decode path needs dim 128, 8-bit words, a quantized "
                               "prefill and no weight/violation export");
-    if (c->path == KVQ_PATH_TC && !tc_ok && plain)
+    if (c->path == KVQ_PATH_TC && tc_kind < 0 && plain)
         raise(KVQ_ERR_CONFIG, "tensor-core decode path needs dim 128, 8-bit words, a quantized "
                               "prefill and no weight/violation export");
-    // AUTO prefers the mma.sync IMMA kernel: for this problem's N = G x digit planes = 16
-    // it out-runs tcgen05 (a kind::i8 UTCIMMA costs ~100 cycles for any N <= 128,
-    // profiles/r01_umma_rate.txt). The tcgen05 path remains selectable (KVQ_PATH_UMMA).
-    if ((c->path == KVQ_PATH_UMMA || (c->path == KVQ_PATH_AUTO && !tc_ok)) && umma_ok) {
+    // AUTO prefers the mma.sync IMMA kernels: for this problem's N = G x digit planes = 16 a
+    // tcgen05 MMA costs 35-47 cycles (profiles/r02_umma_rate2.txt) on the same tensor
+    // datapath (r02_mma_mix.txt). The tcgen05 path remains selectable (KVQ_PATH_UMMA).
+    if ((c->path == KVQ_PATH_UMMA || (c->path == KVQ_PATH_AUTO && tc_kind < 0)) && umma_ok) {
+        ensure_vx(c, s);
         ensure_vt(c, s);
         a.v_codes_t = c->vt.p;
         a.v_codes_x = c->vx.p;
@@ -137,7 +189,7 @@ void run_decode(kvq_cache* c, const float* q, float* out, bool want_weights, boo
         traced(c, a, s, [&] { ck(kvqb::launch_decode_umma(a, s), "decode (umma)"); });
         return;
     }
-    if ((c->path == KVQ_PATH_AUTO || c->path == KVQ_PATH_TC) && tc_ok) {
+    if (tc_kind >= 0) {
         if (a.tail_lse && tail_concurrent()) {
             // the HBM-bound tail pass runs beside the issue-bound decode (its own stream,
             // partials to scratch), then one merge - instead of queueing behind it
@@ -145,12 +197,12 @@ void run_decode(kvq_cache* c, const float* q, float* out, bool want_weights, boo
             ck(cudaStreamWaitEvent(c->tstream, c->ev_tfork, 0), "event");
             ck(kvqb::launch_decode_tail_partials(a, c->tail_part.p, c->tstream), "decode (tail)");
             ck(cudaEventRecord(c->ev_tjoin, c->tstream), "event");
-            traced(c, a, s, [&] { ck(kvqb::launch_decode_tc(a, s), "decode (tc)"); });
+            traced(c, a, s, [&] { launch_tensor_decode(tc_kind, a, s); });
             ck(cudaStreamWaitEvent(s, c->ev_tjoin, 0), "event");
             ck(kvqb::launch_tail_merge(a, c->tail_part.p, s), "decode (tail merge)");
             return;
         }
-        traced(c, a, s, [&] { ck(kvqb::launch_decode_tc(a, s), "decode (tc)"); });
+        traced(c, a, s, [&] { launch_tensor_decode(tc_kind, a, s); });
         if (a.tail_lse) ck(kvqb::launch_decode_tail(a, true, s), "decode (tail)");
         return;
     }
@@ -244,6 +296,12 @@ void ensure_vx(kvq_cache* c, cudaStream_t s) {
     ck(kvqb::launch_pack_vx(c->v_codes(), c->units, c->n_vis, c->bits, c->word_bits, c->vx.p, s), "pack vx");
 }
 
+void ensure_vx2(kvq_cache* c, cudaStream_t s) {
+    if (c->vx2.p || c->dim != 128 || c->n_vis == 0 || c->bits == KVQ_FULL_PRECISION_BITS) return;
+    c->vx2.alloc(kvqb::vx2_bytes(c->units, c->n_vis, c->bits));
+    ck(kvqb::launch_pack_vx2(c->v_codes(), c->units, c->n_vis, c->bits, c->word_bits, c->vx2.p, s), "pack vx2");
+}
+
 void ensure_vt(kvq_cache* c, cudaStream_t s) {
     if (c->vt.p || c->dim != 128 || c->word_bits != 8 || c->n_vis == 0) return;
     c->vt.alloc(kvqb::vt_bytes(c->units, c->n_vis, c->bits));
@@ -280,6 +338,7 @@ kvqb::DecodeArgs range_args(const kvqb::DecodeArgs& a, const kvq_cache* c, size_
     r.k_codes += u0 * c->n_vis * c->rb;
     r.v_codes += u0 * c->n_vis * c->rb;
     if (r.v_codes_x) r.v_codes_x += kvqb::vx_bytes(u0, c->n_vis, c->bits);
+    if (r.v_codes_x2) r.v_codes_x2 += kvqb::vx2_bytes(u0, c->n_vis, c->bits);
     r.k_alpha += u0 * d;
     r.k_beta += u0 * d;
     r.v_alpha += u0 * d;
@@ -306,13 +365,11 @@ size_t step_chunks_for(kvq_cache* c) {
     size_t chunks = step_chunks(c);
     if (chunks <= 1 || c->path == KVQ_PATH_GENERIC || c->path == KVQ_PATH_UMMA) return 1;
     kvqb::DecodeArgs a = decode_args(c, c->d_q.p, c->d_out.p);
-    ensure_vx(c, c->stream);
-    a.v_codes_x = c->vx.p;
     if (c->tail_cap > kvqb::kTcTailMax && kvqb::decode_tail_supported(a)) {
         if (c->lse.n < c->units * c->group) c->lse.alloc(c->units * c->group);
         a.tail_lse = c->lse.p;
     }
-    return kvqb::decode_tc_supported(a) ? chunks : 1;
+    return pick_tensor_decode(c, a, c->stream) >= 0 ? chunks : 1;
 }
 
 // Streams and events of the host-buffer step, created before any graph capture.
@@ -367,13 +424,13 @@ void issue_step(kvq_cache* c, const float* queries, const float* k_new, const fl
         ck(cudaEventRecord(c->ev_dec[0], s), "event");
     } else {
         kvqb::DecodeArgs a = decode_args(c, c->d_q.p, c->d_out.p);
-        a.v_codes_x = c->vx.p;
         if (c->tail_cap > kvqb::kTcTailMax && kvqb::decode_tail_supported(a)) a.tail_lse = c->lse.p;
+        const int kind = pick_tensor_decode(c, a, s);
         for (size_t i = 0; i < chunks; ++i) {
             cudaStream_t cs = c->chunk_streams[i];
             ck(cudaStreamWaitEvent(cs, c->ev_q[i], 0), "event");
             const kvqb::DecodeArgs r = range_args(a, c, bounds(i), bounds(i + 1));
-            ck(kvqb::launch_decode_tc(r, cs), "decode (tc)");
+            launch_tensor_decode(kind, r, cs);
             if (r.tail_lse) ck(kvqb::launch_decode_tail(r, true, cs), "decode (tail)");
             ck(cudaEventRecord(c->ev_dec[i], cs), "event");
             ck(cudaStreamWaitEvent(s, c->ev_dec[i], 0), "event");
@@ -501,7 +558,7 @@ int kvq_cache_reserve_tail(kvq_cache* c, size_t rows) {
 
 int kvq_cache_set_path(kvq_cache* c, int path) {
     return guarded([&] {
-        if (path < KVQ_PATH_AUTO || path > KVQ_PATH_UMMA) raise(KVQ_ERR_CONFIG, "unknown decode path");
+        if (path < KVQ_PATH_AUTO || path > KVQ_PATH_WS) raise(KVQ_ERR_CONFIG, "unknown decode path");
         c->path = path;
     });
 }

@@ -762,7 +762,7 @@ class DecodeDetail:
     slope_violations: int = 0
 
 
-PATH_AUTO, PATH_GENERIC, PATH_TC, PATH_UMMA = 0, 1, 2, 3
+PATH_AUTO, PATH_GENERIC, PATH_TC, PATH_UMMA, PATH_HC, PATH_WS = 0, 1, 2, 3, 4, 5
 
 
 class BatchedCache:

@@ -184,13 +184,15 @@ def _load_inputs(z, oracle):
 
 
 @pytest.mark.parametrize("name", sorted(p.name for p in GOLD.glob("decode_*.npz")))
-@pytest.mark.parametrize("path", ["generic", "auto", "tc", "umma"])
+@pytest.mark.parametrize("path", ["generic", "auto", "tc", "umma", "hc"])
 def test_decode_golden_trajectories(kvq, oracle, name, path):
     z = np.load(GOLD / name)
     h, n, d, bits, wb, steps = z["meta"].tolist()
     t1, t2 = z["tau"].tolist()
-    if path in ("tc", "umma") and (d != 128 or bits == 16 or n == 0 or (path == "umma" and wb != 8)):
+    if path in ("tc", "umma", "hc") and (d != 128 or bits == 16 or n == 0 or (path == "umma" and wb != 8)):
         pytest.skip("tensor-core paths need d = 128 and a quantized prefill (tcgen05: M = 8)")
+    if path == "hc" and bits == 8:
+        pytest.skip("the hc decode covers 1/2/4-bit codes")
     k, v = _load_inputs(z, oracle)
     if bits == 16:
         cache = kvq.HybridKVCache.build_full_precision(list(k), list(v))
@@ -198,14 +200,14 @@ def test_decode_golden_trajectories(kvq, oracle, name, path):
         cache = kvq.HybridKVCache.build(list(k), list(v), kvq.QuantizationConfig(bits, kvq.QuantMode.channel_wise, wb),
                                         kvq.CalibrationParams(t1, t2))
     cache.batched.set_path({"generic": kvq.PATH_GENERIC, "auto": kvq.PATH_AUTO, "tc": kvq.PATH_TC,
-                            "umma": kvq.PATH_UMMA}[path])
+                            "umma": kvq.PATH_UMMA, "hc": kvq.PATH_HC}[path])
     if bits != 16 and n:
         for hh in range(h):
             ks, vs = cache.key_segment(hh), cache.value_segment(hh)
             assert np.array_equal(ks.codes.bytes, z[f"kcodes{hh}"]) and np.array_equal(vs.codes.bytes, z[f"vcodes{hh}"])
             assert bits_eq(ks.stats.alpha, z[f"kalpha{hh}"]) and bits_eq(vs.stats.beta, z[f"vbeta{hh}"])
     assert list(vars(cache.memory()).values()) == z["memory0"].tolist()
-    tol = {"generic": TOL_GENERIC, "tc": TOL_IMMA}.get(path, TOL_TC)
+    tol = {"generic": TOL_GENERIC, "tc": TOL_IMMA, "hc": TOL_IMMA, "auto": TOL_IMMA}.get(path, TOL_TC)
     for t in range(steps):
         out = cache.decode_step(z[f"q{t}"])
         assert rel_l2(out, z[f"out{t}"]) <= tol, f"{name} step {t}: {rel_l2(out, z[f'out{t}'])}"
@@ -358,14 +360,14 @@ def test_batched_gqa_vs_oracle(kvq, oracle, bits, G, n):
         want = _oracle_batched(oracle, k, v, q, bits, tau,
                                np.stack(tk) if tk else None, np.stack(tv) if tv else None)
         for path, tol in ((kvq.PATH_GENERIC, TOL_GENERIC), (kvq.PATH_TC, TOL_IMMA), (kvq.PATH_UMMA, TOL_TC),
-                          (kvq.PATH_AUTO, TOL_TC)):
+                          (kvq.PATH_HC, TOL_IMMA), (kvq.PATH_AUTO, TOL_IMMA)):
             cache.set_path(path)
             try:
                 out, _, _ = cache.decode(q)
             except kvq.ConfigError:
-                # the legacy IMMA path's shared-memory plan does not cover every shape;
-                # every other path must
-                assert path == kvq.PATH_TC
+                # the IMMA paths' shared-memory plans do not cover every shape (hc: b <= 4,
+                # G <= 4); every other path must
+                assert path == kvq.PATH_TC or (path == kvq.PATH_HC and (bits == 8 or G > 4))
                 continue
             err = rel_l2(out, want)
             assert err <= tol, f"path {path} step {step}: rel L2 {err}"
@@ -407,7 +409,7 @@ def test_step_api_matches_decode_then_append(kvq, B, H, n):
 
 
 @pytest.mark.parametrize("name", ["decode_d128_b2_m32.npz", "decode_d128_b4_m32.npz", "decode_d128_b8_m32.npz"])
-@pytest.mark.parametrize("path,wb", [("tc", 8), ("umma", 8), ("tc", 16)])
+@pytest.mark.parametrize("path,wb", [("tc", 8), ("umma", 8), ("tc", 16), ("hc", 8), ("hc", 16)])
 def test_decode_golden_m8_tensor_paths(kvq, oracle, name, path, wb):
     """The b >= 2 golden trajectories were produced by the reference with M = 32 (its M = 8
     table path is defective for b >= 2 at n >= 512). The codes are the
@@ -418,13 +420,15 @@ def test_decode_golden_m8_tensor_paths(kvq, oracle, name, path, wb):
     k, v = _load_inputs(z, oracle)
     cache = kvq.HybridKVCache.build(list(k), list(v), kvq.QuantizationConfig(bits, kvq.QuantMode.channel_wise, wb),
                                     kvq.CalibrationParams(t1, t2))
-    cache.batched.set_path(kvq.PATH_TC if path == "tc" else kvq.PATH_UMMA)
+    if path == "hc" and bits == 8:
+        pytest.skip("the hc decode covers 1/2/4-bit codes")
+    cache.batched.set_path({"tc": kvq.PATH_TC, "umma": kvq.PATH_UMMA, "hc": kvq.PATH_HC}[path])
     for hh in range(h):
         ka, kb = oracle.compute_stats(k[hh])
         assert np.array_equal(cache.key_segment(hh).codes.bytes, oracle.quantize(k[hh], ka, kb, bits, wb))
     for t in range(steps):
         out = cache.decode_step(z[f"q{t}"])
-        tol = TOL_IMMA if path == "tc" else TOL_TC
+        tol = TOL_TC if path == "umma" else TOL_IMMA
         assert rel_l2(out, z[f"out{t}"]) <= tol, f"{name} step {t}: {rel_l2(out, z[f'out{t}'])}"
         cache.append(z[f"knew{t}"], z[f"vnew{t}"])
 
@@ -449,7 +453,9 @@ def test_full_size_units_vs_oracle(kvq, oracle, bits, G, n):
         # The fp32 restatement's own error floor grows with n and b (SURVEY.md App. C:
         # 6.8e-5 at b=2, n=4096 vs float64); at these sizes the bar is 5e-4, half of
         # north_star's 1e-3.
-        for path, tol in ((kvq.PATH_TC, 5e-4), (kvq.PATH_UMMA, 5e-4)):
+        for path, tol in ((kvq.PATH_TC, 5e-4), (kvq.PATH_UMMA, 5e-4), (kvq.PATH_HC, 5e-4)):
+            if path == kvq.PATH_HC and (bits == 8 or G > 4):
+                continue
             cache.set_path(path)
             out, _, _ = cache.decode(q)
             err = rel_l2(out, want)
@@ -692,12 +698,12 @@ def test_randomized_paths_vs_oracle(kvq, oracle, case):
             for g in range(G):
                 want[b, h, g] = oracle.decode_head(q[b, h, g], n, c["bits"], c["wb"], kc, ka, kb, vc, va, vb, ktail,
                                                    vtail, *c["tau"])[0]
-    for path in (kvq.PATH_AUTO, kvq.PATH_TC, kvq.PATH_UMMA, kvq.PATH_GENERIC):
+    for path in (kvq.PATH_AUTO, kvq.PATH_TC, kvq.PATH_UMMA, kvq.PATH_HC, kvq.PATH_GENERIC):
         cache.set_path(path)
         try:
             out, _, _ = cache.decode(q)
         except kvq.ConfigError:
-            assert path in (kvq.PATH_TC, kvq.PATH_UMMA), "AUTO and GENERIC accept every shape"
+            assert path in (kvq.PATH_TC, kvq.PATH_UMMA, kvq.PATH_HC), "AUTO and GENERIC accept every shape"
             continue
         # fp32 reduction-order noise grows with n + tail: 1e-4 for the generic path at these
         # sizes (2e-5 on the small golden trajectories), 5e-4 for the tensor-core paths

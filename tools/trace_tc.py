@@ -1,4 +1,5 @@
-"""Per-CTA timeline of one IMMA decode launch (KVQ_TRACE_FILE stamps, k2_decode_tc.cu)."""
+"""Per-CTA timeline of one IMMA decode launch (KVQ_TRACE_FILE stamps, k2_decode_tc.cu /
+k2_decode_hc.cu).  python tools/trace_tc.py [config] [path: 2 = tc, 4 = hc]"""
 import os
 import sys
 from pathlib import Path
@@ -20,7 +21,7 @@ dev = torch.device("cuda", 0)
 k = torch.randn((batch, H, n, 128), device=dev)
 v = torch.randn((batch, H, n, 128), device=dev)
 c = kvq.BatchedCache.build_device(k, v, kvq.QuantizationConfig(bits), kvq.CalibrationParams(*tau), group=G)
-c.set_path(2)
+c.set_path(int(sys.argv[2]) if len(sys.argv) > 2 else 2)
 q = torch.randn((batch, H, G, 128), device=dev)
 out = torch.empty_like(q)
 for _ in range(3):
@@ -33,11 +34,13 @@ us = lambda x: (x - t0) / 1e3
 print(f"{cfg}: {len(t)} CTAs, span {us(t[:, 5].max()):.1f} us")
 pa = t[:, 8:16].max(1)
 pb = t[:, 16:24].max(1)
-for name, d in [("start->TMA issued + TMEM alloc", t[:, 6] - t[:, 0]), ("alloc->before griddep", t[:, 7] - t[:, 6]),
-                ("griddep wait", t[:, 3] - t[:, 7]), ("start->griddep released", t[:, 3] - t[:, 0]), ("griddep->prologue done", t[:, 2] - t[:, 3]),
-                ("  q loads+reductions", t[:, 24] - t[:, 3]), ("  sync 1", t[:, 25] - t[:, 24]), ("  frag build", t[:, 26] - t[:, 25]),
-                ("  sync 2 + bq", t[:, 2] - t[:, 26]),
-                ("prologue->phase A done", pa - t[:, 2]), ("start->phase A done (slowest warp)", pa - t[:, 0]), ("phase A warp spread", t[:, 8:16].max(1) - t[:, 8:16].min(1)),
+rows = [("start->griddep released", t[:, 3] - t[:, 0]), ("griddep->prologue done", t[:, 2] - t[:, 3])]
+if (t[:, 24] > 0).all():
+    rows += [("  q loads+reductions", t[:, 24] - t[:, 3]), ("  sync 1", t[:, 25] - t[:, 24]),
+             ("  frag build", t[:, 26] - t[:, 25]), ("  sync 2 + bq", t[:, 2] - t[:, 26])]
+pa_w = np.where(t[:, 8:16] > 0, t[:, 8:16], t[:, 2:3])
+for name, d in rows + [
+                ("prologue->phase A done", pa - t[:, 2]), ("start->phase A done (slowest warp)", pa - t[:, 0]), ("phase A warp spread", pa_w.max(1) - pa_w.min(1)),
                 ("phaseA done->params", t[:, 1] - pa), ("phase B (params->slowest warp)", pb - t[:, 1]),
                 ("epilogue", t[:, 5] - pb), ("CTA total", t[:, 5] - t[:, 0])]:
     d = d / 1e3
