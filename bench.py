@@ -10,17 +10,21 @@ of the step's new K/V row. Default workload = BASELINE config 2 (InternVL2.5-8B 
 
 Timing: W warm-up steps, then exactly K steps between barrier + synchronize, CUDA events
 on the launching stream, max over ranks. Each timed step is one CUDA-graph replay of
-[K2 decode + K3 append]; a second pass of up to 200 steps replays the two halves with
-events around the decode for the roofline's kernel time. The packed caches are device-resident; the
+[K2 decode + K3 append]; a second pass replays one graph chaining every replica's decode
+back to back (no events between launches, PDL overlap intact) for the roofline's kernel
+time. After timing, a parity spot check decodes replica 0 and compares three units with the
+float64 reference math on the cache's own codes. The packed caches are device-resident; the
 step rotates over R cache replicas whose total size exceeds the 126 MB L2 (so no step
 reads a cache another step left in L2) and which also bounds every replica's fp32 tail
 to <= tail_window generated tokens. `e2e` repeats the step through the public C-ABI
 (kvq_cache_step) with pinned host buffers: queries/new K,V copied in and outputs copied
 out every step.
 
-Multi-GPU (torchrun, one rank per GPU): units are independent, each rank owns its own
-batch (weak scaling); no collective on the data path, NCCL only for the barrier and the
-max-over-ranks timing.
+Multi-GPU (torchrun, one rank per GPU): a global batch (config batch x GPUs by default =
+weak scaling; --global-batch B = strong scaling) is sharded per SURVEY §8e by
+paper_2502_14882_b200.shard (request slices, or (request, KV head) units round-robin when
+B < GPUs); no collective on the data path, NCCL only for the barrier and the max-over-ranks
+timing. `value` is the whole job's tokens/s; `per_gpu` divides by the GPU count.
 """
 from __future__ import annotations
 
@@ -54,8 +58,34 @@ CONFIGS = {
     "c5b8": (8, 8, 4, 4096, 1, (1.0, 0.0), "BASELINE c5: batch 8, 4096 visual tokens, 1-bit"),
     "c5b512": (512, 8, 4, 4096, 1, (1.0, 0.0), "BASELINE c5: batch 512, 4096 visual tokens, 1-bit"),
 }
+# BASELINE config 3 "with and without post-scaling and calibration": name -> (base config,
+# tau, decode path, CPU arm). "nocal" = tau (0, 0) (the identity g, calibrate.hpp:62-67);
+# "deq" = dequantize-then-dot (every code dequantized in-register, then dotted: the
+# reference's naive_qk(q, dequantize(seg)) / naive_wv, kernels.hpp:401-426 on
+# quantize.hpp:129-146) on the generic decode, next to the same kernel post-scaled ("gen").
+ABLATIONS = {}
+for _b in ("c3b1", "c3b2", "c3b4"):
+    ABLATIONS[_b + "_nocal"] = (_b, (0.0, 0.0), None, "post")
+    ABLATIONS[_b + "_gen"] = (_b, None, "generic", "post")
+    ABLATIONS[_b + "_gen_nocal"] = (_b, (0.0, 0.0), "generic", "post")
+    ABLATIONS[_b + "_deq"] = (_b, None, "dequant", "dequant")
+    ABLATIONS[_b + "_deq_nocal"] = (_b, (0.0, 0.0), "dequant", "dequant")
+
+
+def resolve_config(name: str):
+    """(batch, kv_heads, group, n, bits, tau, description, path override, CPU arm)."""
+    if name in CONFIGS:
+        return (*CONFIGS[name], None, "post")
+    base, tau, path, cpu = ABLATIONS[name]
+    batch, H, G, n, bits, tau0, desc = CONFIGS[base]
+    tau = tau0 if tau is None else tau
+    desc += f"; ablation: tau={tuple(tau)}, " + ("dequantize-then-dot (no post-scaling)" if cpu == "dequant" else
+                                                   "post-scaled") + (f", {path} decode path" if path else "")
+    return batch, H, G, n, bits, tau, desc, path, cpu
+
+
 DIM = 128
-PATHS = {"auto": 0, "generic": 1, "tc": 2, "umma": 3, "hc": 4, "ws": 5}  # KVQ_PATH_* (include/kvq_capi.h)
+PATHS = {"auto": 0, "generic": 1, "tc": 2, "umma": 3, "hc": 4, "ws": 5, "dequant": 6}  # KVQ_PATH_* (include/kvq_capi.h)
 TAIL_WINDOW = 32
 L2_BYTES = 126 * 1024 * 1024
 
@@ -64,6 +94,62 @@ def alg_bytes_unit(n_vis: int, bits: int, group: int, n_tail: int, dim: int = DI
     """Algorithmic HBM bytes of one decode step for one unit:
     packed K+V codes + alpha/beta for K and V + q in/out + fp32 tail K+V."""
     return 2 * n_vis * dim * bits // 8 + 4 * dim * 4 + 2 * group * dim * 4 + 2 * n_tail * dim * 4
+
+
+def workload_config(args, world: int) -> dict:
+    """The workload the line measures - identical in both arms (the driver compares them):
+    BASELINE config name, shape, quantization and the global batch; no implementation keys."""
+    batch, H, G, n, bits, tau, desc, _, _ = resolve_config(args.config)
+    if args.batch:
+        batch = args.batch
+    if args.tail:
+        desc += f", {args.tail} generated tokens in the fp32 tail"
+    global_batch = args.global_batch or batch * world
+    return {"workload": desc, "name": args.config, "global_batch": global_batch, "q_heads": H * G, "kv_heads": H,
+            "head_dim": DIM, "n_vis": n, "bits": bits, "tau": list(tau), "tail_prefill": args.tail,
+            "parallelism": (f"{'request slices' if global_batch >= world else '(request, KV head) units round-robin'}"
+                            f" x{world} GPUs, no collective")}
+
+
+def decode_f64(codes_k, codes_v, ka, kb, va, vb, q, kt, vt, bits, tau) -> np.ndarray:
+    """The reference decode (kvcache.hpp:263-311: post-scaled scores, calibrated softmax
+    over [g(vis) | tail], w.V) in float64 on the cache's own integer codes - the spot
+    check's ground truth (SURVEY.md §8c rule 4)."""
+    f = np.float64
+    L = float((1 << bits) - 1)
+    ka, kb, va, vb, q = (np.asarray(x, f) for x in (ka, kb, va, vb, q))
+    sk = np.where(kb > ka, (kb - ka) / L, 0.0)
+    sv = np.where(vb > va, (vb - va) / L, 0.0)
+    isd = 1.0 / np.sqrt(f(q.size))
+    vis = (codes_k.astype(f) @ (q * sk) + q @ ka) * isd
+    tail = (np.asarray(kt, f) @ q) * isd
+    gamma, delta = vis.min(), vis.max()
+    if delta > gamma:
+        t = (vis - gamma) / (delta - gamma)
+        vis = vis - (tau[0] * (1 - t) + tau[1] * t)
+    else:
+        vis = vis - tau[0]
+    row = np.concatenate([vis, tail])
+    p = np.exp(row - row.max())
+    p /= p.sum()
+    return p[:vis.size] @ (va + codes_v.astype(f) * sv) + p[vis.size:] @ np.asarray(vt, f)
+
+
+def unpack_rows(raw: np.ndarray, n: int, bits: int) -> np.ndarray:
+    """Codes [n][128] of a reference M = 8 segment (MSB-first within bytes, bitpack.hpp:85)."""
+    b = np.asarray(raw, np.uint8).reshape(n, 16 * bits)
+    shifts = 8 - bits * (np.arange(8 // bits) + 1)
+    return ((b[..., None] >> shifts) & ((1 << bits) - 1)).reshape(n, DIM)
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def peak_hbm() -> tuple[float, str]:
@@ -158,7 +244,7 @@ def cpu_reference(cfg_name: str, requests: int, steps: int, threads: int, warmup
     so the timed steps take about `budget_s` seconds when budget_s > 0). Returns
     (tokens/s, detail)."""
     from oracle.oracle import Ref
-    batch, H, G, n, bits, tau, _ = CONFIGS[cfg_name]
+    batch, H, G, n, bits, tau, _, _, cpu_arm = resolve_config(cfg_name)
     requests = min(requests, batch)
     rng = np.random.default_rng(7)
     k = rng.standard_normal((requests, H, n, DIM), dtype=np.float32)
@@ -172,15 +258,17 @@ def cpu_reference(cfg_name: str, requests: int, steps: int, threads: int, warmup
     ref = Ref()
     if budget_s > 0:  # size the run: one probe step
         probe, _ = ref.bench_decode(k, v, requests, H, G, n, DIM, bits, word_bits, tau[0], tau[1], q, kn, vn,
-                                    threads, 2, tail)
+                                    threads, 2, tail, dequant=cpu_arm == "dequant")
         steps = max(3, min(steps, int(budget_s / max(min(probe), 1e-6))))
     secs, _ = ref.bench_decode(k, v, requests, H, G, n, DIM, bits, word_bits, tau[0], tau[1], q, kn, vn, threads,
-                               steps + warmup, tail)
+                               steps + warmup, tail, dequant=cpu_arm == "dequant")
     step_s = statistics.median(secs[warmup:])
     return requests / step_s, {
         "sample": f"{requests} of {batch} requests x {H} KV heads x G={G}, n_vis={n}, b={bits}, M={word_bits}, "
                   f"fp32 tail {tail}+; "
-                  f"median of {steps} steps after {warmup} warm-up; reference HybridKVCache::decode_step + append",
+                  f"median of {steps} steps after {warmup} warm-up; reference "
+                  + ("dequantize + naive_qk/naive_wv (no post-scaling)" if cpu_arm == "dequant"
+                     else "HybridKVCache::decode_step") + " + append",
         "step_seconds": step_s,
         "steps": steps,
     }
@@ -193,7 +281,7 @@ def run_reference(args, world, rank):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    batch, H, G, n, bits, tau, desc = CONFIGS[args.config]
+    batch, H, G, n, bits, tau, desc, _, _ = resolve_config(args.config)
     if args.tail:
         desc += f", {args.tail} generated tokens in the fp32 tail"
     t0 = time.time()
@@ -203,11 +291,10 @@ def run_reference(args, world, rank):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
         "steps": det["steps"], "warmup": warm, "ms_per_step": det["step_seconds"] * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": f"u{bits}", "data": "synthetic (gaussian)",
-        "config": {"workload": desc, "batch": batch, "q_heads": H * G, "kv_heads": H, "n_vis": n, "bits": bits,
-                   "tau": list(tau)},
+        "scaling": "strong" if args.global_batch else "weak", "vs_baseline": None, "dtype": f"u{bits}",
+        "data": "synthetic (gaussian)", "config": workload_config(args, world),
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "reference",
-                         "sample": det["sample"]},
+                         "cpu_model": cpu_model(), "sample": det["sample"]},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "wall_s": time.time() - t0,
     }
@@ -220,11 +307,22 @@ def run_ours(args, world, rank, local):
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    batch, H, G, n, bits, tau, desc = CONFIGS[args.config]
+    batch, H, G, n, bits, tau, desc, path_override, _ = resolve_config(args.config)
+    if path_override:
+        args.path = path_override
     if args.tail:
         desc += f", {args.tail} generated tokens in the fp32 tail"
     if args.batch:
         batch = args.batch
+    # §8(e) sharding: a global batch over the ranks (contiguous request slices, or
+    # (request, KV head) units round-robin when the batch is smaller than the GPU count);
+    # weak scaling by default (config batch per GPU), strong with --global-batch.
+    from paper_2502_14882_b200.shard import ShardSpec
+    global_batch = args.global_batch or batch * world
+    spec = ShardSpec(global_batch, H, G, n, DIM, rank, world)
+    batch, H = spec.local_shape  # this rank's cache: [batch][H] units
+    if batch == 0:
+        raise SystemExit(f"rank {rank}: no units (global batch {global_batch} x {spec.kv_heads} KV heads < {world} GPUs)")
     units = batch * H
     stream = torch.cuda.Stream(device=dev)
     sptr = stream.cuda_stream
@@ -232,8 +330,8 @@ def run_ours(args, world, rank, local):
 
     # Replicas: total packed bytes > L2 and <= TAIL_WINDOW appends per replica.
     cache_bytes = units * (2 * n * DIM * bits // 8 + 16 * DIM)
-    K2 = min(K, 200)  # second timed pass: per-launch decode events for the roofline
-    total_steps = W + K + K2 + args.e2e_steps
+    K2 = min(K, 200)  # second timed pass (decode chain): about this many decode launches
+    total_steps = W + K + args.e2e_steps
     R = max(2, -(-total_steps // TAIL_WINDOW), -(-(3 * L2_BYTES) // cache_bytes))
     tail_cap = -(-(total_steps + 2 * R) // R) + 3  # per replica: warm-up + timed + e2e appends
     gen = torch.Generator(device=dev)
@@ -267,43 +365,37 @@ def run_ours(args, world, rank, local):
         tails[r] += args.tail
     stream.synchronize()
 
-    # Eager warm-up (allocates the decode scratch), then CUDA graphs per replica: one for the
-    # whole step [K2 decode + K3 append] (the timed steps: programmatic dependent launch
-    # edges stay inside the graph, no host launches in the timed region), and one per half
-    # for the second pass, where events between the halves time the decode alone.
+    # Eager warm-up (allocates the decode scratch), then CUDA graphs: per replica the whole
+    # step [K2 decode + K3 append] (the timed steps: programmatic dependent launch edges stay
+    # inside the graph, no host launches in the timed region), and one chain of the R
+    # replicas' decodes back to back (the second pass: the decode kernel's own time with its
+    # PDL overlap intact, no events between launches).
     for t in range(R):
         caches[t].decode_device(q[t % 4], out, sptr)
         caches[t].append_device(kn[t % 4], vn[t % 4], sptr)
         tails[t] += 1
     stream.synchronize()
-    g_dec, g_app, g_step = [], [], []
-    launches_dec = launches_app = 0
+    g_step = []
+    launches_step = 0
     for r in range(R):
-        gd, ga, gs = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        gs = torch.cuda.CUDAGraph()
         l0 = kvq.launch_count()
-        with torch.cuda.graph(gd, stream=stream):
-            caches[r].decode_device(q[r % 4], out, sptr)
-        l1 = kvq.launch_count()
-        with torch.cuda.graph(ga, stream=stream):
-            caches[r].append_device(kn[r % 4], vn[r % 4], sptr)
-        launches_dec, launches_app = l1 - l0, kvq.launch_count() - l1
         with torch.cuda.graph(gs, stream=stream):
             caches[r].decode_device(q[r % 4], out, sptr)
             caches[r].append_device(kn[r % 4], vn[r % 4], sptr)
-        g_dec.append(gd)
-        g_app.append(ga)
+        launches_step = kvq.launch_count() - l0
         g_step.append(gs)
+    g_chain = torch.cuda.CUDAGraph()
+    l0 = kvq.launch_count()
+    with torch.cuda.graph(g_chain, stream=stream):
+        for r in range(R):
+            caches[r].decode_device(q[r % 4], out, sptr)
+    launches_dec = (kvq.launch_count() - l0) // R
 
-    def step(t, ev=None):
+    def step(t):
         r = t % R
         with torch.cuda.stream(stream):
-            if ev is None:
-                g_step[r].replay()
-            else:
-                ev[0].record(stream)
-                g_dec[r].replay()
-                ev[1].record(stream)
-                g_app[r].replay()
+            g_step[r].replay()
         tails[r] += 1
 
     for t in range(W):
@@ -311,9 +403,10 @@ def run_ours(args, world, rank, local):
     stream.synchronize()
     if world > 1:
         torch.distributed.barrier()
-    dec_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K2)]
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    bytes_alg = bytes_alg2 = 0
+    c_start, c_stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    chain_reps = max(2, -(-K2 // R))
+    bytes_alg = 0
     sampler = ClockSampler(local)
     with sampler:
         torch.cuda.synchronize()
@@ -328,29 +421,51 @@ def run_ours(args, world, rank, local):
             step(t)
         stop.record(stream)
         stream.synchronize()
-        # second pass: the same steps with events around each decode (roofline timing)
+        # second pass: the decode chain (roofline timing of the dominant kernel)
         with torch.cuda.stream(stream):
             torch.cuda._sleep(int(2e7))
-        for i in range(K2):
-            t = W + K + i
-            bytes_alg2 += units * alg_bytes_unit(n, bits, G, tails[t % R])
-            step(t, dec_ev[i])
+            c_start.record(stream)
+            for _ in range(chain_reps):
+                g_chain.replay()
+            c_stop.record(stream)
         stream.synchronize()
-    launches = K * (launches_dec + launches_app)
+    bytes_alg2 = sum(units * alg_bytes_unit(n, bits, G, tails[r]) for r in range(R)) / R  # per decode launch
+    launches = K * launches_step
+    # Parity spot check at the measured geometry (outside the timed region): one decode of
+    # replica 0, the first / last / a middle unit against the float64 reference math on the
+    # cache's own codes, stats and tail rows.
+    spot = None
+    if rank == 0 and args.path != "generic":
+        with torch.cuda.stream(stream):
+            caches[0].decode_device(q[0], out, sptr)
+        stream.synchronize()
+        got, qh = out.cpu().numpy(), q[0].cpu().numpy()
+        worst = 0.0
+        checked = sorted({0, units // 2, units - 1})
+        for u in checked:
+            bq, hq_ = divmod(u, H)
+            ks, vs = caches[0].segment(u, 0), caches[0].segment(u, 1)
+            ck, cv = unpack_rows(ks.codes.bytes, n, bits), unpack_rows(vs.codes.bytes, n, bits)
+            kt, vt = caches[0].tail(u, 0), caches[0].tail(u, 1)
+            for g in range(G):
+                want = decode_f64(ck, cv, ks.stats.alpha, ks.stats.beta, vs.stats.alpha, vs.stats.beta, qh[bq, hq_, g],
+                                  kt, vt, bits, tau)
+                worst = max(worst, float(np.linalg.norm(got[bq, hq_, g] - want) / np.linalg.norm(want)))
+        spot = {"units": checked, "heads": G, "max_rel_l2_vs_float64": worst, "tail_rows": int(kt.shape[0])}
     assert max(tails) <= tail_cap + args.tail, "bench tail accounting exceeded the reserved capacity"
     elapsed_ms = start.elapsed_time(stop)
-    dec_ms = [a.elapsed_time(b) for a, b in dec_ev]
+    dec_mean_s = c_start.elapsed_time(c_stop) * 1e-3 / (chain_reps * R)
     if world > 1:
         tt = torch.tensor([elapsed_ms], device=dev)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         elapsed_ms = float(tt.item())
         torch.distributed.barrier()
     ms_per_step = elapsed_ms / K
-    value = world * batch * K / (elapsed_ms * 1e-3)
+    value = global_batch * K / (elapsed_ms * 1e-3)  # every request of the global batch: one token per step
 
-    # Roofline of the dominant kernel (K2 decode), from its own per-launch events.
-    dec_mean_s = statistics.mean(dec_ms) * 1e-3
-    achieved = bytes_alg2 / K2 / dec_mean_s / 1e9
+    # Roofline of the dominant kernel (K2 decode): algorithmic bytes per launch over the mean
+    # launch time in the back-to-back decode chain.
+    achieved = bytes_alg2 / dec_mean_s / 1e9
     peak, peak_kind = peak_hbm()
     prof = ROOT / "profiles" / "decode_ncu_summary.json"
     traffic = None
@@ -379,7 +494,7 @@ def run_ours(args, world, rank, local):
         tt = torch.tensor([e2e_s], device=dev)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         e2e_s = float(tt.item())
-    e2e_value = world * batch * E / e2e_s
+    e2e_value = global_batch * E / e2e_s
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -387,7 +502,7 @@ def run_ours(args, world, rank, local):
             cv, det = cpu_reference(args.config, args.cpu_requests, args.steps_cpu, os.cpu_count() or 1,
                                     tail=args.tail)
             cpu = {"value": cv, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "reference",
-                   "sample": det["sample"]}
+                   "cpu_model": cpu_model(), "sample": det["sample"]}
         except Exception as e:  # keep the GPU line even if the checker is missing
             cpu = {"value": None, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
@@ -395,26 +510,28 @@ def run_ours(args, world, rank, local):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K, "warmup": W,
-            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong" if args.global_batch else "weak", "vs_baseline": None,
             "dtype": f"u{bits}", "data": "synthetic (gaussian K/V/q, torch.randn on device)",
-            "config": {"workload": desc, "batch_per_gpu": batch, "global_batch": batch * world, "q_heads": H * G,
-                       "kv_heads": H, "head_dim": DIM, "n_vis": n, "bits": bits, "tau": list(tau),
-                       "tail_window": TAIL_WINDOW, "parallelism": f"units sharded x{world} (no collective)",
-                       "l2": f"inputs larger than L2: {R} rotating cache replicas x {cache_bytes / 2**20:.1f} MiB",
-                       "step": "K2 decode (all q heads) + K3 append", "decode_path": args.path,
-                       "tail_prefill": args.tail},
+            "config": workload_config(args, world),
+            "per_gpu": {"value": value / world, "unit": "tokens/s/GPU", "rank0_units": units},
+            "impl_details": {"tail_window": TAIL_WINDOW,
+                             "l2": f"inputs larger than L2: {R} rotating cache replicas x {cache_bytes / 2**20:.1f} MiB",
+                             "step": "K2 decode (all q heads) + K3 append", "decode_path": args.path},
             "hbm_gbs": bytes_alg / K / (ms_per_step * 1e-3) / 1e9,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                          "kernel": "K2 decode" + (" + fp32 tail pass" if args.tail + tail_cap > 64 else ""),
-                         "alg_bytes_per_launch": bytes_alg2 / K2,
+                         "alg_bytes_per_launch": bytes_alg2,
                          "launch_us": dec_mean_s * 1e6,
-                         "timing": f"CUDA events around each decode graph over a second timed pass of {K2} steps "
-                                   "(the K timed steps replay whole-step graphs with no events in between)"},
+                         "launches_per_decode": launches_dec,
+                         "timing": f"CUDA events around {chain_reps} replays of one graph chaining the {R} replicas' "
+                                   "decodes back to back (PDL overlap between launches kept, no events in between)"},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": int(hq.nbytes + hk.nbytes + hv.nbytes),
                     "d2h_bytes_per_step": int(hout.nbytes), "steps": E},
             "gpu_launches": int(launches),
+            "spot_check": spot,
             "clocks": sampler.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -425,8 +542,10 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=400)
     ap.add_argument("--warmup", type=int, default=20)
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS) + sorted(ABLATIONS))
     ap.add_argument("--batch", type=int, default=0, help="override the config's per-GPU batch")
+    ap.add_argument("--global-batch", type=int, default=0,
+                    help="fixed global batch sharded over the GPUs (strong scaling); default: config batch per GPU")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=100)
     ap.add_argument("--tail", type=int, default=0,

@@ -46,6 +46,7 @@ extern "C" {
 #define KVQ_PATH_TC 2      /* d = 128, M = 8 legacy mma.sync IMMA path (KVQ_ERR_CONFIG otherwise) */
 #define KVQ_PATH_UMMA 3    /* d = 128, M = 8 tcgen05 UTCIMMA path (KVQ_ERR_CONFIG otherwise) */
 #define KVQ_PATH_HC 4      /* d = 128, b <= 4, G <= 4 8-warp channel-split IMMA path (KVQ_ERR_CONFIG otherwise) */
+#define KVQ_PATH_DEQUANT 6 /* BASELINE c3 ablation: generic decode, dequantize-then-dot (no post-scaling) */
 #define KVQ_PATH_WS 5      /* d = 128, b <= 4, G <= 4, n <= 8192, >= 296 units: persistent warp-specialized IMMA path */
 
 /* ---- diagnostics ------------------------------------------------------------ */
@@ -59,6 +60,9 @@ unsigned long long kvq_last_error_offset(void);
 unsigned long long kvq_launch_count(void);
 /* 1 if a CUDA device is usable (the library never falls back to the CPU). */
 int kvq_device_available(void);
+/* Bind the calling thread's CUDA device (one process per GPU): every later
+   cache of this thread lives on `device`. No reference counterpart (the reference is CPU). */
+int kvq_set_device(int device);
 
 /* ---- bitpack.hpp ------------------------------------------------------------- */
 /* Bytes `pack` produces for `count` codes (PackedBuffer::word_count, bitpack.hpp:22-25). */
@@ -157,6 +161,10 @@ int kvq_cache_build_device(const float* k_vis, const float* v_vis, size_t batch,
 void kvq_cache_free(kvq_cache* c);
 /* Preallocate fp32 tail capacity (rows per unit); append grows it on demand. */
 int kvq_cache_reserve_tail(kvq_cache* c, size_t rows);
+/* Reconcile the host tail counter with the device (appends issued on user streams or
+   replayed from captured graphs advance it on the device only); KVQ_ERR_DOMAIN if appends
+   were dropped at a full tail. info / memory / read_tail / save_image do this implicitly. */
+int kvq_cache_sync_tail(kvq_cache* c);
 /* Decode kernel selection (KVQ_PATH_*); never changes results beyond fp tolerance. */
 int kvq_cache_set_path(kvq_cache* c, int path);
 

@@ -275,6 +275,9 @@ class Ref:
             "kvqr_cache_memory": (C.c_int, [_VP, _SZP]),
             "kvqr_bench_decode": (C.c_int, [_F, _F, _SZ, _SZ, _SZ, _SZ, _SZ, C.c_int, C.c_int, C.c_float, C.c_float,
                                             _F, _F, _F, C.c_int, C.c_int, _SZ, C.POINTER(C.c_double), _F]),
+            "kvqr_bench_decode_dequant": (C.c_int, [_F, _F, _SZ, _SZ, _SZ, _SZ, _SZ, C.c_int, C.c_int, C.c_float,
+                                                    C.c_float, _F, _F, _F, C.c_int, C.c_int, _SZ,
+                                                    C.POINTER(C.c_double), _F]),
             "kvqr_cache_save": (C.c_int, [C.c_void_p, C.c_void_p, _SZ, _SZP]),
             "kvqr_cache_load": (C.c_int, [C.c_void_p, _SZ, C.POINTER(C.c_void_p), C.POINTER(C.c_uint64)]),
             "kvqr_grid_mse_table": (C.c_int, [_F, _F, _U8, _F, _F, _SZ, _SZ, _SZ, C.c_int, C.c_int, _F, _F, _SZ,
@@ -394,10 +397,13 @@ class Ref:
         return RefCache(self, out.value, h, d)
 
     def bench_decode(self, k, v, requests, kv_heads, group, n, dim, bits, word_bits, tau1, tau2, q, k_new, v_new,
-                     threads, steps, prefill_tail=0):
+                     threads, steps, prefill_tail=0, dequant=False):
+        """The reference's decode on host threads; dequant=True: the dequantize-then-dot
+        ablation (dequantize + naive_qk / naive_wv around the calibrated softmax)."""
         secs = (C.c_double * steps)()
         out = np.zeros_like(_f32(q))
-        self._ok(self.L.kvqr_bench_decode(_fp(_f32(k)), _fp(_f32(v)), requests, kv_heads, group, n, dim, bits,
+        fn = self.L.kvqr_bench_decode_dequant if dequant else self.L.kvqr_bench_decode
+        self._ok(fn(_fp(_f32(k)), _fp(_f32(v)), requests, kv_heads, group, n, dim, bits,
                                           word_bits, tau1, tau2, _fp(_f32(q)), _fp(_f32(k_new)), _fp(_f32(v_new)),
                                           threads, steps, prefill_tail, secs, _fp(out)))
         return list(secs), out

@@ -371,37 +371,65 @@ int kvqr_cache_memory(const kvqr_cache* c, std::size_t* out6) {
 // one append of the step's new K/V rows. Requests are spread over `threads` host
 // threads (outer pool, KernelConfig{32, 64, 1} inside — the reference's fastest mode,
 // BASELINE.md §4). Returns per-step wall seconds in step_seconds[steps].
-int kvqr_bench_decode(const float* k_vis, const float* v_vis, std::size_t requests,
-                      std::size_t kv_heads, std::size_t group, std::size_t n, std::size_t dim,
-                      int bits, int word_bits, float tau1, float tau2, const float* queries,
-                      const float* k_new, const float* v_new, int threads, int steps,
-                      std::size_t prefill_tail, double* step_seconds, float* out_last) {
-    try {
-        std::vector<kvq::HybridKVCache> caches(requests);
-        {
-            std::vector<std::thread> pool;
-            std::atomic<std::size_t> next{0};
-            for (int t = 0; t < threads; ++t) {
-                pool.emplace_back([&] {
-                    for (std::size_t r = next++; r < requests; r = next++) {
-                        std::vector<kvq::DenseMatrix> ks, vs;
-                        for (std::size_t h = 0; h < kv_heads; ++h) {
-                            std::size_t off = (r * kv_heads + h) * n * dim;
-                            ks.push_back(mat(k_vis + off, n, dim));
-                            vs.push_back(mat(v_vis + off, n, dim));
-                        }
-                        caches[r] = kvq::HybridKVCache::build(
-                            ks, vs, kvq::QuantizationConfig{bits, kvq::QuantMode::channel_wise, word_bits},
-                            kvq::CalibrationParams{tau1, tau2});
-                        // generated tokens already in the fp32 tail before the timed steps
-                        for (std::size_t t = 0; t < prefill_tail; ++t)
-                            caches[r].append(mat(k_new + r * kv_heads * dim, kv_heads, dim),
-                                             mat(v_new + r * kv_heads * dim, kv_heads, dim));
-                    }
-                });
+// Shared by the two bench arms: per-request caches built with the reference's own API.
+static std::vector<kvq::HybridKVCache> bench_build(const float* k_vis, const float* v_vis, std::size_t requests,
+                                                   std::size_t kv_heads, std::size_t n, std::size_t dim, int bits,
+                                                   int word_bits, float tau1, float tau2, const float* k_new,
+                                                   const float* v_new, int threads, std::size_t prefill_tail) {
+    std::vector<kvq::HybridKVCache> caches(requests);
+    std::vector<std::thread> pool;
+    std::atomic<std::size_t> next{0};
+    for (int t = 0; t < threads; ++t) {
+        pool.emplace_back([&] {
+            for (std::size_t r = next++; r < requests; r = next++) {
+                std::vector<kvq::DenseMatrix> ks, vs;
+                for (std::size_t h = 0; h < kv_heads; ++h) {
+                    std::size_t off = (r * kv_heads + h) * n * dim;
+                    ks.push_back(mat(k_vis + off, n, dim));
+                    vs.push_back(mat(v_vis + off, n, dim));
+                }
+                caches[r] = kvq::HybridKVCache::build(
+                    ks, vs, kvq::QuantizationConfig{bits, kvq::QuantMode::channel_wise, word_bits},
+                    kvq::CalibrationParams{tau1, tau2});
+                // generated tokens already in the fp32 tail before the timed steps
+                for (std::size_t t = 0; t < prefill_tail; ++t)
+                    caches[r].append(mat(k_new + r * kv_heads * dim, kv_heads, dim),
+                                     mat(v_new + r * kv_heads * dim, kv_heads, dim));
             }
-            for (auto& th : pool) th.join();
-        }
+        });
+    }
+    for (auto& th : pool) th.join();
+    return caches;
+}
+
+// One head of the "without post-scaling" ablation (BASELINE config 3): dequantize the
+// packed segments (quantize.hpp:129-146), then the dense products naive_qk / naive_wv
+// (kernels.hpp:401-426) around the same calibrated softmax (calibrate.hpp:100-114).
+static void decode_head_dequant(const kvq::HybridKVCache& c, std::size_t h, std::span<const float> q, float* out) {
+    const std::size_t d = q.size();
+    const float isd = 1.0f / std::sqrt(float(d));
+    const kvq::DenseMatrix kd = kvq::dequantize(c.key_segment(h));
+    const kvq::DenseMatrix vd = kvq::dequantize(c.value_segment(h));
+    std::vector<float> vis = kvq::naive_qk(q, kd);
+    for (float& x : vis) x *= isd;
+    std::vector<float> tail = kvq::naive_qk(q, c.key_tail(h));
+    for (float& x : tail) x *= isd;
+    const std::vector<float> p = kvq::calibrated_softmax_concat(vis, tail, c.calibration());
+    const std::vector<float> ov = kvq::naive_wv(std::span<const float>(p.data(), vis.size()), vd);
+    const std::vector<float> ot = kvq::naive_wv(std::span<const float>(p.data() + vis.size(), tail.size()), c.value_tail(h));
+    for (std::size_t i = 0; i < d; ++i) out[i] = ov[i] + ot[i];
+}
+
+// mode 0: HybridKVCache::decode_step (post-scaled, the reference as shipped);
+// mode 1: dequantize-then-dot (decode_head_dequant) over the same caches.
+static int bench_decode_mode(int mode, const float* k_vis, const float* v_vis, std::size_t requests,
+                             std::size_t kv_heads, std::size_t group, std::size_t n, std::size_t dim, int bits,
+                             int word_bits, float tau1, float tau2, const float* queries, const float* k_new,
+                             const float* v_new, int threads, int steps, std::size_t prefill_tail,
+                             double* step_seconds, float* out_last) {
+    try {
+        std::vector<kvq::HybridKVCache> caches = bench_build(k_vis, v_vis, requests, kv_heads, n, dim, bits, word_bits,
+                                                             tau1, tau2, k_new, v_new, threads, prefill_tail);
         const kvq::KernelConfig inner{32, 64, 1};
         for (int s = 0; s < steps; ++s) {
             auto t0 = std::chrono::steady_clock::now();
@@ -410,17 +438,26 @@ int kvqr_bench_decode(const float* k_vis, const float* v_vis, std::size_t reques
             for (int t = 0; t < threads; ++t) {
                 pool.emplace_back([&] {
                     kvq::DenseMatrix q(kv_heads, dim);
+                    std::vector<float> o1(dim);
                     for (std::size_t r = next++; r < requests; r = next++) {
                         for (std::size_t g = 0; g < group; ++g) {
                             for (std::size_t h = 0; h < kv_heads; ++h) {
                                 const float* src = queries + ((r * kv_heads + h) * group + g) * dim;
                                 std::copy(src, src + dim, q.row(h));
                             }
-                            kvq::DenseMatrix o = caches[r].decode_step(q, inner);
-                            if (out_last && s == steps - 1) {
-                                for (std::size_t h = 0; h < kv_heads; ++h)
-                                    std::copy(o.row(h), o.row(h) + dim,
-                                              out_last + ((r * kv_heads + h) * group + g) * dim);
+                            const bool keep = out_last && s == steps - 1;
+                            if (mode == 0) {
+                                kvq::DenseMatrix o = caches[r].decode_step(q, inner);
+                                if (keep)
+                                    for (std::size_t h = 0; h < kv_heads; ++h)
+                                        std::copy(o.row(h), o.row(h) + dim,
+                                                  out_last + ((r * kv_heads + h) * group + g) * dim);
+                            } else {
+                                for (std::size_t h = 0; h < kv_heads; ++h) {
+                                    decode_head_dequant(caches[r], h, q.row_span(h), o1.data());
+                                    if (keep)
+                                        std::copy(o1.begin(), o1.end(), out_last + ((r * kv_heads + h) * group + g) * dim);
+                                }
                             }
                         }
                         caches[r].append(mat(k_new + r * kv_heads * dim, kv_heads, dim),
@@ -433,6 +470,24 @@ int kvqr_bench_decode(const float* k_vis, const float* v_vis, std::size_t reques
         }
         return 0;
     } catch (const std::exception& e) { return fail(e); }
+}
+
+int kvqr_bench_decode(const float* k_vis, const float* v_vis, std::size_t requests,
+                      std::size_t kv_heads, std::size_t group, std::size_t n, std::size_t dim,
+                      int bits, int word_bits, float tau1, float tau2, const float* queries,
+                      const float* k_new, const float* v_new, int threads, int steps,
+                      std::size_t prefill_tail, double* step_seconds, float* out_last) {
+    return bench_decode_mode(0, k_vis, v_vis, requests, kv_heads, group, n, dim, bits, word_bits, tau1, tau2, queries,
+                             k_new, v_new, threads, steps, prefill_tail, step_seconds, out_last);
+}
+
+int kvqr_bench_decode_dequant(const float* k_vis, const float* v_vis, std::size_t requests,
+                              std::size_t kv_heads, std::size_t group, std::size_t n, std::size_t dim,
+                              int bits, int word_bits, float tau1, float tau2, const float* queries,
+                              const float* k_new, const float* v_new, int threads, int steps,
+                              std::size_t prefill_tail, double* step_seconds, float* out_last) {
+    return bench_decode_mode(1, k_vis, v_vis, requests, kv_heads, group, n, dim, bits, word_bits, tau1, tau2, queries,
+                             k_new, v_new, threads, steps, prefill_tail, step_seconds, out_last);
 }
 
 }  // extern "C"

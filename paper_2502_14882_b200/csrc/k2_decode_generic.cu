@@ -14,7 +14,10 @@
 //   4. out_c = s_c * sum_j w_j code_jc + alpha_c * sum_j w_j + sum_t w_t v_tc
 //      (kernels.hpp:277-283; kvcache.hpp:297-304)
 // Packed K/V are never dequantized: the scales are folded into q (K side) and into the
-// epilogue (V side).
+// epilogue (V side). DecodeArgs::dequant_dot selects BASELINE config 3's "without
+// post-scaling" ablation instead: every code is dequantized in-register (alpha_c + code *
+// s_c, quantize.hpp:129-146) and dotted with q / weighted by w (naive_qk / naive_wv,
+// kernels.hpp:401-426) - the same scores and outputs up to fp32 reassociation.
 #include "kvq_device.cuh"
 #include "kvq_internal.cuh"
 
@@ -35,8 +38,10 @@ decode_generic_kernel(DecodeArgs a) {
     float* scal = red + 32;      // qdota
     // channel c's code: byte cbyte[c] of the row, bits [cshift[c], cshift[c] + b) - codes
     // never straddle a byte (b | 8), so no per-code division or word assembly
-    uint16_t* cbyte = reinterpret_cast<uint16_t*>(scal + 8);  // [d]
-    uint8_t* cshift = reinterpret_cast<uint8_t*>(cbyte + d);   // [d]
+    float* kal = scal + 8;                                      // [d] K alpha (dequant_dot)
+    uint16_t* cbyte = reinterpret_cast<uint16_t*>(kal + d);     // [d]
+    uint8_t* cshift = reinterpret_cast<uint8_t*>(cbyte + d);    // [d]
+    const bool dq = a.dequant_dot != 0;
     const size_t unit = blockIdx.x / a.group;
     const size_t g = blockIdx.x % a.group;
     const size_t b = unit / a.kv_heads;
@@ -59,7 +64,9 @@ decode_generic_kernel(DecodeArgs a) {
         float v = 0.0f;
         if (c < d) {
             float range = __fsub_rn(kb[c], ka[c]);
-            v = range > 0.0f ? __fmul_rn(q[c], __fdiv_rn(range, levels)) : 0.0f;
+            const float stp = range > 0.0f ? __fdiv_rn(range, levels) : 0.0f;
+            v = dq ? stp : (range > 0.0f ? __fmul_rn(q[c], stp) : 0.0f);  // dequant: K step
+            kal[c] = ka[c];
         }
         qs[c] = v;
     }
@@ -84,6 +91,14 @@ decode_generic_kernel(DecodeArgs a) {
     for (size_t j = threadIdx.x; j < n; j += blockDim.x) {
         const uint8_t* r = kc + j * rb;
         float acc = 0.0f;
+        if (dq) {  // dequantize-then-dot: k_jc = alpha_c + code * s_c, then q . k_j
+            for (size_t c = 0; c < d; ++c) acc = __fmaf_rn(q[c], __fmaf_rn(code(r, c), qs[c], kal[c]), acc);
+            const float s = __fmul_rn(acc, inv_sqrt_d);
+            row[j] = s;
+            lo = fminf(lo, s);
+            hi = fmaxf(hi, s);
+            continue;
+        }
         if ((rb & 3) == 0 && a.bits <= 8) {  // 32-bit row words: one load per word, codes in order
             const uint32_t* r32 = reinterpret_cast<const uint32_t*>(r);
             uint32_t w = 0, cur = 0xffffffffu;
@@ -148,6 +163,15 @@ decode_generic_kernel(DecodeArgs a) {
     float* out = a.out + (unit * a.group + g) * d;
     for (size_t c = threadIdx.x; c < d; c += blockDim.x) {
         float acc = 0.0f, wsum = 0.0f;
+        if (dq) {  // dequantize-then-dot: out_c = sum_j w_j (alpha_c + code_jc s_c)
+            const float range = __fsub_rn(vb[c], va[c]);
+            const float step = range > 0.0f ? __fdiv_rn(range, levels) : 0.0f;
+            for (size_t j = 0; j < n; ++j) acc = __fmaf_rn(row[j], __fmaf_rn(code(vc + j * rb, c), step, va[c]), acc);
+            float tacc = 0.0f;
+            for (size_t t = 0; t < nt; ++t) tacc = __fmaf_rn(row[n + t], vt[t * d + c], tacc);
+            out[c] = __fadd_rn(acc, tacc);
+            continue;
+        }
         for (size_t j = 0; j < n; ++j) {
             float w = row[j];
             wsum = __fadd_rn(wsum, w);
@@ -321,7 +345,7 @@ cudaError_t launch_naive_wv(const float* w, const float* v, size_t rows, size_t 
 
 cudaError_t launch_decode_generic(const DecodeArgs& a, cudaStream_t s) {
     const size_t cpr = codes_per_row(a.dim, a.bits, a.word_bits);
-    const size_t smem = sizeof(float) * (cpr + 40) + 3 * a.dim + 16;  // + per-channel byte / shift
+    const size_t smem = sizeof(float) * (cpr + 40 + a.dim) + 3 * a.dim + 16;  // + K alpha, byte / shift
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(decode_generic_kernel,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

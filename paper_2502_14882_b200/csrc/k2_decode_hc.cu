@@ -741,17 +741,12 @@ cudaError_t launch_bits(const DecodeArgs& a, cudaStream_t s) {
     const size_t floor_bytes = 232448 / (max_ctas + 1) + 1;
     if (smem < floor_bytes) smem = floor_bytes;
     auto kern = decode_hc_kernel<BITS>;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    static unsigned attr_done[3] = {0, 0, 0};  // per instantiation, bit per device
-    unsigned& done = attr_done[BITS == 1 ? 0 : (BITS == 2 ? 1 : 2)];
-    if (dev < 32 && !(done & (1u << dev))) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        if (e != cudaSuccess) return e;
-        done |= 1u << dev;
-    }
+    static unsigned attr_done = 0;  // per instantiation, bit per device
+    const cudaError_t ea = once_per_device(attr_done, [&] {
+        cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        return r != cudaSuccess ? r : cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    });
+    if (ea != cudaSuccess) return ea;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(a.units * S));
     cfg.blockDim = dim3(kW * 32);

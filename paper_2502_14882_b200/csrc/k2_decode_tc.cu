@@ -886,14 +886,12 @@ cudaError_t launch_occ(const DecodeArgs& a, cudaStream_t s, int groups = 1) {
     const size_t floor_bytes = 232448 / (max_ctas + 1) + 1;
     if (smem < floor_bytes) smem = floor_bytes;
     auto kern = decode_tc_kernel<BITS, NT, OCC, W>;
-    static bool attr_done = false;  // per instantiation
-    if (!attr_done) {
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-        if (e != cudaSuccess) return e;
-        attr_done = true;
-    }
+    static unsigned attr_done = 0;  // per instantiation, bit per device
+    e = once_per_device(attr_done, [&] {
+        cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        return r != cudaSuccess ? r : cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    });
+    if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(a.units * S * groups));
     cfg.blockDim = dim3(W * 32);

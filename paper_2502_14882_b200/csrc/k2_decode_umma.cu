@@ -911,14 +911,12 @@ cudaError_t launch_bits(const DecodeArgs& a, cudaStream_t s) {
     UParams p{a, a.umma_qb, a.tc_qconst, S, T};
     const size_t smem = smem_for<BITS, NT>(a);
     auto kern = decode_umma_kernel<BITS, NT>;
-    static bool attr_done = false;  // per instantiation
-    if (!attr_done) {
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-        if (e != cudaSuccess) return e;
-        attr_done = true;
-    }
+    static unsigned attr_done = 0;  // per instantiation, bit per device
+    e = once_per_device(attr_done, [&] {
+        cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        return r != cudaSuccess ? r : cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    });
+    if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(a.units * S));
     cfg.blockDim = dim3(kThreads + 64);  // 4 consumer warps + MMA issuer + TMA producer

@@ -732,13 +732,10 @@ cudaError_t launch_bits(const DecodeArgs& a, int T8, cudaStream_t s) {
     WsParams p{a, T8, (int)((a.units + grid - 1) / grid)};
     const size_t smem = ws_smem_bytes();
     auto kern = decode_ws_kernel<BITS>;
-    static unsigned attr_done[3] = {0, 0, 0};  // per instantiation, bit per device
-    unsigned& done = attr_done[BITS == 1 ? 0 : (BITS == 2 ? 1 : 2)];
-    if (dev < 32 && !(done & (1u << dev))) {
-        const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        done |= 1u << dev;
-    }
+    static unsigned attr_done = 0;  // per instantiation, bit per device
+    const cudaError_t ea = once_per_device(
+        attr_done, [&] { return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); });
+    if (ea != cudaSuccess) return ea;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(kThreads);

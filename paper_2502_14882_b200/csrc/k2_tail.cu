@@ -285,7 +285,11 @@ __global__ void __launch_bounds__(kWarps * 32) tail_kernel(const TailParams p) {
     for (int it = 0; it < kItems; ++it) {
         const int idx = threadIdx.x + it * kWarps * 32;
         const int h = idx / kDim, ch = idx % kDim;
-        if (h >= G || RM[it] == -INFINITY) continue;  // no tail rows: the decode's output stands
+        if (h >= G) continue;
+        if (RM[it] == -INFINITY) {  // no tail rows: the decode's output stands; with no decode
+            if (!p.lse) p.out[(unit * G + h) * kDim + ch] = 0.0f;  // (empty cache) the row is 0
+            continue;                                         // (softmax_inplace no-op, naive_wv zeros)
+        }
         const float M = RM[it], D = RD[it], Nn = RN[it];
         float* o = p.out + (unit * G + h) * kDim + ch;
         const float lv = p.lse ? p.lse[unit * G + h] : -INFINITY;
@@ -308,7 +312,10 @@ __global__ void __launch_bounds__(256) tail_merge_kernel(const float* __restrict
     const size_t row = i / kDim, ch = i % kDim;
     const float* rec = part + row * (kDim + 2);
     const float M = rec[0];
-    if (M == -INFINITY) return;  // no tail rows: the decode's output stands
+    if (M == -INFINITY) {  // no tail rows: the decode's output stands (an empty cache: 0)
+        if (!lse) out[i] = 0.0f;
+        return;
+    }
     const float D = rec[1], Nn = rec[2 + ch];
     const float lv = lse ? lse[row] : -INFINITY;
     if (lv == -INFINITY) {
@@ -324,12 +331,10 @@ template <int GP>
 cudaError_t launch_gp(const TailParams& p, size_t units, cudaStream_t s, bool pdl) {
     auto kern = tail_kernel<GP>;
     const size_t smem = sizeof(TailSmem<GP>);
-    static bool attr_done = false;  // per instantiation
-    if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        attr_done = true;
-    }
+    static unsigned attr_done = 0;  // per instantiation, bit per device
+    const cudaError_t ea = once_per_device(
+        attr_done, [&] { return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); });
+    if (ea != cudaSuccess) return ea;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(units * p.S));
     cfg.blockDim = dim3(kWarps * 32);

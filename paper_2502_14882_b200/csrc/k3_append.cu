@@ -8,11 +8,15 @@ namespace kvqb {
 
 namespace {
 
-// One CTA per request: all of its KV heads, then a single increment of its length.
+// One CTA per request: all of its KV heads, then a single increment of its length. A full
+// tail (tail_len == tail_cap: e.g. a captured decode + append graph replayed past the rows
+// reserve_tail made room for) is never written past: the append is dropped and `overflow`
+// set, which the host reports as a domain_error at its next synchronization
+// (kvq_cache_sync_tail) instead of corrupting the neighbouring unit's rows.
 __global__ void append_kernel(const float* __restrict__ k_new, const float* __restrict__ v_new,
                               size_t kv_heads, size_t dim, size_t tail_cap,
                               float* __restrict__ k_tail, float* __restrict__ v_tail,
-                              int* __restrict__ tail_len) {
+                              int* __restrict__ tail_len, int* __restrict__ overflow) {
     // The next decode (launched with programmatic stream serialization) may start its
     // prologue now; it reads the tail only after griddepcontrol.wait (= this grid done).
     asm volatile("griddepcontrol.launch_dependents;");
@@ -33,6 +37,10 @@ __global__ void append_kernel(const float* __restrict__ k_new, const float* __re
         }
         asm volatile("griddepcontrol.wait;" ::: "memory");
         const size_t slot = (size_t)tail_len[b];
+        if (slot >= tail_cap) {
+            if (threadIdx.x == 0) atomicOr(overflow, 1);
+            return;
+        }
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
             const size_t i = threadIdx.x + (size_t)r * blockDim.x;
@@ -49,6 +57,10 @@ __global__ void append_kernel(const float* __restrict__ k_new, const float* __re
     }
     asm volatile("griddepcontrol.wait;" ::: "memory");
     const size_t slot = (size_t)tail_len[b];
+    if (slot >= tail_cap) {
+        if (threadIdx.x == 0) atomicOr(overflow, 1);
+        return;
+    }
     for (size_t i = threadIdx.x; i < (vec ? n / 4 : n); i += blockDim.x) {
         if (vec) {
             size_t h = (i * 4) / dim, c = (i * 4) % dim;
@@ -71,7 +83,7 @@ __global__ void append_kernel(const float* __restrict__ k_new, const float* __re
 
 cudaError_t launch_append(const float* k_new, const float* v_new, size_t batch, size_t kv_heads,
                           size_t dim, size_t tail_cap, float* k_tail, float* v_tail,
-                          int* tail_len, cudaStream_t s) {
+                          int* tail_len, int* overflow, cudaStream_t s) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)batch);
     cfg.blockDim = dim3(256);
@@ -82,7 +94,8 @@ cudaError_t launch_append(const float* k_new, const float* v_new, size_t batch, 
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     note_launch();
-    return cudaLaunchKernelEx(&cfg, append_kernel, k_new, v_new, kv_heads, dim, tail_cap, k_tail, v_tail, tail_len);
+    return cudaLaunchKernelEx(&cfg, append_kernel, k_new, v_new, kv_heads, dim, tail_cap, k_tail, v_tail, tail_len,
+                              overflow);
 }
 
 }  // namespace kvqb

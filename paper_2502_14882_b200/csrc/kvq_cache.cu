@@ -8,8 +8,26 @@
 namespace kvqb::capi {
 
 
+// The host tail counter from the device (after any stream / graph work on the cache):
+// appends issued on user streams or replayed from captured graphs advance tail_len on the
+// device only. A set overflow flag means appends were dropped at a full tail (k3_append.cu):
+// reported once as a domain_error.
+void sync_tail(kvq_cache* c) {
+    if (!c->tail_len.p) return;
+    ck(cudaDeviceSynchronize(), "kernel execution");
+    std::vector<int> h(c->batch + 1);
+    ck(cudaMemcpy(h.data(), c->tail_len.p, sizeof(int) * (c->batch + 1), cudaMemcpyDeviceToHost), "D2H");
+    c->n_tail = (size_t)h[0];  // every request holds the same number of tail rows
+    if (h[c->batch]) {
+        ck(cudaMemset(c->overflow_flag(), 0, sizeof(int)), "memset");
+        raise(KVQ_ERR_DOMAIN, "append: fp32 tail full (tail_cap rows); appends issued past it on the device "
+                              "(e.g. a captured decode + append graph replayed beyond reserve_tail) were dropped");
+    }
+}
+
 void grow_tail(kvq_cache* c, size_t need) {
     if (need <= c->tail_cap) return;
+    sync_tail(c);  // rows appended on the device only must move too
     size_t cap = c->tail_cap ? c->tail_cap : 16;
     while (cap < need) cap *= 2;
     DevBuf<float> nk(c->units * cap * c->dim), nv(c->units * cap * c->dim);
@@ -163,8 +181,9 @@ void run_decode(kvq_cache* c, const float* q, float* out, bool want_weights, boo
         if (c->tail_part.n < c->units * c->group * 130) c->tail_part.alloc(c->units * c->group * 130);
         a.tail_lse = c->lse.p;
     }
-    const int tc_kind = plain && c->path != KVQ_PATH_GENERIC && c->path != KVQ_PATH_UMMA ? pick_tensor_decode(c, a, s)
-                                                                                        : -1;
+    const bool generic_only = c->path == KVQ_PATH_GENERIC || c->path == KVQ_PATH_UMMA || c->path == KVQ_PATH_DEQUANT;
+    const int tc_kind = plain && !generic_only ? pick_tensor_decode(c, a, s) : -1;
+    a.dequant_dot = c->path == KVQ_PATH_DEQUANT ? 1 : 0;
     // Probability-row / violation export (decode_step_detailed) is a generic-path feature:
     // an explicit tensor-core path selection applies to plain decodes only.
     if (c->path == KVQ_PATH_UMMA && !umma_ok && plain)
@@ -207,7 +226,8 @@ void run_decode(kvq_cache* c, const float* q, float* out, bool want_weights, boo
         return;
     }
     // A pure fp32 cache (build_full_precision): the tail pass is the whole decode.
-    if (plain && c->n_vis == 0 && c->path != KVQ_PATH_GENERIC && kvqb::decode_tail_supported(a)) {
+    if (plain && c->n_vis == 0 && c->path != KVQ_PATH_GENERIC && c->path != KVQ_PATH_DEQUANT &&
+        kvqb::decode_tail_supported(a)) {
         ck(kvqb::launch_decode_tail(a, false, s), "decode (tail)");
         return;
     }
@@ -259,8 +279,8 @@ kvq_cache* build_common(size_t batch, size_t kv_heads, size_t group, size_t n_vi
     c->stats.alloc(4 * c->units * dim);
     ck(cudaMemsetAsync(c->stats.p, 0, sizeof(float) * c->stats.n, c->stream), "memset");
     c->codes.alloc(2 * c->units * c->n_vis * c->rb);
-    c->tail_len.alloc(batch);
-    ck(cudaMemsetAsync(c->tail_len.p, 0, sizeof(int) * batch, c->stream), "memset");
+    c->tail_len.alloc(batch + 1);  // + the append overflow flag
+    ck(cudaMemsetAsync(c->tail_len.p, 0, sizeof(int) * (batch + 1), c->stream), "memset");
     c->d_q.alloc(c->q_elems());
     c->d_out.alloc(c->q_elems());
     c->d_knew.alloc(c->units * dim);
@@ -363,7 +383,8 @@ size_t step_chunks(const kvq_cache* c);
 // The chunk count a step will actually use: chunking needs the tensor-core decode.
 size_t step_chunks_for(kvq_cache* c) {
     size_t chunks = step_chunks(c);
-    if (chunks <= 1 || c->path == KVQ_PATH_GENERIC || c->path == KVQ_PATH_UMMA) return 1;
+    if (chunks <= 1 || c->path == KVQ_PATH_GENERIC || c->path == KVQ_PATH_UMMA || c->path == KVQ_PATH_DEQUANT)
+        return 1;
     kvqb::DecodeArgs a = decode_args(c, c->d_q.p, c->d_out.p);
     if (c->tail_cap > kvqb::kTcTailMax && kvqb::decode_tail_supported(a)) {
         if (c->lse.n < c->units * c->group) c->lse.alloc(c->units * c->group);
@@ -445,7 +466,7 @@ void issue_step(kvq_cache* c, const float* queries, const float* k_new, const fl
     ck(cudaEventRecord(c->ev_join, d2h), "event");
     ck(cudaStreamWaitEvent(s, c->ev_kv, 0), "event");
     ck(kvqb::launch_append(c->d_knew.p, c->d_vnew.p, c->batch, c->kv_heads, c->dim, c->tail_cap, c->k_tail.p,
-                           c->v_tail.p, c->tail_len.p, s), "append");
+                           c->v_tail.p, c->tail_len.p, c->overflow_flag(), s), "append");
     ck(cudaStreamWaitEvent(s, c->ev_join, 0), "event");
 }
 
@@ -552,24 +573,29 @@ int kvq_cache_build_device(const float* k_vis, const float* v_vis, size_t batch,
 
 void kvq_cache_free(kvq_cache* c) { delete c; }
 
+int kvq_cache_sync_tail(kvq_cache* c) {
+    return guarded([&] { sync_tail(c); });
+}
+
 int kvq_cache_reserve_tail(kvq_cache* c, size_t rows) {
     return guarded([&] { grow_tail(c, rows); });
 }
 
 int kvq_cache_set_path(kvq_cache* c, int path) {
     return guarded([&] {
-        if (path < KVQ_PATH_AUTO || path > KVQ_PATH_WS) raise(KVQ_ERR_CONFIG, "unknown decode path");
+        if (path < KVQ_PATH_AUTO || path > KVQ_PATH_DEQUANT) raise(KVQ_ERR_CONFIG, "unknown decode path");
         c->path = path;
     });
 }
 
 int kvq_cache_append(kvq_cache* c, const float* k_new, const float* v_new) {
     return guarded([&] {
+        sync_tail(c);
         grow_tail(c, c->n_tail + 1);
         c->d_knew.upload(k_new, c->units * c->dim, c->stream);
         c->d_vnew.upload(v_new, c->units * c->dim, c->stream);
         ck(kvqb::launch_append(c->d_knew.p, c->d_vnew.p, c->batch, c->kv_heads, c->dim, c->tail_cap,
-                               c->k_tail.p, c->v_tail.p, c->tail_len.p, c->stream), "append");
+                               c->k_tail.p, c->v_tail.p, c->tail_len.p, c->overflow_flag(), c->stream), "append");
         sync(c->stream);
         c->n_tail += 1;
     });
@@ -582,13 +608,14 @@ int kvq_cache_append_device(kvq_cache* c, const float* k_new, const float* v_new
             grow_tail(c, c->n_tail + 1);
         }
         ck(kvqb::launch_append(k_new, v_new, c->batch, c->kv_heads, c->dim, c->tail_cap, c->k_tail.p,
-                               c->v_tail.p, c->tail_len.p, (cudaStream_t)stream), "append");
+                               c->v_tail.p, c->tail_len.p, c->overflow_flag(), (cudaStream_t)stream), "append");
         c->n_tail += 1;
     });
 }
 
 int kvq_cache_decode(kvq_cache* c, const float* queries, float* out, float* weights, size_t* slope_violations) {
     return guarded([&] {
+        if (weights) sync_tail(c);  // the probability rows are n_vis + n_tail long
         c->d_q.upload(queries, c->q_elems(), c->stream);
         run_decode(c, c->d_q.p, c->d_out.p, weights != nullptr, slope_violations != nullptr, c->stream);
         c->d_out.download(out, c->q_elems(), c->stream);
@@ -633,7 +660,10 @@ int kvq_cache_step(kvq_cache* c, const float* queries, const float* k_new, const
     });
 }
 
-int kvq_cache_info(const kvq_cache* c, size_t info[10]) {
+int kvq_cache_info(const kvq_cache* cc, size_t info[10]) {
+    kvq_cache* c = const_cast<kvq_cache*>(cc);  // the tail counter is a host mirror of device state
+    const int st = guarded([&] { sync_tail(c); });
+    if (st != KVQ_OK) return st;
     info[0] = c->batch;
     info[1] = c->kv_heads;
     info[2] = c->group;
@@ -653,8 +683,11 @@ int kvq_cache_calibration(const kvq_cache* c, float tau[2]) {
     return KVQ_OK;
 }
 
-int kvq_cache_memory(const kvq_cache* c, size_t mem[6]) {
+int kvq_cache_memory(const kvq_cache* cc, size_t mem[6]) {
     // HybridKVCache::memory (kvcache.hpp:123-135), summed over every unit.
+    kvq_cache* c = const_cast<kvq_cache*>(cc);
+    const int st = guarded([&] { sync_tail(c); });
+    if (st != KVQ_OK) return st;
     mem[0] = 2 * c->units * c->n_vis * c->rb;
     mem[1] = c->units * 4 * 4 * c->dim;
     mem[2] = mem[0] + mem[1];
@@ -678,8 +711,10 @@ int kvq_cache_read_segment(const kvq_cache* c, size_t unit, int which, uint8_t* 
     });
 }
 
-int kvq_cache_read_tail(const kvq_cache* c, size_t unit, int which, float* out) {
+int kvq_cache_read_tail(const kvq_cache* cc, size_t unit, int which, float* out) {
+    kvq_cache* c = const_cast<kvq_cache*>(cc);
     return guarded([&] {
+        sync_tail(c);
         if (unit >= c->units) raise(KVQ_ERR_DOMAIN, "tail index out of range");
         const float* src = (which == 0 ? c->k_tail.p : c->v_tail.p) + unit * c->tail_cap * c->dim;
         if (c->n_tail)

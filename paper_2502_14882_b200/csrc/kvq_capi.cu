@@ -30,6 +30,15 @@ unsigned long long kvq_last_error_offset(void) { return g_err_offset; }
 
 unsigned long long kvq_launch_count(void) { return kvqb::launch_count(); }
 
+int kvq_set_device(int device) {
+    return guarded([&] {
+        int n = 0;
+        ck(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
+        if (device < 0 || device >= n) raise(KVQ_ERR_DOMAIN, "set_device: no such CUDA device");
+        ck(cudaSetDevice(device), "cudaSetDevice");
+    });
+}
+
 int kvq_device_available(void) {
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess) {

@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 #include <cstddef>
 #include <cstdint>
+#include <mutex>
 
 namespace kvqb {
 
@@ -82,6 +83,8 @@ struct DecodeArgs {
                           // split (and so the summation order) is the whole batch's
     size_t unit_base;     // first unit of this launch within the plan_units batch (chunks)
     int split_override;   // tensor-core decode: force this cluster size (0 = plan)
+    int dequant_dot;      // generic path: dequantize-then-dot (BASELINE config 3's "without
+                          // post-scaling" ablation) instead of the post-scaled products
     int dep_wait_at_end;  // tensor-core decode launched behind a sibling grid: skip the early
                           // dependency wait (the sibling did it), wait at exit instead
     int bits, word_bits;
@@ -155,11 +158,29 @@ cudaError_t launch_mse_report(const float* queries, const float* keys, size_t he
                               unsigned long long* counts, double* mse_q, double* mse_qc, cudaStream_t s);
 
 // ---- K3: append --------------------------------------------------------------
+// `overflow` (device int) is set instead of writing past tail_cap.
 cudaError_t launch_append(const float* k_new, const float* v_new, size_t batch, size_t kv_heads,
                           size_t dim, size_t tail_cap, float* k_tail, float* v_tail,
-                          int* tail_len, cudaStream_t s);
+                          int* tail_len, int* overflow, cudaStream_t s);
 
 // ---- misc -------------------------------------------------------------------------
+// Kernel function attributes (dynamic shared memory above 48 KB, non-portable cluster
+// sizes) are per device: `set` runs once per (kernel instantiation, device), under a lock so
+// concurrent first launches from several host threads never race past it.
+template <typename F>
+inline cudaError_t once_per_device(unsigned& mask, F&& set) {
+    static std::mutex m;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev >= 32) return set();
+    std::lock_guard<std::mutex> lock(m);
+    if (mask & (1u << dev)) return cudaSuccess;
+    e = set();
+    if (e == cudaSuccess) mask |= 1u << dev;
+    return e;
+}
+
 // Number of this library's kernels launched so far (bench.py's gpu_launches claim).
 unsigned long long launch_count();
 void note_launch(unsigned n = 1);

@@ -168,11 +168,15 @@ TensorInfo read_tensor(Reader& r) {
 extern "C" {
 
 int kvq_cache_image_bytes(const kvq_cache* c, size_t* bytes) {
-    return guarded([&] { *bytes = kCacheHeader + c->units * Record(c).bytes; });
+    return guarded([&] {
+        sync_tail(const_cast<kvq_cache*>(c));  // tail rows appended on the device count too
+        *bytes = kCacheHeader + c->units * Record(c).bytes;
+    });
 }
 
 int kvq_cache_save_image(const kvq_cache* c, void* image, size_t capacity, int image_on_device, void* stream) {
     return guarded([&] {
+        sync_tail(const_cast<kvq_cache*>(c));
         const Record r(c);
         const size_t total = kCacheHeader + c->units * r.bytes;
         if (capacity < total) raise(KVQ_ERR_DOMAIN, "cache save: image buffer too small");

@@ -71,6 +71,8 @@ def lib() -> C.CDLL:
             "kvq_last_error": (_SZ, [C.c_char_p, _SZ]),
             "kvq_launch_count": (C.c_ulonglong, []),
             "kvq_device_available": (C.c_int, []),
+            "kvq_set_device": (C.c_int, [C.c_int]),
+            "kvq_cache_sync_tail": (C.c_int, [_VP]),
             "kvq_packed_bytes": (_SZ, [_SZ, C.c_int, C.c_int]),
             "kvq_pack": (C.c_int, [_U32, _SZ, C.c_int, C.c_int, _U8, _SZ]),
             "kvq_unpack": (C.c_int, [_U8, _SZ, _SZ, C.c_int, C.c_int, _U32]),
@@ -148,6 +150,11 @@ def launch_count() -> int:
 
 def device_available() -> bool:
     return bool(lib().kvq_device_available())
+
+
+def set_device(device: int) -> None:
+    """Bind this thread's CUDA device for the library (one process per GPU)."""
+    _check(lib().kvq_set_device(int(device)))
 
 
 # ---- bitpack.hpp -----------------------------------------------------------------------
@@ -762,7 +769,7 @@ class DecodeDetail:
     slope_violations: int = 0
 
 
-PATH_AUTO, PATH_GENERIC, PATH_TC, PATH_UMMA, PATH_HC, PATH_WS = 0, 1, 2, 3, 4, 5
+PATH_AUTO, PATH_GENERIC, PATH_TC, PATH_UMMA, PATH_HC, PATH_WS, PATH_DEQUANT = 0, 1, 2, 3, 4, 5, 6
 
 
 class BatchedCache:
@@ -918,8 +925,20 @@ class BatchedCache:
         return out, w, int(viol.value)
 
     def step(self, queries, k_new, v_new, out: np.ndarray) -> None:
-        """decode then append through host buffers, one synchronization (kvq_cache_step)."""
+        """decode then append through host buffers, one synchronization (kvq_cache_step).
+        The buffers are used in place (and a CUDA graph of the step is cached per buffer
+        set), so they must be C-contiguous float32 of exactly the step's sizes."""
+        nq, nkv = self.units * self.group * self.dim, self.units * self.dim
+        for name, arr, n in (("queries", queries, nq), ("k_new", k_new, nkv), ("v_new", v_new, nkv), ("out", out, nq)):
+            if not (isinstance(arr, np.ndarray) and arr.dtype == np.float32 and arr.flags.c_contiguous):
+                raise DomainError(f"step: {name} must be a C-contiguous float32 numpy array")
+            if arr.size != n:
+                raise DomainError(f"step: {name} has {arr.size} elements, expected {n}")
         _check(lib().kvq_cache_step(self._h, _fp(queries), _fp(k_new), _fp(v_new), _fp(out)))
+
+    def sync_tail(self) -> None:
+        """Reconcile the host tail counter with the device (after graph replays)."""
+        _check(lib().kvq_cache_sync_tail(self._h))
 
     # -- hot path (device tensors)
     def decode_device(self, q, out, stream: int = 0) -> None:

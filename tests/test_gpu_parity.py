@@ -359,8 +359,10 @@ def test_batched_gqa_vs_oracle(kvq, oracle, bits, G, n):
         q = rng.normal(size=(B, H, G, d)).astype(np.float32)
         want = _oracle_batched(oracle, k, v, q, bits, tau,
                                np.stack(tk) if tk else None, np.stack(tv) if tv else None)
+        # PATH_DEQUANT: BASELINE c3's "without post-scaling" ablation (dequantize-then-dot),
+        # the same attention up to fp32 reassociation
         for path, tol in ((kvq.PATH_GENERIC, TOL_GENERIC), (kvq.PATH_TC, TOL_IMMA), (kvq.PATH_UMMA, TOL_TC),
-                          (kvq.PATH_HC, TOL_IMMA), (kvq.PATH_AUTO, TOL_IMMA)):
+                          (kvq.PATH_HC, TOL_IMMA), (kvq.PATH_DEQUANT, 1e-4), (kvq.PATH_AUTO, TOL_IMMA)):
             cache.set_path(path)
             try:
                 out, _, _ = cache.decode(q)

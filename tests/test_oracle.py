@@ -336,3 +336,20 @@ def test_report_csv_writers(tmp_path):
     assert lines[1:4] == ["exact,0,-1,0.5,1", "exact,0,0.5,2,2", "quant,0,-1,0.5,3"]
     with pytest.raises(kvq.FormatError):
         kvq.write_mse_csv(tmp_path / "missing" / "x.csv", rep)
+
+
+def test_reference_dequant_then_dot_arm_matches_post_scaled(ref):
+    """The bench's "without post-scaling" CPU arm (dequantize + naive_qk / naive_wv around the
+    calibrated softmax, BASELINE config 3) computes the same attention as the reference's
+    post-scaled decode_step, up to fp32 reassociation."""
+    rng = np.random.default_rng(33)
+    R, H, G, n, d = 2, 2, 2, 300, 32
+    k = rng.normal(size=(R, H, n, d)).astype(np.float32)
+    v = rng.normal(size=(R, H, n, d)).astype(np.float32)
+    q = rng.normal(size=(R, H, G, d)).astype(np.float32)
+    kn = rng.normal(size=(R, H, d)).astype(np.float32)
+    for bits, wb in ((1, 8), (2, 32), (4, 32)):
+        _, post = ref.bench_decode(k, v, R, H, G, n, d, bits, wb, 1.0, 0.0, q, kn, kn, 2, 2, prefill_tail=3)
+        _, deq = ref.bench_decode(k, v, R, H, G, n, d, bits, wb, 1.0, 0.0, q, kn, kn, 2, 2, prefill_tail=3,
+                                  dequant=True)
+        assert np.linalg.norm(post - deq) / np.linalg.norm(post) < 1e-5, bits

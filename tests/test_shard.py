@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 import torch.multiprocessing as mp
 
-from paper_2502_14882_b200.shard import ShardSpec, ShardedCache, partition
+from paper_2502_14882_b200.shard import ShardSpec, ShardedCache, assign_units, partition
 
 
 def test_partition_covers_batch_contiguously():
@@ -20,6 +20,20 @@ def test_partition_covers_batch_contiguously():
             assert all(a[1] == b[0] for a, b in zip(parts, parts[1:]))
             sizes = [e - s for s, e in parts]
             assert max(sizes) - min(sizes) <= 1
+
+
+def test_assign_units_requests_then_round_robin():
+    # batch >= world: contiguous request slices with all KV heads
+    shares = assign_units(5, 2, 2)
+    assert shares[0] == [(0, 0), (0, 1), (1, 0), (1, 1), (2, 0), (2, 1)] and shares[1][0] == (3, 0)
+    # batch < world: (request, KV head) units dealt round-robin - no idle rank while units remain
+    for batch, heads, world in ((1, 8, 8), (1, 2, 4), (3, 8, 4), (2, 3, 8)):
+        shares = assign_units(batch, heads, world)
+        flat = sorted(u for s in shares for u in s)
+        assert flat == [(b, h) for b in range(batch) for h in range(heads)]
+        sizes = [len(s) for s in shares]
+        assert max(sizes) - min(sizes) <= 1
+        assert min(sizes) > 0 or batch * heads < world
 
 
 class OracleCache:
@@ -60,6 +74,7 @@ class OracleCache:
 
 
 def make_problem(seed=5, B=5, H=2, G=2, n=40, d=16, steps=2):
+    B = int(os.environ.get("KVQ_TEST_SHARD_B", B))
     rng = np.random.default_rng(seed)
     k = rng.normal(size=(B, H, n, d)).astype(np.float32)
     v = rng.normal(size=(B, H, n, d)).astype(np.float32)
@@ -97,7 +112,10 @@ def _free_port():
 
 
 @pytest.mark.timeout(300)
-def test_two_rank_gloo_matches_single_process(tmp_path):
+@pytest.mark.parametrize("batch", [5, 1])
+def test_two_rank_gloo_matches_single_process(tmp_path, monkeypatch, batch):
+    """batch 5 on 2 ranks: request slices; batch 1: the 2 units round-robin, one per rank."""
+    monkeypatch.setenv("KVQ_TEST_SHARD_B", str(batch))
     result = tmp_path / "out.npy"
     mp.spawn(_worker, args=(2, _free_port(), str(result)), nprocs=2, join=True)
     sharded = np.load(result)
