@@ -504,10 +504,13 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
                 for (int u2 = 0; u2 < 2; ++u2) {
 #pragma unroll
                     for (int hf = 0; hf < 2; ++hf) {
-                        // digit planes 0..3 of head t, token g (+8): wrapping int32 sum, exact total
-                        const int total = ac[hg][u2][0][2 * hf] + ac[hg][u2][0][2 * hf + 1] * 256 +
-                                          ac[hg][u2][1][2 * hf] * 65536 + ac[hg][u2][1][2 * hf + 1] * (1 << 24);
-                        sc[2 * u2 + hf] = __fmaf_rn((float)total, cA[hg], cB[hg]);
+                        // digit planes 0..3 of head t, token g (+8): the plane sums combine
+                        // modulo 2^32 (unsigned: defined wrap-around); the total is exact in int32
+                        const uint32_t total = (uint32_t)ac[hg][u2][0][2 * hf] +
+                                               ((uint32_t)ac[hg][u2][0][2 * hf + 1] << 8) +
+                                               ((uint32_t)ac[hg][u2][1][2 * hf] << 16) +
+                                               ((uint32_t)ac[hg][u2][1][2 * hf + 1] << 24);
+                        sc[2 * u2 + hf] = __fmaf_rn((float)(int)total, cA[hg], cB[hg]);
                     }
                 }
                 if (tbase_tok + 32 <= nv) {  // full step (warp-uniform): min/max trees, no checks
