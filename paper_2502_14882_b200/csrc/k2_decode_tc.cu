@@ -1133,6 +1133,7 @@ cudaError_t launch_decode_tc(const DecodeArgs& a, cudaStream_t s) {
             cudaError_t e = launch_nt(A, 1, s);
             if (e != cudaSuccess || cut == a.units) return e;
             B.dep_wait_at_end = 1;  // launched behind A (see the kernel's dependency wait)
+            if (B.trace) B.trace += cut * 256;  // debug timelines: A's CTAs first, then B's
         }
         return launch_nt(B, 1, s);
     }

@@ -138,6 +138,17 @@ int pick_tensor_decode(kvq_cache* c, kvqb::DecodeArgs& a, cudaStream_t s) {
             raise(KVQ_ERR_CONFIG, "ws decode path needs dim 128, 1/2/4-bit codes, at most 4 query heads per KV "
                                   "head, n <= 8192, >= 296 units, a quantized prefill and no weight/violation export");
     }
+    if (c->path == KVQ_PATH_PS) {
+        kvqb::DecodeArgs probe = a;
+        probe.v_codes_x = reinterpret_cast<const uint8_t*>(1);
+        if (kvqb::decode_ps_supported(probe)) {
+            ensure_vx(c, s);
+            a.v_codes_x = c->vx.p;
+            return KVQ_PATH_PS;
+        }
+        raise(KVQ_ERR_CONFIG, "ps decode path needs dim 128, 1/2/4-bit codes, at most 4 query heads per KV head, "
+                              "n <= 4096 with n % 128 == 0, a quantized prefill and no weight/violation export");
+    }
     if (c->path == KVQ_PATH_HC) {
         kvqb::DecodeArgs probe = a;
         probe.v_codes_x2 = reinterpret_cast<const uint8_t*>(1);
@@ -163,6 +174,7 @@ int pick_tensor_decode(kvq_cache* c, kvqb::DecodeArgs& a, cudaStream_t s) {
 
 void launch_tensor_decode(int kind, const kvqb::DecodeArgs& a, cudaStream_t s) {
     if (kind == KVQ_PATH_WS) ck(kvqb::launch_decode_ws(a, s), "decode (ws)");
+    else if (kind == KVQ_PATH_PS) ck(kvqb::launch_decode_ps(a, s), "decode (ps)");
     else if (kind == KVQ_PATH_HC) ck(kvqb::launch_decode_hc(a, s), "decode (hc)");
     else ck(kvqb::launch_decode_tc(a, s), "decode (tc)");
 }
@@ -583,7 +595,7 @@ int kvq_cache_reserve_tail(kvq_cache* c, size_t rows) {
 
 int kvq_cache_set_path(kvq_cache* c, int path) {
     return guarded([&] {
-        if (path < KVQ_PATH_AUTO || path > KVQ_PATH_DEQUANT) raise(KVQ_ERR_CONFIG, "unknown decode path");
+        if (path < KVQ_PATH_AUTO || path > KVQ_PATH_PS) raise(KVQ_ERR_CONFIG, "unknown decode path");
         c->path = path;
     });
 }

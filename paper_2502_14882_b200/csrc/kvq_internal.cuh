@@ -119,6 +119,11 @@ bool decode_hc_supported(const DecodeArgs& a);
 // SM pipelined over units through two tensor-memory banks; vx layout; d = 128, b <= 4,
 // G <= 4, n <= 8192, at least two units per SM.
 bool decode_ws_supported(const DecodeArgs& a);
+// Persistent SM-level IMMA decode (k2_decode_ps.cu): one 16-warp CTA per SM, dynamic chunk
+// queues per tensor-memory lane quarter, rounds of up to 4 units; vx layout; d = 128,
+// b <= 4, G <= 4, n <= 4096 with n % 128 == 0.
+bool decode_ps_supported(const DecodeArgs& a);
+cudaError_t launch_decode_ps(const DecodeArgs& a, cudaStream_t s);
 size_t decode_ws_scratch_bytes(size_t units);
 cudaError_t launch_decode_ws(const DecodeArgs& a, cudaStream_t s);
 cudaError_t launch_decode_hc(const DecodeArgs& a, cudaStream_t s);

@@ -24,6 +24,10 @@ case "$cmd" in
       > gpurun_out/launches.log 2>&1 ;;
   trace)
     timeout 300 python tools/trace_tc.py "$1" "$2" > gpurun_out/trace_"$1"_"$2".txt 2>&1 ;;
+  trace2)
+    timeout 300 python tools/trace_tc2.py "$1" > gpurun_out/trace2_"$1".txt 2>&1 ;;
+  traceps)
+    timeout 300 python tools/trace_ps.py "$1" > gpurun_out/traceps_"$1".txt 2>&1 ;;
   tracews)
     timeout 300 python tools/trace_ws.py "$1" > gpurun_out/tracews_"$1".txt 2>&1 ;;
 esac
