@@ -85,7 +85,7 @@ def resolve_config(name: str):
 
 
 DIM = 128
-PATHS = {"auto": 0, "generic": 1, "tc": 2, "umma": 3, "hc": 4, "ws": 5, "dequant": 6, "ps": 7}  # KVQ_PATH_* (include/kvq_capi.h)
+PATHS = {"auto": 0, "generic": 1, "tc": 2, "umma": 3, "dequant": 4}  # KVQ_PATH_* (include/kvq_capi.h)
 TAIL_WINDOW = 32
 L2_BYTES = 126 * 1024 * 1024
 

@@ -45,10 +45,7 @@ extern "C" {
 #define KVQ_PATH_GENERIC 1 /* any shape; also the path that emits probability rows */
 #define KVQ_PATH_TC 2      /* d = 128, M = 8 legacy mma.sync IMMA path (KVQ_ERR_CONFIG otherwise) */
 #define KVQ_PATH_UMMA 3    /* d = 128, M = 8 tcgen05 UTCIMMA path (KVQ_ERR_CONFIG otherwise) */
-#define KVQ_PATH_HC 4      /* d = 128, b <= 4, G <= 4 8-warp channel-split IMMA path (KVQ_ERR_CONFIG otherwise) */
-#define KVQ_PATH_PS 7      /* d = 128, b <= 4, G <= 4, n <= 4096, n % 128 == 0: persistent SM-level IMMA path */
-#define KVQ_PATH_DEQUANT 6 /* BASELINE c3 ablation: generic decode, dequantize-then-dot (no post-scaling) */
-#define KVQ_PATH_WS 5      /* d = 128, b <= 4, G <= 4, n <= 8192, >= 296 units: persistent warp-specialized IMMA path */
+#define KVQ_PATH_DEQUANT 4 /* BASELINE c3 ablation: generic decode, dequantize-then-dot (no post-scaling) */
 
 /* ---- diagnostics ------------------------------------------------------------ */
 /* Copies the calling thread's last error message (NUL-terminated, truncated to cap);

@@ -156,8 +156,7 @@ struct kvq_cache {
     StepKey step_key;
     DevBuf<uint8_t> codes;   // [2][units][n_vis][rb]  (K then V)
     DevBuf<uint8_t> vt;      // token-packed V codes for the tcgen05 decode (d = 128, M = 8)
-    DevBuf<uint8_t> vx;      // V codes pre-arranged as IMMA operands for the first IMMA decode
-    DevBuf<uint8_t> vx2;     // the same words in channel halves for the hc decode (default)
+    DevBuf<uint8_t> vx;      // V codes pre-arranged as IMMA operands for the default decode
     DevBuf<float> stats;     // [2 (K,V)][2 (alpha,beta)][units][dim]
     DevBuf<float> k_tail, v_tail;  // [units][tail_cap][dim]
     DevBuf<float> lse;             // [units][group] decode log-sum-exp for the tail pass
@@ -205,7 +204,6 @@ void run_decode(kvq_cache* c, const float* q, float* out, bool want_weights, boo
 kvq_cache* build_common(size_t batch, size_t kv_heads, size_t group, size_t n_vis, size_t dim, int bitwidth,
                         int mode, int word_bits, float tau1, float tau2);
 void ensure_vx(kvq_cache* c, cudaStream_t s);
-void ensure_vx2(kvq_cache* c, cudaStream_t s);
 void ensure_vt(kvq_cache* c, cudaStream_t s);
 
 }  // namespace kvqb::capi

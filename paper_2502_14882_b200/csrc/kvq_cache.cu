@@ -103,7 +103,6 @@ void traced(kvq_cache* c, kvqb::DecodeArgs& a, cudaStream_t s, F&& launch) {
 
 void ensure_vt(kvq_cache* c, cudaStream_t s);
 void ensure_vx(kvq_cache* c, cudaStream_t s);
-void ensure_vx2(kvq_cache* c, cudaStream_t s);
 
 // Long tails: the tail pass chained behind the decode (programmatic dependent launch) is
 // the default; KVQ_TAIL_CONCURRENT=1 runs it on its own stream beside the decode with a
@@ -114,55 +113,15 @@ static bool tail_concurrent() {
     return env ? std::atoi(env) != 0 : false;
 }
 
-// The tensor-core decode kernel a plain decode of this cache runs: KVQ_PATH_TC (the per-CTA
-// IMMA kernel, k2_decode_tc.cu), KVQ_PATH_WS (persistent warp-specialized, k2_decode_ws.cu),
-// KVQ_PATH_HC (8-warp channel-split, k2_decode_hc.cu), or -1 (none applies). Builds the V
-// operand layout the chosen kernel reads (vx / vx2) on first use.
+// The tensor-core decode a plain decode of this cache runs: KVQ_PATH_TC (the IMMA kernel,
+// k2_decode_tc.cu), or -1 (the shape needs another path). Builds the V operand layout it
+// reads (vx) on first use. (Round 2 measured three alternative schedules of the same
+// kernel - channel-split 8-warp CTAs, persistent warp-specialized, persistent with dynamic
+// chunk queues - all slower at every BASELINE shape: profiles/r02_decode_variants.md.)
 int pick_tensor_decode(kvq_cache* c, kvqb::DecodeArgs& a, cudaStream_t s) {
-    // AUTO runs the per-CTA IMMA kernel: the ws and hc kernels are correct but measured
-    // slower at every BASELINE shape (profiles/r02_ws_trace_c2.txt, r02_hc_*), so they are
-    // selected explicitly only.
-    if (c->path == KVQ_PATH_WS) {
-        kvqb::DecodeArgs probe = a;
-        probe.v_codes_x = reinterpret_cast<const uint8_t*>(1);  // shape check only
-        if (kvqb::decode_ws_supported(probe)) {
-            ensure_vx(c, s);
-            a.v_codes_x = c->vx.p;
-            const size_t need = kvqb::decode_ws_scratch_bytes(c->units);
-            if (c->tc_scratch.n < need) c->tc_scratch.alloc(need);
-            a.q_frag = reinterpret_cast<uint32_t*>(c->tc_scratch.p);
-            a.q_const = reinterpret_cast<float2*>(c->tc_scratch.p + c->units * 512 * sizeof(uint32_t));
-            return KVQ_PATH_WS;
-        }
-        if (c->path == KVQ_PATH_WS)
-            raise(KVQ_ERR_CONFIG, "ws decode path needs dim 128, 1/2/4-bit codes, at most 4 query heads per KV "
-                                  "head, n <= 8192, >= 296 units, a quantized prefill and no weight/violation export");
-    }
-    if (c->path == KVQ_PATH_PS) {
-        kvqb::DecodeArgs probe = a;
-        probe.v_codes_x = reinterpret_cast<const uint8_t*>(1);
-        if (kvqb::decode_ps_supported(probe)) {
-            ensure_vx(c, s);
-            a.v_codes_x = c->vx.p;
-            return KVQ_PATH_PS;
-        }
-        raise(KVQ_ERR_CONFIG, "ps decode path needs dim 128, 1/2/4-bit codes, at most 4 query heads per KV head, "
-                              "n <= 4096 with n % 128 == 0, a quantized prefill and no weight/violation export");
-    }
-    if (c->path == KVQ_PATH_HC) {
-        kvqb::DecodeArgs probe = a;
-        probe.v_codes_x2 = reinterpret_cast<const uint8_t*>(1);
-        if (kvqb::decode_hc_supported(probe)) {
-            ensure_vx2(c, s);
-            a.v_codes_x2 = c->vx2.p;
-            return KVQ_PATH_HC;
-        }
-        raise(KVQ_ERR_CONFIG, "hc decode path needs dim 128, 1/2/4-bit codes, at most 4 query heads per KV "
-                              "head, a quantized prefill and no weight/violation export");
-    }
     if (c->path == KVQ_PATH_AUTO || c->path == KVQ_PATH_TC) {
         kvqb::DecodeArgs probe = a;
-        probe.v_codes_x = reinterpret_cast<const uint8_t*>(1);
+        probe.v_codes_x = reinterpret_cast<const uint8_t*>(1);  // shape check only
         if (kvqb::decode_tc_supported(probe)) {
             ensure_vx(c, s);
             a.v_codes_x = c->vx.p;
@@ -173,10 +132,8 @@ int pick_tensor_decode(kvq_cache* c, kvqb::DecodeArgs& a, cudaStream_t s) {
 }
 
 void launch_tensor_decode(int kind, const kvqb::DecodeArgs& a, cudaStream_t s) {
-    if (kind == KVQ_PATH_WS) ck(kvqb::launch_decode_ws(a, s), "decode (ws)");
-    else if (kind == KVQ_PATH_PS) ck(kvqb::launch_decode_ps(a, s), "decode (ps)");
-    else if (kind == KVQ_PATH_HC) ck(kvqb::launch_decode_hc(a, s), "decode (hc)");
-    else ck(kvqb::launch_decode_tc(a, s), "decode (tc)");
+    (void)kind;
+    ck(kvqb::launch_decode_tc(a, s), "decode (tc)");
 }
 
 void run_decode(kvq_cache* c, const float* q, float* out, bool want_weights, bool want_viol,
@@ -328,12 +285,6 @@ void ensure_vx(kvq_cache* c, cudaStream_t s) {
     ck(kvqb::launch_pack_vx(c->v_codes(), c->units, c->n_vis, c->bits, c->word_bits, c->vx.p, s), "pack vx");
 }
 
-void ensure_vx2(kvq_cache* c, cudaStream_t s) {
-    if (c->vx2.p || c->dim != 128 || c->n_vis == 0 || c->bits == KVQ_FULL_PRECISION_BITS) return;
-    c->vx2.alloc(kvqb::vx2_bytes(c->units, c->n_vis, c->bits));
-    ck(kvqb::launch_pack_vx2(c->v_codes(), c->units, c->n_vis, c->bits, c->word_bits, c->vx2.p, s), "pack vx2");
-}
-
 void ensure_vt(kvq_cache* c, cudaStream_t s) {
     if (c->vt.p || c->dim != 128 || c->word_bits != 8 || c->n_vis == 0) return;
     c->vt.alloc(kvqb::vt_bytes(c->units, c->n_vis, c->bits));
@@ -370,7 +321,6 @@ kvqb::DecodeArgs range_args(const kvqb::DecodeArgs& a, const kvq_cache* c, size_
     r.k_codes += u0 * c->n_vis * c->rb;
     r.v_codes += u0 * c->n_vis * c->rb;
     if (r.v_codes_x) r.v_codes_x += kvqb::vx_bytes(u0, c->n_vis, c->bits);
-    if (r.v_codes_x2) r.v_codes_x2 += kvqb::vx2_bytes(u0, c->n_vis, c->bits);
     r.k_alpha += u0 * d;
     r.k_beta += u0 * d;
     r.v_alpha += u0 * d;
@@ -595,7 +545,7 @@ int kvq_cache_reserve_tail(kvq_cache* c, size_t rows) {
 
 int kvq_cache_set_path(kvq_cache* c, int path) {
     return guarded([&] {
-        if (path < KVQ_PATH_AUTO || path > KVQ_PATH_PS) raise(KVQ_ERR_CONFIG, "unknown decode path");
+        if (path < KVQ_PATH_AUTO || path > KVQ_PATH_DEQUANT) raise(KVQ_ERR_CONFIG, "unknown decode path");
         c->path = path;
     });
 }

@@ -70,12 +70,9 @@ struct DecodeArgs {
     float* scratch;       // generic path: [units][group][n_vis + tail_cap] score rows
     const uint8_t* v_codes_t;  // umma path: token-packed V codes (vt_layout, k2_decode_umma.cu)
     const uint8_t* v_codes_x;  // tc path: V codes as phase-B MMA operands (vx_layout, k2_decode_tc.cu)
-    const uint8_t* v_codes_x2; // hc path: vx words split in channel halves (vx2 layout, k2_decode_hc.cu)
     uint8_t* umma_qb;     // umma path: [units][NT][128][16] s8 q digit planes (prep kernel)
     float2* tc_qconst;    // umma path: [units][8] per-head score scale / offset (prep kernel)
     unsigned long long* trace;  // nullable: [ctas][64] globaltimer stamps (KVQ_TRACE_FILE)
-    uint32_t* q_frag;     // ws path: [units][512] q digit-plane B fragments (prep kernel, k2_decode_ws.cu)
-    float2* q_const;      // ws path: [units][4] per-head score scale / offset (prep kernel)
     float* tail_lse;      // nullable: the fp32 tail is left to the tail pass (k2_tail.cu); the
                           // decode writes its base-2 log-sum-exp per (unit, head) here
     size_t units, kv_heads, group, dim, n_vis, tail_cap, weights_stride;
@@ -109,24 +106,6 @@ constexpr size_t kTcTailMax = KVQ_TC_TAIL_MAX;  // tail capacity the tensor-core
 size_t vx_bytes(size_t units, size_t n_vis, int bits);
 cudaError_t launch_pack_vx(const uint8_t* rows, size_t units, size_t n_vis, int bits, int word_bits, uint8_t* vx,
                            cudaStream_t s);
-// Second-generation IMMA decode (k2_decode_hc.cu): 8-warp CTAs, p.V in channel halves over
-// the vx2 layout; d = 128, b in {1, 2, 4}, G <= 4.
-size_t vx2_bytes(size_t units, size_t n_vis, int bits);
-cudaError_t launch_pack_vx2(const uint8_t* rows, size_t units, size_t n_vis, int bits, int word_bits, uint8_t* vx2,
-                            cudaStream_t s);
-bool decode_hc_supported(const DecodeArgs& a);
-// Persistent warp-specialized IMMA decode (k2_decode_ws.cu): score warps / value warps per
-// SM pipelined over units through two tensor-memory banks; vx layout; d = 128, b <= 4,
-// G <= 4, n <= 8192, at least two units per SM.
-bool decode_ws_supported(const DecodeArgs& a);
-// Persistent SM-level IMMA decode (k2_decode_ps.cu): one 16-warp CTA per SM, dynamic chunk
-// queues per tensor-memory lane quarter, rounds of up to 4 units; vx layout; d = 128,
-// b <= 4, G <= 4, n <= 4096 with n % 128 == 0.
-bool decode_ps_supported(const DecodeArgs& a);
-cudaError_t launch_decode_ps(const DecodeArgs& a, cudaStream_t s);
-size_t decode_ws_scratch_bytes(size_t units);
-cudaError_t launch_decode_ws(const DecodeArgs& a, cudaStream_t s);
-cudaError_t launch_decode_hc(const DecodeArgs& a, cudaStream_t s);
 // tcgen05 (UTCIMMA) path, d = 128, M = 8: needs the token-packed V copy.
 size_t vt_bytes(size_t units, size_t n_vis, int bits);
 cudaError_t launch_pack_vt(const uint8_t* rows, size_t units, size_t n_vis, int bits, uint8_t* vt, cudaStream_t s);

@@ -769,7 +769,7 @@ class DecodeDetail:
     slope_violations: int = 0
 
 
-PATH_AUTO, PATH_GENERIC, PATH_TC, PATH_UMMA, PATH_HC, PATH_WS, PATH_DEQUANT, PATH_PS = 0, 1, 2, 3, 4, 5, 6, 7
+PATH_AUTO, PATH_GENERIC, PATH_TC, PATH_UMMA, PATH_DEQUANT = 0, 1, 2, 3, 4
 
 
 class BatchedCache:

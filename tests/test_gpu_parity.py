@@ -184,15 +184,13 @@ def _load_inputs(z, oracle):
 
 
 @pytest.mark.parametrize("name", sorted(p.name for p in GOLD.glob("decode_*.npz")))
-@pytest.mark.parametrize("path", ["generic", "auto", "tc", "umma", "hc"])
+@pytest.mark.parametrize("path", ["generic", "auto", "tc", "umma"])
 def test_decode_golden_trajectories(kvq, oracle, name, path):
     z = np.load(GOLD / name)
     h, n, d, bits, wb, steps = z["meta"].tolist()
     t1, t2 = z["tau"].tolist()
-    if path in ("tc", "umma", "hc") and (d != 128 or bits == 16 or n == 0 or (path == "umma" and wb != 8)):
+    if path in ("tc", "umma") and (d != 128 or bits == 16 or n == 0 or (path == "umma" and wb != 8)):
         pytest.skip("tensor-core paths need d = 128 and a quantized prefill (tcgen05: M = 8)")
-    if path == "hc" and bits == 8:
-        pytest.skip("the hc decode covers 1/2/4-bit codes")
     k, v = _load_inputs(z, oracle)
     if bits == 16:
         cache = kvq.HybridKVCache.build_full_precision(list(k), list(v))
@@ -200,14 +198,14 @@ def test_decode_golden_trajectories(kvq, oracle, name, path):
         cache = kvq.HybridKVCache.build(list(k), list(v), kvq.QuantizationConfig(bits, kvq.QuantMode.channel_wise, wb),
                                         kvq.CalibrationParams(t1, t2))
     cache.batched.set_path({"generic": kvq.PATH_GENERIC, "auto": kvq.PATH_AUTO, "tc": kvq.PATH_TC,
-                            "umma": kvq.PATH_UMMA, "hc": kvq.PATH_HC}[path])
+                            "umma": kvq.PATH_UMMA}[path])
     if bits != 16 and n:
         for hh in range(h):
             ks, vs = cache.key_segment(hh), cache.value_segment(hh)
             assert np.array_equal(ks.codes.bytes, z[f"kcodes{hh}"]) and np.array_equal(vs.codes.bytes, z[f"vcodes{hh}"])
             assert bits_eq(ks.stats.alpha, z[f"kalpha{hh}"]) and bits_eq(vs.stats.beta, z[f"vbeta{hh}"])
     assert list(vars(cache.memory()).values()) == z["memory0"].tolist()
-    tol = {"generic": TOL_GENERIC, "tc": TOL_IMMA, "hc": TOL_IMMA, "auto": TOL_IMMA}.get(path, TOL_TC)
+    tol = {"generic": TOL_GENERIC, "tc": TOL_IMMA, "auto": TOL_IMMA}.get(path, TOL_TC)
     for t in range(steps):
         out = cache.decode_step(z[f"q{t}"])
         assert rel_l2(out, z[f"out{t}"]) <= tol, f"{name} step {t}: {rel_l2(out, z[f'out{t}'])}"
@@ -362,16 +360,14 @@ def test_batched_gqa_vs_oracle(kvq, oracle, bits, G, n):
         # PATH_DEQUANT: BASELINE c3's "without post-scaling" ablation (dequantize-then-dot),
         # the same attention up to fp32 reassociation
         for path, tol in ((kvq.PATH_GENERIC, TOL_GENERIC), (kvq.PATH_TC, TOL_IMMA), (kvq.PATH_UMMA, TOL_TC),
-                          (kvq.PATH_HC, TOL_IMMA), (kvq.PATH_DEQUANT, 1e-4), (kvq.PATH_PS, TOL_IMMA),
-                          (kvq.PATH_AUTO, TOL_IMMA)):
+                          (kvq.PATH_DEQUANT, 1e-4), (kvq.PATH_AUTO, TOL_IMMA)):
             cache.set_path(path)
             try:
                 out, _, _ = cache.decode(q)
             except kvq.ConfigError:
-                # the IMMA paths' shared-memory plans do not cover every shape (hc: b <= 4,
-                # G <= 4); every other path must
-                assert path == kvq.PATH_TC or (path == kvq.PATH_HC and (bits == 8 or G > 4)) or \
-                    (path == kvq.PATH_PS and (bits == 8 or G > 4 or n % 128))
+                # the IMMA path's shared-memory plan does not cover every shape; every
+                # other path must
+                assert path == kvq.PATH_TC
                 continue
             err = rel_l2(out, want)
             assert err <= tol, f"path {path} step {step}: rel L2 {err}"
@@ -413,7 +409,7 @@ def test_step_api_matches_decode_then_append(kvq, B, H, n):
 
 
 @pytest.mark.parametrize("name", ["decode_d128_b2_m32.npz", "decode_d128_b4_m32.npz", "decode_d128_b8_m32.npz"])
-@pytest.mark.parametrize("path,wb", [("tc", 8), ("umma", 8), ("tc", 16), ("hc", 8), ("hc", 16)])
+@pytest.mark.parametrize("path,wb", [("tc", 8), ("umma", 8), ("tc", 16)])
 def test_decode_golden_m8_tensor_paths(kvq, oracle, name, path, wb):
     """The b >= 2 golden trajectories were produced by the reference with M = 32 (its M = 8
     table path is defective for b >= 2 at n >= 512). The codes are the
@@ -424,9 +420,7 @@ def test_decode_golden_m8_tensor_paths(kvq, oracle, name, path, wb):
     k, v = _load_inputs(z, oracle)
     cache = kvq.HybridKVCache.build(list(k), list(v), kvq.QuantizationConfig(bits, kvq.QuantMode.channel_wise, wb),
                                     kvq.CalibrationParams(t1, t2))
-    if path == "hc" and bits == 8:
-        pytest.skip("the hc decode covers 1/2/4-bit codes")
-    cache.batched.set_path({"tc": kvq.PATH_TC, "umma": kvq.PATH_UMMA, "hc": kvq.PATH_HC}[path])
+    cache.batched.set_path({"tc": kvq.PATH_TC, "umma": kvq.PATH_UMMA}[path])
     for hh in range(h):
         ka, kb = oracle.compute_stats(k[hh])
         assert np.array_equal(cache.key_segment(hh).codes.bytes, oracle.quantize(k[hh], ka, kb, bits, wb))
@@ -457,11 +451,7 @@ def test_full_size_units_vs_oracle(kvq, oracle, bits, G, n):
         # The fp32 restatement's own error floor grows with n and b (SURVEY.md App. C:
         # 6.8e-5 at b=2, n=4096 vs float64); at these sizes the bar is 5e-4, half of
         # north_star's 1e-3.
-        for path, tol in ((kvq.PATH_TC, 5e-4), (kvq.PATH_UMMA, 5e-4), (kvq.PATH_HC, 5e-4), (kvq.PATH_PS, 5e-4)):
-            if path in (kvq.PATH_HC, kvq.PATH_PS) and (bits == 8 or G > 4):
-                continue
-            if path == kvq.PATH_PS and n > 4096:
-                continue
+        for path, tol in ((kvq.PATH_TC, 5e-4), (kvq.PATH_UMMA, 5e-4)):
             cache.set_path(path)
             out, _, _ = cache.decode(q)
             err = rel_l2(out, want)
@@ -704,12 +694,12 @@ def test_randomized_paths_vs_oracle(kvq, oracle, case):
             for g in range(G):
                 want[b, h, g] = oracle.decode_head(q[b, h, g], n, c["bits"], c["wb"], kc, ka, kb, vc, va, vb, ktail,
                                                    vtail, *c["tau"])[0]
-    for path in (kvq.PATH_AUTO, kvq.PATH_TC, kvq.PATH_UMMA, kvq.PATH_HC, kvq.PATH_PS, kvq.PATH_GENERIC):
+    for path in (kvq.PATH_AUTO, kvq.PATH_TC, kvq.PATH_UMMA, kvq.PATH_GENERIC):
         cache.set_path(path)
         try:
             out, _, _ = cache.decode(q)
         except kvq.ConfigError:
-            assert path in (kvq.PATH_TC, kvq.PATH_UMMA, kvq.PATH_HC, kvq.PATH_PS), "AUTO and GENERIC accept every shape"
+            assert path in (kvq.PATH_TC, kvq.PATH_UMMA), "AUTO and GENERIC accept every shape"
             continue
         # fp32 reduction-order noise grows with n + tail: 1e-4 for the generic path at these
         # sizes (2e-5 on the small golden trajectories), 5e-4 for the tensor-core paths
@@ -770,40 +760,3 @@ def test_sixteen_bit_codes_standalone_kernels(kvq, oracle, word_bits):
     got_o = kvq.wv_output(w, seg)
     want_o = oracle.wv_output(w, seg.codes.bytes, n, d, st.alpha, st.beta, 16, word_bits)
     assert rel_l2(got_o, want_o) <= 1e-6
-
-
-@pytest.mark.parametrize("bits,G,n,tail,B", [(1, 4, 4096, 3, 64), (2, 4, 1024, 0, 40), (4, 2, 2048, 70, 24),
-                                             (1, 1, 128, 5, 8), (2, 3, 4096, 9, 80)])
-def test_persistent_sm_decode_vs_oracle(kvq, oracle, bits, G, n, tail, B):
-    """The persistent SM-level decode (KVQ_PATH_PS: one CTA per SM, dynamic chunk queues,
-    rounds of units): every SM's first / last unit and a spread, vs the C restatement; a
-    70-row tail takes the tail pass; a second decode is bit-identical."""
-    rng = np.random.default_rng(bits * 7 + n + B)
-    H, d = 8, 128
-    k = rng.normal(size=(B, H, n, d)).astype(np.float32)
-    v = rng.normal(size=(B, H, n, d)).astype(np.float32)
-    tau = (1.0, 0.0)
-    cache = kvq.BatchedCache.build(k, v, kvq.QuantizationConfig(bits), kvq.CalibrationParams(*tau), group=G)
-    tk, tv = [], []
-    for _ in range(tail):
-        kn = rng.normal(size=(B, H, d)).astype(np.float32)
-        vn = rng.normal(size=(B, H, d)).astype(np.float32)
-        cache.append(kn, vn)
-        tk.append(kn)
-        tv.append(vn)
-    q = rng.normal(size=(B, H, G, d)).astype(np.float32)
-    cache.set_path(kvq.PATH_PS)
-    out, _, _ = cache.decode(q)
-    again, _, _ = cache.decode(q)
-    assert np.array_equal(out, again)
-    units = B * H
-    for u in sorted({0, 1, 147, 148, units // 2, units - 149, units - 1} & set(range(units))):
-        b, h = divmod(u, H)
-        ka, kb = oracle.compute_stats(k[b, h])
-        va, vb = oracle.compute_stats(v[b, h])
-        kc, vc = oracle.quantize(k[b, h], ka, kb, bits), oracle.quantize(v[b, h], va, vb, bits)
-        kt = np.stack([x[b, h] for x in tk]) if tk else np.zeros((0, d), np.float32)
-        vt = np.stack([x[b, h] for x in tv]) if tv else np.zeros((0, d), np.float32)
-        for g in range(G):
-            want = oracle.decode_head(q[b, h, g], n, bits, 8, kc, ka, kb, vc, va, vb, kt, vt, *tau)[0]
-            assert rel_l2(out[b, h, g], want) <= 5e-4, (u, g, rel_l2(out[b, h, g], want))

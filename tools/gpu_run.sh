@@ -5,6 +5,7 @@
 #   tools/gpu_run.sh ncu   <kernel-regex> [bench.py args...]  -> gpurun_out/prof_<regex>.ncu-rep
 #   tools/gpu_run.sh launches [bench.py args...]   -> gpurun_out/launches.csv (ncu launch list)
 #   tools/gpu_run.sh trace <config> <path-id>      -> gpurun_out/trace_<config>_<path>.txt
+#   tools/gpu_run.sh trace2 <config>               -> gpurun_out/trace2_<config>.txt (both balanced grids)
 # Several commands can be chained with ';' inside one gpurun call.
 mkdir -p gpurun_out
 cmd=$1; shift
@@ -26,8 +27,4 @@ case "$cmd" in
     timeout 300 python tools/trace_tc.py "$1" "$2" > gpurun_out/trace_"$1"_"$2".txt 2>&1 ;;
   trace2)
     timeout 300 python tools/trace_tc2.py "$1" > gpurun_out/trace2_"$1".txt 2>&1 ;;
-  traceps)
-    timeout 300 python tools/trace_ps.py "$1" > gpurun_out/traceps_"$1".txt 2>&1 ;;
-  tracews)
-    timeout 300 python tools/trace_ws.py "$1" > gpurun_out/tracews_"$1".txt 2>&1 ;;
 esac

@@ -36,10 +36,23 @@ def main():
     pat = re.compile(sys.argv[2]) if len(sys.argv) > 2 else None
     rows = list(csv.reader(io.StringIO(ncu(rep, "--page", "raw", "--csv"))))
     hdr, units = rows[0], rows[1]
-    launch = next(r for r in rows[2:] if not pat or pat.search(r[hdr.index("Kernel Name")]))
+    matching = [r for r in rows[2:] if not pat or pat.search(r[hdr.index("Kernel Name")])]
+    launch = matching[0]
     col = dict(zip(hdr, launch))
     unit = dict(zip(hdr, units))
-    out = {"kernel": col["Kernel Name"][:160]}
+    out = {"kernel": col["Kernel Name"][:160], "launches_in_report": len(matching)}
+    # every launch of the report (a balanced decode is two grids): durations and DRAM bytes
+    def num(r, k):
+        try:
+            return float(r[hdr.index(k)].replace(",", ""))
+        except (ValueError, IndexError):
+            return 0.0
+    out["per_launch"] = [{"kernel": r[hdr.index("Kernel Name")][:80], "grid": r[hdr.index("Grid Size")] if "Grid Size" in hdr else None,
+                          "us": num(r, "gpu__time_duration.sum"),
+                          "dram_bytes": num(r, "dram__bytes_read.sum") * (1e6 if unit.get("dram__bytes_read.sum") == "Mbyte" else 1)
+                          + num(r, "dram__bytes_write.sum") * (1e6 if unit.get("dram__bytes_write.sum") == "Mbyte" else
+                                                                1e3 if unit.get("dram__bytes_write.sum") == "Kbyte" else 1)}
+                         for r in matching]
     for k in KEYS:
         if k in col:
             v = col[k].replace(",", "")

@@ -1,5 +1,5 @@
-"""Per-CTA timeline of one IMMA decode launch (KVQ_TRACE_FILE stamps, k2_decode_tc.cu /
-k2_decode_hc.cu).  python tools/trace_tc.py [config] [path: 2 = tc, 4 = hc]"""
+"""Per-CTA timeline of one IMMA decode launch (KVQ_TRACE_FILE stamps, k2_decode_tc.cu).
+python tools/trace_tc.py [config] [path id, default 2 = tc]"""
 import os
 import sys
 from pathlib import Path
