@@ -47,9 +47,8 @@ constexpr int kTailMax = 64;   // fp32 tail tokens per CTA
 constexpr int kMaxCluster = 16;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: float -> int rounding trick
-constexpr float kPScale = 4190000.0f;  // p in [0, 1(+eps)] -> integer < 2^22 (22-bit digits)
-constexpr float kLog2PScale = 21.9985188f;  // log2(kPScale): weights are on the kPScale scale
-constexpr int kPRow = 12;              // words per p-plane smem row (stride avoids bank conflicts)
+constexpr int kPxHead = 24;            // P transpose tile: words per head (2 planes x 8 + pad: no bank conflicts)
+constexpr int kPxWords = 4 * kPxHead;  // one 32-token block of one head group
 
 template <int BITS, int SB = kStageBytes>
 struct Geo {
@@ -146,13 +145,13 @@ constexpr int ring_stages() {
 struct Smem {  // carve-up of the dynamic shared memory of one decode CTA
     uint8_t* ring;       // [kWarps][kStages][kStageBytes]: per-warp TMA landing zones;
                          // after the V stream: the cluster receive buffer
-    uint32_t* acc;       // [NT][16 nc][32 lanes][4]: CTA sum of the warps' p.V accumulators
-    uint32_t* pw;        // [kWarps][2][NT][12][kPRow] p digit planes of a warp's block
+    float* acc;          // [kWarps][NT][16 channel rows][32 lanes]: the warps' p.V partials
+    uint32_t* pw;        // [kWarps][4 blocks][NT][kPxWords] P transpose tiles (prologue scratch first)
     float* tail_s;       // [8][kTailMax] fp32 tail scores (rank 0)
     float* wpart;        // [kWarps][24] per-warp (min, max, tail max) per head
     float* allpart;      // [S][24] per-CTA partials (pushed by every CTA of the cluster)
     float* gpar;         // [8][4] softmax parameters per head
-    uint32_t* wsum;      // [kWarps][8] per-warp u22 weight sums per head
+    float* wsum;         // [kWarps][8] per-warp weight sums per head (unit scale)
     uint64_t* full;      // [kWarps][kStages] TMA completion barriers
     uint32_t* tmem_slot;
 };
@@ -170,8 +169,8 @@ __host__ __device__ inline size_t tc_smem_bytes(int S, Smem* out = nullptr, uint
     const size_t ring_bytes = (size_t)W * ring_stages<BITS, OCC, W>() * stage;
     const size_t tail_use = recv_bytes;
     uint8_t* ring = take(ring_bytes > tail_use ? ring_bytes : tail_use);
-    uint8_t* acc = take((size_t)NT * 16 * 32 * 4 * 4);
-    uint8_t* pw = take((size_t)W * 2 * NT * 12 * kPRow * 4);
+    uint8_t* acc = take((size_t)W * NT * 16 * 32 * 4);
+    uint8_t* pw = take((size_t)W * 4 * NT * kPxWords * 4);
     uint8_t* tail_s = take((size_t)8 * kTailMax * 4);
     uint8_t* wpart = take((size_t)W * 24 * 4);
     uint8_t* allpart = take((size_t)(S > 0 ? S : 1) * 24 * 4);
@@ -181,13 +180,13 @@ __host__ __device__ inline size_t tc_smem_bytes(int S, Smem* out = nullptr, uint
     uint8_t* slot = take(16);
     if (out) {
         out->ring = ring;
-        out->acc = reinterpret_cast<uint32_t*>(acc);
+        out->acc = reinterpret_cast<float*>(acc);
         out->pw = reinterpret_cast<uint32_t*>(pw);
         out->tail_s = reinterpret_cast<float*>(tail_s);
         out->wpart = reinterpret_cast<float*>(wpart);
         out->allpart = reinterpret_cast<float*>(allpart);
         out->gpar = reinterpret_cast<float*>(gpar);
-        out->wsum = reinterpret_cast<uint32_t*>(wsum);
+        out->wsum = reinterpret_cast<float*>(wsum);
         out->full = reinterpret_cast<uint64_t*>(full);
         out->tmem_slot = reinterpret_cast<uint32_t*>(slot);
     }
@@ -215,8 +214,28 @@ __device__ __forceinline__ void tmem_ld4(uint32_t taddr, float (&v)[4]) {
     tmem_ld_wait(r);
     v[0] = __uint_as_float(r[0]), v[1] = __uint_as_float(r[1]), v[2] = __uint_as_float(r[2]), v[3] = __uint_as_float(r[3]);
 }
-__device__ __forceinline__ void red_add_u32(uint32_t* p, uint32_t v) {
-    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+// N consecutive lane-private columns (N = 16 or 32), one load + one wait.
+template <int N>
+__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t (&r)[N]) {
+    static_assert(N == 16 || N == 32, "tmem_ld_cols: 16 or 32 columns");
+    if constexpr (N == 16) {
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+            "tcgen05.wait::ld.sync.aligned;"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+            : "r"(taddr));
+    } else {
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+            "tcgen05.wait::ld.sync.aligned;"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+              "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+              "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+            : "r"(taddr));
+    }
 }
 
 // CTA = W warps (8, or 4 for many short units); warp w owns visual tokens [w T/W, (w+1) T/W)
@@ -288,8 +307,7 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         for (int i = 0; i < min(kStagesW, total_stages); ++i) issue(i);
     }
-    // zero the CTA accumulator image; allocate the lane-private score columns
-    for (int i = threadIdx.x; i < NT * 16 * 32 * 4; i += W * 32) sm.acc[i] = 0u;
+    // allocate the lane-private score columns
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(sm.tmem_slot)),
                      "r"(kTmemCols));
@@ -645,133 +663,158 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
 
     if (threadIdx.x == 0) TTRACE(1);  // softmax parameters known
     // ---------------- phase B: p . V over this warp's tokens ----------------
-    // D[16 head-planes x 8 ch] += P[16 head-planes x 32 tok] * V[32 tok x 8 ch], 16 channel
-    // tiles per 32-token block. Lane (g, t) turns its own four scores of head t (tokens
-    // g, g+8, g+16, g+24 = k-group g) into p = exp(g(s) - m) in [0, 1], a 22-bit integer
-    // split in three u8 planes, and writes them as one word per plane of the P tile (A
-    // rows plane*4 + head, k-group word g). V codes are the B operand: four tokens per
-    // register (PRMT byte transpose) x 2^sh (LOP3 slot select) - never dequantized.
-    int vacc[NT][16][4];
-#pragma unroll
-    for (int mt = 0; mt < NT; ++mt)
-#pragma unroll
-        for (int nc = 0; nc < 16; ++nc)
-#pragma unroll
-            for (int r = 0; r < 4; ++r) vacc[mt][nc][r] = 0;
-    uint32_t wacc[NT];  // sum of this lane's u22 probabilities (head 4 mt + t)
+    // D[16 channels x 8 (head, plane)] += V^T[16 ch x 32 tok] * P[32 tok x 8 (head, plane)]:
+    // 8 channel tiles per 32-token block and head group (half the MMAs of a P-rows tile).
+    // A operand = the V codes of 4 tokens of one channel row per register, x 2^sh (one LOP3
+    // slot select on the vy layout; the per-channel 2^sh is divided out at the end). B = the
+    // probabilities of the block as two u8 planes of a 16-bit integer, normalised per
+    // 128-token group and head: P = round(2^(z - zmax_grp) (2^16 - 1)), so each group keeps
+    // 16 bits relative to its own largest weight; the group's integer sums are folded into
+    // fp32 accumulators with the group's exact scale 2^zmax_grp / (2^16 - 1).
+    // Lane (g, t) owns the scores of head t for tokens {g + 8 j} of each block (phase A C
+    // fragment); the P tile is transposed through shared memory so that B register 0 / 1 of
+    // lane (g', t') holds the 4 tokens {2t' + 8 j} / {2t' + 1 + 8 j} of column g' - the
+    // k-order the vy layout stores the V codes in.
+    constexpr int cpb = Gm::kCpb;
+    float fac[NT][16];  // channel rows rho = 2 mt + r (channel 16 mt + 8 r + g), head 4 hg + t
+    float fw[NT];       // weight sum of head 4 hg + t (lane's tokens), unit scale
     float pa[NT], pb[NT];
 #pragma unroll
-    for (int mt = 0; mt < NT; ++mt) {
-        wacc[mt] = 0;
-        pa[mt] = sm.gpar[(4 * mt + t) * 4 + 0];
-        pb[mt] = sm.gpar[(4 * mt + t) * 4 + 1];
+    for (int hg = 0; hg < NT; ++hg) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) fac[hg][i] = 0.0f;
+        fw[hg] = 0.0f;
+        pa[hg] = sm.gpar[(4 * hg + t) * 4 + 0];
+        pb[hg] = sm.gpar[(4 * hg + t) * 4 + 1];
     }
-    uint32_t* pw = sm.pw + warp * 2 * NT * 12 * kPRow;
-    auto p_write = [&](int blk, uint32_t* tile) {
-#pragma unroll
-        for (int mt = 0; mt < NT; ++mt) {
-            float sc[4];
-            tmem_ld4(tmem_w + (uint32_t)((blk * NT + mt) * 4), sc);
-            uint32_t v[4];
-            if (blk * 32 + 32 <= nv) {  // full block (warp-uniform): no per-token checks
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const float pr = ex2(__fmaf_rn(sc[j], pa[mt], pb[mt]));
-                    v[j] = __float_as_uint(__fmaf_rn(pr, kPScale, kMagic));  // round(p * kPScale) in low bits
-                }
-            } else {
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int tok = blk * 32 + 16 * (j >> 1) + 8 * (j & 1) + g;
-                    const float pr = tok < nv ? ex2(__fmaf_rn(sc[j], pa[mt], pb[mt])) : 0.0f;
-                    v[j] = __float_as_uint(__fmaf_rn(pr, kPScale, kMagic));
-                }
-            }
-            wacc[mt] += (v[0] + v[1]) + (v[2] + v[3]) - 4u * 0x4B400000u;
-            const uint32_t p01 = prmt(v[0], v[1], 0x5140), p23 = prmt(v[2], v[3], 0x5140);
-            const uint32_t q01 = prmt(v[0], v[1], 0x7362), q23 = prmt(v[2], v[3], 0x7362);
-            uint32_t* rowp = tile + (mt * 12 + t) * kPRow + g;
-            rowp[0 * 4 * kPRow] = prmt(p01, p23, 0x5410);                // bits 0-7
-            rowp[1 * 4 * kPRow] = prmt(p01, p23, 0x7632);                // bits 8-15
-            rowp[2 * 4 * kPRow] = prmt(q01, q23, 0x5410) & 0x3F3F3F3Fu;  // bits 16-21
-        }
-    };
+    uint32_t* px = sm.pw + warp * (4 * NT * kPxWords);  // [4 blocks][NT][head 4][plane 2][8 (+pad)]
     constexpr int kBps = Gm::kStageTokens / 32;  // 32-token blocks per stage
     const int nblk_all = (nv + 31) >> 5;
-    if (nblk_all > 0) p_write(0, pw);
-    __syncwarp();
-    for (int st = 0; st < nstage; ++st) {
-        const int i = nstage + st;
-        const int slot = i % kStagesW;
-        mbar_wait(&full[slot], (i / kStagesW) & 1);
-        const uint8_t* buf = ring + slot * Gm::kStageBytesB;
-        const int nb = min(kBps, nblk_all - st * kBps);
+    for (int b0 = 0; b0 < nblk_all; b0 += 4) {
+        const int nbg = min(4, nblk_all - b0);
+        // scores of the group (4 blocks x NT x 4, one TMEM load) -> z = log2 weight (<= 0)
+        uint32_t zr[4 * NT * 4];
+        tmem_ld_cols<4 * NT * 4>(tmem_w + (uint32_t)(b0 * NT * 4), zr);
+        float z[4][NT][4], zm[NT];
 #pragma unroll
-        for (int blk = 0; blk < kBps; ++blk) {
-            if (blk >= nb) break;  // warp-uniform
-            const int b = st * kBps + blk;
-            uint32_t* cur = pw + (b & 1) * NT * 12 * kPRow;
-            uint32_t afr[NT][4];
+        for (int hg = 0; hg < NT; ++hg) zm[hg] = -INFINITY;
 #pragma unroll
-            for (int mt = 0; mt < NT; ++mt) {
-                const uint32_t* r0 = cur + (mt * 12 + g) * kPRow;
-                afr[mt][0] = r0[t];
-                afr[mt][2] = r0[4 + t];
-                afr[mt][1] = g < 4 ? r0[8 * kPRow + t] : 0u;
-                afr[mt][3] = g < 4 ? r0[8 * kPRow + 4 + t] : 0u;
+        for (int bb = 0; bb < 4; ++bb)
+#pragma unroll
+            for (int hg = 0; hg < NT; ++hg)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int tok = (b0 + bb) * 32 + 16 * (j >> 1) + 8 * (j & 1) + g;
+                    const float zz = __fmaf_rn(__uint_as_float(zr[(bb * NT + hg) * 4 + j]), pa[hg], pb[hg]);
+                    z[bb][hg][j] = tok < nv ? zz : -INFINITY;
+                    zm[hg] = fmaxf(zm[hg], z[bb][hg][j]);
+                }
+        float sc[NT];
+#pragma unroll
+        for (int hg = 0; hg < NT; ++hg) {
+            zm[hg] = fmaxf(zm[hg], __shfl_xor_sync(0xffffffffu, zm[hg], 4));
+            zm[hg] = fmaxf(zm[hg], __shfl_xor_sync(0xffffffffu, zm[hg], 8));
+            zm[hg] = fmaxf(zm[hg], __shfl_xor_sync(0xffffffffu, zm[hg], 16));
+            if (zm[hg] == -INFINITY) zm[hg] = 0.0f;  // no live token (absent head): all weights 0
+            sc[hg] = ex2(zm[hg]) * (1.0f / 65535.0f);
+        }
+        __syncwarp();  // the previous group's P tiles are consumed
+        uint32_t wg[NT];
+#pragma unroll
+        for (int hg = 0; hg < NT; ++hg) wg[hg] = 0u;
+#pragma unroll
+        for (int bb = 0; bb < 4; ++bb) {
+            if (bb >= nbg) break;
+#pragma unroll
+            for (int hg = 0; hg < NT; ++hg) {
+                uint32_t v[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j)  // round(2^(z - zm) * 65535) in the low mantissa bits
+                    v[j] = __float_as_uint(__fmaf_rn(ex2(z[bb][hg][j] - zm[hg]), 65535.0f, kMagic));
+                wg[hg] += (v[0] + v[1]) + (v[2] + v[3]) - 4u * 0x4B400000u;
+                const uint32_t p01 = prmt(v[0], v[1], 0x5140), p23 = prmt(v[2], v[3], 0x5140);
+                uint32_t* tile = px + (bb * NT + hg) * kPxWords + t * kPxHead + g;
+                tile[0] = prmt(p01, p23, 0x5410);  // plane 0: bits 0-7 of tokens g + 8 j
+                tile[8] = prmt(p01, p23, 0x7632);  // plane 1: bits 8-15
             }
-            if (b + 1 < nblk_all) p_write(b + 1, pw + ((b + 1) & 1) * NT * 12 * kPRow);
-            // B operand: V codes of this lane's 2*BITS bytes for the 4 tokens of k-group t
-            // (grp 0) / 4 + t (grp 1), byte-transposed ahead of time (vx_layout): one
-            // conflict-free 16*BITS-byte load per lane.
-            uint32_t X[2][2 * BITS];
+        }
+        __syncwarp();
+        int acc[NT][8][4];
+#pragma unroll
+        for (int bb = 0; bb < 4; ++bb) {
+            if (bb >= nbg) break;  // warp-uniform
+            const int b = b0 + bb;
+            const int i = nstage + b / kBps;  // V stage of this block
+            const int slot = i % kStagesW;
+            if (b % kBps == 0) mbar_wait(&full[slot], (i / kStagesW) & 1);
+            const uint8_t* buf = ring + slot * Gm::kStageBytesB;
+            uint32_t X[2][2 * BITS];  // [token half][word x]: channel rows x cpb + s, 4 tokens each
             {
-                const uint4* xp = reinterpret_cast<const uint4*>(buf + (size_t)(blk * 32 + lane) * 16 * BITS);
+                const uint4* xp = reinterpret_cast<const uint4*>(buf + (size_t)((b % kBps) * 32 + lane) * 16 * BITS);
 #pragma unroll
                 for (int u = 0; u < BITS; ++u) {
                     const uint4 v4 = xp[u];
                     const uint32_t w4[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const int idx = 4 * u + k;
-                        X[idx / (2 * BITS)][idx % (2 * BITS)] = w4[k];
-                    }
+                    for (int k = 0; k < 4; ++k) X[(4 * u + k) / (2 * BITS)][(4 * u + k) % (2 * BITS)] = w4[k];
                 }
             }
+            uint32_t bf[NT][2];
 #pragma unroll
-            for (int nc = 0; nc < 16; ++nc) {
-                constexpr int cpb = Gm::kCpb;
-                const uint32_t m = Gm::kMask << ((nc % cpb) * BITS);
-                const uint32_t b0 = X[0][nc / cpb] & m, b1 = X[1][nc / cpb] & m;
-#pragma unroll
-                for (int mt = 0; mt < NT; ++mt)
-                    imma_u8u8(vacc[mt][nc], afr[mt][0], afr[mt][1], afr[mt][2], afr[mt][3], b0, b1);
+            for (int hg = 0; hg < NT; ++hg) {
+                const uint2 w2 = *reinterpret_cast<const uint2*>(px + (bb * NT + hg) * kPxWords + (g >> 1) * kPxHead +
+                                                                 (g & 1) * 8 + 2 * t);
+                bf[hg][0] = w2.x, bf[hg][1] = w2.y;
             }
-            __syncwarp();
+#pragma unroll
+            for (int mt = 0; mt < 8; ++mt) {
+                const int rho0 = 2 * mt, rho1 = 2 * mt + 1;
+                const uint32_t m0 = Gm::kMask << ((rho0 % cpb) * BITS), m1 = Gm::kMask << ((rho1 % cpb) * BITS);
+                const uint32_t a0 = X[0][rho0 / cpb] & m0, a1 = X[0][rho1 / cpb] & m1;
+                const uint32_t a2 = X[1][rho0 / cpb] & m0, a3 = X[1][rho1 / cpb] & m1;
+#pragma unroll
+                for (int hg = 0; hg < NT; ++hg) {
+                    if (bb == 0) acc[hg][mt][0] = acc[hg][mt][1] = acc[hg][mt][2] = acc[hg][mt][3] = 0;
+                    imma_u8u8(acc[hg][mt], a0, a1, a2, a3, bf[hg][0], bf[hg][1]);
+                }
+            }
+            if (b % kBps == kBps - 1 || b == nblk_all - 1) {  // stage consumed: refill its slot
+                __syncwarp();
+                if (lane == 0 && i + kStagesW < total_stages) issue(i + kStagesW);
+            }
         }
-        if (lane == 0 && i + kStagesW < total_stages) issue(i + kStagesW);
+        // fold the group into fp32: column pair (2t, 2t+1) = planes 0 / 1 of head 4 hg + t
+#pragma unroll
+        for (int hg = 0; hg < NT; ++hg) {
+#pragma unroll
+            for (int mt = 0; mt < 8; ++mt) {
+                const uint32_t c0 = (uint32_t)acc[hg][mt][0] + ((uint32_t)acc[hg][mt][1] << 8);
+                const uint32_t c1 = (uint32_t)acc[hg][mt][2] + ((uint32_t)acc[hg][mt][3] << 8);
+                fac[hg][2 * mt] = __fmaf_rn(__uint2float_rn(c0), sc[hg], fac[hg][2 * mt]);
+                fac[hg][2 * mt + 1] = __fmaf_rn(__uint2float_rn(c1), sc[hg], fac[hg][2 * mt + 1]);
+            }
+            fw[hg] = __fmaf_rn(__uint2float_rn(wg[hg]), sc[hg], fw[hg]);
+        }
     }
 
     if (lane == 0) TTRACE(16 + warp);  // phase B done, per warp
-    // ---------------- CTA reduction (exact integer sums in shared memory) ----------------
-    // Image layout [mt][nc][r][lane]: consecutive lanes hit consecutive banks.
+    // ---------------- CTA reduction (fixed order, deterministic) ----------------
+    // Image [warp][hg][rho][lane]: consecutive lanes hit consecutive banks.
 #pragma unroll
-    for (int mt = 0; mt < NT; ++mt) {
+    for (int hg = 0; hg < NT; ++hg) {
 #pragma unroll
-        for (int nc = 0; nc < 16; ++nc)
-#pragma unroll
-            for (int r = 0; r < 4; ++r) red_add_u32(sm.acc + ((mt * 16 + nc) * 4 + r) * 32 + lane, (uint32_t)vacc[mt][nc][r]);
-        uint32_t w = wacc[mt];
+        for (int rho = 0; rho < 16; ++rho) sm.acc[((warp * NT + hg) * 16 + rho) * 32 + lane] = fac[hg][rho];
+        float w = fw[hg];
         w += __shfl_xor_sync(0xffffffffu, w, 4);
         w += __shfl_xor_sync(0xffffffffu, w, 8);
         w += __shfl_xor_sync(0xffffffffu, w, 16);
-        if (lane < 4) sm.wsum[warp * 8 + 4 * mt + lane] = w;
+        if (lane < 4) sm.wsum[warp * 8 + 4 * hg + lane] = w;
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();  // (the V stream is drained: the ring is free from here on)
-    // Output, thread per (head, channel), straight from the accumulator image:
+    // Output, thread per (head, channel), from the per-warp images (unit weight scale):
     //   out = (s_c V / 2^sh + alpha_c W_vis + sum_t p_t v_tc) / (W_vis + sum_t p_t)
-    // on the common kPScale weight scale; tail weights recomputed in fp32 (rank 0).
+    // tail weights recomputed in fp32 (rank 0).
     float* recv = reinterpret_cast<float*>(sm.ring);
     if (S > 1) {  // every CTA's ring is drained before rank 0's becomes the receive buffer
         __syncwarp();
@@ -780,25 +823,14 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
     }
     for (int idx = threadIdx.x; idx < G * kDim; idx += W * 32) {
         const int h = idx / kDim, ch = idx % kDim;
-        constexpr int cpb = Gm::kCpb;
-        // invert v_channel: ch = (2 BITS g' + q) cpb + (cpb - 1 - s), nc = q cpb + s, and
-        // accumulator column g' = 2 tt + (r & 1), row = plane*4 + head%4 = gg + 8 (r >> 1)
-        const int s_slot = cpb - 1 - ch % cpb, rem = ch / cpb;
-        const int gcol = rem / (2 * BITS), qq = rem % (2 * BITS);
-        const int nc = qq * cpb + s_slot, tt = gcol >> 1, rlo = gcol & 1;
-        const int mt = h >> 2, hh = h & 3;
-        uint32_t pl[3];
-#pragma unroll
-        for (int plane = 0; plane < 3; ++plane) {
-            const int row = plane * 4 + hh;
-            const int gg = row & 7, r = ((row >> 3) << 1) | rlo;
-            pl[plane] = sm.acc[((mt * 16 + nc) * 4 + r) * 32 + gg * 4 + tt];
+        const int hg = h >> 2, tt = h & 3;
+        const int mt = ch >> 4, r = (ch >> 3) & 1, gg = ch & 7, rho = 2 * mt + r;
+        float V = 0.0f, wv = 0.0f;
+        for (int w2 = 0; w2 < W; ++w2) {
+            V += sm.acc[((w2 * NT + hg) * 16 + rho) * 32 + 4 * gg + tt];
+            wv += sm.wsum[w2 * 8 + h];
         }
-        const float V = __fmaf_rn((float)pl[2], 65536.0f, __fmaf_rn((float)pl[1], 256.0f, (float)pl[0])) *
-                        __int_as_float((127 - s_slot * BITS) << 23);
-        unsigned long long ws = 0;
-        for (int w2 = 0; w2 < W; ++w2) ws += sm.wsum[w2 * 8 + h];
-        const float wv = (float)ws;
+        V *= __int_as_float((127 - (rho % cpb) * BITS) << 23);  // divide out the slot's 2^sh
         constexpr float kInvLevelsV = 1.0f / (float)((1u << BITS) - 1u);
         const float v_step = fmaxf(__fsub_rn(v_b, v_a) * kInvLevelsV, 0.0f);
         float num = __fmaf_rn(v_step, V, v_a * wv), den = wv;
@@ -810,19 +842,19 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
             for (int u = 0; u < 8; ++u) vv[u] = __ldg(vt + (size_t)(j + u) * kDim);
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
-                const float pt = ex2(__fmaf_rn(sm.tail_s[h * kTailMax + j + u], kLog2e, sm.gpar[h * 4 + 2])) * kPScale;
+                const float pt = ex2(__fmaf_rn(sm.tail_s[h * kTailMax + j + u], kLog2e, sm.gpar[h * 4 + 2]));
                 den += pt;
                 num = __fmaf_rn(pt, vv[u], num);
             }
         }
         for (; j < ntl; ++j) {
-            const float pt = ex2(__fmaf_rn(sm.tail_s[h * kTailMax + j], kLog2e, sm.gpar[h * 4 + 2])) * kPScale;
+            const float pt = ex2(__fmaf_rn(sm.tail_s[h * kTailMax + j], kLog2e, sm.gpar[h * 4 + 2]));
             den += pt;
             num = __fmaf_rn(pt, __ldg(vt + (size_t)j * kDim), num);
         }
         if (S == 1) {
             a.out[qrow(h) * kDim + ch] = num / den;
-            if (a.tail_lse && ch == 0) a.tail_lse[qrow(h)] = log2f(den) - kLog2PScale - sm.gpar[h * 4 + 2];
+            if (a.tail_lse && ch == 0) a.tail_lse[qrow(h)] = log2f(den) - sm.gpar[h * 4 + 2];
         } else {
             st_cluster_f32(recv + rank * (8 * kDim + 8) + idx, 0, num);
             if (ch == 0) st_cluster_f32(recv + rank * (8 * kDim + 8) + 8 * kDim + h, 0, den);
@@ -842,7 +874,7 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
                 }
                 a.out[qrow(idx / kDim) * kDim + (idx % kDim)] = num / den;
                 if (a.tail_lse && idx % kDim == 0)
-                    a.tail_lse[qrow(h)] = log2f(den) - kLog2PScale - sm.gpar[h * 4 + 2];
+                    a.tail_lse[qrow(h)] = log2f(den) - sm.gpar[h * 4 + 2];
             }
         }
     }
@@ -916,55 +948,40 @@ cudaError_t launch_occ(const DecodeArgs& a, cudaStream_t s, int groups = 1) {
 
 }  // namespace
 
-// ---- vx_layout: V codes pre-arranged as the phase-B B operand ---------------------------
-// [unit][32-token block][lane 32][2 grp][2*BITS words]: word w of group grp of lane (g, t)
-// holds, byte-transposed, the 2*BITS code bytes of channel group g of the four tokens
-// 4 grp + t + 8 ii (ii = 0..3) of the block - exactly the registers the decode used to
-// build from token-major rows with PRMT. Tokens past n are zero codes. Built once per
-// cache (pack_vx_kernel); the reference-layout V copy stays for read-back.
+// ---- vx_layout: V codes pre-arranged as the phase-B A operand (V^T registers) ------------
+// [unit][32-token block][lane 32][half 2][2*BITS words]: byte j of word (half, x) of lane
+// (g, t) holds, in slot s (bits [s BITS, s BITS + BITS)), the code of token
+// 2 t + half + 8 j of the block and channel 16 mt + 8 r + g, where rho = x cpb + s = 2 mt + r
+// - one LOP3 then yields the A register "4 tokens of channel row g (+8) of tile mt, x 2^(s
+// BITS)". Tokens past n are zero codes. Built once per cache (pack_vx_kernel); the
+// reference-layout copy stays for read-back.
 namespace {
 template <int BITS>
 __global__ void __launch_bounds__(32) pack_vx_kernel(const uint8_t* __restrict__ rows, size_t n, size_t nb32,
                                                      int bx, uint8_t* __restrict__ vx) {
     constexpr int kRowBytes = 16 * BITS;
-    constexpr int NW = (2 * BITS + 3) / 4;
+    constexpr int cpb = 8 / BITS;
+    constexpr uint32_t kLevel = (1u << BITS) - 1u;
     const size_t unit = blockIdx.y, blk = blockIdx.x;
     const int lane = threadIdx.x, g = lane >> 2, t = lane & 3;
-    uint32_t X[2][2 * BITS];
-#pragma unroll
-    for (int grp = 0; grp < 2; ++grp) {
-        uint32_t raw[4][NW];
-#pragma unroll
-        for (int ii = 0; ii < 4; ++ii) {
-            const size_t tok = blk * 32 + 4 * grp + t + 8 * ii;
-            const uint8_t* rp = rows + (unit * n + tok) * kRowBytes;  // byte (2 BITS g + k) ^ bx
-#pragma unroll
-            for (int wi = 0; wi < NW; ++wi) {
-                uint32_t w = 0;
-                for (int by = 0; by < 4 && 4 * wi + by < 2 * BITS; ++by)
-                    w |= (tok < n ? (uint32_t)rp[(2 * BITS * g + 4 * wi + by) ^ bx] : 0u) << (8 * by);
-                raw[ii][wi] = w;
+    uint32_t* dst = reinterpret_cast<uint32_t*>(vx + ((unit * nb32 + blk) * 32 + lane) * (size_t)(16 * BITS));
+    for (int half = 0; half < 2; ++half) {
+        for (int x = 0; x < 2 * BITS; ++x) {
+            uint32_t w = 0;
+            for (int j = 0; j < 4; ++j) {
+                const size_t tok = blk * 32 + 2 * t + half + 8 * j;
+                if (tok >= n) continue;
+                const uint8_t* rp = rows + (unit * n + tok) * kRowBytes;
+                for (int sl = 0; sl < cpb; ++sl) {
+                    const int rho = x * cpb + sl, c = 16 * (rho >> 1) + 8 * (rho & 1) + g;
+                    const int i = c % cpb;  // MSB-first code slot in its byte (bitpack.hpp:76-88)
+                    const uint32_t code = ((uint32_t)rp[(c / cpb) ^ bx] >> (8 - BITS * (i + 1))) & kLevel;
+                    w |= code << (8 * j + BITS * sl);
+                }
             }
-        }
-#pragma unroll
-        for (int wi = 0; wi < NW; ++wi) {
-            const uint32_t P0 = prmt(raw[0][wi], raw[1][wi], 0x5140);
-            const uint32_t P2 = prmt(raw[2][wi], raw[3][wi], 0x5140);
-            X[grp][(4 * wi + 0) % (2 * BITS)] = prmt(P0, P2, 0x5410);
-            X[grp][(4 * wi + 1) % (2 * BITS)] = prmt(P0, P2, 0x7632);
-            if (2 * BITS > 2) {
-                const uint32_t P1 = prmt(raw[0][wi], raw[1][wi], 0x7362);
-                const uint32_t P3 = prmt(raw[2][wi], raw[3][wi], 0x7362);
-                X[grp][(4 * wi + 2) % (2 * BITS)] = prmt(P1, P3, 0x5410);
-                X[grp][(4 * wi + 3) % (2 * BITS)] = prmt(P1, P3, 0x7632);
-            }
+            dst[half * 2 * BITS + x] = w;
         }
     }
-    uint32_t* dst = reinterpret_cast<uint32_t*>(vx + ((unit * nb32 + blk) * 32 + lane) * (size_t)(16 * BITS));
-#pragma unroll
-    for (int grp = 0; grp < 2; ++grp)
-#pragma unroll
-        for (int w = 0; w < 2 * BITS; ++w) dst[grp * 2 * BITS + w] = X[grp][w];
 }
 
 }  // namespace
