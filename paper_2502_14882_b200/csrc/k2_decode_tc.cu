@@ -569,31 +569,53 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");  // scores are in tensor memory
     if (lane == 0) TTRACE(8 + warp);  // phase A done, per warp
 
-    // fp32 tail rows (rank 0): warp w takes rows w, w + NW, ...; lanes split the 128
-    // channels; q rows are loaded once.
+    // fp32 tail rows (rank 0, naive_qk kernels.hpp:401-413): warp w takes rows w, w + W, ...
+    // in batches of RB rows whose loads are all in flight at once; lane = 4 channels; the
+    // RB x HB partial dots of a batch are reduced with one warp reduce-scatter (31 shuffles:
+    // lane l ends with the full dot of row l / HB, head l % HB).
     const float isd = __fdiv_rn(1.0f, sqrtf((float)kDim));
-    float tmax = -INFINITY;  // for head (lane & 7)
-    if (warp < W && ntl > warp) {
-        float4 qv[8];
+    constexpr int HB = 4 * NT, RB = 32 / HB;
+    float tmax = -INFINITY;  // head lane % HB
+    if (ntl > warp) {
+        float4 qv[HB];
 #pragma unroll
-        for (int h = 0; h < 8; ++h)
+        for (int h = 0; h < HB; ++h)
             qv[h] = h < G ? *reinterpret_cast<const float4*>(a.q + qrow(h) * kDim + 4 * lane)
                           : make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int j = warp; j < ntl; j += W) {
-            const float4 kv = *reinterpret_cast<const float4*>(a.k_tail + ((size_t)unit * a.tail_cap + j) * kDim + 4 * lane);
+        for (int j0 = warp; j0 < ntl; j0 += RB * W) {
+            float4 kv[RB];
 #pragma unroll
-            for (int h = 0; h < 8; ++h) {
-                if (h < G) {
-                    float d = kv.x * qv[h].x + kv.y * qv[h].y + kv.z * qv[h].z + kv.w * qv[h].w;
+            for (int r = 0; r < RB; ++r) {
+                const int j = j0 + r * W;
+                kv[r] = j < ntl ? __ldcg(reinterpret_cast<const float4*>(a.k_tail + ((size_t)unit * a.tail_cap + j) * kDim) + lane)
+                                : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            float v[32];
 #pragma unroll
-                    for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-                    d *= isd;
-                    if (lane == 0) sm.tail_s[h * kTailMax + j] = d;
-                    if ((lane & 7) == h) tmax = fmaxf(tmax, d);
+            for (int r = 0; r < RB; ++r)
+#pragma unroll
+                for (int h = 0; h < HB; ++h)
+                    v[r * HB + h] = kv[r].x * qv[h].x + kv[r].y * qv[h].y + kv[r].z * qv[h].z + kv[r].w * qv[h].w;
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                const bool up = (lane & o) != 0;
+#pragma unroll
+                for (int i = 0; i < o; ++i) {
+                    const float send = up ? v[i] : v[i + o], keep = up ? v[i + o] : v[i];
+                    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
                 }
+            }
+            const int j = j0 + (lane / HB) * W, h = lane % HB;
+            if (j < ntl && h < G) {
+                const float d = v[0] * isd;
+                sm.tail_s[h * kTailMax + j] = d;
+                tmax = fmaxf(tmax, d);
             }
         }
     }
+#pragma unroll
+    for (int o = HB; o < 32; o <<= 1) tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
+    if ((lane & 7) >= HB) tmax = -INFINITY;  // lane & 7 = head below (heads >= HB absent)
     // Per-warp partial record (min[8], max[8], tail max[8]); lane k < 24 owns entry k.
     float mine = -INFINITY;
 #pragma unroll
@@ -660,6 +682,11 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
         sm.gpar[h * 4 + 2] = -m * kLog2e;
     }
     __syncthreads();
+    // tail scores -> weights on the unit scale (read by the output pass after the next barrier)
+    for (int e = threadIdx.x; e < G * ntl; e += W * 32) {
+        const int h = e / ntl, j = e % ntl;
+        sm.tail_s[h * kTailMax + j] = ex2(__fmaf_rn(sm.tail_s[h * kTailMax + j], kLog2e, sm.gpar[h * 4 + 2]));
+    }
 
     if (threadIdx.x == 0) TTRACE(1);  // softmax parameters known
     // ---------------- phase B: p . V over this warp's tokens ----------------
@@ -821,43 +848,55 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
         cluster_arrive();  // #2a
         cluster_wait();
     }
-    for (int idx = threadIdx.x; idx < G * kDim; idx += W * 32) {
-        const int h = idx / kDim, ch = idx % kDim;
-        const int hg = h >> 2, tt = h & 3;
+    if (threadIdx.x < kDim) {  // thread = channel, all heads
+        const int ch = threadIdx.x;
         const int mt = ch >> 4, r = (ch >> 3) & 1, gg = ch & 7, rho = 2 * mt + r;
-        float V = 0.0f, wv = 0.0f;
-        for (int w2 = 0; w2 < W; ++w2) {
-            V += sm.acc[((w2 * NT + hg) * 16 + rho) * 32 + 4 * gg + tt];
-            wv += sm.wsum[w2 * 8 + h];
-        }
-        V *= __int_as_float((127 - (rho % cpb) * BITS) << 23);  // divide out the slot's 2^sh
+        const float unshift = __int_as_float((127 - (rho % cpb) * BITS) << 23);  // divide out the slot's 2^sh
         constexpr float kInvLevelsV = 1.0f / (float)((1u << BITS) - 1u);
         const float v_step = fmaxf(__fsub_rn(v_b, v_a) * kInvLevelsV, 0.0f);
-        float num = __fmaf_rn(v_step, V, v_a * wv), den = wv;
+        float num[HB], den[HB];
+#pragma unroll
+        for (int h = 0; h < HB; ++h) {
+            float V = 0.0f, wv = 0.0f;
+            if (h < G) {
+                for (int w2 = 0; w2 < W; ++w2) {
+                    V += sm.acc[((w2 * NT + (h >> 2)) * 16 + rho) * 32 + 4 * gg + (h & 3)];
+                    wv += sm.wsum[w2 * 8 + h];
+                }
+            }
+            num[h] = __fmaf_rn(v_step, V * unshift, v_a * wv);
+            den[h] = wv;
+        }
+        // fp32 tail (naive_wv kernels.hpp:414-426): each row value loaded once for all heads,
+        // 16 loads in flight; weights precomputed in tail_s
         const float* vt = a.v_tail + (size_t)unit * a.tail_cap * kDim + ch;
-        int j = 0;
-        for (; j + 8 <= ntl; j += 8) {  // 8 independent loads in flight, j ascending
-            float vv[8];
+        for (int j0 = 0; j0 < ntl; j0 += 16) {
+            float vv[16];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) vv[u] = __ldg(vt + (size_t)(j + u) * kDim);
+            for (int u = 0; u < 16; ++u) vv[u] = j0 + u < ntl ? __ldcg(vt + (size_t)(j0 + u) * kDim) : 0.0f;
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const float pt = ex2(__fmaf_rn(sm.tail_s[h * kTailMax + j + u], kLog2e, sm.gpar[h * 4 + 2]));
-                den += pt;
-                num = __fmaf_rn(pt, vv[u], num);
+            for (int u = 0; u < 16; ++u) {
+                if (j0 + u >= ntl) break;
+#pragma unroll
+                for (int h = 0; h < HB; ++h) {
+                    if (h < G) {
+                        const float pt = sm.tail_s[h * kTailMax + j0 + u];
+                        den[h] += pt;
+                        num[h] = __fmaf_rn(pt, vv[u], num[h]);
+                    }
+                }
             }
         }
-        for (; j < ntl; ++j) {
-            const float pt = ex2(__fmaf_rn(sm.tail_s[h * kTailMax + j], kLog2e, sm.gpar[h * 4 + 2]));
-            den += pt;
-            num = __fmaf_rn(pt, __ldg(vt + (size_t)j * kDim), num);
-        }
-        if (S == 1) {
-            a.out[qrow(h) * kDim + ch] = num / den;
-            if (a.tail_lse && ch == 0) a.tail_lse[qrow(h)] = log2f(den) - sm.gpar[h * 4 + 2];
-        } else {
-            st_cluster_f32(recv + rank * (8 * kDim + 8) + idx, 0, num);
-            if (ch == 0) st_cluster_f32(recv + rank * (8 * kDim + 8) + 8 * kDim + h, 0, den);
+#pragma unroll
+        for (int h = 0; h < HB; ++h) {
+            if (h >= G) break;
+            if (S == 1) {
+                a.out[qrow(h) * kDim + ch] = num[h] / den[h];
+                if (a.tail_lse && ch == 0) a.tail_lse[qrow(h)] = log2f(den[h]) - sm.gpar[h * 4 + 2];
+            } else {
+                st_cluster_f32(recv + rank * (8 * kDim + 8) + h * kDim + ch, 0, num[h]);
+                if (ch == 0) st_cluster_f32(recv + rank * (8 * kDim + 8) + 8 * kDim + h, 0, den[h]);
+            }
         }
     }
     if (S > 1) {

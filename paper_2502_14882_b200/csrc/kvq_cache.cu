@@ -78,7 +78,9 @@ kvqb::DecodeArgs decode_args(kvq_cache* c, const float* q, float* out) {
 }
 
 // Debug timeline: KVQ_TRACE_FILE=path dumps 256 globaltimer stamps per CTA of each
-// tensor-core decode (tools/trace_decode.py reads it). Off the measured path.
+// tensor-core decode (tools/trace_decode.py reads it). KVQ_TRACE_CHAIN=k keeps one buffer
+// for k consecutive decodes (slot i = call i, no synchronisation in between) and dumps it
+// after the k-th, so back-to-back launches can be compared. Off the measured path.
 template <typename F>
 void traced(kvq_cache* c, kvqb::DecodeArgs& a, cudaStream_t s, F&& launch) {
     static const char* trace_file = std::getenv("KVQ_TRACE_FILE");
@@ -86,19 +88,28 @@ void traced(kvq_cache* c, kvqb::DecodeArgs& a, cudaStream_t s, F&& launch) {
         launch();
         return;
     }
+    static const int chain = std::getenv("KVQ_TRACE_CHAIN") ? std::max(1, std::atoi(std::getenv("KVQ_TRACE_CHAIN"))) : 1;
+    static int call = 0;
+    static DevBuf<unsigned long long>* buf = nullptr;
     const size_t trace_n = c->units * 256 * 16;
-    DevBuf<unsigned long long> trace(trace_n);
-    ck(cudaMemsetAsync(trace.p, 0, trace_n * 8, s), "trace");
-    a.trace = trace.p;
+    if (call == 0) {
+        buf = new DevBuf<unsigned long long>(trace_n * chain);
+        ck(cudaMemsetAsync(buf->p, 0, trace_n * chain * 8, s), "trace");
+    }
+    a.trace = buf->p + trace_n * call;
     launch();
-    std::vector<unsigned long long> h(trace_n);
-    trace.download(h.data(), trace_n, s);
+    a.trace = nullptr;
+    if (++call < chain) return;
+    call = 0;
+    std::vector<unsigned long long> h(trace_n * chain);
+    buf->download(h.data(), h.size(), s);
     sync(s);
+    delete buf;
+    buf = nullptr;
     if (FILE* f = std::fopen(trace_file, "wb")) {
         std::fwrite(h.data(), 8, h.size(), f);
         std::fclose(f);
     }
-    a.trace = nullptr;
 }
 
 void ensure_vt(kvq_cache* c, cudaStream_t s);
