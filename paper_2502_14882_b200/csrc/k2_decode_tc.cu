@@ -722,7 +722,11 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
         // scores of the group (4 blocks x NT x 4, one TMEM load) -> z = log2 weight (<= 0)
         uint32_t zr[4 * NT * 4];
         tmem_ld_cols<4 * NT * 4>(tmem_w + (uint32_t)(b0 * NT * 4), zr);
-        float z[4][NT][4], zm[NT];
+        // e = 2^z issued at once; the group max zm (per head, over the 8 lanes of the head)
+        // then scales e onto the 16-bit grid: P = round(e 2^-zm (2^16 - 2)). zm is clamped at
+        // -100 (a group that far below the row max weighs < 2^-84 of it; also absent heads).
+        const bool gfull = (b0 + 4) * 32 <= nv;  // warp-uniform: no per-token checks
+        float e[4][NT][4], zm[NT];
 #pragma unroll
         for (int hg = 0; hg < NT; ++hg) zm[hg] = -INFINITY;
 #pragma unroll
@@ -731,19 +735,23 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
             for (int hg = 0; hg < NT; ++hg)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                    const int tok = (b0 + bb) * 32 + 16 * (j >> 1) + 8 * (j & 1) + g;
-                    const float zz = __fmaf_rn(__uint_as_float(zr[(bb * NT + hg) * 4 + j]), pa[hg], pb[hg]);
-                    z[bb][hg][j] = tok < nv ? zz : -INFINITY;
-                    zm[hg] = fmaxf(zm[hg], z[bb][hg][j]);
+                    float zz = __fmaf_rn(__uint_as_float(zr[(bb * NT + hg) * 4 + j]), pa[hg], pb[hg]);
+                    if (!gfull) {
+                        const int tok = (b0 + bb) * 32 + 16 * (j >> 1) + 8 * (j & 1) + g;
+                        zz = tok < nv ? zz : -INFINITY;
+                    }
+                    zm[hg] = fmaxf(zm[hg], zz);
+                    e[bb][hg][j] = ex2(zz);
                 }
-        float sc[NT];
+        float sc[NT], up[NT];
 #pragma unroll
         for (int hg = 0; hg < NT; ++hg) {
             zm[hg] = fmaxf(zm[hg], __shfl_xor_sync(0xffffffffu, zm[hg], 4));
             zm[hg] = fmaxf(zm[hg], __shfl_xor_sync(0xffffffffu, zm[hg], 8));
             zm[hg] = fmaxf(zm[hg], __shfl_xor_sync(0xffffffffu, zm[hg], 16));
-            if (zm[hg] == -INFINITY) zm[hg] = 0.0f;  // no live token (absent head): all weights 0
-            sc[hg] = ex2(zm[hg]) * (1.0f / 65535.0f);
+            zm[hg] = fmaxf(zm[hg], -100.0f);
+            up[hg] = ex2(-zm[hg]) * 65534.0f;
+            sc[hg] = ex2(zm[hg]) * (1.0f / 65534.0f);
         }
         __syncwarp();  // the previous group's P tiles are consumed
         uint32_t wg[NT];
@@ -756,8 +764,8 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
             for (int hg = 0; hg < NT; ++hg) {
                 uint32_t v[4];
 #pragma unroll
-                for (int j = 0; j < 4; ++j)  // round(2^(z - zm) * 65535) in the low mantissa bits
-                    v[j] = __float_as_uint(__fmaf_rn(ex2(z[bb][hg][j] - zm[hg]), 65535.0f, kMagic));
+                for (int j = 0; j < 4; ++j)  // round(2^(z - zm) (2^16 - 2)) in the low mantissa bits
+                    v[j] = __float_as_uint(__fmaf_rn(e[bb][hg][j], up[hg], kMagic));
                 wg[hg] += (v[0] + v[1]) + (v[2] + v[3]) - 4u * 0x4B400000u;
                 const uint32_t p01 = prmt(v[0], v[1], 0x5140), p23 = prmt(v[2], v[3], 0x5140);
                 uint32_t* tile = px + (bb * NT + hg) * kPxWords + t * kPxHead + g;
@@ -825,6 +833,12 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
     }
 
     if (lane == 0) TTRACE(16 + warp);  // phase B done, per warp
+    // the output pass's first 16 fp32 tail V values of this thread's channel: loads go out
+    // now, under the CTA reduction below
+    float tvv[16];
+    const float* vt = a.v_tail + (size_t)unit * a.tail_cap * kDim + (threadIdx.x & (kDim - 1));
+#pragma unroll
+    for (int u = 0; u < 16; ++u) tvv[u] = threadIdx.x < kDim && u < ntl ? __ldcg(vt + (size_t)u * kDim) : 0.0f;
     // ---------------- CTA reduction (fixed order, deterministic) ----------------
     // Image [warp][hg][rho][lane]: consecutive lanes hit consecutive banks.
 #pragma unroll
@@ -869,11 +883,10 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
         }
         // fp32 tail (naive_wv kernels.hpp:414-426): each row value loaded once for all heads,
         // 16 loads in flight; weights precomputed in tail_s
-        const float* vt = a.v_tail + (size_t)unit * a.tail_cap * kDim + ch;
         for (int j0 = 0; j0 < ntl; j0 += 16) {
             float vv[16];
 #pragma unroll
-            for (int u = 0; u < 16; ++u) vv[u] = j0 + u < ntl ? __ldcg(vt + (size_t)(j0 + u) * kDim) : 0.0f;
+            for (int u = 0; u < 16; ++u) vv[u] = j0 == 0 ? tvv[u] : j0 + u < ntl ? __ldcg(vt + (size_t)(j0 + u) * kDim) : 0.0f;
 #pragma unroll
             for (int u = 0; u < 16; ++u) {
                 if (j0 + u >= ntl) break;
