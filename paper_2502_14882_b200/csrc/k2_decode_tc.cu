@@ -64,6 +64,9 @@ struct TcParams {
     DecodeArgs a;
     int S, T;    // cluster size, visual tokens per CTA (multiple of 256)
     int groups;  // head groups per unit handled by separate CTAs (1, or 2 for G > 4 at NT = 1)
+    int whole;   // mixed launch: CTAs [0, whole) each own a whole unit alone (T1 tokens); the
+    int T1;      // rest are S-CTA clusters of the remaining units (0: uniform launch)
+    int split_first;  // mixed launch: the split units' CTAs come first in the grid
 };
 
 // ---- PTX helpers (mbarriers, bulk copies, cluster barriers, PDL: kvq_ptx.cuh) ---------
@@ -257,11 +260,19 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
     constexpr int kSteps = warp_tokens<NT>() / 32;                 // 32-token steps per warp, at most
     constexpr uint32_t kTmemCols = (W / 4) * kSteps * 4 * NT;        // lane-sharing warps; 256 / 128
     const DecodeArgs& a = p.a;
-    const int S = p.S;
-    const int rank = S > 1 ? (int)cg::this_cluster().block_rank() : 0;
     // Grid: (head group, unit, rank). With two head groups a CTA serves query heads
     // [4 grp, 4 grp + G) of its unit (softmax rows are per head, so the split is exact).
-    const int unit_g = blockIdx.x / S;
+    // A mixed launch (balanced batches) puts `whole` solo CTAs first: unit = CTA index.
+    // Mixed launch order: the split units' clusters first (the block scheduler deals them
+    // out one per SM), then the solo CTAs fill the remaining slots.
+    const int nsplit_ctas = p.whole > 0 ? (int)gridDim.x - p.whole : 0;
+    const int solo_base = p.split_first ? nsplit_ctas : 0;  // first solo CTA
+    const int split_base = p.split_first ? 0 : p.whole;     // first split CTA
+    const bool solo = p.whole > 0 && (int)blockIdx.x >= solo_base && (int)blockIdx.x < solo_base + p.whole;
+    const int S = solo ? 1 : p.S;
+    const int T = solo ? p.T1 : p.T;
+    const int rank = S > 1 ? (int)cg::this_cluster().block_rank() : 0;
+    const int unit_g = solo ? (int)blockIdx.x - solo_base : p.whole + ((int)blockIdx.x - split_base) / S;
     const int grp = unit_g / (int)a.units;
     const int unit = unit_g % (int)a.units;
     const int G_all = (int)a.group;
@@ -275,12 +286,17 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
     Smem sm;
     tc_smem_bytes<BITS, NT, OCC, W>(S, &sm, smem_raw);
     if (threadIdx.x == 0) TTRACE(0);
+    if (threadIdx.x == 0 && a.trace) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        a.trace[(size_t)blockIdx.x * 256 + 31] = smid + 1;
+    }
     uint8_t* ring = sm.ring + warp * kStagesW * Gm::kStageBytesB;
     uint64_t* full = sm.full + warp * kStagesW;
 
     const int n = (int)a.n_vis;
-    const int wt = p.T / W;                        // tokens per warp (multiple of 32, <= 1024)
-    const int tok0 = rank * p.T + warp * wt;              // this warp's first token
+    const int wt = T / W;                          // tokens per warp (multiple of 32, <= 1024)
+    const int tok0 = rank * T + warp * wt;                // this warp's first token
     const int nv = max(0, min(wt, n - tok0));
     // fp32 tail: rank 0, unless a separate tail pass owns it (a.tail_lse). tail_len is written
     // by the previous step's append: the pre-dependency read is an L2 prefetch hint only.
@@ -616,6 +632,7 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
 #pragma unroll
     for (int o = HB; o < 32; o <<= 1) tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
     if ((lane & 7) >= HB) tmax = -INFINITY;  // lane & 7 = head below (heads >= HB absent)
+    if (threadIdx.x == 0) TTRACE(27);  // tail scores done (warp 0)
     // Per-warp partial record (min[8], max[8], tail max[8]); lane k < 24 owns entry k.
     float mine = -INFINITY;
 #pragma unroll
@@ -636,6 +653,7 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
     if (lane >= 16 && lane < 24) mine = tm8;
     if (lane < 24) sm.wpart[warp * 24 + lane] = mine;
     __syncthreads();
+    if (threadIdx.x == 0) TTRACE(30);  // warp partials complete
     if (threadIdx.x < 24) {  // CTA partial
         const int kk = threadIdx.x;
         float v = sm.wpart[kk];
@@ -853,6 +871,7 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();  // (the V stream is drained: the ring is free from here on)
+    if (threadIdx.x == 0) TTRACE(28);  // CTA image complete
     // Output, thread per (head, channel), from the per-warp images (unit weight scale):
     //   out = (s_c V / 2^sh + alpha_c W_vis + sum_t p_t v_tc) / (W_vis + sum_t p_t)
     // tail weights recomputed in fp32 (rank 0).
@@ -900,6 +919,7 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
                 }
             }
         }
+        if (threadIdx.x == 0) TTRACE(29);  // output sums done (thread 0)
 #pragma unroll
         for (int h = 0; h < HB; ++h) {
             if (h >= G) break;
@@ -961,11 +981,20 @@ void plan(const DecodeArgs& a, int NT, int& S, int& T, int W = kWarps) {
 }
 
 template <int BITS, int NT, int OCC, int W = kWarps>
-cudaError_t launch_occ(const DecodeArgs& a, cudaStream_t s, int groups = 1) {
-    int S, T;
-    plan(a, NT, S, T, W);
+cudaError_t launch_occ(const DecodeArgs& a, cudaStream_t s, int groups = 1, int whole = 0) {
+    int S, T, S1 = 1, T1 = 0;
+    if (whole > 0) {  // mixed: solo whole units, then 2-CTA clusters of half units
+        DecodeArgs a1 = a, a2 = a;
+        a1.split_override = 1, a2.split_override = 2;
+        plan(a1, NT, S1, T1, W);
+        plan(a2, NT, S, T, W);
+        if (S1 != 1 || S != 2) return cudaErrorInvalidValue;
+    } else {
+        plan(a, NT, S, T, W);
+    }
     cudaError_t e = cudaSuccess;
-    TcParams p{a, S, T, groups};
+    static const int split_first = std::getenv("KVQ_TC_SPLIT_FIRST") ? std::atoi(std::getenv("KVQ_TC_SPLIT_FIRST")) : 0;
+    TcParams p{a, S, T, groups, whole, T1, split_first};
     // TMEM: 512 columns per SM; never let more CTAs share an SM than TMEM can serve (a
     // blocked tcgen05.alloc inside a cluster could deadlock against its partners).
     const size_t max_ctas = W == 4 ? 4 : (OCC == 1 ? 1 : 2);
@@ -980,7 +1009,7 @@ cudaError_t launch_occ(const DecodeArgs& a, cudaStream_t s, int groups = 1) {
     });
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(a.units * S * groups));
+    cfg.gridDim = dim3(whole > 0 ? (unsigned)(whole + 2 * (a.units - whole)) : (unsigned)(a.units * S * groups));
     cfg.blockDim = dim3(W * 32);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
@@ -1086,13 +1115,13 @@ static int tc_occ() {
 
 // G > 4 (two head groups) needs ~180 registers: one CTA per SM, no spills.
 template <int BITS, int NT>
-cudaError_t launch_bits(const DecodeArgs& a, cudaStream_t s) {
+cudaError_t launch_bits(const DecodeArgs& a, cudaStream_t s, int whole = 0) {
     if constexpr (NT == 2) {
         return launch_occ<BITS, NT, 1>(a, s);
     } else {
         // G > 4 at NT = 1: two head groups as separate CTAs (two CTAs per SM each)
         const int groups = a.group > 4 ? 2 : 1;
-        if (tc_w4(a)) return launch_occ<BITS, NT, 4, 4>(a, s, groups);
+        if (tc_w4(a)) return launch_occ<BITS, NT, 4, 4>(a, s, groups, whole);
         return tc_occ() == 3 ? launch_occ<BITS, NT, 3>(a, s, groups) : launch_occ<BITS, NT, 2>(a, s, groups);
     }
 }
@@ -1162,7 +1191,7 @@ static DecodeArgs unit_range(const DecodeArgs& a, size_t u0, size_t u1) {
     return r;
 }
 
-static cudaError_t launch_nt(const DecodeArgs& a, int NT, cudaStream_t s);
+static cudaError_t launch_nt(const DecodeArgs& a, int NT, cudaStream_t s, int whole = 0);
 
 // 4-warp CTAs (four slots per SM) with k whole units per SM plus a remainder r: the SMs
 // holding k + 1 whole units set the makespan. The r remainder units are instead cut in
@@ -1194,6 +1223,13 @@ cudaError_t launch_decode_tc(const DecodeArgs& a, cudaStream_t s) {
         // this launch covers batch units [unit_base, unit_base + units); split from `first`
         const size_t first = total - nsplit;
         const size_t cut = first <= a.unit_base ? 0 : std::min(a.units, first - a.unit_base);
+        if (cut > 0 && cut < a.units && cut % 2 == 0 && !std::getenv("KVQ_TC_TWO_LAUNCH")) {
+            // one launch: `cut` solo CTAs, then 2-CTA clusters of half units (uniform cluster
+            // dimension 2: consecutive solo CTAs pair up as independent cluster mates)
+            DecodeArgs M = a;
+            M.plan_units = total;
+            return launch_nt(M, 1, s, (int)cut);
+        }
         DecodeArgs A = unit_range(a, 0, cut), B = unit_range(a, cut, a.units);
         A.plan_units = B.plan_units = total;  // same CTA shape for both
         B.unit_base = a.unit_base + cut;
@@ -1209,15 +1245,16 @@ cudaError_t launch_decode_tc(const DecodeArgs& a, cudaStream_t s) {
     return launch_nt(a, tc_nt(a), s);
 }
 
-static cudaError_t launch_nt(const DecodeArgs& a, int NT, cudaStream_t s) {
+static cudaError_t launch_nt(const DecodeArgs& a, int NT, cudaStream_t s, int whole) {
+    if (whole > 0 && NT != 1) return cudaErrorInvalidValue;
     switch (a.bits * 10 + NT) {
-        case 11: return launch_bits<1, 1>(a, s);
+        case 11: return launch_bits<1, 1>(a, s, whole);
         case 12: return launch_bits<1, 2>(a, s);
-        case 21: return launch_bits<2, 1>(a, s);
+        case 21: return launch_bits<2, 1>(a, s, whole);
         case 22: return launch_bits<2, 2>(a, s);
-        case 41: return launch_bits<4, 1>(a, s);
+        case 41: return launch_bits<4, 1>(a, s, whole);
         case 42: return launch_bits<4, 2>(a, s);
-        case 81: return launch_bits<8, 1>(a, s);
+        case 81: return launch_bits<8, 1>(a, s, whole);
         case 82: return launch_bits<8, 2>(a, s);
         default: return cudaErrorInvalidValue;
     }

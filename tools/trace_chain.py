@@ -56,3 +56,35 @@ for i in range(K):
         if len(x):
             line.append(f"{label} {us(x.min()):6.1f}/{us(x.mean()):6.1f}/{us(x.max()):6.1f}")
     print("  ".join(line))
+
+# finer breakdown of the last decode (thread 0 of each CTA): slot pairs
+rows = t[K - 1][t[K - 1][:, 0] > 0]
+names = {0: "start", 6: "tmem alloc", 7: "stats ld", 3: "dep wait", 24: "q fold", 25: "sync1", 26: "digits",
+         2: "prologue", 8: "phase A (w0)", 27: "tail scores", 30: "partials", 1: "params", 16: "phase B (w0)",
+         28: "image", 29: "output sums", 5: "end"}
+order = [0, 6, 7, 3, 24, 25, 26, 2, 8, 27, 30, 1, 16, 28, 29, 5]
+print("last decode, mean per step (us):")
+prev = None
+for k in order:
+    x = rows[:, k]
+    if (x > 0).all():
+        if prev is not None:
+            print(f"  {names[prev]:>13s} -> {names[k]:<13s} {np.mean(x - rows[:, prev]) / 1e3:6.2f}")
+        prev = k
+
+# per-SM load of the last decode: CTAs per SM and the SM's last end
+sm = rows[:, 31] - 1
+end = (rows[:, 5] - t0) / 1e3
+from collections import Counter
+per = {}
+for i in range(len(rows)):
+    per.setdefault(int(sm[i]), []).append((i, end[i]))
+ends = sorted((max(e for _, e in v), k, len(v)) for k, v in per.items())
+cnt = Counter(len(v) for v in per.values())
+print("CTAs per SM:", dict(cnt), " SMs used:", len(per))
+print("latest SMs (end us, sm, ctas, cta ids):")
+for e, k, nn in ends[-6:]:
+    print(f"  {e:7.1f} sm {k:3d} ctas {nn} ids {[i for i, _ in per[k]]}")
+print("earliest SMs:")
+for e, k, nn in ends[:4]:
+    print(f"  {e:7.1f} sm {k:3d} ctas {nn} ids {[i for i, _ in per[k]]}")
