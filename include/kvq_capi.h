@@ -190,6 +190,11 @@ int kvq_cache_info(const kvq_cache* c, size_t info[10]);
 int kvq_cache_calibration(const kvq_cache* c, float tau[2]);
 /* CacheMemory (kvcache.hpp:28-35, 123-135): code, stats, quantized, tail, fp32_vis, total. */
 int kvq_cache_memory(const kvq_cache* c, size_t mem[6]);
+/* Device bytes actually resident for the packed codes (no reference counterpart; the
+   reference holds one copy, kvcache.hpp:123-135): [0] K rows, [1] V rows (reference layout,
+   0 when V lives only in the decode's operand layout), [2] V operand layout (vx),
+   [3] derived layouts built on demand (tcgen05 V, rebuilt V rows). */
+int kvq_cache_resident_bytes(const kvq_cache* c, size_t bytes[4]);
 /* key_segment / value_segment (93-94) of unit u = b*kv_heads + h, which 0 = K, 1 = V:
  * bytes (kvq_segment_bytes(n_vis, ...)) in the reference layout, alpha/beta [dim]. */
 int kvq_cache_read_segment(const kvq_cache* c, size_t unit, int which, uint8_t* bytes,

@@ -154,9 +154,14 @@ struct kvq_cache {
     cudaEvent_t ev_fork = nullptr, ev_kv = nullptr, ev_join = nullptr;  // kvq_cache_step fork / join
     cudaGraphExec_t step_exec = nullptr;  // kvq_cache_step replay for the buffers in step_key
     StepKey step_key;
-    DevBuf<uint8_t> codes;   // [2][units][n_vis][rb]  (K then V)
+    // K codes in the reference layout. V codes: a tensor-core-eligible cache (d = 128, G <= 8)
+    // holds them ONLY as the decode's operand layout (vx) - one resident copy; the reference
+    // rows are rebuilt on demand (v_ref / read-back / snapshots). Others keep [2][...] rows.
+    DevBuf<uint8_t> codes;   // [1 or 2][units][n_vis][rb]  (K, then V unless v_operand_only)
+    bool v_operand_only = false;
     DevBuf<uint8_t> vt;      // token-packed V codes for the tcgen05 decode (d = 128, M = 8)
     DevBuf<uint8_t> vx;      // V codes pre-arranged as IMMA operands for the default decode
+    DevBuf<uint8_t> vref;    // reference-layout V rebuilt from vx for the generic / tcgen05 paths
     DevBuf<float> stats;     // [2 (K,V)][2 (alpha,beta)][units][dim]
     DevBuf<float> k_tail, v_tail;  // [units][tail_cap][dim]
     DevBuf<float> lse;             // [units][group] decode log-sum-exp for the tail pass
@@ -169,7 +174,7 @@ struct kvq_cache {
     DevBuf<int> viol;
 
     uint8_t* k_codes() const { return codes.p; }
-    uint8_t* v_codes() const { return codes.p ? codes.p + units * n_vis * rb : nullptr; }
+    uint8_t* v_codes() const { return codes.p && !v_operand_only ? codes.p + units * n_vis * rb : nullptr; }
     float* k_alpha() const { return stats.p; }
     float* k_beta() const { return stats.p + units * dim; }
     float* v_alpha() const { return stats.p + 2 * units * dim; }
@@ -205,5 +210,11 @@ kvq_cache* build_common(size_t batch, size_t kv_heads, size_t group, size_t n_vi
                         int mode, int word_bits, float tau1, float tau2);
 void ensure_vx(kvq_cache* c, cudaStream_t s);
 void ensure_vt(kvq_cache* c, cudaStream_t s);
+// Reference-layout V rows: the resident copy, or rebuilt from vx into c->vref (kept).
+const uint8_t* v_ref(kvq_cache* c, cudaStream_t s);
+// Reference-layout V rows into `tmp` when V is held only as vx (one-off read-backs).
+const uint8_t* v_ref_tmp(kvq_cache* c, DevBuf<uint8_t>& tmp, cudaStream_t s);
+// Store reference-layout V rows (build / load): into the cache, or packed into vx.
+void store_v_rows(kvq_cache* c, const uint8_t* rows, cudaStream_t s);
 
 }  // namespace kvqb::capi

@@ -1067,6 +1067,57 @@ __global__ void __launch_bounds__(32) pack_vx_kernel(const uint8_t* __restrict__
 
 }  // namespace
 
+// Inverse of pack_vx_kernel: the reference rows (bitpack.hpp:64-90, M-bit words via the byte
+// fold) of every token, for read-back, snapshots and the generic path when V is resident
+// only in the operand layout. Thread = token of a 32-token block.
+namespace {
+template <int BITS>
+__global__ void __launch_bounds__(32) unpack_vx_kernel(const uint8_t* __restrict__ vx, size_t n, size_t nb32, int bx,
+                                                       uint8_t* __restrict__ rows) {
+    constexpr int kRowBytes = 16 * BITS;
+    constexpr int cpb = 8 / BITS;
+    constexpr uint32_t kLevel = (1u << BITS) - 1u;
+    const size_t unit = blockIdx.y, blk = blockIdx.x;
+    const int ti = threadIdx.x;  // token 2 t + half + 8 j of the block
+    const size_t tok = blk * 32 + ti;
+    if (tok >= n) return;
+    const int j = ti >> 3, t = (ti & 7) >> 1, half = ti & 1;
+    const uint32_t* words = reinterpret_cast<const uint32_t*>(vx + (unit * nb32 + blk) * 32 * (size_t)(16 * BITS));
+    uint8_t row[kRowBytes];
+#pragma unroll
+    for (int k = 0; k < kRowBytes; ++k) row[k] = 0;
+#pragma unroll 4
+    for (int c = 0; c < 128; ++c) {
+        const int rho = 2 * (c >> 4) + ((c >> 3) & 1), lane = 4 * (c & 7) + t;
+        const int x = rho / cpb, sl = rho % cpb;
+        const uint32_t w = __ldg(words + lane * 4 * BITS + half * 2 * BITS + x);
+        const uint32_t code = (w >> (8 * j + BITS * sl)) & kLevel;
+        const int i = c % cpb;
+        row[(c / cpb) ^ bx] |= (uint8_t)(code << (8 - BITS * (i + 1)));
+    }
+    uint8_t* dst = rows + (unit * n + tok) * kRowBytes;
+#pragma unroll
+    for (int k = 0; k < kRowBytes; ++k) dst[k] = row[k];
+}
+}  // namespace
+
+cudaError_t launch_unpack_vx(const uint8_t* vx, size_t units, size_t n_vis, int bits, int word_bits, uint8_t* rows,
+                             cudaStream_t s) {
+    if (n_vis == 0 || units == 0) return cudaSuccess;
+    const size_t nb32 = (n_vis + 31) / 32;
+    dim3 grid((unsigned)nb32, (unsigned)units);
+    const int bx = word_bits / 8 - 1;
+    switch (bits) {
+        case 1: unpack_vx_kernel<1><<<grid, 32, 0, s>>>(vx, n_vis, nb32, bx, rows); break;
+        case 2: unpack_vx_kernel<2><<<grid, 32, 0, s>>>(vx, n_vis, nb32, bx, rows); break;
+        case 4: unpack_vx_kernel<4><<<grid, 32, 0, s>>>(vx, n_vis, nb32, bx, rows); break;
+        case 8: unpack_vx_kernel<8><<<grid, 32, 0, s>>>(vx, n_vis, nb32, bx, rows); break;
+        default: return cudaErrorInvalidValue;
+    }
+    note_launch();
+    return cudaGetLastError();
+}
+
 size_t vx_bytes(size_t units, size_t n_vis, int bits) { return units * ((n_vis + 31) / 32) * 32 * 16 * (size_t)bits; }
 
 cudaError_t launch_pack_vx(const uint8_t* rows, size_t units, size_t n_vis, int bits, int word_bits, uint8_t* vx,
@@ -1180,7 +1231,7 @@ static DecodeArgs unit_range(const DecodeArgs& a, size_t u0, size_t u1) {
     DecodeArgs r = a;
     const size_t rb = row_bytes(a.dim, a.bits, a.word_bits), d = a.dim, G = a.group;
     r.k_codes += u0 * a.n_vis * rb;
-    r.v_codes += u0 * a.n_vis * rb;
+    if (r.v_codes) r.v_codes += u0 * a.n_vis * rb;
     if (r.v_codes_x) r.v_codes_x += vx_bytes(u0, a.n_vis, a.bits);
     r.k_alpha += u0 * d, r.k_beta += u0 * d, r.v_alpha += u0 * d, r.v_beta += u0 * d;
     r.k_tail += u0 * a.tail_cap * d, r.v_tail += u0 * a.tail_cap * d;

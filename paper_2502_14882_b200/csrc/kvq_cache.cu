@@ -224,6 +224,7 @@ void run_decode(kvq_cache* c, const float* q, float* out, bool want_weights, boo
         if (c->viol.n < c->units * c->group) c->viol.alloc(c->units * c->group);
         a.violations = c->viol.p;
     }
+    a.v_codes = v_ref(c, s);
     ck(kvqb::launch_decode_generic(a, s), "decode (generic)");
 }
 
@@ -258,7 +259,11 @@ kvq_cache* build_common(size_t batch, size_t kv_heads, size_t group, size_t n_vi
     ck(cudaEventCreateWithFlags(&c->ev_tjoin, cudaEventDisableTiming), "event");
     c->stats.alloc(4 * c->units * dim);
     ck(cudaMemsetAsync(c->stats.p, 0, sizeof(float) * c->stats.n, c->stream), "memset");
-    c->codes.alloc(2 * c->units * c->n_vis * c->rb);
+    // one resident V copy: eligible caches keep V only in the tensor-core operand layout
+    static const bool keep_rows = std::getenv("KVQ_KEEP_V_ROWS") != nullptr;  // (debug)
+    c->v_operand_only = !full && dim == 128 && c->n_vis > 0 && group <= 8 && !keep_rows;
+    c->codes.alloc((c->v_operand_only ? 1 : 2) * c->units * c->n_vis * c->rb);
+    if (c->v_operand_only) c->vx.alloc(kvqb::vx_bytes(c->units, c->n_vis, c->bits));
     c->tail_len.alloc(batch + 1);  // + the append overflow flag
     ck(cudaMemsetAsync(c->tail_len.p, 0, sizeof(int) * (batch + 1), c->stream), "memset");
     c->d_q.alloc(c->q_elems());
@@ -273,8 +278,10 @@ kvq_cache* build_common(size_t batch, size_t kv_heads, size_t group, size_t n_vi
 void quantize_prefill(kvq_cache* c, const float* dk, const float* dv, cudaStream_t s) {
     const size_t u = c->units, n = c->n_vis, d = c->dim;
     const float* srcs[2] = {dk, dv};
+    DevBuf<uint8_t> vrows;  // V rows staged for the operand layout (v_operand_only)
+    if (c->v_operand_only) vrows.alloc(u * n * c->rb);
     for (int which = 0; which < 2; ++which) {
-        uint8_t* codes = which == 0 ? c->k_codes() : c->v_codes();
+        uint8_t* codes = which == 0 ? c->k_codes() : (c->v_operand_only ? vrows.p : c->v_codes());
         float* alpha = which == 0 ? c->k_alpha() : c->v_alpha();
         float* beta = which == 0 ? c->k_beta() : c->v_beta();
         if (kvqb::quantize_fused_supported(n, d, c->word_bits, c->mode)) {
@@ -286,20 +293,50 @@ void quantize_prefill(kvq_cache* c, const float* dk, const float* dv, cudaStream
                "quantize");
         }
     }
+    if (c->v_operand_only) {
+        store_v_rows(c, vrows.p, s);
+        sync(s);  // the staged rows are released on return
+    }
 }
 
-// Device layout for the tcgen05 decode: V codes re-packed along the token axis. Built on
-// first use of that path (the default IMMA path reads the reference layout).
+// V operand layout of the IMMA decode (vx). An eligible cache built it at build / load time
+// and holds V only there; a cache that keeps reference rows (KVQ_KEEP_V_ROWS) builds it on
+// first use.
 void ensure_vx(kvq_cache* c, cudaStream_t s) {
-    if (c->vx.p || c->dim != 128 || c->n_vis == 0 || c->bits == KVQ_FULL_PRECISION_BITS) return;
+    if (c->v_operand_only || c->vx.p || c->dim != 128 || c->n_vis == 0 || c->bits == KVQ_FULL_PRECISION_BITS) return;
     c->vx.alloc(kvqb::vx_bytes(c->units, c->n_vis, c->bits));
     ck(kvqb::launch_pack_vx(c->v_codes(), c->units, c->n_vis, c->bits, c->word_bits, c->vx.p, s), "pack vx");
+}
+
+void store_v_rows(kvq_cache* c, const uint8_t* rows, cudaStream_t s) {
+    if (c->n_vis == 0) return;
+    if (c->v_operand_only)
+        ck(kvqb::launch_pack_vx(rows, c->units, c->n_vis, c->bits, c->word_bits, c->vx.p, s), "pack vx");
+    else if (rows != c->v_codes())
+        ck(cudaMemcpyAsync(c->v_codes(), rows, c->units * c->n_vis * c->rb, cudaMemcpyDeviceToDevice, s), "V rows");
+}
+
+const uint8_t* v_ref_tmp(kvq_cache* c, DevBuf<uint8_t>& tmp, cudaStream_t s) {
+    if (!c->v_operand_only) return c->v_codes();
+    if (c->vref.p) return c->vref.p;
+    tmp.alloc(c->units * c->n_vis * c->rb);
+    ck(kvqb::launch_unpack_vx(c->vx.p, c->units, c->n_vis, c->bits, c->word_bits, tmp.p, s), "unpack vx");
+    return tmp.p;
+}
+
+const uint8_t* v_ref(kvq_cache* c, cudaStream_t s) {
+    if (!c->v_operand_only) return c->v_codes();
+    if (!c->vref.p) {
+        c->vref.alloc(c->units * c->n_vis * c->rb);
+        ck(kvqb::launch_unpack_vx(c->vx.p, c->units, c->n_vis, c->bits, c->word_bits, c->vref.p, s), "unpack vx");
+    }
+    return c->vref.p;
 }
 
 void ensure_vt(kvq_cache* c, cudaStream_t s) {
     if (c->vt.p || c->dim != 128 || c->word_bits != 8 || c->n_vis == 0) return;
     c->vt.alloc(kvqb::vt_bytes(c->units, c->n_vis, c->bits));
-    ck(kvqb::launch_pack_vt(c->v_codes(), c->units, c->n_vis, c->bits, c->vt.p, s), "pack vt");
+    ck(kvqb::launch_pack_vt(v_ref(c, s), c->units, c->n_vis, c->bits, c->vt.p, s), "pack vt");
 }
 
 void fill_full_precision_tail(kvq_cache* c, const float* k, const float* v, size_t n, cudaMemcpyKind kind) {
@@ -330,7 +367,7 @@ kvqb::DecodeArgs range_args(const kvqb::DecodeArgs& a, const kvq_cache* c, size_
     kvqb::DecodeArgs r = a;
     const size_t u0 = b0 * c->kv_heads, d = c->dim, G = c->group;
     r.k_codes += u0 * c->n_vis * c->rb;
-    r.v_codes += u0 * c->n_vis * c->rb;
+    if (r.v_codes) r.v_codes += u0 * c->n_vis * c->rb;
     if (r.v_codes_x) r.v_codes_x += kvqb::vx_bytes(u0, c->n_vis, c->bits);
     r.k_alpha += u0 * d;
     r.k_beta += u0 * d;
@@ -670,11 +707,21 @@ int kvq_cache_memory(const kvq_cache* cc, size_t mem[6]) {
     return KVQ_OK;
 }
 
+int kvq_cache_resident_bytes(const kvq_cache* c, size_t bytes[4]) {
+    const size_t seg = c->units * c->n_vis * c->rb;
+    bytes[0] = seg;
+    bytes[1] = c->v_operand_only ? 0 : seg;
+    bytes[2] = c->vx.n;
+    bytes[3] = c->vt.n + c->vref.n;
+    return KVQ_OK;
+}
+
 int kvq_cache_read_segment(const kvq_cache* c, size_t unit, int which, uint8_t* bytes, float* alpha, float* beta) {
     return guarded([&] {
         if (unit >= c->units) raise(KVQ_ERR_DOMAIN, "segment index out of range");
         const size_t seg = c->n_vis * c->rb;
-        const uint8_t* src = (which == 0 ? c->k_codes() : c->v_codes());
+        DevBuf<uint8_t> tmp;
+        const uint8_t* src = which == 0 ? c->k_codes() : v_ref_tmp(const_cast<kvq_cache*>(c), tmp, c->stream);
         if (seg && bytes) ck(cudaMemcpyAsync(bytes, src + unit * seg, seg, cudaMemcpyDeviceToHost, c->stream), "D2H");
         const float* a = (which == 0 ? c->k_alpha() : c->v_alpha()) + unit * c->dim;
         const float* b = (which == 0 ? c->k_beta() : c->v_beta()) + unit * c->dim;
@@ -698,7 +745,12 @@ int kvq_cache_read_tail(const kvq_cache* cc, size_t unit, int which, float* out)
 
 int kvq_cache_device_pointers(const kvq_cache* c, void* ptrs[9]) {
     ptrs[0] = c->k_codes();
-    ptrs[1] = c->v_codes();
+    // V reference rows: rebuilt from the operand layout (and kept) for an eligible cache
+    const int st = guarded([&] {
+        ptrs[1] = const_cast<uint8_t*>(v_ref(const_cast<kvq_cache*>(c), c->stream));
+        sync(c->stream);
+    });
+    if (st != KVQ_OK) return st;
     ptrs[2] = c->k_alpha();
     ptrs[3] = c->k_beta();
     ptrs[4] = c->v_alpha();

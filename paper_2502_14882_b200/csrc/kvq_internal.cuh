@@ -104,6 +104,8 @@ cudaError_t launch_tail_merge(const DecodeArgs& a, const float* part, cudaStream
 #endif
 constexpr size_t kTcTailMax = KVQ_TC_TAIL_MAX;  // tail capacity the tensor-core decodes keep in-kernel
 size_t vx_bytes(size_t units, size_t n_vis, int bits);
+cudaError_t launch_unpack_vx(const uint8_t* vx, size_t units, size_t n_vis, int bits, int word_bits, uint8_t* rows,
+                             cudaStream_t s);
 cudaError_t launch_pack_vx(const uint8_t* rows, size_t units, size_t n_vis, int bits, int word_bits, uint8_t* vx,
                            cudaStream_t s);
 // tcgen05 (UTCIMMA) path, d = 128, M = 8: needs the token-packed V copy.

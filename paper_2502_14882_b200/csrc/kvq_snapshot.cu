@@ -218,11 +218,12 @@ int kvq_cache_save_image(const kvq_cache* c, void* image, size_t capacity, int i
         } else {
             std::memcpy(img, head, kCacheHeader);
         }
+        DevBuf<uint8_t> vtmp;  // V rows rebuilt from the operand layout (v_operand_only)
         for (int w = 0; w < 2; ++w) {
             put_headers(seg_at[w], hdr.data(), kSegHeader);
             put_headers(seg_at[w] + kSegHeader + r.code_bytes, hdr.data() + kSegHeader, 8);
             put_headers(ten_at[w], hdr.data() + kSegHeader + 8, kTensorHeader);
-            const uint8_t* codes = w == 0 ? c->k_codes() : c->v_codes();
+            const uint8_t* codes = w == 0 ? c->k_codes() : v_ref_tmp(const_cast<kvq_cache*>(c), vtmp, s);
             if (r.code_bytes)
                 ck(cudaMemcpy2DAsync(rec0 + seg_at[w] + kSegHeader, pitch, codes, r.code_bytes, r.code_bytes, U, to, s),
                    "save");
@@ -295,9 +296,11 @@ int kvq_cache_load_image(const void* image, size_t bytes, size_t batch, size_t g
             // records are equal-sized, so each payload is one strided copy
             const size_t pitch = heads > 1 ? segs[2].codes_at - segs[0].codes_at : 0;
             const size_t rb_bytes = n_vis * c->rb;
+            DevBuf<uint8_t> vtmp;  // V rows staged for the operand layout (v_operand_only)
             for (int w = 0; w < 2; ++w) {
                 const SegInfo& s0 = segs[w];
-                uint8_t* codes = w == 0 ? c->k_codes() : c->v_codes();
+                if (w == 1 && c->v_operand_only && rb_bytes) vtmp.alloc(U * rb_bytes);
+                uint8_t* codes = w == 0 ? c->k_codes() : (c->v_operand_only ? vtmp.p : c->v_codes());
                 if (rb_bytes)
                     ck(cudaMemcpy2DAsync(codes, rb_bytes, img + s0.codes_at, pitch ? pitch : rb_bytes, rb_bytes, U,
                                          cudaMemcpyHostToDevice, c->stream), "load");
@@ -314,6 +317,7 @@ int kvq_cache_load_image(const void* image, size_t bytes, size_t batch, size_t g
                                          c->stream), "load");
             }
             std::vector<int> lens(c->batch, (int)n_txt);
+            if (c->v_operand_only) store_v_rows(c, vtmp.p, c->stream);
             c->tail_len.upload(lens.data(), c->batch, c->stream);
             c->n_tail = n_txt;
             sync(c->stream);

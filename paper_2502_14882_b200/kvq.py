@@ -105,6 +105,7 @@ def lib() -> C.CDLL:
             "kvq_cache_info": (C.c_int, [_VP, _SZP]),
             "kvq_cache_calibration": (C.c_int, [_VP, _F]),
             "kvq_cache_memory": (C.c_int, [_VP, _SZP]),
+            "kvq_cache_resident_bytes": (C.c_int, [_VP, _SZP]),
             "kvq_cache_read_segment": (C.c_int, [_VP, _SZ, C.c_int, _U8, _F, _F]),
             "kvq_cache_read_tail": (C.c_int, [_VP, _SZ, C.c_int, _F]),
             "kvq_cache_device_pointers": (C.c_int, [_VP, C.POINTER(_VP)]),
@@ -876,6 +877,13 @@ class BatchedCache:
         m = (C.c_size_t * 6)()
         _check(lib().kvq_cache_memory(self._h, m))
         return CacheMemory(*[int(x) for x in m])
+
+    def resident_bytes(self) -> dict:
+        """Device bytes held for the codes: K rows, V rows (0 when V lives only in the
+        decode's operand layout), the V operand layout, derived layouts built on demand."""
+        m = (C.c_size_t * 4)()
+        _check(lib().kvq_cache_resident_bytes(self._h, m))
+        return dict(zip(("k_rows", "v_rows", "v_operand", "derived"), (int(x) for x in m)))
 
     def segment(self, unit: int, which: int) -> QuantizedSegment:
         n, d = self.vis_tokens(), self.dim

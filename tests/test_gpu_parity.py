@@ -128,6 +128,41 @@ def test_quantize_device_matches_oracle_d128(kvq, oracle, bits, word_bits):
         assert np.array_equal(codes[m], oracle.quantize(x[m], a, b, bits, word_bits)), f"unit {m}"
 
 
+@pytest.mark.parametrize("bits", [1, 2, 4, 8])
+@pytest.mark.parametrize("word_bits", [8, 16, 32])
+def test_single_resident_v_copy(kvq, oracle, bits, word_bits):
+    """A d = 128 cache holds V once - only in the decode's operand layout (vx) - and rebuilds
+    the reference rows on demand: value_segment (kvcache.hpp:93-94) is still bit-exact,
+    and the generic path (which reads reference rows) agrees with the tensor-core path."""
+    rng = np.random.default_rng(40 + bits + word_bits)
+    B, H, G, n, d = 2, 3, 2, 777, 128  # n not a multiple of 32: the last block is padded
+    k = rng.normal(size=(B, H, n, d)).astype(np.float32)
+    v = rng.normal(size=(B, H, n, d)).astype(np.float32)
+    v[0, 1, :, 5] = 0.25  # degenerate channel
+    cfg = kvq.QuantizationConfig(bits, kvq.QuantMode.channel_wise, word_bits)
+    cache = kvq.BatchedCache.build(k, v, cfg, kvq.CalibrationParams(1.0, 0.0), group=G)
+    rb = d * bits // 8
+    res = cache.resident_bytes()
+    assert res["k_rows"] == B * H * n * rb
+    assert res["v_rows"] == 0, "a second resident V copy"
+    assert res["v_operand"] == B * H * (-(-n // 32) * 32) * rb
+    assert res["derived"] == 0
+    for u in range(B * H):
+        b, h = divmod(u, H)
+        va, vb = oracle.compute_stats(v[b, h])
+        seg = cache.segment(u, 1)
+        assert bits_eq(seg.stats.alpha, va) and bits_eq(seg.stats.beta, vb)
+        assert np.array_equal(seg.codes.bytes, oracle.quantize(v[b, h], va, vb, bits, word_bits)), f"unit {u}"
+    assert cache.resident_bytes()["derived"] == 0  # read-back staged, not kept
+    q = rng.normal(size=(B, H, G, d)).astype(np.float32)
+    cache.set_path(kvq.PATH_AUTO)
+    tc = cache.decode(q)[0]
+    cache.set_path(kvq.PATH_GENERIC)
+    gen = cache.decode(q)[0]
+    assert cache.resident_bytes()["derived"] == B * H * n * rb  # generic path: rows kept
+    assert rel_l2(tc, gen) <= TOL_IMMA
+
+
 # ---- standalone kernels.hpp / calibrate.hpp -------------------------------------------------
 
 def test_kernel_golden_fixtures(kvq):
