@@ -365,26 +365,29 @@ def run_ours(args, world, rank, local):
         tails[r] += args.tail
     stream.synchronize()
 
-    # Eager warm-up (allocates the decode scratch), then CUDA graphs: per replica the whole
-    # step [K2 decode + K3 append] (the timed steps: programmatic dependent launch edges stay
-    # inside the graph, no host launches in the timed region), and one chain of the R
-    # replicas' decodes back to back (the second pass: the decode kernel's own time with its
-    # PDL overlap intact, no events between launches).
+    # Eager warm-up (allocates the decode scratch), then CUDA graphs of whole steps [K2 decode
+    # + K3 append] through kvq_cache_step_device (one kernel per step when the decode owns
+    # the fp32 tail in-kernel: the append is fused into it). A serving engine captures a
+    # decode iteration as one graph, so consecutive kernels keep their programmatic
+    # dependent launch edges: the timed steps replay graphs of consecutive steps (one per
+    # round over the R replicas, plus one of the first K % R steps) - no host launch and no
+    # graph boundary between steps. A second graph chains the R replicas' decodes alone (the
+    # roofline's kernel time, no events between launches).
     for t in range(R):
-        caches[t].decode_device(q[t % 4], out, sptr)
-        caches[t].append_device(kn[t % 4], vn[t % 4], sptr)
+        caches[t].step_device(q[t % 4], out, kn[t % 4], vn[t % 4], sptr)
         tails[t] += 1
     stream.synchronize()
-    g_step = []
-    launches_step = 0
-    for r in range(R):
-        gs = torch.cuda.CUDAGraph()
+
+    def capture_steps(count):
+        g = torch.cuda.CUDAGraph()
         l0 = kvq.launch_count()
-        with torch.cuda.graph(gs, stream=stream):
-            caches[r].decode_device(q[r % 4], out, sptr)
-            caches[r].append_device(kn[r % 4], vn[r % 4], sptr)
-        launches_step = kvq.launch_count() - l0
-        g_step.append(gs)
+        with torch.cuda.graph(g, stream=stream):
+            for r in range(count):
+                caches[r].step_device(q[r % 4], out, kn[r % 4], vn[r % 4], sptr)
+        return g, (kvq.launch_count() - l0) // count
+
+    g_round, launches_step = capture_steps(R)
+    g_part = capture_steps(K % R)[0] if K % R else None
     g_chain = torch.cuda.CUDAGraph()
     l0 = kvq.launch_count()
     with torch.cuda.graph(g_chain, stream=stream):
@@ -392,14 +395,18 @@ def run_ours(args, world, rank, local):
             caches[r].decode_device(q[r % 4], out, sptr)
     launches_dec = (kvq.launch_count() - l0) // R
 
-    def step(t):
-        r = t % R
+    def run_steps(count):  # `count` steps from replica 0: whole rounds, then the first count % R
         with torch.cuda.stream(stream):
-            g_step[r].replay()
-        tails[r] += 1
+            for _ in range(count // R):
+                g_round.replay()
+            if count % R:
+                assert count % R == K % R
+                g_part.replay()
+        for t in range(count):
+            tails[t % R] += 1
 
-    for t in range(W):
-        step(t)
+    W_run = -(-W // R) * R  # warm-up in whole rounds (>= the requested W steps)
+    run_steps(W_run)
     stream.synchronize()
     if world > 1:
         torch.distributed.barrier()
@@ -414,11 +421,10 @@ def run_ours(args, world, rank, local):
         # while all K steps are enqueued, so no launch gap lands inside an event interval.
         with torch.cuda.stream(stream):
             torch.cuda._sleep(int(4e7))
+        for i in range(K):  # the timed steps' tail lengths (replica i % R, before its append)
+            bytes_alg += units * alg_bytes_unit(n, bits, G, tails[i % R] + i // R)
         start.record(stream)
-        for i in range(K):
-            t = W + i
-            bytes_alg += units * alg_bytes_unit(n, bits, G, tails[t % R])
-            step(t)
+        run_steps(K)
         stop.record(stream)
         stream.synchronize()
         # second pass: the decode chain (roofline timing of the dominant kernel)
@@ -515,7 +521,9 @@ def run_ours(args, world, rank, local):
             "dtype": f"u{bits}", "data": "synthetic (gaussian K/V/q, torch.randn on device)",
             "config": workload_config(args, world),
             "per_gpu": {"value": value / world, "unit": "tokens/s/GPU", "rank0_units": units},
-            "impl_details": {"tail_window": TAIL_WINDOW,
+            "impl_details": {"tail_window": TAIL_WINDOW, "warmup_steps_run": W_run,
+                             "graph": f"steps replayed as CUDA graphs of {R} consecutive steps (one round over the "
+                                      "replicas; PDL edges between steps kept)",
                              "l2": f"inputs larger than L2: {R} rotating cache replicas x {cache_bytes / 2**20:.1f} MiB",
                              "step": "K2 decode (all q heads) + K3 append", "decode_path": args.path},
             "hbm_gbs": bytes_alg / K / (ms_per_step * 1e-3) / 1e9,

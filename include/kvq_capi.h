@@ -177,6 +177,12 @@ int kvq_cache_append_device(kvq_cache* c, const float* k_new, const float* v_new
 int kvq_cache_decode(kvq_cache* c, const float* queries, float* out, float* weights,
                      size_t* slope_violations);
 int kvq_cache_decode_device(kvq_cache* c, const float* queries, float* out, void* stream);
+/* decode_step(queries) then append(k_new, v_new) on device buffers and a user stream
+ * (graph-capturable): one kernel when the tensor-core decode owns the fp32 tail in-kernel
+ * (it writes the new rows and moves tail_len on after every unit read it), else the decode
+ * and the append kernel. Same results as kvq_cache_decode_device + kvq_cache_append_device. */
+int kvq_cache_step_device(kvq_cache* c, const float* queries, const float* k_new, const float* v_new,
+                          float* out, void* stream);
 
 /* One serving step through host buffers, in the reference bench order (kvq_main.cpp:
  * 313-321): decode_step(queries) then append(k_new, v_new). Host->device copies, both

@@ -168,7 +168,8 @@ struct kvq_cache {
     DevBuf<float> tail_part;       // [units][group][130] tail-pass partials (concurrent schedule)
     cudaStream_t tstream = nullptr;  // the tail pass, concurrent with the decode
     cudaEvent_t ev_tfork = nullptr, ev_tjoin = nullptr;
-    DevBuf<int> tail_len;    // [batch + 1]: rows per request, then the append overflow flag
+    DevBuf<int> tail_len;    // [2 batch + 1]: rows per request, the append overflow flag, the
+                             // fused-append counters per request (self-resetting)
     DevBuf<float> d_q, d_out, d_knew, d_vnew, scratch, weights;
     DevBuf<uint8_t> tc_scratch;  // prep-kernel outputs of the tcgen05 decode path
     DevBuf<int> viol;
@@ -181,6 +182,7 @@ struct kvq_cache {
     float* v_beta() const { return stats.p + 3 * units * dim; }
     size_t q_elems() const { return units * group * dim; }
     int* overflow_flag() const { return tail_len.p ? tail_len.p + batch : nullptr; }
+    int* append_counters() const { return tail_len.p ? tail_len.p + batch + 1 : nullptr; }  // fused append
     ~kvq_cache() {
         if (stream) cudaStreamDestroy(stream);
         if (side) cudaStreamDestroy(side);
@@ -205,7 +207,8 @@ namespace kvqb::capi {
 void grow_tail(kvq_cache* c, size_t need);
 void sync_tail(kvq_cache* c);
 kvqb::DecodeArgs decode_args(kvq_cache* c, const float* q, float* out);
-void run_decode(kvq_cache* c, const float* q, float* out, bool want_weights, bool want_viol, cudaStream_t s);
+void run_decode(kvq_cache* c, const float* q, float* out, bool want_weights, bool want_viol, cudaStream_t s,
+                const float* k_new = nullptr, const float* v_new = nullptr);
 kvq_cache* build_common(size_t batch, size_t kv_heads, size_t group, size_t n_vis, size_t dim, int bitwidth,
                         int mode, int word_bits, float tau1, float tau2);
 void ensure_vx(kvq_cache* c, cudaStream_t s);

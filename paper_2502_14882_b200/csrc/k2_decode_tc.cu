@@ -27,6 +27,7 @@
 #include <cooperative_groups.h>
 
 #include <cstdlib>
+#include <type_traits>
 
 #include "kvq_internal.cuh"
 #include "kvq_ptx.cuh"
@@ -67,6 +68,7 @@ struct TcParams {
     int whole;   // mixed launch: CTAs [0, whole) each own a whole unit alone (T1 tokens); the
     int T1;      // rest are S-CTA clusters of the remaining units (0: uniform launch)
     int split_first;  // mixed launch: the split units' CTAs come first in the grid
+    int late_trigger; // release dependents at exit instead of after the dependency wait
 };
 
 // ---- PTX helpers (mbarriers, bulk copies, cluster barriers, PDL: kvq_ptx.cuh) ---------
@@ -343,8 +345,24 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
     // grid dependency resolves; only q and the tail come from the preceding kernel.
     const float v_a = __ldg(a.v_alpha + unit * kDim + (threadIdx.x & (kDim - 1)));   // output channel
     const float v_b = __ldg(a.v_beta + unit * kDim + (threadIdx.x & (kDim - 1)));
-    const float k_a = __ldg(a.k_alpha + unit * kDim + (threadIdx.x & (kDim - 1)));   // prologue channel
-    const float k_b = __ldg(a.k_beta + unit * kDim + (threadIdx.x & (kDim - 1)));
+    // q fold: warp w < 4 NT folds head slot w (heads >= G fold to zero digits); lane l
+    // owns channels l + 32 i. The K step per channel (quantize.hpp:91-127 grid) is ready
+    // before the dependency wait.
+    constexpr int kHeadSlots = 4 * NT;
+    const bool folder = warp < kHeadSlots;
+    const int fh = warp;  // head slot folded by this warp
+    const float levels = (float)((1u << BITS) - 1u);
+    float f_ka[4], f_stp[4];
+    if (folder) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int c = lane + 32 * i;
+            const float ka = __ldg(a.k_alpha + unit * kDim + c), kbeta = __ldg(a.k_beta + unit * kDim + c);
+            const float range = __fsub_rn(kbeta, ka);
+            f_ka[i] = ka;
+            f_stp[i] = range > 0.0f ? __fdiv_rn(range, levels) : -1.0f;  // < 0: degenerate channel
+        }
+    }
     if (threadIdx.x == 0) TTRACE(7);
     // The previous step's append (tail rows, tail_len) and q are visible from here on. A
     // balancing sibling launch (dep_wait_at_end) starts only once every CTA of the first
@@ -354,54 +372,67 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
     const int ntl = own_tail ? __ldcg(a.tail_len + unit / a.kv_heads) : 0;
     // Dependents (the tail pass, or the append) may launch now: this grid is fully resident
     // once every CTA has passed here, and they wait for its completion before writing.
-    griddep_launch();
+    if (!p.late_trigger) griddep_launch();
     if (threadIdx.x == 0) TTRACE(3);
 
     // ---- fold the K scales into the query (scale_query, kernels.hpp:183-194) ----
     // Q'_c = round(S_h qs_c / 2^sh_c) in 4 balanced int8 digit planes, S_h bounding the
-    // int32 score so IMMA accumulation is exact; computed by every CTA for its own unit
-    // while its TMA ring fills (the pw tiles are idle until phase B). Two barriers.
-    float* s_red = reinterpret_cast<float*>(sm.pw);  // [2][8][4]: per-warp sum|qs|, sum q.alpha
-    uint32_t* s_frag = reinterpret_cast<uint32_t*>(s_red + 64);  // [NT][512] B fragments
-    const float levels = (float)((1u << BITS) - 1u);
+    // int32 score so IMMA accumulation is exact. One warp per head slot: warp-level sums,
+    // digits scattered straight into the B-fragment tiles (the pw tiles are idle until
+    // phase B); one barrier publishes tiles, per-head constants and the TMEM allocation.
+    float* s_head = reinterpret_cast<float*>(sm.pw);               // [8][2]: S_h, q.alpha
+    uint32_t* s_frag = reinterpret_cast<uint32_t*>(s_head + 16);   // [NT][512] B fragments
     const float isd0 = __fdiv_rn(1.0f, sqrtf((float)kDim));
-    // S_h: |score_int| <= (2^b - 1) * sum|Q_c| <= 2^30 (exact int32 accumulation). Any S_h
-    // with that bound is exact; the same value scales Q and the score back (cA).
-    auto scale_of = [&](int h) {
-        const float sum_abs = (s_red[h * 4 + 0] + s_red[h * 4 + 1]) + (s_red[h * 4 + 2] + s_red[h * 4 + 3]);
-        return sum_abs > 0.0f ? 1073741824.0f * __frcp_rn(levels * sum_abs) : 0.0f;
-    };
-    for (int e = threadIdx.x; e < NT * 512; e += W * 32) s_frag[e] = 0u;  // heads >= G stay 0
-    float qsv[8];
-    if (threadIdx.x < kDim) {
-        const int c = threadIdx.x;
-        const float ka = k_a, kbeta = k_b;
-        float qv[8];
+    if (folder) {
+        const bool live = fh < G;
+        float qsv[4], ab = 0.0f, sa = 0.0f;
 #pragma unroll
-        for (int h = 0; h < 8; ++h) qv[h] = h < G ? a.q[qrow(h) * kDim + c] : 0.0f;
-        const float range = __fsub_rn(kbeta, ka);
-        const float stp = range > 0.0f ? __fdiv_rn(range, levels) : 0.0f;
-        float ab[8], sa[8];
-#pragma unroll
-        for (int h = 0; h < 8; ++h) {
-            qsv[h] = range > 0.0f ? __fmul_rn(qv[h], stp) : 0.0f;
-            ab[h] = fabsf(qsv[h]);
-            sa[h] = __fmul_rn(qv[h], ka);
+        for (int i = 0; i < 4; ++i) {
+            const float qv = live ? a.q[qrow(fh) * kDim + lane + 32 * i] : 0.0f;
+            qsv[i] = f_stp[i] > 0.0f ? __fmul_rn(qv, f_stp[i]) : 0.0f;
+            ab += fabsf(qsv[i]);
+            sa += __fmul_rn(qv, f_ka[i]);
         }
 #pragma unroll
-        for (int o = 16; o; o >>= 1)
+        for (int o = 16; o; o >>= 1) {
+            ab += __shfl_xor_sync(0xffffffffu, ab, o);
+            sa += __shfl_xor_sync(0xffffffffu, sa, o);
+        }
+        // S_h: |score_int| <= (2^b - 1) * sum|Q_c| <= 2^30 (exact int32 accumulation). Any
+        // S_h with that bound is exact; the same value scales Q and the score back (cA).
+        const float S_h = ab > 0.0f ? 1073741824.0f * __frcp_rn(levels * ab) : 0.0f;
+        if (lane == 0) s_head[2 * fh] = S_h, s_head[2 * fh + 1] = sa;
+        // B fragments: entry (hg, pp, kb, r, lane(gg, tt)) byte j = digit plane 2pp + gg%2 of
+        // head 4hg + gg/2 at channel k_channel(tt, 2kb + r, j): invert k_channel
+        // (ch = (4 (t BITS + u) + j) cpb + cpb - 1 - s, rho = u cpb + s).
+        constexpr int cpb = Gm::kCpb;
+        uint8_t* fb = reinterpret_cast<uint8_t*>(s_frag);
+        const int hg = fh >> 2;
 #pragma unroll
-            for (int h = 0; h < 8; ++h) {
-                ab[h] += __shfl_xor_sync(0xffffffffu, ab[h], o);
-                sa[h] += __shfl_xor_sync(0xffffffffu, sa[h], o);
+        for (int i = 0; i < 4; ++i) {
+            const int c = lane + 32 * i;
+            // raw row byte of channel c: c / cpb for M = 8, the same byte of the reversed LE
+            // word for M = 16 / 32 (bitpack.hpp:85)
+            const int s_slot = cpb - 1 - c % cpb, qidx = (c / cpb) ^ (a.word_bits / 8 - 1);
+            const int j = qidx & 3, tb = qidx >> 2;
+            const int tt = tb / BITS, u = tb % BITS;
+            const int rho = u * cpb + s_slot, kb = rho >> 1, r = rho & 1;
+            const int sh = s_slot * BITS;
+            const int Q = __float2int_rn(__fmul_rn(qsv[i], S_h) * __int_as_float((127 - sh) << 23));
+            // balanced base-256 digits: Q = d0 + 2^8 d1 + 2^16 d2 + 2^24 d3
+            const int d0 = ((Q + 128) & 255) - 128;
+            const int q1 = (Q - d0) >> 8;
+            const int d1 = ((q1 + 128) & 255) - 128;
+            const int q2 = (q1 - d1) >> 8;
+            const int d2 = ((q2 + 128) & 255) - 128;
+            const int d3 = (q2 - d2) >> 8;
+            const int dg[4] = {d0, d1, d2, d3};
+#pragma unroll
+            for (int plane = 0; plane < 4; ++plane) {
+                const int gg = 2 * (fh & 3) + (plane & 1), pp = plane >> 1;
+                const int e = ((((hg * 2 + pp) * 4 + kb) * 2 + r) * 32) + gg * 4 + tt;
+                fb[4 * e + j] = (uint8_t)(dg[plane] & 255);
             }
-        if (lane < 8) {
-            float x = ab[0], y = sa[0];
-#pragma unroll
-            for (int h = 1; h < 8; ++h)
-                if (lane == h) x = ab[h], y = sa[h];
-            s_red[(0 * 8 + lane) * 4 + warp] = x;
-            s_red[(1 * 8 + lane) * 4 + warp] = y;
         }
     }
     if (threadIdx.x == 0) TTRACE(24);
@@ -412,43 +443,33 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
     const uint32_t tbase = *sm.tmem_slot;
     // lanes of warp quarter (warp % 4); warps 4..7 use the upper half of the columns
     const uint32_t tmem_w = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * kSteps * 4 * NT);
-    // B fragments: entry (hg, pp, kb, r, lane(gg, tt)) byte j = digit plane 2pp + gg%2 of
-    // head 4hg + gg/2 at channel k_channel(tt, 2kb + r, j). Thread c scatters its channel's
-    // digits: invert k_channel (ch = (4 (t BITS + u) + j) cpb + cpb - 1 - s, rho = u cpb + s).
-    if (threadIdx.x < kDim) {
-        constexpr int cpb = Gm::kCpb;
-        const int c = threadIdx.x;
-        // raw row byte of channel c: c / cpb for M = 8, the same byte of the reversed LE word
-        // for M = 16 / 32 (bitpack.hpp:85)
-        const int s_slot = cpb - 1 - c % cpb, qidx = (c / cpb) ^ (a.word_bits / 8 - 1);
-        const int j = qidx & 3, tb = qidx >> 2;
-        const int tt = tb / BITS, u = tb % BITS;
-        const int rho = u * cpb + s_slot, kb = rho >> 1, r = rho & 1;
-        const int sh = s_slot * BITS;
-        uint8_t* fb = reinterpret_cast<uint8_t*>(s_frag);
-#pragma unroll
-        for (int h = 0; h < 8; ++h) {
-            if (h >= G) break;
-            const int Q = __float2int_rn(__fmul_rn(qsv[h], scale_of(h)) * __int_as_float((127 - sh) << 23));
-            // balanced base-256 digits: Q = d0 + 2^8 d1 + 2^16 d2 + 2^24 d3
-            const int d0 = ((Q + 128) & 255) - 128;
-            const int q1 = (Q - d0) >> 8;
-            const int d1 = ((q1 + 128) & 255) - 128;
-            const int q2 = (q1 - d1) >> 8;
-            const int d2 = ((q2 + 128) & 255) - 128;
-            const int d3 = (q2 - d2) >> 8;
-            const int dg[4] = {d0, d1, d2, d3};
-            const int hg = h >> 2;
-#pragma unroll
-            for (int plane = 0; plane < 4; ++plane) {
-                const int gg = 2 * (h & 3) + (plane & 1), pp = plane >> 1;
-                const int e = ((((hg * 2 + pp) * 4 + kb) * 2 + r) * 32) + gg * 4 + tt;
-                fb[4 * e + j] = (uint8_t)(dg[plane] & 255);
+    if (threadIdx.x == 0) TTRACE(26);
+    // Fused append (K3, kvcache.hpp:99-109; semantics of k3_append.cu): rank 0 of head group
+    // 0 writes its unit's new K / V row to slot ntl - the decode reads rows < ntl only; every
+    // tail-owning CTA of the request then counts itself (after the barrier above, so its
+    // threads have read tail_len) and the last one moves tail_len on. The next decode sees
+    // both after its dependency wait (this grid complete).
+    if (a.k_new && own_tail) {
+        const int req = unit / (int)a.kv_heads;
+        const bool fits = ntl < (int)a.tail_cap;
+        if (fits && grp == 0 && threadIdx.x < kDim / 4) {
+            const size_t src = (size_t)unit * kDim + 4 * threadIdx.x;
+            const size_t dst = ((size_t)unit * a.tail_cap + ntl) * kDim + 4 * threadIdx.x;
+            *reinterpret_cast<float4*>(const_cast<float*>(a.k_tail) + dst) = *reinterpret_cast<const float4*>(a.k_new + src);
+            *reinterpret_cast<float4*>(const_cast<float*>(a.v_tail) + dst) = *reinterpret_cast<const float4*>(a.v_new + src);
+        }
+        if (threadIdx.x == 0) {
+            __threadfence();
+            const int owners = (int)a.kv_heads * p.groups;
+            if (atomicAdd(a.append_cnt + req, 1) == owners - 1) {
+                a.append_cnt[req] = 0;
+                if (fits)
+                    const_cast<int*>(a.tail_len)[req] = ntl + 1;
+                else
+                    atomicOr(a.overflow, 1);
             }
         }
     }
-    if (threadIdx.x == 0) TTRACE(26);
-    __syncthreads();
     uint32_t bq[NT][2][4][2];  // [head group][digit-plane pair][k-block][reg]
     float cA[NT], cB[NT], lo[NT], hi[NT];
 #pragma unroll
@@ -464,11 +485,9 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
         const int h = 4 * hg + t;  // this lane's head in C columns 2t, 2t+1
         float ca = 0.f, cb = 0.f;
         if (h < G) {
-            const float S_h = scale_of(h);
-            const float qdota = (s_red[(8 + h) * 4 + 0] + s_red[(8 + h) * 4 + 1]) +
-                                (s_red[(8 + h) * 4 + 2] + s_red[(8 + h) * 4 + 3]);
+            const float S_h = s_head[2 * h];
             ca = S_h > 0.0f ? isd0 / S_h : 0.0f;
-            cb = qdota * isd0;
+            cb = s_head[2 * h + 1] * isd0;
         }
         cA[hg] = ca, cB[hg] = cb;
         lo[hg] = INFINITY, hi[hg] = -INFINITY;
@@ -747,20 +766,26 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
         float e[4][NT][4], zm[NT];
 #pragma unroll
         for (int hg = 0; hg < NT; ++hg) zm[hg] = -INFINITY;
+        auto exps = [&](auto masked) {  // two instantiations: no per-token checks in full groups
 #pragma unroll
-        for (int bb = 0; bb < 4; ++bb)
+            for (int bb = 0; bb < 4; ++bb)
 #pragma unroll
-            for (int hg = 0; hg < NT; ++hg)
+                for (int hg = 0; hg < NT; ++hg)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    float zz = __fmaf_rn(__uint_as_float(zr[(bb * NT + hg) * 4 + j]), pa[hg], pb[hg]);
-                    if (!gfull) {
-                        const int tok = (b0 + bb) * 32 + 16 * (j >> 1) + 8 * (j & 1) + g;
-                        zz = tok < nv ? zz : -INFINITY;
+                    for (int j = 0; j < 4; ++j) {
+                        float zz = __fmaf_rn(__uint_as_float(zr[(bb * NT + hg) * 4 + j]), pa[hg], pb[hg]);
+                        if constexpr (decltype(masked)::value) {
+                            const int tok = (b0 + bb) * 32 + 16 * (j >> 1) + 8 * (j & 1) + g;
+                            zz = tok < nv ? zz : -INFINITY;
+                        }
+                        zm[hg] = fmaxf(zm[hg], zz);
+                        e[bb][hg][j] = ex2(zz);
                     }
-                    zm[hg] = fmaxf(zm[hg], zz);
-                    e[bb][hg][j] = ex2(zz);
-                }
+        };
+        if (gfull)
+            exps(std::false_type{});
+        else
+            exps(std::true_type{});
         float sc[NT], up[NT];
 #pragma unroll
         for (int hg = 0; hg < NT; ++hg) {
@@ -851,6 +876,7 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
     }
 
     if (lane == 0) TTRACE(16 + warp);  // phase B done, per warp
+    if (p.late_trigger == 2) griddep_launch();
     // the output pass's first 16 fp32 tail V values of this thread's channel: loads go out
     // now, under the CTA reduction below
     float tvv[16];
@@ -994,7 +1020,14 @@ cudaError_t launch_occ(const DecodeArgs& a, cudaStream_t s, int groups = 1, int 
     }
     cudaError_t e = cudaSuccess;
     static const int split_first = std::getenv("KVQ_TC_SPLIT_FIRST") ? std::atoi(std::getenv("KVQ_TC_SPLIT_FIRST")) : 0;
-    TcParams p{a, S, T, groups, whole, T1, split_first};
+    // Dependents are released after phase B (late_trigger 2), so the next grid's CTAs are
+    // placed once this grid's slots drain: released right after the dependency wait, they
+    // land on the SMs that finish first and stack four whole units there (c2: 40 SMs with
+    // 4.0 units instead of 3.5, profiles/r02_decode_c2.md). Early release (0) where a
+    // dependent must overlap this grid: the fp32 tail pass, a sibling balancing grid.
+    static const int trig_env = std::getenv("KVQ_TC_TRIGGER") ? std::atoi(std::getenv("KVQ_TC_TRIGGER")) : -1;
+    const int late = a.early_trigger || a.tail_lse ? 0 : trig_env >= 0 ? trig_env : 2;
+    TcParams p{a, S, T, groups, whole, T1, split_first, late};
     // TMEM: 512 columns per SM; never let more CTAs share an SM than TMEM can serve (a
     // blocked tcgen05.alloc inside a cluster could deadlock against its partners).
     const size_t max_ctas = W == 4 ? 4 : (OCC == 1 ? 1 : 2);
@@ -1236,6 +1269,7 @@ static DecodeArgs unit_range(const DecodeArgs& a, size_t u0, size_t u1) {
     r.k_alpha += u0 * d, r.k_beta += u0 * d, r.v_alpha += u0 * d, r.v_beta += u0 * d;
     r.k_tail += u0 * a.tail_cap * d, r.v_tail += u0 * a.tail_cap * d;
     r.tail_len += u0 / a.kv_heads;
+    if (r.k_new) r.k_new += u0 * d, r.v_new += u0 * d, r.append_cnt += u0 / a.kv_heads;
     r.q += u0 * G * d, r.out += u0 * G * d;
     if (r.tail_lse) r.tail_lse += u0 * G;
     r.units = u1 - u0;
@@ -1286,6 +1320,7 @@ cudaError_t launch_decode_tc(const DecodeArgs& a, cudaStream_t s) {
         B.unit_base = a.unit_base + cut;
         B.split_override = 2;
         if (cut > 0) {
+            A.early_trigger = 1;  // B overlaps A
             cudaError_t e = launch_nt(A, 1, s);
             if (e != cudaSuccess || cut == a.units) return e;
             B.dep_wait_at_end = 1;  // launched behind A (see the kernel's dependency wait)

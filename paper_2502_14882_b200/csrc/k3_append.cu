@@ -17,9 +17,6 @@ __global__ void append_kernel(const float* __restrict__ k_new, const float* __re
                               size_t kv_heads, size_t dim, size_t tail_cap,
                               float* __restrict__ k_tail, float* __restrict__ v_tail,
                               int* __restrict__ tail_len, int* __restrict__ overflow) {
-    // The next decode (launched with programmatic stream serialization) may start its
-    // prologue now; it reads the tail only after griddepcontrol.wait (= this grid done).
-    asm volatile("griddepcontrol.launch_dependents;");
     const size_t b = blockIdx.x;
     const size_t n = kv_heads * dim;
     const bool vec = (dim % 4) == 0;
@@ -36,6 +33,11 @@ __global__ void append_kernel(const float* __restrict__ k_new, const float* __re
             }
         }
         asm volatile("griddepcontrol.wait;" ::: "memory");
+        // The next decode (programmatic stream serialization) may start its prologue now; it
+        // reads the tail only after its own griddepcontrol.wait (= this grid done). Released
+        // only here - once the preceding decode has drained - so the decode's CTAs are placed
+        // evenly over free SMs rather than stacked on the first SMs to finish.
+        asm volatile("griddepcontrol.launch_dependents;");
         const size_t slot = (size_t)tail_len[b];
         if (slot >= tail_cap) {
             if (threadIdx.x == 0) atomicOr(overflow, 1);
@@ -56,6 +58,7 @@ __global__ void append_kernel(const float* __restrict__ k_new, const float* __re
         return;
     }
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;");
     const size_t slot = (size_t)tail_len[b];
     if (slot >= tail_cap) {
         if (threadIdx.x == 0) atomicOr(overflow, 1);

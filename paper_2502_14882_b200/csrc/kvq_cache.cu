@@ -62,6 +62,8 @@ kvqb::DecodeArgs decode_args(kvq_cache* c, const float* q, float* out) {
     a.k_tail = c->k_tail.p;
     a.v_tail = c->v_tail.p;
     a.tail_len = c->tail_len.p;
+    a.append_cnt = c->append_counters();
+    a.overflow = c->overflow_flag();
     a.q = q;
     a.out = out;
     a.units = c->units;
@@ -124,6 +126,14 @@ static bool tail_concurrent() {
     return env ? std::atoi(env) != 0 : false;
 }
 
+// Step = decode + append as ONE kernel when the tensor-core decode owns the tail in-kernel
+// (one dependency hop per step instead of two); KVQ_FUSED_APPEND=0 issues the append
+// kernel behind the decode instead (same results).
+static bool fused_append() {
+    static const char* env = std::getenv("KVQ_FUSED_APPEND");
+    return env ? std::atoi(env) != 0 : true;
+}
+
 // The tensor-core decode a plain decode of this cache runs: KVQ_PATH_TC (the IMMA kernel,
 // k2_decode_tc.cu), or -1 (the shape needs another path). Builds the V operand layout it
 // reads (vx) on first use. (Round 2 measured three alternative schedules of the same
@@ -147,9 +157,17 @@ void launch_tensor_decode(int kind, const kvqb::DecodeArgs& a, cudaStream_t s) {
     ck(kvqb::launch_decode_tc(a, s), "decode (tc)");
 }
 
+// k_new / v_new (device, nullable): the step's append, fused into the tensor-core decode
+// when it owns the fp32 tail in-kernel, else issued as the append kernel right behind.
 void run_decode(kvq_cache* c, const float* q, float* out, bool want_weights, bool want_viol,
-                cudaStream_t s) {
+                cudaStream_t s, const float* k_new, const float* v_new) {
     kvqb::DecodeArgs a = decode_args(c, q, out);
+    bool appended = false;
+    auto append_rest = [&] {
+        if (k_new && !appended)
+            ck(kvqb::launch_append(k_new, v_new, c->batch, c->kv_heads, c->dim, c->tail_cap, c->k_tail.p,
+                                   c->v_tail.p, c->tail_len.p, c->overflow_flag(), s), "append");
+    };
     const bool plain = !want_weights && !want_viol;
     kvqb::DecodeArgs probe = a;
     probe.v_codes_t = reinterpret_cast<const uint8_t*>(1);  // shape check only
@@ -186,6 +204,7 @@ void run_decode(kvq_cache* c, const float* q, float* out, bool want_weights, boo
         a.umma_qb = c->tc_scratch.p;
         a.tc_qconst = reinterpret_cast<float2*>(c->tc_scratch.p + c->units * 2 * 512 * sizeof(uint32_t));
         traced(c, a, s, [&] { ck(kvqb::launch_decode_umma(a, s), "decode (umma)"); });
+        append_rest();
         return;
     }
     if (tc_kind >= 0) {
@@ -199,16 +218,23 @@ void run_decode(kvq_cache* c, const float* q, float* out, bool want_weights, boo
             traced(c, a, s, [&] { launch_tensor_decode(tc_kind, a, s); });
             ck(cudaStreamWaitEvent(s, c->ev_tjoin, 0), "event");
             ck(kvqb::launch_tail_merge(a, c->tail_part.p, s), "decode (tail merge)");
+            append_rest();
             return;
+        }
+        if (k_new && !a.tail_lse && fused_append()) {  // in-kernel tail: the decode appends
+            a.k_new = k_new, a.v_new = v_new;
+            appended = true;
         }
         traced(c, a, s, [&] { launch_tensor_decode(tc_kind, a, s); });
         if (a.tail_lse) ck(kvqb::launch_decode_tail(a, true, s), "decode (tail)");
+        append_rest();
         return;
     }
     // A pure fp32 cache (build_full_precision): the tail pass is the whole decode.
     if (plain && c->n_vis == 0 && c->path != KVQ_PATH_GENERIC && c->path != KVQ_PATH_DEQUANT &&
         kvqb::decode_tail_supported(a)) {
         ck(kvqb::launch_decode_tail(a, false, s), "decode (tail)");
+        append_rest();
         return;
     }
     size_t need = c->units * c->group * (c->n_vis + c->tail_cap);
@@ -226,6 +252,7 @@ void run_decode(kvq_cache* c, const float* q, float* out, bool want_weights, boo
     }
     a.v_codes = v_ref(c, s);
     ck(kvqb::launch_decode_generic(a, s), "decode (generic)");
+    append_rest();
 }
 
 kvq_cache* build_common(size_t batch, size_t kv_heads, size_t group, size_t n_vis, size_t dim,
@@ -264,8 +291,8 @@ kvq_cache* build_common(size_t batch, size_t kv_heads, size_t group, size_t n_vi
     c->v_operand_only = !full && dim == 128 && c->n_vis > 0 && group <= 8 && !keep_rows;
     c->codes.alloc((c->v_operand_only ? 1 : 2) * c->units * c->n_vis * c->rb);
     if (c->v_operand_only) c->vx.alloc(kvqb::vx_bytes(c->units, c->n_vis, c->bits));
-    c->tail_len.alloc(batch + 1);  // + the append overflow flag
-    ck(cudaMemsetAsync(c->tail_len.p, 0, sizeof(int) * (batch + 1), c->stream), "memset");
+    c->tail_len.alloc(2 * batch + 1);  // + the append overflow flag + fused-append counters
+    ck(cudaMemsetAsync(c->tail_len.p, 0, sizeof(int) * (2 * batch + 1), c->stream), "memset");
     c->d_q.alloc(c->q_elems());
     c->d_out.alloc(c->q_elems());
     c->d_knew.alloc(c->units * dim);
@@ -376,6 +403,8 @@ kvqb::DecodeArgs range_args(const kvqb::DecodeArgs& a, const kvq_cache* c, size_
     r.k_tail += u0 * c->tail_cap * d;
     r.v_tail += u0 * c->tail_cap * d;
     r.tail_len += b0;
+    if (r.append_cnt) r.append_cnt += b0;
+    if (r.k_new) r.k_new += u0 * d, r.v_new += u0 * d;
     r.q += u0 * G * d;
     r.out += u0 * G * d;
     if (r.tail_lse) r.tail_lse += u0 * G;
@@ -646,6 +675,18 @@ int kvq_cache_decode(kvq_cache* c, const float* queries, float* out, float* weig
 
 int kvq_cache_decode_device(kvq_cache* c, const float* queries, float* out, void* stream) {
     return guarded([&] { run_decode(c, queries, out, false, false, (cudaStream_t)stream); });
+}
+
+int kvq_cache_step_device(kvq_cache* c, const float* queries, const float* k_new, const float* v_new, float* out,
+                          void* stream) {
+    return guarded([&] {
+        if (c->n_tail + 1 > c->tail_cap) {
+            ck(cudaStreamSynchronize((cudaStream_t)stream), "sync");
+            grow_tail(c, c->n_tail + 1);
+        }
+        run_decode(c, queries, out, false, false, (cudaStream_t)stream, k_new, v_new);
+        c->n_tail += 1;
+    });
 }
 
 

@@ -84,6 +84,17 @@ struct DecodeArgs {
                           // post-scaling" ablation) instead of the post-scaled products
     int dep_wait_at_end;  // tensor-core decode launched behind a sibling grid: skip the early
                           // dependency wait (the sibling did it), wait at exit instead
+    // Fused append (tensor-core decode with the in-kernel tail): the step's new K / V rows
+    // [units][dim] go to tail slot tail_len[request] (the reference's append after the
+    // decode, kvcache.hpp:99-109); append_cnt [batch] counts the request's CTAs that read
+    // tail_len, the last one bumps it. nullptr: no append.
+    const float* k_new;
+    const float* v_new;
+    int* append_cnt;
+    int* overflow;
+    int early_trigger;    // tensor-core decode: release dependents right after the dependency
+                          // wait (a dependent that must overlap: the sibling grid) instead of
+                          // after phase B
     int bits, word_bits;
     float tau1, tau2;
 };

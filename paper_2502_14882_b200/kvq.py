@@ -101,6 +101,7 @@ def lib() -> C.CDLL:
             "kvq_cache_append_device": (C.c_int, [_VP, _VP, _VP, _VP]),
             "kvq_cache_decode": (C.c_int, [_VP, _F, _F, _F, _SZP]),
             "kvq_cache_decode_device": (C.c_int, [_VP, _VP, _VP, _VP]),
+            "kvq_cache_step_device": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP]),
             "kvq_cache_step": (C.c_int, [_VP, _F, _F, _F, _F]),
             "kvq_cache_info": (C.c_int, [_VP, _SZP]),
             "kvq_cache_calibration": (C.c_int, [_VP, _F]),
@@ -954,6 +955,12 @@ class BatchedCache:
 
     def append_device(self, k_new, v_new, stream: int = 0) -> None:
         _check(lib().kvq_cache_append_device(self._h, k_new.data_ptr(), v_new.data_ptr(), stream))
+
+    def step_device(self, q, out, k_new, v_new, stream: int = 0) -> None:
+        """decode_device(q, out) then append_device(k_new, v_new), fused into one kernel when
+        the tensor-core decode owns the fp32 tail (graph-capturable, same results)."""
+        _check(lib().kvq_cache_step_device(self._h, q.data_ptr(), k_new.data_ptr(), v_new.data_ptr(),
+                                           out.data_ptr(), stream))
 
 
 class HybridKVCache:

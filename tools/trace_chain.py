@@ -12,7 +12,7 @@ sys.path.insert(0, str(ROOT))
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
 K = int(sys.argv[2]) if len(sys.argv) > 2 else 4
 (ROOT / "gpurun_out").mkdir(exist_ok=True)
-raw = str(ROOT / "gpurun_out" / "trace_chain.bin")
+raw = str(ROOT / "gpurun_out" / f"trace_chain_{cfg}.bin")
 os.environ["KVQ_TRACE_FILE"] = raw
 os.environ["KVQ_TRACE_CHAIN"] = str(K)
 import torch  # noqa: E402
@@ -31,16 +31,26 @@ TAIL = int(sys.argv[4]) if len(sys.argv) > 4 else 0  # fp32 tail rows appended f
 kn = torch.randn((batch, H, 128), device=dev)
 for c in caches:
     c.set_path(2)
-    c.reserve_tail(TAIL + 4)
+    c.reserve_tail(TAIL + 4 + (4 * K if os.environ.get('KVQ_TRACE_STEP') == '1' else 0))
     for _ in range(TAIL):
         c.append_device(kn, kn, 0)
 q = torch.randn((batch, H, G, 128), device=dev)
 out = torch.empty_like(q)
+STEP = os.environ.get("KVQ_TRACE_STEP", "0") == "1"  # fused decode + append steps (bench's step)
+
+
+def one(c):
+    if STEP:
+        c.step_device(q, out, kn, kn, 0)
+    else:
+        c.decode_device(q, out, 0)
+
+
 for i in range(K):  # warm-up chain (also dumped; overwritten below)
-    caches[i % R].decode_device(q, out, 0)
+    one(caches[i % R])
 torch.cuda.synchronize()
 for i in range(K):
-    caches[i % R].decode_device(q, out, 0)
+    one(caches[i % R])
 torch.cuda.synchronize()
 t = np.fromfile(raw, dtype=np.uint64).reshape(K, -1, 256).astype(np.int64)
 t0 = t[0][t[0][:, 0] > 0, 0].min()
