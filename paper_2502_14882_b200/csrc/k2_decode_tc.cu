@@ -158,6 +158,7 @@ struct Smem {  // carve-up of the dynamic shared memory of one decode CTA
     float* gpar;         // [8][4] softmax parameters per head
     float* wsum;         // [kWarps][8] per-warp weight sums per head (unit scale)
     uint64_t* full;      // [kWarps][kStages] TMA completion barriers
+    float* arow;         // [2][kDim] the fused append's new K / V row (staged by cp.async)
     uint32_t* tmem_slot;
 };
 
@@ -182,6 +183,7 @@ __host__ __device__ inline size_t tc_smem_bytes(int S, Smem* out = nullptr, uint
     uint8_t* gpar = take(32 * 4);
     uint8_t* wsum = take((size_t)W * 8 * 4);
     uint8_t* full = take((size_t)W * ring_stages<BITS, OCC, W>() * 8);
+    uint8_t* arow = take(2 * kDim * 4);
     uint8_t* slot = take(16);
     if (out) {
         out->ring = ring;
@@ -193,6 +195,7 @@ __host__ __device__ inline size_t tc_smem_bytes(int S, Smem* out = nullptr, uint
         out->gpar = reinterpret_cast<float*>(gpar);
         out->wsum = reinterpret_cast<float*>(wsum);
         out->full = reinterpret_cast<uint64_t*>(full);
+        out->arow = reinterpret_cast<float*>(arow);
         out->tmem_slot = reinterpret_cast<uint32_t*>(slot);
     }
     return off;
@@ -341,6 +344,10 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
         const float* ptr = base + ((size_t)unit * a.tail_cap + (l >> 3)) * kDim + 32 * (l & 3);
         asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
     }
+    // ... and with the unit's query rows (written by the preceding kernel: a prefetch is only
+    // a hint - L2 is the point of coherence, the loads proper come after the dependency wait)
+    if (threadIdx.x < 4 * G)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a.q + qrow(threadIdx.x >> 2) * kDim + 32 * (threadIdx.x & 3)));
     // Cache-build data (stats: stable since the build synchronized) is loaded before the
     // grid dependency resolves; only q and the tail come from the preceding kernel.
     const float v_a = __ldg(a.v_alpha + unit * kDim + (threadIdx.x & (kDim - 1)));   // output channel
@@ -369,7 +376,14 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
     // launch has passed this wait, so it may skip it; it waits at exit instead, keeping
     // "this grid done" = "both launches done" for the kernel that follows.
     if (!a.dep_wait_at_end) griddep_wait();
-    const int ntl = own_tail ? __ldcg(a.tail_len + unit / a.kv_heads) : 0;
+    // tail_len is read by ONE thread and broadcast through shared memory (after the prologue
+    // barrier): with the fused append, that thread also counts this CTA in (relaxed atomic,
+    // its operand data-dependent on the loaded length so it issues only after the read
+    // returned - no fence; the barrier orders the broadcast); the request's last counter
+    // moves tail_len on at exit.
+    const bool fused_append = a.k_new != nullptr && own_tail;
+    int cnt_old = -1;
+    const int ntl_read = threadIdx.x == (W - 1) * 32 && own_tail ? __ldcg(a.tail_len + unit / a.kv_heads) : 0;
     // Dependents (the tail pass, or the append) may launch now: this grid is fully resident
     // once every CTA has passed here, and they wait for its completion before writing.
     if (!p.late_trigger) griddep_launch();
@@ -435,41 +449,35 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
             }
         }
     }
+    if (threadIdx.x == (W - 1) * 32) {  // (the load has long returned: no stall here)
+        reinterpret_cast<volatile int*>(sm.tmem_slot)[1] = ntl_read;
+        if (fused_append) cnt_old = atomicAdd(a.append_cnt + unit / (int)a.kv_heads, 1 + min(ntl_read, 0));
+    }
     if (threadIdx.x == 0) TTRACE(24);
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();  // also publishes the TMEM allocation
+    __syncthreads();  // also publishes the TMEM allocation and the tail length
     if (threadIdx.x == 0) TTRACE(25);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tbase = *sm.tmem_slot;
+    const int ntl = reinterpret_cast<volatile int*>(sm.tmem_slot)[1];
+    const bool append_rows = fused_append && grp == 0 && ntl < (int)a.tail_cap;
+    if (append_rows && warp == 0) {  // K row then V row, 16 B per lane each (no register staging)
+        const size_t src = (size_t)unit * kDim + 4 * lane;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sm.arow + 4 * lane)), "l"(a.k_new + src)
+                     : "memory");
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sm.arow + kDim + 4 * lane)),
+                     "l"(a.v_new + src)
+                     : "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
     // lanes of warp quarter (warp % 4); warps 4..7 use the upper half of the columns
     const uint32_t tmem_w = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * kSteps * 4 * NT);
     if (threadIdx.x == 0) TTRACE(26);
-    // Fused append (K3, kvcache.hpp:99-109; semantics of k3_append.cu): rank 0 of head group
-    // 0 writes its unit's new K / V row to slot ntl - the decode reads rows < ntl only; every
-    // tail-owning CTA of the request then counts itself (after the barrier above, so its
-    // threads have read tail_len) and the last one moves tail_len on. The next decode sees
-    // both after its dependency wait (this grid complete).
-    if (a.k_new && own_tail) {
-        const int req = unit / (int)a.kv_heads;
-        const bool fits = ntl < (int)a.tail_cap;
-        if (fits && grp == 0 && threadIdx.x < kDim / 4) {
-            const size_t src = (size_t)unit * kDim + 4 * threadIdx.x;
-            const size_t dst = ((size_t)unit * a.tail_cap + ntl) * kDim + 4 * threadIdx.x;
-            *reinterpret_cast<float4*>(const_cast<float*>(a.k_tail) + dst) = *reinterpret_cast<const float4*>(a.k_new + src);
-            *reinterpret_cast<float4*>(const_cast<float*>(a.v_tail) + dst) = *reinterpret_cast<const float4*>(a.v_new + src);
-        }
-        if (threadIdx.x == 0) {
-            __threadfence();
-            const int owners = (int)a.kv_heads * p.groups;
-            if (atomicAdd(a.append_cnt + req, 1) == owners - 1) {
-                a.append_cnt[req] = 0;
-                if (fits)
-                    const_cast<int*>(a.tail_len)[req] = ntl + 1;
-                else
-                    atomicOr(a.overflow, 1);
-            }
-        }
-    }
+    // Fused append (K3, kvcache.hpp:99-109; semantics of k3_append.cu): the new rows were
+    // staged into shared memory by cp.async after the dependency wait and are written to slot
+    // ntl at exit (the decode reads rows < ntl only); the request's last tail owner (cnt_old,
+    // counted above) moves tail_len on at exit. The next decode sees both after its
+    // dependency wait (this grid complete).
     uint32_t bq[NT][2][4][2];  // [head group][digit-plane pair][k-block][reg]
     float cA[NT], cB[NT], lo[NT], hi[NT];
 #pragma unroll
@@ -879,10 +887,11 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
     if (p.late_trigger == 2) griddep_launch();
     // the output pass's first 16 fp32 tail V values of this thread's channel: loads go out
     // now, under the CTA reduction below
-    float tvv[16];
+    constexpr int kTvv = 32;  // tail V rows in flight per thread (phase-B registers are free here)
+    float tvv[kTvv];
     const float* vt = a.v_tail + (size_t)unit * a.tail_cap * kDim + (threadIdx.x & (kDim - 1));
 #pragma unroll
-    for (int u = 0; u < 16; ++u) tvv[u] = threadIdx.x < kDim && u < ntl ? __ldcg(vt + (size_t)u * kDim) : 0.0f;
+    for (int u = 0; u < kTvv; ++u) tvv[u] = threadIdx.x < kDim && u < ntl ? __ldcg(vt + (size_t)u * kDim) : 0.0f;
     // ---------------- CTA reduction (fixed order, deterministic) ----------------
     // Image [warp][hg][rho][lane]: consecutive lanes hit consecutive banks.
 #pragma unroll
@@ -928,12 +937,13 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
         }
         // fp32 tail (naive_wv kernels.hpp:414-426): each row value loaded once for all heads,
         // 16 loads in flight; weights precomputed in tail_s
-        for (int j0 = 0; j0 < ntl; j0 += 16) {
-            float vv[16];
+        for (int j0 = 0; j0 < ntl; j0 += kTvv) {
+            float vv[kTvv];
 #pragma unroll
-            for (int u = 0; u < 16; ++u) vv[u] = j0 == 0 ? tvv[u] : j0 + u < ntl ? __ldcg(vt + (size_t)(j0 + u) * kDim) : 0.0f;
+            for (int u = 0; u < kTvv; ++u)
+                vv[u] = j0 == 0 ? tvv[u] : j0 + u < ntl ? __ldcg(vt + (size_t)(j0 + u) * kDim) : 0.0f;
 #pragma unroll
-            for (int u = 0; u < 16; ++u) {
+            for (int u = 0; u < kTvv; ++u) {
                 if (j0 + u >= ntl) break;
 #pragma unroll
                 for (int h = 0; h < HB; ++h) {
@@ -977,6 +987,21 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
         }
     }
     if (threadIdx.x == 0) TTRACE(5);
+    if (append_rows && warp == 0) {
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        const size_t dst = ((size_t)unit * a.tail_cap + ntl) * kDim + 4 * lane;
+        *reinterpret_cast<float4*>(const_cast<float*>(a.k_tail) + dst) = *reinterpret_cast<const float4*>(sm.arow + 4 * lane);
+        *reinterpret_cast<float4*>(const_cast<float*>(a.v_tail) + dst) =
+            *reinterpret_cast<const float4*>(sm.arow + kDim + 4 * lane);
+    }
+    if (cnt_old == (int)a.kv_heads * p.groups - 1) {  // the request's last tail owner
+        const int req = unit / (int)a.kv_heads;
+        a.append_cnt[req] = 0;
+        if (ntl < (int)a.tail_cap)
+            const_cast<int*>(a.tail_len)[req] = ntl + 1;
+        else
+            atomicOr(a.overflow, 1);
+    }
     if (warp == 0) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(kTmemCols));
