@@ -16,8 +16,11 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
-OBJ = PKG / "build"
-LIB = PKG / "libkvq_b200.so"
+# KVQ_BUILD_VARIANT=name (experiments only): objects in build_<name>/, library
+# libkvq_b200_<name>.so, loaded with KVQ_LIB_PATH - the product library is untouched.
+_VARIANT = os.environ.get("KVQ_BUILD_VARIANT", "")
+OBJ = PKG / (f"build_{_VARIANT}" if _VARIANT else "build")
+LIB = PKG / (f"libkvq_b200_{_VARIANT}.so" if _VARIANT else "libkvq_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",

@@ -40,6 +40,9 @@ namespace {
 
 constexpr int kDim = 128;
 constexpr int kStages = 2;
+#ifndef KVQ_TC_PAIR  // phase A: two 1-bit blocks' IMMAs interleaved (8 independent accumulator
+#define KVQ_TC_PAIR 1  // chains between dependent IMMAs; C2 33.4 -> 33.0 us); 0 = one block at a time
+#endif
 #ifndef KVQ_TC_STAGE_BYTES  // (tuning builds)
 #define KVQ_TC_STAGE_BYTES 4096
 #endif
@@ -265,7 +268,7 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
     constexpr int kSteps = warp_tokens<NT>() / 32;                 // 32-token steps per warp, at most
     constexpr uint32_t kTmemCols = (W / 4) * kSteps * 4 * NT;        // lane-sharing warps; 256 / 128
     const DecodeArgs& a = p.a;
-    // Grid: (head group, unit, rank). With two head groups a CTA serves query heads
+    // Grid: (unit, head group, rank). With two head groups a CTA serves query heads
     // [4 grp, 4 grp + G) of its unit (softmax rows are per head, so the split is exact).
     // A mixed launch (balanced batches) puts `whole` solo CTAs first: unit = CTA index.
     // Mixed launch order: the split units' clusters first (the block scheduler deals them
@@ -278,8 +281,10 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
     const int T = solo ? p.T1 : p.T;
     const int rank = S > 1 ? (int)cg::this_cluster().block_rank() : 0;
     const int unit_g = solo ? (int)blockIdx.x - solo_base : p.whole + ((int)blockIdx.x - split_base) / S;
-    const int grp = unit_g / (int)a.units;
-    const int unit = unit_g % (int)a.units;
+    // the head groups of one unit (G > 4) are adjacent clusters: they stream the same code
+    // bytes at about the same time, so the second stream is served from L2
+    const int grp = unit_g % p.groups;
+    const int unit = unit_g / p.groups;
     const int G_all = (int)a.group;
     const int h0 = 4 * grp;
     const int G = p.groups > 1 ? min(4, G_all - h0) : G_all;
@@ -353,8 +358,7 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
     const float v_a = __ldg(a.v_alpha + unit * kDim + (threadIdx.x & (kDim - 1)));   // output channel
     const float v_b = __ldg(a.v_beta + unit * kDim + (threadIdx.x & (kDim - 1)));
     // q fold: warp w < 4 NT folds head slot w (heads >= G fold to zero digits); lane l
-    // owns channels l + 32 i. The K step per channel (quantize.hpp:91-127 grid) is ready
-    // before the dependency wait.
+    // owns channels l + 32 i. The K stats are loaded before the dependency wait.
     constexpr int kHeadSlots = 4 * NT;
     const bool folder = warp < kHeadSlots;
     const int fh = warp;  // head slot folded by this warp
@@ -364,10 +368,8 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const int c = lane + 32 * i;
-            const float ka = __ldg(a.k_alpha + unit * kDim + c), kbeta = __ldg(a.k_beta + unit * kDim + c);
-            const float range = __fsub_rn(kbeta, ka);
-            f_ka[i] = ka;
-            f_stp[i] = range > 0.0f ? __fdiv_rn(range, levels) : -1.0f;  // < 0: degenerate channel
+            f_ka[i] = __ldg(a.k_alpha + unit * kDim + c);  // in flight across the dependency wait:
+            f_stp[i] = __ldg(a.k_beta + unit * kDim + c);  // used only after it (no stall before it)
         }
     }
     if (threadIdx.x == 0) TTRACE(7);
@@ -388,6 +390,13 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
     // once every CTA has passed here, and they wait for its completion before writing.
     if (!p.late_trigger) griddep_launch();
     if (threadIdx.x == 0) TTRACE(3);
+    if (folder) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {  // the K grid step per channel (quantize.hpp:91-127)
+            const float range = __fsub_rn(f_stp[i], f_ka[i]);
+            f_stp[i] = range > 0.0f ? __fdiv_rn(range, levels) : -1.0f;  // < 0: degenerate channel
+        }
+    }
 
     // ---- fold the K scales into the query (scale_query, kernels.hpp:183-194) ----
     // Q'_c = round(S_h qs_c / 2^sh_c) in 4 balanced int8 digit planes, S_h bounding the
@@ -591,6 +600,65 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
             }
         };
         const int nsteps = (ns + 31) >> 5;  // >= 1
+        if constexpr (KVQ_TC_PAIR != 0 && BITS == 1) {
+        // two blocks' IMMAs interleaved per k-block: 8 independent accumulator chains instead
+        // of 4 between dependent IMMAs (1-bit rows are one 32-bit word per lane and row half)
+        auto mma_pair = [&](int t0, int (&a0)[NT][2][2][4], int t1, int (&a1)[NT][2][2][4]) {
+            uint32_t w[2][2][2][BITS];  // [block][u2][hf][word]
+#pragma unroll
+            for (int bk = 0; bk < 2; ++bk)
+#pragma unroll
+                for (int u2 = 0; u2 < 2; ++u2)
+#pragma unroll
+                    for (int hf = 0; hf < 2; ++hf) {
+                        const uint8_t* rowp =
+                            buf + ((bk ? t1 : t0) + 16 * u2 + 8 * hf + g) * Gm::kRowBytes + t * 4 * BITS;
+#pragma unroll
+                        for (int u = 0; u < BITS; ++u) w[bk][u2][hf][u] = reinterpret_cast<const uint32_t*>(rowp)[u];
+                    }
+#pragma unroll
+            for (int hg = 0; hg < NT; ++hg)
+#pragma unroll
+                for (int u2 = 0; u2 < 2; ++u2)
+#pragma unroll
+                    for (int pp = 0; pp < 2; ++pp)
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) a0[hg][u2][pp][e] = a1[hg][u2][pp][e] = 0;
+#pragma unroll
+            for (int kb = 0; kb < 4; ++kb)
+#pragma unroll
+                for (int bk = 0; bk < 2; ++bk) {
+                    auto& ac = bk ? a1 : a0;
+#pragma unroll
+                    for (int u2 = 0; u2 < 2; ++u2) {
+                        uint32_t r[2][2];  // [hf][rho - 2 kb]
+#pragma unroll
+                        for (int hf = 0; hf < 2; ++hf)
+#pragma unroll
+                            for (int i = 0; i < 2; ++i) {
+                                const int rho = 2 * kb + i;
+                                r[hf][i] = w[bk][u2][hf][rho / Gm::kCpb] & (Gm::kMask << ((rho % Gm::kCpb) * BITS));
+                            }
+#pragma unroll
+                        for (int hg = 0; hg < NT; ++hg)
+#pragma unroll
+                            for (int pp = 0; pp < 2; ++pp)
+                                imma_u8s8(ac[hg][u2][pp], r[0][0], r[1][0], r[0][1], r[1][1], bq[hg][pp][kb][0],
+                                          bq[hg][pp][kb][1]);
+                    }
+                }
+        };
+        int k = 0;
+        for (; k + 1 < nsteps; k += 2) {
+            mma_pair(32 * k, accA, 32 * (k + 1), accB);
+            epilogue(32 * k, accA);
+            epilogue(32 * (k + 1), accB);
+        }
+        if (k < nsteps) {
+            mma_step(32 * k, accA);
+            epilogue(32 * k, accA);
+        }
+        } else {
         mma_step(0, accA);
         int k = 1;
         for (; k + 1 < nsteps; k += 2) {  // unrolled by two: register-resident pipeline slots
@@ -605,6 +673,7 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
             epilogue(32 * k, accB);
         } else {
             epilogue(32 * (k - 1), accA);
+        }
         }
         __syncwarp();
         if (lane == 0 && st + kStagesW < total_stages) issue(st + kStagesW);
@@ -1211,7 +1280,10 @@ static bool tc_w4(const DecodeArgs& a) {
     if (env) return std::atoi(env) != 0;
     size_t pu = a.plan_units ? a.plan_units : a.units;
     if (a.group > 4) pu *= 2;
-    return pu > 2 * 148 && a.n_vis <= (size_t)cta_tokens(1, 4);
+    // long units (n > 8192) run in several rounds of CTAs either way: the 4-warp shape
+    // keeps more, smaller CTAs in flight (C4 137.5 -> 131.3 us; C3's 8192-token units stay
+    // 8-warp: 35.8 vs 39.6 us, profiles/r02_configs.md)
+    return (pu > 2 * 148 && a.n_vis <= (size_t)cta_tokens(1, 4)) || a.n_vis > (size_t)cta_tokens(1, 8);
 }
 
 static int tc_occ() {

@@ -12,6 +12,7 @@ tensors (torch is only plumbing for device memory and streams).
 from __future__ import annotations
 
 import ctypes as C
+import os
 import struct
 from dataclasses import dataclass, field
 from enum import IntEnum
@@ -20,7 +21,7 @@ from typing import Sequence
 
 import numpy as np
 
-_LIB_PATH = Path(__file__).resolve().parent / "libkvq_b200.so"
+_LIB_PATH = Path(os.environ.get("KVQ_LIB_PATH") or Path(__file__).resolve().parent / "libkvq_b200.so")
 _lib = None
 
 # ---- errors (errors.hpp:11-33) ------------------------------------------------------

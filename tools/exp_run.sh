@@ -1,0 +1,3 @@
+timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/tests_full.txt 2>&1; tail -3 gpurun_out/tests_full.txt
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.txt 2>&1
+bash tools/bench_all.sh

@@ -98,3 +98,13 @@ for e, k, nn in ends[-6:]:
 print("earliest SMs:")
 for e, k, nn in ends[:4]:
     print(f"  {e:7.1f} sm {k:3d} ctas {nn} ids {[i for i, _ in per[k]]}")
+
+# warp imbalance inside a CTA (last decode): spread of the per-warp phase A / phase B ends
+pa = rows[:, 8:16].astype(np.float64)
+pb = rows[:, 16:24].astype(np.float64)
+pa[pa == 0] = np.nan
+pb[pb == 0] = np.nan
+sa = (np.nanmax(pa, 1) - np.nanmin(pa, 1)) / 1e3
+sb = (np.nanmax(pb, 1) - np.nanmin(pb, 1)) / 1e3
+print(f"warp spread in a CTA (us): phase A end mean {np.nanmean(sa):.2f} p90 {np.nanpercentile(sa, 90):.2f}; "
+      f"phase B end mean {np.nanmean(sb):.2f} p90 {np.nanpercentile(sb, 90):.2f}")
