@@ -463,6 +463,9 @@ void step_resources(kvq_cache* c, size_t chunks) {
 //   stream  : the append, after every decode read the tail and the new rows are uploaded
 void issue_step(kvq_cache* c, const float* queries, const float* k_new, const float* v_new, float* out,
                 size_t chunks) {
+    // (Tried: the decode writing `out` straight into pinned host memory, and reading the
+    // queries from it - zero-copy, one chunk: C2 e2e 619 k -> 589 k / 386 k tok/s, C5 B=512
+    // 1.39 M -> 1.18 M; the staged, chunked copies stay.)
     cudaStream_t s = c->stream, s2 = c->side, d2h = c->d2h;
     ck(cudaEventRecord(c->ev_fork, s), "event");
     ck(cudaStreamWaitEvent(s2, c->ev_fork, 0), "event");

@@ -90,3 +90,23 @@ def test_fused_step_graph_replay_past_capacity(kvq):
     c.decode_device(q, o2, s.cuda_stream)
     s.synchronize()
     assert torch.isfinite(o2).all()
+
+
+def test_host_step_pinned_matches_pageable(kvq):
+    """kvq_cache_step (the host-buffer serving step, captured and replayed as a graph per
+    buffer set) gives the same outputs and tail for pinned and pageable host buffers."""
+    torch = pytest.importorskip("torch")
+    B, H, G, n = 4, 8, 4, 1024
+    a, b, _ = _pair(kvq, torch, B, H, G, n, 1)
+    rng = np.random.default_rng(3)
+    for step in range(3):
+        q = rng.normal(size=(B, H, G, 128)).astype(np.float32)
+        k = rng.normal(size=(B, H, 128)).astype(np.float32)
+        v = rng.normal(size=(B, H, 128)).astype(np.float32)
+        pq, pk, pv = (torch.from_numpy(x).pin_memory().numpy() for x in (q, k, v))
+        pout = torch.empty((B, H, G, 128)).pin_memory().numpy()
+        out = np.empty((B, H, G, 128), np.float32)
+        a.step(pq, pk, pv, pout)
+        b.step(q, k, v, out)
+        assert np.array_equal(pout, out), f"step {step}"
+    assert a.tail_tokens() == b.tail_tokens() == 3

@@ -47,10 +47,16 @@ def main():
             out = subprocess.run([sys.executable, str(ROOT / "tools" / "ncu_summary.py"), str(rep), "decode"],
                                  capture_output=True, text=True).stdout
             (ROOT / "profiles" / f"r02_ncu_{cfg}.json").write_text(out)
-        if not (NCU / f"{cfg}_launches.csv").exists():
-            continue
-        per, dec = launches(cfg)
-        if not dec:
+        per, dec = launches(cfg) if (NCU / f"{cfg}_launches.csv").exists() else ({}, [])
+        if not dec:  # the launch list ended before the timed steps (many replicas to build):
+            full = ROOT / "profiles" / f"r02_ncu_{cfg}.json"  # the --set full capture's launch
+            if full.exists() and full.stat().st_size > 0:
+                pl = json.loads(full.read_text())["per_launch"][0]
+                summary[cfg] = {"kernel": pl["kernel"], "dram_bytes_per_launch": round(pl["dram_bytes"]),
+                                "us_per_launch_ncu": pl["us"], "launches_averaged": 1,
+                                "source": f"ncu --set full of one decode launch of bench.py --config {cfg} "
+                                          "(tools/ncu_all.sh), round 2"}
+                print(f"| {cfg} | 1 (--set full) | {pl['us']:.1f} | {pl['dram_bytes'] / 1e6:.2f} MB | - |")
             continue
         us = sum(m.get("gpu__time_duration.sum", 0) for m in dec) / len(dec)
         byts = sum(m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0) for m in dec) / len(dec)
