@@ -1087,10 +1087,14 @@ void plan(const DecodeArgs& a, int NT, int& S, int& T, int W = kWarps) {
     int s_min = std::max(1, (n + ct - 1) / ct);
     size_t pu = a.plan_units ? a.plan_units : a.units;  // a chunk plans as its whole batch
     if (NT == 1 && a.group > 4) pu *= 2;                 // two head-group CTAs per unit
-    // split a unit only while the units leave SMs without a CTA: about one CTA per SM is the
-    // sweet spot (profiles/r01_tc_split2.txt: >= 128 units S = 1, 64 units S = 2; splitting
-    // further pays per-CTA prologues and cluster merges for no occupancy gain)
-    const int want = (int)((128 + pu - 1) / pu);
+    // split a unit only while the units leave CTA slots empty: fill the slots of one wave
+    // (2 x 148 for 8-warp CTAs), never more (round 2, c5 B = 8 = 64 units: S = 4 12.6 us vs
+    // S = 2 13.6 us vs S = 1 14.7 us; round 1 aimed at one CTA per SM,
+    // profiles/r01_tc_split2.txt). (Also measured in round 2 and dropped: the fp32 tail scores
+    // before phase A with their rows preloaded under the q fold, and every warp computing the
+    // softmax parameters itself instead of two more CTA barriers - C2 32.96 -> 34.24 / 33.68 us.)
+    const int slots = (W == 4 ? 4 : 2) * 148;
+    const int want = std::max(1, (int)(slots / pu));
     int s = std::max(s_min, std::min(want, kMaxCluster));
     static const int force = std::getenv("KVQ_TC_SPLIT") ? std::atoi(std::getenv("KVQ_TC_SPLIT")) : 0;  // tuning
     if (force > 0) s = std::max(s_min, std::min(force, kMaxCluster));
@@ -1141,8 +1145,8 @@ cudaError_t launch_occ(const DecodeArgs& a, cudaStream_t s, int groups = 1, int 
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attrs[2];
-    attrs[0].id = cudaLaunchAttributeClusterDimension;
-    attrs[0].val.clusterDim.x = (unsigned)S;
+    attrs[0].id = cudaLaunchAttributeClusterDimension;  // (S = 1 grids launch as fast without it,
+    attrs[0].val.clusterDim.x = (unsigned)S;            //  measured: c3b1 35.50 vs 35.51 us)
     attrs[0].val.clusterDim.y = 1;
     attrs[0].val.clusterDim.z = 1;
     attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
