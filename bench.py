@@ -72,10 +72,20 @@ for _b in ("c3b1", "c3b2", "c3b4"):
     ABLATIONS[_b + "_deq_nocal"] = (_b, (0.0, 0.0), "dequant", "dequant")
 
 
+# Opt-in token-wise V (north_star "token-wise min/max for V"; KVQ_MODE_V_TOKEN_WISE) on a
+# BASELINE shape: name -> base config. The CPU arm runs the reference's own (channel-wise V)
+# decode of the same shape - the reference has no token-wise mode.
+VTOKEN = {"c2_vtok": "c2", "c3b1_vtok": "c3b1", "c3b4_vtok": "c3b4"}
+
+
 def resolve_config(name: str):
     """(batch, kv_heads, group, n, bits, tau, description, path override, CPU arm)."""
     if name in CONFIGS:
         return (*CONFIGS[name], None, "post")
+    if name in VTOKEN:
+        batch, H, G, n, bits, tau, desc = CONFIGS[VTOKEN[name]]
+        desc += "; opt-in token-wise V quantization (K channel-wise); CPU arm: the reference's channel-wise V"
+        return batch, H, G, n, bits, tau, desc, None, "post"
     base, tau, path, cpu = ABLATIONS[name]
     batch, H, G, n, bits, tau0, desc = CONFIGS[base]
     tau = tau0 if tau is None else tau
@@ -90,10 +100,11 @@ TAIL_WINDOW = 32
 L2_BYTES = 126 * 1024 * 1024
 
 
-def alg_bytes_unit(n_vis: int, bits: int, group: int, n_tail: int, dim: int = DIM) -> int:
+def alg_bytes_unit(n_vis: int, bits: int, group: int, n_tail: int, dim: int = DIM, v_token_wise: bool = False) -> int:
     """Algorithmic HBM bytes of one decode step for one unit:
-    packed K+V codes + alpha/beta for K and V + q in/out + fp32 tail K+V."""
-    return 2 * n_vis * dim * bits // 8 + 4 * dim * 4 + 2 * group * dim * 4 + 2 * n_tail * dim * 4
+    packed K+V codes + alpha/beta for K and V (token-wise V: per token) + q in/out + fp32 tail K+V."""
+    v_stats = 2 * n_vis * 4 if v_token_wise else 2 * dim * 4
+    return 2 * n_vis * dim * bits // 8 + 2 * dim * 4 + v_stats + 2 * group * dim * 4 + 2 * n_tail * dim * 4
 
 
 def workload_config(args, world: int) -> dict:
@@ -111,7 +122,7 @@ def workload_config(args, world: int) -> dict:
                             f" x{world} GPUs, no collective")}
 
 
-def decode_f64(codes_k, codes_v, ka, kb, va, vb, q, kt, vt, bits, tau) -> np.ndarray:
+def decode_f64(codes_k, codes_v, ka, kb, va, vb, q, kt, vt, bits, tau, v_token_wise: bool = False) -> np.ndarray:
     """The reference decode (kvcache.hpp:263-311: post-scaled scores, calibrated softmax
     over [g(vis) | tail], w.V) in float64 on the cache's own integer codes - the spot
     check's ground truth (SURVEY.md §8c rule 4)."""
@@ -132,6 +143,8 @@ def decode_f64(codes_k, codes_v, ka, kb, va, vb, q, kt, vt, bits, tau) -> np.nda
     row = np.concatenate([vis, tail])
     p = np.exp(row - row.max())
     p /= p.sum()
+    if v_token_wise:  # va / vb per token: alpha_j + code_jc (beta_j - alpha_j) / L
+        return p[:vis.size] @ (va[:, None] + codes_v.astype(f) * sv[:, None]) + p[vis.size:] @ np.asarray(vt, f)
     return p[:vis.size] @ (va + codes_v.astype(f) * sv) + p[vis.size:] @ np.asarray(vt, f)
 
 
@@ -342,7 +355,8 @@ def run_ours(args, world, rank, local):
         k = torch.randn((batch, H, n, DIM), device=dev, dtype=torch.float32, generator=gen)
         v = torch.randn((batch, H, n, DIM), device=dev, dtype=torch.float32, generator=gen)
         for r in range(R):
-            c = kvq.BatchedCache.build_device(k, v, kvq.QuantizationConfig(bits), kvq.CalibrationParams(*tau),
+            qmode = kvq.QuantMode.v_token_wise if args.config in VTOKEN else kvq.QuantMode.channel_wise
+            c = kvq.BatchedCache.build_device(k, v, kvq.QuantizationConfig(bits, qmode), kvq.CalibrationParams(*tau),
                                               group=G, stream=sptr)
             c.reserve_tail(tail_cap + args.tail)
             c.set_path(PATHS[args.path])
@@ -422,7 +436,7 @@ def run_ours(args, world, rank, local):
         with torch.cuda.stream(stream):
             torch.cuda._sleep(int(4e7))
         for i in range(K):  # the timed steps' tail lengths (replica i % R, before its append)
-            bytes_alg += units * alg_bytes_unit(n, bits, G, tails[i % R] + i // R)
+            bytes_alg += units * alg_bytes_unit(n, bits, G, tails[i % R] + i // R, v_token_wise=args.config in VTOKEN)
         start.record(stream)
         run_steps(K)
         stop.record(stream)
@@ -435,7 +449,7 @@ def run_ours(args, world, rank, local):
                 g_chain.replay()
             c_stop.record(stream)
         stream.synchronize()
-    bytes_alg2 = sum(units * alg_bytes_unit(n, bits, G, tails[r]) for r in range(R)) / R  # per decode launch
+    bytes_alg2 = sum(units * alg_bytes_unit(n, bits, G, tails[r], v_token_wise=args.config in VTOKEN) for r in range(R)) / R  # per decode launch
     launches = K * launches_step
     # Parity spot check at the measured geometry (outside the timed region): one decode of
     # replica 0, the first / last / a middle unit against the float64 reference math on the
@@ -453,9 +467,11 @@ def run_ours(args, world, rank, local):
             ks, vs = caches[0].segment(u, 0), caches[0].segment(u, 1)
             ck, cv = unpack_rows(ks.codes.bytes, n, bits), unpack_rows(vs.codes.bytes, n, bits)
             kt, vt = caches[0].tail(u, 0), caches[0].tail(u, 1)
+            vtok = args.config in VTOKEN
+            va, vb = caches[0].value_token_stats(u) if vtok else (vs.stats.alpha, vs.stats.beta)
             for g in range(G):
-                want = decode_f64(ck, cv, ks.stats.alpha, ks.stats.beta, vs.stats.alpha, vs.stats.beta, qh[bq, hq_, g],
-                                  kt, vt, bits, tau)
+                want = decode_f64(ck, cv, ks.stats.alpha, ks.stats.beta, va, vb, qh[bq, hq_, g], kt, vt, bits, tau,
+                                  v_token_wise=vtok)
                 worst = max(worst, float(np.linalg.norm(got[bq, hq_, g] - want) / np.linalg.norm(want)))
         spot = {"units": checked, "heads": G, "max_rel_l2_vs_float64": worst, "tail_rows": int(kt.shape[0])}
     assert max(tails) <= tail_cap + args.tail, "bench tail accounting exceeded the reserved capacity"
@@ -560,7 +576,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=400)
     ap.add_argument("--warmup", type=int, default=20)
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS) + sorted(ABLATIONS))
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS) + sorted(ABLATIONS) + sorted(VTOKEN))
     ap.add_argument("--batch", type=int, default=0, help="override the config's per-GPU batch")
     ap.add_argument("--global-batch", type=int, default=0,
                     help="fixed global batch sharded over the GPUs (strong scaling); default: config batch per GPU")

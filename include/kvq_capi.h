@@ -39,6 +39,11 @@ extern "C" {
 
 #define KVQ_MODE_CHANNEL_WISE 0 /* QuantMode::channel_wise (quantize.hpp:31) */
 #define KVQ_MODE_GLOBAL 1       /* QuantMode::global */
+/* Opt-in extension (not in the reference): K channel-wise, V token-wise - min / max per
+ * visual token over its d channels (north_star; KIVI's V axis). Caches only: d = 128, a
+ * quantized prefill, the tensor-core decode (no generic-path export, no KVQC snapshot, no
+ * per-channel V segment stats: kvq_cache_read_value_token_stats reads them). */
+#define KVQ_MODE_V_TOKEN_WISE 2
 #define KVQ_FULL_PRECISION_BITS 16 /* kvcache.hpp:26 */
 
 #define KVQ_PATH_AUTO 0    /* per-CTA IMMA path when the shape allows, else tcgen05, else generic */
@@ -207,6 +212,8 @@ int kvq_cache_read_segment(const kvq_cache* c, size_t unit, int which, uint8_t* 
                            float* alpha, float* beta);
 /* key_tail / value_tail (95-96): [n_tail][dim] fp32. */
 int kvq_cache_read_tail(const kvq_cache* c, size_t unit, int which, float* out);
+/* Token-wise V caches (KVQ_MODE_V_TOKEN_WISE): the V stats of one unit, alpha / beta [n_vis]. */
+int kvq_cache_read_value_token_stats(const kvq_cache* c, size_t unit, float* alpha, float* beta);
 /* Raw device pointers (k_codes, v_codes, k_alpha, k_beta, v_alpha, v_beta, k_tail, v_tail,
  * tail_len) for zero-copy integration with a serving engine. */
 int kvq_cache_device_pointers(const kvq_cache* c, void* ptrs[9]);

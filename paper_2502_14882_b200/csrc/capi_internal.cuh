@@ -163,6 +163,7 @@ struct kvq_cache {
     DevBuf<uint8_t> vx;      // V codes pre-arranged as IMMA operands for the default decode
     DevBuf<uint8_t> vref;    // reference-layout V rebuilt from vx for the generic / tcgen05 paths
     DevBuf<float> stats;     // [2 (K,V)][2 (alpha,beta)][units][dim]
+    DevBuf<float> vtok;      // token-wise V (KVQ_MODE_V_TOKEN_WISE): [2 (alpha,beta)][units][n_vis]
     DevBuf<float> k_tail, v_tail;  // [units][tail_cap][dim]
     DevBuf<float> lse;             // [units][group] decode log-sum-exp for the tail pass
     DevBuf<float> tail_part;       // [units][group][130] tail-pass partials (concurrent schedule)
@@ -181,6 +182,7 @@ struct kvq_cache {
     float* v_alpha() const { return stats.p + 2 * units * dim; }
     float* v_beta() const { return stats.p + 3 * units * dim; }
     size_t q_elems() const { return units * group * dim; }
+    bool v_token_wise() const { return mode == KVQ_MODE_V_TOKEN_WISE; }
     int* overflow_flag() const { return tail_len.p ? tail_len.p + batch : nullptr; }
     int* append_counters() const { return tail_len.p ? tail_len.p + batch + 1 : nullptr; }  // fused append
     ~kvq_cache() {

@@ -94,7 +94,70 @@ quantize_rows_d128(const float* __restrict__ x, size_t rows, const float* __rest
     }
 }
 
+// Token-wise stats (the opt-in V mode, north_star "token-wise min/max for V"): the
+// reference quantizer (quantize.hpp:64-127) with the reduction axis swapped - alpha_j /
+// beta_j are the min / max over the 128 channels of token j, codes use that token's step.
+// One pass (a row's stats depend on the row only): warp per row, lane c owns channels
+// c + 32 w; min / max carry the channel index so ties (-0 vs +0) resolve to the first
+// channel, as std::min / std::max folding in channel order do.
+template <int BITS>
+__global__ void __launch_bounds__(kWarpsPerCta * 32)
+quantize_rows_tok_d128(const float* __restrict__ x, size_t rows, float* __restrict__ alpha, float* __restrict__ beta,
+                       uint8_t* __restrict__ codes, int word_bits) {
+    constexpr int kRowBytes = 16 * BITS;
+    const float levels = (float)((1u << BITS) - 1u);
+    const size_t m = blockIdx.y;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const float* src = x + m * rows * kDim;
+    uint8_t* dst = codes + m * rows * kRowBytes;
+    const size_t stride = (size_t)gridDim.x * kWarpsPerCta;
+    for (size_t r = (size_t)blockIdx.x * kWarpsPerCta + warp; r < rows; r += stride) {
+        float v[4];
+#pragma unroll
+        for (int w = 0; w < 4; ++w) v[w] = __ldcs(src + r * kDim + 32 * w + lane);
+        float lo = v[0], hi = v[0];
+        int li = lane, hi_i = lane;
+#pragma unroll
+        for (int w = 1; w < 4; ++w) {  // this lane's channels in order: lane, 32 + lane, ...
+            if (v[w] < lo) lo = v[w], li = 32 * w + lane;
+            if (hi < v[w]) hi = v[w], hi_i = 32 * w + lane;
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            const float l2 = __shfl_xor_sync(0xffffffffu, lo, o), h2 = __shfl_xor_sync(0xffffffffu, hi, o);
+            const int li2 = __shfl_xor_sync(0xffffffffu, li, o), hi2 = __shfl_xor_sync(0xffffffffu, hi_i, o);
+            if (l2 < lo || (l2 == lo && li2 < li)) lo = l2, li = li2;
+            if (hi < h2 || (h2 == hi && hi2 < hi_i)) hi = h2, hi_i = hi2;
+        }
+        const float range = __fsub_rn(hi, lo);
+        const float inv = range > 0.0f ? __fdiv_rn(levels, range) : 0.0f;  // quantize.hpp:102-106
+        if (lane == 0) alpha[m * rows + r] = lo, beta[m * rows + r] = hi;
+        uint32_t code[4];
+#pragma unroll
+        for (int w = 0; w < 4; ++w) code[w] = code_of(v[w], lo, inv, levels);
+        pack_store<BITS>(code, dst + r * kRowBytes, lane, word_bits);
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_quantize_tokenwise(const float* x, size_t mats, size_t rows, int bits, int word_bits,
+                                      float* alpha, float* beta, uint8_t* codes, cudaStream_t s) {
+    if (rows == 0 || mats == 0) return cudaSuccess;
+    size_t gx = (rows + kWarpsPerCta - 1) / kWarpsPerCta;
+    const size_t cap = (148 * 16 + mats - 1) / mats;
+    if (gx > cap) gx = cap < 1 ? 1 : cap;
+    dim3 grid((unsigned)gx, (unsigned)mats);
+    switch (bits) {
+        case 1: quantize_rows_tok_d128<1><<<grid, kWarpsPerCta * 32, 0, s>>>(x, rows, alpha, beta, codes, word_bits); break;
+        case 2: quantize_rows_tok_d128<2><<<grid, kWarpsPerCta * 32, 0, s>>>(x, rows, alpha, beta, codes, word_bits); break;
+        case 4: quantize_rows_tok_d128<4><<<grid, kWarpsPerCta * 32, 0, s>>>(x, rows, alpha, beta, codes, word_bits); break;
+        case 8: quantize_rows_tok_d128<8><<<grid, kWarpsPerCta * 32, 0, s>>>(x, rows, alpha, beta, codes, word_bits); break;
+        default: return cudaErrorInvalidValue;
+    }
+    note_launch();
+    return cudaGetLastError();
+}
 
 bool quantize_fused_supported(size_t rows, size_t dim, int word_bits, int mode) {
     (void)rows;

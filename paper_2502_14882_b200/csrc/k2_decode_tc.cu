@@ -159,7 +159,8 @@ struct Smem {  // carve-up of the dynamic shared memory of one decode CTA
     float* wpart;        // [kWarps][24] per-warp (min, max, tail max) per head
     float* allpart;      // [S][24] per-CTA partials (pushed by every CTA of the cluster)
     float* gpar;         // [8][4] softmax parameters per head
-    float* wsum;         // [kWarps][8] per-warp weight sums per head (unit scale)
+    float* wsum;         // [kWarps][16] per-warp weight sums per head (unit scale); [8..16):
+                         // token-wise V: the per-head sums of weight x alpha_j
     uint64_t* full;      // [kWarps][kStages] TMA completion barriers
     float* arow;         // [2][kDim] the fused append's new K / V row (staged by cp.async)
     uint32_t* tmem_slot;
@@ -184,7 +185,7 @@ __host__ __device__ inline size_t tc_smem_bytes(int S, Smem* out = nullptr, uint
     uint8_t* wpart = take((size_t)W * 24 * 4);
     uint8_t* allpart = take((size_t)(S > 0 ? S : 1) * 24 * 4);
     uint8_t* gpar = take(32 * 4);
-    uint8_t* wsum = take((size_t)W * 8 * 4);
+    uint8_t* wsum = take((size_t)W * 16 * 4);
     uint8_t* full = take((size_t)W * ring_stages<BITS, OCC, W>() * 8);
     uint8_t* arow = take(2 * kDim * 4);
     uint8_t* slot = take(16);
@@ -261,7 +262,7 @@ __device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t (&r)[N]) {
 // tensor memory (lane-private columns, tcgen05.st/ld) between the phases.
 // Cross-warp reductions of the p.V accumulators are exact integer shared-memory atomics
 // (deterministic); cross-CTA traffic is push-only.
-template <int BITS, int NT, int OCC, int W = kWarps>
+template <int BITS, int NT, int OCC, int W = kWarps, bool VTOK = false>
 __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p) {
     using Gm = Geo<BITS, stage_bytes<W>()>;
     constexpr int kStagesW = ring_stages<BITS, OCC, W>();
@@ -355,8 +356,9 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
         asm volatile("prefetch.global.L2 [%0];" ::"l"(a.q + qrow(threadIdx.x >> 2) * kDim + 32 * (threadIdx.x & 3)));
     // Cache-build data (stats: stable since the build synchronized) is loaded before the
     // grid dependency resolves; only q and the tail come from the preceding kernel.
-    const float v_a = __ldg(a.v_alpha + unit * kDim + (threadIdx.x & (kDim - 1)));   // output channel
-    const float v_b = __ldg(a.v_beta + unit * kDim + (threadIdx.x & (kDim - 1)));
+    // output channel's V stats (token-wise V: per-token stats, read in phase B instead)
+    const float v_a = VTOK ? 0.0f : __ldg(a.v_alpha + unit * kDim + (threadIdx.x & (kDim - 1)));
+    const float v_b = VTOK ? 0.0f : __ldg(a.v_beta + unit * kDim + (threadIdx.x & (kDim - 1)));
     // q fold: warp w < 4 NT folds head slot w (heads >= G fold to zero digits); lane l
     // owns channels l + 32 i. The K stats are loaded before the dependency wait.
     constexpr int kHeadSlots = 4 * NT;
@@ -819,12 +821,14 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
     constexpr int cpb = Gm::kCpb;
     float fac[NT][16];  // channel rows rho = 2 mt + r (channel 16 mt + 8 r + g), head 4 hg + t
     float fw[NT];       // weight sum of head 4 hg + t (lane's tokens), unit scale
+    float fa[NT];       // token-wise V: sum of weight x alpha_j (lane's tokens)
     float pa[NT], pb[NT];
 #pragma unroll
     for (int hg = 0; hg < NT; ++hg) {
 #pragma unroll
         for (int i = 0; i < 16; ++i) fac[hg][i] = 0.0f;
         fw[hg] = 0.0f;
+        fa[hg] = 0.0f;
         pa[hg] = sm.gpar[(4 * hg + t) * 4 + 0];
         pb[hg] = sm.gpar[(4 * hg + t) * 4 + 1];
     }
@@ -864,22 +868,70 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
         else
             exps(std::true_type{});
         float sc[NT], up[NT];
+        if constexpr (VTOK) {
+            // token-wise V (out_c = sum_j p_j alpha_j + sum_j (p_j s_j) code_jc, s_j the token's
+            // step): the IMMA weights are e_j s_j, normalised per group by their own maximum;
+            // sum_j e_j and sum_j e_j alpha_j accumulate in fp32
+            constexpr float kInvLevels = 1.0f / (float)((1u << BITS) - 1u);
+            float gm[NT];
 #pragma unroll
-        for (int hg = 0; hg < NT; ++hg) {
-            zm[hg] = fmaxf(zm[hg], __shfl_xor_sync(0xffffffffu, zm[hg], 4));
-            zm[hg] = fmaxf(zm[hg], __shfl_xor_sync(0xffffffffu, zm[hg], 8));
-            zm[hg] = fmaxf(zm[hg], __shfl_xor_sync(0xffffffffu, zm[hg], 16));
-            zm[hg] = fmaxf(zm[hg], -100.0f);
-            up[hg] = ex2(-zm[hg]) * 65534.0f;
-            sc[hg] = ex2(zm[hg]) * (1.0f / 65534.0f);
+            for (int hg = 0; hg < NT; ++hg) gm[hg] = 0.0f;
+#pragma unroll
+            for (int bb = 0; bb < 4; ++bb)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int tl = (b0 + bb) * 32 + 16 * (j >> 1) + 8 * (j & 1) + g;  // warp-local token
+                    const size_t ti = (size_t)unit * n + tok0 + min(tl, max(nv - 1, 0));
+                    const float al = __ldg(a.v_alpha + ti), be = __ldg(a.v_beta + ti);
+                    const float st = fmaxf(__fsub_rn(be, al) * kInvLevels, 0.0f);
+#pragma unroll
+                    for (int hg = 0; hg < NT; ++hg) {
+                        const float ev = e[bb][hg][j];  // 0 for masked tokens
+                        fw[hg] += ev;
+                        if (st == 0.0f) fa[hg] = __fmaf_rn(ev, al, fa[hg]);  // a flat token: v = alpha
+                        e[bb][hg][j] = ev * st;
+                        gm[hg] = fmaxf(gm[hg], e[bb][hg][j]);
+                    }
+                }
+#pragma unroll
+            for (int hg = 0; hg < NT; ++hg) {
+                gm[hg] = fmaxf(gm[hg], __shfl_xor_sync(0xffffffffu, gm[hg], 4));
+                gm[hg] = fmaxf(gm[hg], __shfl_xor_sync(0xffffffffu, gm[hg], 8));
+                gm[hg] = fmaxf(gm[hg], __shfl_xor_sync(0xffffffffu, gm[hg], 16));
+                up[hg] = gm[hg] > 0.0f ? __fdividef(65534.0f, gm[hg]) : 0.0f;
+                sc[hg] = gm[hg] * (1.0f / 65534.0f);
+            }
+        } else {
+#pragma unroll
+            for (int hg = 0; hg < NT; ++hg) {
+                zm[hg] = fmaxf(zm[hg], __shfl_xor_sync(0xffffffffu, zm[hg], 4));
+                zm[hg] = fmaxf(zm[hg], __shfl_xor_sync(0xffffffffu, zm[hg], 8));
+                zm[hg] = fmaxf(zm[hg], __shfl_xor_sync(0xffffffffu, zm[hg], 16));
+                zm[hg] = fmaxf(zm[hg], -100.0f);
+                up[hg] = ex2(-zm[hg]) * 65534.0f;
+                sc[hg] = ex2(zm[hg]) * (1.0f / 65534.0f);
+            }
         }
         __syncwarp();  // the previous group's P tiles are consumed
         uint32_t wg[NT];
+        float fo[NT];  // token-wise V: sum_j P_j o_j, o_j = alpha_j / s_j (the alpha term on the
+                       // same integer weights as the codes: v_jc = s_j (code_jc + o_j))
 #pragma unroll
-        for (int hg = 0; hg < NT; ++hg) wg[hg] = 0u;
+        for (int hg = 0; hg < NT; ++hg) wg[hg] = 0u, fo[hg] = 0.0f;
 #pragma unroll
         for (int bb = 0; bb < 4; ++bb) {
             if (bb >= nbg) break;
+            float oj[4];
+            if constexpr (VTOK) {
+                constexpr float kLevelsV = (float)((1u << BITS) - 1u);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int tl = (b0 + bb) * 32 + 16 * (j >> 1) + 8 * (j & 1) + g;
+                    const size_t ti = (size_t)unit * n + tok0 + min(tl, max(nv - 1, 0));
+                    const float al = __ldg(a.v_alpha + ti), rg = __fsub_rn(__ldg(a.v_beta + ti), al);
+                    oj[j] = rg > 0.0f ? __fdividef(al * kLevelsV, rg) : 0.0f;
+                }
+            }
 #pragma unroll
             for (int hg = 0; hg < NT; ++hg) {
                 uint32_t v[4];
@@ -887,6 +939,10 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
                 for (int j = 0; j < 4; ++j)  // round(2^(z - zm) (2^16 - 2)) in the low mantissa bits
                     v[j] = __float_as_uint(__fmaf_rn(e[bb][hg][j], up[hg], kMagic));
                 wg[hg] += (v[0] + v[1]) + (v[2] + v[3]) - 4u * 0x4B400000u;
+                if constexpr (VTOK) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) fo[hg] = __fmaf_rn(__uint_as_float(v[j]) - kMagic, oj[j], fo[hg]);
+                }
                 const uint32_t p01 = prmt(v[0], v[1], 0x5140), p23 = prmt(v[2], v[3], 0x5140);
                 uint32_t* tile = px + (bb * NT + hg) * kPxWords + t * kPxHead + g;
                 tile[0] = prmt(p01, p23, 0x5410);  // plane 0: bits 0-7 of tokens g + 8 j
@@ -948,7 +1004,8 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
                 fac[hg][2 * mt] = __fmaf_rn(__uint2float_rn(c0), sc[hg], fac[hg][2 * mt]);
                 fac[hg][2 * mt + 1] = __fmaf_rn(__uint2float_rn(c1), sc[hg], fac[hg][2 * mt + 1]);
             }
-            fw[hg] = __fmaf_rn(__uint2float_rn(wg[hg]), sc[hg], fw[hg]);
+            if constexpr (!VTOK) fw[hg] = __fmaf_rn(__uint2float_rn(wg[hg]), sc[hg], fw[hg]);
+            if constexpr (VTOK) fa[hg] = __fmaf_rn(fo[hg], sc[hg], fa[hg]);
         }
     }
 
@@ -971,7 +1028,14 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
         w += __shfl_xor_sync(0xffffffffu, w, 4);
         w += __shfl_xor_sync(0xffffffffu, w, 8);
         w += __shfl_xor_sync(0xffffffffu, w, 16);
-        if (lane < 4) sm.wsum[warp * 8 + 4 * hg + lane] = w;
+        if (lane < 4) sm.wsum[warp * 16 + 4 * hg + lane] = w;
+        if constexpr (VTOK) {
+            float wa = fa[hg];
+            wa += __shfl_xor_sync(0xffffffffu, wa, 4);
+            wa += __shfl_xor_sync(0xffffffffu, wa, 8);
+            wa += __shfl_xor_sync(0xffffffffu, wa, 16);
+            if (lane < 4) sm.wsum[warp * 16 + 8 + 4 * hg + lane] = wa;
+        }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();  // (the V stream is drained: the ring is free from here on)
@@ -994,14 +1058,17 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
         float num[HB], den[HB];
 #pragma unroll
         for (int h = 0; h < HB; ++h) {
-            float V = 0.0f, wv = 0.0f;
+            float V = 0.0f, wv = 0.0f, wa = 0.0f;
             if (h < G) {
                 for (int w2 = 0; w2 < W; ++w2) {
                     V += sm.acc[((w2 * NT + (h >> 2)) * 16 + rho) * 32 + 4 * gg + (h & 3)];
-                    wv += sm.wsum[w2 * 8 + h];
+                    wv += sm.wsum[w2 * 16 + h];
+                    if constexpr (VTOK) wa += sm.wsum[w2 * 16 + 8 + h];
                 }
             }
-            num[h] = __fmaf_rn(v_step, V * unshift, v_a * wv);
+            // channel-wise V: s_c V / 2^sh + alpha_c W; token-wise V: the per-token steps are in
+            // the weights (V / 2^sh) and the alphas in wa
+            num[h] = VTOK ? V * unshift + wa : __fmaf_rn(v_step, V * unshift, v_a * wv);
             den[h] = wv;
         }
         // fp32 tail (naive_wv kernels.hpp:414-426): each row value loaded once for all heads,
@@ -1104,7 +1171,7 @@ void plan(const DecodeArgs& a, int NT, int& S, int& T, int W = kWarps) {
     S = (n + T - 1) / T;
 }
 
-template <int BITS, int NT, int OCC, int W = kWarps>
+template <int BITS, int NT, int OCC, int W = kWarps, bool VTOK = false>
 cudaError_t launch_occ(const DecodeArgs& a, cudaStream_t s, int groups = 1, int whole = 0) {
     int S, T, S1 = 1, T1 = 0;
     if (whole > 0) {  // mixed: solo whole units, then 2-CTA clusters of half units
@@ -1132,7 +1199,7 @@ cudaError_t launch_occ(const DecodeArgs& a, cudaStream_t s, int groups = 1, int 
     size_t smem = tc_smem_bytes<BITS, NT, OCC, W>(S);
     const size_t floor_bytes = 232448 / (max_ctas + 1) + 1;
     if (smem < floor_bytes) smem = floor_bytes;
-    auto kern = decode_tc_kernel<BITS, NT, OCC, W>;
+    auto kern = decode_tc_kernel<BITS, NT, OCC, W, VTOK>;
     static unsigned attr_done = 0;  // per instantiation, bit per device
     e = once_per_device(attr_done, [&] {
         cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -1302,10 +1369,14 @@ static int tc_occ() {
 template <int BITS, int NT>
 cudaError_t launch_bits(const DecodeArgs& a, cudaStream_t s, int whole = 0) {
     if constexpr (NT == 2) {
+        if (a.v_token_wise) return cudaErrorNotSupported;  // (token-wise V: head-split CTAs only)
         return launch_occ<BITS, NT, 1>(a, s);
     } else {
         // G > 4 at NT = 1: two head groups as separate CTAs (two CTAs per SM each)
         const int groups = a.group > 4 ? 2 : 1;
+        if (a.v_token_wise)  // (opt-in token-wise V: the default occupancy variants only)
+            return tc_w4(a) ? launch_occ<BITS, NT, 4, 4, true>(a, s, groups, whole)
+                            : launch_occ<BITS, NT, 2, kWarps, true>(a, s, groups);
         if (tc_w4(a)) return launch_occ<BITS, NT, 4, 4>(a, s, groups, whole);
         return tc_occ() == 3 ? launch_occ<BITS, NT, 3>(a, s, groups) : launch_occ<BITS, NT, 2>(a, s, groups);
     }
@@ -1367,7 +1438,8 @@ static DecodeArgs unit_range(const DecodeArgs& a, size_t u0, size_t u1) {
     r.k_codes += u0 * a.n_vis * rb;
     if (r.v_codes) r.v_codes += u0 * a.n_vis * rb;
     if (r.v_codes_x) r.v_codes_x += vx_bytes(u0, a.n_vis, a.bits);
-    r.k_alpha += u0 * d, r.k_beta += u0 * d, r.v_alpha += u0 * d, r.v_beta += u0 * d;
+    const size_t vs = a.v_token_wise ? a.n_vis : d;  // V stats per unit: per channel or per token
+    r.k_alpha += u0 * d, r.k_beta += u0 * d, r.v_alpha += u0 * vs, r.v_beta += u0 * vs;
     r.k_tail += u0 * a.tail_cap * d, r.v_tail += u0 * a.tail_cap * d;
     r.tail_len += u0 / a.kv_heads;
     if (r.k_new) r.k_new += u0 * d, r.v_new += u0 * d, r.append_cnt += u0 / a.kv_heads;

@@ -57,8 +57,9 @@ kvqb::DecodeArgs decode_args(kvq_cache* c, const float* q, float* out) {
     a.v_codes_x = c->vx.p;
     a.k_alpha = c->k_alpha();
     a.k_beta = c->k_beta();
-    a.v_alpha = c->v_alpha();
-    a.v_beta = c->v_beta();
+    a.v_alpha = c->v_token_wise() ? c->vtok.p : c->v_alpha();
+    a.v_beta = c->v_token_wise() ? c->vtok.p + c->units * c->n_vis : c->v_beta();
+    a.v_token_wise = c->v_token_wise() ? 1 : 0;
     a.k_tail = c->k_tail.p;
     a.v_tail = c->v_tail.p;
     a.tail_len = c->tail_len.p;
@@ -180,7 +181,12 @@ void run_decode(kvq_cache* c, const float* q, float* out, bool want_weights, boo
         a.tail_lse = c->lse.p;
     }
     const bool generic_only = c->path == KVQ_PATH_GENERIC || c->path == KVQ_PATH_UMMA || c->path == KVQ_PATH_DEQUANT;
+    if (c->v_token_wise() && (!plain || generic_only))
+        raise(KVQ_ERR_CONFIG, "token-wise V decodes on the tensor-core path only (no probability / violation "
+                              "export, no generic / tcgen05 / dequant path)");
     const int tc_kind = plain && !generic_only ? pick_tensor_decode(c, a, s) : -1;
+    if (c->v_token_wise() && tc_kind < 0)
+        raise(KVQ_ERR_CONFIG, "token-wise V: this shape has no tensor-core decode");
     a.dequant_dot = c->path == KVQ_PATH_DEQUANT ? 1 : 0;
     // Probability-row / violation export (decode_step_detailed) is a generic-path feature:
     // an explicit tensor-core path selection applies to plain decodes only.
@@ -260,7 +266,11 @@ kvq_cache* build_common(size_t batch, size_t kv_heads, size_t group, size_t n_vi
     require_device();
     const bool full = bitwidth == KVQ_FULL_PRECISION_BITS;
     if (!full) validate_config(bitwidth, word_bits);
-    if (mode != KVQ_MODE_CHANNEL_WISE && mode != KVQ_MODE_GLOBAL) raise(KVQ_ERR_CONFIG, "unknown quant mode");
+    if (mode != KVQ_MODE_CHANNEL_WISE && mode != KVQ_MODE_GLOBAL && mode != KVQ_MODE_V_TOKEN_WISE)
+        raise(KVQ_ERR_CONFIG, "unknown quant mode");
+    if (mode == KVQ_MODE_V_TOKEN_WISE && (full || dim != 128 || n_vis == 0 || group > 8 || std::getenv("KVQ_KEEP_V_ROWS")))
+        raise(KVQ_ERR_CONFIG, "token-wise V needs head dim 128, a quantized prefill and query groups <= 8 "
+                              "(tensor-core decode)");
     // check_prefill (kvcache.hpp:224-236)
     if (batch == 0 || kv_heads == 0) raise(KVQ_ERR_DOMAIN, "cache build: need matching per-head key/value lists");
     if (group == 0) raise(KVQ_ERR_DOMAIN, "cache build: query group must be >= 1");
@@ -291,6 +301,7 @@ kvq_cache* build_common(size_t batch, size_t kv_heads, size_t group, size_t n_vi
     c->v_operand_only = !full && dim == 128 && c->n_vis > 0 && group <= 8 && !keep_rows;
     c->codes.alloc((c->v_operand_only ? 1 : 2) * c->units * c->n_vis * c->rb);
     if (c->v_operand_only) c->vx.alloc(kvqb::vx_bytes(c->units, c->n_vis, c->bits));
+    if (c->v_token_wise()) c->vtok.alloc(2 * c->units * c->n_vis);
     c->tail_len.alloc(2 * batch + 1);  // + the append overflow flag + fused-append counters
     ck(cudaMemsetAsync(c->tail_len.p, 0, sizeof(int) * (2 * batch + 1), c->stream), "memset");
     c->d_q.alloc(c->q_elems());
@@ -311,11 +322,18 @@ void quantize_prefill(kvq_cache* c, const float* dk, const float* dv, cudaStream
         uint8_t* codes = which == 0 ? c->k_codes() : (c->v_operand_only ? vrows.p : c->v_codes());
         float* alpha = which == 0 ? c->k_alpha() : c->v_alpha();
         float* beta = which == 0 ? c->k_beta() : c->v_beta();
-        if (kvqb::quantize_fused_supported(n, d, c->word_bits, c->mode)) {
-            ck(kvqb::launch_quantize_fused(srcs[which], u, n, d, c->bits, c->word_bits, c->mode, alpha, beta, codes, s),
+        if (which == 1 && c->v_token_wise()) {  // opt-in: V stats per token (one pass)
+            ck(kvqb::launch_quantize_tokenwise(srcs[1], u, n, c->bits, c->word_bits, c->vtok.p, c->vtok.p + u * n,
+                                               codes, s),
+               "quantize (token-wise V)");
+            continue;
+        }
+        const int mode = c->v_token_wise() ? KVQ_MODE_CHANNEL_WISE : c->mode;  // K stays channel-wise
+        if (kvqb::quantize_fused_supported(n, d, c->word_bits, mode)) {
+            ck(kvqb::launch_quantize_fused(srcs[which], u, n, d, c->bits, c->word_bits, mode, alpha, beta, codes, s),
                "quantize");
         } else {
-            ck(kvqb::launch_compute_stats(srcs[which], u, n, d, c->mode, alpha, beta, s), "compute_stats");
+            ck(kvqb::launch_compute_stats(srcs[which], u, n, d, mode, alpha, beta, s), "compute_stats");
             ck(kvqb::launch_quantize_pack(srcs[which], u, n, d, alpha, beta, c->bits, c->word_bits, codes, s),
                "quantize");
         }
@@ -398,8 +416,9 @@ kvqb::DecodeArgs range_args(const kvqb::DecodeArgs& a, const kvq_cache* c, size_
     if (r.v_codes_x) r.v_codes_x += kvqb::vx_bytes(u0, c->n_vis, c->bits);
     r.k_alpha += u0 * d;
     r.k_beta += u0 * d;
-    r.v_alpha += u0 * d;
-    r.v_beta += u0 * d;
+    const size_t vs = r.v_token_wise ? c->n_vis : d;  // V stats per unit: per channel or per token
+    r.v_alpha += u0 * vs;
+    r.v_beta += u0 * vs;
     r.k_tail += u0 * c->tail_cap * d;
     r.v_tail += u0 * c->tail_cap * d;
     r.tail_len += b0;
@@ -744,6 +763,7 @@ int kvq_cache_memory(const kvq_cache* cc, size_t mem[6]) {
     if (st != KVQ_OK) return st;
     mem[0] = 2 * c->units * c->n_vis * c->rb;
     mem[1] = c->units * 4 * 4 * c->dim;
+    if (c->v_token_wise()) mem[1] = c->units * 2 * 4 * (c->dim + c->n_vis);  // K per channel, V per token
     mem[2] = mem[0] + mem[1];
     mem[3] = c->units * 2 * c->n_tail * c->dim * 4;
     mem[4] = c->units * 2 * c->n_vis * c->dim * 4;
@@ -767,10 +787,24 @@ int kvq_cache_read_segment(const kvq_cache* c, size_t unit, int which, uint8_t* 
         DevBuf<uint8_t> tmp;
         const uint8_t* src = which == 0 ? c->k_codes() : v_ref_tmp(const_cast<kvq_cache*>(c), tmp, c->stream);
         if (seg && bytes) ck(cudaMemcpyAsync(bytes, src + unit * seg, seg, cudaMemcpyDeviceToHost, c->stream), "D2H");
+        if (which == 1 && c->v_token_wise() && (alpha || beta))
+            raise(KVQ_ERR_CONFIG, "token-wise V: per-channel stats do not exist (kvq_cache_read_value_token_stats)");
         const float* a = (which == 0 ? c->k_alpha() : c->v_alpha()) + unit * c->dim;
         const float* b = (which == 0 ? c->k_beta() : c->v_beta()) + unit * c->dim;
         if (alpha) ck(cudaMemcpyAsync(alpha, a, c->dim * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
         if (beta) ck(cudaMemcpyAsync(beta, b, c->dim * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+        sync(c->stream);
+    });
+}
+
+int kvq_cache_read_value_token_stats(const kvq_cache* c, size_t unit, float* alpha, float* beta) {
+    return guarded([&] {
+        if (!c->v_token_wise()) raise(KVQ_ERR_CONFIG, "not a token-wise V cache");
+        if (unit >= c->units) raise(KVQ_ERR_DOMAIN, "segment index out of range");
+        const size_t n = c->n_vis;
+        if (alpha) ck(cudaMemcpyAsync(alpha, c->vtok.p + unit * n, n * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+        if (beta)
+            ck(cudaMemcpyAsync(beta, c->vtok.p + (c->units + unit) * n, n * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
         sync(c->stream);
     });
 }

@@ -42,6 +42,10 @@ cudaError_t launch_quantize_pack(const float* x, size_t mats, size_t rows, size_
 bool quantize_fused_supported(size_t rows, size_t dim, int word_bits, int mode);
 cudaError_t launch_quantize_fused(const float* x, size_t mats, size_t rows, size_t dim, int bits, int word_bits,
                                   int mode, float* alpha, float* beta, uint8_t* codes, cudaStream_t s);
+// Token-wise stats + codes (opt-in V mode; d = 128): alpha / beta [mats][rows], codes in
+// the reference row layout (M-bit words).
+cudaError_t launch_quantize_tokenwise(const float* x, size_t mats, size_t rows, int bits, int word_bits,
+                                      float* alpha, float* beta, uint8_t* codes, cudaStream_t s);
 // Generic bit packing of explicit u32 codes (bitpack.hpp:161-187). err_flag set to 1 on
 // an out-of-range code.
 cudaError_t launch_pack_codes(const uint32_t* codes, size_t count, int bits, int word_bits,
@@ -92,6 +96,8 @@ struct DecodeArgs {
     const float* v_new;
     int* append_cnt;
     int* overflow;
+    int v_token_wise;     // V stats per token (v_alpha / v_beta [units][n_vis]; opt-in mode,
+                          // tensor-core decode only)
     int early_trigger;    // tensor-core decode: release dependents right after the dependency
                           // wait (a dependent that must overlap: the sibling grid) instead of
                           // after phase B

@@ -177,6 +177,7 @@ int kvq_cache_image_bytes(const kvq_cache* c, size_t* bytes) {
 int kvq_cache_save_image(const kvq_cache* c, void* image, size_t capacity, int image_on_device, void* stream) {
     return guarded([&] {
         sync_tail(const_cast<kvq_cache*>(c));
+        if (c->v_token_wise()) raise(KVQ_ERR_CONFIG, "cache save: KVQC has no token-wise V stats");
         const Record r(c);
         const size_t total = kCacheHeader + c->units * r.bytes;
         if (capacity < total) raise(KVQ_ERR_DOMAIN, "cache save: image buffer too small");

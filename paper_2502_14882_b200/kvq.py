@@ -110,6 +110,7 @@ def lib() -> C.CDLL:
             "kvq_cache_resident_bytes": (C.c_int, [_VP, _SZP]),
             "kvq_cache_read_segment": (C.c_int, [_VP, _SZ, C.c_int, _U8, _F, _F]),
             "kvq_cache_read_tail": (C.c_int, [_VP, _SZ, C.c_int, _F]),
+            "kvq_cache_read_value_token_stats": (C.c_int, [_VP, _SZ, _F, _F]),
             "kvq_cache_device_pointers": (C.c_int, [_VP, C.POINTER(_VP)]),
             "kvq_last_error_offset": (C.c_ulonglong, []),
             "kvq_cache_image_bytes": (C.c_int, [_VP, _SZP]),
@@ -213,6 +214,9 @@ def unpack(buf: PackedBuffer) -> np.ndarray:
 class QuantMode(IntEnum):
     channel_wise = 0
     global_ = 1
+    # Opt-in extension (not in the reference): K channel-wise, V token-wise (north_star;
+    # KVQ_MODE_V_TOKEN_WISE) - BatchedCache only, d = 128, tensor-core decode.
+    v_token_wise = 2
 
 
 @dataclass
@@ -888,13 +892,17 @@ class BatchedCache:
         return dict(zip(("k_rows", "v_rows", "v_operand", "derived"), (int(x) for x in m)))
 
     def segment(self, unit: int, which: int) -> QuantizedSegment:
+        """Packed codes and per-channel stats of one unit's K (0) or V (1) segment. A token-wise
+        V cache's V segment carries no per-channel stats (zeros here; value_token_stats)."""
         n, d = self.vis_tokens(), self.dim
         bits = self.bitwidth if self.bitwidth != FULL_PRECISION_BITS else 8
         nbytes = lib().kvq_segment_bytes(n, d, bits, self.word_bits)
         raw = np.zeros(max(nbytes, 1), np.uint8)
         a = np.zeros(d, np.float32)
         b = np.zeros(d, np.float32)
-        _check(lib().kvq_cache_read_segment(self._h, unit, which, _u8p(raw), _fp(a), _fp(b)))
+        tokwise_v = which == 1 and self._info()[8] == int(QuantMode.v_token_wise)
+        _check(lib().kvq_cache_read_segment(self._h, unit, which, _u8p(raw), None if tokwise_v else _fp(a),
+                                            None if tokwise_v else _fp(b)))
         g = self.word_bits // bits
         cpr = (d + g - 1) // g * g
         return QuantizedSegment(PackedBuffer(raw[:nbytes].copy(), bits, self.word_bits, n * cpr),
@@ -904,6 +912,13 @@ class BatchedCache:
         out = np.zeros((max(self.tail_tokens(), 1), self.dim), np.float32)
         _check(lib().kvq_cache_read_tail(self._h, unit, which, _fp(out)))
         return out[:self.tail_tokens()].copy()
+
+    def value_token_stats(self, unit: int) -> tuple[np.ndarray, np.ndarray]:
+        """Token-wise V caches: the V (alpha, beta) of every visual token of one unit."""
+        n = self._info()[4]
+        a, b = np.zeros(max(n, 1), np.float32), np.zeros(max(n, 1), np.float32)
+        _check(lib().kvq_cache_read_value_token_stats(self._h, unit, _fp(a), _fp(b)))
+        return a[:n], b[:n]
 
     def device_pointers(self) -> list[int]:
         p = (C.c_void_p * 9)()
