@@ -133,3 +133,37 @@ def test_token_wise_v_unsupported_uses_raise(kvq):
         kvq.BatchedCache.build(rng.normal(size=(1, 1, 16, 64)).astype(np.float32),
                                rng.normal(size=(1, 1, 16, 64)).astype(np.float32),
                                kvq.QuantizationConfig(1, kvq.QuantMode.v_token_wise), kvq.CalibrationParams(), group=1)
+
+
+def test_token_wise_v_long_tail_and_host_step(kvq):
+    """Token-wise V through the fp32 tail pass (tail capacity > 64 rows: the decode writes its
+    log-sum-exp, the tail pass merges) and through the chunked host-buffer step
+    (kvq_cache_step: per-chunk stats offsets), against the same cache decoded directly."""
+    from oracle import tokenwise as tw
+    B, H, G, n = 32, 8, 4, 512  # 256 units: the host step runs 2 request chunks
+    rng = np.random.default_rng(21)
+    k = rng.normal(size=(B, H, n, 128)).astype(np.float32)
+    v = rng.normal(size=(B, H, n, 128)).astype(np.float32)
+    cfg = kvq.QuantizationConfig(1, kvq.QuantMode.v_token_wise)
+    a = kvq.BatchedCache.build(k, v, cfg, kvq.CalibrationParams(1.0, 0.0), group=G)
+    b = kvq.BatchedCache.build(k, v, cfg, kvq.CalibrationParams(1.0, 0.0), group=G)
+    a.reserve_tail(100)  # tail pass path
+    for step in range(3):
+        q = rng.normal(size=(B, H, G, 128)).astype(np.float32)
+        kn = rng.normal(size=(B, H, 128)).astype(np.float32)
+        vn = rng.normal(size=(B, H, 128)).astype(np.float32)
+        out_a, _, _ = a.decode(q)
+        a.append(kn, vn)
+        out_b = np.empty_like(q)
+        b.step(q, kn, vn, out_b)
+        assert np.allclose(out_a, out_b, rtol=0, atol=5e-5 * np.abs(out_a).max()), step
+    u = 77
+    bq, hq = divmod(u, H)
+    ks, vs = a.segment(u, 0), a.segment(u, 1)
+    va, vb = a.value_token_stats(u)
+    q = rng.normal(size=(B, H, G, 128)).astype(np.float32)
+    out, _, _ = a.decode(q)
+    for g in range(G):
+        want = tw.decode_f64(_unpack(ks.codes.bytes, n, 1), ks.stats.alpha, ks.stats.beta, _unpack(vs.codes.bytes, n, 1),
+                             va, vb, q[bq, hq, g], a.tail(u, 0), a.tail(u, 1), 1, (1.0, 0.0))
+        assert _rel(out[bq, hq, g], want) <= TOL
