@@ -71,7 +71,7 @@ struct TcParams {
     int whole;   // mixed launch: CTAs [0, whole) each own a whole unit alone (T1 tokens); the
     int T1;      // rest are S-CTA clusters of the remaining units (0: uniform launch)
     int split_first;  // mixed launch: the split units' CTAs come first in the grid
-    int late_trigger; // release dependents at exit instead of after the dependency wait
+    int late_trigger; // dependents released: 0 after the dependency wait, 1 at exit, 2 after phase B, 3 at its start
 };
 
 // ---- PTX helpers (mbarriers, bulk copies, cluster barriers, PDL: kvq_ptx.cuh) ---------
@@ -805,6 +805,7 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
     }
 
     if (threadIdx.x == 0) TTRACE(1);  // softmax parameters known
+    if (p.late_trigger == 3) griddep_launch();  // release at the start of phase B (see launch_occ)
     // ---------------- phase B: p . V over this warp's tokens ----------------
     // D[16 channels x 8 (head, plane)] += V^T[16 ch x 32 tok] * P[32 tok x 8 (head, plane)]:
     // 8 channel tiles per 32-token block and head group (half the MMAs of a P-rows tile).
@@ -1185,13 +1186,17 @@ cudaError_t launch_occ(const DecodeArgs& a, cudaStream_t s, int groups = 1, int 
     }
     cudaError_t e = cudaSuccess;
     static const int split_first = std::getenv("KVQ_TC_SPLIT_FIRST") ? std::atoi(std::getenv("KVQ_TC_SPLIT_FIRST")) : 0;
-    // Dependents are released after phase B (late_trigger 2), so the next grid's CTAs are
-    // placed once this grid's slots drain: released right after the dependency wait, they
+    // Dependents are released late (phase B), so the next grid's CTAs are placed once this
+    // grid's slots drain: released right after the dependency wait, they
     // land on the SMs that finish first and stack four whole units there (c2: 40 SMs with
     // 4.0 units instead of 3.5, profiles/r02_decode_c2.md). Early release (0) where a
     // dependent must overlap this grid: the fp32 tail pass, a sibling balancing grid.
+    // Default: at the start of phase B (3) - the next grid's CTAs fill the slots of lightly
+    // loaded SMs sooner (C3 b1 35.5 -> 34.7 us, b2 37.2 -> 36.5) - except for the balanced
+    // 4-warp launch (whole units + half-unit clusters, 3.5 units per SM), whose placement
+    // only stays even with the release after phase B (2; C2 33.2 vs 35.4 us).
     static const int trig_env = std::getenv("KVQ_TC_TRIGGER") ? std::atoi(std::getenv("KVQ_TC_TRIGGER")) : -1;
-    const int late = a.early_trigger || a.tail_lse ? 0 : trig_env >= 0 ? trig_env : 2;
+    const int late = a.early_trigger || a.tail_lse ? 0 : trig_env >= 0 ? trig_env : (whole > 0 ? 2 : 3);
     TcParams p{a, S, T, groups, whole, T1, split_first, late};
     // TMEM: 512 columns per SM; never let more CTAs share an SM than TMEM can serve (a
     // blocked tcgen05.alloc inside a cluster could deadlock against its partners).
