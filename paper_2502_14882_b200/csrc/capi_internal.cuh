@@ -164,6 +164,7 @@ struct kvq_cache {
     DevBuf<uint8_t> vref;    // reference-layout V rebuilt from vx for the generic / tcgen05 paths
     DevBuf<float> stats;     // [2 (K,V)][2 (alpha,beta)][units][dim]
     DevBuf<float> vtok;      // token-wise V (KVQ_MODE_V_TOKEN_WISE): [2 (alpha,beta)][units][n_vis]
+    DevBuf<float2> vtok_so;  //   and the decode's (step, alpha / step) per token [units][n_vis]
     DevBuf<float> k_tail, v_tail;  // [units][tail_cap][dim]
     DevBuf<float> lse;             // [units][group] decode log-sum-exp for the tail pass
     DevBuf<float> tail_part;       // [units][group][130] tail-pass partials (concurrent schedule)

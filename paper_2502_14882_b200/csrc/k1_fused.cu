@@ -103,7 +103,7 @@ quantize_rows_d128(const float* __restrict__ x, size_t rows, const float* __rest
 template <int BITS>
 __global__ void __launch_bounds__(kWarpsPerCta * 32)
 quantize_rows_tok_d128(const float* __restrict__ x, size_t rows, float* __restrict__ alpha, float* __restrict__ beta,
-                       uint8_t* __restrict__ codes, int word_bits) {
+                       float2* __restrict__ step_off, uint8_t* __restrict__ codes, int word_bits) {
     constexpr int kRowBytes = 16 * BITS;
     const float levels = (float)((1u << BITS) - 1u);
     const size_t m = blockIdx.y;
@@ -131,7 +131,13 @@ quantize_rows_tok_d128(const float* __restrict__ x, size_t rows, float* __restri
         }
         const float range = __fsub_rn(hi, lo);
         const float inv = range > 0.0f ? __fdiv_rn(levels, range) : 0.0f;  // quantize.hpp:102-106
-        if (lane == 0) alpha[m * rows + r] = lo, beta[m * rows + r] = hi;
+        if (lane == 0) {
+            alpha[m * rows + r] = lo, beta[m * rows + r] = hi;
+            // the decode's per-token pair: step s = (beta - alpha) / L and offset o = alpha / s
+            // (v = s (code + o)); a flat token keeps s = 0, o = alpha
+            const float st = fmaxf(range * (1.0f / levels), 0.0f);
+            step_off[m * rows + r] = make_float2(st, range > 0.0f ? __fdividef(lo * levels, range) : lo);
+        }
         uint32_t code[4];
 #pragma unroll
         for (int w = 0; w < 4; ++w) code[w] = code_of(v[w], lo, inv, levels);
@@ -142,17 +148,17 @@ quantize_rows_tok_d128(const float* __restrict__ x, size_t rows, float* __restri
 }  // namespace
 
 cudaError_t launch_quantize_tokenwise(const float* x, size_t mats, size_t rows, int bits, int word_bits,
-                                      float* alpha, float* beta, uint8_t* codes, cudaStream_t s) {
+                                      float* alpha, float* beta, float2* step_off, uint8_t* codes, cudaStream_t s) {
     if (rows == 0 || mats == 0) return cudaSuccess;
     size_t gx = (rows + kWarpsPerCta - 1) / kWarpsPerCta;
     const size_t cap = (148 * 16 + mats - 1) / mats;
     if (gx > cap) gx = cap < 1 ? 1 : cap;
     dim3 grid((unsigned)gx, (unsigned)mats);
     switch (bits) {
-        case 1: quantize_rows_tok_d128<1><<<grid, kWarpsPerCta * 32, 0, s>>>(x, rows, alpha, beta, codes, word_bits); break;
-        case 2: quantize_rows_tok_d128<2><<<grid, kWarpsPerCta * 32, 0, s>>>(x, rows, alpha, beta, codes, word_bits); break;
-        case 4: quantize_rows_tok_d128<4><<<grid, kWarpsPerCta * 32, 0, s>>>(x, rows, alpha, beta, codes, word_bits); break;
-        case 8: quantize_rows_tok_d128<8><<<grid, kWarpsPerCta * 32, 0, s>>>(x, rows, alpha, beta, codes, word_bits); break;
+        case 1: quantize_rows_tok_d128<1><<<grid, kWarpsPerCta * 32, 0, s>>>(x, rows, alpha, beta, step_off, codes, word_bits); break;
+        case 2: quantize_rows_tok_d128<2><<<grid, kWarpsPerCta * 32, 0, s>>>(x, rows, alpha, beta, step_off, codes, word_bits); break;
+        case 4: quantize_rows_tok_d128<4><<<grid, kWarpsPerCta * 32, 0, s>>>(x, rows, alpha, beta, step_off, codes, word_bits); break;
+        case 8: quantize_rows_tok_d128<8><<<grid, kWarpsPerCta * 32, 0, s>>>(x, rows, alpha, beta, step_off, codes, word_bits); break;
         default: return cudaErrorInvalidValue;
     }
     note_launch();

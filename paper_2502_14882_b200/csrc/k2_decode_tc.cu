@@ -838,6 +838,18 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
     const int nblk_all = (nv + 31) >> 5;
     for (int b0 = 0; b0 < nblk_all; b0 += 4) {
         const int nbg = min(4, nblk_all - b0);
+        // token-wise V: the group's per-token (step, offset) pairs, loaded once, under the
+        // TMEM load and the exponentials
+        float2 tso[4][VTOK ? 4 : 1];
+        if constexpr (VTOK) {
+#pragma unroll
+            for (int bb = 0; bb < 4; ++bb)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int tl = (b0 + bb) * 32 + 16 * (j >> 1) + 8 * (j & 1) + g;  // warp-local token
+                    tso[bb][j] = __ldg(a.v_tok_so + (size_t)unit * n + tok0 + min(tl, max(nv - 1, 0)));
+                }
+        }
         // scores of the group (4 blocks x NT x 4, one TMEM load) -> z = log2 weight (<= 0)
         uint32_t zr[4 * NT * 4];
         tmem_ld_cols<4 * NT * 4>(tmem_w + (uint32_t)(b0 * NT * 4), zr);
@@ -873,7 +885,6 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
             // token-wise V (out_c = sum_j p_j alpha_j + sum_j (p_j s_j) code_jc, s_j the token's
             // step): the IMMA weights are e_j s_j, normalised per group by their own maximum;
             // sum_j e_j and sum_j e_j alpha_j accumulate in fp32
-            constexpr float kInvLevels = 1.0f / (float)((1u << BITS) - 1u);
             float gm[NT];
 #pragma unroll
             for (int hg = 0; hg < NT; ++hg) gm[hg] = 0.0f;
@@ -881,15 +892,12 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
             for (int bb = 0; bb < 4; ++bb)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                    const int tl = (b0 + bb) * 32 + 16 * (j >> 1) + 8 * (j & 1) + g;  // warp-local token
-                    const size_t ti = (size_t)unit * n + tok0 + min(tl, max(nv - 1, 0));
-                    const float al = __ldg(a.v_alpha + ti), be = __ldg(a.v_beta + ti);
-                    const float st = fmaxf(__fsub_rn(be, al) * kInvLevels, 0.0f);
+                    const float st = tso[bb][j].x;
 #pragma unroll
                     for (int hg = 0; hg < NT; ++hg) {
                         const float ev = e[bb][hg][j];  // 0 for masked tokens
                         fw[hg] += ev;
-                        if (st == 0.0f) fa[hg] = __fmaf_rn(ev, al, fa[hg]);  // a flat token: v = alpha
+                        if (st == 0.0f) fa[hg] = __fmaf_rn(ev, tso[bb][j].y, fa[hg]);  // a flat token: v = alpha
                         e[bb][hg][j] = ev * st;
                         gm[hg] = fmaxf(gm[hg], e[bb][hg][j]);
                     }
@@ -924,14 +932,8 @@ __global__ void __launch_bounds__(W * 32, OCC) decode_tc_kernel(const TcParams p
             if (bb >= nbg) break;
             float oj[4];
             if constexpr (VTOK) {
-                constexpr float kLevelsV = (float)((1u << BITS) - 1u);
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int tl = (b0 + bb) * 32 + 16 * (j >> 1) + 8 * (j & 1) + g;
-                    const size_t ti = (size_t)unit * n + tok0 + min(tl, max(nv - 1, 0));
-                    const float al = __ldg(a.v_alpha + ti), rg = __fsub_rn(__ldg(a.v_beta + ti), al);
-                    oj[j] = rg > 0.0f ? __fdividef(al * kLevelsV, rg) : 0.0f;
-                }
+                for (int j = 0; j < 4; ++j) oj[j] = tso[bb][j].x > 0.0f ? tso[bb][j].y : 0.0f;
             }
 #pragma unroll
             for (int hg = 0; hg < NT; ++hg) {
@@ -1480,6 +1482,7 @@ static DecodeArgs unit_range(const DecodeArgs& a, size_t u0, size_t u1) {
     if (r.v_codes_x) r.v_codes_x += vx_bytes(u0, a.n_vis, a.bits);
     const size_t vs = a.v_token_wise ? a.n_vis : d;  // V stats per unit: per channel or per token
     r.k_alpha += u0 * d, r.k_beta += u0 * d, r.v_alpha += u0 * vs, r.v_beta += u0 * vs;
+    if (r.v_tok_so) r.v_tok_so += u0 * a.n_vis;
     r.k_tail += u0 * a.tail_cap * d, r.v_tail += u0 * a.tail_cap * d;
     r.tail_len += u0 / a.kv_heads;
     if (r.k_new) r.k_new += u0 * d, r.v_new += u0 * d, r.append_cnt += u0 / a.kv_heads;

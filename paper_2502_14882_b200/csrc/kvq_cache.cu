@@ -60,6 +60,7 @@ kvqb::DecodeArgs decode_args(kvq_cache* c, const float* q, float* out) {
     a.v_alpha = c->v_token_wise() ? c->vtok.p : c->v_alpha();
     a.v_beta = c->v_token_wise() ? c->vtok.p + c->units * c->n_vis : c->v_beta();
     a.v_token_wise = c->v_token_wise() ? 1 : 0;
+    a.v_tok_so = c->vtok_so.p;
     a.k_tail = c->k_tail.p;
     a.v_tail = c->v_tail.p;
     a.tail_len = c->tail_len.p;
@@ -301,7 +302,7 @@ kvq_cache* build_common(size_t batch, size_t kv_heads, size_t group, size_t n_vi
     c->v_operand_only = !full && dim == 128 && c->n_vis > 0 && group <= 8 && !keep_rows;
     c->codes.alloc((c->v_operand_only ? 1 : 2) * c->units * c->n_vis * c->rb);
     if (c->v_operand_only) c->vx.alloc(kvqb::vx_bytes(c->units, c->n_vis, c->bits));
-    if (c->v_token_wise()) c->vtok.alloc(2 * c->units * c->n_vis);
+    if (c->v_token_wise()) c->vtok.alloc(2 * c->units * c->n_vis), c->vtok_so.alloc(c->units * c->n_vis);
     c->tail_len.alloc(2 * batch + 1);  // + the append overflow flag + fused-append counters
     ck(cudaMemsetAsync(c->tail_len.p, 0, sizeof(int) * (2 * batch + 1), c->stream), "memset");
     c->d_q.alloc(c->q_elems());
@@ -324,7 +325,7 @@ void quantize_prefill(kvq_cache* c, const float* dk, const float* dv, cudaStream
         float* beta = which == 0 ? c->k_beta() : c->v_beta();
         if (which == 1 && c->v_token_wise()) {  // opt-in: V stats per token (one pass)
             ck(kvqb::launch_quantize_tokenwise(srcs[1], u, n, c->bits, c->word_bits, c->vtok.p, c->vtok.p + u * n,
-                                               codes, s),
+                                               c->vtok_so.p, codes, s),
                "quantize (token-wise V)");
             continue;
         }
@@ -419,6 +420,7 @@ kvqb::DecodeArgs range_args(const kvqb::DecodeArgs& a, const kvq_cache* c, size_
     const size_t vs = r.v_token_wise ? c->n_vis : d;  // V stats per unit: per channel or per token
     r.v_alpha += u0 * vs;
     r.v_beta += u0 * vs;
+    if (r.v_tok_so) r.v_tok_so += u0 * c->n_vis;
     r.k_tail += u0 * c->tail_cap * d;
     r.v_tail += u0 * c->tail_cap * d;
     r.tail_len += b0;
@@ -763,7 +765,7 @@ int kvq_cache_memory(const kvq_cache* cc, size_t mem[6]) {
     if (st != KVQ_OK) return st;
     mem[0] = 2 * c->units * c->n_vis * c->rb;
     mem[1] = c->units * 4 * 4 * c->dim;
-    if (c->v_token_wise()) mem[1] = c->units * 2 * 4 * (c->dim + c->n_vis);  // K per channel, V per token
+    if (c->v_token_wise()) mem[1] = c->units * (2 * 4 * c->dim + 4 * 4 * c->n_vis);  // K per channel; V per token (+ decode pair)
     mem[2] = mem[0] + mem[1];
     mem[3] = c->units * 2 * c->n_tail * c->dim * 4;
     mem[4] = c->units * 2 * c->n_vis * c->dim * 4;

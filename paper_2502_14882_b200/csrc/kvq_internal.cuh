@@ -45,7 +45,7 @@ cudaError_t launch_quantize_fused(const float* x, size_t mats, size_t rows, size
 // Token-wise stats + codes (opt-in V mode; d = 128): alpha / beta [mats][rows], codes in
 // the reference row layout (M-bit words).
 cudaError_t launch_quantize_tokenwise(const float* x, size_t mats, size_t rows, int bits, int word_bits,
-                                      float* alpha, float* beta, uint8_t* codes, cudaStream_t s);
+                                      float* alpha, float* beta, float2* step_off, uint8_t* codes, cudaStream_t s);
 // Generic bit packing of explicit u32 codes (bitpack.hpp:161-187). err_flag set to 1 on
 // an out-of-range code.
 cudaError_t launch_pack_codes(const uint32_t* codes, size_t count, int bits, int word_bits,
@@ -98,6 +98,7 @@ struct DecodeArgs {
     int* overflow;
     int v_token_wise;     // V stats per token (v_alpha / v_beta [units][n_vis]; opt-in mode,
                           // tensor-core decode only)
+    const float2* v_tok_so;  // token-wise V: per token (step, alpha / step) [units][n_vis]
     int early_trigger;    // tensor-core decode: release dependents right after the dependency
                           // wait (a dependent that must overlap: the sibling grid) instead of
                           // after phase B
