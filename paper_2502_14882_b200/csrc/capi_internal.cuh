@@ -208,6 +208,7 @@ namespace kvqb::capi {
 
 // Cache internals shared by the cache and snapshot translation units (kvq_cache.cu).
 void grow_tail(kvq_cache* c, size_t need);
+void ensure_tail_room(kvq_cache* c, size_t extra);
 void sync_tail(kvq_cache* c);
 kvqb::DecodeArgs decode_args(kvq_cache* c, const float* q, float* out);
 void run_decode(kvq_cache* c, const float* q, float* out, bool want_weights, bool want_viol, cudaStream_t s,

@@ -25,6 +25,18 @@ void sync_tail(kvq_cache* c) {
     }
 }
 
+// Room for `extra` more tail rows. The host counter runs ahead of the device after graph
+// captures (a captured append counts, runs later or never) and behind it after replays, so
+// a shortfall is first checked against the device's own count (sync_tail) before the tail
+// is reallocated - a spurious growth would change tail_cap (the host-step graph key, and
+// past 64 rows the decode path).
+void ensure_tail_room(kvq_cache* c, size_t extra) {
+    if (c->n_tail + extra <= c->tail_cap) return;
+    sync_tail(c);
+    if (c->n_tail + extra <= c->tail_cap) return;
+    grow_tail(c, c->n_tail + extra);
+}
+
 void grow_tail(kvq_cache* c, size_t need) {
     if (need <= c->tail_cap) return;
     sync_tail(c);  // rows appended on the device only must move too
@@ -654,7 +666,7 @@ int kvq_cache_set_path(kvq_cache* c, int path) {
 int kvq_cache_append(kvq_cache* c, const float* k_new, const float* v_new) {
     return guarded([&] {
         sync_tail(c);
-        grow_tail(c, c->n_tail + 1);
+        ensure_tail_room(c, 1);
         c->d_knew.upload(k_new, c->units * c->dim, c->stream);
         c->d_vnew.upload(v_new, c->units * c->dim, c->stream);
         ck(kvqb::launch_append(c->d_knew.p, c->d_vnew.p, c->batch, c->kv_heads, c->dim, c->tail_cap,
@@ -668,7 +680,7 @@ int kvq_cache_append_device(kvq_cache* c, const float* k_new, const float* v_new
     return guarded([&] {
         if (c->n_tail + 1 > c->tail_cap) {
             ck(cudaStreamSynchronize((cudaStream_t)stream), "sync");
-            grow_tail(c, c->n_tail + 1);
+            ensure_tail_room(c, 1);
         }
         ck(kvqb::launch_append(k_new, v_new, c->batch, c->kv_heads, c->dim, c->tail_cap, c->k_tail.p,
                                c->v_tail.p, c->tail_len.p, c->overflow_flag(), (cudaStream_t)stream), "append");
@@ -706,7 +718,7 @@ int kvq_cache_step_device(kvq_cache* c, const float* queries, const float* k_new
     return guarded([&] {
         if (c->n_tail + 1 > c->tail_cap) {
             ck(cudaStreamSynchronize((cudaStream_t)stream), "sync");
-            grow_tail(c, c->n_tail + 1);
+            ensure_tail_room(c, 1);
         }
         run_decode(c, queries, out, false, false, (cudaStream_t)stream, k_new, v_new);
         c->n_tail += 1;
@@ -717,7 +729,7 @@ int kvq_cache_step_device(kvq_cache* c, const float* queries, const float* k_new
 
 int kvq_cache_step(kvq_cache* c, const float* queries, const float* k_new, const float* v_new, float* out) {
     return guarded([&] {
-        grow_tail(c, c->n_tail + 1);
+        ensure_tail_room(c, 1);
         cudaStream_t s = c->stream;
         const size_t chunks = step_chunks_for(c);
         step_resources(c, chunks);

@@ -110,3 +110,29 @@ def test_host_step_pinned_matches_pageable(kvq):
         b.step(q, k, v, out)
         assert np.array_equal(pout, out), f"step {step}"
     assert a.tail_tokens() == b.tail_tokens() == 3
+
+
+def test_tail_not_grown_on_a_stale_host_count(kvq):
+    """Graph captures advance the host's tail counter without appending on the device; an
+    append that only *looks* past the reserved rows must reconcile with the device first
+    instead of reallocating the tail (which would change the decode geometry and the
+    host-step graph key)."""
+    torch = pytest.importorskip("torch")
+    B, H, G = 2, 2, 4
+    c, _, dev = _pair(kvq, torch, B, H, G, 256, 1, reserve=16)
+    cap = c._info()[9]
+    q = torch.randn((B, H, G, 128), device=dev)
+    out = torch.empty_like(q)
+    kn = torch.randn((B, H, 128), device=dev)
+    s = torch.cuda.Stream()
+    graphs = []
+    for _ in range(cap - 2):  # captures only: the host counter runs ahead by cap - 2
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            c.step_device(q, out, kn, kn, s.cuda_stream)
+        graphs.append(g)
+    for _ in range(4):  # real appends: host count would pass cap, the device holds 4 rows
+        c.append_device(kn, kn, s.cuda_stream)
+    s.synchronize()
+    assert c._info()[9] == cap, "tail reallocated on a stale host count"
+    assert c.tail_tokens() == 4
