@@ -234,6 +234,20 @@ int kvq_cache_save_image(const kvq_cache* c, void* image, size_t capacity, int i
 int kvq_cache_load_image(const void* image, size_t bytes, size_t batch, size_t group,
                          size_t* consumed, kvq_cache** out);
 
+/* ---- multi-GPU split (no reference counterpart - the reference splits a
+ * request's heads over std::thread, kvcache.hpp:272-274, and has no multi-device code) ------
+ * The (request, KV head) units rank `rank` of `world` owns, as global indices u = b * H + h:
+ * contiguous request slices when batch >= world, else round-robin. *count = the share size;
+ * units (nullable) receives it (DOMAIN when capacity is smaller). */
+int kvq_shard_assign(size_t batch, size_t kv_heads, int world, int rank, long long* units, size_t capacity,
+                     size_t* count);
+/* The gather's last hop on the destination rank: `parts` (device) = [world][width] floats,
+ * rank r's output rows ([share_r][row], row = group * dim, in kvq_shard_assign order) at
+ * parts + r * width; scattered to out [batch * kv_heads][row] (host, or device when
+ * out_on_device) by one kernel on `stream`, then synchronised. */
+int kvq_shard_place(const float* parts, int world, size_t width, size_t batch, size_t kv_heads, size_t row,
+                    float* out, int out_on_device, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -117,6 +117,8 @@ def lib() -> C.CDLL:
             "kvq_cache_image_bytes": (C.c_int, [_VP, _SZP]),
             "kvq_cache_save_image": (C.c_int, [_VP, _VP, _SZ, C.c_int, _VP]),
             "kvq_cache_load_image": (C.c_int, [_VP, _SZ, _SZ, _SZ, _SZP, C.POINTER(_VP)]),
+            "kvq_shard_assign": (C.c_int, [_SZ, _SZ, C.c_int, C.c_int, C.POINTER(C.c_longlong), _SZ, _SZP]),
+            "kvq_shard_place": (C.c_int, [_VP, C.c_int, _SZ, _SZ, _SZ, _SZ, _VP, C.c_int, _VP]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -160,6 +162,29 @@ def device_available() -> bool:
 def set_device(device: int) -> None:
     """Bind this thread's CUDA device for the library (one process per GPU)."""
     _check(lib().kvq_set_device(int(device)))
+
+
+def shard_assign(batch: int, kv_heads: int, world: int, rank: int) -> np.ndarray:
+    """Global unit indices (b * H + h) rank `rank` owns (kvq_shard_assign):
+    contiguous request slices when batch >= world, else round-robin. Host-only."""
+    n = C.c_size_t(0)
+    _check(lib().kvq_shard_assign(batch, kv_heads, world, rank, None, 0, C.byref(n)))
+    out = np.empty(n.value, np.int64)
+    _check(lib().kvq_shard_assign(batch, kv_heads, world, rank, out.ctypes.data_as(C.POINTER(C.c_longlong)),
+                                  out.size, C.byref(n)))
+    return out
+
+
+def shard_place(parts_ptr: int, world: int, width: int, batch: int, kv_heads: int, row: int, out,
+                stream: int = 0) -> None:
+    """kvq_shard_place: scatter the gathered [world][width] device rows into the global
+    [batch * kv_heads][row] order. `out` is a float32 numpy array (host) or a device pointer."""
+    if isinstance(out, np.ndarray):
+        if out.dtype != np.float32 or not out.flags.c_contiguous or out.size < batch * kv_heads * row:
+            raise DomainError("shard_place: out must be a contiguous float32 array of batch * kv_heads * row")
+        _check(lib().kvq_shard_place(parts_ptr, world, width, batch, kv_heads, row, out.ctypes.data, 0, stream))
+    else:
+        _check(lib().kvq_shard_place(parts_ptr, world, width, batch, kv_heads, row, int(out), 1, stream))
 
 
 # ---- bitpack.hpp -----------------------------------------------------------------------

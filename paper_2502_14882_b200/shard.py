@@ -12,7 +12,9 @@ Each rank builds its own device-resident BatchedCache from its share of the pref
 packed KV never crosses GPUs), decodes and appends its units, and the outputs are gathered
 to one rank off the timed path: every rank's rows come off the device through the C-ABI
 (kvq_cache_decode's device-to-host copy) and travel as tensors (torch.distributed gather,
-NCCL between B200s, gloo in the CPU tests) - no pickling. One process per GPU (torchrun);
+NCCL between B200s, gloo in the CPU tests) - no pickling; under NCCL the destination places
+them in the global order with one kernel and one device-to-host copy (kvq_shard_place).
+The unit assignment itself is native (kvq_shard_assign). One process per GPU (torchrun);
 the rank binds its device from LOCAL_RANK before any CUDA work.
 """
 from __future__ import annotations
@@ -38,11 +40,11 @@ def partition(batch: int, world: int) -> list[tuple[int, int]]:
 
 def assign_units(batch: int, kv_heads: int, world: int) -> list[list[tuple[int, int]]]:
     """(request, KV head) units per rank per §8(e): contiguous request slices when every
-    rank gets at least one request, else units dealt round-robin (u = b * H + h)."""
-    if batch >= world:
-        return [[(b, h) for b in range(s, e) for h in range(kv_heads)] for s, e in partition(batch, world)]
-    units = [(b, h) for b in range(batch) for h in range(kv_heads)]
-    return [units[r::world] for r in range(world)]
+    rank gets at least one request, else units dealt round-robin (u = b * H + h). The
+    assignment is the library's (kvq_shard_assign, csrc/kvq_shard.cu), so the Python driver
+    and the native gather (kvq_shard_place) agree by construction."""
+    from . import kvq
+    return [[divmod(int(u), kv_heads) for u in kvq.shard_assign(batch, kv_heads, world, r)] for r in range(world)]
 
 
 @dataclass
@@ -171,6 +173,12 @@ class ShardedCache:
         if spec.rank != dst:
             return None
         out = np.zeros(full_shape, np.float32)
+        if dev.type == "cuda":  # NCCL: the rows are on this GPU - one placement kernel, one D2H copy
+            from . import kvq
+            stacked = torch.stack(parts)
+            kvq.shard_place(stacked.data_ptr(), spec.world, width, spec.batch, spec.kv_heads, row, out,
+                            torch.cuda.current_stream().cuda_stream)
+            return out
         for r, p in enumerate(parts):
             n = len(shares[r])
             if not n:

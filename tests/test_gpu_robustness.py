@@ -167,3 +167,32 @@ def test_sharded_gpu_backend_matches_whole_batch(kvq, tmp_path, monkeypatch, bat
         want, _, _ = whole.decode(q)
         whole.append(kn, kn)
         np.testing.assert_allclose(got[t], want, rtol=0, atol=2e-6)
+
+
+@pytest.mark.parametrize("batch,heads,world", [(7, 8, 3), (1, 8, 3), (2, 3, 8), (64, 8, 8)])
+def test_shard_place_matches_host_placement(kvq, batch, heads, world):
+    """kvq_shard_place (the NCCL gather's last hop: one placement kernel + one D2H copy)
+    against ShardSpec.place on the same gathered rows, request slices and round-robin,
+    host and device destinations."""
+    torch = pytest.importorskip("torch")
+    from paper_2502_14882_b200.shard import ShardSpec, assign_units
+    G, d = 4, 128
+    row = G * d
+    shares = assign_units(batch, heads, world)
+    width = max(len(s) for s in shares) * row + 5  # odd padding: the scalar copy path too
+    rng = np.random.default_rng(batch * 100 + world)
+    parts = rng.normal(size=(world, width)).astype(np.float32)
+    want = np.zeros((batch, heads, G, d), np.float32)
+    for r in range(world):
+        spec = ShardSpec(batch, heads, G, 16, d, r, world)
+        n = len(shares[r])
+        if n:
+            lb, lh = spec.local_shape
+            spec.place(want, parts[r, :n * row].reshape(lb, lh, G, d), r)
+    dev = torch.from_numpy(parts).cuda()
+    got = np.full(want.shape, np.nan, np.float32)
+    kvq.shard_place(dev.data_ptr(), world, width, batch, heads, row, got)
+    assert np.array_equal(got, want)
+    got_dev = torch.full(want.shape, float("nan"), device="cuda")
+    kvq.shard_place(dev.data_ptr(), world, width, batch, heads, row, got_dev.data_ptr())
+    assert np.array_equal(got_dev.cpu().numpy(), want)

@@ -125,3 +125,18 @@ def test_two_rank_gloo_matches_single_process(tmp_path, monkeypatch, batch):
         want = single.decode(qs[t])
         single.append(kn[t], vn[t])
         assert np.array_equal(sharded[t], want)
+
+
+def test_native_assignment_matches_the_spec_and_validates(kvq_host):
+    """kvq_shard_assign (the library's assignment, used by assign_units and the native
+    gather) against §8(e) written out in Python; bad ranks are domain errors."""
+    for batch, heads, world in ((5, 2, 2), (64, 8, 8), (3, 8, 4), (1, 8, 8), (2, 3, 8), (0, 8, 2)):
+        for r in range(world):
+            if batch >= world:
+                s, e = partition(batch, world)[r]
+                spec = [b * heads + h for b in range(s, e) for h in range(heads)]
+            else:
+                spec = list(range(r, batch * heads, world))
+            assert kvq_host.shard_assign(batch, heads, world, r).tolist() == spec
+    with pytest.raises(kvq_host.DomainError):
+        kvq_host.shard_assign(4, 8, 2, 2)
