@@ -585,9 +585,10 @@ void capture_step(kvq_cache* c, const StepKey& key) {
 
 size_t step_chunks(const kvq_cache* c) {
     static const char* env = std::getenv("KVQ_STEP_CHUNKS");
-    // measured (profiles/r01_e2e_chunks.txt): c5 B=512 706 -> 519 us/step with 4 chunks,
-    // c2 B=64 unchanged at 2 (its uploads are short next to the decode)
-    size_t k = env ? (size_t)std::max(1, std::atoi(env)) : (c->batch >= 256 ? 4 : c->batch >= 32 ? 2 : 1);
+    // measured (profiles/r02_e2e_chunks.txt, 1/2/3/4/8 chunks per config): C5 B=512 best at 4,
+    // C2 / C3 at 2, long rows (C4, 32 k tokens, B=16) at 3 (174 -> 163 us per step)
+    size_t k = env ? (size_t)std::max(1, std::atoi(env))
+                   : (c->batch >= 256 ? 4 : c->batch >= 32 ? 2 : (c->n_vis >= 16384 && c->batch >= 3) ? 3 : 1);
     return std::min(k, c->batch);
 }
 

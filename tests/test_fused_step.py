@@ -136,3 +136,30 @@ def test_tail_not_grown_on_a_stale_host_count(kvq):
     s.synchronize()
     assert c._info()[9] == cap, "tail reallocated on a stale host count"
     assert c.tail_tokens() == 4
+
+
+def test_host_step_three_chunks_long_rows(kvq):
+    """Long rows (n >= 16384) take the 3-chunk host step (batch 5: chunks of 2 / 2 / 1
+    requests, uneven); outputs and tails against the whole-batch device decode + append. A
+    chunk plans its own CTA split, so the fp32 merge order of a unit's parts may differ."""
+    torch = pytest.importorskip("torch")
+    B, H, G, n = 5, 2, 6, 16384
+    a, b, dev = _pair(kvq, torch, B, H, G, n, 1)
+    rng = np.random.default_rng(8)
+    s = torch.cuda.Stream()
+    for step in range(3):
+        q = rng.normal(size=(B, H, G, 128)).astype(np.float32)
+        k = rng.normal(size=(B, H, 128)).astype(np.float32)
+        v = rng.normal(size=(B, H, 128)).astype(np.float32)
+        out = np.empty_like(q)
+        a.step(q, k, v, out)
+        qd, od = torch.from_numpy(q).to(dev), torch.empty((B, H, G, 128), device=dev)
+        b.decode_device(qd, od, s.cuda_stream)
+        b.append_device(torch.from_numpy(k).to(dev), torch.from_numpy(v).to(dev), s.cuda_stream)
+        s.synchronize()
+        want = od.cpu().numpy()
+        np.testing.assert_allclose(out, want, rtol=0, atol=2e-6 * np.abs(want).max())
+    b.sync_tail()
+    assert a.tail_tokens() == b.tail_tokens() == 3
+    for u in (0, B * H - 1):
+        assert np.array_equal(a.tail(u, 0), b.tail(u, 0))
