@@ -273,7 +273,7 @@ def cpu_reference(cfg_name: str, requests: int, steps: int, threads: int, warmup
     if budget_s > 0:  # size the run: one probe step
         probe, _ = ref.bench_decode(k, v, requests, H, G, n, DIM, bits, word_bits, tau[0], tau[1], q, kn, vn,
                                     threads, 2, tail, dequant=cpu_arm == "dequant")
-        steps = max(3, min(steps, int(budget_s / max(min(probe), 1e-6))))
+        steps = max(1, min(steps, int(budget_s / max(min(probe), 1e-6))))
     secs, _ = ref.bench_decode(k, v, requests, H, G, n, DIM, bits, word_bits, tau[0], tau[1], q, kn, vn, threads,
                                steps + warmup, tail, dequant=cpu_arm == "dequant")
     step_s = statistics.median(secs[warmup:])
