@@ -1,8 +1,10 @@
 """K1 prefill (stats + codes, kvq_quantize_device) per GiB of fp32 input at a BASELINE
-shape, plus a hash of codes / stats to compare variants bit for bit.
+shape, plus a hash of codes / stats to compare variants bit for bit (KVQ_K1_CHUNK_MB: the
+chunked stats / codes pipeline, read once per process).
     python tools/k1_time.py [units] [n] [bits] [mode]"""
 import ctypes as C
 import hashlib
+import os
 import sys
 from pathlib import Path
 
@@ -39,5 +41,5 @@ torch.cuda.synchronize()
 us = e0.elapsed_time(e1) * 1e3 / reps
 gib = x.numel() * 4 / 2**30
 h = hashlib.sha1(codes.cpu().numpy().tobytes() + a.cpu().numpy().tobytes() + b.cpu().numpy().tobytes()).hexdigest()[:16]
-print(f"U={U} n={n} b={bits} mode={mode}: {us:.1f} us "
+print(f"chunk_mb={os.environ.get('KVQ_K1_CHUNK_MB', 'default')} U={U} n={n} b={bits} mode={mode}: {us:.1f} us "
       f"({us / gib:.1f} us/GiB, {x.numel() * 4 / us / 1e6:.2f} TB/s read-once) sha={h}")
