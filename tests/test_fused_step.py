@@ -43,6 +43,7 @@ def test_fused_step_matches_decode_then_append(kvq, B, H, G, n, bits):
     torch = pytest.importorskip("torch")
     fused, plain, dev = _pair(kvq, torch, B, H, G, n, bits)
     s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())  # inputs come from the current stream
     gen = torch.Generator(device=dev)
     gen.manual_seed(5)
     for step in range(6):
@@ -50,6 +51,7 @@ def test_fused_step_matches_decode_then_append(kvq, B, H, G, n, bits):
         kn = torch.randn((B, H, 128), device=dev, generator=gen)
         vn = torch.randn((B, H, 128), device=dev, generator=gen)
         o1, o2 = torch.empty_like(q), torch.empty_like(q)
+        s.wait_stream(torch.cuda.current_stream())
         fused.step_device(q, o1, kn, vn, s.cuda_stream)
         plain.decode_device(q, o2, s.cuda_stream)
         plain.append_device(kn, vn, s.cuda_stream)
@@ -71,6 +73,7 @@ def test_fused_step_graph_replay_past_capacity(kvq):
     kn = torch.stack([torch.full((H, 128), float(b + 1), device=dev) for b in range(B)])
     vn = kn.clone()
     s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())  # inputs come from the current stream
     c.decode_device(q, out, s.cuda_stream)
     torch.cuda.synchronize()
     graph = torch.cuda.CUDAGraph()
@@ -125,6 +128,7 @@ def test_tail_not_grown_on_a_stale_host_count(kvq):
     out = torch.empty_like(q)
     kn = torch.randn((B, H, 128), device=dev)
     s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())  # inputs come from the current stream
     graphs = []
     for _ in range(cap - 2):  # captures only: the host counter runs ahead by cap - 2
         g = torch.cuda.CUDAGraph()
@@ -147,6 +151,7 @@ def test_host_step_three_chunks_long_rows(kvq):
     a, b, dev = _pair(kvq, torch, B, H, G, n, 1)
     rng = np.random.default_rng(8)
     s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())  # inputs come from the current stream
     for step in range(3):
         q = rng.normal(size=(B, H, G, 128)).astype(np.float32)
         k = rng.normal(size=(B, H, 128)).astype(np.float32)
@@ -154,8 +159,10 @@ def test_host_step_three_chunks_long_rows(kvq):
         out = np.empty_like(q)
         a.step(q, k, v, out)
         qd, od = torch.from_numpy(q).to(dev), torch.empty((B, H, G, 128), device=dev)
+        kd, vd = torch.from_numpy(k).to(dev), torch.from_numpy(v).to(dev)
+        s.wait_stream(torch.cuda.current_stream())
         b.decode_device(qd, od, s.cuda_stream)
-        b.append_device(torch.from_numpy(k).to(dev), torch.from_numpy(v).to(dev), s.cuda_stream)
+        b.append_device(kd, vd, s.cuda_stream)
         s.synchronize()
         want = od.cpu().numpy()
         np.testing.assert_allclose(out, want, rtol=0, atol=2e-6 * np.abs(want).max())

@@ -41,6 +41,7 @@ def test_graph_replay_within_capacity_reconciles_host_counters(kvq):
     kn = torch.randn((B, H, 128), device=dev)
     vn = torch.randn((B, H, 128), device=dev)
     s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())  # inputs come from the current stream
     c.decode_device(q, out, s.cuda_stream)
     c.append_device(kn, vn, s.cuda_stream)  # 1 row
     torch.cuda.synchronize()
@@ -69,6 +70,7 @@ def test_graph_replay_past_capacity_is_an_error_not_corruption(kvq):
     kn = torch.stack([torch.full((H, 128), float(b + 1), device=dev) for b in range(B)])
     vn = kn.clone()
     s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())  # inputs come from the current stream
     c.decode_device(q, out, s.cuda_stream)
     torch.cuda.synchronize()
     graph = torch.cuda.CUDAGraph()

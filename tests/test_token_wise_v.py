@@ -90,10 +90,12 @@ def test_token_wise_v_fused_step_and_device_build(kvq):
     for c in (a, b):
         c.reserve_tail(8)
     s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())  # inputs come from the current stream
     for step in range(3):
         q = torch.randn((B, H, G, 128), device=dev, generator=gen)
         kn = torch.randn((B, H, 128), device=dev, generator=gen)
         o1, o2 = torch.empty_like(q), torch.empty_like(q)
+        s.wait_stream(torch.cuda.current_stream())
         a.step_device(q, o1, kn, kn, s.cuda_stream)
         b.decode_device(q, o2, s.cuda_stream)
         b.append_device(kn, kn, s.cuda_stream)
@@ -107,6 +109,7 @@ def test_token_wise_v_fused_step_and_device_build(kvq):
     va, vb = a.value_token_stats(u)
     q = torch.randn((B, H, G, 128), device=dev, generator=gen)
     out = torch.empty_like(q)
+    s.wait_stream(torch.cuda.current_stream())
     a.decode_device(q, out, s.cuda_stream)
     s.synchronize()
     kt, vt = a.tail(u, 0), a.tail(u, 1)
