@@ -11,6 +11,7 @@ Bars (written here):
     (test_kvcache.cpp:161-182).
 """
 import hashlib
+import os
 from pathlib import Path
 
 import numpy as np
@@ -396,6 +397,8 @@ def test_batched_gqa_vs_oracle(kvq, oracle, bits, G, n):
         # the same attention up to fp32 reassociation
         for path, tol in ((kvq.PATH_GENERIC, TOL_GENERIC), (kvq.PATH_TC, TOL_IMMA), (kvq.PATH_UMMA, TOL_TC),
                           (kvq.PATH_DEQUANT, 1e-4), (kvq.PATH_AUTO, TOL_IMMA)):
+            if path == kvq.PATH_UMMA and os.environ.get("KVQ_TEST_SKIP_UMMA") == "1":
+                continue
             cache.set_path(path)
             try:
                 out, _, _ = cache.decode(q)
@@ -729,7 +732,12 @@ def test_randomized_paths_vs_oracle(kvq, oracle, case):
             for g in range(G):
                 want[b, h, g] = oracle.decode_head(q[b, h, g], n, c["bits"], c["wb"], kc, ka, kb, vc, va, vb, ktail,
                                                    vtail, *c["tau"])[0]
-    for path in (kvq.PATH_AUTO, kvq.PATH_TC, kvq.PATH_UMMA, kvq.PATH_GENERIC):
+    # KVQ_TEST_SKIP_UMMA=1 (sanitizer runs): the tcgen05 decode's mbarrier watchdog traps
+    # under compute-sanitizer's slowdown, which poisons the context for every later test
+    paths = (kvq.PATH_AUTO, kvq.PATH_TC, kvq.PATH_UMMA, kvq.PATH_GENERIC)
+    if os.environ.get("KVQ_TEST_SKIP_UMMA") == "1":
+        paths = tuple(x for x in paths if x != kvq.PATH_UMMA)
+    for path in paths:
         cache.set_path(path)
         try:
             out, _, _ = cache.decode(q)
